@@ -1,0 +1,264 @@
+/* tierkv_b200 — C-ABI of the B200 KV-cache data-movement path.
+ *
+ * Drop-in boundary for the reference tierkv hot path (arXiv 2510.09665,
+ * /root/reference/proj). Every entry point is extern "C", takes plain
+ * pointers and sizes, and returns an int status whose values are the
+ * reference's Errc (include/tierkv/common.hpp:13-31) plus TKV_CUDA_ERROR.
+ * Device pointers are marked _dev; `stream` is a cudaStream_t passed as
+ * void*. tkv_last_error() returns the detail string of the calling thread's
+ * last failure.
+ *
+ * Two layers:
+ *  1. kernel level (stream-ordered, no host sync, no allocation):
+ *     tkv_gather_layers / tkv_scatter_layers (K1/K2), tkv_hash_chains (K3),
+ *     tkv_synth_pages / tkv_verify_pages / tkv_synth_chunk (K4);
+ *  2. object level, mirroring the reference C++ classes the engine binds:
+ *     tkv_pages_* (PagedKVStore), tkv_store_* (TieredStore RAM tier),
+ *     tkv_connector_* + tkv_meta_* (Connector + ConnectorMetadata),
+ *     tkv_pd_* (PdStaging + NVLink/P2P chunk sends).
+ */
+#ifndef TIERKV_B200_H
+#define TIERKV_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- status codes: include/tierkv/common.hpp:13-31 ----------------------- */
+enum {
+    TKV_OK = 0,
+    TKV_NOT_FOUND,
+    TKV_TIER_FULL,
+    TKV_OUT_OF_PAGES,
+    TKV_DUPLICATE_KEY,
+    TKV_CORRUPT_CHUNK,
+    TKV_SIZE_MISMATCH,
+    TKV_UNPOPULATED_PAGE,
+    TKV_UNKNOWN_CODEC,
+    TKV_UNKNOWN_INSTANCE,
+    TKV_UNKNOWN_QUERY,
+    TKV_INCONSISTENT_ALLOC,
+    TKV_CHUNK_MISSING,
+    TKV_PINNED,
+    TKV_PROTOCOL_ERROR,
+    TKV_IO_ERROR,
+    TKV_INVALID_ARGUMENT,
+    TKV_CUDA_ERROR /* device failure; no reference equivalent */
+};
+
+const char* tkv_last_error(void);
+const char* tkv_errc_name(int code);
+/* Library version / build id of the loaded kernels. */
+const char* tkv_build_info(void);
+
+/* ---- geometry: include/tierkv/model.hpp:11-33 ----------------------------- */
+typedef struct tkv_model_spec {
+    uint32_t num_layers;
+    uint32_t bytes_per_token_per_layer;
+    uint32_t page_tokens;
+    uint32_t vocab_size;
+    const char* model_tag;
+} tkv_model_spec;
+
+/* ========================================================================== *
+ * 1. Kernel level
+ * ========================================================================== */
+
+/* Paged side of K1/K2. Reference layout (paged_store.hpp:19-82): n_planes=1,
+ * token_stride=plane_bytes=bpt, page_stride=page_tokens*bpt, per-layer page
+ * lists. vLLM layout: n_planes=2 (K,V), plane_bytes=H*D*elt, per-layer bases
+ * in layer_base_dev, shared_table=1 (one block table for all layers). */
+typedef struct tkv_paged_layout {
+    uint64_t base;
+    const uint64_t* layer_base_dev;
+    uint64_t page_stride;
+    uint64_t plane_stride;
+    uint32_t token_stride;
+    uint32_t plane_bytes;
+    uint32_t n_planes;
+    uint32_t page_tokens;
+    uint32_t bpt;
+    uint32_t shared_table;
+} tkv_paged_layout;
+
+/* One chunk transfer (ChunkDescriptor, connector.hpp:22-27): rows
+ * [first_page*page_tokens, +n_tokens) of every moved layer, chunk side at
+ * chunk + layer*layer_stride + row*bpt (HBM, mapped pinned host or peer). */
+typedef struct tkv_xfer_desc {
+    uint64_t chunk;
+    uint64_t layer_stride;
+    const int32_t* table_dev; /* [layers][table_stride] page ids */
+    uint32_t table_stride;
+    uint32_t first_page;
+    uint32_t n_tokens;
+    uint32_t pad;
+} tkv_xfer_desc;
+
+/* Host helper: tile prefix (n+1 entries) for a launch over n_layers layers.
+ * pages_per_tile = 0 picks the default (about 64 KiB per tile). Returns the
+ * pages_per_tile used through *ppt_out. */
+int tkv_plan_tiles(const tkv_xfer_desc* descs, uint32_t n, uint32_t page_tokens,
+                   uint32_t page_bytes, uint32_t pages_per_tile, uint32_t n_layers,
+                   uint32_t* tile_base_out, uint32_t* ppt_out);
+
+/* K1: pages -> chunk buffers. Replaces PagedKVStore::gather_tokens_into
+ * (src/paged_store.cpp:123-140) for every (chunk, layer) of a batch in one
+ * launch. addr_or = OR of all desc.chunk and desc.layer_stride (alignment). */
+int tkv_gather_layers(const tkv_paged_layout* layout, const tkv_xfer_desc* descs_dev,
+                      const uint32_t* tile_base_dev, uint32_t n_desc, uint32_t total_tiles,
+                      uint32_t layer_begin, uint32_t n_layers, uint32_t pages_per_tile,
+                      uint64_t addr_or, int ctas, void* stream);
+/* K2: chunk buffers -> pages. Replaces PagedKVStore::scatter_tokens
+ * (src/paged_store.cpp:147-175). */
+int tkv_scatter_layers(const tkv_paged_layout* layout, const tkv_xfer_desc* descs_dev,
+                       const uint32_t* tile_base_dev, uint32_t n_desc, uint32_t total_tiles,
+                       uint32_t layer_begin, uint32_t n_layers, uint32_t pages_per_tile,
+                       uint64_t addr_or, int ctas, void* stream);
+
+/* K3: one chained SHA-256 key sequence per chain (KeyChain::next,
+ * src/tokens.cpp:22-42). out_dev gets 32 bytes per chunk at rows
+ * out_first.. of each chain. tag_len <= 256. */
+typedef struct tkv_chain_desc {
+    uint64_t token_off;
+    uint32_t n_tokens;
+    uint32_t out_first;
+    uint8_t parent[32];
+} tkv_chain_desc;
+int tkv_hash_chains(const uint32_t* tokens_dev, const tkv_chain_desc* chains_dev, uint32_t n_chains,
+                    uint32_t chunk_size, const char* tag, uint32_t tag_len, uint8_t* out_dev,
+                    void* stream);
+
+/* K4: synth_token_kv (src/synth.cpp:7-20) into pages for positions
+ * [pos_begin, pos_end) and layers [layer_begin, layer_end). */
+int tkv_synth_pages(const tkv_paged_layout* layout, const uint32_t* tokens_dev,
+                    const int32_t* table_dev, uint32_t table_stride, uint64_t seed,
+                    uint32_t pos_begin, uint32_t pos_end, uint32_t layer_begin,
+                    uint32_t layer_end, void* stream);
+/* Adds the number of 8-byte words differing from synth to *mismatches_dev. */
+int tkv_verify_pages(const tkv_paged_layout* layout, const uint32_t* tokens_dev,
+                     const int32_t* table_dev, uint32_t table_stride, uint64_t seed,
+                     uint32_t pos_begin, uint32_t pos_end, uint32_t layer_begin,
+                     uint32_t layer_end, unsigned long long* mismatches_dev, void* stream);
+/* Synthetic chunk payload [n_layers][n][bpt] (KVChunk layout, kv_chunk.hpp:12-36). */
+int tkv_synth_chunk(const uint32_t* tokens_dev, uint64_t seed, uint32_t start, uint32_t n,
+                    uint32_t n_layers, uint32_t bpt, uint8_t* out_dev, void* stream);
+
+/* ========================================================================== *
+ * 2. Object level
+ * ========================================================================== */
+
+/* Chunk keys of one token sequence computed on the device (chunk_keys,
+ * src/tokens.cpp:49-57). Writes n_chunks*32 bytes. */
+int tkv_chunk_keys(const char* model_tag, size_t chunk_size, const uint32_t* tokens, size_t n,
+                   uint8_t* digests_out, size_t* n_chunks);
+/* One KeyChain link after reset(parent) (src/tokens.cpp:22-47). */
+int tkv_keychain_next(const char* model_tag, size_t chunk_size, const uint8_t* parent,
+                      const uint32_t* tokens, size_t n, uint8_t* digest_out);
+
+/* ---- PagedKVStore (include/tierkv/paged_store.hpp:19-60) ----------------- */
+typedef struct tkv_pages tkv_pages;
+int tkv_pages_create(const tkv_model_spec* spec, uint32_t num_pages, int device, tkv_pages** out);
+void tkv_pages_destroy(tkv_pages* p);
+int tkv_pages_alloc(tkv_pages* p, uint64_t query, size_t n, uint32_t* ids_out);
+int tkv_pages_bind_layer(tkv_pages* p, uint64_t query, uint32_t layer, const uint32_t* ids,
+                         size_t n);
+size_t tkv_pages_layer_pages(tkv_pages* p, uint64_t query, uint32_t layer, uint32_t* ids_out,
+                             size_t cap);
+size_t tkv_pages_release(tkv_pages* p, uint64_t query);
+size_t tkv_pages_free_count(tkv_pages* p);
+size_t tkv_pages_allocated_count(tkv_pages* p);
+size_t tkv_pages_pool_pages(tkv_pages* p);
+int tkv_pages_mark_populated(tkv_pages* p, uint32_t page, uint32_t layer);
+int tkv_pages_populated(tkv_pages* p, uint32_t page);
+/* Synchronous host-buffer gather/scatter of one layer (reference semantics
+ * and checks; ordered after all previously enqueued device work). */
+int tkv_pages_gather(tkv_pages* p, const uint32_t* ids, size_t n_ids, uint32_t layer,
+                     size_t token_count, uint8_t* out, size_t out_bytes);
+int tkv_pages_scatter(tkv_pages* p, const uint8_t* buf, size_t buf_bytes, const uint32_t* ids,
+                      size_t n_ids, uint32_t layer, size_t token_count);
+int tkv_pages_layout(tkv_pages* p, tkv_paged_layout* out);
+int tkv_pages_device_table(tkv_pages* p, uint64_t query, void* stream, const int32_t** table_dev,
+                           uint32_t* stride);
+/* Engine compute stand-in (SimEngine::write_tokens, src/sim_engine.cpp:43-64):
+ * K4 into the query's pages for positions [from, to), layers [l0, l1), and
+ * marks them populated. tokens_dev holds the whole prompt. */
+int tkv_pages_compute(tkv_pages* p, uint64_t query, const uint32_t* tokens_dev, uint32_t from,
+                      uint32_t to, uint32_t layer_begin, uint32_t layer_end, void* stream);
+/* Device byte oracle over [from, to) x [l0, l1): adds mismatching words. */
+int tkv_pages_verify(tkv_pages* p, uint64_t query, const uint32_t* tokens_dev, uint32_t from,
+                     uint32_t to, uint32_t layer_begin, uint32_t layer_end,
+                     unsigned long long* mismatches_dev, void* stream);
+
+/* ---- TieredStore RAM tier (include/tierkv/store.hpp:142-262) ------------- */
+typedef struct tkv_store tkv_store;
+int tkv_store_create(const tkv_model_spec* spec, size_t chunk_size, size_t ram_pool_bytes,
+                     tkv_store** out);
+void tkv_store_destroy(tkv_store* s);
+int tkv_store_put(tkv_store* s, const uint8_t* digest, uint32_t token_count,
+                  const uint8_t* payload, size_t payload_bytes, int pin);
+int tkv_store_get(tkv_store* s, const uint8_t* digest, uint8_t* out, size_t cap, size_t* n);
+int tkv_store_get_layer(tkv_store* s, const uint8_t* digest, uint32_t layer, uint8_t* out,
+                        size_t cap, size_t* n);
+int tkv_store_contains(tkv_store* s, const uint8_t* digest);
+int tkv_store_pin(tkv_store* s, const uint8_t* digest, int on);
+int tkv_store_clear(tkv_store* s, const uint8_t* digests, size_t n, size_t* removed,
+                    size_t* refused);
+/* entries, ram_slots_total, ram_slots_used, ram_entries */
+int tkv_store_stats(tkv_store* s, size_t out[4]);
+
+/* ---- Connector (include/tierkv/connector.hpp:74-152) --------------------- */
+typedef struct tkv_connector tkv_connector;
+typedef struct tkv_meta tkv_meta;
+typedef struct tkv_connector_config {
+    int layerwise;               /* TransferMode: 1 layerwise, 0 blocking */
+    int pin_stores;
+    size_t staging_budget_bytes; /* one layer of loads must fit, else blocking */
+    uint32_t staging_depth;      /* device staging ring depth (layers) */
+    int load_zero_copy;          /* 1: K2 reads pinned slots directly */
+    int store_ctas;              /* K1 grid for zero-copy stores (0 = default) */
+    int load_ctas;               /* K2 grid (0 = 2 x SMs) */
+    void* engine_stream;         /* stream the engine computes on */
+} tkv_connector_config;
+void tkv_connector_config_default(tkv_connector_config* cfg);
+int tkv_connector_create(tkv_store* s, tkv_pages* p, const tkv_connector_config* cfg,
+                         tkv_connector** out);
+void tkv_connector_destroy(tkv_connector* c);
+int tkv_connector_get_num_new_matched_tokens(tkv_connector* c, uint64_t query,
+                                             const uint32_t* tokens, size_t n, size_t* matched);
+int tkv_connector_lookup_batch(tkv_connector* c, size_t n_queries, const uint64_t* queries,
+                               const uint32_t* const* prompts, const size_t* lens,
+                               size_t* matched_out);
+int tkv_connector_update_state_after_alloc(tkv_connector* c, uint64_t query, size_t blocks,
+                                           size_t num_external_blocks);
+int tkv_connector_build_meta(tkv_connector* c, size_t n_queries, const uint64_t* queries,
+                             const uint32_t* const* prompts, const size_t* lens, tkv_meta** out);
+int tkv_connector_start_load_kv(tkv_connector* c, tkv_meta* m);
+int tkv_connector_wait_load_kv(tkv_connector* c, tkv_meta* m, uint32_t layer);
+int tkv_connector_start_store_kv(tkv_connector* c, tkv_meta* m);
+int tkv_connector_wait_store_kv(tkv_connector* c, tkv_meta* m, uint32_t layer);
+int tkv_connector_begin_decode(tkv_connector* c, uint64_t query);
+int tkv_connector_append_decode(tkv_connector* c, uint64_t query, uint32_t token);
+int tkv_connector_finish_query(tkv_connector* c, uint64_t query, uint8_t* digests_out, size_t cap,
+                               size_t* n);
+size_t tkv_connector_staging_peak(tkv_connector* c);
+uint64_t tkv_connector_hash_launches(tkv_connector* c);
+
+void tkv_meta_destroy(tkv_meta* m);
+int tkv_meta_layerwise(tkv_meta* m);
+size_t tkv_meta_loaded_tokens(tkv_meta* m, uint64_t query);
+size_t tkv_meta_num_plans(tkv_meta* m);
+/* kind 0 = load plan, 1 = store plan; spans4 = (start, end, record_tokens,
+ * chunk_index) per descriptor; digests 32 B each. */
+int tkv_meta_plan(tkv_meta* m, size_t plan_index, int kind, uint64_t* spans4, uint8_t* digests,
+                  size_t cap, size_t* n, uint64_t* matched);
+int tkv_meta_store_results(tkv_meta* m, uint64_t query, int* codes, uint8_t* digests, size_t cap,
+                           size_t* n);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* TIERKV_B200_H */

@@ -1,0 +1,359 @@
+"""Python face of the B200 path: thin wrappers over the C-ABI objects.
+
+``Engine`` bundles one PagedKVStore (device pages), one TieredStore (pinned
+host tier) and one Connector, with the same method names and return
+conventions as ``oracle.RefEngine`` (the reference engine stack) so that a
+test scenario can be run against both and compared. Connector calls return
+the reference's Errc codes as ints; everything else raises TkvError.
+
+PyTorch is used only as plumbing: device buffers for prompt tokens and the
+engine stream handle.
+"""
+from __future__ import annotations
+
+import ctypes as ct
+
+import numpy as np
+import torch
+
+from ._lib import (ChainDescC, ConnectorConfigC, ModelSpecC, PagedLayoutC, XferDescC, check, lib,
+                   u8p, u32p, u64p)
+
+__all__ = ["Engine", "chunk_keys", "keychain_next", "PagedLayoutC", "XferDescC", "ChainDescC",
+           "plan_tiles", "hash_chains", "ErrcOK"]
+
+ErrcOK = 0
+
+
+def _tokens(tokens) -> np.ndarray:
+    return np.ascontiguousarray(np.asarray(tokens, dtype=np.uint32))
+
+
+def _u8(b: bytes) -> np.ndarray:
+    return np.frombuffer(b, dtype=np.uint8).copy()
+
+
+def chunk_keys(tokens, chunk_size: int, tag: str) -> list[bytes]:
+    """Chunk keys of one sequence, computed by the K3 device kernel."""
+    t = _tokens(tokens)
+    n_chunks = (t.size + chunk_size - 1) // chunk_size
+    out = np.zeros(max(1, n_chunks) * 32, np.uint8)
+    n = ct.c_size_t(0)
+    check(lib().tkv_chunk_keys(tag.encode(), chunk_size, t.ctypes.data_as(u32p), t.size,
+                               out.ctypes.data_as(u8p), ct.byref(n)))
+    return [out[32 * i:32 * i + 32].tobytes() for i in range(n.value)]
+
+
+def keychain_next(tag: str, chunk_size: int, parent: bytes, tokens) -> bytes:
+    t = _tokens(tokens)
+    p = _u8(parent)
+    out = np.zeros(32, np.uint8)
+    check(lib().tkv_keychain_next(tag.encode(), chunk_size, p.ctypes.data_as(u8p), t.ctypes.data_as(u32p),
+                                  t.size, out.ctypes.data_as(u8p)))
+    return out.tobytes()
+
+
+def plan_tiles(descs: list[XferDescC], page_tokens: int, page_bytes: int, n_layers: int,
+               pages_per_tile: int = 0):
+    """Host tile prefix for a K1/K2 launch: (tile_base uint32 array, ppt)."""
+    arr = (XferDescC * max(1, len(descs)))(*descs)
+    tb = np.zeros(len(descs) + 1, np.uint32)
+    ppt = ct.c_uint32(0)
+    check(lib().tkv_plan_tiles(ct.cast(arr, ct.c_void_p), len(descs), page_tokens, page_bytes,
+                               pages_per_tile, n_layers, tb.ctypes.data_as(u32p), ct.byref(ppt)))
+    return tb, ppt.value
+
+
+def hash_chains(tokens_dev: torch.Tensor, chains_dev: torch.Tensor, n_chains: int, chunk_size: int,
+                tag: str, out_dev: torch.Tensor, stream=None) -> None:
+    s = stream.cuda_stream if stream is not None else torch.cuda.current_stream().cuda_stream
+    tb = tag.encode()
+    check(lib().tkv_hash_chains(tokens_dev.data_ptr(), chains_dev.data_ptr(), n_chains, chunk_size, tb,
+                                len(tb), out_dev.data_ptr(), s))
+
+
+class Engine:
+    """Device pages + pinned host tier + connector (one engine stack)."""
+
+    def __init__(self, num_layers: int, bpt: int, page_tokens: int, tag: str, chunk_size: int,
+                 ram_slots: int, num_pages: int, layerwise: bool = True, staging_budget: int = 64 << 20,
+                 io_threads: int = 2, store_io_threads: int = 4, pin_stores: bool = False,
+                 staging_depth: int = 2, load_zero_copy: bool = False, store_ctas: int = 0,
+                 load_ctas: int = 0, device: int = 0, stream: torch.cuda.Stream | None = None):
+        del io_threads, store_io_threads  # host thread pools do not exist on this path
+        self.L = lib()
+        self.num_layers, self.bpt, self.page_tokens = num_layers, bpt, page_tokens
+        self.tag, self.chunk_size = tag, chunk_size
+        self.device = device
+        torch.cuda.set_device(device)
+        self.stream = stream
+        self._tag_b = tag.encode()
+        spec = ModelSpecC(num_layers, bpt, page_tokens, 32000, self._tag_b)
+        self.pages = ct.c_void_p()
+        self.store = ct.c_void_p()
+        self.conn = ct.c_void_p()
+        check(self.L.tkv_pages_create(ct.byref(spec), num_pages, device, ct.byref(self.pages)))
+        ram = ram_slots * num_layers * chunk_size * bpt
+        check(self.L.tkv_store_create(ct.byref(spec), chunk_size, ram, ct.byref(self.store)))
+        cfg = ConnectorConfigC()
+        self.L.tkv_connector_config_default(ct.byref(cfg))
+        cfg.layerwise = int(layerwise)
+        cfg.pin_stores = int(pin_stores)
+        cfg.staging_budget_bytes = staging_budget
+        cfg.staging_depth = staging_depth
+        cfg.load_zero_copy = int(load_zero_copy)
+        if store_ctas:
+            cfg.store_ctas = store_ctas
+        cfg.load_ctas = load_ctas
+        cfg.engine_stream = self.stream_handle
+        check(self.L.tkv_connector_create(self.store, self.pages, ct.byref(cfg), ct.byref(self.conn)))
+        self._metas: list[ct.c_void_p | None] = []
+        self._dev_prompts: dict[int, torch.Tensor] = {}
+        self._mism = torch.zeros(1, dtype=torch.int64, device=f"cuda:{device}")
+
+    @property
+    def stream_handle(self):
+        return self.stream.cuda_stream if self.stream is not None else None
+
+    def close(self):
+        if getattr(self, "conn", None):
+            for i in range(len(self._metas)):
+                self.drop_meta(i)
+            self.L.tkv_connector_destroy(self.conn)
+            self.conn = None
+            self.L.tkv_store_destroy(self.store)
+            self.L.tkv_pages_destroy(self.pages)
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def synchronize(self):
+        torch.cuda.synchronize(self.device)
+
+    # --- engine-side helpers (mirror oracle.RefEngine) ---
+    def bind_pages(self, qid: int, tokens: int) -> int:
+        blocks = (tokens + self.page_tokens - 1) // self.page_tokens
+        ids = np.zeros(max(1, blocks * self.num_layers), np.uint32)
+        rc = self.L.tkv_pages_alloc(self.pages, qid, blocks * self.num_layers, ids.ctypes.data_as(u32p))
+        if rc:
+            return rc
+        for layer in range(self.num_layers):
+            sl = np.ascontiguousarray(ids[layer * blocks:(layer + 1) * blocks])
+            check(self.L.tkv_pages_bind_layer(self.pages, qid, layer, sl.ctypes.data_as(u32p), blocks))
+        return 0
+
+    def layer_pages(self, qid: int, layer: int) -> np.ndarray:
+        n = self.L.tkv_pages_layer_pages(self.pages, qid, layer, None, 0)
+        out = np.zeros(max(1, n), np.uint32)
+        self.L.tkv_pages_layer_pages(self.pages, qid, layer, out.ctypes.data_as(u32p), n)
+        return out[:n]
+
+    def release_query(self, qid: int) -> int:
+        self.synchronize()
+        self._dev_prompts.pop(qid, None)
+        return self.L.tkv_pages_release(self.pages, qid)
+
+    def free_page_count(self) -> int:
+        return self.L.tkv_pages_free_count(self.pages)
+
+    def dev_prompt(self, qid: int, prompt) -> torch.Tensor:
+        t = _tokens(prompt)
+        cur = self._dev_prompts.get(qid)
+        if cur is None or cur.numel() != t.size:
+            cur = torch.from_numpy(t.view(np.int32)).to(f"cuda:{self.device}", non_blocking=False)
+            self._dev_prompts[qid] = cur
+        return cur
+
+    def compute_range(self, qid: int, prompt, start: int, end: int, layers=None) -> None:
+        """Engine compute stand-in: synth KV for [start, end) into pages (K4)."""
+        if end <= start:
+            return
+        toks = self.dev_prompt(qid, prompt)
+        l0, l1 = layers if layers is not None else (0, self.num_layers)
+        check(self.L.tkv_pages_compute(self.pages, qid, toks.data_ptr(), start, end, l0, l1,
+                                       self.stream_handle))
+
+    def verify_range(self, qid: int, prompt, start: int, end: int) -> int:
+        """Device byte oracle: number of 8-byte words differing from synth."""
+        toks = self.dev_prompt(qid, prompt)
+        self._mism.zero_()
+        self.synchronize()
+        check(self.L.tkv_pages_verify(self.pages, qid, toks.data_ptr(), start, end, 0, self.num_layers,
+                                      self._mism.data_ptr(), self.stream_handle))
+        self.synchronize()
+        return int(self._mism.item())
+
+    def gather_layer(self, qid: int, layer: int, n: int) -> np.ndarray:
+        pages = self.layer_pages(qid, layer)
+        pages = np.ascontiguousarray(pages[:(n + self.page_tokens - 1) // self.page_tokens])
+        out = np.zeros(max(1, n * self.bpt), np.uint8)
+        check(self.L.tkv_pages_gather(self.pages, pages.ctypes.data_as(u32p), pages.size, layer, n,
+                                      out.ctypes.data_as(u8p), n * self.bpt))
+        return out[:n * self.bpt]
+
+    def seed_store(self, prompt, n: int) -> None:
+        """Store device-synthesized chunk payloads for prompt[0, n)."""
+        t = _tokens(prompt)[:n]
+        keys = chunk_keys(t, self.chunk_size, self.tag)
+        dev = torch.from_numpy(t.view(np.int32)).to(f"cuda:{self.device}")
+        seed = _model_seed(self.tag)
+        for i, k in enumerate(keys):
+            s = i * self.chunk_size
+            cnt = min(self.chunk_size, n - s)
+            buf = torch.empty(self.num_layers * cnt * self.bpt, dtype=torch.uint8, device=dev.device)
+            check(self.L.tkv_synth_chunk(dev.data_ptr(), seed, s, cnt, self.num_layers, self.bpt,
+                                         buf.data_ptr(), None))
+            host = buf.cpu().numpy()
+            d = _u8(k)
+            check(self.L.tkv_store_put(self.store, d.ctypes.data_as(u8p), cnt, host.ctypes.data_as(u8p),
+                                       host.size, 0))
+
+    # --- connector ---
+    def get_num_new_matched_tokens(self, qid: int, prompt) -> int:
+        t = _tokens(prompt)
+        m = ct.c_size_t(0)
+        check(self.L.tkv_connector_get_num_new_matched_tokens(self.conn, qid, t.ctypes.data_as(u32p), t.size,
+                                                              ct.byref(m)))
+        return m.value
+
+    def lookup_batch(self, qids, prompts) -> list[int]:
+        arrs = [_tokens(p) for p in prompts]
+        ids = (ct.c_uint64 * len(arrs))(*qids)
+        ptrs = (u32p * len(arrs))(*[a.ctypes.data_as(u32p) for a in arrs])
+        lens = (ct.c_size_t * len(arrs))(*[a.size for a in arrs])
+        out = (ct.c_size_t * len(arrs))()
+        check(self.L.tkv_connector_lookup_batch(self.conn, len(arrs), ids, ptrs, lens, out))
+        return list(out)
+
+    def update_state_after_alloc(self, qid: int, blocks: int, ext: int) -> int:
+        return self.L.tkv_connector_update_state_after_alloc(self.conn, qid, blocks, ext)
+
+    def build_connector_meta(self, queries) -> int:
+        arrs = [_tokens(p) for _, p in queries]
+        ids = (ct.c_uint64 * len(arrs))(*[q for q, _ in queries])
+        ptrs = (u32p * len(arrs))(*[a.ctypes.data_as(u32p) for a in arrs])
+        lens = (ct.c_size_t * len(arrs))(*[a.size for a in arrs])
+        m = ct.c_void_p()
+        check(self.L.tkv_connector_build_meta(self.conn, len(arrs), ids, ptrs, lens, ct.byref(m)))
+        self._metas.append(m)
+        return len(self._metas) - 1
+
+    def start_load_kv(self, m: int) -> int:
+        return self.L.tkv_connector_start_load_kv(self.conn, self._metas[m])
+
+    def wait_load_kv(self, m: int, layer: int) -> int:
+        return self.L.tkv_connector_wait_load_kv(self.conn, self._metas[m], layer)
+
+    def start_store_kv(self, m: int) -> int:
+        return self.L.tkv_connector_start_store_kv(self.conn, self._metas[m])
+
+    def wait_store_kv(self, m: int, layer: int) -> int:
+        return self.L.tkv_connector_wait_store_kv(self.conn, self._metas[m], layer)
+
+    def meta_layerwise(self, m: int) -> bool:
+        return bool(self.L.tkv_meta_layerwise(self._metas[m]))
+
+    def loaded_tokens(self, m: int, qid: int) -> int:
+        return int(self.L.tkv_meta_loaded_tokens(self._metas[m], qid))
+
+    def plan(self, m: int, qi: int, kind: str):
+        cap = 1 << 14
+        spans = np.zeros(4 * cap, np.uint64)
+        dig = np.zeros(32 * cap, np.uint8)
+        n = ct.c_size_t(0)
+        matched = ct.c_uint64(0)
+        check(self.L.tkv_meta_plan(self._metas[m], qi, 0 if kind == "load" else 1, spans.ctypes.data_as(u64p),
+                                   dig.ctypes.data_as(u8p), cap, ct.byref(n), ct.byref(matched)))
+        out = [(int(spans[4 * i]), int(spans[4 * i + 1]), int(spans[4 * i + 2]), int(spans[4 * i + 3]),
+                dig[32 * i:32 * i + 32].tobytes()) for i in range(n.value)]
+        return out, int(matched.value)
+
+    def store_results(self, m: int, qid: int):
+        cap = 1 << 14
+        codes = (ct.c_int * cap)()
+        dig = np.zeros(32 * cap, np.uint8)
+        n = ct.c_size_t(0)
+        check(self.L.tkv_meta_store_results(self._metas[m], qid, codes, dig.ctypes.data_as(u8p), cap,
+                                            ct.byref(n)))
+        return [(dig[32 * i:32 * i + 32].tobytes(), int(codes[i])) for i in range(n.value)]
+
+    def begin_decode(self, qid: int) -> int:
+        return self.L.tkv_connector_begin_decode(self.conn, qid)
+
+    def append_decode(self, qid: int, token: int) -> int:
+        return self.L.tkv_connector_append_decode(self.conn, qid, token)
+
+    def finish_query(self, qid: int) -> int:
+        keys, rc = self.finish_query_keys(qid)
+        return rc
+
+    def finish_query_keys(self, qid: int):
+        cap = 4096
+        dig = np.zeros(32 * cap, np.uint8)
+        n = ct.c_size_t(0)
+        rc = self.L.tkv_connector_finish_query(self.conn, qid, dig.ctypes.data_as(u8p), cap, ct.byref(n))
+        return [dig[32 * i:32 * i + 32].tobytes() for i in range(n.value)], rc
+
+    def drop_meta(self, m: int) -> None:
+        h = self._metas[m]
+        if h is not None:
+            self.L.tkv_meta_destroy(h)
+            self._metas[m] = None
+
+    def staging_peak(self) -> int:
+        return int(self.L.tkv_connector_staging_peak(self.conn))
+
+    def hash_launches(self) -> int:
+        return int(self.L.tkv_connector_hash_launches(self.conn))
+
+    # --- store ---
+    def contains(self, digest: bytes) -> bool:
+        d = _u8(digest)
+        return bool(self.L.tkv_store_contains(self.store, d.ctypes.data_as(u8p)))
+
+    def store_get(self, digest: bytes) -> np.ndarray | None:
+        self.synchronize()
+        d = _u8(digest)
+        n = ct.c_size_t(0)
+        rc = self.L.tkv_store_get(self.store, d.ctypes.data_as(u8p), None, 0, ct.byref(n))
+        if rc:
+            return None
+        out = np.zeros(n.value, np.uint8)
+        check(self.L.tkv_store_get(self.store, d.ctypes.data_as(u8p), out.ctypes.data_as(u8p), n.value,
+                                   ct.byref(n)))
+        return out
+
+    def store_clear(self, digest: bytes) -> int:
+        d = _u8(digest)
+        removed = ct.c_size_t(0)
+        refused = ct.c_size_t(0)
+        check(self.L.tkv_store_clear(self.store, d.ctypes.data_as(u8p), 1, ct.byref(removed), ct.byref(refused)))
+        return removed.value
+
+    def store_entries(self) -> int:
+        out = (ct.c_size_t * 4)()
+        check(self.L.tkv_store_stats(self.store, out))
+        return int(out[0])
+
+    def layout(self) -> PagedLayoutC:
+        L = PagedLayoutC()
+        check(self.L.tkv_pages_layout(self.pages, ct.byref(L)))
+        return L
+
+    def device_table(self, qid: int):
+        ptr = ct.c_void_p()
+        stride = ct.c_uint32(0)
+        check(self.L.tkv_pages_device_table(self.pages, qid, self.stream_handle, ct.byref(ptr), ct.byref(stride)))
+        return ptr.value, stride.value
+
+
+def _model_seed(tag: str) -> int:
+    """fnv1a64(model_tag) (synth.hpp:27-30): a per-model constant."""
+    h = 0xcbf29ce484222325
+    for b in tag.encode():
+        h ^= b
+        h = (h * 0x100000001b3) & 0xFFFFFFFFFFFFFFFF
+    return h

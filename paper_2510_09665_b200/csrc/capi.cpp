@@ -1,0 +1,534 @@
+// extern "C" boundary (include/tierkv_b200.h) over the host C++ mirror.
+#include "../../include/tierkv_b200.h"
+
+#include <cstring>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <string>
+
+#include "connector.hpp"
+#include "kernels.hpp"
+#include "paged_store.hpp"
+#include "store.hpp"
+#include "tokens.hpp"
+
+using namespace tkv;
+
+static_assert(sizeof(tkv_paged_layout) == sizeof(PagedLayout));
+static_assert(sizeof(tkv_xfer_desc) == sizeof(XferDesc));
+static_assert(sizeof(tkv_chain_desc) == sizeof(ChainDesc));
+
+struct tkv_pages {
+    std::unique_ptr<PagedKVStore> p;
+};
+struct tkv_store {
+    std::unique_ptr<TieredStore> s;
+};
+struct tkv_connector {
+    std::unique_ptr<Connector> c;
+};
+struct tkv_meta {
+    ConnectorMetadata m;
+};
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(Errc c, const std::string& msg) {
+    g_err = msg;
+    return int(c);
+}
+int st(const Status& s) {
+    if (!s.ok()) g_err = s.to_string();
+    return int(s.code);
+}
+
+template <typename F>
+int guard(F&& f) {
+    try {
+        return f();
+    } catch (const CudaError& e) {
+        return fail(Errc::cuda_error, e.what());
+    } catch (const std::invalid_argument& e) {
+        return fail(Errc::invalid_argument, e.what());
+    } catch (const std::exception& e) {
+        return fail(Errc::io_error, e.what());
+    }
+}
+
+int cuda(cudaError_t e) {
+    if (e == cudaSuccess) return 0;
+    return fail(Errc::cuda_error, cudaGetErrorString(e));
+}
+
+ModelSpec to_spec(const tkv_model_spec* s) {
+    ModelSpec m;
+    m.num_layers = s->num_layers;
+    m.bytes_per_token_per_layer = s->bytes_per_token_per_layer;
+    m.page_tokens = s->page_tokens;
+    m.vocab_size = s->vocab_size ? s->vocab_size : 32000;
+    m.model_tag = s->model_tag ? s->model_tag : "";
+    return m;
+}
+
+Digest to_digest(const uint8_t* p) {
+    Digest d;
+    std::memcpy(d.data(), p, 32);
+    return d;
+}
+
+PagedLayout to_layout(const tkv_paged_layout* l) {
+    PagedLayout L;
+    std::memcpy(&L, l, sizeof L);
+    return L;
+}
+
+std::mutex g_hashers_mu;
+std::map<std::pair<std::string, size_t>, std::unique_ptr<KeyHasher>> g_hashers;
+KeyHasher& hasher_for(const char* tag, size_t cs) {
+    std::lock_guard lock(g_hashers_mu);
+    int dev = 0;
+    cudaGetDevice(&dev);
+    auto key = std::make_pair(std::string(tag) + "#" + std::to_string(dev), cs);
+    auto& h = g_hashers[key];
+    if (!h) h = std::make_unique<KeyHasher>(tag, cs);
+    return *h;
+}
+
+std::vector<std::vector<TokenId>> to_queries(size_t n, const uint32_t* const* prompts,
+                                             const size_t* lens) {
+    std::vector<std::vector<TokenId>> v(n);
+    for (size_t i = 0; i < n; ++i) v[i].assign(prompts[i], prompts[i] + lens[i]);
+    return v;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* tkv_last_error(void) { return g_err.c_str(); }
+const char* tkv_errc_name(int code) { return errc_name(Errc(code)); }
+const char* tkv_build_info(void) { return "tierkv_b200 sm_100a " __DATE__ " " __TIME__; }
+
+// ---- kernel level -----------------------------------------------------------
+
+int tkv_plan_tiles(const tkv_xfer_desc* descs, uint32_t n, uint32_t page_tokens,
+                   uint32_t page_bytes, uint32_t ppt, uint32_t n_layers, uint32_t* tb,
+                   uint32_t* ppt_out) {
+    if (!page_tokens) return fail(Errc::invalid_argument, "page_tokens == 0");
+    if (ppt == 0) {
+        size_t p = 65536 / (page_bytes ? page_bytes : 1);
+        ppt = uint32_t(p < 1 ? 1 : (p > 64 ? 64 : p));
+    }
+    tb[0] = 0;
+    for (uint32_t i = 0; i < n; ++i)
+        tb[i + 1] = tb[i] + tiles_for(descs[i].n_tokens, page_tokens, ppt, n_layers);
+    if (ppt_out) *ppt_out = ppt;
+    return 0;
+}
+
+static int paged(const tkv_paged_layout* layout, const tkv_xfer_desc* descs, const uint32_t* tb,
+                 uint32_t n_desc, uint32_t tiles, uint32_t l0, uint32_t nl, uint32_t ppt,
+                 uint64_t addr_or, int ctas, void* stream, CopyDir dir) {
+    PagedCopyPlan P;
+    P.descs = reinterpret_cast<const XferDesc*>(descs);
+    P.tile_base = tb;
+    P.n_desc = n_desc;
+    P.total_tiles = tiles;
+    P.layer_begin = l0;
+    P.n_layers = nl;
+    P.pages_per_tile = ppt;
+    P.addr_or = addr_or;
+    return cuda(launch_paged_copy(to_layout(layout), P, dir, ctas, cudaStream_t(stream)));
+}
+
+int tkv_gather_layers(const tkv_paged_layout* layout, const tkv_xfer_desc* descs, const uint32_t* tb,
+                      uint32_t n_desc, uint32_t tiles, uint32_t l0, uint32_t nl, uint32_t ppt,
+                      uint64_t addr_or, int ctas, void* stream) {
+    return paged(layout, descs, tb, n_desc, tiles, l0, nl, ppt, addr_or, ctas, stream,
+                 CopyDir::gather);
+}
+
+int tkv_scatter_layers(const tkv_paged_layout* layout, const tkv_xfer_desc* descs,
+                       const uint32_t* tb, uint32_t n_desc, uint32_t tiles, uint32_t l0,
+                       uint32_t nl, uint32_t ppt, uint64_t addr_or, int ctas, void* stream) {
+    return paged(layout, descs, tb, n_desc, tiles, l0, nl, ppt, addr_or, ctas, stream,
+                 CopyDir::scatter);
+}
+
+int tkv_hash_chains(const uint32_t* tokens, const tkv_chain_desc* chains, uint32_t n_chains,
+                    uint32_t chunk_size, const char* tag, uint32_t tag_len, uint8_t* out,
+                    void* stream) {
+    if (tag_len > uint32_t(kMaxTagBytes)) return fail(Errc::invalid_argument, "tag too long");
+    HashParams p;
+    p.chunk_size = chunk_size;
+    p.tag_len = tag_len;
+    std::memcpy(p.tag, tag, tag_len);
+    return cuda(launch_hash_chains(tokens, reinterpret_cast<const ChainDesc*>(chains), n_chains, p,
+                                   out, cudaStream_t(stream)));
+}
+
+static SynthArgs synth_args(const uint32_t* tokens, const int32_t* table, uint32_t stride,
+                            uint64_t seed, uint32_t p0, uint32_t p1, uint32_t l0, uint32_t l1) {
+    SynthArgs a;
+    a.tokens = tokens;
+    a.table = table;
+    a.table_stride = stride;
+    a.seed = seed;
+    a.pos_begin = p0;
+    a.pos_end = p1;
+    a.layer_begin = l0;
+    a.layer_end = l1;
+    return a;
+}
+
+int tkv_synth_pages(const tkv_paged_layout* layout, const uint32_t* tokens, const int32_t* table,
+                    uint32_t stride, uint64_t seed, uint32_t p0, uint32_t p1, uint32_t l0,
+                    uint32_t l1, void* stream) {
+    return cuda(launch_synth_pages(to_layout(layout), synth_args(tokens, table, stride, seed, p0, p1, l0, l1),
+                                   cudaStream_t(stream)));
+}
+
+int tkv_verify_pages(const tkv_paged_layout* layout, const uint32_t* tokens, const int32_t* table,
+                     uint32_t stride, uint64_t seed, uint32_t p0, uint32_t p1, uint32_t l0,
+                     uint32_t l1, unsigned long long* mism, void* stream) {
+    return cuda(launch_verify_pages(to_layout(layout),
+                                    synth_args(tokens, table, stride, seed, p0, p1, l0, l1), mism,
+                                    cudaStream_t(stream)));
+}
+
+int tkv_synth_chunk(const uint32_t* tokens, uint64_t seed, uint32_t start, uint32_t n,
+                    uint32_t n_layers, uint32_t bpt, uint8_t* out, void* stream) {
+    return cuda(launch_synth_chunk(tokens, seed, start, n, n_layers, bpt, out, cudaStream_t(stream)));
+}
+
+// ---- keys -------------------------------------------------------------------
+
+int tkv_chunk_keys(const char* tag, size_t cs, const uint32_t* tokens, size_t n, uint8_t* out,
+                   size_t* n_chunks) {
+    return guard([&] {
+        auto keys = chunk_keys(hasher_for(tag, cs), TokenSpanView(tokens, n));
+        for (size_t i = 0; i < keys.size(); ++i) std::memcpy(out + 32 * i, keys[i].digest.data(), 32);
+        *n_chunks = keys.size();
+        return 0;
+    });
+}
+
+int tkv_keychain_next(const char* tag, size_t cs, const uint8_t* parent, const uint32_t* tokens,
+                      size_t n, uint8_t* out) {
+    return guard([&] {
+        KeyChain chain(hasher_for(tag, cs));
+        chain.reset(to_digest(parent), 0);
+        auto k = chain.next(TokenSpanView(tokens, n));
+        std::memcpy(out, k.digest.data(), 32);
+        return 0;
+    });
+}
+
+// ---- pages ------------------------------------------------------------------
+
+int tkv_pages_create(const tkv_model_spec* spec, uint32_t num_pages, int device, tkv_pages** out) {
+    return guard([&] {
+        if (device >= 0) TKV_CUDA(cudaSetDevice(device));
+        auto* p = new tkv_pages;
+        p->p = std::make_unique<PagedKVStore>(to_spec(spec), num_pages, device);
+        *out = p;
+        return 0;
+    });
+}
+void tkv_pages_destroy(tkv_pages* p) {
+    if (p) cudaDeviceSynchronize();
+    delete p;
+}
+int tkv_pages_alloc(tkv_pages* p, uint64_t q, size_t n, uint32_t* ids) {
+    return guard([&] {
+        auto r = p->p->alloc_pages(q, n);
+        if (!r.ok()) return st(r.status());
+        std::memcpy(ids, r.value().data(), n * sizeof(uint32_t));
+        return 0;
+    });
+}
+int tkv_pages_bind_layer(tkv_pages* p, uint64_t q, uint32_t layer, const uint32_t* ids, size_t n) {
+    return guard([&] {
+        p->p->bind_layer(q, layer, std::vector<PageId>(ids, ids + n));
+        return 0;
+    });
+}
+size_t tkv_pages_layer_pages(tkv_pages* p, uint64_t q, uint32_t layer, uint32_t* ids, size_t cap) {
+    auto v = p->p->layer_pages(q, layer);
+    if (ids) std::memcpy(ids, v.data(), std::min(cap, v.size()) * sizeof(uint32_t));
+    return v.size();
+}
+size_t tkv_pages_release(tkv_pages* p, uint64_t q) { return p->p->release_query(q).size(); }
+size_t tkv_pages_free_count(tkv_pages* p) { return p->p->free_page_count(); }
+size_t tkv_pages_allocated_count(tkv_pages* p) { return p->p->allocated_page_count(); }
+size_t tkv_pages_pool_pages(tkv_pages* p) { return p->p->pool_pages(); }
+int tkv_pages_mark_populated(tkv_pages* p, uint32_t page, uint32_t layer) {
+    if (page >= p->p->pool_pages()) return fail(Errc::invalid_argument, "page id out of range");
+    p->p->mark_populated(page, layer);
+    return 0;
+}
+int tkv_pages_populated(tkv_pages* p, uint32_t page) {
+    return page < p->p->pool_pages() && p->p->populated(page);
+}
+int tkv_pages_gather(tkv_pages* p, const uint32_t* ids, size_t n_ids, uint32_t layer, size_t tokens,
+                     uint8_t* out, size_t out_bytes) {
+    return guard([&] {
+        TKV_CUDA(cudaDeviceSynchronize());
+        return st(p->p->gather_tokens_into(std::vector<PageId>(ids, ids + n_ids), layer, tokens, out,
+                                           out_bytes));
+    });
+}
+int tkv_pages_scatter(tkv_pages* p, const uint8_t* buf, size_t bytes, const uint32_t* ids,
+                      size_t n_ids, uint32_t layer, size_t tokens) {
+    return guard([&] {
+        TKV_CUDA(cudaDeviceSynchronize());
+        return st(p->p->scatter_tokens(buf, bytes, std::vector<PageId>(ids, ids + n_ids), layer, tokens));
+    });
+}
+int tkv_pages_layout(tkv_pages* p, tkv_paged_layout* out) {
+    PagedLayout L = p->p->layout();
+    std::memcpy(out, &L, sizeof L);
+    return 0;
+}
+int tkv_pages_device_table(tkv_pages* p, uint64_t q, void* stream, const int32_t** table,
+                           uint32_t* stride) {
+    return guard([&] {
+        auto t = p->p->device_table(q, cudaStream_t(stream));
+        if (!t.ok()) return st(t.status());
+        *table = t.value().ptr;
+        *stride = t.value().stride;
+        return 0;
+    });
+}
+
+static int pages_synth(tkv_pages* p, uint64_t q, const uint32_t* tokens, uint32_t from, uint32_t to,
+                       uint32_t l0, uint32_t l1, unsigned long long* mism, void* stream) {
+    return guard([&] {
+        const auto& sp = p->p->spec();
+        if (l1 > sp.num_layers || l0 > l1 || from > to)
+            return fail(Errc::invalid_argument, "range");
+        for (uint32_t l = l0; l < l1; ++l) {
+            const size_t have = p->p->layer_pages(q, l).size() * sp.page_tokens;
+            if (to > have) return fail(Errc::size_mismatch, "positions beyond the query's pages");
+        }
+        auto t = p->p->device_table(q, cudaStream_t(stream));
+        if (!t.ok()) return st(t.status());
+        SynthArgs a = synth_args(tokens, t.value().ptr, t.value().stride, sp.model_seed(), from, to, l0, l1);
+        if (mism) return cuda(launch_verify_pages(p->p->layout(), a, mism, cudaStream_t(stream)));
+        int rc = cuda(launch_synth_pages(p->p->layout(), a, cudaStream_t(stream)));
+        if (rc) return rc;
+        if (to > from) {
+            const uint32_t pt = sp.page_tokens;
+            for (uint32_t l = l0; l < l1; ++l) {
+                auto list = p->p->layer_pages(q, l);
+                for (uint32_t pg = from / pt; pg <= (to - 1) / pt; ++pg) p->p->mark_populated(list[pg], l);
+            }
+        }
+        return 0;
+    });
+}
+
+int tkv_pages_compute(tkv_pages* p, uint64_t q, const uint32_t* tokens, uint32_t from, uint32_t to,
+                      uint32_t l0, uint32_t l1, void* stream) {
+    return pages_synth(p, q, tokens, from, to, l0, l1, nullptr, stream);
+}
+int tkv_pages_verify(tkv_pages* p, uint64_t q, const uint32_t* tokens, uint32_t from, uint32_t to,
+                     uint32_t l0, uint32_t l1, unsigned long long* mism, void* stream) {
+    if (!mism) return fail(Errc::invalid_argument, "null mismatch counter");
+    return pages_synth(p, q, tokens, from, to, l0, l1, mism, stream);
+}
+
+// ---- store ------------------------------------------------------------------
+
+int tkv_store_create(const tkv_model_spec* spec, size_t chunk_size, size_t ram_bytes, tkv_store** out) {
+    return guard([&] {
+        StoreConfig cfg;
+        cfg.model = to_spec(spec);
+        cfg.chunk_size = chunk_size;
+        cfg.ram_pool_bytes = ram_bytes;
+        auto* s = new tkv_store;
+        s->s = std::make_unique<TieredStore>(cfg);
+        *out = s;
+        return 0;
+    });
+}
+void tkv_store_destroy(tkv_store* s) { delete s; }
+int tkv_store_put(tkv_store* s, const uint8_t* digest, uint32_t tokens, const uint8_t* payload,
+                  size_t bytes, int pin) {
+    return guard([&] { return st(s->s->put(to_digest(digest), tokens, payload, bytes, pin != 0).wait()); });
+}
+int tkv_store_get(tkv_store* s, const uint8_t* digest, uint8_t* out, size_t cap, size_t* n) {
+    return guard([&] {
+        auto r = s->s->get(to_digest(digest));
+        if (!r.ok()) return st(r.status());
+        *n = r.value().size();
+        if (out && r.value().size() <= cap) std::memcpy(out, r.value().data(), r.value().size());
+        return 0;
+    });
+}
+int tkv_store_get_layer(tkv_store* s, const uint8_t* digest, uint32_t layer, uint8_t* out,
+                        size_t cap, size_t* n) {
+    return guard([&] {
+        auto r = s->s->get_layer(to_digest(digest), layer);
+        if (!r.ok()) return st(r.status());
+        *n = r.value().size();
+        if (out && r.value().size() <= cap) std::memcpy(out, r.value().data(), r.value().size());
+        return 0;
+    });
+}
+int tkv_store_contains(tkv_store* s, const uint8_t* digest) { return s->s->contains(to_digest(digest)); }
+int tkv_store_pin(tkv_store* s, const uint8_t* digest, int on) {
+    return st(s->s->pin(to_digest(digest), on != 0));
+}
+int tkv_store_clear(tkv_store* s, const uint8_t* digests, size_t n, size_t* removed, size_t* refused) {
+    std::vector<Digest> v(n);
+    for (size_t i = 0; i < n; ++i) v[i] = to_digest(digests + 32 * i);
+    auto r = s->s->clear(v);
+    if (removed) *removed = r.removed;
+    if (refused) *refused = r.refused;
+    return 0;
+}
+int tkv_store_stats(tkv_store* s, size_t out[4]) {
+    auto r = s->s->stats();
+    out[0] = r.entries;
+    out[1] = r.ram_slots_total;
+    out[2] = r.ram_slots_used;
+    out[3] = r.ram_entries;
+    return 0;
+}
+
+// ---- connector --------------------------------------------------------------
+
+void tkv_connector_config_default(tkv_connector_config* cfg) {
+    Connector::Config d;
+    cfg->layerwise = d.mode == TransferMode::layerwise;
+    cfg->pin_stores = d.pin_stores;
+    cfg->staging_budget_bytes = d.staging_budget_bytes;
+    cfg->staging_depth = d.staging_depth;
+    cfg->load_zero_copy = d.load_path == LoadPath::zero_copy;
+    cfg->store_ctas = d.store_ctas;
+    cfg->load_ctas = d.load_ctas;
+    cfg->engine_stream = d.engine_stream;
+}
+
+int tkv_connector_create(tkv_store* s, tkv_pages* p, const tkv_connector_config* cfg,
+                         tkv_connector** out) {
+    return guard([&] {
+        Connector::Config c;
+        if (cfg) {
+            c.mode = cfg->layerwise ? TransferMode::layerwise : TransferMode::blocking;
+            c.pin_stores = cfg->pin_stores != 0;
+            c.staging_budget_bytes = cfg->staging_budget_bytes;
+            c.staging_depth = cfg->staging_depth;
+            c.load_path = cfg->load_zero_copy ? LoadPath::zero_copy : LoadPath::copy_engine;
+            c.store_ctas = cfg->store_ctas > 0 ? cfg->store_ctas : c.store_ctas;
+            c.load_ctas = cfg->load_ctas;
+            c.engine_stream = cudaStream_t(cfg->engine_stream);
+        }
+        auto* h = new tkv_connector;
+        h->c = std::make_unique<Connector>(*s->s, *p->p, c);
+        *out = h;
+        return 0;
+    });
+}
+void tkv_connector_destroy(tkv_connector* c) { delete c; }
+
+int tkv_connector_get_num_new_matched_tokens(tkv_connector* c, uint64_t q, const uint32_t* tokens,
+                                             size_t n, size_t* matched) {
+    return guard([&] {
+        *matched = c->c->get_num_new_matched_tokens(q, TokenSpanView(tokens, n));
+        return 0;
+    });
+}
+int tkv_connector_lookup_batch(tkv_connector* c, size_t nq, const uint64_t* ids,
+                               const uint32_t* const* prompts, const size_t* lens, size_t* matched) {
+    return guard([&] {
+        std::vector<QueryId> q(ids, ids + nq);
+        std::vector<TokenSpanView> v(nq);
+        for (size_t i = 0; i < nq; ++i) v[i] = TokenSpanView(prompts[i], lens[i]);
+        auto r = c->c->get_num_new_matched_tokens(q, v);
+        std::memcpy(matched, r.data(), nq * sizeof(size_t));
+        return 0;
+    });
+}
+int tkv_connector_update_state_after_alloc(tkv_connector* c, uint64_t q, size_t blocks, size_t ext) {
+    return guard([&] { return st(c->c->update_state_after_alloc(q, blocks, ext)); });
+}
+int tkv_connector_build_meta(tkv_connector* c, size_t nq, const uint64_t* ids,
+                             const uint32_t* const* prompts, const size_t* lens, tkv_meta** out) {
+    return guard([&] {
+        SchedulerOutput so;
+        auto qs = to_queries(nq, prompts, lens);
+        for (size_t i = 0; i < nq; ++i) so.queries.push_back({ids[i], std::move(qs[i])});
+        auto* m = new tkv_meta;
+        m->m = c->c->build_connector_meta(so);
+        *out = m;
+        return 0;
+    });
+}
+int tkv_connector_start_load_kv(tkv_connector* c, tkv_meta* m) {
+    return guard([&] { return st(c->c->start_load_kv(m->m)); });
+}
+int tkv_connector_wait_load_kv(tkv_connector* c, tkv_meta* m, uint32_t layer) {
+    return guard([&] { return st(c->c->wait_load_kv(m->m, layer)); });
+}
+int tkv_connector_start_store_kv(tkv_connector* c, tkv_meta* m) {
+    return guard([&] { return st(c->c->start_store_kv(m->m)); });
+}
+int tkv_connector_wait_store_kv(tkv_connector* c, tkv_meta* m, uint32_t layer) {
+    return guard([&] { return st(c->c->wait_store_kv(m->m, layer)); });
+}
+int tkv_connector_begin_decode(tkv_connector* c, uint64_t q) {
+    return guard([&] { return st(c->c->begin_decode(q)); });
+}
+int tkv_connector_append_decode(tkv_connector* c, uint64_t q, uint32_t token) {
+    return guard([&] { return st(c->c->append_decode(q, token)); });
+}
+int tkv_connector_finish_query(tkv_connector* c, uint64_t q, uint8_t* out, size_t cap, size_t* n) {
+    return guard([&] {
+        auto r = c->c->finish_query(q);
+        if (!r.ok()) return st(r.status());
+        *n = r.value().size();
+        for (size_t i = 0; i < r.value().size() && i < cap; ++i)
+            std::memcpy(out + 32 * i, r.value()[i].digest.data(), 32);
+        return 0;
+    });
+}
+size_t tkv_connector_staging_peak(tkv_connector* c) { return c->c->staging_peak_bytes(); }
+uint64_t tkv_connector_hash_launches(tkv_connector* c) { return c->c->hasher().launches(); }
+
+void tkv_meta_destroy(tkv_meta* m) { delete m; }
+int tkv_meta_layerwise(tkv_meta* m) { return m->m.mode() == TransferMode::layerwise; }
+size_t tkv_meta_loaded_tokens(tkv_meta* m, uint64_t q) { return m->m.loaded_tokens(q); }
+size_t tkv_meta_num_plans(tkv_meta* m) { return m->m.plans().size(); }
+int tkv_meta_plan(tkv_meta* m, size_t qi, int kind, uint64_t* spans, uint8_t* digests, size_t cap,
+                  size_t* n, uint64_t* matched) {
+    const auto& plans = m->m.plans();
+    if (qi >= plans.size()) return fail(Errc::invalid_argument, "plan index");
+    const auto& v = kind == 0 ? plans[qi].load_plan : plans[qi].store_plan;
+    if (matched) *matched = plans[qi].matched_tokens;
+    *n = v.size();
+    for (size_t i = 0; i < v.size() && i < cap; ++i) {
+        spans[4 * i] = v[i].span.start;
+        spans[4 * i + 1] = v[i].span.end;
+        spans[4 * i + 2] = v[i].record_tokens;
+        spans[4 * i + 3] = v[i].key.chunk_index;
+        std::memcpy(digests + 32 * i, v[i].key.digest.data(), 32);
+    }
+    return 0;
+}
+int tkv_meta_store_results(tkv_meta* m, uint64_t q, int* codes, uint8_t* digests, size_t cap,
+                           size_t* n) {
+    auto r = m->m.store_results(q);
+    *n = r.size();
+    for (size_t i = 0; i < r.size() && i < cap; ++i) {
+        codes[i] = int(r[i].second.code);
+        std::memcpy(digests + 32 * i, r[i].first.digest.data(), 32);
+    }
+    return 0;
+}
+
+}  // extern "C"

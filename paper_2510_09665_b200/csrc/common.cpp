@@ -1,0 +1,98 @@
+#include "common.hpp"
+
+#include <utility>
+
+namespace tkv {
+
+const char* errc_name(Errc e) {
+    switch (e) {
+        case Errc::ok: return "ok";
+        case Errc::not_found: return "not_found";
+        case Errc::tier_full: return "tier_full";
+        case Errc::out_of_pages: return "out_of_pages";
+        case Errc::duplicate_key: return "duplicate_key";
+        case Errc::corrupt_chunk: return "corrupt_chunk";
+        case Errc::size_mismatch: return "size_mismatch";
+        case Errc::unpopulated_page: return "unpopulated_page";
+        case Errc::unknown_codec: return "unknown_codec";
+        case Errc::unknown_instance: return "unknown_instance";
+        case Errc::unknown_query: return "unknown_query";
+        case Errc::inconsistent_alloc: return "inconsistent_alloc";
+        case Errc::chunk_missing: return "chunk_missing";
+        case Errc::pinned: return "pinned";
+        case Errc::protocol_error: return "protocol_error";
+        case Errc::io_error: return "io_error";
+        case Errc::invalid_argument: return "invalid_argument";
+        case Errc::cuda_error: return "cuda_error";
+    }
+    return "unknown";
+}
+
+std::string Status::to_string() const {
+    std::string s = errc_name(code);
+    if (!detail.empty()) s += ": " + detail;
+    return s;
+}
+
+void cuda_check(cudaError_t e, const char* what, const char* file, int line) {
+    if (e == cudaSuccess) return;
+    throw CudaError(std::string(cudaGetErrorString(e)) + " in " + what + " at " + file + ":" +
+                    std::to_string(line));
+}
+
+PinnedBuffer::PinnedBuffer(size_t n) { reserve(n); }
+
+PinnedBuffer::~PinnedBuffer() {
+    if (host) cudaFreeHost(host);
+}
+
+void PinnedBuffer::reserve(size_t n) {
+    if (n <= bytes) return;
+    if (host) TKV_CUDA(cudaFreeHost(host));
+    host = dev = nullptr;
+    bytes = 0;
+    void* p = nullptr;
+    TKV_CUDA(cudaHostAlloc(&p, n, cudaHostAllocMapped | cudaHostAllocPortable));
+    host = static_cast<uint8_t*>(p);
+    void* d = nullptr;
+    TKV_CUDA(cudaHostGetDevicePointer(&d, p, 0));
+    dev = static_cast<uint8_t*>(d);
+    bytes = n;
+}
+
+DeviceBuffer::DeviceBuffer(size_t n) { reserve(n); }
+
+DeviceBuffer::~DeviceBuffer() {
+    if (ptr) cudaFree(ptr);
+}
+
+void DeviceBuffer::reserve(size_t n) {
+    if (n <= bytes) return;
+    if (ptr) TKV_CUDA(cudaFree(ptr));
+    ptr = nullptr;
+    bytes = 0;
+    void* p = nullptr;
+    TKV_CUDA(cudaMalloc(&p, n));
+    ptr = static_cast<uint8_t*>(p);
+    bytes = n;
+}
+
+Stream Stream::create(int priority) {
+    cudaStream_t s = nullptr;
+    TKV_CUDA(cudaStreamCreateWithPriority(&s, cudaStreamNonBlocking, priority));
+    return Stream{s, true};
+}
+
+Stream::~Stream() {
+    if (owned && s) cudaStreamDestroy(s);
+}
+
+Event::Event() { TKV_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming)); }
+Event::~Event() {
+    if (e) cudaEventDestroy(e);
+}
+void Event::record(cudaStream_t s) const { TKV_CUDA(cudaEventRecord(e, s)); }
+void Event::wait_on(cudaStream_t s) const { TKV_CUDA(cudaStreamWaitEvent(s, e, 0)); }
+void Event::sync() const { TKV_CUDA(cudaEventSynchronize(e)); }
+
+}  // namespace tkv

@@ -1,0 +1,731 @@
+#include "connector.hpp"
+
+#include <algorithm>
+#include <cstring>
+
+namespace tkv {
+
+namespace {
+
+constexpr uint32_t pages_per_tile(size_t page_bytes) {
+    size_t p = 65536 / (page_bytes ? page_bytes : 1);
+    return uint32_t(p < 1 ? 1 : (p > 64 ? 64 : p));
+}
+
+std::vector<uint32_t> tile_prefix(const std::vector<XferDesc>& d, uint32_t page_tokens,
+                                  uint32_t ppt, uint32_t n_layers) {
+    std::vector<uint32_t> tb(d.size() + 1, 0);
+    for (size_t i = 0; i < d.size(); ++i)
+        tb[i + 1] = tb[i] + tiles_for(d[i].n_tokens, page_tokens, ppt, n_layers);
+    return tb;
+}
+
+// Host-built copy plan uploaded once per batch: descriptor variants (one per
+// staging ring slot, or one for direct slot access) and tile prefixes for
+// one-layer and all-layer launches.
+struct DevicePlan {
+    size_t n_desc = 0;
+    size_t variants = 0;
+    uint32_t tiles_1 = 0, tiles_all = 0;
+    uint64_t addr_or = 0;
+    PinnedBuffer host;
+    DeviceBuffer dev;
+    size_t off_tb1 = 0, off_tball = 0;
+
+    void build(const std::vector<std::vector<XferDesc>>& vars, uint32_t page_tokens, uint32_t ppt,
+               uint32_t n_layers, cudaStream_t s) {
+        variants = vars.size();
+        n_desc = vars.empty() ? 0 : vars[0].size();
+        if (n_desc == 0) return;
+        auto tb1 = tile_prefix(vars[0], page_tokens, ppt, 1);
+        auto tball = tile_prefix(vars[0], page_tokens, ppt, n_layers);
+        tiles_1 = tb1.back();
+        tiles_all = tball.back();
+        const size_t desc_bytes = variants * n_desc * sizeof(XferDesc);
+        off_tb1 = (desc_bytes + 15) & ~size_t(15);
+        off_tball = off_tb1 + ((tb1.size() * 4 + 15) & ~size_t(15));
+        const size_t total = off_tball + tball.size() * 4;
+        host.reserve(total);
+        dev.reserve(total);
+        addr_or = 0;
+        for (size_t v = 0; v < variants; ++v) {
+            std::memcpy(host.host + v * n_desc * sizeof(XferDesc), vars[v].data(),
+                        n_desc * sizeof(XferDesc));
+            for (const auto& d : vars[v]) addr_or |= d.chunk | d.layer_stride;
+        }
+        std::memcpy(host.host + off_tb1, tb1.data(), tb1.size() * 4);
+        std::memcpy(host.host + off_tball, tball.data(), tball.size() * 4);
+        TKV_CUDA(cudaMemcpyAsync(dev.ptr, host.host, total, cudaMemcpyHostToDevice, s));
+    }
+
+    PagedCopyPlan plan(size_t variant, uint32_t layer_begin, uint32_t n_layers, uint32_t ppt) const {
+        PagedCopyPlan p;
+        p.descs = reinterpret_cast<const XferDesc*>(dev.ptr) + variant * n_desc;
+        const bool one = n_layers == 1;
+        p.tile_base = reinterpret_cast<const uint32_t*>(dev.ptr + (one ? off_tb1 : off_tball));
+        p.n_desc = uint32_t(n_desc);
+        p.total_tiles = one ? tiles_1 : tiles_all;
+        p.layer_begin = layer_begin;
+        p.n_layers = n_layers;
+        p.pages_per_tile = ppt;
+        p.addr_or = addr_or;
+        return p;
+    }
+};
+
+struct ReleaseCtx {
+    TieredStore* store;
+    std::vector<Digest> digests;
+};
+void CUDART_CB release_cb(void* p) {
+    auto* c = static_cast<ReleaseCtx*>(p);
+    for (const auto& d : c->digests) c->store->release(d);
+    delete c;
+}
+
+struct CommitCtx {
+    TieredStore* store;
+    std::vector<Digest> digests;
+    std::atomic<bool>* committed;
+};
+void CUDART_CB commit_cb(void* p) {
+    auto* c = static_cast<CommitCtx*>(p);
+    for (const auto& d : c->digests) c->store->commit_write(d, Status::success());
+    if (c->committed) c->committed->store(true);
+    delete c;
+}
+
+}  // namespace
+
+namespace detail {
+
+struct PerQueryState {
+    size_t loaded = 0;
+    std::vector<std::pair<ChunkKey, Status>> store_results;
+};
+
+struct LoadItem {
+    QueryId id;
+    Digest digest;
+    SlotRead slot;
+    ChunkSpan span;
+    uint32_t record_tokens;
+    size_t staging_off;
+};
+
+struct StoreItem {
+    size_t plan;
+    size_t desc;
+    Status status;  // reservation outcome
+    SlotWrite w;
+};
+
+struct BatchState {
+    Connector* conn = nullptr;
+    TransferMode mode = TransferMode::layerwise;
+    uint32_t num_layers = 0;
+    std::vector<QueryPlan> plans;
+    std::unordered_map<QueryId, PerQueryState> per_query;
+    std::mutex mu;
+
+    // loads
+    bool loads_started = false;
+    std::vector<LoadItem> loads;
+    std::vector<Event> h2d_done, load_done;
+    DevicePlan load_plan;
+    size_t ring_slot_bytes = 0;
+
+    // stores
+    bool stores_reserved = false;
+    uint32_t next_store_layer = 0;
+    std::vector<bool> store_done;
+    bool stores_sealed = false, stores_waited = false;
+    std::vector<StoreItem> stores;
+    std::vector<Event> compute_done;
+    Event store_complete;
+    DevicePlan store_plan;
+    std::atomic<bool> committed{false};
+    bool any_store_writes = false;
+
+    ~BatchState() {
+        // Device buffers above may still feed in-flight work: drain first.
+        try {
+            if (loads_started && !load_done.empty()) load_done.back().sync();
+            if (any_store_writes) {
+                TKV_CUDA(cudaStreamSynchronize(conn->store_stream_));
+                if (!committed.load()) {
+                    for (auto& s : stores)
+                        if (s.w.kind == SlotWrite::Kind::write)
+                            conn->store().commit_write(
+                                plans[s.plan].store_plan[s.desc].key.digest,
+                                Status{Errc::io_error, "batch dropped before stores finished"});
+                }
+            }
+        } catch (...) {
+        }
+    }
+};
+
+}  // namespace detail
+
+using detail::BatchState;
+
+TransferMode ConnectorMetadata::mode() const {
+    std::lock_guard lock(state_->mu);
+    return state_->mode;
+}
+const std::vector<QueryPlan>& ConnectorMetadata::plans() const { return state_->plans; }
+size_t ConnectorMetadata::loaded_tokens(QueryId id) const {
+    std::lock_guard lock(state_->mu);
+    auto it = state_->per_query.find(id);
+    return it == state_->per_query.end() ? 0 : it->second.loaded;
+}
+std::vector<std::pair<ChunkKey, Status>> ConnectorMetadata::store_results(QueryId id) const {
+    std::lock_guard lock(state_->mu);
+    auto it = state_->per_query.find(id);
+    if (it == state_->per_query.end()) return {};
+    return it->second.store_results;
+}
+
+Connector::Connector(TieredStore& store, PagedKVStore& pages, Config cfg)
+    : store_(store),
+      pages_(pages),
+      cfg_(cfg),
+      hasher_(store.config().model.model_tag, store.config().chunk_size, pages.device()) {
+    TKV_CUDA(cudaSetDevice(pages_.device()));
+    if (cfg_.staging_depth == 0) cfg_.staging_depth = 1;
+    h2d_stream_ = Stream::create();
+    load_stream_ = Stream::create();
+    store_stream_ = Stream::create();
+}
+
+Connector::Connector(TieredStore& store, PagedKVStore& pages) : Connector(store, pages, Config{}) {}
+
+Connector::~Connector() {
+    try {
+        TKV_CUDA(cudaStreamSynchronize(h2d_stream_));
+        TKV_CUDA(cudaStreamSynchronize(load_stream_));
+        TKV_CUDA(cudaStreamSynchronize(store_stream_));
+    } catch (...) {
+    }
+}
+
+const std::vector<ChunkKey>& Connector::keys_for(QueryState& qs, TokenSpanView prompt) {
+    if (qs.keys.empty() || qs.prompt.size() != prompt.size() ||
+        !std::equal(prompt.begin(), prompt.end(), qs.prompt.begin())) {
+        qs.prompt.assign(prompt.begin(), prompt.end());
+        qs.keys = chunk_keys(hasher_, prompt);
+    }
+    return qs.keys;
+}
+
+size_t Connector::get_num_new_matched_tokens(QueryId id, TokenSpanView prompt) {
+    return get_num_new_matched_tokens(std::vector<QueryId>{id}, {prompt})[0];
+}
+
+std::vector<size_t> Connector::get_num_new_matched_tokens(
+    const std::vector<QueryId>& ids, const std::vector<TokenSpanView>& prompts) {
+    const size_t cs = store_.config().chunk_size;
+    auto digests = hasher_.hash(prompts);  // one K3 launch for the whole batch
+    KeyIndex index = [this](const ChunkKey& k) { return store_.contains(k.digest); };
+    std::vector<size_t> out(ids.size());
+    for (size_t q = 0; q < ids.size(); ++q) {
+        std::vector<ChunkKey> keys(digests[q].size());
+        for (size_t i = 0; i < keys.size(); ++i)
+            keys[i] = ChunkKey{digests[q][i], store_.config().model.model_tag, uint32_t(i)};
+        const size_t n = prompts[q].size();
+        const size_t lpm = longest_prefix_match(keys, n, cs, index);
+        const size_t cap = n == 0 ? 0 : n - 1;  // connector.cpp:75-76
+        const size_t matched = std::min(lpm, cap);
+        std::lock_guard lock(mu_);
+        QueryState& qs = queries_[ids[q]];
+        qs.prompt.assign(prompts[q].begin(), prompts[q].end());
+        qs.keys = std::move(keys);
+        qs.lpm = lpm;
+        qs.matched = matched;
+        out[q] = matched;
+    }
+    return out;
+}
+
+Status Connector::update_state_after_alloc(QueryId id, size_t blocks, size_t num_external_blocks) {
+    std::lock_guard lock(mu_);
+    auto it = queries_.find(id);
+    if (it == queries_.end()) return Status{Errc::invalid_argument, "unknown query"};
+    const size_t pt = store_.config().model.page_tokens;
+    const size_t needed = (it->second.matched + pt - 1) / pt;
+    if (num_external_blocks != needed)
+        return Status{Errc::invalid_argument, "external block count mismatch"};
+    if (blocks < needed) return Status{Errc::invalid_argument, "inconsistent alloc"};
+    it->second.blocks = blocks;
+    return Status::success();
+}
+
+ConnectorMetadata Connector::build_connector_meta(const SchedulerOutput& out) {
+    const auto& cfg = store_.config();
+    auto b = std::make_shared<BatchState>();
+    b->conn = this;
+    b->mode = cfg_.mode;
+    b->num_layers = cfg.model.num_layers;
+    b->store_done.assign(b->num_layers, false);
+
+    for (const auto& sq : out.queries) {
+        QueryPlan plan;
+        plan.id = sq.id;
+        plan.prompt_tokens = sq.prompt.size();
+        std::vector<ChunkKey> keys;
+        size_t lpm = 0, matched = 0;
+        {
+            std::lock_guard lock(mu_);
+            QueryState& qs = queries_[sq.id];
+            keys = keys_for(qs, sq.prompt);  // cached from lookup: no re-hash
+            lpm = qs.lpm;
+            matched = qs.matched;
+        }
+        plan.matched_tokens = matched;
+        const auto spans = chunk_tokens(sq.prompt.size(), cfg.chunk_size);
+        // Load descriptors: stored chunking of the uncapped match, spans
+        // clipped to the capped match (connector.cpp:136-147).
+        for (size_t i = 0; i < spans.size() && spans[i].end <= lpm; ++i) {
+            ChunkSpan span = spans[i];
+            const uint32_t record_tokens = uint32_t(span.length());
+            if (span.start >= matched) break;
+            span.end = std::min(span.end, matched);
+            plan.load_plan.push_back({keys[i], span, record_tokens});
+        }
+        // Store descriptors: chunks absent at build time (connector.cpp:100-110).
+        for (size_t i = 0; i < spans.size(); ++i) {
+            if (store_.contains(keys[i].digest)) continue;
+            plan.store_plan.push_back({keys[i], spans[i], uint32_t(spans[i].length())});
+        }
+        detail::PerQueryState pq;
+        pq.loaded = matched;
+        b->per_query.emplace(sq.id, std::move(pq));
+        b->plans.push_back(std::move(plan));
+    }
+    ConnectorMetadata meta;
+    meta.state_ = std::move(b);
+    return meta;
+}
+
+// --- loads -----------------------------------------------------------------
+
+Status Connector::enqueue_loads(BatchState& b) {
+    const auto& model = store_.config().model;
+    const uint32_t L = b.num_layers;
+    const uint32_t pt = model.page_tokens;
+    const size_t bpt = model.bytes_per_token_per_layer;
+    const uint32_t ppt = pages_per_tile(pages_.page_bytes());
+
+    // Safe prefix per query (connector.cpp:196-216): a chunk that vanished, a
+    // record whose geometry differs from the plan, or pages that cannot take
+    // the span end the deliverable prefix at that chunk.
+    for (const auto& plan : b.plans) {
+        size_t safe = plan.matched_tokens;
+        for (const auto& d : plan.load_plan) {
+            bool ok = true;
+            for (uint32_t l = 0; l < L && ok; ++l)
+                ok = pages_.check_writable_span(plan.id, l, d.span.start / pt, d.span.length()).ok();
+            Result<SlotRead> r = ok ? store_.acquire(d.key.digest, d.record_tokens)
+                                    : Result<SlotRead>(Status{Errc::size_mismatch, "pages"});
+            if (!r.ok()) {
+                safe = d.span.start;
+                break;
+            }
+            b.loads.push_back({plan.id, d.key.digest, r.value(), d.span, d.record_tokens, 0});
+        }
+        std::lock_guard lock(b.mu);
+        auto& pq = b.per_query.at(plan.id);
+        pq.loaded = std::min(pq.loaded, safe);
+    }
+
+    size_t layer_bytes = 0;
+    for (auto& it : b.loads) {
+        it.staging_off = layer_bytes;
+        layer_bytes += ((it.span.length() * bpt + 255) / 256) * 256;
+    }
+    const bool blocking = b.mode == TransferMode::blocking;
+    const bool zero_copy = blocking || cfg_.load_path == LoadPath::zero_copy;
+    b.h2d_done.resize(L);
+    b.load_done.resize(L);
+    b.loads_started = true;
+    if (b.loads.empty()) {
+        for (uint32_t l = 0; l < L; ++l) b.load_done[l].record(load_stream_);
+        return Status::success();
+    }
+
+    // Device page tables, then the copy plan (ordered on the load stream).
+    std::unordered_map<QueryId, PagedKVStore::DeviceTable> tables;
+    for (const auto& it : b.loads) {
+        if (tables.count(it.id)) continue;
+        auto t = pages_.device_table(it.id, load_stream_);
+        if (!t.ok()) return t.status();
+        tables.emplace(it.id, t.value());
+    }
+    const uint32_t depth = std::min<uint32_t>(cfg_.staging_depth, L);
+    std::vector<std::vector<XferDesc>> vars(zero_copy ? 1 : depth);
+    if (!zero_copy) {
+        b.ring_slot_bytes = layer_bytes;
+        staging_.reserve(size_t(depth) * layer_bytes);
+        staging_peak_ = std::max(staging_peak_, size_t(depth) * layer_bytes);
+    }
+    for (size_t v = 0; v < vars.size(); ++v) {
+        for (const auto& it : b.loads) {
+            XferDesc d;
+            const auto& t = tables.at(it.id);
+            d.table = t.ptr;
+            d.table_stride = t.stride;
+            d.first_page = uint32_t(it.span.start / pt);
+            d.n_tokens = uint32_t(it.span.length());
+            if (zero_copy) {
+                d.chunk = reinterpret_cast<uint64_t>(it.slot.dev);
+                d.layer_stride = uint64_t(it.record_tokens) * bpt;
+            } else {
+                d.chunk = reinterpret_cast<uint64_t>(staging_.ptr + v * layer_bytes + it.staging_off);
+                d.layer_stride = 0;
+            }
+            vars[v].push_back(d);
+        }
+    }
+    b.load_plan.build(vars, pt, ppt, L, load_stream_);
+    const PagedLayout layout = pages_.layout();
+
+    if (zero_copy && blocking) {
+        TKV_CUDA(launch_paged_copy(layout, b.load_plan.plan(0, 0, L, ppt), CopyDir::scatter,
+                                   cfg_.load_ctas, load_stream_));
+        for (uint32_t l = 0; l < L; ++l) b.load_done[l].record(load_stream_);
+    } else if (zero_copy) {
+        for (uint32_t l = 0; l < L; ++l) {
+            TKV_CUDA(launch_paged_copy(layout, b.load_plan.plan(0, l, 1, ppt), CopyDir::scatter,
+                                       cfg_.load_ctas, load_stream_));
+            b.load_done[l].record(load_stream_);
+        }
+    } else {
+        // Layerwise copy-engine pipeline through a `depth`-layer staging ring.
+        if (ring_used_) ring_free_.wait_on(h2d_stream_);  // previous batch done with the ring
+        const size_t n = b.loads.size();
+        std::vector<void*> dst(n), src(n);
+        std::vector<size_t> sizes(n);
+        cudaMemcpyAttributes attr{};
+        attr.srcAccessOrder = cudaMemcpySrcAccessOrderStream;
+        size_t attr_idx = 0, fail_idx = 0;
+        for (uint32_t l = 0; l < L; ++l) {
+            const uint32_t r = l % depth;
+            if (l >= depth) b.load_done[l - depth].wait_on(h2d_stream_);
+            for (size_t i = 0; i < n; ++i) {
+                const auto& it = b.loads[i];
+                src[i] = it.slot.host + size_t(l) * it.record_tokens * bpt;
+                dst[i] = staging_.ptr + size_t(r) * layer_bytes + it.staging_off;
+                sizes[i] = it.span.length() * bpt;
+            }
+            TKV_CUDA(cudaMemcpyBatchAsync(dst.data(), src.data(), sizes.data(), n, &attr, &attr_idx,
+                                          1, &fail_idx, h2d_stream_));
+            b.h2d_done[l].record(h2d_stream_);
+            b.h2d_done[l].wait_on(load_stream_);
+            TKV_CUDA(launch_paged_copy(layout, b.load_plan.plan(r, l, 1, ppt), CopyDir::scatter,
+                                       cfg_.load_ctas, load_stream_));
+            b.load_done[l].record(load_stream_);
+        }
+        ring_free_.record(load_stream_);
+        ring_used_ = true;
+    }
+    // Pages hold the bytes once the stream reaches them; the slots are free
+    // for eviction after the last scatter.
+    for (const auto& it : b.loads)
+        for (uint32_t l = 0; l < L; ++l)
+            pages_.mark_span_populated(it.id, l, it.span.start / pt, it.span.length());
+    auto* ctx = new ReleaseCtx{&store_, {}};
+    for (const auto& it : b.loads) ctx->digests.push_back(it.digest);
+    TKV_CUDA(cudaLaunchHostFunc(load_stream_, release_cb, ctx));
+    if (blocking) TKV_CUDA(cudaStreamSynchronize(load_stream_));
+    return Status::success();
+}
+
+Status Connector::start_load_kv(ConnectorMetadata& meta) {
+    if (!meta) return Status{Errc::invalid_argument, "empty metadata"};
+    BatchState& b = *meta.state_;
+    std::lock_guard io(io_mu_);
+    if (b.loads_started) return Status::success();
+    const size_t bpt = store_.config().model.bytes_per_token_per_layer;
+    size_t layer_bytes = 0;
+    for (const auto& plan : b.plans)
+        for (const auto& d : plan.load_plan) layer_bytes += d.span.length() * bpt;
+    if (layer_bytes > cfg_.staging_budget_bytes) {  // connector.cpp:244-256
+        std::lock_guard lock(b.mu);
+        b.mode = TransferMode::blocking;
+    }
+    try {
+        return enqueue_loads(b);
+    } catch (const CudaError& e) {
+        return Status{Errc::cuda_error, e.what()};
+    }
+}
+
+Status Connector::wait_load_kv(ConnectorMetadata& meta, uint32_t layer) {
+    if (!meta) return Status{Errc::invalid_argument, "empty metadata"};
+    BatchState& b = *meta.state_;
+    if (layer >= b.num_layers) return Status{Errc::invalid_argument, "layer out of range"};
+    if (!b.loads_started) {
+        Status st = start_load_kv(meta);
+        if (!st.ok()) return st;
+    }
+    try {
+        b.load_done[layer].wait_on(cfg_.engine_stream);  // engine stream, not the host, waits
+    } catch (const CudaError& e) {
+        return Status{Errc::cuda_error, e.what()};
+    }
+    return Status::success();
+}
+
+// --- stores ----------------------------------------------------------------
+
+Status Connector::reserve_stores(BatchState& b) {
+    const auto& model = store_.config().model;
+    const uint32_t pt = model.page_tokens;
+    const size_t bpt = model.bytes_per_token_per_layer;
+    const uint32_t ppt = pages_per_tile(pages_.page_bytes());
+    std::vector<XferDesc> descs;
+    std::unordered_map<QueryId, PagedKVStore::DeviceTable> tables;
+    for (size_t p = 0; p < b.plans.size(); ++p) {
+        const auto& plan = b.plans[p];
+        for (size_t i = 0; i < plan.store_plan.size(); ++i) {
+            const auto& d = plan.store_plan[i];
+            detail::StoreItem item{p, i, Status::success(), {}};
+            auto w = store_.begin_write(d.key.digest, d.record_tokens, cfg_.pin_stores);
+            if (!w.ok()) {
+                item.status = w.status();
+            } else {
+                item.w = w.value();
+                if (item.w.kind == SlotWrite::Kind::write) {
+                    if (!tables.count(plan.id)) {
+                        auto t = pages_.device_table(plan.id, store_stream_);
+                        if (!t.ok()) return t.status();
+                        tables.emplace(plan.id, t.value());
+                    }
+                    XferDesc x;
+                    x.chunk = reinterpret_cast<uint64_t>(item.w.dev);
+                    x.layer_stride = uint64_t(d.record_tokens) * bpt;
+                    x.table = tables.at(plan.id).ptr;
+                    x.table_stride = tables.at(plan.id).stride;
+                    x.first_page = uint32_t(d.span.start / pt);
+                    x.n_tokens = uint32_t(d.span.length());
+                    descs.push_back(x);
+                }
+            }
+            b.stores.push_back(std::move(item));
+        }
+    }
+    b.any_store_writes = !descs.empty();
+    b.store_plan.build({descs}, pt, ppt, b.num_layers, store_stream_);
+    b.compute_done.resize(b.num_layers);
+    b.stores_reserved = true;
+    return Status::success();
+}
+
+Status Connector::store_layers(BatchState& b, uint32_t first, uint32_t last) {
+    const auto& model = store_.config().model;
+    const uint32_t pt = model.page_tokens;
+    const uint32_t ppt = pages_per_tile(pages_.page_bytes());
+    // Gather readability (check_readable, paged_store.cpp:94-111) per layer.
+    for (uint32_t l = first; l < last; ++l)
+        for (const auto& s : b.stores) {
+            if (s.w.kind != SlotWrite::Kind::write) continue;
+            const auto& plan = b.plans[s.plan];
+            const auto& d = plan.store_plan[s.desc];
+            Status st = pages_.check_readable_span(plan.id, l, d.span.start / pt, d.span.length());
+            if (!st.ok()) return st;
+        }
+    if (b.store_plan.n_desc == 0) return Status::success();
+    const PagedLayout layout = pages_.layout();
+    // K1 for these layers, ordered after the engine's compute of them.
+    b.compute_done[first].record(cfg_.engine_stream);
+    b.compute_done[first].wait_on(store_stream_);
+    TKV_CUDA(launch_paged_copy(layout, b.store_plan.plan(0, first, last - first, ppt),
+                               CopyDir::gather, cfg_.store_ctas, store_stream_));
+    return Status::success();
+}
+
+Status Connector::start_store_kv(ConnectorMetadata& meta) {
+    if (!meta) return Status{Errc::invalid_argument, "empty metadata"};
+    BatchState& b = *meta.state_;
+    uint32_t first = 0, last = 0;
+    {
+        std::lock_guard lock(b.mu);
+        if (b.mode == TransferMode::blocking) {
+            first = 0;
+            last = b.num_layers;
+            b.next_store_layer = b.num_layers;
+        } else {
+            if (b.next_store_layer >= b.num_layers) return Status::success();
+            first = b.next_store_layer;
+            last = ++b.next_store_layer;
+        }
+    }
+    try {
+        std::lock_guard io(io_mu_);
+        if (!b.stores_reserved) {
+            Status st = reserve_stores(b);
+            if (!st.ok()) return st;
+        }
+        Status st = store_layers(b, first, last);
+        if (!st.ok()) return st;
+        {
+            std::lock_guard lock(b.mu);
+            for (uint32_t l = first; l < last; ++l) b.store_done[l] = true;
+        }
+        if (last == b.num_layers && !b.stores_sealed) {
+            b.stores_sealed = true;
+            b.store_complete.record(store_stream_);
+            if (b.any_store_writes) {
+                auto* ctx = new CommitCtx{&store_, {}, &b.committed};
+                for (const auto& s : b.stores)
+                    if (s.w.kind == SlotWrite::Kind::write)
+                        ctx->digests.push_back(b.plans[s.plan].store_plan[s.desc].key.digest);
+                TKV_CUDA(cudaLaunchHostFunc(store_stream_, commit_cb, ctx));
+            } else {
+                b.committed.store(true);
+            }
+        }
+    } catch (const CudaError& e) {
+        return Status{Errc::cuda_error, e.what()};
+    }
+    if (b.mode == TransferMode::blocking) return wait_store_kv(meta, b.num_layers - 1);
+    return Status::success();
+}
+
+Status Connector::wait_store_kv(ConnectorMetadata& meta, uint32_t layer) {
+    if (!meta) return Status{Errc::invalid_argument, "empty metadata"};
+    BatchState& b = *meta.state_;
+    if (layer >= b.num_layers) return Status{Errc::invalid_argument, "layer out of range"};
+    {
+        std::lock_guard lock(b.mu);
+        if (!b.store_done[layer]) return Status{Errc::invalid_argument, "store for layer not started"};
+        if (layer + 1 < b.num_layers || b.stores_waited) return Status::success();
+    }
+    // Final wait: the bytes landed, then per-chunk statuses (connector.cpp:372-391).
+    try {
+        b.store_complete.sync();
+    } catch (const CudaError& e) {
+        return Status{Errc::cuda_error, e.what()};
+    }
+    std::unordered_map<QueryId, std::vector<std::pair<ChunkKey, Status>>> results;
+    for (auto& s : b.stores) {
+        const auto& plan = b.plans[s.plan];
+        Status st = s.status.ok() ? s.w.handle.wait() : s.status;
+        results[plan.id].emplace_back(plan.store_plan[s.desc].key, st);
+    }
+    std::lock_guard lock(b.mu);
+    for (auto& [id, r] : results) b.per_query.at(id).store_results = std::move(r);
+    b.stores_waited = true;
+    return Status::success();
+}
+
+// --- decode ----------------------------------------------------------------
+
+Status Connector::begin_decode(QueryId id) {
+    std::lock_guard lock(mu_);
+    auto it = queries_.find(id);
+    if (it == queries_.end() || it->second.prompt.empty())
+        return Status{Errc::invalid_argument, "no planned query"};
+    QueryState& qs = it->second;
+    if (qs.decode) return Status{Errc::duplicate_key, "decode already open"};
+    const size_t cs = store_.config().chunk_size;
+    const auto& keys = keys_for(qs, qs.prompt);
+    const size_t full = qs.prompt.size() / cs;
+    auto ds = std::make_unique<DecodeState>(DecodeState{KeyChain(hasher_), {}, full * cs, {}, {}});
+    if (full > 0) ds->chain.reset(keys[full - 1].digest, uint32_t(full));
+    ds->tokens.assign(qs.prompt.begin() + full * cs, qs.prompt.end());
+    qs.decode = std::move(ds);
+    return Status::success();
+}
+
+Status Connector::flush_decode(QueryId id, QueryState& qs) {
+    DecodeState& ds = *qs.decode;
+    if (ds.tokens.empty()) return Status::success();
+    const auto& model = store_.config().model;
+    const uint32_t pt = model.page_tokens;
+    const size_t n = ds.tokens.size();
+    ChunkKey key = ds.chain.next(ds.tokens);
+    key.model_tag = model.model_tag;
+    for (uint32_t l = 0; l < model.num_layers; ++l) {
+        Status st = pages_.check_readable_span(id, l, ds.chunk_start / pt, n);
+        if (!st.ok()) return st;
+    }
+    auto w = store_.begin_write(key.digest, uint32_t(n), cfg_.pin_stores);
+    if (!w.ok()) {
+        ds.puts.push_back(PutHandle::immediate(w.status()));
+    } else if (w.value().kind != SlotWrite::Kind::write) {
+        ds.puts.push_back(w.value().handle);
+    } else {
+        std::lock_guard io(io_mu_);
+        auto t = pages_.device_table(id, store_stream_);
+        if (!t.ok()) return t.status();
+        XferDesc x;
+        x.chunk = reinterpret_cast<uint64_t>(w.value().dev);
+        x.layer_stride = uint64_t(n) * model.bytes_per_token_per_layer;
+        x.table = t.value().ptr;
+        x.table_stride = t.value().stride;
+        x.first_page = uint32_t(ds.chunk_start / pt);
+        x.n_tokens = uint32_t(n);
+        auto plan = std::make_shared<DevicePlan>();
+        const uint32_t ppt = pages_per_tile(pages_.page_bytes());
+        plan->build({{x}}, pt, ppt, model.num_layers, store_stream_);
+        Event computed;
+        computed.record(cfg_.engine_stream);
+        computed.wait_on(store_stream_);
+        TKV_CUDA(launch_paged_copy(pages_.layout(), plan->plan(0, 0, model.num_layers, ppt),
+                                   CopyDir::gather, cfg_.store_ctas, store_stream_));
+        auto* ctx = new CommitCtx{&store_, {key.digest}, nullptr};
+        TKV_CUDA(cudaLaunchHostFunc(store_stream_, commit_cb, ctx));
+        // Keep the plan buffers alive until the gather ran.
+        TKV_CUDA(cudaStreamSynchronize(store_stream_));
+        ds.puts.push_back(w.value().handle);
+    }
+    ds.flushed.push_back(key);
+    ds.chunk_start += n;
+    ds.tokens.clear();
+    return Status::success();
+}
+
+Status Connector::append_decode(QueryId id, TokenId token) {
+    std::lock_guard lock(mu_);
+    auto it = queries_.find(id);
+    if (it == queries_.end() || !it->second.decode)
+        return Status{Errc::unknown_query, "decode not open"};
+    DecodeState& ds = *it->second.decode;
+    ds.tokens.push_back(token);
+    if (ds.tokens.size() == store_.config().chunk_size) {
+        try {
+            return flush_decode(id, it->second);
+        } catch (const CudaError& e) {
+            return Status{Errc::cuda_error, e.what()};
+        }
+    }
+    return Status::success();
+}
+
+Result<std::vector<ChunkKey>> Connector::finish_query(QueryId id) {
+    std::vector<ChunkKey> keys;
+    std::unique_ptr<DecodeState> ds;
+    {
+        std::lock_guard lock(mu_);
+        auto it = queries_.find(id);
+        if (it != queries_.end() && it->second.decode) {
+            try {
+                Status st = flush_decode(id, it->second);
+                if (!st.ok()) return st;
+            } catch (const CudaError& e) {
+                return Status{Errc::cuda_error, e.what()};
+            }
+            ds = std::move(it->second.decode);
+        }
+        if (it != queries_.end()) queries_.erase(it);
+    }
+    if (ds) {
+        for (const auto& h : ds->puts) h.wait();
+        keys = std::move(ds->flushed);
+    }
+    return keys;
+}
+
+}  // namespace tkv

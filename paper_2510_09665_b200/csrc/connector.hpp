@@ -1,0 +1,165 @@
+// Engine-facing connector (mirror of include/tierkv/connector.hpp:14-152):
+// the seven Table-1 functions plus decode storing, with
+// the reference's names, argument meaning and error behaviour.
+//
+// What changes is the execution model. The reference runs every byte on host
+// threads: a TaskPool task per layer for loads (connector.cpp:179-237) and
+// inline memcpys plus a record encode per chunk for stores (:281-358). Here
+//   * lookup hashes each prompt once on the GPU (K3) and caches the keys;
+//   * loads are enqueued at start_load_kv for ALL layers: per layer one
+//     batched copy-engine H2D of every chunk-layer slice from the pinned
+//     slots into a device staging ring, then one K2 scatter launch into the
+//     pages; wait_load_kv(l) makes the engine stream wait on layer l's event
+//     instead of blocking the host;
+//   * stores run K1 per layer on a side stream ordered after the engine's
+//     compute of that layer, writing each chunk straight into its pinned
+//     slot (zero-copy over PCIe, no staging, no full-size assembly
+//     buffers); a stream callback marks the chunks present when the last
+//     layer landed.
+// Blocking mode (configured, or a batch whose one-layer staging exceeds the
+// budget, connector.cpp:244-256) moves all layers in one launch and returns
+// only after the bytes are in place, like the reference.
+#pragma once
+
+#include <atomic>
+#include <memory>
+#include <mutex>
+#include <unordered_map>
+#include <vector>
+
+#include "common.hpp"
+#include "paged_store.hpp"
+#include "store.hpp"
+#include "tokens.hpp"
+
+namespace tkv {
+
+enum class TransferMode : uint8_t { layerwise, blocking };
+enum class LoadPath : uint8_t { copy_engine, zero_copy };
+
+struct ChunkDescriptor {
+    ChunkKey key;
+    ChunkSpan span;
+    uint32_t record_tokens = 0;
+};
+
+struct ScheduledQuery {
+    QueryId id = 0;
+    std::vector<TokenId> prompt;
+};
+
+struct SchedulerOutput {
+    std::vector<ScheduledQuery> queries;
+};
+
+struct QueryPlan {
+    QueryId id = 0;
+    size_t prompt_tokens = 0;
+    size_t matched_tokens = 0;
+    std::vector<ChunkDescriptor> load_plan;
+    std::vector<ChunkDescriptor> store_plan;
+};
+
+namespace detail {
+struct BatchState;
+}
+
+class ConnectorMetadata {
+public:
+    ConnectorMetadata() = default;
+    TransferMode mode() const;
+    const std::vector<QueryPlan>& plans() const;
+    size_t loaded_tokens(QueryId id) const;
+    std::vector<std::pair<ChunkKey, Status>> store_results(QueryId id) const;
+    explicit operator bool() const { return state_ != nullptr; }
+
+private:
+    friend class Connector;
+    std::shared_ptr<detail::BatchState> state_;
+};
+
+class Connector {
+public:
+    struct Config {
+        TransferMode mode = TransferMode::layerwise;
+        bool pin_stores = false;
+        // One layer of load bytes must fit, else the batch degrades to blocking.
+        size_t staging_budget_bytes = 64ull << 20;
+        uint32_t staging_depth = 2;      // layers of device staging in flight
+        LoadPath load_path = LoadPath::copy_engine;
+        int store_ctas = 64;             // zero-copy K1 grid (PCIe-bound)
+        int load_ctas = 0;               // K2 grid (0 = 2 x SMs)
+        cudaStream_t engine_stream = nullptr;
+    };
+
+    Connector(TieredStore& store, PagedKVStore& pages, Config cfg);
+    Connector(TieredStore& store, PagedKVStore& pages);
+    ~Connector();
+    Connector(const Connector&) = delete;
+    Connector& operator=(const Connector&) = delete;
+
+    size_t get_num_new_matched_tokens(QueryId id, TokenSpanView prompt);
+    // Batched lookup: one K3 launch for every prompt (extension).
+    std::vector<size_t> get_num_new_matched_tokens(const std::vector<QueryId>& ids,
+                                                   const std::vector<TokenSpanView>& prompts);
+    Status update_state_after_alloc(QueryId id, size_t blocks, size_t num_external_blocks);
+    ConnectorMetadata build_connector_meta(const SchedulerOutput& out);
+    Status start_load_kv(ConnectorMetadata& meta);
+    Status wait_load_kv(ConnectorMetadata& meta, uint32_t layer);
+    Status start_store_kv(ConnectorMetadata& meta);
+    Status wait_store_kv(ConnectorMetadata& meta, uint32_t layer);
+
+    // Delayed decode storing (connector.cpp:434-497): the decode tokens' KV
+    // lives in the query's pages; full chunks are gathered straight from the
+    // pages into pinned slots (K1) as they complete.
+    Status begin_decode(QueryId id);
+    Status append_decode(QueryId id, TokenId token);
+    Result<std::vector<ChunkKey>> finish_query(QueryId id);
+
+    const Config& config() const { return cfg_; }
+    TieredStore& store() { return store_; }
+    PagedKVStore& pages() { return pages_; }
+    KeyHasher& hasher() { return hasher_; }
+    // Device staging high-water mark (bytes) across batches.
+    size_t staging_peak_bytes() const { return staging_peak_; }
+
+private:
+    friend struct detail::BatchState;
+    struct DecodeState {
+        KeyChain chain;
+        std::vector<TokenId> tokens;   // tokens of the open (partial) chunk
+        size_t chunk_start = 0;        // absolute position of tokens[0]
+        std::vector<PutHandle> puts;
+        std::vector<ChunkKey> flushed;
+    };
+    struct QueryState {
+        std::vector<TokenId> prompt;
+        std::vector<ChunkKey> keys;  // chain of the whole prompt, hashed once
+        size_t lpm = 0;
+        size_t matched = 0;
+        size_t blocks = 0;
+        std::unique_ptr<DecodeState> decode;
+    };
+
+    const std::vector<ChunkKey>& keys_for(QueryState& qs, TokenSpanView prompt);
+    Status enqueue_loads(detail::BatchState& b);
+    Status store_layers(detail::BatchState& b, uint32_t first, uint32_t last);
+    Status reserve_stores(detail::BatchState& b);
+    Status flush_decode(QueryId id, QueryState& qs);
+
+    TieredStore& store_;
+    PagedKVStore& pages_;
+    Config cfg_;
+    KeyHasher hasher_;
+    Stream h2d_stream_, load_stream_, store_stream_;
+    DeviceBuffer staging_;
+    Event ring_free_;
+    bool ring_used_ = false;
+    size_t staging_peak_ = 0;
+    std::mutex io_mu_;  // one batch enqueues at a time
+
+    mutable std::mutex mu_;
+    std::unordered_map<QueryId, QueryState> queries_;
+};
+
+}  // namespace tkv

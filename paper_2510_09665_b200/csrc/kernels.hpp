@@ -1,0 +1,120 @@
+// Launch interface of the sm_100a kernels. POD structs only: these are what
+// the host C++ (and the C-ABI in include/tierkv_b200.h) hand to the device.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+namespace tkv {
+
+// ---------------------------------------------------------------------------
+// K1/K2: multi-layer paged KV gather (store) and scatter (retrieve).
+//
+// Replaces PagedKVStore::gather_tokens_into / scatter_tokens
+// (src/paged_store.cpp:123-175) as called per (layer, chunk) from
+// Connector::start_store_kv (src/connector.cpp:300-323) and
+// Connector::run_load_layer (src/connector.cpp:179-219): ONE launch moves
+// every chunk descriptor of a batch for a range of layers.
+//
+// Paged side. Reference layout (paged_store.hpp:19-82): a page holds
+// page_tokens rows of ONE layer, row = bpt opaque bytes, page p at
+// base + p * page_stride; each (query, layer) has its own page list.
+// vLLM layout: per-layer tensors [planes=2 (K,V)][blocks][page_tokens][H*D],
+// one block table shared by all layers; the chunk row is K(H*D) | V(H*D).
+// Both are expressed by PagedLayout.
+struct PagedLayout {
+    uint64_t base = 0;                // pool base (used when layer_base == nullptr)
+    const uint64_t* layer_base = nullptr;  // optional device array [num_layers]
+    uint64_t page_stride = 0;         // bytes between consecutive page ids
+    uint64_t plane_stride = 0;        // bytes between the K and V planes
+    uint32_t token_stride = 0;        // bytes between rows inside a page
+    uint32_t plane_bytes = 0;         // bytes of one row in one plane
+    uint32_t n_planes = 1;            // 1 = opaque row, 2 = K|V planes
+    uint32_t page_tokens = 16;
+    uint32_t bpt = 0;                 // chunk row bytes = n_planes * plane_bytes
+    uint32_t shared_table = 0;        // 1: page-table row 0 serves every layer
+};
+
+// One chunk transfer (a ChunkDescriptor of a load or store plan,
+// connector.hpp:22-43). Spans start on a chunk boundary, hence page-aligned
+// (ModelSpec::validate requires page_tokens | chunk_size).
+struct XferDesc {
+    uint64_t chunk = 0;          // device-visible chunk base: HBM, mapped pinned host, or peer
+    uint64_t layer_stride = 0;   // bytes between layers in the chunk buffer (slot: T*bpt)
+    const int32_t* table = nullptr;  // device page table, [layers][table_stride]
+    uint32_t table_stride = 0;
+    uint32_t first_page = 0;     // span.start / page_tokens
+    uint32_t n_tokens = 0;       // rows to move (span length; may clip a record)
+    uint32_t pad = 0;
+};
+
+enum class CopyDir : int { gather = 0, scatter = 1 };  // gather: pages -> chunk
+
+struct PagedCopyPlan {
+    const XferDesc* descs = nullptr;   // device
+    const uint32_t* tile_base = nullptr;  // device, [n_desc + 1] prefix of tiles
+    uint32_t n_desc = 0;
+    uint32_t total_tiles = 0;
+    uint32_t layer_begin = 0;
+    uint32_t n_layers = 1;             // layers moved by this launch
+    uint32_t pages_per_tile = 1;
+    uint64_t addr_or = 0;              // OR of every desc chunk base and layer stride (alignment)
+};
+
+// Tiles of one descriptor for a launch over n_layers (host + device agree).
+inline uint32_t tiles_for(uint32_t n_tokens, uint32_t page_tokens, uint32_t pages_per_tile,
+                          uint32_t n_layers) {
+    uint32_t pages = (n_tokens + page_tokens - 1) / page_tokens;
+    return n_layers * ((pages + pages_per_tile - 1) / pages_per_tile);
+}
+
+// Launches the copy; `ctas` = grid size (0 = 2 x SM count). Returns launch error.
+cudaError_t launch_paged_copy(const PagedLayout& layout, const PagedCopyPlan& plan, CopyDir dir,
+                              int ctas, cudaStream_t stream);
+
+// ---------------------------------------------------------------------------
+// K3: chained SHA-256 chunk keys (KeyChain::next, src/tokens.cpp:22-42).
+// digest_i = SHA-256(u16le(|tag|) | tag | digest_{i-1} | u32le tokens of chunk i)
+// One thread per chain (request); chains are independent.
+struct ChainDesc {
+    uint64_t token_off = 0;     // first token in the packed token buffer
+    uint32_t n_tokens = 0;      // tokens of this chain (chunked by chunk_size)
+    uint32_t out_first = 0;     // first digest row of this chain in `out`
+    uint8_t parent[32] = {};    // KeyChain::reset parent (zeros for a fresh chain)
+};
+
+inline constexpr int kMaxTagBytes = 256;
+struct HashParams {
+    uint32_t chunk_size = 256;
+    uint32_t tag_len = 0;
+    uint8_t tag[kMaxTagBytes] = {};
+};
+
+cudaError_t launch_hash_chains(const uint32_t* tokens, const ChainDesc* chains, uint32_t n_chains,
+                               const HashParams& params, uint8_t* out, cudaStream_t stream);
+
+// ---------------------------------------------------------------------------
+// K4: synthetic KV (synth_token_kv, src/synth.cpp:7-20) written straight into
+// pages for tokens [pos_begin, pos_end) of one query over layers
+// [layer_begin, layer_end). Word at byte offset i of a row is
+// splitmix64(base + i), base = splitmix64(seed ^ tok<<32 ^ layer<<16 ^ splitmix64(pos)).
+struct SynthArgs {
+    const uint32_t* tokens = nullptr;  // device, the query's prompt (absolute positions)
+    const int32_t* table = nullptr;    // device page table [layers][table_stride]
+    uint32_t table_stride = 0;
+    uint64_t seed = 0;
+    uint32_t pos_begin = 0, pos_end = 0;
+    uint32_t layer_begin = 0, layer_end = 0;
+};
+cudaError_t launch_synth_pages(const PagedLayout& layout, const SynthArgs& args,
+                               cudaStream_t stream);
+// Counts rows (layer, token) whose page bytes differ from synth; adds to *mismatches.
+cudaError_t launch_verify_pages(const PagedLayout& layout, const SynthArgs& args,
+                                unsigned long long* mismatches, cudaStream_t stream);
+// Synthetic chunk payload [n_layers][n][bpt] into a flat device buffer.
+cudaError_t launch_synth_chunk(const uint32_t* tokens, uint64_t seed, uint32_t start, uint32_t n,
+                               uint32_t n_layers, uint32_t bpt, uint8_t* out,
+                               cudaStream_t stream);
+
+}  // namespace tkv

@@ -1,0 +1,284 @@
+#include "paged_store.hpp"
+
+#include <algorithm>
+#include <cstring>
+
+namespace tkv {
+
+PagedKVStore::PagedKVStore(ModelSpec spec, uint32_t num_pages, int device)
+    : spec_(std::move(spec)), device_(device) {
+    if (device_ < 0) TKV_CUDA(cudaGetDevice(&device_));
+    TKV_CUDA(cudaSetDevice(device_));
+    pool_.reserve(std::max<size_t>(1, size_t(num_pages) * spec_.page_bytes()));
+    pages_.resize(num_pages);
+    free_list_.reserve(num_pages);
+    for (uint32_t i = num_pages; i > 0; --i) free_list_.push_back(i - 1);  // page 0 first
+    io_stream_ = Stream::create();
+}
+
+Result<std::vector<PageId>> PagedKVStore::alloc_pages(QueryId query, size_t n) {
+    std::lock_guard lock(mu_);
+    if (free_list_.size() < n)
+        return Status{Errc::out_of_pages, "need " + std::to_string(n) + " pages, " +
+                                              std::to_string(free_list_.size()) + " free"};
+    std::vector<PageId> out;
+    out.reserve(n);
+    for (size_t i = 0; i < n; ++i) {
+        PageId id = free_list_.back();
+        free_list_.pop_back();
+        pages_[id] = PageMeta{query, kNoLayer, false};
+        out.push_back(id);
+    }
+    auto& owned = owned_[query];
+    owned.insert(owned.end(), out.begin(), out.end());
+    return out;
+}
+
+void PagedKVStore::bind_layer(QueryId query, uint32_t layer, const std::vector<PageId>& pages) {
+    std::lock_guard lock(mu_);
+    auto& t = tables_[query];
+    if (t.layers.size() <= layer) t.layers.resize(layer + 1);
+    t.layers[layer] = pages;
+    t.dirty = true;
+    for (PageId id : pages) pages_[id].layer = layer;
+}
+
+std::vector<PageId> PagedKVStore::layer_pages(QueryId query, uint32_t layer) const {
+    std::lock_guard lock(mu_);
+    auto it = tables_.find(query);
+    if (it == tables_.end() || it->second.layers.size() <= layer) return {};
+    return it->second.layers[layer];
+}
+
+std::vector<PageId> PagedKVStore::release_query(QueryId query) {
+    std::lock_guard lock(mu_);
+    auto it = owned_.find(query);
+    if (it == owned_.end()) return {};
+    std::vector<PageId> freed = std::move(it->second);
+    owned_.erase(it);
+    tables_.erase(query);
+    for (PageId id : freed) {
+        pages_[id] = PageMeta{};
+        free_list_.push_back(id);
+    }
+    return freed;
+}
+
+size_t PagedKVStore::free_page_count() const {
+    std::lock_guard lock(mu_);
+    return free_list_.size();
+}
+
+size_t PagedKVStore::allocated_page_count() const {
+    std::lock_guard lock(mu_);
+    return pages_.size() - free_list_.size();
+}
+
+void PagedKVStore::mark_populated(PageId id, uint32_t layer) {
+    std::lock_guard lock(mu_);
+    pages_[id].layer = layer;
+    pages_[id].populated = true;
+}
+
+bool PagedKVStore::populated(PageId id) const {
+    std::lock_guard lock(mu_);
+    return pages_[id].populated;
+}
+
+PagedLayout PagedKVStore::layout() const {
+    PagedLayout L;
+    L.base = reinterpret_cast<uint64_t>(pool_.ptr);
+    L.page_stride = page_bytes();
+    L.token_stride = spec_.bytes_per_token_per_layer;
+    L.plane_bytes = spec_.bytes_per_token_per_layer;
+    L.plane_stride = 0;
+    L.n_planes = 1;
+    L.page_tokens = spec_.page_tokens;
+    L.bpt = spec_.bytes_per_token_per_layer;
+    L.shared_table = 0;
+    return L;
+}
+
+Result<PagedKVStore::DeviceTable> PagedKVStore::device_table(QueryId query, cudaStream_t stream) {
+    std::lock_guard lock(mu_);
+    auto it = tables_.find(query);
+    if (it == tables_.end()) return Status{Errc::unknown_query, "query has no page table"};
+    QueryTable& t = it->second;
+    if (t.dirty) {
+        size_t stride = 1;
+        for (const auto& l : t.layers) stride = std::max(stride, l.size());
+        const size_t rows = std::max<size_t>(spec_.num_layers, t.layers.size());
+        const size_t bytes = rows * stride * sizeof(int32_t);
+        // The pinned mirror may still feed an in-flight upload on another
+        // stream; order the rewrite after everything queued on `stream`.
+        if (t.host.bytes) TKV_CUDA(cudaStreamSynchronize(stream));
+        t.host.reserve(bytes);
+        t.dev.reserve(bytes);
+        auto* h = reinterpret_cast<int32_t*>(t.host.host);
+        std::fill(h, h + rows * stride, -1);
+        for (size_t l = 0; l < t.layers.size(); ++l)
+            std::copy(t.layers[l].begin(), t.layers[l].end(), h + l * stride);
+        TKV_CUDA(cudaMemcpyAsync(t.dev.ptr, t.host.host, bytes, cudaMemcpyHostToDevice, stream));
+        t.stride = uint32_t(stride);
+        t.dirty = false;
+    }
+    return DeviceTable{reinterpret_cast<const int32_t*>(t.dev.ptr), t.stride};
+}
+
+Status PagedKVStore::check_readable(const std::vector<PageId>& pages, uint32_t layer,
+                                    size_t token_count) const {
+    size_t capacity = pages.size() * spec_.page_tokens;
+    if (token_count > capacity)
+        return Status{Errc::size_mismatch, std::to_string(token_count) + " tokens across " +
+                                               std::to_string(pages.size()) + " pages"};
+    std::lock_guard lock(mu_);
+    for (PageId id : pages) {
+        if (id >= pages_.size()) return Status{Errc::invalid_argument, "page id out of range"};
+        const PageMeta& m = pages_[id];
+        if (!m.populated || m.layer != layer)
+            return Status{Errc::unpopulated_page,
+                          "page " + std::to_string(id) + " layer " + std::to_string(layer)};
+    }
+    return Status::success();
+}
+
+Status PagedKVStore::check_readable_span(QueryId query, uint32_t layer, size_t first_page,
+                                         size_t token_count) const {
+    std::lock_guard lock(mu_);
+    auto it = tables_.find(query);
+    if (it == tables_.end() || it->second.layers.size() <= layer)
+        return Status{Errc::size_mismatch, "no pages for layer " + std::to_string(layer)};
+    const auto& list = it->second.layers[layer];
+    const size_t need = (token_count + spec_.page_tokens - 1) / spec_.page_tokens;
+    if (first_page + need > list.size())
+        return Status{Errc::size_mismatch, std::to_string(token_count) + " tokens beyond pages"};
+    for (size_t i = first_page; i < first_page + need; ++i) {
+        const PageMeta& m = pages_[list[i]];
+        if (!m.populated || m.layer != layer)
+            return Status{Errc::unpopulated_page,
+                          "page " + std::to_string(list[i]) + " layer " + std::to_string(layer)};
+    }
+    return Status::success();
+}
+
+Status PagedKVStore::check_writable_span(QueryId query, uint32_t layer, size_t first_page,
+                                         size_t token_count) const {
+    std::lock_guard lock(mu_);
+    auto it = tables_.find(query);
+    if (it == tables_.end() || it->second.layers.size() <= layer)
+        return Status{Errc::size_mismatch, "scatter exceeds page capacity"};
+    const auto& list = it->second.layers[layer];
+    const size_t need = (token_count + spec_.page_tokens - 1) / spec_.page_tokens;
+    if (first_page + need > list.size())
+        return Status{Errc::size_mismatch, "scatter exceeds page capacity"};
+    for (size_t i = first_page; i < first_page + need; ++i) {
+        if (list[i] >= pages_.size()) return Status{Errc::invalid_argument, "page id out of range"};
+        if (pages_[list[i]].owner == kFree)
+            return Status{Errc::invalid_argument, "scatter into free page"};
+    }
+    return Status::success();
+}
+
+void PagedKVStore::mark_span_populated(QueryId query, uint32_t layer, size_t first_page,
+                                       size_t token_count) {
+    std::lock_guard lock(mu_);
+    auto it = tables_.find(query);
+    if (it == tables_.end() || it->second.layers.size() <= layer) return;
+    const auto& list = it->second.layers[layer];
+    const size_t need = (token_count + spec_.page_tokens - 1) / spec_.page_tokens;
+    for (size_t i = first_page; i < first_page + need && i < list.size(); ++i) {
+        pages_[list[i]].layer = layer;
+        pages_[list[i]].populated = true;
+    }
+}
+
+Status PagedKVStore::host_copy(const std::vector<PageId>& pages, uint32_t layer,
+                               size_t token_count, uint8_t* host, CopyDir dir) {
+    if (token_count == 0) return Status::success();
+    std::lock_guard lock(io_mu_);
+    TKV_CUDA(cudaSetDevice(device_));
+    const size_t bpt = spec_.bytes_per_token_per_layer;
+    const size_t bytes = token_count * bpt;
+    const size_t used_pages = (token_count + spec_.page_tokens - 1) / spec_.page_tokens;
+    // Device scratch: [XferDesc][tile_base x2][table]
+    const size_t table_off = 64;
+    const size_t scratch = table_off + used_pages * sizeof(int32_t);
+    io_dev_.reserve(scratch);
+    io_host_.reserve(scratch + bytes + 16);
+    uint8_t* payload = io_host_.host + ((scratch + 15) & ~size_t(15));
+    uint8_t* payload_dev = io_host_.dev + ((scratch + 15) & ~size_t(15));
+
+    const uint32_t ppt = std::max<uint32_t>(1, std::min<uint32_t>(64, 65536 / page_bytes()));
+    XferDesc d;
+    d.chunk = reinterpret_cast<uint64_t>(payload_dev);
+    d.layer_stride = 0;
+    d.table = reinterpret_cast<const int32_t*>(io_dev_.ptr + table_off);
+    d.table_stride = uint32_t(used_pages);
+    d.first_page = 0;
+    d.n_tokens = uint32_t(token_count);
+    uint32_t tiles = tiles_for(d.n_tokens, spec_.page_tokens, ppt, 1);
+    std::memcpy(io_host_.host, &d, sizeof d);
+    uint32_t tb[2] = {0, tiles};
+    std::memcpy(io_host_.host + 40, tb, sizeof tb);
+    auto* tab = reinterpret_cast<int32_t*>(io_host_.host + table_off);
+    for (size_t i = 0; i < used_pages; ++i) tab[i] = int32_t(pages[i]);
+    if (dir == CopyDir::scatter) std::memcpy(payload, host, bytes);
+    TKV_CUDA(cudaMemcpyAsync(io_dev_.ptr, io_host_.host, scratch, cudaMemcpyHostToDevice,
+                             io_stream_));
+    PagedLayout L = layout();
+    L.shared_table = 1;  // the single table row serves the requested layer
+    PagedCopyPlan P;
+    P.descs = reinterpret_cast<const XferDesc*>(io_dev_.ptr);
+    P.tile_base = reinterpret_cast<const uint32_t*>(io_dev_.ptr + 40);
+    P.n_desc = 1;
+    P.total_tiles = tiles;
+    P.layer_begin = layer;
+    P.n_layers = 1;
+    P.pages_per_tile = ppt;
+    P.addr_or = d.chunk;
+    TKV_CUDA(launch_paged_copy(L, P, dir, 0, io_stream_));
+    TKV_CUDA(cudaStreamSynchronize(io_stream_));
+    if (dir == CopyDir::gather) std::memcpy(host, payload, bytes);
+    return Status::success();
+}
+
+Status PagedKVStore::gather_tokens_into(const std::vector<PageId>& pages, uint32_t layer,
+                                        size_t token_count, uint8_t* out, size_t out_bytes) {
+    if (out_bytes != token_count * spec_.bytes_per_token_per_layer)
+        return Status{Errc::size_mismatch, "gather output size"};
+    Status st = check_readable(pages, layer, token_count);
+    if (!st.ok()) return st;
+    return host_copy(pages, layer, token_count, out, CopyDir::gather);
+}
+
+Result<std::vector<uint8_t>> PagedKVStore::gather_tokens(const std::vector<PageId>& pages,
+                                                         uint32_t layer, size_t token_count) {
+    std::vector<uint8_t> out(token_count * spec_.bytes_per_token_per_layer);
+    Status st = gather_tokens_into(pages, layer, token_count, out.data(), out.size());
+    if (!st.ok()) return st;
+    return out;
+}
+
+Status PagedKVStore::scatter_tokens(const uint8_t* buf, size_t buf_bytes,
+                                    const std::vector<PageId>& pages, uint32_t layer,
+                                    size_t token_count) {
+    if (buf_bytes != token_count * spec_.bytes_per_token_per_layer)
+        return Status{Errc::size_mismatch, "scatter input size"};
+    if (token_count > pages.size() * spec_.page_tokens)
+        return Status{Errc::size_mismatch, "scatter exceeds page capacity"};
+    {
+        std::lock_guard lock(mu_);
+        for (PageId id : pages) {
+            if (id >= pages_.size()) return Status{Errc::invalid_argument, "page id out of range"};
+            if (pages_[id].owner == kFree)
+                return Status{Errc::invalid_argument, "scatter into free page"};
+        }
+    }
+    Status st = host_copy(pages, layer, token_count, const_cast<uint8_t*>(buf), CopyDir::scatter);
+    if (!st.ok()) return st;
+    const size_t used = (token_count + spec_.page_tokens - 1) / spec_.page_tokens;
+    for (size_t i = 0; i < used; ++i) mark_populated(pages[i], layer);
+    return Status::success();
+}
+
+}  // namespace tkv

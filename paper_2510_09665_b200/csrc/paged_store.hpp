@@ -1,0 +1,108 @@
+// Engine-resident paged KV memory on the device (mirror of
+// include/tierkv/paged_store.hpp:19-82).
+//
+// Same bookkeeping as the reference — a pool of fixed pages, a stack free
+// list (page 0 handed out first, paged_store.cpp:8-14), per-(query, layer)
+// page lists, owner/layer/populated metadata and the same checks — but the
+// pool is ONE cudaMalloc slab in HBM (page p at base + p * page_bytes) and
+// each query's page lists are mirrored into a device page table
+// [num_layers][blocks] of int32 that the K1/K2/K4 kernels index directly.
+#pragma once
+
+#include <mutex>
+#include <unordered_map>
+#include <vector>
+
+#include "common.hpp"
+#include "kernels.hpp"
+
+namespace tkv {
+
+class PagedKVStore {
+public:
+    PagedKVStore(ModelSpec spec, uint32_t num_pages, int device = -1);
+
+    const ModelSpec& spec() const { return spec_; }
+    size_t page_bytes() const { return spec_.page_bytes(); }
+    uint32_t pool_pages() const { return uint32_t(pages_.size()); }
+    int device() const { return device_; }
+
+    Result<std::vector<PageId>> alloc_pages(QueryId query, size_t n);
+    void bind_layer(QueryId query, uint32_t layer, const std::vector<PageId>& pages);
+    std::vector<PageId> layer_pages(QueryId query, uint32_t layer) const;
+    std::vector<PageId> release_query(QueryId query);
+    size_t free_page_count() const;
+    size_t allocated_page_count() const;
+
+    uint8_t* page_data(PageId id) const { return pool_.ptr + size_t(id) * page_bytes(); }
+    void mark_populated(PageId id, uint32_t layer);
+    bool populated(PageId id) const;
+
+    // --- device view -------------------------------------------------------
+    PagedLayout layout() const;
+    struct DeviceTable {
+        const int32_t* ptr = nullptr;
+        uint32_t stride = 0;  // entries per layer row
+    };
+    // Uploads the query's page lists if they changed since the last upload
+    // (stream-ordered on `stream`). Fails for an unknown query.
+    Result<DeviceTable> device_table(QueryId query, cudaStream_t stream);
+
+    // --- checks shared by every data path (paged_store.cpp:94-111,147-162) --
+    // Pages [first, first+ceil(n/pt)) of (query, layer) exist, are owned and
+    // hold `layer` data (gather side).
+    Status check_readable_span(QueryId query, uint32_t layer, size_t first_page,
+                               size_t token_count) const;
+    // Same pages exist and are owned (scatter side).
+    Status check_writable_span(QueryId query, uint32_t layer, size_t first_page,
+                               size_t token_count) const;
+    // Marks the pages covering [first_page, +ceil(n/pt)) of the span populated.
+    void mark_span_populated(QueryId query, uint32_t layer, size_t first_page, size_t token_count);
+
+    // --- reference-shaped single-layer host API (tests, tools) -------------
+    // Synchronous: these move bytes between host memory and pages with the
+    // K1/K2 kernels on an internal stream.
+    Status gather_tokens_into(const std::vector<PageId>& pages, uint32_t layer,
+                              size_t token_count, uint8_t* out, size_t out_bytes);
+    Result<std::vector<uint8_t>> gather_tokens(const std::vector<PageId>& pages, uint32_t layer,
+                                               size_t token_count);
+    Status scatter_tokens(const uint8_t* buf, size_t buf_bytes, const std::vector<PageId>& pages,
+                          uint32_t layer, size_t token_count);
+
+private:
+    static constexpr QueryId kFree = ~QueryId(0);
+    static constexpr uint32_t kNoLayer = ~uint32_t(0);
+    struct PageMeta {
+        QueryId owner = kFree;
+        uint32_t layer = kNoLayer;
+        bool populated = false;
+    };
+    struct QueryTable {
+        std::vector<std::vector<PageId>> layers;
+        bool dirty = true;
+        uint32_t stride = 0;
+        PinnedBuffer host;
+        DeviceBuffer dev;
+    };
+
+    Status check_readable(const std::vector<PageId>& pages, uint32_t layer,
+                          size_t token_count) const;
+    Status host_copy(const std::vector<PageId>& pages, uint32_t layer, size_t token_count,
+                     uint8_t* host, CopyDir dir);
+
+    ModelSpec spec_;
+    int device_;
+    DeviceBuffer pool_;
+    std::vector<PageMeta> pages_;
+    std::vector<PageId> free_list_;
+    std::unordered_map<QueryId, QueryTable> tables_;
+    std::unordered_map<QueryId, std::vector<PageId>> owned_;
+    mutable std::mutex mu_;
+
+    std::mutex io_mu_;  // serialises the synchronous host API
+    Stream io_stream_;
+    PinnedBuffer io_host_;
+    DeviceBuffer io_dev_;
+};
+
+}  // namespace tkv

@@ -1,0 +1,184 @@
+// K3 — chained SHA-256 chunk keys, bit-exact with KeyChain::next
+// (src/tokens.cpp:22-42) over OpenSSL SHA-256 (src/hash.cpp:9-29).
+//
+// Message of chunk i of a chain (put_string16 / put_le, common.hpp:92-164):
+//     u16le(|tag|) | tag | digest_{i-1} (32 B, zeros for i = 0) | u32le tokens
+// With the 12-character tag of the configs that is 46 + 4*256 = 1070 bytes =
+// 17 SHA-256 blocks per 256-token chunk.
+//
+// Parallelism. The chain is serial: block 0 of chunk i holds digest_{i-1},
+// so chunks of one sequence cannot be compressed in parallel. One thread owns
+// one chain (request) and walks its chunks; independent requests fill the
+// GPU. Within a chunk the message words of the token-only blocks are packed
+// straight from the u32 token array with one byte-permute per word
+// (PRMT), so only the header block and the padding block take the generic
+// byte path.
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "kernels.hpp"
+
+namespace tkv {
+namespace {
+
+__constant__ uint32_t kK[64] = {
+    0x428a2f98, 0x71374491, 0xb5c0fbcf, 0xe9b5dba5, 0x3956c25b, 0x59f111f1, 0x923f82a4,
+    0xab1c5ed5, 0xd807aa98, 0x12835b01, 0x243185be, 0x550c7dc3, 0x72be5d74, 0x80deb1fe,
+    0x9bdc06a7, 0xc19bf174, 0xe49b69c1, 0xefbe4786, 0x0fc19dc6, 0x240ca1cc, 0x2de92c6f,
+    0x4a7484aa, 0x5cb0a9dc, 0x76f988da, 0x983e5152, 0xa831c66d, 0xb00327c8, 0xbf597fc7,
+    0xc6e00bf3, 0xd5a79147, 0x06ca6351, 0x14292967, 0x27b70a85, 0x2e1b2138, 0x4d2c6dfc,
+    0x53380d13, 0x650a7354, 0x766a0abb, 0x81c2c92e, 0x92722c85, 0xa2bfe8a1, 0xa81a664b,
+    0xc24b8b70, 0xc76c51a3, 0xd192e819, 0xd6990624, 0xf40e3585, 0x106aa070, 0x19a4c116,
+    0x1e376c08, 0x2748774c, 0x34b0bcb5, 0x391c0cb3, 0x4ed8aa4a, 0x5b9cca4f, 0x682e6ff3,
+    0x748f82ee, 0x78a5636f, 0x84c87814, 0x8cc70208, 0x90befffa, 0xa4506ceb, 0xbef9a3f7,
+    0xc67178f2};
+
+__device__ __forceinline__ uint32_t rotr(uint32_t x, int n) { return __funnelshift_r(x, x, n); }
+
+__device__ __forceinline__ void compress(uint32_t h[8], uint32_t w[16]) {
+    uint32_t a = h[0], b = h[1], c = h[2], d = h[3], e = h[4], f = h[5], g = h[6], hh = h[7];
+#pragma unroll
+    for (int t = 0; t < 64; ++t) {
+        uint32_t wt;
+        if (t < 16) {
+            wt = w[t];
+        } else {
+            const uint32_t w15 = w[(t - 15) & 15], w2 = w[(t - 2) & 15];
+            const uint32_t s0 = rotr(w15, 7) ^ rotr(w15, 18) ^ (w15 >> 3);
+            const uint32_t s1 = rotr(w2, 17) ^ rotr(w2, 19) ^ (w2 >> 10);
+            wt = w[t & 15] + s0 + w[(t - 7) & 15] + s1;
+            w[t & 15] = wt;
+        }
+        const uint32_t S1 = rotr(e, 6) ^ rotr(e, 11) ^ rotr(e, 25);
+        const uint32_t ch = (e & f) ^ (~e & g);
+        const uint32_t t1 = hh + S1 + ch + kK[t] + wt;
+        const uint32_t S0 = rotr(a, 2) ^ rotr(a, 13) ^ rotr(a, 22);
+        const uint32_t mj = (a & b) ^ (a & c) ^ (b & c);
+        hh = g;
+        g = f;
+        f = e;
+        e = d + t1;
+        d = c;
+        c = b;
+        b = a;
+        a = t1 + S0 + mj;
+    }
+    h[0] += a; h[1] += b; h[2] += c; h[3] += d;
+    h[4] += e; h[5] += f; h[6] += g; h[7] += hh;
+}
+
+struct ChunkMsg {
+    const uint32_t* tok;  // this chunk's tokens
+    uint32_t n;           // tokens in this chunk
+    uint32_t hdr;         // 2 + tag_len + 32: first token byte offset
+    uint32_t len;         // message bytes = hdr + 4n
+    uint32_t nblocks;     // padded blocks
+};
+
+// Generic message byte (header, parent, token, padding or length byte).
+__device__ __forceinline__ uint32_t msg_byte(const ChunkMsg& m, const HashParams& P,
+                                             const uint32_t parent[8], uint32_t o) {
+    const uint32_t tl = P.tag_len;
+    if (o < 2) return (tl >> (8 * o)) & 0xff;
+    if (o < 2 + tl) return P.tag[o - 2];
+    if (o < m.hdr) {
+        const uint32_t j = o - 2 - tl;
+        return (parent[j >> 2] >> (24 - 8 * (j & 3))) & 0xff;
+    }
+    if (o < m.len) {
+        const uint32_t k = o - m.hdr;
+        return (__ldg(m.tok + (k >> 2)) >> (8 * (k & 3))) & 0xff;
+    }
+    if (o == m.len) return 0x80;
+    const uint32_t end = 64 * m.nblocks;
+    if (o >= end - 8) {
+        const uint64_t bits = uint64_t(m.len) * 8;
+        return uint32_t(bits >> (8 * (end - 1 - o))) & 0xff;
+    }
+    return 0;
+}
+
+__device__ __forceinline__ void load_block(const ChunkMsg& m, const HashParams& P,
+                                           const uint32_t parent[8], uint32_t blk, uint32_t w[16]) {
+    const uint32_t o0 = 64 * blk;
+    if (o0 >= m.hdr && o0 + 64 <= m.len) {
+        // Token-only block: word at offset o = BE of stream bytes k..k+3,
+        // k = o - hdr, which straddle tokens k>>2 and (k>>2)+1 when k & 3 != 0.
+        const uint32_t k0 = o0 - m.hdr;
+        const uint32_t sh = k0 & 3;
+        const uint32_t sel = (sh + 3) | ((sh + 2) << 4) | ((sh + 1) << 8) | (sh << 12);
+        const uint32_t* t = m.tok + (k0 >> 2);
+        if (sh == 0) {
+#pragma unroll
+            for (int i = 0; i < 16; ++i) w[i] = __byte_perm(__ldg(t + i), 0, 0x0123);
+        } else {
+            uint32_t cur = __ldg(t);
+#pragma unroll
+            for (int i = 0; i < 16; ++i) {
+                const uint32_t nxt = __ldg(t + i + 1);
+                w[i] = __byte_perm(cur, nxt, sel);
+                cur = nxt;
+            }
+        }
+        return;
+    }
+#pragma unroll 1
+    for (int i = 0; i < 16; ++i) {
+        const uint32_t o = o0 + 4 * i;
+        w[i] = (msg_byte(m, P, parent, o) << 24) | (msg_byte(m, P, parent, o + 1) << 16) |
+               (msg_byte(m, P, parent, o + 2) << 8) | msg_byte(m, P, parent, o + 3);
+    }
+}
+
+__global__ void __launch_bounds__(128)
+hash_chains_kernel(const uint32_t* __restrict__ tokens, const ChainDesc* __restrict__ chains,
+                   uint32_t n_chains, const HashParams P, uint8_t* __restrict__ out) {
+    const uint32_t c = blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= n_chains) return;
+    const ChainDesc cd = chains[c];
+    uint32_t parent[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+        parent[i] = (uint32_t(cd.parent[4 * i]) << 24) | (uint32_t(cd.parent[4 * i + 1]) << 16) |
+                    (uint32_t(cd.parent[4 * i + 2]) << 8) | uint32_t(cd.parent[4 * i + 3]);
+    const uint32_t hdr = 2 + P.tag_len + 32;
+    uint32_t row = cd.out_first;
+    for (uint32_t start = 0; start < cd.n_tokens; start += P.chunk_size, ++row) {
+        ChunkMsg m;
+        m.tok = tokens + cd.token_off + start;
+        m.n = min(P.chunk_size, cd.n_tokens - start);
+        m.hdr = hdr;
+        m.len = hdr + 4 * m.n;
+        m.nblocks = (m.len + 9 + 63) / 64;
+        uint32_t h[8] = {0x6a09e667, 0xbb67ae85, 0x3c6ef372, 0xa54ff53a,
+                         0x510e527f, 0x9b05688c, 0x1f83d9ab, 0x5be0cd19};
+#pragma unroll 1
+        for (uint32_t b = 0; b < m.nblocks; ++b) {
+            uint32_t w[16];
+            load_block(m, P, parent, b, w);
+            compress(h, w);
+        }
+        uint32_t* o = reinterpret_cast<uint32_t*>(out + 32ull * row);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            parent[i] = h[i];
+            o[i] = __byte_perm(h[i], 0, 0x0123);  // digest bytes are big-endian words
+        }
+    }
+}
+
+}  // namespace
+
+cudaError_t launch_hash_chains(const uint32_t* tokens, const ChainDesc* chains, uint32_t n_chains,
+                               const HashParams& params, uint8_t* out, cudaStream_t stream) {
+    if (n_chains == 0) return cudaSuccess;
+    if (params.tag_len > uint32_t(kMaxTagBytes) || params.chunk_size == 0)
+        return cudaErrorInvalidValue;
+    const int threads = 128;
+    const int blocks = int((n_chains + threads - 1) / threads);
+    hash_chains_kernel<<<blocks, threads, 0, stream>>>(tokens, chains, n_chains, params, out);
+    return cudaGetLastError();
+}
+
+}  // namespace tkv

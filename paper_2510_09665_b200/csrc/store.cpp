@@ -1,0 +1,238 @@
+#include "store.hpp"
+
+#include <algorithm>
+#include <cstring>
+
+namespace tkv {
+
+const Status& PutHandle::wait() const {
+    std::unique_lock lock(st_->m);
+    st_->cv.wait(lock, [&] { return st_->done; });
+    return st_->status;
+}
+
+bool PutHandle::done() const {
+    std::lock_guard lock(st_->m);
+    return st_->done;
+}
+
+PutHandle PutHandle::immediate(Status st) {
+    auto s = std::make_shared<detail::PutState>();
+    s->done = true;
+    s->status = std::move(st);
+    return PutHandle(s);
+}
+
+namespace {
+void finish(const std::shared_ptr<detail::PutState>& s, Status st) {
+    {
+        std::lock_guard lock(s->m);
+        s->status = std::move(st);
+        s->done = true;
+    }
+    s->cv.notify_all();
+}
+}  // namespace
+
+TieredStore::TieredStore(StoreConfig cfg) : cfg_(std::move(cfg)) {
+    cfg_.model.validate(cfg_.chunk_size);
+    slot_bytes_ = cfg_.model.chunk_bytes(cfg_.chunk_size);
+    const size_t slots = cfg_.ram_pool_bytes / slot_bytes_;
+    if (slots) slab_.reserve(slots * slot_bytes_);
+    free_slots_.reserve(slots);
+    for (size_t i = slots; i > 0; --i) free_slots_.push_back(uint32_t(i - 1));  // slot 0 first
+}
+
+TieredStore::~TieredStore() = default;
+
+bool TieredStore::reserve_slot_locked(uint32_t& slot) {
+    if (free_slots_.empty()) evict_until_locked(slot_bytes_);
+    if (free_slots_.empty()) return false;
+    slot = free_slots_.back();
+    free_slots_.pop_back();
+    return true;
+}
+
+// LRU over present, unpinned, unshared entries (store.cpp:198-263, RAM branch).
+size_t TieredStore::evict_until_locked(size_t bytes_needed) {
+    size_t freed = 0;
+    while (freed < bytes_needed) {
+        const Digest* victim = nullptr;
+        uint64_t oldest = ~uint64_t(0);
+        for (const auto& [d, e] : index_) {
+            if (e.share_count > 0 || e.state != Entry::State::present || e.pinned) continue;
+            if (e.last_touch < oldest) {
+                oldest = e.last_touch;
+                victim = &d;
+            }
+        }
+        if (!victim) break;
+        auto it = index_.find(*victim);
+        free_slots_.push_back(it->second.slot);
+        index_.erase(it);
+        freed += slot_bytes_;
+    }
+    return freed;
+}
+
+size_t TieredStore::evict_until(size_t bytes_needed) {
+    std::lock_guard lock(mu_);
+    return evict_until_locked(bytes_needed);
+}
+
+Result<SlotWrite> TieredStore::begin_write(const Digest& digest, uint32_t token_count, bool pin) {
+    if (token_count == 0 || token_count > cfg_.chunk_size)
+        return Status{Errc::invalid_argument, "chunk geometry does not match store"};
+    std::lock_guard lock(mu_);
+    auto it = index_.find(digest);
+    if (it != index_.end()) {
+        Entry& e = it->second;
+        if (e.token_count != token_count)
+            return Status{Errc::invalid_argument, "digest indexed with other geometry"};
+        SlotWrite w;
+        if (e.state == Entry::State::present) {
+            // Idempotent: already stored, no new bytes (store.cpp:322-329).
+            if (pin) e.pinned = true;
+            touch(e);
+            w.kind = SlotWrite::Kind::already_present;
+            w.handle = PutHandle::immediate(Status::success());
+        } else {
+            w.kind = SlotWrite::Kind::in_flight;
+            w.handle = PutHandle(e.writer);
+            if (pin) e.pinned = true;
+        }
+        return w;
+    }
+    uint32_t slot = 0;
+    if (!reserve_slot_locked(slot)) return Status{Errc::tier_full, "ram pool exhausted"};
+    Entry e;
+    e.state = Entry::State::writing;
+    e.token_count = uint16_t(token_count);
+    e.slot = slot;
+    e.pinned = pin;
+    e.writer = std::make_shared<detail::PutState>();
+    SlotWrite w;
+    w.kind = SlotWrite::Kind::write;
+    w.host = slab_.host + size_t(slot) * slot_bytes_;
+    w.dev = slab_.dev + size_t(slot) * slot_bytes_;
+    w.handle = PutHandle(e.writer);
+    index_.emplace(digest, std::move(e));
+    return w;
+}
+
+void TieredStore::commit_write(const Digest& digest, const Status& status) {
+    std::shared_ptr<detail::PutState> writer;
+    {
+        std::lock_guard lock(mu_);
+        auto it = index_.find(digest);
+        if (it == index_.end() || it->second.state != Entry::State::writing) return;
+        writer = std::move(it->second.writer);
+        if (status.ok()) {
+            it->second.state = Entry::State::present;
+            touch(it->second);
+        } else {
+            free_slots_.push_back(it->second.slot);
+            index_.erase(it);
+        }
+    }
+    if (writer) finish(writer, status);
+}
+
+Result<SlotRead> TieredStore::acquire(const Digest& digest, uint32_t expect_tokens) {
+    std::lock_guard lock(mu_);
+    auto it = index_.find(digest);
+    if (it == index_.end() || it->second.state != Entry::State::present)
+        return Status{Errc::not_found, "no such chunk"};
+    Entry& e = it->second;
+    if (expect_tokens && e.token_count != expect_tokens)
+        return Status{Errc::size_mismatch, "record token count differs from plan"};
+    e.share_count++;
+    touch(e);
+    return SlotRead{slab_.host + size_t(e.slot) * slot_bytes_,
+                    slab_.dev + size_t(e.slot) * slot_bytes_, e.token_count};
+}
+
+void TieredStore::release(const Digest& digest) {
+    std::lock_guard lock(mu_);
+    auto it = index_.find(digest);
+    if (it != index_.end() && it->second.share_count > 0) it->second.share_count--;
+}
+
+PutHandle TieredStore::put(const Digest& digest, uint32_t token_count, const uint8_t* payload,
+                           size_t payload_bytes, bool pin) {
+    if (payload_bytes != size_t(token_count) * cfg_.model.num_layers *
+                             cfg_.model.bytes_per_token_per_layer)
+        return PutHandle::immediate(Status{Errc::invalid_argument, "chunk geometry does not match store"});
+    auto w = begin_write(digest, token_count, pin);
+    if (!w.ok()) return PutHandle::immediate(w.status());
+    if (w.value().kind != SlotWrite::Kind::write) return w.value().handle;
+    std::memcpy(w.value().host, payload, payload_bytes);
+    commit_write(digest, Status::success());
+    return w.value().handle;
+}
+
+Result<std::vector<uint8_t>> TieredStore::get(const Digest& digest) {
+    auto r = acquire(digest, 0);
+    if (!r.ok()) return r.status();
+    const size_t n = size_t(r.value().token_count) * cfg_.model.num_layers *
+                     cfg_.model.bytes_per_token_per_layer;
+    std::vector<uint8_t> out(r.value().host, r.value().host + n);
+    release(digest);
+    return out;
+}
+
+Result<std::vector<uint8_t>> TieredStore::get_layer(const Digest& digest, uint32_t layer) {
+    if (layer >= cfg_.model.num_layers) return Status{Errc::invalid_argument, "layer out of range"};
+    auto r = acquire(digest, 0);
+    if (!r.ok()) return r.status();
+    const size_t lb = size_t(r.value().token_count) * cfg_.model.bytes_per_token_per_layer;
+    const uint8_t* src = r.value().host + size_t(layer) * lb;
+    std::vector<uint8_t> out(src, src + lb);
+    release(digest);
+    return out;
+}
+
+bool TieredStore::contains(const Digest& digest) const {
+    std::lock_guard lock(mu_);
+    auto it = index_.find(digest);
+    return it != index_.end() && it->second.state == Entry::State::present;
+}
+
+Status TieredStore::pin(const Digest& digest, bool on) {
+    std::lock_guard lock(mu_);
+    auto it = index_.find(digest);
+    if (it == index_.end()) return Status{Errc::not_found, "no such chunk"};
+    it->second.pinned = on;
+    return Status::success();
+}
+
+ClearResult TieredStore::clear(const std::vector<Digest>& digests) {
+    ClearResult r;
+    std::lock_guard lock(mu_);
+    for (const auto& d : digests) {
+        auto it = index_.find(d);
+        if (it == index_.end()) continue;
+        Entry& e = it->second;
+        if (e.state != Entry::State::present || e.pinned || e.share_count > 0) {
+            r.refused++;
+            continue;
+        }
+        free_slots_.push_back(e.slot);
+        index_.erase(it);
+        r.removed++;
+    }
+    return r;
+}
+
+StoreStats TieredStore::stats() const {
+    std::lock_guard lock(mu_);
+    StoreStats s;
+    s.entries = index_.size();
+    s.ram_slots_total = slot_bytes_ ? slab_.bytes / slot_bytes_ : 0;
+    s.ram_slots_used = s.ram_slots_total - free_slots_.size();
+    for (const auto& [_, e] : index_)
+        if (e.state == Entry::State::present) s.ram_entries++;
+    return s;
+}
+
+}  // namespace tkv

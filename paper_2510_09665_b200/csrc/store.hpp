@@ -1,0 +1,148 @@
+// The pinned host tier (mirror of TieredStore's RAM tier,
+// include/tierkv/store.hpp:142-262, src/store.cpp).
+//
+// Same slot geometry as the reference RAM slab (store.cpp:96-102): a
+// pre-allocated slab of fixed slots of L * chunk_size * bpt bytes, one chunk
+// per slot, payload layer-major [L][T][bpt] with layer l at offset l*T*bpt
+// (store.cpp:343-345, 703-709). The slab is cudaHostAlloc'ed
+// (Mapped|Portable), so the gather kernel writes a chunk straight into its
+// slot over PCIe and the copy engine reads slot slices for loads.
+//
+// Same index semantics: digest-keyed entries, `writing` -> `present` only
+// after the bytes landed (store.cpp:333-357), idempotent duplicate puts
+// (:322-329), geometry checks (:439-443, 454-470), LRU eviction of present,
+// unpinned, unshared entries (:198-263), share counts that block eviction
+// and clear while a transfer reads a slot (:687-701, 836), pin and clear
+// (:808-862). Disk / remote tiers, codecs and the event pump are out of
+// scope.
+#pragma once
+
+#include <condition_variable>
+#include <memory>
+#include <mutex>
+#include <optional>
+#include <unordered_map>
+#include <vector>
+
+#include "common.hpp"
+
+namespace tkv {
+
+struct StoreConfig {
+    ModelSpec model;
+    size_t chunk_size = 256;
+    size_t ram_pool_bytes = 64ull << 20;
+};
+
+struct StoreStats {
+    size_t entries = 0;
+    size_t ram_slots_total = 0;
+    size_t ram_slots_used = 0;
+    size_t ram_entries = 0;
+};
+
+struct ClearResult {
+    size_t removed = 0;
+    size_t refused = 0;
+};
+
+namespace detail {
+struct PutState {
+    std::mutex m;
+    std::condition_variable cv;
+    bool done = false;
+    Status status;
+};
+}  // namespace detail
+
+// Awaitable completion of one chunk write (store.hpp:58-76).
+class PutHandle {
+public:
+    PutHandle() = default;
+    explicit PutHandle(std::shared_ptr<detail::PutState> st) : st_(std::move(st)) {}
+    const Status& wait() const;
+    bool done() const;
+    static PutHandle immediate(Status st);
+
+private:
+    std::shared_ptr<detail::PutState> st_;
+};
+
+// A reserved slot about to be written by the device.
+struct SlotWrite {
+    enum class Kind { write, already_present, in_flight } kind = Kind::write;
+    uint8_t* host = nullptr;   // slot base (host address)
+    uint8_t* dev = nullptr;    // slot base (device-visible alias)
+    PutHandle handle;          // completes when the bytes are present
+};
+
+// A slot pinned against eviction/clear while a transfer reads it.
+struct SlotRead {
+    uint8_t* host = nullptr;
+    uint8_t* dev = nullptr;
+    uint32_t token_count = 0;
+};
+
+class TieredStore {
+public:
+    explicit TieredStore(StoreConfig cfg);
+    ~TieredStore();
+    TieredStore(const TieredStore&) = delete;
+    TieredStore& operator=(const TieredStore&) = delete;
+
+    const StoreConfig& config() const { return cfg_; }
+    size_t slot_bytes() const { return slot_bytes_; }
+
+    // --- device write path (used by the connector's K1 store) --------------
+    // Claims a slot for `digest` (token_count rows per layer). Errors:
+    // invalid_argument for geometry mismatch, tier_full when no slot can be
+    // freed. The entry stays invisible to contains() until commit_write.
+    Result<SlotWrite> begin_write(const Digest& digest, uint32_t token_count, bool pin);
+    // Marks the entry present (ok) or drops the claim (error). Safe to call
+    // from a CUDA host callback (no CUDA API calls inside).
+    void commit_write(const Digest& digest, const Status& status);
+
+    // --- device read path (used by the connector's K2 load) ----------------
+    // Shares the entry (blocks eviction/clear) if present with the expected
+    // token count; release() when the transfer finished.
+    Result<SlotRead> acquire(const Digest& digest, uint32_t expect_tokens);
+    void release(const Digest& digest);
+
+    // --- reference-shaped API (store.hpp:153-171) ---------------------------
+    // Host payload put ([L][T][bpt]), synchronous; used to seed the tier.
+    PutHandle put(const Digest& digest, uint32_t token_count, const uint8_t* payload,
+                  size_t payload_bytes, bool pin = false);
+    Result<std::vector<uint8_t>> get(const Digest& digest);
+    Result<std::vector<uint8_t>> get_layer(const Digest& digest, uint32_t layer);
+    bool contains(const Digest& digest) const;
+    Status pin(const Digest& digest, bool on);
+    ClearResult clear(const std::vector<Digest>& digests);
+    size_t evict_until(size_t bytes_needed);
+    StoreStats stats() const;
+
+private:
+    struct Entry {
+        enum class State : uint8_t { writing, present };
+        State state = State::writing;
+        uint16_t token_count = 0;
+        uint32_t slot = 0;
+        bool pinned = false;
+        uint32_t share_count = 0;
+        uint64_t last_touch = 0;
+        std::shared_ptr<detail::PutState> writer;  // set while writing
+    };
+
+    bool reserve_slot_locked(uint32_t& slot);
+    size_t evict_until_locked(size_t bytes_needed);
+    void touch(Entry& e) { e.last_touch = ++clock_; }
+
+    StoreConfig cfg_;
+    size_t slot_bytes_ = 0;
+    PinnedBuffer slab_;
+    mutable std::mutex mu_;
+    std::unordered_map<Digest, Entry, DigestHasher> index_;
+    std::vector<uint32_t> free_slots_;
+    uint64_t clock_ = 0;
+};
+
+}  // namespace tkv

@@ -1,0 +1,125 @@
+#include "tokens.hpp"
+
+#include <algorithm>
+#include <stdexcept>
+
+namespace tkv {
+
+std::vector<ChunkSpan> chunk_tokens(size_t n, size_t chunk_size) {
+    if (chunk_size < 1) throw std::invalid_argument("chunk_size must be >= 1");
+    std::vector<ChunkSpan> spans;
+    spans.reserve((n + chunk_size - 1) / chunk_size);
+    for (size_t start = 0; start < n; start += chunk_size)
+        spans.push_back({start, std::min(start + chunk_size, n)});
+    return spans;
+}
+
+KeyHasher::KeyHasher(std::string model_tag, size_t chunk_size, int device)
+    : tag_(std::move(model_tag)), chunk_size_(chunk_size), device_(device) {
+    if (chunk_size_ < 1) throw std::invalid_argument("chunk_size must be >= 1");
+    if (tag_.size() > size_t(kMaxTagBytes))
+        throw std::invalid_argument("model tag longer than the device hash supports");
+    if (device_ < 0) TKV_CUDA(cudaGetDevice(&device_));
+    stream_ = Stream::create();
+}
+
+std::vector<std::vector<Digest>> KeyHasher::hash(const std::vector<TokenSpanView>& seqs,
+                                                 const std::vector<Digest>* parents) {
+    std::lock_guard lock(mu_);
+    TKV_CUDA(cudaSetDevice(device_));
+    size_t total_tokens = 0, total_chunks = 0;
+    for (const auto& s : seqs) {
+        total_tokens += s.size();
+        total_chunks += (s.size() + chunk_size_ - 1) / chunk_size_;
+    }
+    std::vector<std::vector<Digest>> out(seqs.size());
+    if (total_chunks == 0) return out;
+
+    h_tokens_.reserve(total_tokens * sizeof(TokenId) + 4);
+    h_chains_.reserve(seqs.size() * sizeof(ChainDesc));
+    h_out_.reserve(total_chunks * 32);
+    d_tokens_.reserve(total_tokens * sizeof(TokenId) + 4);
+    d_chains_.reserve(seqs.size() * sizeof(ChainDesc));
+    d_out_.reserve(total_chunks * 32);
+
+    auto* tok = reinterpret_cast<TokenId*>(h_tokens_.host);
+    auto* ch = reinterpret_cast<ChainDesc*>(h_chains_.host);
+    size_t toff = 0, row = 0;
+    for (size_t i = 0; i < seqs.size(); ++i) {
+        std::copy(seqs[i].begin(), seqs[i].end(), tok + toff);
+        ChainDesc d;
+        d.token_off = toff;
+        d.n_tokens = uint32_t(seqs[i].size());
+        d.out_first = uint32_t(row);
+        if (parents) std::copy((*parents)[i].begin(), (*parents)[i].end(), d.parent);
+        ch[i] = d;
+        toff += seqs[i].size();
+        row += (seqs[i].size() + chunk_size_ - 1) / chunk_size_;
+    }
+    HashParams p;
+    p.chunk_size = uint32_t(chunk_size_);
+    p.tag_len = uint32_t(tag_.size());
+    std::copy(tag_.begin(), tag_.end(), p.tag);
+
+    TKV_CUDA(cudaMemcpyAsync(d_tokens_.ptr, h_tokens_.host, total_tokens * sizeof(TokenId),
+                             cudaMemcpyHostToDevice, stream_));
+    TKV_CUDA(cudaMemcpyAsync(d_chains_.ptr, h_chains_.host, seqs.size() * sizeof(ChainDesc),
+                             cudaMemcpyHostToDevice, stream_));
+    TKV_CUDA(launch_hash_chains(reinterpret_cast<const uint32_t*>(d_tokens_.ptr),
+                                reinterpret_cast<const ChainDesc*>(d_chains_.ptr),
+                                uint32_t(seqs.size()), p, d_out_.ptr, stream_));
+    TKV_CUDA(cudaMemcpyAsync(h_out_.host, d_out_.ptr, total_chunks * 32, cudaMemcpyDeviceToHost,
+                             stream_));
+    TKV_CUDA(cudaStreamSynchronize(stream_));
+    ++launches_;
+    chunks_ += total_chunks;
+
+    row = 0;
+    for (size_t i = 0; i < seqs.size(); ++i) {
+        size_t n = (seqs[i].size() + chunk_size_ - 1) / chunk_size_;
+        out[i].resize(n);
+        for (size_t c = 0; c < n; ++c, ++row)
+            std::copy(h_out_.host + 32 * row, h_out_.host + 32 * row + 32, out[i][c].begin());
+    }
+    return out;
+}
+
+std::vector<Digest> KeyHasher::hash_one(TokenSpanView seq, const Digest& parent) {
+    std::vector<Digest> parents{parent};
+    return std::move(hash({seq}, &parents)[0]);
+}
+
+std::vector<ChunkKey> chunk_keys(KeyHasher& hasher, TokenSpanView tokens) {
+    auto digests = hasher.hash_one(tokens);
+    std::vector<ChunkKey> keys(digests.size());
+    for (size_t i = 0; i < digests.size(); ++i)
+        keys[i] = ChunkKey{digests[i], hasher.model_tag(), uint32_t(i)};
+    return keys;
+}
+
+ChunkKey KeyChain::next(TokenSpanView tokens) {
+    if (tokens.empty() || tokens.size() > hasher_->chunk_size())
+        throw std::invalid_argument("chunk token count out of range");  // tokens.cpp:23-24
+    auto d = hasher_->hash_one(tokens, parent_);
+    ChunkKey key{d.at(0), hasher_->model_tag(), index_};
+    parent_ = key.digest;
+    ++index_;
+    return key;
+}
+
+size_t longest_prefix_match(const std::vector<ChunkKey>& keys, size_t n_tokens, size_t chunk_size,
+                            const KeyIndex& index) {
+    size_t matched = 0;
+    for (size_t i = 0; i < keys.size(); ++i) {
+        if (!index(keys[i])) break;
+        matched = std::min(n_tokens, (i + 1) * chunk_size);
+    }
+    return matched;
+}
+
+size_t longest_prefix_match(KeyHasher& hasher, TokenSpanView tokens, const KeyIndex& index) {
+    return longest_prefix_match(chunk_keys(hasher, tokens), tokens.size(), hasher.chunk_size(),
+                                index);
+}
+
+}  // namespace tkv

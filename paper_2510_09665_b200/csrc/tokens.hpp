@@ -1,0 +1,96 @@
+// Chunking and chunk keys (mirror of include/tierkv/tokens.hpp:13-73).
+//
+// The arithmetic is the reference's: 256-token spans (only the last may be
+// short), digest_i = SHA-256(u16le(|tag|) | tag | digest_{i-1} | u32le tokens).
+// The difference is where it runs: every digest is computed by the K3 kernel
+// (sha256_chain.cu) through a KeyHasher, one thread per sequence, and a
+// sequence is hashed ONCE per query — the reference re-derives the same chain
+// three to four times (connector.cpp:74,103,139,446-450).
+#pragma once
+
+#include <functional>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "common.hpp"
+#include "kernels.hpp"
+
+namespace tkv {
+
+struct ChunkSpan {
+    size_t start = 0;
+    size_t end = 0;
+    size_t length() const { return end - start; }
+    bool operator==(const ChunkSpan&) const = default;
+};
+
+struct ChunkKey {
+    Digest digest = kZeroDigest;
+    std::string model_tag;
+    uint32_t chunk_index = 0;
+    bool operator==(const ChunkKey& o) const { return digest == o.digest; }  // tokens.hpp:33
+};
+
+// tokens.cpp:7-15. Throws std::invalid_argument for chunk_size < 1.
+std::vector<ChunkSpan> chunk_tokens(size_t n_tokens, size_t chunk_size);
+
+// Device SHA-256 chain engine. Thread-safe (one launch at a time).
+class KeyHasher {
+public:
+    KeyHasher(std::string model_tag, size_t chunk_size, int device = -1);
+
+    const std::string& model_tag() const { return tag_; }
+    size_t chunk_size() const { return chunk_size_; }
+
+    // Digests of every chunk of every sequence, in one kernel launch.
+    // parents (optional, one per sequence) resume a chain (KeyChain::reset).
+    std::vector<std::vector<Digest>> hash(const std::vector<TokenSpanView>& seqs,
+                                          const std::vector<Digest>* parents = nullptr);
+    std::vector<Digest> hash_one(TokenSpanView seq, const Digest& parent = kZeroDigest);
+
+    // Launch counters (tests assert the once-per-query property).
+    uint64_t launches() const { return launches_; }
+    uint64_t chunks_hashed() const { return chunks_; }
+
+private:
+    std::string tag_;
+    size_t chunk_size_;
+    int device_;
+    std::mutex mu_;
+    Stream stream_;
+    PinnedBuffer h_tokens_, h_chains_, h_out_;
+    DeviceBuffer d_tokens_, d_chains_, d_out_;
+    uint64_t launches_ = 0, chunks_ = 0;
+};
+
+// tokens.cpp:49-57.
+std::vector<ChunkKey> chunk_keys(KeyHasher& hasher, TokenSpanView tokens);
+
+// Incremental chain (tokens.hpp:41-63); each next() is one device launch.
+class KeyChain {
+public:
+    explicit KeyChain(KeyHasher& hasher) : hasher_(&hasher) {}
+    ChunkKey next(TokenSpanView chunk_tokens);
+    const Digest& parent() const { return parent_; }
+    uint32_t next_index() const { return index_; }
+    void reset(const Digest& parent, uint32_t next_index) {
+        parent_ = parent;
+        index_ = next_index;
+    }
+
+private:
+    KeyHasher* hasher_;
+    Digest parent_ = kZeroDigest;
+    uint32_t index_ = 0;
+};
+
+using KeyIndex = std::function<bool(const ChunkKey&)>;
+
+// tokens.cpp:59-69 over precomputed keys: k full chunks matched -> k * cs,
+// plus the partial tail when that is present too; stops at the first miss.
+size_t longest_prefix_match(const std::vector<ChunkKey>& keys, size_t n_tokens, size_t chunk_size,
+                            const KeyIndex& index);
+size_t longest_prefix_match(KeyHasher& hasher, TokenSpanView tokens, const KeyIndex& index);
+
+}  // namespace tkv

@@ -1,0 +1,299 @@
+"""Engine-agnostic scenarios ported from the reference's connector tests
+(tests/test_connector.cpp). Each takes an engine factory — either
+``oracle.RefEngine`` (the unmodified reference, CPU) or
+``paper_2510_09665_b200.api.Engine`` (this repo, B200) — drives it exactly
+like the reference test drives its Connector, and returns a plain dict of
+observable outcomes (hit lengths, plans, loaded tokens, page bytes, stored
+payloads, statuses). Parity = the two dicts are equal.
+"""
+from __future__ import annotations
+
+import hashlib
+
+import numpy as np
+
+CONN = dict(num_layers=4, bpt=64, page_tokens=16, tag="conn-test", chunk_size=32)
+
+
+def make_prompt(n: int, seed: int, vocab: int = 32000) -> np.ndarray:
+    rng = np.random.default_rng(seed)
+    return rng.integers(0, vocab, size=n, dtype=np.uint32)
+
+
+def run_transfer_ref(e, m, qid, prompt):
+    """Reference flavour: compute_range covers all layers (test helper)."""
+    n_layers = e.num_layers
+    assert e.start_load_kv(m) == 0
+    layerwise = e.meta_layerwise(m)
+    for layer in range(n_layers):
+        if layerwise:
+            assert e.wait_load_kv(m, layer) == 0
+        loaded = e.loaded_tokens(m, qid)
+        e.compute_range(qid, prompt, loaded, len(prompt))
+        if layerwise:
+            if layer > 0:
+                assert e.wait_store_kv(m, layer - 1) == 0
+            assert e.start_store_kv(m) == 0
+    if layerwise:
+        assert e.wait_store_kv(m, n_layers - 1) == 0
+    else:
+        assert e.start_store_kv(m) == 0
+
+
+def transfer(e, m, qid, prompt):
+    if hasattr(e, "stream_handle"):
+        # B200 engine: compute each layer just before its store (engine order).
+        n_layers = e.num_layers
+        assert e.start_load_kv(m) == 0
+        layerwise = e.meta_layerwise(m)
+        for layer in range(n_layers):
+            if layerwise:
+                assert e.wait_load_kv(m, layer) == 0
+            loaded = e.loaded_tokens(m, qid)
+            e.compute_range(qid, prompt, loaded, len(prompt), layers=(layer, layer + 1))
+            if layerwise:
+                if layer > 0:
+                    assert e.wait_store_kv(m, layer - 1) == 0
+                assert e.start_store_kv(m) == 0
+        if layerwise:
+            assert e.wait_store_kv(m, n_layers - 1) == 0
+        else:
+            assert e.start_store_kv(m) == 0
+    else:
+        run_transfer_ref(e, m, qid, prompt)
+
+
+def page_image(e, qid, n_tokens):
+    """sha256 of every layer's gathered bytes for tokens [0, n)."""
+    h = hashlib.sha256()
+    for layer in range(e.num_layers):
+        h.update(e.gather_layer(qid, layer, n_tokens).tobytes())
+    return h.hexdigest()
+
+
+def pages_equal_synth(e, qid, prompt, n_tokens, C):
+    seed = C.model_seed(e.tag)
+    for layer in range(e.num_layers):
+        want = C.synth_layer_kv(seed, prompt[:n_tokens], layer, 0, e.bpt)
+        if not np.array_equal(e.gather_layer(qid, layer, n_tokens), want):
+            return False
+    return True
+
+
+def plan_view(e, m, qi):
+    lp, matched = e.plan(m, qi, "load")
+    sp, _ = e.plan(m, qi, "store")
+    return {"matched": matched, "load": [(a, b, r, d.hex()) for a, b, r, _, d in lp],
+            "store": [(a, b, r, d.hex()) for a, b, r, _, d in sp]}
+
+
+# ---------------------------------------------------------------- scenarios
+
+def sc_match_cap(factory, C):
+    """test_connector.cpp:182-212."""
+    out = {}
+    prompt = make_prompt(10000, 7)
+    for name, n, p in [("9984", 9984, prompt), ("10000", 10000, prompt), ("512", 512, prompt[:512]),
+                       ("cold", 0, prompt)]:
+        e = factory(num_layers=2, bpt=8, page_tokens=16, tag="match-cap", chunk_size=256, ram_slots=64,
+                    num_pages=8)
+        if n:
+            e.seed_store(p, n)
+        out[name] = e.get_num_new_matched_tokens(1, p)
+        e.close()
+    return out
+
+
+def sc_load_plan_clip(factory, C):
+    """test_connector.cpp:214-242."""
+    e = factory(**CONN, ram_slots=16, num_pages=64)
+    prompt = make_prompt(70, 11)
+    e.seed_store(prompt, 70)
+    out = {"match": e.get_num_new_matched_tokens(9, prompt)}
+    e.bind_pages(9, 70)
+    out["update"] = e.update_state_after_alloc(9, 5, 5)
+    m = e.build_connector_meta([(9, prompt)])
+    out["plan"] = plan_view(e, m, 0)
+    e.release_query(9)
+    e.close()
+    return out
+
+
+def sc_inconsistent_alloc(factory, C):
+    """test_connector.cpp:244-258."""
+    e = factory(**CONN, ram_slots=16, num_pages=64)
+    prompt = make_prompt(64, 13)
+    e.seed_store(prompt, 64)
+    out = {"match": e.get_num_new_matched_tokens(2, prompt),
+           "a": e.update_state_after_alloc(2, 4, 3), "b": e.update_state_after_alloc(2, 3, 4),
+           "c": e.update_state_after_alloc(99, 4, 4), "d": e.update_state_after_alloc(2, 4, 4)}
+    e.close()
+    return out
+
+
+def sc_partial_match(factory, C):
+    """test_connector.cpp:260-312: load the stored prefix, store the rest, rerun."""
+    e = factory(**CONN, ram_slots=16, num_pages=64)
+    prompt = make_prompt(64, 17)
+    e.seed_store(prompt, 32)
+    out = {"match1": e.get_num_new_matched_tokens(5, prompt)}
+    e.bind_pages(5, 64)
+    out["upd1"] = e.update_state_after_alloc(5, 4, 2)
+    m = e.build_connector_meta([(5, prompt)])
+    out["plan1"] = plan_view(e, m, 0)
+    transfer(e, m, 5, prompt)
+    out["loaded1"] = e.loaded_tokens(m, 5)
+    out["pages1_ok"] = pages_equal_synth(e, 5, prompt, 64, C)
+    res = e.store_results(m, 5)
+    out["results1"] = [(d.hex(), c) for d, c in res]
+    stored = e.store_get(res[0][0])
+    want = C.synth_chunk(C.model_seed(e.tag), prompt, 32, 32, e.num_layers, e.bpt)
+    out["stored_ok"] = stored is not None and np.array_equal(stored, want)
+    out["finish1"] = e.finish_query(5)
+    e.release_query(5)
+    out["match2"] = e.get_num_new_matched_tokens(6, prompt)
+    e.bind_pages(6, 64)
+    out["upd2"] = e.update_state_after_alloc(6, 4, 4)
+    m2 = e.build_connector_meta([(6, prompt)])
+    out["plan2"] = plan_view(e, m2, 0)
+    transfer(e, m2, 6, prompt)
+    out["loaded2"] = e.loaded_tokens(m2, 6)
+    out["pages2_ok"] = pages_equal_synth(e, 6, prompt, 64, C)
+    out["finish2"] = e.finish_query(6)
+    e.release_query(6)
+    out["free_all"] = e.free_page_count() == 64
+    e.close()
+    return out
+
+
+def sc_layerwise_vs_blocking(factory, C):
+    """test_connector.cpp:314-358: same end state in both modes."""
+    prompt = make_prompt(96, 23)
+    out = {}
+    for layerwise in (True, False):
+        e = factory(**CONN, ram_slots=16, num_pages=64, layerwise=layerwise)
+        e.seed_store(prompt, 64)
+        key = "layerwise" if layerwise else "blocking"
+        out[key + "_match"] = e.get_num_new_matched_tokens(1, prompt)
+        e.bind_pages(1, 96)
+        e.update_state_after_alloc(1, 6, 4)
+        m = e.build_connector_meta([(1, prompt)])
+        transfer(e, m, 1, prompt)
+        out[key + "_loaded"] = e.loaded_tokens(m, 1)
+        res = e.store_results(m, 1)
+        stored = e.store_get(res[0][0])
+        out[key + "_image"] = page_image(e, 1, 96) + hashlib.sha256(stored.tobytes()).hexdigest()
+        out[key + "_ok"] = pages_equal_synth(e, 1, prompt, 96, C)
+        e.finish_query(1)
+        e.release_query(1)
+        e.close()
+    return out
+
+
+def sc_vanishing_chunk(factory, C):
+    """test_connector.cpp:360-385: a chunk cleared after planning shortens
+    the delivered prefix; the engine recomputes the tail."""
+    e = factory(**CONN, ram_slots=16, num_pages=64)
+    prompt = make_prompt(96, 29)
+    e.seed_store(prompt, 64)
+    keys = C.chunk_keys(prompt[:64], 32, CONN["tag"])
+    out = {"match": e.get_num_new_matched_tokens(3, prompt)}
+    e.bind_pages(3, 96)
+    e.update_state_after_alloc(3, 6, 4)
+    m = e.build_connector_meta([(3, prompt)])
+    out["cleared"] = e.store_clear(keys[1])
+    transfer(e, m, 3, prompt)
+    out["loaded"] = e.loaded_tokens(m, 3)
+    out["pages_ok"] = pages_equal_synth(e, 3, prompt, 96, C)
+    e.finish_query(3)
+    e.release_query(3)
+    e.close()
+    return out
+
+
+def sc_tier_full(factory, C):
+    """test_connector.cpp:429-461: one slot, pinned stores -> one ok, one tier_full."""
+    e = factory(**CONN, ram_slots=1, num_pages=64, pin_stores=True)
+    prompt = make_prompt(64, 41)
+    out = {"match": e.get_num_new_matched_tokens(4, prompt)}
+    e.bind_pages(4, 64)
+    out["upd"] = e.update_state_after_alloc(4, 4, 0)
+    m = e.build_connector_meta([(4, prompt)])
+    out["n_store"] = len(e.plan(m, 0, "store")[0])
+    transfer(e, m, 4, prompt)
+    codes = sorted(c for _, c in e.store_results(m, 4))
+    out["codes"] = codes  # [0 (ok), 2 (tier_full)]
+    e.finish_query(4)
+    e.release_query(4)
+    e.close()
+    return out
+
+
+def sc_degrade_blocking(factory, C):
+    """test_connector.cpp:463-490: over-budget batch degrades to blocking."""
+    e = factory(**CONN, ram_slots=16, num_pages=64, staging_budget=100)
+    prompt = make_prompt(64, 43)
+    e.seed_store(prompt, 64)
+    out = {"match": e.get_num_new_matched_tokens(8, prompt)}
+    e.bind_pages(8, 64)
+    out["upd"] = e.update_state_after_alloc(8, 4, 4)
+    m = e.build_connector_meta([(8, prompt)])
+    out["mode_before"] = e.meta_layerwise(m)
+    out["start"] = e.start_load_kv(m)
+    out["mode_after"] = e.meta_layerwise(m)
+    loaded = e.loaded_tokens(m, 8)
+    out["loaded"] = loaded
+    e.compute_range(8, prompt, loaded, len(prompt))
+    out["store"] = e.start_store_kv(m)
+    out["pages_ok"] = pages_equal_synth(e, 8, prompt, 64, C)
+    e.finish_query(8)
+    e.release_query(8)
+    e.close()
+    return out
+
+
+def sc_multi_query_batch(factory, C):
+    """Several queries in one scheduling iteration (SchedulerOutput with
+    multiple queries): mixed warm / partial / cold, one metadata."""
+    e = factory(**CONN, ram_slots=32, num_pages=256)
+    prompts = {10: make_prompt(96, 101), 11: make_prompt(70, 102), 12: make_prompt(50, 103)}
+    e.seed_store(prompts[10], 96)
+    e.seed_store(prompts[11], 32)
+    out = {}
+    for q, p in prompts.items():
+        out[f"match{q}"] = e.get_num_new_matched_tokens(q, p)
+        e.bind_pages(q, len(p))
+        blocks = (len(p) + 15) // 16
+        e.update_state_after_alloc(q, blocks, (out[f"match{q}"] + 15) // 16)
+    m = e.build_connector_meta(list(prompts.items()))
+    for i, q in enumerate(prompts):
+        out[f"plan{q}"] = plan_view(e, m, i)
+    # Engine order for a batch: every query's layer computed, then stores.
+    assert e.start_load_kv(m) == 0
+    layerwise = e.meta_layerwise(m)
+    for layer in range(e.num_layers):
+        if layerwise:
+            assert e.wait_load_kv(m, layer) == 0
+        for q, p in prompts.items():
+            lo = e.loaded_tokens(m, q)
+            if hasattr(e, "stream_handle"):
+                e.compute_range(q, p, lo, len(p), layers=(layer, layer + 1))
+            else:
+                e.compute_range(q, p, lo, len(p))
+        if layer > 0:
+            assert e.wait_store_kv(m, layer - 1) == 0
+        assert e.start_store_kv(m) == 0
+    assert e.wait_store_kv(m, e.num_layers - 1) == 0
+    for q, p in prompts.items():
+        out[f"loaded{q}"] = e.loaded_tokens(m, q)
+        out[f"ok{q}"] = pages_equal_synth(e, q, p, len(p), C)
+        out[f"res{q}"] = [(d.hex(), c) for d, c in e.store_results(m, q)]
+        e.finish_query(q)
+        e.release_query(q)
+    out["entries"] = e.store_entries()
+    e.close()
+    return out
+
+
+ALL = [sc_match_cap, sc_load_plan_clip, sc_inconsistent_alloc, sc_partial_match, sc_layerwise_vs_blocking,
+       sc_vanishing_chunk, sc_tier_full, sc_degrade_blocking, sc_multi_query_batch]

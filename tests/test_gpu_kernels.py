@@ -1,0 +1,270 @@
+"""Kernel parity on the B200: K3 (chained SHA-256 keys), K1/K2 (paged
+gather/scatter), K4 (synthetic KV) against the CPU oracle (oracle/), byte for
+byte. Shapes cover the reference tests' edge cases (empty, ragged tails,
+chunk sizes 1/16/256/257, tag lengths that push the parent digest across a
+SHA block boundary) and the configs' geometries (bpt 4096 / 512)."""
+import ctypes as ct
+import random
+
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+
+def rand_tokens(rng, n, vocab=128256):
+    return rng.integers(0, vocab, size=n, dtype=np.uint32)
+
+
+# ---------------------------------------------------------------- K3 -------
+
+def test_keys_appendix_a(tkv):
+    from paper_2510_09665_b200.api import chunk_keys
+    got = [k.hex() for k in chunk_keys(list(range(600)), 256, "m")]
+    assert got == ["5adb258b77fe3a6f5d2341135db04896c6bd5d5e13bb18923c88e5247cef9dc0",
+                   "c153731d406774e9d83ac9fbad6414e6ffa2c838afd908b48a3701230faac9b3",
+                   "7764a4adf62fa1e539afebddb8905ff5457aee5ce4c234d036cc8dd90a0376d4"]
+    t2 = [(i * 7919) % 128256 for i in range(1000)]
+    got = [k.hex() for k in chunk_keys(t2, 256, "llama-3.1-8b")]
+    assert got == ["4ac68da485c720853487c36c92e79af957b3bfb514b4cd0a8c1a75d28e574831",
+                   "e67ecd2e864d42958ce0f1e3a5da5e69ddb87e47b57c76fbf63579f5417516d7",
+                   "39da76fef676a9ed6f0f7a91db987bbe60dde3c0fcd477ef80059af788910a9e",
+                   "b051f7c6957dd2d1db868787f5054fab9a067435807a75ef271bd34f941884e2"]
+
+
+@pytest.mark.parametrize("cs", [1, 16, 256, 257])
+def test_keys_match_oracle_random(tkv, C, cs):
+    from paper_2510_09665_b200.api import chunk_keys
+    rng = np.random.default_rng(cs)
+    for n in [0, 1, cs - 1 if cs > 1 else 2, cs, cs + 1, 3 * cs + 7, 1000]:
+        t = rand_tokens(rng, n)
+        assert chunk_keys(t, cs, "m") == C.chunk_keys(t, cs, "m"), (cs, n)
+
+
+@pytest.mark.parametrize("tag", ["", "m", "llama-3.1-8b", "x" * 29, "y" * 30, "z" * 40, "t" * 200])
+def test_keys_tag_lengths(tkv, C, tag):
+    """Tag length moves the parent digest and the token stream across SHA
+    block boundaries and changes the token byte misalignment."""
+    from paper_2510_09665_b200.api import chunk_keys
+    rng = np.random.default_rng(len(tag))
+    for n in [1, 5, 255, 256, 600]:
+        t = rand_tokens(rng, n)
+        assert chunk_keys(t, 256, tag) == C.chunk_keys(t, 256, tag), (len(tag), n)
+
+
+def test_keychain_resume(tkv, C):
+    from paper_2510_09665_b200.api import chunk_keys, keychain_next
+    rng = np.random.default_rng(14)
+    t = rand_tokens(rng, 700)
+    direct = chunk_keys(t, 256, "m")
+    assert keychain_next("m", 256, direct[1], t[512:700]) == direct[2]
+
+
+def test_hash_chains_many_requests(tkv, C):
+    """One launch over many independent chains of ragged lengths (K3 over
+    requests), checked chain by chain against the oracle."""
+    from paper_2510_09665_b200.api import ChainDescC, hash_chains
+    rng = np.random.default_rng(7)
+    lens = [int(x) for x in rng.integers(0, 3000, size=97)] + [0, 1, 256, 4096]
+    toks = [rand_tokens(rng, n) for n in lens]
+    flat = np.concatenate(toks + [np.zeros(1, np.uint32)])
+    chains = (ChainDescC * len(lens))()
+    off = row = 0
+    for i, n in enumerate(lens):
+        chains[i].token_off = off
+        chains[i].n_tokens = n
+        chains[i].out_first = row
+        off += n
+        row += (n + 255) // 256
+    dev_t = torch.from_numpy(flat.view(np.int32)).cuda()
+    dev_c = torch.frombuffer(bytearray(bytes(chains)), dtype=torch.uint8).cuda()
+    out = torch.zeros(max(1, row) * 32, dtype=torch.uint8, device="cuda")
+    hash_chains(dev_t, dev_c, len(lens), 256, "llama-3.1-8b", out)
+    torch.cuda.synchronize()
+    o = out.cpu().numpy()
+    row = 0
+    for t in toks:
+        want = C.chunk_keys(t, 256, "llama-3.1-8b")
+        got = [o[32 * (row + i):32 * (row + i + 1)].tobytes() for i in range(len(want))]
+        assert got == want
+        row += len(want)
+
+
+# ---------------------------------------------------------------- K4 -------
+
+def test_synth_chunk_matches_oracle(tkv, C):
+    from paper_2510_09665_b200._lib import check, lib
+    rng = np.random.default_rng(3)
+    seed = C.model_seed("llama-3.1-8b")
+    for bpt, n, L in [(4096, 256, 3), (512, 100, 4), (64, 33, 2), (12, 17, 3), (8, 5, 1)]:
+        prompt = rand_tokens(rng, 300)
+        start = 16
+        dev_t = torch.from_numpy(prompt.view(np.int32)).cuda()
+        out = torch.zeros(L * n * bpt, dtype=torch.uint8, device="cuda")
+        check(lib().tkv_synth_chunk(dev_t.data_ptr(), seed, start, n, L, bpt, out.data_ptr(), None))
+        torch.cuda.synchronize()
+        want = C.synth_chunk(seed, prompt, start, n, L, bpt)
+        assert np.array_equal(out.cpu().numpy(), want), (bpt, n, L)
+
+
+# ------------------------------------------------------------- K1/K2 -------
+
+def _engine(tkv, L, bpt, pages, tag="k-test"):
+    from paper_2510_09665_b200.api import Engine
+    return Engine(num_layers=L, bpt=bpt, page_tokens=16, tag=tag, chunk_size=256, ram_slots=2,
+                  num_pages=pages)
+
+
+@pytest.mark.parametrize("bpt", [8, 64, 512, 4096])
+def test_scatter_gather_roundtrip(tkv, bpt):
+    """test_kv_core.cpp:136-156 — token counts {1,16,33,48,255} x 4 layers."""
+    from paper_2510_09665_b200._lib import check, u8p, u32p
+    e = _engine(tkv, 4, bpt, 64)
+    rng = np.random.default_rng(21)
+    for n in [1, 16, 33, 48, 255]:
+        need = (n + 15) // 16
+        ids = np.zeros(need, np.uint32)
+        check(e.L.tkv_pages_alloc(e.pages, 7, need, ids.ctypes.data_as(u32p)))
+        for layer in range(4):
+            buf = rng.integers(0, 256, size=n * bpt, dtype=np.uint8)
+            check(e.L.tkv_pages_scatter(e.pages, buf.ctypes.data_as(u8p), buf.size, ids.ctypes.data_as(u32p),
+                                        ids.size, layer, n))
+            back = np.zeros(n * bpt, np.uint8)
+            check(e.L.tkv_pages_gather(e.pages, ids.ctypes.data_as(u32p), ids.size, layer, n,
+                                       back.ctypes.data_as(u8p), back.size))
+            assert np.array_equal(back, buf)
+        e.L.tkv_pages_release(e.pages, 7)
+    e.close()
+
+
+def test_gather_checks(tkv):
+    """test_kv_core.cpp:158-189 — unpopulated / wrong layer / size mismatch."""
+    from paper_2510_09665_b200._lib import check, u8p, u32p
+    e = _engine(tkv, 4, 64, 8)
+    ids = np.zeros(2, np.uint32)
+    check(e.L.tkv_pages_alloc(e.pages, 1, 2, ids.ctypes.data_as(u32p)))
+    out = np.zeros(32 * 64, np.uint8)
+    rc = e.L.tkv_pages_gather(e.pages, ids.ctypes.data_as(u32p), 2, 0, 32, out.ctypes.data_as(u8p), out.size)
+    assert rc == 7  # unpopulated_page
+    buf = np.full(32 * 64, 0xAB, np.uint8)
+    check(e.L.tkv_pages_scatter(e.pages, buf.ctypes.data_as(u8p), buf.size, ids.ctypes.data_as(u32p), 2, 1, 32))
+    rc = e.L.tkv_pages_gather(e.pages, ids.ctypes.data_as(u32p), 2, 0, 32, out.ctypes.data_as(u8p), out.size)
+    assert rc == 7
+    check(e.L.tkv_pages_gather(e.pages, ids.ctypes.data_as(u32p), 2, 1, 32, out.ctypes.data_as(u8p), out.size))
+    small = np.zeros(3, np.uint8)
+    assert e.L.tkv_pages_scatter(e.pages, small.ctypes.data_as(u8p), 3, ids.ctypes.data_as(u32p), 2, 0, 16) == 6
+    big = np.zeros(64 * 64, np.uint8)
+    assert e.L.tkv_pages_scatter(e.pages, big.ctypes.data_as(u8p), big.size, ids.ctypes.data_as(u32p), 2, 0, 64) == 6
+    e.close()
+
+
+def _multi_layer_case(tkv, C, bpt, L, spans, seed, ppt=0):
+    """K1 then K2 over random page tables for several chunk descriptors and
+    all layers in ONE launch each, checked against the oracle's per-page
+    memcpy restatement (paged_store.cpp:123-175)."""
+    from paper_2510_09665_b200.api import XferDescC, plan_tiles
+    from paper_2510_09665_b200._lib import check, lib
+    rng = np.random.default_rng(seed)
+    pt = 16
+    page_bytes = pt * bpt
+    n_pages = sum(L * ((s[1] - s[0] + pt - 1) // pt) for s in spans) + 8
+    pool_h = rng.integers(0, 256, size=n_pages * page_bytes, dtype=np.uint8)
+    perm = rng.permutation(n_pages).astype(np.int32)
+    pool = torch.from_numpy(pool_h).cuda()
+    descs, tables, chunks, used = [], [], [], 0
+    for (start, end, rec) in spans:
+        npg = (end - start + pt - 1) // pt
+        first = start // pt
+        tab = np.full((L, first + npg), -1, np.int32)
+        for layer in range(L):
+            tab[layer, first:] = perm[used:used + npg]
+            used += npg
+        tables.append(torch.from_numpy(tab).cuda())
+        chunks.append(torch.zeros(L * rec * bpt, dtype=torch.uint8, device="cuda"))
+    for (start, end, rec), tab, ch in zip(spans, tables, chunks):
+        d = XferDescC()
+        d.chunk = ch.data_ptr()
+        d.layer_stride = rec * bpt
+        d.table_dev = tab.data_ptr()
+        d.table_stride = tab.shape[1]
+        d.first_page = start // pt
+        d.n_tokens = end - start
+        descs.append(d)
+    tb, ppt_used = plan_tiles(descs, pt, page_bytes, L, ppt)
+    arr = (XferDescC * len(descs))(*descs)
+    d_descs = torch.frombuffer(bytearray(bytes(arr)), dtype=torch.uint8).cuda()
+    d_tb = torch.from_numpy(tb.view(np.int32)).cuda()
+    layout = tkv.api.PagedLayoutC(base=pool.data_ptr(), layer_base_dev=None, page_stride=page_bytes,
+                                  plane_stride=0, token_stride=bpt, plane_bytes=bpt, n_planes=1,
+                                  page_tokens=pt, bpt=bpt, shared_table=0)
+    addr_or = 0
+    for d in descs:
+        addr_or |= d.chunk | d.layer_stride
+    check(lib().tkv_gather_layers(ct.byref(layout), d_descs.data_ptr(), d_tb.data_ptr(), len(descs),
+                                  int(tb[-1]), 0, L, ppt_used, addr_or, 0, None))
+    torch.cuda.synchronize()
+    for (start, end, rec), tab, ch in zip(spans, tables, chunks):
+        got = ch.cpu().numpy()
+        t = tab.cpu().numpy()
+        for layer in range(L):
+            want = C.gather_tokens(pool_h, page_bytes, t[layer, start // pt:], bpt, end - start)
+            seg = got[layer * rec * bpt: layer * rec * bpt + (end - start) * bpt]
+            assert np.array_equal(seg, want), (bpt, layer, start, end)
+    # K2: scatter fresh chunk bytes back, compare the whole pool with the oracle.
+    ref_pool = pool_h.copy()
+    for (start, end, rec), tab, ch in zip(spans, tables, chunks):
+        src = rng.integers(0, 256, size=L * rec * bpt, dtype=np.uint8)
+        ch.copy_(torch.from_numpy(src))
+        t = tab.cpu().numpy()
+        for layer in range(L):
+            C.scatter_tokens(ref_pool, page_bytes, t[layer, start // pt:], bpt, end - start,
+                             src[layer * rec * bpt: layer * rec * bpt + (end - start) * bpt])
+    check(lib().tkv_scatter_layers(ct.byref(layout), d_descs.data_ptr(), d_tb.data_ptr(), len(descs),
+                                   int(tb[-1]), 0, L, ppt_used, addr_or, 0, None))
+    torch.cuda.synchronize()
+    assert np.array_equal(pool.cpu().numpy(), ref_pool)
+
+
+@pytest.mark.parametrize("bpt", [8, 12, 64, 512, 4096])
+def test_multilayer_gather_scatter(tkv, C, bpt):
+    spans = [(0, 256, 256), (256, 512, 256), (512, 600, 88), (768, 1000, 256)]  # last clips a record
+    _multi_layer_case(tkv, C, bpt, 5, spans, seed=bpt)
+
+
+def test_multilayer_small_tiles(tkv, C):
+    _multi_layer_case(tkv, C, 512, 3, [(0, 256, 256), (256, 300, 256)], seed=5, ppt=3)
+
+
+def test_vllm_two_plane_layout(tkv):
+    """K/V planes per layer with a shared block table (vLLM layout): chunk row
+    = K(h*D) | V(h*D). Checked against a numpy restatement."""
+    from paper_2510_09665_b200.api import XferDescC, plan_tiles
+    from paper_2510_09665_b200._lib import check, lib
+    rng = np.random.default_rng(9)
+    L, blocks, pt, hd = 3, 20, 16, 256  # plane bytes per token
+    layers = [torch.from_numpy(rng.integers(0, 256, size=2 * blocks * pt * hd, dtype=np.uint8)).cuda()
+              for _ in range(L)]
+    bases = torch.tensor([t.data_ptr() for t in layers], dtype=torch.int64).cuda()
+    table = rng.permutation(blocks).astype(np.int32)
+    tab = torch.from_numpy(table).cuda()
+    n_tok = 70
+    ch = torch.zeros(L * n_tok * 2 * hd, dtype=torch.uint8, device="cuda")
+    d = XferDescC(chunk=ch.data_ptr(), layer_stride=n_tok * 2 * hd, table_dev=tab.data_ptr(),
+                  table_stride=blocks, first_page=0, n_tokens=n_tok)
+    tb, ppt = plan_tiles([d], pt, pt * hd, L)
+    d_descs = torch.frombuffer(bytearray(bytes(d)), dtype=torch.uint8).cuda()
+    d_tb = torch.from_numpy(tb.view(np.int32)).cuda()
+    layout = tkv.api.PagedLayoutC(base=0, layer_base_dev=bases.data_ptr(), page_stride=pt * hd,
+                                  plane_stride=blocks * pt * hd, token_stride=hd, plane_bytes=hd, n_planes=2,
+                                  page_tokens=pt, bpt=2 * hd, shared_table=1)
+    check(lib().tkv_gather_layers(ct.byref(layout), d_descs.data_ptr(), d_tb.data_ptr(), 1, int(tb[-1]), 0, L,
+                                  ppt, d.chunk | d.layer_stride, 0, None))
+    torch.cuda.synchronize()
+    got = ch.cpu().numpy().reshape(L, n_tok, 2, hd)
+    for layer in range(L):
+        kv = layers[layer].cpu().numpy().reshape(2, blocks, pt, hd)
+        for t in range(n_tok):
+            b = table[t // pt]
+            assert np.array_equal(got[layer, t, 0], kv[0, b, t % pt])
+            assert np.array_equal(got[layer, t, 1], kv[1, b, t % pt])
