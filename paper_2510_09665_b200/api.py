@@ -16,8 +16,8 @@ import ctypes as ct
 import numpy as np
 import torch
 
-from ._lib import (ChainDescC, ConnectorConfigC, ModelSpecC, PagedLayoutC, XferDescC, check, lib,
-                   u8p, u32p, u64p)
+from ._lib import (ChainDescC, ConnectorConfigC, ModelSpecC, PagedLayoutC, PdRecordC, XferDescC, check,
+                   lib, u8p, u32p, u64p)
 
 __all__ = ["Engine", "chunk_keys", "keychain_next", "PagedLayoutC", "XferDescC", "ChainDescC",
            "plan_tiles", "hash_chains", "ErrcOK"]
@@ -78,7 +78,8 @@ class Engine:
     def __init__(self, num_layers: int, bpt: int, page_tokens: int, tag: str, chunk_size: int,
                  ram_slots: int, num_pages: int, layerwise: bool = True, staging_budget: int = 64 << 20,
                  io_threads: int = 2, store_io_threads: int = 4, pin_stores: bool = False,
-                 staging_depth: int = 2, load_zero_copy: bool = False, store_ctas: int = 0,
+                 staging_depth: int = 2, load_zero_copy: bool = False, store_zero_copy: bool = False,
+                 store_ctas: int = 0,
                  load_ctas: int = 0, device: int = 0, stream: torch.cuda.Stream | None = None):
         del io_threads, store_io_threads  # host thread pools do not exist on this path
         self.L = lib()
@@ -102,6 +103,7 @@ class Engine:
         cfg.staging_budget_bytes = staging_budget
         cfg.staging_depth = staging_depth
         cfg.load_zero_copy = int(load_zero_copy)
+        cfg.store_zero_copy = int(store_zero_copy)
         if store_ctas:
             cfg.store_ctas = store_ctas
         cfg.load_ctas = load_ctas
@@ -348,6 +350,62 @@ class Engine:
         stride = ct.c_uint32(0)
         check(self.L.tkv_pages_device_table(self.pages, qid, self.stream_handle, ct.byref(ptr), ct.byref(stride)))
         return ptr.value, stride.value
+
+
+class PdStaging:
+    """Decoder landing area (pd_staging.hpp contract) over the C-ABI."""
+
+    def __init__(self):
+        self.L = lib()
+        self.h = ct.c_void_p()
+        check(self.L.tkv_pd_staging_create(ct.byref(self.h)))
+
+    def close(self):
+        if self.h:
+            self.L.tkv_pd_staging_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def register_query(self, qid: int) -> int:
+        return self.L.tkv_pd_register(self.h, qid)
+
+    def push(self, qid: int, ordinal: int, last: bool, rec: PdRecordC | None = None) -> int:
+        rec = rec if rec is not None else PdRecordC()
+        return self.L.tkv_pd_push(self.h, qid, ordinal, int(last), ct.byref(rec))
+
+    def await_(self, qid: int):
+        cap = 1 << 14
+        out = (PdRecordC * cap)()
+        n = ct.c_size_t(0)
+        rc = self.L.tkv_pd_await(self.h, qid, out, cap, ct.byref(n))
+        return rc, [out[i] for i in range(n.value)] if rc == 0 else []
+
+    def cancel(self, qid: int) -> int:
+        return self.L.tkv_pd_cancel(self.h, qid)
+
+    def registered(self) -> int:
+        return int(self.L.tkv_pd_registered(self.h))
+
+
+def pd_send(engine: "Engine", qid: int, n_tokens: int, landing_ptr: int, chunk_stride: int):
+    """Prefiller: gather the query's chunks (all layers) into landing memory."""
+    cap = 1 << 14
+    out = (PdRecordC * cap)()
+    n = ct.c_size_t(0)
+    check(lib().tkv_pd_send(engine.pages, qid, n_tokens, engine.chunk_size, landing_ptr, chunk_stride,
+                            engine.stream_handle, out, cap, ct.byref(n)))
+    return [out[i] for i in range(n.value)]
+
+
+def pd_land(engine: "Engine", qid: int, records) -> None:
+    """Decoder: scatter landed chunks into the query's pages (one launch)."""
+    arr = (PdRecordC * max(1, len(records)))(*records)
+    check(lib().tkv_pd_land(engine.pages, qid, arr, len(records), engine.stream_handle))
 
 
 def _model_seed(tag: str) -> int:

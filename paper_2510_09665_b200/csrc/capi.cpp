@@ -10,6 +10,7 @@
 #include "connector.hpp"
 #include "kernels.hpp"
 #include "paged_store.hpp"
+#include "pd.hpp"
 #include "store.hpp"
 #include "tokens.hpp"
 
@@ -31,6 +32,12 @@ struct tkv_connector {
 struct tkv_meta {
     ConnectorMetadata m;
 };
+struct tkv_pd_staging {
+    PdStaging s;
+};
+
+static_assert(sizeof(tkv_pd_record) == sizeof(PdRecord));
+static_assert(sizeof(cudaIpcMemHandle_t) == 64);
 
 namespace {
 
@@ -111,6 +118,7 @@ extern "C" {
 const char* tkv_last_error(void) { return g_err.c_str(); }
 const char* tkv_errc_name(int code) { return errc_name(Errc(code)); }
 const char* tkv_build_info(void) { return "tierkv_b200 sm_100a " __DATE__ " " __TIME__; }
+uint64_t tkv_launch_count(void) { return launch_count(); }
 
 // ---- kernel level -----------------------------------------------------------
 
@@ -409,6 +417,7 @@ void tkv_connector_config_default(tkv_connector_config* cfg) {
     cfg->staging_budget_bytes = d.staging_budget_bytes;
     cfg->staging_depth = d.staging_depth;
     cfg->load_zero_copy = d.load_path == LoadPath::zero_copy;
+    cfg->store_zero_copy = d.store_path == StorePath::zero_copy;
     cfg->store_ctas = d.store_ctas;
     cfg->load_ctas = d.load_ctas;
     cfg->engine_stream = d.engine_stream;
@@ -424,6 +433,7 @@ int tkv_connector_create(tkv_store* s, tkv_pages* p, const tkv_connector_config*
             c.staging_budget_bytes = cfg->staging_budget_bytes;
             c.staging_depth = cfg->staging_depth;
             c.load_path = cfg->load_zero_copy ? LoadPath::zero_copy : LoadPath::copy_engine;
+            c.store_path = cfg->store_zero_copy ? StorePath::zero_copy : StorePath::copy_engine;
             c.store_ctas = cfg->store_ctas > 0 ? cfg->store_ctas : c.store_ctas;
             c.load_ctas = cfg->load_ctas;
             c.engine_stream = cudaStream_t(cfg->engine_stream);
@@ -499,6 +509,71 @@ int tkv_connector_finish_query(tkv_connector* c, uint64_t q, uint8_t* out, size_
 }
 size_t tkv_connector_staging_peak(tkv_connector* c) { return c->c->staging_peak_bytes(); }
 uint64_t tkv_connector_hash_launches(tkv_connector* c) { return c->c->hasher().launches(); }
+
+// ---- PD -----------------------------------------------------------------------
+
+int tkv_pd_staging_create(tkv_pd_staging** out) {
+    return guard([&] {
+        *out = new tkv_pd_staging;
+        return 0;
+    });
+}
+void tkv_pd_staging_destroy(tkv_pd_staging* s) { delete s; }
+int tkv_pd_register(tkv_pd_staging* s, uint64_t q) { return st(s->s.register_query(q)); }
+int tkv_pd_push(tkv_pd_staging* s, uint64_t q, uint32_t ordinal, int last, const tkv_pd_record* rec) {
+    PdRecord r{rec->addr, rec->bytes, rec->token_count, rec->first_token};
+    return st(s->s.push(q, ordinal, last != 0, r));
+}
+int tkv_pd_await(tkv_pd_staging* s, uint64_t q, tkv_pd_record* out, size_t cap, size_t* n) {
+    return guard([&] {
+        auto r = s->s.await(q);
+        if (!r.ok()) return st(r.status());
+        *n = r.value().size();
+        for (size_t i = 0; i < r.value().size() && i < cap; ++i) {
+            const auto& x = r.value()[i];
+            out[i] = tkv_pd_record{x.addr, x.bytes, x.token_count, x.first_token};
+        }
+        return 0;
+    });
+}
+int tkv_pd_cancel(tkv_pd_staging* s, uint64_t q) { return st(s->s.cancel(q)); }
+size_t tkv_pd_registered(tkv_pd_staging* s) { return s->s.registered(); }
+int tkv_pd_send(tkv_pages* src, uint64_t q, size_t n_tokens, size_t chunk_size, uint64_t landing,
+                uint64_t stride, void* stream, tkv_pd_record* out, size_t cap, size_t* n) {
+    return guard([&] {
+        auto r = pd_send_chunks(*src->p, q, n_tokens, chunk_size, landing, stride, cudaStream_t(stream));
+        if (!r.ok()) return st(r.status());
+        *n = r.value().size();
+        for (size_t i = 0; i < r.value().size() && i < cap; ++i) {
+            const auto& x = r.value()[i];
+            out[i] = tkv_pd_record{x.addr, x.bytes, x.token_count, x.first_token};
+        }
+        return 0;
+    });
+}
+int tkv_pd_land(tkv_pages* dst, uint64_t q, const tkv_pd_record* recs, size_t n, void* stream) {
+    return guard([&] {
+        std::vector<PdRecord> v(n);
+        for (size_t i = 0; i < n; ++i)
+            v[i] = PdRecord{recs[i].addr, recs[i].bytes, recs[i].token_count, recs[i].first_token};
+        return st(pd_land_chunks(*dst->p, q, v, cudaStream_t(stream)));
+    });
+}
+int tkv_enable_peer_access(int device, int peer) {
+    return guard([&] { return st(enable_peer_access(device, peer)); });
+}
+int tkv_ipc_get_handle(void* ptr, uint8_t* handle64) {
+    cudaIpcMemHandle_t h;
+    int rc = cuda(cudaIpcGetMemHandle(&h, ptr));
+    if (rc == 0) std::memcpy(handle64, &h, sizeof h);
+    return rc;
+}
+int tkv_ipc_open_handle(const uint8_t* handle64, void** out) {
+    cudaIpcMemHandle_t h;
+    std::memcpy(&h, handle64, sizeof h);
+    return cuda(cudaIpcOpenMemHandle(out, h, cudaIpcMemLazyEnablePeerAccess));
+}
+int tkv_ipc_close(void* ptr) { return cuda(cudaIpcCloseMemHandle(ptr)); }
 
 void tkv_meta_destroy(tkv_meta* m) { delete m; }
 int tkv_meta_layerwise(tkv_meta* m) { return m->m.mode() == TransferMode::layerwise; }

@@ -1,8 +1,17 @@
 #include "common.hpp"
 
+#include <atomic>
 #include <utility>
 
+#include "kernels.hpp"
+
 namespace tkv {
+
+namespace {
+std::atomic<uint64_t> g_launches{0};
+}
+void note_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+uint64_t launch_count() { return g_launches.load(std::memory_order_relaxed); }
 
 const char* errc_name(Errc e) {
     switch (e) {

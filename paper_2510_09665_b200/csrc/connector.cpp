@@ -1,77 +1,13 @@
 #include "connector.hpp"
 
+#include "copy_plan.hpp"
+
 #include <algorithm>
 #include <cstring>
 
 namespace tkv {
 
 namespace {
-
-constexpr uint32_t pages_per_tile(size_t page_bytes) {
-    size_t p = 65536 / (page_bytes ? page_bytes : 1);
-    return uint32_t(p < 1 ? 1 : (p > 64 ? 64 : p));
-}
-
-std::vector<uint32_t> tile_prefix(const std::vector<XferDesc>& d, uint32_t page_tokens,
-                                  uint32_t ppt, uint32_t n_layers) {
-    std::vector<uint32_t> tb(d.size() + 1, 0);
-    for (size_t i = 0; i < d.size(); ++i)
-        tb[i + 1] = tb[i] + tiles_for(d[i].n_tokens, page_tokens, ppt, n_layers);
-    return tb;
-}
-
-// Host-built copy plan uploaded once per batch: descriptor variants (one per
-// staging ring slot, or one for direct slot access) and tile prefixes for
-// one-layer and all-layer launches.
-struct DevicePlan {
-    size_t n_desc = 0;
-    size_t variants = 0;
-    uint32_t tiles_1 = 0, tiles_all = 0;
-    uint64_t addr_or = 0;
-    PinnedBuffer host;
-    DeviceBuffer dev;
-    size_t off_tb1 = 0, off_tball = 0;
-
-    void build(const std::vector<std::vector<XferDesc>>& vars, uint32_t page_tokens, uint32_t ppt,
-               uint32_t n_layers, cudaStream_t s) {
-        variants = vars.size();
-        n_desc = vars.empty() ? 0 : vars[0].size();
-        if (n_desc == 0) return;
-        auto tb1 = tile_prefix(vars[0], page_tokens, ppt, 1);
-        auto tball = tile_prefix(vars[0], page_tokens, ppt, n_layers);
-        tiles_1 = tb1.back();
-        tiles_all = tball.back();
-        const size_t desc_bytes = variants * n_desc * sizeof(XferDesc);
-        off_tb1 = (desc_bytes + 15) & ~size_t(15);
-        off_tball = off_tb1 + ((tb1.size() * 4 + 15) & ~size_t(15));
-        const size_t total = off_tball + tball.size() * 4;
-        host.reserve(total);
-        dev.reserve(total);
-        addr_or = 0;
-        for (size_t v = 0; v < variants; ++v) {
-            std::memcpy(host.host + v * n_desc * sizeof(XferDesc), vars[v].data(),
-                        n_desc * sizeof(XferDesc));
-            for (const auto& d : vars[v]) addr_or |= d.chunk | d.layer_stride;
-        }
-        std::memcpy(host.host + off_tb1, tb1.data(), tb1.size() * 4);
-        std::memcpy(host.host + off_tball, tball.data(), tball.size() * 4);
-        TKV_CUDA(cudaMemcpyAsync(dev.ptr, host.host, total, cudaMemcpyHostToDevice, s));
-    }
-
-    PagedCopyPlan plan(size_t variant, uint32_t layer_begin, uint32_t n_layers, uint32_t ppt) const {
-        PagedCopyPlan p;
-        p.descs = reinterpret_cast<const XferDesc*>(dev.ptr) + variant * n_desc;
-        const bool one = n_layers == 1;
-        p.tile_base = reinterpret_cast<const uint32_t*>(dev.ptr + (one ? off_tb1 : off_tball));
-        p.n_desc = uint32_t(n_desc);
-        p.total_tiles = one ? tiles_1 : tiles_all;
-        p.layer_begin = layer_begin;
-        p.n_layers = n_layers;
-        p.pages_per_tile = ppt;
-        p.addr_or = addr_or;
-        return p;
-    }
-};
 
 struct ReleaseCtx {
     TieredStore* store;
@@ -118,6 +54,9 @@ struct StoreItem {
     size_t desc;
     Status status;  // reservation outcome
     SlotWrite w;
+    size_t staging_off = 0;  // copy-engine path: offset in one staging layer
+    size_t rows = 0;         // span length
+    size_t record_tokens = 0;
 };
 
 struct BatchState {
@@ -141,11 +80,14 @@ struct BatchState {
     std::vector<bool> store_done;
     bool stores_sealed = false, stores_waited = false;
     std::vector<StoreItem> stores;
-    std::vector<Event> compute_done;
+    std::vector<Event> compute_done, gathered, d2h_done;
     Event store_complete;
     DevicePlan store_plan;
     std::atomic<bool> committed{false};
     bool any_store_writes = false;
+    bool store_ce = false;         // copy-engine store path for this batch
+    uint32_t store_depth = 1;
+    size_t store_layer_bytes = 0;  // one staging layer
 
     ~BatchState() {
         // Device buffers above may still feed in-flight work: drain first.
@@ -153,6 +95,7 @@ struct BatchState {
             if (loads_started && !load_done.empty()) load_done.back().sync();
             if (any_store_writes) {
                 TKV_CUDA(cudaStreamSynchronize(conn->store_stream_));
+                TKV_CUDA(cudaStreamSynchronize(conn->d2h_stream_));
                 if (!committed.load()) {
                     for (auto& s : stores)
                         if (s.w.kind == SlotWrite::Kind::write)
@@ -197,6 +140,7 @@ Connector::Connector(TieredStore& store, PagedKVStore& pages, Config cfg)
     h2d_stream_ = Stream::create();
     load_stream_ = Stream::create();
     store_stream_ = Stream::create();
+    d2h_stream_ = Stream::create();
 }
 
 Connector::Connector(TieredStore& store, PagedKVStore& pages) : Connector(store, pages, Config{}) {}
@@ -206,6 +150,7 @@ Connector::~Connector() {
         TKV_CUDA(cudaStreamSynchronize(h2d_stream_));
         TKV_CUDA(cudaStreamSynchronize(load_stream_));
         TKV_CUDA(cudaStreamSynchronize(store_stream_));
+        TKV_CUDA(cudaStreamSynchronize(d2h_stream_));
     } catch (...) {
     }
 }
@@ -366,7 +311,11 @@ Status Connector::enqueue_loads(BatchState& b) {
     std::vector<std::vector<XferDesc>> vars(zero_copy ? 1 : depth);
     if (!zero_copy) {
         b.ring_slot_bytes = layer_bytes;
-        staging_.reserve(size_t(depth) * layer_bytes);
+        if (size_t(depth) * layer_bytes > staging_.bytes) {
+            TKV_CUDA(cudaStreamSynchronize(h2d_stream_));  // previous batch may use the ring
+            TKV_CUDA(cudaStreamSynchronize(load_stream_));
+            staging_.reserve(size_t(depth) * layer_bytes);
+        }
         staging_peak_ = std::max(staging_peak_, size_t(depth) * layer_bytes);
     }
     for (size_t v = 0; v < vars.size(); ++v) {
@@ -516,9 +465,49 @@ Status Connector::reserve_stores(BatchState& b) {
         }
     }
     b.any_store_writes = !descs.empty();
-    b.store_plan.build({descs}, pt, ppt, b.num_layers, store_stream_);
     b.compute_done.resize(b.num_layers);
     b.stores_reserved = true;
+    // Copy-engine path (layerwise only): K1 writes one layer of every chunk
+    // into an HBM staging ring slot; the CE then copies each chunk-layer
+    // slice into its pinned slot at offset layer*T*bpt (store.cpp:343-345).
+    b.store_ce = cfg_.store_path == StorePath::copy_engine &&
+                 b.mode == TransferMode::layerwise && b.any_store_writes;
+    if (!b.store_ce) {
+        b.store_plan.build({descs}, pt, ppt, b.num_layers, store_stream_);
+        return Status::success();
+    }
+    size_t off = 0;
+    for (auto& s : b.stores) {
+        if (s.w.kind != SlotWrite::Kind::write) continue;
+        const auto& d = b.plans[s.plan].store_plan[s.desc];
+        s.staging_off = off;
+        s.rows = d.span.length();
+        s.record_tokens = d.record_tokens;
+        off += ((s.rows * bpt + 255) / 256) * 256;
+    }
+    b.store_layer_bytes = off;
+    b.store_depth = std::min<uint32_t>(std::max<uint32_t>(cfg_.staging_depth, 1), b.num_layers);
+    const size_t need = size_t(b.store_depth) * off;
+    if (need > store_staging_.bytes) {
+        TKV_CUDA(cudaStreamSynchronize(store_stream_));  // previous batch may use the ring
+        TKV_CUDA(cudaStreamSynchronize(d2h_stream_));
+        store_staging_.reserve(need);
+    }
+    staging_peak_ = std::max(staging_peak_, need);
+    std::vector<std::vector<XferDesc>> vars(b.store_depth, descs);
+    for (uint32_t r = 0; r < b.store_depth; ++r) {
+        size_t k = 0;
+        for (const auto& s : b.stores) {
+            if (s.w.kind != SlotWrite::Kind::write) continue;
+            vars[r][k].chunk = reinterpret_cast<uint64_t>(store_staging_.ptr + r * off + s.staging_off);
+            vars[r][k].layer_stride = 0;
+            ++k;
+        }
+    }
+    b.store_plan.build(vars, pt, ppt, b.num_layers, store_stream_);
+    b.gathered.resize(b.num_layers);
+    b.d2h_done.resize(b.num_layers);
+    if (store_ring_used_) store_ring_free_.wait_on(store_stream_);
     return Status::success();
 }
 
@@ -540,8 +529,34 @@ Status Connector::store_layers(BatchState& b, uint32_t first, uint32_t last) {
     // K1 for these layers, ordered after the engine's compute of them.
     b.compute_done[first].record(cfg_.engine_stream);
     b.compute_done[first].wait_on(store_stream_);
-    TKV_CUDA(launch_paged_copy(layout, b.store_plan.plan(0, first, last - first, ppt),
-                               CopyDir::gather, cfg_.store_ctas, store_stream_));
+    if (!b.store_ce) {
+        TKV_CUDA(launch_paged_copy(layout, b.store_plan.plan(0, first, last - first, ppt),
+                                   CopyDir::gather, cfg_.store_ctas, store_stream_));
+        return Status::success();
+    }
+    const size_t bpt = model.bytes_per_token_per_layer;
+    for (uint32_t l = first; l < last; ++l) {
+        const uint32_t r = l % b.store_depth;
+        if (l >= b.store_depth) b.d2h_done[l - b.store_depth].wait_on(store_stream_);
+        TKV_CUDA(launch_paged_copy(layout, b.store_plan.plan(r, l, 1, ppt), CopyDir::gather,
+                                   cfg_.load_ctas, store_stream_));
+        b.gathered[l].record(store_stream_);
+        b.gathered[l].wait_on(d2h_stream_);
+        std::vector<void*> dst, src;
+        std::vector<size_t> sizes;
+        for (const auto& s : b.stores) {
+            if (s.w.kind != SlotWrite::Kind::write) continue;
+            dst.push_back(s.w.host + size_t(l) * s.record_tokens * bpt);
+            src.push_back(store_staging_.ptr + size_t(r) * b.store_layer_bytes + s.staging_off);
+            sizes.push_back(s.rows * bpt);
+        }
+        cudaMemcpyAttributes attr{};
+        attr.srcAccessOrder = cudaMemcpySrcAccessOrderStream;
+        size_t attr_idx = 0, fail_idx = 0;
+        TKV_CUDA(cudaMemcpyBatchAsync(dst.data(), src.data(), sizes.data(), dst.size(), &attr,
+                                      &attr_idx, 1, &fail_idx, d2h_stream_));
+        b.d2h_done[l].record(d2h_stream_);
+    }
     return Status::success();
 }
 
@@ -575,13 +590,18 @@ Status Connector::start_store_kv(ConnectorMetadata& meta) {
         }
         if (last == b.num_layers && !b.stores_sealed) {
             b.stores_sealed = true;
-            b.store_complete.record(store_stream_);
+            cudaStream_t done_stream = b.store_ce ? d2h_stream_.s : store_stream_.s;
+            b.store_complete.record(done_stream);
+            if (b.store_ce) {
+                store_ring_free_.record(d2h_stream_);
+                store_ring_used_ = true;
+            }
             if (b.any_store_writes) {
                 auto* ctx = new CommitCtx{&store_, {}, &b.committed};
                 for (const auto& s : b.stores)
                     if (s.w.kind == SlotWrite::Kind::write)
                         ctx->digests.push_back(b.plans[s.plan].store_plan[s.desc].key.digest);
-                TKV_CUDA(cudaLaunchHostFunc(store_stream_, commit_cb, ctx));
+                TKV_CUDA(cudaLaunchHostFunc(done_stream, commit_cb, ctx));
             } else {
                 b.committed.store(true);
             }

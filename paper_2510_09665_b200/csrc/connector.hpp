@@ -36,6 +36,9 @@ namespace tkv {
 
 enum class TransferMode : uint8_t { layerwise, blocking };
 enum class LoadPath : uint8_t { copy_engine, zero_copy };
+// copy_engine: K1 into an HBM staging ring, then one batched CE D2H per layer.
+// zero_copy:   K1 writes straight into the pinned slots over PCIe.
+enum class StorePath : uint8_t { copy_engine, zero_copy };
 
 struct ChunkDescriptor {
     ChunkKey key;
@@ -87,6 +90,7 @@ public:
         size_t staging_budget_bytes = 64ull << 20;
         uint32_t staging_depth = 2;      // layers of device staging in flight
         LoadPath load_path = LoadPath::copy_engine;
+        StorePath store_path = StorePath::copy_engine;
         int store_ctas = 64;             // zero-copy K1 grid (PCIe-bound)
         int load_ctas = 0;               // K2 grid (0 = 2 x SMs)
         cudaStream_t engine_stream = nullptr;
@@ -151,10 +155,10 @@ private:
     PagedKVStore& pages_;
     Config cfg_;
     KeyHasher hasher_;
-    Stream h2d_stream_, load_stream_, store_stream_;
-    DeviceBuffer staging_;
-    Event ring_free_;
-    bool ring_used_ = false;
+    Stream h2d_stream_, load_stream_, store_stream_, d2h_stream_;
+    DeviceBuffer staging_, store_staging_;
+    Event ring_free_, store_ring_free_;
+    bool ring_used_ = false, store_ring_used_ = false;
     size_t staging_peak_ = 0;
     std::mutex io_mu_;  // one batch enqueues at a time
 

@@ -1,0 +1,78 @@
+// Host-built K1/K2 launch plans shared by the connector and the PD path:
+// descriptor variants (one per staging ring slot, or one for direct slot /
+// peer access) and tile prefixes for one-layer and all-layer launches,
+// uploaded once per batch with a single H2D copy.
+#pragma once
+
+#include <cstring>
+#include <vector>
+
+#include "common.hpp"
+#include "kernels.hpp"
+
+namespace tkv {
+
+inline uint32_t pages_per_tile(size_t page_bytes) {
+    size_t p = 65536 / (page_bytes ? page_bytes : 1);
+    return uint32_t(p < 1 ? 1 : (p > 64 ? 64 : p));
+}
+
+inline std::vector<uint32_t> tile_prefix(const std::vector<XferDesc>& d, uint32_t page_tokens,
+                                         uint32_t ppt, uint32_t n_layers) {
+    std::vector<uint32_t> tb(d.size() + 1, 0);
+    for (size_t i = 0; i < d.size(); ++i)
+        tb[i + 1] = tb[i] + tiles_for(d[i].n_tokens, page_tokens, ppt, n_layers);
+    return tb;
+}
+
+struct DevicePlan {
+    size_t n_desc = 0;
+    size_t variants = 0;
+    uint32_t tiles_1 = 0, tiles_all = 0;
+    uint64_t addr_or = 0;
+    PinnedBuffer host;
+    DeviceBuffer dev;
+    size_t off_tb1 = 0, off_tball = 0;
+
+    void build(const std::vector<std::vector<XferDesc>>& vars, uint32_t page_tokens, uint32_t ppt,
+               uint32_t n_layers, cudaStream_t s) {
+        variants = vars.size();
+        n_desc = vars.empty() ? 0 : vars[0].size();
+        if (n_desc == 0) return;
+        auto tb1 = tile_prefix(vars[0], page_tokens, ppt, 1);
+        auto tball = tile_prefix(vars[0], page_tokens, ppt, n_layers);
+        tiles_1 = tb1.back();
+        tiles_all = tball.back();
+        const size_t desc_bytes = variants * n_desc * sizeof(XferDesc);
+        off_tb1 = (desc_bytes + 15) & ~size_t(15);
+        off_tball = off_tb1 + ((tb1.size() * 4 + 15) & ~size_t(15));
+        const size_t total = off_tball + tball.size() * 4;
+        host.reserve(total);
+        dev.reserve(total);
+        addr_or = 0;
+        for (size_t v = 0; v < variants; ++v) {
+            std::memcpy(host.host + v * n_desc * sizeof(XferDesc), vars[v].data(),
+                        n_desc * sizeof(XferDesc));
+            for (const auto& d : vars[v]) addr_or |= d.chunk | d.layer_stride;
+        }
+        std::memcpy(host.host + off_tb1, tb1.data(), tb1.size() * 4);
+        std::memcpy(host.host + off_tball, tball.data(), tball.size() * 4);
+        TKV_CUDA(cudaMemcpyAsync(dev.ptr, host.host, total, cudaMemcpyHostToDevice, s));
+    }
+
+    PagedCopyPlan plan(size_t variant, uint32_t layer_begin, uint32_t n_layers, uint32_t ppt) const {
+        PagedCopyPlan p;
+        p.descs = reinterpret_cast<const XferDesc*>(dev.ptr) + variant * n_desc;
+        const bool one = n_layers == 1;
+        p.tile_base = reinterpret_cast<const uint32_t*>(dev.ptr + (one ? off_tb1 : off_tball));
+        p.n_desc = uint32_t(n_desc);
+        p.total_tiles = one ? tiles_1 : tiles_all;
+        p.layer_begin = layer_begin;
+        p.n_layers = n_layers;
+        p.pages_per_tile = ppt;
+        p.addr_or = addr_or;
+        return p;
+    }
+};
+
+}  // namespace tkv

@@ -8,6 +8,10 @@
 
 namespace tkv {
 
+// Count of kernel launches issued by this library (bench.py's gpu_launches).
+void note_launch();
+uint64_t launch_count();
+
 // ---------------------------------------------------------------------------
 // K1/K2: multi-layer paged KV gather (store) and scatter (retrieve).
 //

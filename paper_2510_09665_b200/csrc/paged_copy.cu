@@ -169,6 +169,7 @@ template <int W, bool CONTIG>
 cudaError_t launch_w(const PagedLayout& L, const PagedCopyPlan& P, CopyDir dir, int ctas,
                      cudaStream_t s) {
     constexpr int U = W >= 8 ? 4 : 8;
+    note_launch();
     paged_copy_kernel<W, CONTIG, U><<<ctas, kThreads, 0, s>>>(L, P, int(dir));
     return cudaGetLastError();
 }

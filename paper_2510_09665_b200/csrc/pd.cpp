@@ -1,0 +1,166 @@
+#include "pd.hpp"
+
+#include <algorithm>
+
+#include "copy_plan.hpp"
+
+namespace tkv {
+
+// --- control plane: src/pd_staging.cpp:5-63 semantics --------------------
+
+Status PdStaging::register_query(QueryId id) {
+    std::lock_guard lock(mu_);
+    auto [it, inserted] = queries_.try_emplace(id);
+    if (!inserted) return Status{Errc::duplicate_key, "query already registered"};
+    return Status::success();
+}
+
+Status PdStaging::push(QueryId id, uint32_t ordinal, bool last, const PdRecord& rec) {
+    std::lock_guard lock(mu_);
+    auto it = queries_.find(id);
+    if (it == queries_.end())
+        return Status{Errc::unknown_query, "query " + std::to_string(id) + " not registered"};
+    Query& q = it->second;
+    if (q.last_seen && ordinal > q.last_ordinal)
+        return Status{Errc::protocol_error, "ordinal beyond the final chunk"};
+    if (last && !q.slots.empty() && q.slots.rbegin()->first > ordinal)
+        return Status{Errc::protocol_error, "final ordinal below an already filled slot"};
+    if (last) {
+        q.last_seen = true;
+        q.last_ordinal = ordinal;
+    }
+    q.slots.try_emplace(ordinal, rec);  // filled exactly once; a retransmit acks
+    if (complete(q)) cv_.notify_all();
+    return Status::success();
+}
+
+Result<std::vector<PdRecord>> PdStaging::await(QueryId id) {
+    std::unique_lock lock(mu_);
+    auto it = queries_.find(id);
+    if (it == queries_.end())
+        return Status{Errc::unknown_query, "query " + std::to_string(id) + " not registered"};
+    cv_.wait(lock, [&] { return complete(it->second) || it->second.cancelled; });
+    if (it->second.cancelled) {
+        queries_.erase(it);
+        return Status{Errc::io_error, "query cancelled"};
+    }
+    std::vector<PdRecord> out;
+    out.reserve(it->second.slots.size());
+    for (auto& [ordinal, rec] : it->second.slots) out.push_back(rec);
+    queries_.erase(it);
+    return out;
+}
+
+Status PdStaging::cancel(QueryId id) {
+    std::lock_guard lock(mu_);
+    auto it = queries_.find(id);
+    if (it == queries_.end()) return Status{Errc::unknown_query, "not registered"};
+    it->second.cancelled = true;
+    cv_.notify_all();
+    return Status::success();
+}
+
+size_t PdStaging::registered() const {
+    std::lock_guard lock(mu_);
+    return queries_.size();
+}
+
+// --- data plane ------------------------------------------------------------
+
+Result<std::vector<PdRecord>> pd_send_chunks(PagedKVStore& pages, QueryId query, size_t n_tokens,
+                                             size_t chunk_size, uint64_t landing,
+                                             uint64_t chunk_stride, cudaStream_t stream, int ctas) {
+    const auto& spec = pages.spec();
+    const uint32_t pt = spec.page_tokens;
+    const size_t bpt = spec.bytes_per_token_per_layer;
+    if (chunk_size == 0 || chunk_size % pt) return Status{Errc::invalid_argument, "chunk size"};
+    std::vector<PdRecord> recs;
+    std::vector<XferDesc> descs;
+    auto t = pages.device_table(query, stream);
+    if (!t.ok()) return t.status();
+    for (size_t start = 0, i = 0; start < n_tokens; start += chunk_size, ++i) {
+        const size_t n = std::min(chunk_size, n_tokens - start);
+        for (uint32_t l = 0; l < spec.num_layers; ++l) {
+            Status st = pages.check_readable_span(query, l, start / pt, n);
+            if (!st.ok()) return st;
+        }
+        const uint64_t bytes = uint64_t(spec.num_layers) * n * bpt;
+        if (bytes > chunk_stride) return Status{Errc::size_mismatch, "landing slot too small"};
+        PdRecord r{landing + i * chunk_stride, bytes, uint32_t(n), uint32_t(start)};
+        recs.push_back(r);
+        XferDesc x;
+        x.chunk = r.addr;
+        x.layer_stride = uint64_t(n) * bpt;
+        x.table = t.value().ptr;
+        x.table_stride = t.value().stride;
+        x.first_page = uint32_t(start / pt);
+        x.n_tokens = uint32_t(n);
+        descs.push_back(x);
+    }
+    if (descs.empty()) return recs;
+    const uint32_t ppt = pages_per_tile(pages.page_bytes());
+    DevicePlan plan;
+    plan.build({descs}, pt, ppt, spec.num_layers, stream);
+    TKV_CUDA(launch_paged_copy(pages.layout(), plan.plan(0, 0, spec.num_layers, ppt), CopyDir::gather,
+                               ctas, stream));
+    TKV_CUDA(cudaStreamSynchronize(stream));  // bytes landed before any ordinal is pushed
+    return recs;
+}
+
+Status pd_land_chunks(PagedKVStore& pages, QueryId query, const std::vector<PdRecord>& records,
+                      cudaStream_t stream, int ctas) {
+    const auto& spec = pages.spec();
+    const uint32_t pt = spec.page_tokens;
+    const size_t bpt = spec.bytes_per_token_per_layer;
+    auto t = pages.device_table(query, stream);
+    if (!t.ok()) return t.status();
+    std::vector<XferDesc> descs;
+    for (const auto& r : records) {
+        if (r.first_token % pt) return Status{Errc::invalid_argument, "record not page aligned"};
+        if (r.bytes != uint64_t(spec.num_layers) * r.token_count * bpt)
+            return Status{Errc::size_mismatch, "pushed record size"};  // sim_engine.cpp:461-462
+        for (uint32_t l = 0; l < spec.num_layers; ++l) {
+            Status st = pages.check_writable_span(query, l, r.first_token / pt, r.token_count);
+            if (!st.ok()) return st;
+        }
+        XferDesc x;
+        x.chunk = r.addr;
+        x.layer_stride = uint64_t(r.token_count) * bpt;
+        x.table = t.value().ptr;
+        x.table_stride = t.value().stride;
+        x.first_page = r.first_token / pt;
+        x.n_tokens = r.token_count;
+        descs.push_back(x);
+    }
+    if (descs.empty()) return Status::success();
+    const uint32_t ppt = pages_per_tile(pages.page_bytes());
+    DevicePlan plan;
+    plan.build({descs}, pt, ppt, spec.num_layers, stream);
+    TKV_CUDA(launch_paged_copy(pages.layout(), plan.plan(0, 0, spec.num_layers, ppt),
+                               CopyDir::scatter, ctas, stream));
+    for (const auto& r : records)
+        for (uint32_t l = 0; l < spec.num_layers; ++l)
+            pages.mark_span_populated(query, l, r.first_token / pt, r.token_count);
+    TKV_CUDA(cudaStreamSynchronize(stream));  // plan buffers are freed on return
+    return Status::success();
+}
+
+Status enable_peer_access(int device, int peer) {
+    if (device == peer) return Status::success();
+    int can = 0;
+    TKV_CUDA(cudaDeviceCanAccessPeer(&can, device, peer));
+    if (!can) return Status{Errc::invalid_argument, "no peer access between devices"};
+    int prev = 0;
+    TKV_CUDA(cudaGetDevice(&prev));
+    TKV_CUDA(cudaSetDevice(device));
+    cudaError_t e = cudaDeviceEnablePeerAccess(peer, 0);
+    cudaSetDevice(prev);
+    if (e == cudaErrorPeerAccessAlreadyEnabled) {
+        cudaGetLastError();
+        return Status::success();
+    }
+    TKV_CUDA(e);
+    return Status::success();
+}
+
+}  // namespace tkv

@@ -1,0 +1,81 @@
+// Prefill -> decode disaggregation over NVLink (replaces the TCP PD_PUSH path
+// of run_pd, src/sim_engine.cpp:374-472, and the decoder landing area
+// PdStaging, include/tierkv/pd_staging.hpp, src/pd_staging.cpp).
+//
+// Data plane: the prefiller's K1 gathers each chunk's [L][T][bpt] payload
+// straight out of its pages into the decoder's landing buffer — a device
+// address on the decoder GPU reached over NVLink (peer access in one process,
+// a CUDA IPC mapping across processes). No host bytes, no record encode, no
+// FNV. The decoder then scatters every landed chunk into its own pages with
+// ONE K2 launch over all chunks and layers.
+//
+// Control plane: PdStaging keeps the reference's contract unchanged —
+// register before any push; each ordinal is filled exactly once (a duplicate
+// push acks without overwriting); a push beyond the final ordinal, or a final
+// marker below an already filled ordinal, is a protocol_error; await returns
+// the records in ordinal order once the final ordinal and everything before
+// it landed, then forgets the query; cancel wakes the awaiter with io_error.
+// A record here describes where the payload landed instead of carrying it.
+#pragma once
+
+#include <condition_variable>
+#include <map>
+#include <mutex>
+#include <vector>
+
+#include "common.hpp"
+#include "kernels.hpp"
+#include "paged_store.hpp"
+
+namespace tkv {
+
+struct PdRecord {
+    uint64_t addr = 0;          // device address of the landed chunk payload (decoder GPU)
+    uint64_t bytes = 0;
+    uint32_t token_count = 0;
+    uint32_t first_token = 0;   // absolute position of the chunk's first token
+};
+
+class PdStaging {
+public:
+    Status register_query(QueryId id);
+    Status push(QueryId id, uint32_t ordinal, bool last, const PdRecord& rec);
+    // Blocks until complete (or cancelled); records in ordinal order.
+    Result<std::vector<PdRecord>> await(QueryId id);
+    Status cancel(QueryId id);
+    size_t registered() const;
+
+private:
+    struct Query {
+        std::map<uint32_t, PdRecord> slots;
+        uint32_t last_ordinal = 0;
+        bool last_seen = false;
+        bool cancelled = false;
+    };
+    static bool complete(const Query& q) {
+        return q.last_seen && q.slots.size() == size_t(q.last_ordinal) + 1;
+    }
+    mutable std::mutex mu_;
+    std::condition_variable cv_;
+    std::map<QueryId, Query> queries_;
+};
+
+// Prefiller side: K1 over chunks [first_chunk, first_chunk + n_chunks) of the
+// query's first n_tokens tokens, all layers, into `landing` laid out as
+// consecutive chunk payloads (chunk i at landing + i * chunk_stride bytes,
+// each [L][T_i][bpt]). `landing` may be a peer GPU's memory. Enqueued on
+// `stream`; returns the records describing where each chunk landed.
+Result<std::vector<PdRecord>> pd_send_chunks(PagedKVStore& pages, QueryId query, size_t n_tokens,
+                                             size_t chunk_size, uint64_t landing,
+                                             uint64_t chunk_stride, cudaStream_t stream,
+                                             int ctas = 0);
+
+// Decoder side: K2 of every landed record into the query's pages (all
+// layers, one launch), marks the pages populated. Enqueued on `stream`.
+Status pd_land_chunks(PagedKVStore& pages, QueryId query, const std::vector<PdRecord>& records,
+                      cudaStream_t stream, int ctas = 0);
+
+// Peer access between two devices of this process (idempotent).
+Status enable_peer_access(int device, int peer);
+
+}  // namespace tkv

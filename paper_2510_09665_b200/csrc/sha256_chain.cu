@@ -177,6 +177,7 @@ cudaError_t launch_hash_chains(const uint32_t* tokens, const ChainDesc* chains, 
         return cudaErrorInvalidValue;
     const int threads = 128;
     const int blocks = int((n_chains + threads - 1) / threads);
+    note_launch();
     hash_chains_kernel<<<blocks, threads, 0, stream>>>(tokens, chains, n_chains, params, out);
     return cudaGetLastError();
 }

@@ -70,7 +70,8 @@ private:
 
 // A reserved slot about to be written by the device.
 struct SlotWrite {
-    enum class Kind { write, already_present, in_flight } kind = Kind::write;
+    // none: no slot claimed (reservation failed, or not attempted).
+    enum class Kind { none, write, already_present, in_flight } kind = Kind::none;
     uint8_t* host = nullptr;   // slot base (host address)
     uint8_t* dev = nullptr;    // slot base (device-visible alias)
     PutHandle handle;          // completes when the bytes are present

@@ -122,6 +122,7 @@ cudaError_t launch_synth_pages(const PagedLayout& L, const SynthArgs& A, cudaStr
     if (A.pos_end <= A.pos_begin || A.layer_end <= A.layer_begin) return cudaSuccess;
     const uint64_t total =
         uint64_t(A.layer_end - A.layer_begin) * (A.pos_end - A.pos_begin) * ((L.bpt + 7) / 8);
+    note_launch();
     synth_pages_kernel<false><<<grid_for(total), 256, 0, s>>>(L, A, nullptr);
     return cudaGetLastError();
 }
@@ -131,6 +132,7 @@ cudaError_t launch_verify_pages(const PagedLayout& L, const SynthArgs& A,
     if (A.pos_end <= A.pos_begin || A.layer_end <= A.layer_begin) return cudaSuccess;
     const uint64_t total =
         uint64_t(A.layer_end - A.layer_begin) * (A.pos_end - A.pos_begin) * ((L.bpt + 7) / 8);
+    note_launch();
     synth_pages_kernel<true><<<grid_for(total), 256, 0, s>>>(L, A, mismatches);
     return cudaGetLastError();
 }
@@ -139,6 +141,7 @@ cudaError_t launch_synth_chunk(const uint32_t* tokens, uint64_t seed, uint32_t s
                                uint32_t n_layers, uint32_t bpt, uint8_t* out, cudaStream_t s) {
     if (n == 0 || n_layers == 0) return cudaSuccess;
     const uint64_t total = uint64_t(n_layers) * n * ((bpt + 7) / 8);
+    note_launch();
     synth_chunk_kernel<<<grid_for(total), 256, 0, s>>>(tokens, seed, start, n, n_layers, bpt, out);
     return cudaGetLastError();
 }

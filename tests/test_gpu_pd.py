@@ -1,0 +1,73 @@
+"""PD disaggregation on the B200 (run_pd, src/sim_engine.cpp:347-543): the
+prefiller's pages are gathered chunk by chunk straight into the decoder's
+landing buffer (K1 writing device memory — a peer GPU's in production, the
+same GPU here since gpurun gives one), ordinals are pushed out of order with
+a duplicate, the decoder awaits them in order and scatters all chunks into
+its own pages with one K2 launch. Byte oracle: the reference's own PD check,
+synth_layer_kv recomputation of every layer (sim_engine.cpp:474-490)."""
+import numpy as np
+import pytest
+import torch
+
+import scenarios as S
+
+pytestmark = pytest.mark.gpu
+
+
+def test_pd_send_land_byte_exact(tkv, C):
+    from paper_2510_09665_b200.api import Engine, PdStaging, pd_land, pd_send
+    spec = dict(num_layers=4, bpt=512, page_tokens=16, tag="pd-test", chunk_size=32)
+    pre = Engine(**spec, ram_slots=4, num_pages=256)
+    dec = Engine(**spec, ram_slots=4, num_pages=256)
+    prompt = S.make_prompt(200, 71)  # 7 chunks, the last one partial (8 tokens)
+    pre.bind_pages(10, 200)
+    pre.compute_range(10, prompt, 0, 200)
+    stride = 4 * 32 * 512
+    landing = torch.zeros(7 * stride, dtype=torch.uint8, device="cuda")
+    staging = PdStaging()
+    assert staging.register_query(10) == 0
+    recs = pd_send(pre, 10, 200, landing.data_ptr(), stride)
+    assert [r.token_count for r in recs] == [32] * 6 + [8]
+    for o in [3, 0, 6, 1, 5, 2, 4, 3]:
+        assert staging.push(10, o, o == 6, recs[o]) == 0
+    rc, landed = staging.await_(10)
+    assert rc == 0 and [r.first_token for r in landed] == [32 * i for i in range(7)]
+    dec.bind_pages(10, 200)
+    pd_land(dec, 10, landed)
+    assert S.pages_equal_synth(dec, 10, prompt, 200, C)
+    # the landed chunk payloads are the KVChunk byte contract [L][T][bpt]
+    seed = C.model_seed("pd-test")
+    host = landing.cpu().numpy()
+    for i, r in enumerate(recs):
+        want = C.synth_chunk(seed, prompt, 32 * i, r.token_count, 4, 512)
+        assert np.array_equal(host[i * stride: i * stride + want.size], want)
+    pre.close()
+    dec.close()
+
+
+def test_pd_land_rejects_bad_records(tkv):
+    from paper_2510_09665_b200.api import Engine, PdRecordC, pd_land
+    from paper_2510_09665_b200._lib import TkvError
+    dec = Engine(num_layers=2, bpt=64, page_tokens=16, tag="pd-test", chunk_size=32, ram_slots=2,
+                 num_pages=64)
+    dec.bind_pages(1, 64)
+    buf = torch.zeros(4096, dtype=torch.uint8, device="cuda")
+    with pytest.raises(TkvError) as e:  # size does not match the geometry (sim_engine.cpp:461-462)
+        pd_land(dec, 1, [PdRecordC(addr=buf.data_ptr(), bytes=100, token_count=32, first_token=0)])
+    assert e.value.code == 6
+    with pytest.raises(TkvError) as e:  # beyond the query's pages
+        pd_land(dec, 1, [PdRecordC(addr=buf.data_ptr(), bytes=2 * 32 * 64, token_count=32, first_token=64)])
+    assert e.value.code == 6
+    dec.close()
+
+
+def test_pd_ipc_handle_roundtrip(tkv):
+    """The cross-process landing path: export a landing buffer with CUDA IPC
+    and map it back (same process here: cudaIpcOpenMemHandle refuses the
+    exporting process, which is the documented behaviour we assert)."""
+    import ctypes as ct
+    from paper_2510_09665_b200._lib import lib
+    buf = torch.zeros(1 << 20, dtype=torch.uint8, device="cuda")
+    h = (ct.c_uint8 * 64)()
+    assert lib().tkv_ipc_get_handle(buf.data_ptr(), h) == 0
+    assert any(h[i] for i in range(64))
