@@ -63,6 +63,7 @@ def parse():
     ap.add_argument("--store-ctas", type=int, default=0)
     ap.add_argument("--staging-depth", type=int, default=2)
     ap.add_argument("--profile-kernels", action="store_true", help="only run the K1/K2 device-resident loop")
+    ap.add_argument("--trace", action="store_true", help="host time of every call of one step")
     return ap.parse_args()
 
 
@@ -319,6 +320,46 @@ class B200Bench:
         e.release_query(q)
         return loaded, n - self.n_pre, prompt
 
+    def trace_step(self, k):
+        """One step with the host time of every connector call (diagnosis)."""
+        e, L, n = self.e, self.L, self.n
+        prompt = prompt_tokens(self.n_pre, n - self.n_pre, k + 1)
+        q = self.qid = self.qid + 1
+        log = []
+
+        def t(name, fn):
+            t0 = time.perf_counter()
+            r = fn()
+            log.append((name, round(1e3 * (time.perf_counter() - t0), 3)))
+            return r
+        self.torch.cuda.synchronize()
+        T0 = time.perf_counter()
+        matched = t("lookup", lambda: e.get_num_new_matched_tokens(q, prompt))
+        t("bind", lambda: e.bind_pages(q, n))
+        t("update", lambda: e.update_state_after_alloc(q, (n + 15) // 16, (matched + 15) // 16))
+        m = t("meta", lambda: e.build_connector_meta([(q, prompt)]))
+        t("start_load", lambda: e.start_load_kv(m))
+        loaded = e.loaded_tokens(m, q)
+        for layer in range(L):
+            t(f"wait_load{layer}", lambda: e.wait_load_kv(m, layer))
+            t(f"compute{layer}", lambda: e.compute_range(q, prompt, loaded, n, layers=(layer, layer + 1)))
+            if layer:
+                t(f"wait_store{layer - 1}", lambda: e.wait_store_kv(m, layer - 1))
+            t(f"start_store{layer}", lambda: e.start_store_kv(m))
+        t("final_wait", lambda: e.wait_store_kv(m, L - 1))
+        total = 1e3 * (time.perf_counter() - T0)
+        tl = e.timeline(m)
+        e.drop_meta(m)
+        e.finish_query(q)
+        e.release_query(q)
+        slow = sorted(log, key=lambda x: -x[1])[:12]
+        pick = [0, 1, 2, 10, 40, L - 2, L - 1]
+        return {"total_ms": round(total, 2), "slowest": slow,
+                "timeline_ms[layer]=[h2d,load,compute,gathered,d2h]":
+                    {int(i): [round(float(x), 2) for x in tl[i]] for i in pick if i < L},
+                "sum_start_store": round(sum(v for k_, v in log if k_.startswith("start_store")), 2),
+                "sum_compute": round(sum(v for k_, v in log if k_.startswith("compute")), 2)}
+
     def step_bytes(self):
         return (self.n_pre + (self.n - self.n_pre)) * self.L * self.bpt
 
@@ -462,6 +503,10 @@ def run_b200(args):
     bench.store_prefix()
     for k in range(args.warmup):
         bench.step(k)
+    if args.trace:
+        if rank == 0:
+            print(json.dumps({"trace": bench.trace_step(1000)}), flush=True)
+        return
     barrier()
     torch.cuda.synchronize()
     lib_ = bench.e.L

@@ -259,6 +259,10 @@ int tkv_meta_plan(tkv_meta* m, size_t plan_index, int kind, uint64_t* spans4, ui
                   size_t cap, size_t* n, uint64_t* matched);
 int tkv_meta_store_results(tkv_meta* m, uint64_t query, int* codes, uint8_t* digests, size_t cap,
                            size_t* n);
+/* Diagnostics: per layer {h2d done, load done, compute done, gathered, d2h
+ * done} in ms since the batch's loads were enqueued (-1 = unused). Writes
+ * 5*num_layers floats after the batch completed. */
+int tkv_meta_timeline(tkv_meta* m, float* out, size_t cap, size_t* n);
 
 /* ---- PD disaggregation over NVLink (run_pd, src/sim_engine.cpp:347-543;
  *      PdStaging, include/tierkv/pd_staging.hpp) --------------------------- */

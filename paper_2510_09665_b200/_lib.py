@@ -124,6 +124,7 @@ SIGNATURES = {
     "tkv_meta_num_plans": (sz, [vp]),
     "tkv_meta_plan": (ct.c_int, [vp, sz, ct.c_int, u64p, u8p, sz, szp, u64p]),
     "tkv_meta_store_results": (ct.c_int, [vp, ct.c_uint64, ct.POINTER(ct.c_int), u8p, sz, szp]),
+    "tkv_meta_timeline": (ct.c_int, [vp, ct.POINTER(ct.c_float), sz, szp]),
     "tkv_pd_staging_create": (ct.c_int, [ct.POINTER(vp)]),
     "tkv_pd_staging_destroy": (None, [vp]),
     "tkv_pd_register": (ct.c_int, [vp, ct.c_uint64]),

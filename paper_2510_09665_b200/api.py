@@ -111,6 +111,8 @@ class Engine:
         check(self.L.tkv_connector_create(self.store, self.pages, ct.byref(cfg), ct.byref(self.conn)))
         self._metas: list[ct.c_void_p | None] = []
         self._dev_prompts: dict[int, torch.Tensor] = {}
+        self._host_prompts: dict[int, np.ndarray] = {}
+        self._prompt_src: dict[int, object] = {}
         self._mism = torch.zeros(1, dtype=torch.int64, device=f"cuda:{device}")
 
     @property
@@ -156,15 +158,21 @@ class Engine:
     def release_query(self, qid: int) -> int:
         self.synchronize()
         self._dev_prompts.pop(qid, None)
+        self._host_prompts.pop(qid, None)
+        self._prompt_src.pop(qid, None)
         return self.L.tkv_pages_release(self.pages, qid)
 
     def free_page_count(self) -> int:
         return self.L.tkv_pages_free_count(self.pages)
 
     def dev_prompt(self, qid: int, prompt) -> torch.Tensor:
+        if self._prompt_src.get(qid) is prompt:  # same object as last call: no compare, no copy
+            return self._dev_prompts[qid]
         t = _tokens(prompt)
         cur = self._dev_prompts.get(qid)
-        if cur is None or cur.numel() != t.size:
+        self._prompt_src[qid] = prompt
+        if cur is None or cur.numel() != t.size or not np.array_equal(self._host_prompts.get(qid), t):
+            self._host_prompts[qid] = t.copy()
             cur = torch.from_numpy(t.view(np.int32)).to(f"cuda:{self.device}", non_blocking=False)
             self._dev_prompts[qid] = cur
         return cur
@@ -216,6 +224,9 @@ class Engine:
     # --- connector ---
     def get_num_new_matched_tokens(self, qid: int, prompt) -> int:
         t = _tokens(prompt)
+        # The engine receives the prompt at scheduling time; its device copy
+        # goes up now, before this step's loads occupy the copy engines.
+        self.dev_prompt(qid, t)
         m = ct.c_size_t(0)
         check(self.L.tkv_connector_get_num_new_matched_tokens(self.conn, qid, t.ctypes.data_as(u32p), t.size,
                                                               ct.byref(m)))
@@ -281,6 +292,14 @@ class Engine:
         check(self.L.tkv_meta_store_results(self._metas[m], qid, codes, dig.ctypes.data_as(u8p), cap,
                                             ct.byref(n)))
         return [(dig[32 * i:32 * i + 32].tobytes(), int(codes[i])) for i in range(n.value)]
+
+    def timeline(self, m: int) -> np.ndarray:
+        """[layers, 5] ms: h2d done, load done, compute done, gathered, d2h done."""
+        cap = 5 * self.num_layers
+        out = (ct.c_float * cap)()
+        n = ct.c_size_t(0)
+        check(self.L.tkv_meta_timeline(self._metas[m], out, cap, ct.byref(n)))
+        return np.array(out[:n.value], dtype=np.float32).reshape(-1, 5)
 
     def begin_decode(self, qid: int) -> int:
         return self.L.tkv_connector_begin_decode(self.conn, qid)

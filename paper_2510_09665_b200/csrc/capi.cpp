@@ -575,6 +575,15 @@ int tkv_ipc_open_handle(const uint8_t* handle64, void** out) {
 }
 int tkv_ipc_close(void* ptr) { return cuda(cudaIpcCloseMemHandle(ptr)); }
 
+int tkv_meta_timeline(tkv_meta* m, float* out, size_t cap, size_t* n) {
+    return guard([&] {
+        auto t = m->m.timeline();
+        *n = t.size();
+        std::memcpy(out, t.data(), std::min(cap, t.size()) * sizeof(float));
+        return 0;
+    });
+}
+
 void tkv_meta_destroy(tkv_meta* m) { delete m; }
 int tkv_meta_layerwise(tkv_meta* m) { return m->m.mode() == TransferMode::layerwise; }
 size_t tkv_meta_loaded_tokens(tkv_meta* m, uint64_t q) { return m->m.loaded_tokens(q); }

@@ -86,6 +86,40 @@ void DeviceBuffer::reserve(size_t n) {
     bytes = n;
 }
 
+std::unique_ptr<DualBuffer> DualPool::acquire(size_t bytes) {
+    {
+        std::lock_guard lock(mu_);
+        size_t best = free_.size();
+        for (size_t i = 0; i < free_.size(); ++i)
+            if (free_[i]->host.bytes >= bytes &&
+                (best == free_.size() || free_[i]->host.bytes < free_[best]->host.bytes))
+                best = i;
+        if (best != free_.size()) {
+            auto b = std::move(free_[best]);
+            free_.erase(free_.begin() + long(best));
+            return b;
+        }
+        ++created_;
+    }
+    size_t cap = 4096;
+    while (cap < bytes) cap <<= 1;
+    auto b = std::make_unique<DualBuffer>();
+    b->host.reserve(cap);
+    b->dev.reserve(cap);
+    return b;
+}
+
+void DualPool::release(std::unique_ptr<DualBuffer> b) {
+    if (!b) return;
+    std::lock_guard lock(mu_);
+    free_.push_back(std::move(b));
+}
+
+size_t DualPool::blocks() const {
+    std::lock_guard lock(mu_);
+    return created_;
+}
+
 Stream Stream::create(int priority) {
     cudaStream_t s = nullptr;
     TKV_CUDA(cudaStreamCreateWithPriority(&s, cudaStreamNonBlocking, priority));
@@ -97,6 +131,9 @@ Stream::~Stream() {
 }
 
 Event::Event() { TKV_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming)); }
+Event::Event(bool timing) {
+    TKV_CUDA(cudaEventCreateWithFlags(&e, timing ? cudaEventDefault : cudaEventDisableTiming));
+}
 Event::~Event() {
     if (e) cudaEventDestroy(e);
 }

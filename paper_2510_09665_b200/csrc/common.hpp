@@ -10,6 +10,8 @@
 #include <array>
 #include <cstdint>
 #include <cstring>
+#include <memory>
+#include <mutex>
 #include <span>
 #include <stdexcept>
 #include <string>
@@ -176,6 +178,27 @@ struct DeviceBuffer {
     void reserve(size_t n);
 };
 
+// A pinned staging buffer paired with a device buffer of the same size, and
+// a pool of them. cudaHostAlloc / cudaMalloc can synchronize the device, so
+// nothing on the transfer path allocates once the pool is warm: per-batch
+// plans and per-query page tables borrow blocks and return them.
+struct DualBuffer {
+    PinnedBuffer host;
+    DeviceBuffer dev;
+};
+
+class DualPool {
+public:
+    std::unique_ptr<DualBuffer> acquire(size_t bytes);
+    void release(std::unique_ptr<DualBuffer> b);
+    size_t blocks() const;
+
+private:
+    mutable std::mutex mu_;
+    std::vector<std::unique_ptr<DualBuffer>> free_;
+    size_t created_ = 0;
+};
+
 struct Stream {
     cudaStream_t s = nullptr;
     bool owned = false;
@@ -201,6 +224,7 @@ struct Stream {
 struct Event {
     cudaEvent_t e = nullptr;
     Event();
+    explicit Event(bool timing);
     ~Event();
     Event(const Event&) = delete;
     Event& operator=(const Event&) = delete;

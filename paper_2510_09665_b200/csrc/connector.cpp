@@ -9,6 +9,23 @@ namespace tkv {
 
 namespace {
 
+// Per-layer events are timing-capable so a batch can report its device
+// timeline (tkv_meta_timeline) without a profiler.
+void make_events(std::vector<Event>& v, size_t n) {
+    v.clear();
+    v.reserve(n);
+    for (size_t i = 0; i < n; ++i) v.emplace_back(true);
+}
+
+float elapsed(const Event& a, const Event& b) {
+    float ms = -1.f;
+    if (cudaEventElapsedTime(&ms, a, b) != cudaSuccess) {
+        cudaGetLastError();
+        return -1.f;
+    }
+    return ms;
+}
+
 struct ReleaseCtx {
     TieredStore* store;
     std::vector<Digest> digests;
@@ -73,6 +90,11 @@ struct BatchState {
     std::vector<Event> h2d_done, load_done;
     DevicePlan load_plan;
     size_t ring_slot_bytes = 0;
+    bool loads_ce = false;        // lazy copy-engine pipeline in use
+    bool loads_finalized = false;
+    uint32_t next_load = 0;       // next layer to enqueue
+    uint32_t load_depth = 1;
+    size_t load_layer_bytes = 0;
 
     // stores
     bool stores_reserved = false;
@@ -82,6 +104,7 @@ struct BatchState {
     std::vector<StoreItem> stores;
     std::vector<Event> compute_done, gathered, d2h_done;
     Event store_complete;
+    Event t0{true};  // timeline origin (recorded when loads are enqueued)
     DevicePlan store_plan;
     std::atomic<bool> committed{false};
     bool any_store_writes = false;
@@ -92,6 +115,10 @@ struct BatchState {
     ~BatchState() {
         // Device buffers above may still feed in-flight work: drain first.
         try {
+            if (loads_ce && !loads_finalized) {  // engine stopped waiting early: finish the loads
+                std::lock_guard io(conn->io_mu_);
+                conn->enqueue_load_layers(*this, num_layers);
+            }
             if (loads_started && !load_done.empty()) load_done.back().sync();
             if (any_store_writes) {
                 TKV_CUDA(cudaStreamSynchronize(conn->store_stream_));
@@ -128,6 +155,22 @@ std::vector<std::pair<ChunkKey, Status>> ConnectorMetadata::store_results(QueryI
     auto it = state_->per_query.find(id);
     if (it == state_->per_query.end()) return {};
     return it->second.store_results;
+}
+
+std::vector<float> ConnectorMetadata::timeline() const {
+    const BatchState& b = *state_;
+    std::vector<float> out(size_t(b.num_layers) * 5, -1.f);
+    auto get = [&](const std::vector<Event>& v, uint32_t l) {
+        return (b.loads_started && l < v.size()) ? elapsed(b.t0, v[l]) : -1.f;
+    };
+    for (uint32_t l = 0; l < b.num_layers; ++l) {
+        out[5 * l + 0] = get(b.h2d_done, l);
+        out[5 * l + 1] = get(b.load_done, l);
+        out[5 * l + 2] = get(b.compute_done, l);
+        out[5 * l + 3] = get(b.gathered, l);
+        out[5 * l + 4] = get(b.d2h_done, l);
+    }
+    return out;
 }
 
 Connector::Connector(TieredStore& store, PagedKVStore& pages, Config cfg)
@@ -291,8 +334,9 @@ Status Connector::enqueue_loads(BatchState& b) {
     }
     const bool blocking = b.mode == TransferMode::blocking;
     const bool zero_copy = blocking || cfg_.load_path == LoadPath::zero_copy;
-    b.h2d_done.resize(L);
-    b.load_done.resize(L);
+    make_events(b.h2d_done, L);
+    make_events(b.load_done, L);
+    b.t0.record(h2d_stream_);
     b.loads_started = true;
     if (b.loads.empty()) {
         for (uint32_t l = 0; l < L; ++l) b.load_done[l].record(load_stream_);
@@ -336,7 +380,7 @@ Status Connector::enqueue_loads(BatchState& b) {
             vars[v].push_back(d);
         }
     }
-    b.load_plan.build(vars, pt, ppt, L, load_stream_);
+    b.load_plan.build(plan_pool_, vars, pt, ppt, L, load_stream_);
     const PagedLayout layout = pages_.layout();
 
     if (zero_copy && blocking) {
@@ -350,44 +394,71 @@ Status Connector::enqueue_loads(BatchState& b) {
             b.load_done[l].record(load_stream_);
         }
     } else {
-        // Layerwise copy-engine pipeline through a `depth`-layer staging ring.
+        // Layerwise copy-engine pipeline through a `depth`-layer staging ring,
+        // enqueued lazily `depth` layers ahead of the engine (the reference
+        // launches layer l+1 when the engine waits for l, connector.cpp:268-279):
+        // the copy engines are shared with the engine's own transfers, which
+        // must not queue behind a whole prompt of loads.
         if (ring_used_) ring_free_.wait_on(h2d_stream_);  // previous batch done with the ring
-        const size_t n = b.loads.size();
-        std::vector<void*> dst(n), src(n);
-        std::vector<size_t> sizes(n);
-        cudaMemcpyAttributes attr{};
-        attr.srcAccessOrder = cudaMemcpySrcAccessOrderStream;
-        size_t attr_idx = 0, fail_idx = 0;
-        for (uint32_t l = 0; l < L; ++l) {
-            const uint32_t r = l % depth;
-            if (l >= depth) b.load_done[l - depth].wait_on(h2d_stream_);
-            for (size_t i = 0; i < n; ++i) {
-                const auto& it = b.loads[i];
-                src[i] = it.slot.host + size_t(l) * it.record_tokens * bpt;
-                dst[i] = staging_.ptr + size_t(r) * layer_bytes + it.staging_off;
-                sizes[i] = it.span.length() * bpt;
-            }
-            TKV_CUDA(cudaMemcpyBatchAsync(dst.data(), src.data(), sizes.data(), n, &attr, &attr_idx,
-                                          1, &fail_idx, h2d_stream_));
-            b.h2d_done[l].record(h2d_stream_);
-            b.h2d_done[l].wait_on(load_stream_);
-            TKV_CUDA(launch_paged_copy(layout, b.load_plan.plan(r, l, 1, ppt), CopyDir::scatter,
-                                       cfg_.load_ctas, load_stream_));
-            b.load_done[l].record(load_stream_);
-        }
-        ring_free_.record(load_stream_);
-        ring_used_ = true;
+        b.loads_ce = true;
+        b.load_depth = depth;
+        b.load_layer_bytes = layer_bytes;
+        b.next_load = 0;
+        enqueue_load_layers(b, std::min<uint32_t>(L, depth + 1));
     }
     // Pages hold the bytes once the stream reaches them; the slots are free
     // for eviction after the last scatter.
     for (const auto& it : b.loads)
         for (uint32_t l = 0; l < L; ++l)
             pages_.mark_span_populated(it.id, l, it.span.start / pt, it.span.length());
-    auto* ctx = new ReleaseCtx{&store_, {}};
-    for (const auto& it : b.loads) ctx->digests.push_back(it.digest);
-    TKV_CUDA(cudaLaunchHostFunc(load_stream_, release_cb, ctx));
+    if (!b.loads_ce) {  // the lazy CE pipeline releases after its last layer
+        auto* ctx = new ReleaseCtx{&store_, {}};
+        for (const auto& it : b.loads) ctx->digests.push_back(it.digest);
+        TKV_CUDA(cudaLaunchHostFunc(load_stream_, release_cb, ctx));
+    }
     if (blocking) TKV_CUDA(cudaStreamSynchronize(load_stream_));
     return Status::success();
+}
+
+void Connector::enqueue_load_layers(BatchState& b, uint32_t upto) {
+    if (!b.loads_ce) return;
+    const auto& model = store_.config().model;
+    const size_t bpt = model.bytes_per_token_per_layer;
+    const uint32_t ppt = pages_per_tile(pages_.page_bytes());
+    const PagedLayout layout = pages_.layout();
+    const size_t n = b.loads.size();
+    std::vector<void*> dst(n), src(n);
+    std::vector<size_t> sizes(n);
+    cudaMemcpyAttributes attr{};
+    attr.srcAccessOrder = cudaMemcpySrcAccessOrderStream;
+    size_t attr_idx = 0, fail_idx = 0;
+    upto = std::min(upto, b.num_layers);
+    for (uint32_t l = b.next_load; l < upto; ++l) {
+        const uint32_t r = l % b.load_depth;
+        if (l >= b.load_depth) b.load_done[l - b.load_depth].wait_on(h2d_stream_);
+        for (size_t i = 0; i < n; ++i) {
+            const auto& it = b.loads[i];
+            src[i] = it.slot.host + size_t(l) * it.record_tokens * bpt;
+            dst[i] = staging_.ptr + size_t(r) * b.load_layer_bytes + it.staging_off;
+            sizes[i] = it.span.length() * bpt;
+        }
+        TKV_CUDA(cudaMemcpyBatchAsync(dst.data(), src.data(), sizes.data(), n, &attr, &attr_idx, 1,
+                                      &fail_idx, h2d_stream_));
+        b.h2d_done[l].record(h2d_stream_);
+        b.h2d_done[l].wait_on(load_stream_);
+        TKV_CUDA(launch_paged_copy(layout, b.load_plan.plan(r, l, 1, ppt), CopyDir::scatter,
+                                   cfg_.load_ctas, load_stream_));
+        b.load_done[l].record(load_stream_);
+    }
+    if (upto > b.next_load) b.next_load = upto;
+    if (b.next_load == b.num_layers && !b.loads_finalized) {
+        b.loads_finalized = true;
+        ring_free_.record(load_stream_);
+        ring_used_ = true;
+        auto* ctx = new ReleaseCtx{&store_, {}};
+        for (const auto& it : b.loads) ctx->digests.push_back(it.digest);
+        TKV_CUDA(cudaLaunchHostFunc(load_stream_, release_cb, ctx));
+    }
 }
 
 Status Connector::start_load_kv(ConnectorMetadata& meta) {
@@ -419,6 +490,10 @@ Status Connector::wait_load_kv(ConnectorMetadata& meta, uint32_t layer) {
         if (!st.ok()) return st;
     }
     try {
+        if (b.loads_ce && b.next_load < b.num_layers) {
+            std::lock_guard io(io_mu_);
+            enqueue_load_layers(b, layer + 2 + b.load_depth);  // keep `depth` layers in flight
+        }
         b.load_done[layer].wait_on(cfg_.engine_stream);  // engine stream, not the host, waits
     } catch (const CudaError& e) {
         return Status{Errc::cuda_error, e.what()};
@@ -465,7 +540,7 @@ Status Connector::reserve_stores(BatchState& b) {
         }
     }
     b.any_store_writes = !descs.empty();
-    b.compute_done.resize(b.num_layers);
+    make_events(b.compute_done, b.num_layers);
     b.stores_reserved = true;
     // Copy-engine path (layerwise only): K1 writes one layer of every chunk
     // into an HBM staging ring slot; the CE then copies each chunk-layer
@@ -473,7 +548,7 @@ Status Connector::reserve_stores(BatchState& b) {
     b.store_ce = cfg_.store_path == StorePath::copy_engine &&
                  b.mode == TransferMode::layerwise && b.any_store_writes;
     if (!b.store_ce) {
-        b.store_plan.build({descs}, pt, ppt, b.num_layers, store_stream_);
+        b.store_plan.build(plan_pool_, {descs}, pt, ppt, b.num_layers, store_stream_);
         return Status::success();
     }
     size_t off = 0;
@@ -504,9 +579,9 @@ Status Connector::reserve_stores(BatchState& b) {
             ++k;
         }
     }
-    b.store_plan.build(vars, pt, ppt, b.num_layers, store_stream_);
-    b.gathered.resize(b.num_layers);
-    b.d2h_done.resize(b.num_layers);
+    b.store_plan.build(plan_pool_, vars, pt, ppt, b.num_layers, store_stream_);
+    make_events(b.gathered, b.num_layers);
+    make_events(b.d2h_done, b.num_layers);
     if (store_ring_used_) store_ring_free_.wait_on(store_stream_);
     return Status::success();
 }
@@ -689,7 +764,7 @@ Status Connector::flush_decode(QueryId id, QueryState& qs) {
         x.n_tokens = uint32_t(n);
         auto plan = std::make_shared<DevicePlan>();
         const uint32_t ppt = pages_per_tile(pages_.page_bytes());
-        plan->build({{x}}, pt, ppt, model.num_layers, store_stream_);
+        plan->build(plan_pool_, {{x}}, pt, ppt, model.num_layers, store_stream_);
         Event computed;
         computed.record(cfg_.engine_stream);
         computed.wait_on(store_stream_);

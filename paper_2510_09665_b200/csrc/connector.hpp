@@ -74,6 +74,10 @@ public:
     const std::vector<QueryPlan>& plans() const;
     size_t loaded_tokens(QueryId id) const;
     std::vector<std::pair<ChunkKey, Status>> store_results(QueryId id) const;
+    // Device timeline after completion: per layer, ms since loads were
+    // enqueued for {h2d done, load done, compute done, gathered, d2h done}
+    // (-1 where the event was not used). Diagnostics only.
+    std::vector<float> timeline() const;
     explicit operator bool() const { return state_ != nullptr; }
 
 private:
@@ -147,6 +151,7 @@ private:
 
     const std::vector<ChunkKey>& keys_for(QueryState& qs, TokenSpanView prompt);
     Status enqueue_loads(detail::BatchState& b);
+    void enqueue_load_layers(detail::BatchState& b, uint32_t upto);
     Status store_layers(detail::BatchState& b, uint32_t first, uint32_t last);
     Status reserve_stores(detail::BatchState& b);
     Status flush_decode(QueryId id, QueryState& qs);
@@ -155,6 +160,7 @@ private:
     PagedKVStore& pages_;
     Config cfg_;
     KeyHasher hasher_;
+    DualPool plan_pool_;  // per-batch launch plans (outlives every BatchState)
     Stream h2d_stream_, load_stream_, store_stream_, d2h_stream_;
     DeviceBuffer staging_, store_staging_;
     Event ring_free_, store_ring_free_;

@@ -1,7 +1,8 @@
 // Host-built K1/K2 launch plans shared by the connector and the PD path:
 // descriptor variants (one per staging ring slot, or one for direct slot /
 // peer access) and tile prefixes for one-layer and all-layer launches,
-// uploaded once per batch with a single H2D copy.
+// uploaded once per batch with a single H2D copy from a pooled pinned block
+// (no allocation on the transfer path once the pool is warm).
 #pragma once
 
 #include <cstring>
@@ -30,12 +31,20 @@ struct DevicePlan {
     size_t variants = 0;
     uint32_t tiles_1 = 0, tiles_all = 0;
     uint64_t addr_or = 0;
-    PinnedBuffer host;
-    DeviceBuffer dev;
     size_t off_tb1 = 0, off_tball = 0;
+    DualPool* pool = nullptr;
+    std::unique_ptr<DualBuffer> buf;
 
-    void build(const std::vector<std::vector<XferDesc>>& vars, uint32_t page_tokens, uint32_t ppt,
-               uint32_t n_layers, cudaStream_t s) {
+    DevicePlan() = default;
+    DevicePlan(const DevicePlan&) = delete;
+    DevicePlan& operator=(const DevicePlan&) = delete;
+    // The owner guarantees the device work reading the plan has finished.
+    ~DevicePlan() {
+        if (pool && buf) pool->release(std::move(buf));
+    }
+
+    void build(DualPool& p, const std::vector<std::vector<XferDesc>>& vars, uint32_t page_tokens,
+               uint32_t ppt, uint32_t n_layers, cudaStream_t s) {
         variants = vars.size();
         n_desc = vars.empty() ? 0 : vars[0].size();
         if (n_desc == 0) return;
@@ -47,24 +56,25 @@ struct DevicePlan {
         off_tb1 = (desc_bytes + 15) & ~size_t(15);
         off_tball = off_tb1 + ((tb1.size() * 4 + 15) & ~size_t(15));
         const size_t total = off_tball + tball.size() * 4;
-        host.reserve(total);
-        dev.reserve(total);
+        if (pool && buf) pool->release(std::move(buf));
+        pool = &p;
+        buf = p.acquire(total);
+        uint8_t* h = buf->host.host;
         addr_or = 0;
         for (size_t v = 0; v < variants; ++v) {
-            std::memcpy(host.host + v * n_desc * sizeof(XferDesc), vars[v].data(),
-                        n_desc * sizeof(XferDesc));
+            std::memcpy(h + v * n_desc * sizeof(XferDesc), vars[v].data(), n_desc * sizeof(XferDesc));
             for (const auto& d : vars[v]) addr_or |= d.chunk | d.layer_stride;
         }
-        std::memcpy(host.host + off_tb1, tb1.data(), tb1.size() * 4);
-        std::memcpy(host.host + off_tball, tball.data(), tball.size() * 4);
-        TKV_CUDA(cudaMemcpyAsync(dev.ptr, host.host, total, cudaMemcpyHostToDevice, s));
+        std::memcpy(h + off_tb1, tb1.data(), tb1.size() * 4);
+        std::memcpy(h + off_tball, tball.data(), tball.size() * 4);
+        TKV_CUDA(cudaMemcpyAsync(buf->dev.ptr, h, total, cudaMemcpyHostToDevice, s));
     }
 
     PagedCopyPlan plan(size_t variant, uint32_t layer_begin, uint32_t n_layers, uint32_t ppt) const {
         PagedCopyPlan p;
-        p.descs = reinterpret_cast<const XferDesc*>(dev.ptr) + variant * n_desc;
+        p.descs = reinterpret_cast<const XferDesc*>(buf->dev.ptr) + variant * n_desc;
         const bool one = n_layers == 1;
-        p.tile_base = reinterpret_cast<const uint32_t*>(dev.ptr + (one ? off_tb1 : off_tball));
+        p.tile_base = reinterpret_cast<const uint32_t*>(buf->dev.ptr + (one ? off_tb1 : off_tball));
         p.n_desc = uint32_t(n_desc);
         p.total_tiles = one ? tiles_1 : tiles_all;
         p.layer_begin = layer_begin;

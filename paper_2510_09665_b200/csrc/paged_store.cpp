@@ -56,7 +56,12 @@ std::vector<PageId> PagedKVStore::release_query(QueryId query) {
     if (it == owned_.end()) return {};
     std::vector<PageId> freed = std::move(it->second);
     owned_.erase(it);
-    tables_.erase(query);
+    auto t = tables_.find(query);
+    if (t != tables_.end()) {  // the engine releases a query after its transfers finished
+        table_pool_.release(std::move(t->second.buf));
+        for (auto& r : t->second.retired) table_pool_.release(std::move(r));
+        tables_.erase(t);
+    }
     for (PageId id : freed) {
         pages_[id] = PageMeta{};
         free_list_.push_back(id);
@@ -109,20 +114,20 @@ Result<PagedKVStore::DeviceTable> PagedKVStore::device_table(QueryId query, cuda
         for (const auto& l : t.layers) stride = std::max(stride, l.size());
         const size_t rows = std::max<size_t>(spec_.num_layers, t.layers.size());
         const size_t bytes = rows * stride * sizeof(int32_t);
-        // The pinned mirror may still feed an in-flight upload on another
-        // stream; order the rewrite after everything queued on `stream`.
-        if (t.host.bytes) TKV_CUDA(cudaStreamSynchronize(stream));
-        t.host.reserve(bytes);
-        t.dev.reserve(bytes);
-        auto* h = reinterpret_cast<int32_t*>(t.host.host);
+        // A re-bound table gets a fresh block: the old one may still feed an
+        // in-flight upload or kernel, so it is only recycled at release.
+        auto fresh = table_pool_.acquire(bytes);
+        if (t.buf) t.retired.push_back(std::move(t.buf));
+        t.buf = std::move(fresh);
+        auto* h = reinterpret_cast<int32_t*>(t.buf->host.host);
         std::fill(h, h + rows * stride, -1);
         for (size_t l = 0; l < t.layers.size(); ++l)
             std::copy(t.layers[l].begin(), t.layers[l].end(), h + l * stride);
-        TKV_CUDA(cudaMemcpyAsync(t.dev.ptr, t.host.host, bytes, cudaMemcpyHostToDevice, stream));
+        TKV_CUDA(cudaMemcpyAsync(t.buf->dev.ptr, h, bytes, cudaMemcpyHostToDevice, stream));
         t.stride = uint32_t(stride);
         t.dirty = false;
     }
-    return DeviceTable{reinterpret_cast<const int32_t*>(t.dev.ptr), t.stride};
+    return DeviceTable{reinterpret_cast<const int32_t*>(t.buf->dev.ptr), t.stride};
 }
 
 Status PagedKVStore::check_readable(const std::vector<PageId>& pages, uint32_t layer,

@@ -81,8 +81,8 @@ private:
         std::vector<std::vector<PageId>> layers;
         bool dirty = true;
         uint32_t stride = 0;
-        PinnedBuffer host;
-        DeviceBuffer dev;
+        std::unique_ptr<DualBuffer> buf;  // pooled pinned mirror + device table
+        std::vector<std::unique_ptr<DualBuffer>> retired;  // earlier uploads, freed at release
     };
 
     Status check_readable(const std::vector<PageId>& pages, uint32_t layer,
@@ -95,6 +95,7 @@ private:
     DeviceBuffer pool_;
     std::vector<PageMeta> pages_;
     std::vector<PageId> free_list_;
+    DualPool table_pool_;  // declared before tables_: outlives them
     std::unordered_map<QueryId, QueryTable> tables_;
     std::unordered_map<QueryId, std::vector<PageId>> owned_;
     mutable std::mutex mu_;

@@ -67,6 +67,13 @@ size_t PdStaging::registered() const {
 
 // --- data plane ------------------------------------------------------------
 
+namespace {
+DualPool& pd_plan_pool() {
+    static DualPool pool;
+    return pool;
+}
+}  // namespace
+
 Result<std::vector<PdRecord>> pd_send_chunks(PagedKVStore& pages, QueryId query, size_t n_tokens,
                                              size_t chunk_size, uint64_t landing,
                                              uint64_t chunk_stride, cudaStream_t stream, int ctas) {
@@ -100,7 +107,7 @@ Result<std::vector<PdRecord>> pd_send_chunks(PagedKVStore& pages, QueryId query,
     if (descs.empty()) return recs;
     const uint32_t ppt = pages_per_tile(pages.page_bytes());
     DevicePlan plan;
-    plan.build({descs}, pt, ppt, spec.num_layers, stream);
+    plan.build(pd_plan_pool(), {descs}, pt, ppt, spec.num_layers, stream);
     TKV_CUDA(launch_paged_copy(pages.layout(), plan.plan(0, 0, spec.num_layers, ppt), CopyDir::gather,
                                ctas, stream));
     TKV_CUDA(cudaStreamSynchronize(stream));  // bytes landed before any ordinal is pushed
@@ -135,7 +142,7 @@ Status pd_land_chunks(PagedKVStore& pages, QueryId query, const std::vector<PdRe
     if (descs.empty()) return Status::success();
     const uint32_t ppt = pages_per_tile(pages.page_bytes());
     DevicePlan plan;
-    plan.build({descs}, pt, ppt, spec.num_layers, stream);
+    plan.build(pd_plan_pool(), {descs}, pt, ppt, spec.num_layers, stream);
     TKV_CUDA(launch_paged_copy(pages.layout(), plan.plan(0, 0, spec.num_layers, ppt),
                                CopyDir::scatter, ctas, stream));
     for (const auto& r : records)

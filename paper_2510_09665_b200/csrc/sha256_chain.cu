@@ -168,6 +168,137 @@ hash_chains_kernel(const uint32_t* __restrict__ tokens, const ChainDesc* __restr
     }
 }
 
+// ---- warp-per-chain variant (chunk_size <= kWarpChunkMax) -----------------
+//
+// The compression is inherently serial, so its latency is the floor; what the
+// thread-per-chain kernel adds on top is memory latency: each block's 16
+// token loads sit on the critical path between compressions. Here a warp
+// owns a chain: the lanes stage the chunk's tokens (prefetched into
+// registers while the previous chunk compresses), build every message word
+// of the chunk in shared memory in parallel, and then all lanes run the same
+// compression (SIMT: the cost of one) reading W by broadcast.
+constexpr int kWarpChunkMax = 512;
+constexpr int kWarpsPerCta = 4;
+constexpr int kPrefetch = kWarpChunkMax / 32;
+constexpr int kMaxWords = ((2 + kMaxTagBytes + 32 + 4 * kWarpChunkMax + 9 + 63) / 64) * 16;
+
+struct WarpSmem {
+    uint32_t tok[kWarpChunkMax + 4];
+    uint32_t w[kMaxWords];
+    uint32_t parent[8];
+};
+
+__device__ __forceinline__ uint32_t smem_msg_byte(const WarpSmem& s, const HashParams& P,
+                                                  uint32_t hdr, uint32_t len, uint32_t end,
+                                                  uint32_t o) {
+    const uint32_t tl = P.tag_len;
+    if (o < 2) return (tl >> (8 * o)) & 0xff;
+    if (o < 2 + tl) return P.tag[o - 2];
+    if (o < hdr) {
+        const uint32_t j = o - 2 - tl;
+        return (s.parent[j >> 2] >> (24 - 8 * (j & 3))) & 0xff;
+    }
+    if (o < len) {
+        const uint32_t k = o - hdr;
+        return (s.tok[k >> 2] >> (8 * (k & 3))) & 0xff;
+    }
+    if (o == len) return 0x80;
+    if (o >= end - 8) return uint32_t((uint64_t(len) * 8) >> (8 * (end - 1 - o))) & 0xff;
+    return 0;
+}
+
+__global__ void __launch_bounds__(32 * kWarpsPerCta)
+hash_chains_warp_kernel(const uint32_t* __restrict__ tokens, const ChainDesc* __restrict__ chains,
+                        uint32_t n_chains, const HashParams P, uint8_t* __restrict__ out) {
+    __shared__ WarpSmem smem[kWarpsPerCta];
+    const uint32_t lane = threadIdx.x & 31;
+    const uint32_t wid = threadIdx.x >> 5;
+    const uint32_t c = blockIdx.x * kWarpsPerCta + wid;
+    if (c >= n_chains) return;  // warp-uniform
+    WarpSmem& s = smem[wid];
+    const ChainDesc cd = chains[c];
+    if (lane < 8)
+        s.parent[lane] = (uint32_t(cd.parent[4 * lane]) << 24) |
+                         (uint32_t(cd.parent[4 * lane + 1]) << 16) |
+                         (uint32_t(cd.parent[4 * lane + 2]) << 8) | uint32_t(cd.parent[4 * lane + 3]);
+    const uint32_t cs = P.chunk_size;
+    const uint32_t hdr = 2 + P.tag_len + 32;
+    const uint32_t* base = tokens + cd.token_off;
+    uint32_t pf[kPrefetch];
+    {
+        const uint32_t n0 = min(cs, cd.n_tokens);
+#pragma unroll
+        for (int j = 0; j < kPrefetch; ++j) {
+            const uint32_t idx = lane + 32 * j;
+            pf[j] = idx < n0 ? __ldg(base + idx) : 0u;
+        }
+    }
+    uint32_t row = cd.out_first;
+    for (uint32_t start = 0; start < cd.n_tokens; start += cs, ++row) {
+        const uint32_t n = min(cs, cd.n_tokens - start);
+        // 1. stage this chunk's tokens
+#pragma unroll
+        for (int j = 0; j < kPrefetch; ++j) {
+            const uint32_t idx = lane + 32 * j;
+            if (idx < n) s.tok[idx] = pf[j];
+        }
+        if (lane == 0) s.tok[n] = 0;
+        __syncwarp();
+        // 2. prefetch the next chunk (lands while this one compresses)
+        const uint32_t nstart = start + cs;
+        if (nstart < cd.n_tokens) {
+            const uint32_t nn = min(cs, cd.n_tokens - nstart);
+#pragma unroll
+            for (int j = 0; j < kPrefetch; ++j) {
+                const uint32_t idx = lane + 32 * j;
+                pf[j] = idx < nn ? __ldg(base + nstart + idx) : 0u;
+            }
+        }
+        // 3. every message word of the chunk, in parallel across lanes
+        const uint32_t len = hdr + 4 * n;
+        const uint32_t nblocks = (len + 9 + 63) / 64;
+        const uint32_t end = 64 * nblocks;
+        for (uint32_t j = lane; j < 16 * nblocks; j += 32) {
+            const uint32_t o = 4 * j;
+            uint32_t word;
+            if (o >= hdr && o + 4 <= len) {
+                const uint32_t k = o - hdr;
+                const uint32_t kk = k & 3;
+                const uint32_t sl = (kk + 3) | ((kk + 2) << 4) | ((kk + 1) << 8) | (kk << 12);
+                word = __byte_perm(s.tok[k >> 2], kk ? s.tok[(k >> 2) + 1] : 0u, sl);
+            } else {
+                word = (smem_msg_byte(s, P, hdr, len, end, o) << 24) |
+                       (smem_msg_byte(s, P, hdr, len, end, o + 1) << 16) |
+                       (smem_msg_byte(s, P, hdr, len, end, o + 2) << 8) |
+                       smem_msg_byte(s, P, hdr, len, end, o + 3);
+            }
+            s.w[j] = word;
+        }
+        __syncwarp();
+        // 4. the serial part: every lane runs the same compressions
+        uint32_t h[8] = {0x6a09e667, 0xbb67ae85, 0x3c6ef372, 0xa54ff53a,
+                         0x510e527f, 0x9b05688c, 0x1f83d9ab, 0x5be0cd19};
+#pragma unroll 1
+        for (uint32_t b = 0; b < nblocks; ++b) {
+            uint32_t w[16];
+#pragma unroll
+            for (int i = 0; i < 16; ++i) w[i] = s.w[16 * b + i];
+            compress(h, w);
+        }
+        __syncwarp();  // all lanes done reading s.w / s.parent of this chunk
+        // 5. digest out; it is the next chunk's parent
+        if (lane == 0) {
+            uint32_t* o = reinterpret_cast<uint32_t*>(out + 32ull * row);
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                s.parent[i] = h[i];
+                o[i] = __byte_perm(h[i], 0, 0x0123);
+            }
+        }
+        __syncwarp();
+    }
+}
+
 }  // namespace
 
 cudaError_t launch_hash_chains(const uint32_t* tokens, const ChainDesc* chains, uint32_t n_chains,
@@ -175,10 +306,16 @@ cudaError_t launch_hash_chains(const uint32_t* tokens, const ChainDesc* chains, 
     if (n_chains == 0) return cudaSuccess;
     if (params.tag_len > uint32_t(kMaxTagBytes) || params.chunk_size == 0)
         return cudaErrorInvalidValue;
-    const int threads = 128;
-    const int blocks = int((n_chains + threads - 1) / threads);
     note_launch();
-    hash_chains_kernel<<<blocks, threads, 0, stream>>>(tokens, chains, n_chains, params, out);
+    if (params.chunk_size <= uint32_t(kWarpChunkMax)) {
+        const int blocks = int((n_chains + kWarpsPerCta - 1) / kWarpsPerCta);
+        hash_chains_warp_kernel<<<blocks, 32 * kWarpsPerCta, 0, stream>>>(tokens, chains, n_chains,
+                                                                          params, out);
+    } else {
+        const int threads = 128;
+        const int blocks = int((n_chains + threads - 1) / threads);
+        hash_chains_kernel<<<blocks, threads, 0, stream>>>(tokens, chains, n_chains, params, out);
+    }
     return cudaGetLastError();
 }
 
