@@ -293,13 +293,23 @@ class B200Bench:
         e.finish_query(q)
         e.release_query(q)
 
-    def step(self, k):
-        """One scheduling iteration: retrieve the prefix, store the new suffix."""
-        e, L, n = self.e, self.L, self.n
-        prompt = prompt_tokens(self.n_pre, n - self.n_pre, k + 1)
+    def lookup(self, k):
+        """Scheduler-side lookup of request k (K3 keys + LPM)."""
+        prompt = prompt_tokens(self.n_pre, self.n - self.n_pre, k + 1)
         q = self.qid = self.qid + 1
-        matched = e.get_num_new_matched_tokens(q, prompt)
-        assert matched == min(self.n_pre, n - 1), matched
+        matched = self.e.get_num_new_matched_tokens(q, prompt)
+        assert matched == min(self.n_pre, self.n - 1), matched
+        return q, prompt, matched
+
+    def step(self, k, looked_up=None, next_k=None):
+        """One scheduling iteration: retrieve the prefix, store the new suffix.
+
+        `looked_up` is request k's lookup if the scheduler already did it;
+        with `next_k` the lookup of the next request is issued while this
+        step's layers transfer (a serving scheduler's overlap) and returned.
+        """
+        e, L, n = self.e, self.L, self.n
+        q, prompt, matched = looked_up if looked_up is not None else self.lookup(k)
         assert e.bind_pages(q, n) == 0
         assert e.update_state_after_alloc(q, (n + 15) // 16, (matched + 15) // 16) == 0
         m = e.build_connector_meta([(q, prompt)])
@@ -311,6 +321,7 @@ class B200Bench:
             if layer:
                 e.wait_store_kv(m, layer - 1)
             assert e.start_store_kv(m) == 0
+        nxt = self.lookup(next_k) if next_k is not None else None
         assert e.wait_store_kv(m, L - 1) == 0
         res = e.store_results(m, q)
         assert len(res) == (n - self.n_pre + 255) // 256 and all(c == 0 for _, c in res), res[:2]
@@ -318,7 +329,7 @@ class B200Bench:
         e.drop_meta(m)
         e.finish_query(q)
         e.release_query(q)
-        return loaded, n - self.n_pre, prompt
+        return loaded, n - self.n_pre, nxt
 
     def trace_step(self, k):
         """One step with the host time of every connector call (diagnosis)."""
@@ -516,8 +527,10 @@ def run_b200(args):
         end = torch.cuda.Event(enable_timing=True)
         start.record(bench.stream)
         t0 = time.perf_counter()
+        nxt = bench.lookup(args.warmup)
         for k in range(args.steps):
-            loaded, stored, last_prompt = bench.step(args.warmup + k)
+            kk = args.warmup + k
+            loaded, stored, nxt = bench.step(kk, looked_up=nxt, next_k=kk + 1 if k + 1 < args.steps else None)
         end.record(bench.stream)
         torch.cuda.synchronize()
         wall = time.perf_counter() - t0

@@ -167,6 +167,9 @@ void tkv_pages_destroy(tkv_pages* p);
 int tkv_pages_alloc(tkv_pages* p, uint64_t query, size_t n, uint32_t* ids_out);
 int tkv_pages_bind_layer(tkv_pages* p, uint64_t query, uint32_t layer, const uint32_t* ids,
                          size_t n);
+/* SimEngine::admit (src/sim_engine.cpp:83-95): allocate ceil(tokens/page)*L
+ * pages and bind layer l to the l-th block run. */
+int tkv_pages_admit(tkv_pages* p, uint64_t query, size_t tokens);
 size_t tkv_pages_layer_pages(tkv_pages* p, uint64_t query, uint32_t layer, uint32_t* ids_out,
                              size_t cap);
 size_t tkv_pages_release(tkv_pages* p, uint64_t query);

@@ -79,6 +79,7 @@ SIGNATURES = {
     "tkv_pages_destroy": (None, [vp]),
     "tkv_pages_alloc": (ct.c_int, [vp, ct.c_uint64, sz, u32p]),
     "tkv_pages_bind_layer": (ct.c_int, [vp, ct.c_uint64, ct.c_uint32, u32p, sz]),
+    "tkv_pages_admit": (ct.c_int, [vp, ct.c_uint64, sz]),
     "tkv_pages_layer_pages": (sz, [vp, ct.c_uint64, ct.c_uint32, u32p, sz]),
     "tkv_pages_release": (sz, [vp, ct.c_uint64]),
     "tkv_pages_free_count": (sz, [vp]),

@@ -139,15 +139,8 @@ class Engine:
 
     # --- engine-side helpers (mirror oracle.RefEngine) ---
     def bind_pages(self, qid: int, tokens: int) -> int:
-        blocks = (tokens + self.page_tokens - 1) // self.page_tokens
-        ids = np.zeros(max(1, blocks * self.num_layers), np.uint32)
-        rc = self.L.tkv_pages_alloc(self.pages, qid, blocks * self.num_layers, ids.ctypes.data_as(u32p))
-        if rc:
-            return rc
-        for layer in range(self.num_layers):
-            sl = np.ascontiguousarray(ids[layer * blocks:(layer + 1) * blocks])
-            check(self.L.tkv_pages_bind_layer(self.pages, qid, layer, sl.ctypes.data_as(u32p), blocks))
-        return 0
+        """Pages for `tokens`, bound per layer (SimEngine::admit)."""
+        return self.L.tkv_pages_admit(self.pages, qid, tokens)
 
     def layer_pages(self, qid: int, layer: int) -> np.ndarray:
         n = self.L.tkv_pages_layer_pages(self.pages, qid, layer, None, 0)

@@ -264,6 +264,9 @@ int tkv_pages_bind_layer(tkv_pages* p, uint64_t q, uint32_t layer, const uint32_
         return 0;
     });
 }
+int tkv_pages_admit(tkv_pages* p, uint64_t q, size_t tokens) {
+    return guard([&] { return st(p->p->admit(q, tokens)); });
+}
 size_t tkv_pages_layer_pages(tkv_pages* p, uint64_t q, uint32_t layer, uint32_t* ids, size_t cap) {
     auto v = p->p->layer_pages(q, layer);
     if (ids) std::memcpy(ids, v.data(), std::min(cap, v.size()) * sizeof(uint32_t));

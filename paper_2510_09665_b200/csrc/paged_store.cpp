@@ -43,6 +43,22 @@ void PagedKVStore::bind_layer(QueryId query, uint32_t layer, const std::vector<P
     for (PageId id : pages) pages_[id].layer = layer;
 }
 
+Status PagedKVStore::admit(QueryId query, size_t tokens) {
+    const size_t blocks = (tokens + spec_.page_tokens - 1) / spec_.page_tokens;
+    auto alloc = alloc_pages(query, blocks * spec_.num_layers);
+    if (!alloc.ok()) return alloc.status();
+    std::lock_guard lock(mu_);
+    auto& t = tables_[query];
+    t.layers.resize(spec_.num_layers);
+    for (uint32_t l = 0; l < spec_.num_layers; ++l) {
+        auto first = alloc.value().begin() + long(size_t(l) * blocks);
+        t.layers[l].assign(first, first + long(blocks));
+        for (size_t i = 0; i < blocks; ++i) pages_[t.layers[l][i]].layer = l;
+    }
+    t.dirty = true;
+    return Status::success();
+}
+
 std::vector<PageId> PagedKVStore::layer_pages(QueryId query, uint32_t layer) const {
     std::lock_guard lock(mu_);
     auto it = tables_.find(query);

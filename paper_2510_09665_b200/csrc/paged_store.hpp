@@ -29,6 +29,9 @@ public:
 
     Result<std::vector<PageId>> alloc_pages(QueryId query, size_t n);
     void bind_layer(QueryId query, uint32_t layer, const std::vector<PageId>& pages);
+    // SimEngine::admit (src/sim_engine.cpp:83-95): blocks*L pages for a
+    // `tokens`-long sequence, layer l bound to pages [l*blocks, (l+1)*blocks).
+    Status admit(QueryId query, size_t tokens);
     std::vector<PageId> layer_pages(QueryId query, uint32_t layer) const;
     std::vector<PageId> release_query(QueryId query);
     size_t free_page_count() const;

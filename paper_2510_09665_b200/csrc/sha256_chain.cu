@@ -177,16 +177,63 @@ hash_chains_kernel(const uint32_t* __restrict__ tokens, const ChainDesc* __restr
 // registers while the previous chunk compresses), build every message word
 // of the chunk in shared memory in parallel, and then all lanes run the same
 // compression (SIMT: the cost of one) reading W by broadcast.
-constexpr int kWarpChunkMax = 512;
+constexpr int kWarpChunkMax = 256;  // the reference chunk size; larger chunks use the kernel above
 constexpr int kWarpsPerCta = 4;
 constexpr int kPrefetch = kWarpChunkMax / 32;
 constexpr int kMaxWords = ((2 + kMaxTagBytes + 32 + 4 * kWarpChunkMax + 9 + 63) / 64) * 16;
 
+constexpr int kMaxBlocks = kMaxWords / 16;
+
 struct WarpSmem {
     uint32_t tok[kWarpChunkMax + 4];
     uint32_t w[kMaxWords];
+    uint32_t kw[kMaxBlocks * 64];  // K[t] + W[t] of every block, expanded in parallel
     uint32_t parent[8];
 };
+
+// Message schedule of one block (FIPS 180-4 §6.2.2 step 1) folded with the
+// round constants: out[t] = K[t] + W[t]. Independent of the chaining state,
+// so one lane per block expands them all before the serial rounds start.
+__device__ __forceinline__ void expand_block(const uint32_t* in, uint32_t* out) {
+    uint32_t w[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+        w[i] = in[i];
+        out[i] = w[i] + kK[i];
+    }
+#pragma unroll
+    for (int t = 16; t < 64; ++t) {
+        const uint32_t w15 = w[(t - 15) & 15], w2 = w[(t - 2) & 15];
+        const uint32_t s0 = rotr(w15, 7) ^ rotr(w15, 18) ^ (w15 >> 3);
+        const uint32_t s1 = rotr(w2, 17) ^ rotr(w2, 19) ^ (w2 >> 10);
+        const uint32_t wt = w[t & 15] + s0 + w[(t - 7) & 15] + s1;
+        w[t & 15] = wt;
+        out[t] = wt + kK[t];
+    }
+}
+
+// The 64 rounds with K+W precomputed: only the state recurrence is serial.
+__device__ __forceinline__ void compress_kw(uint32_t h[8], const uint32_t* kw) {
+    uint32_t a = h[0], b = h[1], c = h[2], d = h[3], e = h[4], f = h[5], g = h[6], hh = h[7];
+#pragma unroll
+    for (int t = 0; t < 64; ++t) {
+        const uint32_t S1 = rotr(e, 6) ^ rotr(e, 11) ^ rotr(e, 25);
+        const uint32_t ch = (e & f) ^ (~e & g);
+        const uint32_t t1 = hh + kw[t] + S1 + ch;
+        const uint32_t S0 = rotr(a, 2) ^ rotr(a, 13) ^ rotr(a, 22);
+        const uint32_t mj = (a & b) ^ (a & c) ^ (b & c);
+        hh = g;
+        g = f;
+        f = e;
+        e = d + t1;
+        d = c;
+        c = b;
+        b = a;
+        a = t1 + S0 + mj;
+    }
+    h[0] += a; h[1] += b; h[2] += c; h[3] += d;
+    h[4] += e; h[5] += f; h[6] += g; h[7] += hh;
+}
 
 __device__ __forceinline__ uint32_t smem_msg_byte(const WarpSmem& s, const HashParams& P,
                                                   uint32_t hdr, uint32_t len, uint32_t end,
@@ -275,16 +322,14 @@ hash_chains_warp_kernel(const uint32_t* __restrict__ tokens, const ChainDesc* __
             s.w[j] = word;
         }
         __syncwarp();
-        // 4. the serial part: every lane runs the same compressions
+        // 3b. message schedules of all blocks, one lane per block
+        for (uint32_t b = lane; b < nblocks; b += 32) expand_block(s.w + 16 * b, s.kw + 64 * b);
+        __syncwarp();
+        // 4. the serial part: every lane runs the same rounds
         uint32_t h[8] = {0x6a09e667, 0xbb67ae85, 0x3c6ef372, 0xa54ff53a,
                          0x510e527f, 0x9b05688c, 0x1f83d9ab, 0x5be0cd19};
 #pragma unroll 1
-        for (uint32_t b = 0; b < nblocks; ++b) {
-            uint32_t w[16];
-#pragma unroll
-            for (int i = 0; i < 16; ++i) w[i] = s.w[16 * b + i];
-            compress(h, w);
-        }
+        for (uint32_t b = 0; b < nblocks; ++b) compress_kw(h, s.kw + 64 * b);
         __syncwarp();  // all lanes done reading s.w / s.parent of this chunk
         // 5. digest out; it is the next chunk's parent
         if (lane == 0) {

@@ -35,12 +35,12 @@ std::vector<std::vector<Digest>> KeyHasher::hash(const std::vector<TokenSpanView
     std::vector<std::vector<Digest>> out(seqs.size());
     if (total_chunks == 0) return out;
 
-    h_tokens_.reserve(total_tokens * sizeof(TokenId) + 4);
+    // Tokens, chain descriptors and digests live in mapped pinned memory: K3
+    // reads and writes them over PCIe directly (a few KiB per chain), so a
+    // lookup never queues on the copy engines behind in-flight KV transfers.
+    h_tokens_.reserve(total_tokens * sizeof(TokenId) + 64);
     h_chains_.reserve(seqs.size() * sizeof(ChainDesc));
     h_out_.reserve(total_chunks * 32);
-    d_tokens_.reserve(total_tokens * sizeof(TokenId) + 4);
-    d_chains_.reserve(seqs.size() * sizeof(ChainDesc));
-    d_out_.reserve(total_chunks * 32);
 
     auto* tok = reinterpret_cast<TokenId*>(h_tokens_.host);
     auto* ch = reinterpret_cast<ChainDesc*>(h_chains_.host);
@@ -61,15 +61,9 @@ std::vector<std::vector<Digest>> KeyHasher::hash(const std::vector<TokenSpanView
     p.tag_len = uint32_t(tag_.size());
     std::copy(tag_.begin(), tag_.end(), p.tag);
 
-    TKV_CUDA(cudaMemcpyAsync(d_tokens_.ptr, h_tokens_.host, total_tokens * sizeof(TokenId),
-                             cudaMemcpyHostToDevice, stream_));
-    TKV_CUDA(cudaMemcpyAsync(d_chains_.ptr, h_chains_.host, seqs.size() * sizeof(ChainDesc),
-                             cudaMemcpyHostToDevice, stream_));
-    TKV_CUDA(launch_hash_chains(reinterpret_cast<const uint32_t*>(d_tokens_.ptr),
-                                reinterpret_cast<const ChainDesc*>(d_chains_.ptr),
-                                uint32_t(seqs.size()), p, d_out_.ptr, stream_));
-    TKV_CUDA(cudaMemcpyAsync(h_out_.host, d_out_.ptr, total_chunks * 32, cudaMemcpyDeviceToHost,
-                             stream_));
+    TKV_CUDA(launch_hash_chains(reinterpret_cast<const uint32_t*>(h_tokens_.dev),
+                                reinterpret_cast<const ChainDesc*>(h_chains_.dev),
+                                uint32_t(seqs.size()), p, h_out_.dev, stream_));
     TKV_CUDA(cudaStreamSynchronize(stream_));
     ++launches_;
     chunks_ += total_chunks;

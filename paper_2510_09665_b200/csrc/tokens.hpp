@@ -59,8 +59,7 @@ private:
     int device_;
     std::mutex mu_;
     Stream stream_;
-    PinnedBuffer h_tokens_, h_chains_, h_out_;
-    DeviceBuffer d_tokens_, d_chains_, d_out_;
+    PinnedBuffer h_tokens_, h_chains_, h_out_;  // mapped: K3 reads/writes them directly
     uint64_t launches_ = 0, chunks_ = 0;
 };
 
