@@ -64,14 +64,27 @@ def parse():
     ap.add_argument("--staging-depth", type=int, default=2)
     ap.add_argument("--profile-kernels", action="store_true", help="only run the K1/K2 device-resident loop")
     ap.add_argument("--trace", action="store_true", help="host time of every call of one step")
+    ap.add_argument("--no-pd", action="store_true", help="skip the N>=2 PD-over-NVLink pairs")
     return ap.parse_args()
 
 
 def dist_env():
+    """(world, rank, device index). TKV_BENCH_DEVICE pins every rank to one
+    device (single-GPU exercise of the multi-rank paths, with
+    TKV_DIST_BACKEND=gloo since NCCL refuses two ranks on one GPU)."""
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
+    local = int(os.environ.get("TKV_BENCH_DEVICE", os.environ.get("LOCAL_RANK", "0")))
     return world, rank, local
+
+
+def backend():
+    return os.environ.get("TKV_DIST_BACKEND", "nccl")
+
+
+def coll_device(dev):
+    """Where collective tensors live: the GPU for NCCL, the host for gloo."""
+    return dev if backend() == "nccl" else "cpu"
 
 
 def prompt_tokens(n_prefix, n_suffix, step, vocab=128256):
@@ -471,6 +484,92 @@ def kernel_loop(bench, steps, warmup):
             "pre_bytes": pre_bytes, "suf_bytes": suf_bytes, "launches": launches, "mismatch_words": mism}
 
 
+def run_pd_pairs(args, world, rank, local):
+    """Config 5 (N >= 2): prefill ranks [0, N/2) send a 32K-token prompt's KV
+    (70B, TP = N/2 head shards) to decode ranks r + N/2. The prefiller's K1
+    gathers every chunk straight into the decoder's landing buffer (CUDA IPC
+    mapping -> NVLink writes); ordinals go over the process group; the decoder
+    checks the PdStaging contract, lands with one K2 and verifies the bytes
+    on device. Returns per-pair NVLink GB/s (rank 0 aggregates)."""
+    import ctypes as ct
+
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+    from paper_2510_09665_b200._lib import check, lib
+    from paper_2510_09665_b200.api import Engine, PdRecordC, PdStaging, pd_land, pd_send
+    half = world // 2
+    tp = half
+    bpt = args.bpt_full // tp
+    n, L = args.prompt, args.layers
+    chunks = (n + 255) // 256
+    stride = L * 256 * bpt
+    dev = torch.device(f"cuda:{local}")
+    prefill = rank < half
+    peer = rank + half if prefill else rank - half
+    e = Engine(num_layers=L, bpt=bpt, page_tokens=16, tag=TAG, chunk_size=256, ram_slots=2,
+               num_pages=(n // 16 + 16) * L, device=local)
+    prompt = prompt_tokens(n, 0, 999)
+    qid = 5000
+    landing = None
+    handle = np.zeros(64, np.uint8)
+    if not prefill:
+        landing = torch.empty(chunks * stride, dtype=torch.uint8, device=dev)
+        check(lib().tkv_ipc_get_handle(landing.data_ptr(), handle.ctypes.data_as(ct.POINTER(ct.c_uint8))))
+    handles = [None] * world
+    dist.all_gather_object(handles, handle.tobytes())
+    result = {}
+    if prefill:
+        peer_ptr = ct.c_void_p()
+        h = np.frombuffer(handles[peer], np.uint8).copy()
+        check(lib().tkv_ipc_open_handle(h.ctypes.data_as(ct.POINTER(ct.c_uint8)), ct.byref(peer_ptr)))
+        e.bind_pages(qid, n)
+        e.compute_range(qid, prompt, 0, n)  # prefill compute stand-in
+        torch.cuda.synchronize(dev)
+        times = []
+        for it in range(1 + args.steps):
+            torch.cuda.synchronize(dev)
+            t0 = time.perf_counter()
+            recs = pd_send(e, qid, n, peer_ptr.value, stride)
+            dt = time.perf_counter() - t0
+            if it:
+                times.append(dt)
+        meta = torch.tensor([[r.addr - peer_ptr.value, r.bytes, r.token_count, r.first_token] for r in recs],
+                            dtype=torch.int64, device=coll_device(dev))
+        dist.send(meta, dst=peer)
+        lib().tkv_ipc_close(peer_ptr)
+        moved = sum(r.bytes for r in recs)
+        result = {"pair": f"{rank}->{peer}", "gbps": moved / min(times) / 1e9, "bytes": moved,
+                  "ms": 1e3 * min(times)}
+    else:
+        meta = torch.zeros((chunks, 4), dtype=torch.int64, device=coll_device(dev))
+        dist.recv(meta, src=peer)
+        st = PdStaging()
+        assert st.register_query(qid) == 0
+        m = meta.cpu().tolist()
+        order = list(range(chunks))[::-1] + [0]  # out of order + a duplicate
+        for o in order:
+            off, nbytes, cnt, first = m[o]
+            rec = PdRecordC(addr=landing.data_ptr() + off, bytes=nbytes, token_count=cnt, first_token=first)
+            assert st.push(qid, o, o == chunks - 1, rec) == 0
+        rc, landed = st.await_(qid)
+        assert rc == 0 and len(landed) == chunks
+        e.bind_pages(qid, n)
+        torch.cuda.synchronize(dev)
+        t0 = time.perf_counter()
+        pd_land(e, qid, landed)
+        torch.cuda.synchronize(dev)
+        land_ms = 1e3 * (time.perf_counter() - t0)
+        mism = e.verify_range(qid, prompt, 0, n)
+        result = {"pair": f"{peer}->{rank}", "land_ms": land_ms, "mismatch_words": mism}
+    out = [None] * world
+    dist.all_gather_object(out, result)
+    e.close()
+    del landing
+    torch.cuda.empty_cache()
+    return out
+
+
 def run_b200(args):
     import numpy as np  # noqa: F401
     import torch
@@ -478,7 +577,10 @@ def run_b200(args):
 
     world, rank, local = dist_env()
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+        if backend() == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+        else:
+            dist.init_process_group(backend())
     bench = B200Bench(args, world, rank, local)
     peaks = {}
     try:
@@ -496,7 +598,7 @@ def run_b200(args):
     def max_over_ranks(x):
         if world == 1:
             return x
-        t = torch.tensor([x], dtype=torch.float64, device=bench.dev)
+        t = torch.tensor([x], dtype=torch.float64, device=coll_device(bench.dev))
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
@@ -541,6 +643,23 @@ def run_b200(args):
     e2e = e2e_bytes_rank * world / (e2e_ms / 1e3) / 1e9
     tokens_per_s = (loaded + stored) / (e2e_ms / 1e3)
 
+    pd = None
+    if world >= 2 and world % 2 == 0 and not args.no_pd:
+        try:
+            res = run_pd_pairs(args, world, rank, local)
+            sends = [r for r in res if "gbps" in r]
+            lands = [r for r in res if "land_ms" in r]
+            agg = sum(r["gbps"] for r in sends)
+            pd = {"pairs": len(sends), "per_pair_gbps": [round(r["gbps"], 1) for r in sends],
+                  "aggregate_gbps": round(agg, 1), "bytes_per_pair": sends[0]["bytes"],
+                  "land_ms": [round(r["land_ms"], 3) for r in lands],
+                  "mismatch_words": sum(r["mismatch_words"] for r in lands),
+                  "nvlink_peak_gbps_per_direction": 770.0,
+                  "frac_of_peak": round(min(r["gbps"] for r in sends) / 770.0, 4),
+                  "path": "K1 gather into the peer decoder's landing buffer (CUDA IPC, NVLink writes), "
+                          "PdStaging ordinal contract, one K2 land"}
+        except Exception as ex:  # keep the headline line even if PD fails
+            pd = {"error": repr(ex)[:300]}
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         threads = os.cpu_count() or 1
@@ -583,6 +702,8 @@ def run_b200(args):
         "cpu_baseline": cpu,
         "clocks": clk.summary(),
     }
+    if pd is not None:
+        line["pd"] = pd
     print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()

@@ -88,6 +88,45 @@ __global__ void synth_pages_kernel(const PagedLayout L, const SynthArgs A,
     }
 }
 
+// Fast path (16-byte aligned rows, one plane or plane_bytes % 16 == 0): one
+// warp per (layer, position) row computes the row base once and writes or
+// checks two words per lane per step with 16-byte accesses.
+template <bool VERIFY>
+__global__ void __launch_bounds__(256)
+synth_rows_kernel(const PagedLayout L, const SynthArgs A, unsigned long long* mismatches) {
+    const uint32_t lane = threadIdx.x & 31;
+    const uint32_t ntok = A.pos_end - A.pos_begin;
+    const uint64_t rows = uint64_t(A.layer_end - A.layer_begin) * ntok;
+    const uint64_t warps = uint64_t(gridDim.x) * (blockDim.x >> 5);
+    const uint32_t pairs = L.bpt / 16;
+    unsigned long long bad = 0;
+    for (uint64_t row = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; row < rows;
+         row += warps) {
+        const uint32_t layer = A.layer_begin + uint32_t(row / ntok);
+        const uint32_t pos = A.pos_begin + uint32_t(row % ntok);
+        const uint64_t base = row_base(A.seed, A.tokens[pos], layer, pos);
+        for (uint32_t p = lane; p < pairs; p += 32) {
+            const uint32_t i0 = 16 * p;
+            const uint64_t w0 = splitmix64(base + i0), w1 = splitmix64(base + i0 + 8);
+            ulonglong2* dst = reinterpret_cast<ulonglong2*>(row_byte(L, A, layer, pos, i0));
+            if constexpr (VERIFY) {
+                const ulonglong2 v = *dst;
+                bad += (v.x != w0) + (v.y != w1);
+            } else {
+                *dst = make_ulonglong2(w0, w1);
+            }
+        }
+    }
+    if constexpr (VERIFY) {
+        if (bad) atomicAdd(mismatches, bad);
+    }
+}
+
+bool rows_fast(const PagedLayout& L) {
+    return L.bpt % 16 == 0 && L.plane_bytes % 16 == 0 && L.token_stride % 16 == 0 &&
+           L.page_stride % 16 == 0 && L.plane_stride % 16 == 0 && L.base % 16 == 0;
+}
+
 __global__ void synth_chunk_kernel(const uint32_t* __restrict__ tokens, uint64_t seed,
                                    uint32_t start, uint32_t n, uint32_t n_layers, uint32_t bpt,
                                    uint8_t* __restrict__ out) {
@@ -123,7 +162,12 @@ cudaError_t launch_synth_pages(const PagedLayout& L, const SynthArgs& A, cudaStr
     const uint64_t total =
         uint64_t(A.layer_end - A.layer_begin) * (A.pos_end - A.pos_begin) * ((L.bpt + 7) / 8);
     note_launch();
-    synth_pages_kernel<false><<<grid_for(total), 256, 0, s>>>(L, A, nullptr);
+    if (rows_fast(L)) {
+        const uint64_t rows = uint64_t(A.layer_end - A.layer_begin) * (A.pos_end - A.pos_begin);
+        synth_rows_kernel<false><<<grid_for(rows * 32), 256, 0, s>>>(L, A, nullptr);
+    } else {
+        synth_pages_kernel<false><<<grid_for(total), 256, 0, s>>>(L, A, nullptr);
+    }
     return cudaGetLastError();
 }
 
@@ -133,7 +177,12 @@ cudaError_t launch_verify_pages(const PagedLayout& L, const SynthArgs& A,
     const uint64_t total =
         uint64_t(A.layer_end - A.layer_begin) * (A.pos_end - A.pos_begin) * ((L.bpt + 7) / 8);
     note_launch();
-    synth_pages_kernel<true><<<grid_for(total), 256, 0, s>>>(L, A, mismatches);
+    if (rows_fast(L)) {
+        const uint64_t rows = uint64_t(A.layer_end - A.layer_begin) * (A.pos_end - A.pos_begin);
+        synth_rows_kernel<true><<<grid_for(rows * 32), 256, 0, s>>>(L, A, mismatches);
+    } else {
+        synth_pages_kernel<true><<<grid_for(total), 256, 0, s>>>(L, A, mismatches);
+    }
     return cudaGetLastError();
 }
 
