@@ -148,6 +148,24 @@ int tkv_verify_pages(const tkv_paged_layout* layout, const uint32_t* tokens_dev,
 int tkv_synth_chunk(const uint32_t* tokens_dev, uint64_t seed, uint32_t start, uint32_t n,
                     uint32_t n_layers, uint32_t bpt, uint8_t* out_dev, void* stream);
 
+/* q8-scale codec (Q8ScaleCodec, src/codec.cpp:27-91), bit-exact, over a
+ * batch of payloads. Encode: src = payload, dst = blob, bytes = payload
+ * length; blob = u32 len | f32 scale | int8 lanes | odd tail byte
+ * (tkv_q8_blob_bytes). Decode: src = blob, dst = payload, bytes = original
+ * length. seg_base (n+1 entries) comes from tkv_codec_plan; maxabs_dev is
+ * n ints of scratch. */
+typedef struct tkv_codec_item {
+    const uint8_t* src_dev;
+    uint8_t* dst_dev;
+    uint64_t bytes;
+} tkv_codec_item;
+uint64_t tkv_q8_blob_bytes(uint64_t payload_bytes);
+int tkv_codec_plan(const tkv_codec_item* items, uint32_t n, uint32_t* seg_base_out);
+int tkv_q8_encode(const tkv_codec_item* items_dev, const uint32_t* seg_base_dev, uint32_t n,
+                  uint32_t total_segs, int* maxabs_dev, void* stream);
+int tkv_q8_decode(const tkv_codec_item* items_dev, const uint32_t* seg_base_dev, uint32_t n,
+                  uint32_t total_segs, void* stream);
+
 /* ========================================================================== *
  * 2. Object level
  * ========================================================================== */
@@ -213,6 +231,17 @@ int tkv_store_clear(tkv_store* s, const uint8_t* digests, size_t n, size_t* remo
                     size_t* refused);
 /* entries, ram_slots_total, ram_slots_used, ram_entries */
 int tkv_store_stats(tkv_store* s, size_t out[4]);
+/* LMCK records (chunk_file.hpp:12-56): export a present chunk / import a
+ * record (checksum + geometry verified; corrupt_chunk / invalid_argument as
+ * the reference). tkv_model_tag_hash = first 8 LE bytes of SHA-256(tag)
+ * (hash.cpp:41-44), computed on the device. tkv_record_peek reads the
+ * header: digest, {token_count, num_layers, bytes_per_token}, tag hash. */
+int tkv_model_tag_hash(const char* tag, uint64_t* out);
+int tkv_store_export_record(tkv_store* s, const uint8_t* digest, uint64_t model_tag_hash,
+                            uint8_t* out, size_t cap, size_t* n);
+int tkv_store_import_record(tkv_store* s, const uint8_t* record, size_t n, int pin);
+int tkv_record_peek(const uint8_t* record, size_t n, uint8_t* digest_out, uint32_t* geometry3,
+                    uint64_t* model_tag_hash);
 
 /* ---- Connector (include/tierkv/connector.hpp:74-152) --------------------- */
 typedef struct tkv_connector tkv_connector;
@@ -227,6 +256,7 @@ typedef struct tkv_connector_config {
     int store_ctas;              /* K1 grid for zero-copy stores (0 = default) */
     int load_ctas;               /* K2 grid (0 = 2 x SMs) */
     void* engine_stream;         /* stream the engine computes on */
+    size_t memo_entries;         /* device prefix-digest memo links (0 = off) */
 } tkv_connector_config;
 void tkv_connector_config_default(tkv_connector_config* cfg);
 int tkv_connector_create(tkv_store* s, tkv_pages* p, const tkv_connector_config* cfg,
@@ -250,6 +280,8 @@ int tkv_connector_append_decode(tkv_connector* c, uint64_t query, uint32_t token
 int tkv_connector_finish_query(tkv_connector* c, uint64_t query, uint8_t* digests_out, size_t cap,
                                size_t* n);
 size_t tkv_connector_staging_peak(tkv_connector* c);
+/* Prefix-digest memo counters: hits, misses (chunk links), capacity, resets. */
+int tkv_connector_memo_stats(tkv_connector* c, uint64_t out[4]);
 uint64_t tkv_connector_hash_launches(tkv_connector* c);
 
 void tkv_meta_destroy(tkv_meta* m);

@@ -72,6 +72,10 @@ class _COracle:
                                             ct.c_size_t, _u8p]
         lib.tkvo_synth_chunk.argtypes = [ct.c_uint64, _u32p, ct.c_size_t, ct.c_size_t, ct.c_uint32,
                                          ct.c_size_t, _u8p]
+        lib.tkvo_q8_encode.argtypes = [_u8p, ct.c_size_t, _u8p]
+        lib.tkvo_q8_encode.restype = ct.c_size_t
+        lib.tkvo_q8_decode.argtypes = [_u8p, ct.c_size_t, _u8p]
+        lib.tkvo_q8_decode.restype = ct.c_size_t
         lib.tkvo_gather_tokens.argtypes = [_u8p, ct.c_size_t, _u32p, ct.c_size_t, ct.c_size_t, ct.c_size_t, _u8p]
         lib.tkvo_scatter_tokens.argtypes = [_u8p, ct.c_size_t, _u32p, ct.c_size_t, ct.c_size_t, ct.c_size_t, _u8p]
         self.lib = lib
@@ -137,6 +141,23 @@ class _COracle:
         out = np.zeros(num_layers * n * bpt, np.uint8)
         self.lib.tkvo_synth_chunk(seed, _ptr(t, _u32p), start, n, num_layers, bpt, _ptr(out, _u8p))
         return out
+
+    def q8_encode(self, payload: np.ndarray) -> np.ndarray:
+        p = np.ascontiguousarray(payload, np.uint8)
+        out = np.zeros(8 + p.size // 2 + (p.size & 1), np.uint8)
+        n = self.lib.tkvo_q8_encode(_ptr(p, _u8p), p.size, _ptr(out, _u8p))
+        return out[:n]
+
+    def q8_decode(self, blob: np.ndarray) -> np.ndarray | None:
+        b = np.ascontiguousarray(blob, np.uint8)
+        if b.size < 8:
+            return None
+        length = int(b[:4].view(np.uint32)[0])
+        out = np.zeros(max(1, length), np.uint8)
+        n = self.lib.tkvo_q8_decode(_ptr(b, _u8p), b.size, _ptr(out, _u8p))
+        if n != length or (n == 0 and b.size != 8):  # malformed blob
+            return None
+        return out[:length]
 
     def gather_tokens(self, pool: np.ndarray, page_bytes: int, pages, bpt: int, token_count: int) -> np.ndarray:
         p = _tokens(pages)

@@ -12,6 +12,8 @@
 #include <string>
 #include <vector>
 
+#include "tierkv/chunk_file.hpp"
+#include "tierkv/codec.hpp"
 #include "tierkv/connector.hpp"
 #include "tierkv/hash.hpp"
 #include "tierkv/paged_store.hpp"
@@ -96,6 +98,46 @@ void ref_synth_layer_kv(uint64_t seed, const uint32_t* tokens, size_t n, uint32_
                         uint64_t first_pos, uint32_t bpt, uint8_t* out) {
     synth_layer_kv(seed, TokenSpanView(tokens, n), layer, first_pos, bpt,
                    MutByteSpan(out, n * size_t(bpt)));
+}
+
+// --- codec.hpp: Q8ScaleCodec ---------------------------------------------------
+
+size_t ref_q8_encode(const uint8_t* payload, size_t n, uint8_t* out) {
+    auto blob = q8_scale_codec().encode(ByteSpan(payload, n));
+    std::memcpy(out, blob.data(), blob.size());
+    return blob.size();
+}
+
+// Returns the payload size, or 0 when decode fails (writes Errc to *code).
+size_t ref_q8_decode(const uint8_t* blob, size_t n, uint8_t* out, int* code) {
+    auto r = q8_scale_codec().decode(ByteSpan(blob, n));
+    *code = int(r.code());
+    if (!r.ok()) return 0;
+    std::memcpy(out, r.value().data(), r.value().size());
+    return r.value().size();
+}
+
+// --- chunk_file.hpp: LMCK records --------------------------------------------
+
+size_t ref_encode_record(const char* tag, const uint8_t* digest, uint32_t token_count,
+                         uint32_t layers, uint32_t bpt, const uint8_t* payload, uint8_t* out) {
+    ChunkKey key;
+    std::memcpy(key.digest.data(), digest, 32);
+    key.model_tag = tag;
+    const size_t n = size_t(token_count) * layers * bpt;
+    KVChunk c = KVChunk::from_payload(key, token_count, layers, bpt,
+                                      std::vector<uint8_t>(payload, payload + n));
+    auto rec = encode_chunk_record(c);
+    std::memcpy(out, rec.data(), rec.size());
+    return rec.size();
+}
+
+// Errc of parse_chunk_record (0 = ok); payload copied to out when ok.
+int ref_parse_record(const uint8_t* rec, size_t n, uint8_t* out) {
+    auto r = parse_chunk_record(ByteSpan(rec, n));
+    if (!r.ok()) return int(r.code());
+    std::memcpy(out, r.value().payload().data(), r.value().payload().size());
+    return 0;
 }
 
 // --- engine stack (store + pages + connector) -------------------------------

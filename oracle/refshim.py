@@ -40,6 +40,10 @@ class _Ref:
             "ref_fnv1a64": (ct.c_uint64, [_u8p, _sz]),
             "ref_model_seed": (ct.c_uint64, [ct.c_char_p]),
             "ref_synth_layer_kv": (None, [ct.c_uint64, _u32p, _sz, ct.c_uint32, ct.c_uint64, ct.c_uint32, _u8p]),
+            "ref_encode_record": (_sz, [ct.c_char_p, _u8p, ct.c_uint32, ct.c_uint32, ct.c_uint32, _u8p, _u8p]),
+            "ref_parse_record": (ct.c_int, [_u8p, _sz, _u8p]),
+            "ref_q8_encode": (_sz, [_u8p, _sz, _u8p]),
+            "ref_q8_decode": (_sz, [_u8p, _sz, _u8p, ct.POINTER(ct.c_int)]),
             "ref_engine_create": (_vp, [ct.c_uint32, ct.c_uint32, ct.c_uint32, ct.c_char_p, _sz, _sz, _sz,
                                         ct.c_uint32, ct.c_int, _sz, _sz, ct.c_int]),
             "ref_engine_destroy": (None, [_vp]),
@@ -124,6 +128,36 @@ class _Ref:
         self.lib.ref_synth_layer_kv(seed, t.ctypes.data_as(_u32p), t.size, layer, first_pos, bpt,
                                     out.ctypes.data_as(_u8p))
         return out
+
+    def encode_record(self, tag: str, digest: bytes, token_count: int, layers: int, bpt: int,
+                      payload: np.ndarray) -> np.ndarray:
+        p = np.ascontiguousarray(payload, np.uint8)
+        d = np.frombuffer(digest, np.uint8).copy()
+        out = np.zeros(52 + p.size + 8, np.uint8)
+        n = self.lib.ref_encode_record(tag.encode(), d.ctypes.data_as(_u8p), token_count, layers, bpt,
+                                       p.ctypes.data_as(_u8p), out.ctypes.data_as(_u8p))
+        return out[:n]
+
+    def parse_record(self, rec: np.ndarray, payload_bytes: int):
+        r = np.ascontiguousarray(rec, np.uint8)
+        out = np.zeros(max(1, payload_bytes), np.uint8)
+        code = self.lib.ref_parse_record(r.ctypes.data_as(_u8p), r.size, out.ctypes.data_as(_u8p))
+        return code, out[:payload_bytes]
+
+    def q8_encode(self, payload: np.ndarray) -> np.ndarray:
+        p = np.ascontiguousarray(payload, np.uint8)
+        out = np.zeros(8 + p.size // 2 + (p.size & 1), np.uint8)
+        n = self.lib.ref_q8_encode(p.ctypes.data_as(_u8p), p.size, out.ctypes.data_as(_u8p))
+        return out[:n]
+
+    def q8_decode(self, blob: np.ndarray):
+        """(payload or None, Errc code)."""
+        b = np.ascontiguousarray(blob, np.uint8)
+        length = int(b[:4].view(np.uint32)[0]) if b.size >= 4 else 0
+        out = np.zeros(max(1, length), np.uint8)
+        code = ct.c_int(0)
+        n = self.lib.ref_q8_decode(b.ctypes.data_as(_u8p), b.size, out.ctypes.data_as(_u8p), ct.byref(code))
+        return (out[:n] if code.value == 0 else None), code.value
 
 
 _ref_singleton: _Ref | None = None

@@ -3,6 +3,7 @@
  * pin. Plain C99, single-threaded, no dependencies. */
 #include "tierkv_oracle.h"
 
+#include <math.h>
 #include <stdlib.h>
 #include <string.h>
 
@@ -205,6 +206,60 @@ void tkvo_synth_chunk(uint64_t seed, const uint32_t* prompt, size_t start, size_
                       uint32_t num_layers, size_t bpt, uint8_t* out) {
     for (uint32_t l = 0; l < num_layers; ++l)
         tkvo_synth_layer_kv(seed, prompt + start, n, l, start, bpt, out + (size_t)l * n * bpt);
+}
+
+/* ---- q8-scale codec (src/codec.cpp:27-94) ------------------------------ */
+
+static int16_t q8_lane(const uint8_t* p, size_t i) {
+    return (int16_t)(uint16_t)(p[2 * i] | ((uint16_t)p[2 * i + 1] << 8));
+}
+
+size_t tkvo_q8_encode(const uint8_t* payload, size_t n, uint8_t* blob) {
+    size_t lanes = n / 2;
+    int32_t max_abs = 0;
+    for (size_t i = 0; i < lanes; ++i) {
+        int32_t v = q8_lane(payload, i);
+        if (v < 0) v = -v;
+        if (v > max_abs) max_abs = v;
+    }
+    float scale = (float)((double)max_abs / 127.0);
+    uint32_t len = (uint32_t)n, sb;
+    memcpy(&sb, &scale, 4);
+    for (int i = 0; i < 4; ++i) {
+        blob[i] = (uint8_t)(len >> (8 * i));
+        blob[4 + i] = (uint8_t)(sb >> (8 * i));
+    }
+    for (size_t i = 0; i < lanes; ++i) {
+        double q = scale > 0 ? round((double)q8_lane(payload, i) / scale) : 0.0;
+        if (q > 127.0) q = 127.0;
+        if (q < -127.0) q = -127.0;
+        blob[8 + i] = (uint8_t)(int8_t)q;
+    }
+    if (n & 1) blob[8 + lanes] = payload[n - 1];
+    return 8 + lanes + (n & 1);
+}
+
+size_t tkvo_q8_decode(const uint8_t* blob, size_t n, uint8_t* payload) {
+    if (n < 8) return 0;
+    uint32_t len = 0, sb = 0;
+    for (int i = 3; i >= 0; --i) {
+        len = (len << 8) | blob[i];
+        sb = (sb << 8) | blob[4 + i];
+    }
+    float scale;
+    memcpy(&scale, &sb, 4);
+    size_t lanes = len / 2;
+    if (n != 8 + lanes + (len & 1)) return 0;
+    for (size_t i = 0; i < lanes; ++i) {
+        double v = round((double)(int8_t)blob[8 + i] * (double)scale);
+        if (v > 32767.0) v = 32767.0;
+        if (v < -32768.0) v = -32768.0;
+        uint16_t lane = (uint16_t)(int16_t)v;
+        payload[2 * i] = (uint8_t)(lane & 0xff);
+        payload[2 * i + 1] = (uint8_t)(lane >> 8);
+    }
+    if (len & 1) payload[len - 1] = blob[n - 1];
+    return len;
 }
 
 /* ---- paged data movement (src/paged_store.cpp:123-175) ----------------- */

@@ -63,6 +63,12 @@ void tkvo_gather_tokens(const uint8_t* pool, size_t page_bytes, const uint32_t* 
 void tkvo_scatter_tokens(uint8_t* pool, size_t page_bytes, const uint32_t* pages, size_t n_pages,
                          size_t bpt, size_t token_count, const uint8_t* in);
 
+/* Q8ScaleCodec, src/codec.cpp:27-94: blob = u32le len | f32le scale |
+ * int8 lanes | raw odd tail. Returns bytes written (encode) / 0 on a
+ * malformed blob (decode writes `len` payload bytes). */
+size_t tkvo_q8_encode(const uint8_t* payload, size_t n, uint8_t* blob);
+size_t tkvo_q8_decode(const uint8_t* blob, size_t n, uint8_t* payload);
+
 #ifdef __cplusplus
 }
 #endif

@@ -47,7 +47,11 @@ class ConnectorConfigC(ct.Structure):
     _fields_ = [("layerwise", ct.c_int), ("pin_stores", ct.c_int), ("staging_budget_bytes", ct.c_size_t),
                 ("staging_depth", ct.c_uint32), ("load_zero_copy", ct.c_int), ("store_zero_copy", ct.c_int),
                 ("store_ctas", ct.c_int),
-                ("load_ctas", ct.c_int), ("engine_stream", ct.c_void_p)]
+                ("load_ctas", ct.c_int), ("engine_stream", ct.c_void_p), ("memo_entries", ct.c_size_t)]
+
+
+class CodecItemC(ct.Structure):
+    _fields_ = [("src_dev", ct.c_void_p), ("dst_dev", ct.c_void_p), ("bytes", ct.c_uint64)]
 
 
 class PdRecordC(ct.Structure):
@@ -73,6 +77,10 @@ SIGNATURES = {
     "tkv_verify_pages": (ct.c_int, [ct.POINTER(PagedLayoutC), vp, vp, ct.c_uint32, ct.c_uint64, ct.c_uint32,
                                     ct.c_uint32, ct.c_uint32, ct.c_uint32, vp, vp]),
     "tkv_synth_chunk": (ct.c_int, [vp, ct.c_uint64, ct.c_uint32, ct.c_uint32, ct.c_uint32, ct.c_uint32, vp, vp]),
+    "tkv_q8_blob_bytes": (ct.c_uint64, [ct.c_uint64]),
+    "tkv_codec_plan": (ct.c_int, [vp, ct.c_uint32, u32p]),
+    "tkv_q8_encode": (ct.c_int, [vp, vp, ct.c_uint32, ct.c_uint32, vp, vp]),
+    "tkv_q8_decode": (ct.c_int, [vp, vp, ct.c_uint32, ct.c_uint32, vp]),
     "tkv_chunk_keys": (ct.c_int, [ct.c_char_p, sz, u32p, sz, u8p, szp]),
     "tkv_keychain_next": (ct.c_int, [ct.c_char_p, sz, u8p, u32p, sz, u8p]),
     "tkv_pages_create": (ct.c_int, [ct.POINTER(ModelSpecC), ct.c_uint32, ct.c_int, ct.POINTER(vp)]),
@@ -103,6 +111,10 @@ SIGNATURES = {
     "tkv_store_pin": (ct.c_int, [vp, u8p, ct.c_int]),
     "tkv_store_clear": (ct.c_int, [vp, u8p, sz, szp, szp]),
     "tkv_store_stats": (ct.c_int, [vp, szp]),
+    "tkv_model_tag_hash": (ct.c_int, [ct.c_char_p, u64p]),
+    "tkv_store_export_record": (ct.c_int, [vp, u8p, ct.c_uint64, u8p, sz, szp]),
+    "tkv_store_import_record": (ct.c_int, [vp, u8p, sz, ct.c_int]),
+    "tkv_record_peek": (ct.c_int, [u8p, sz, u8p, u32p, u64p]),
     "tkv_connector_config_default": (None, [ct.POINTER(ConnectorConfigC)]),
     "tkv_connector_create": (ct.c_int, [vp, vp, ct.POINTER(ConnectorConfigC), ct.POINTER(vp)]),
     "tkv_connector_destroy": (None, [vp]),
@@ -118,6 +130,7 @@ SIGNATURES = {
     "tkv_connector_append_decode": (ct.c_int, [vp, ct.c_uint64, ct.c_uint32]),
     "tkv_connector_finish_query": (ct.c_int, [vp, ct.c_uint64, u8p, sz, szp]),
     "tkv_connector_staging_peak": (sz, [vp]),
+    "tkv_connector_memo_stats": (ct.c_int, [vp, u64p]),
     "tkv_connector_hash_launches": (ct.c_uint64, [vp]),
     "tkv_meta_destroy": (None, [vp]),
     "tkv_meta_layerwise": (ct.c_int, [vp]),

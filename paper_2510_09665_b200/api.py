@@ -80,7 +80,8 @@ class Engine:
                  io_threads: int = 2, store_io_threads: int = 4, pin_stores: bool = False,
                  staging_depth: int = 2, load_zero_copy: bool = False, store_zero_copy: bool = False,
                  store_ctas: int = 0,
-                 load_ctas: int = 0, device: int = 0, stream: torch.cuda.Stream | None = None):
+                 load_ctas: int = 0, device: int = 0, stream: torch.cuda.Stream | None = None,
+                 memo_entries: int | None = None):
         del io_threads, store_io_threads  # host thread pools do not exist on this path
         self.L = lib()
         self.num_layers, self.bpt, self.page_tokens = num_layers, bpt, page_tokens
@@ -108,6 +109,8 @@ class Engine:
             cfg.store_ctas = store_ctas
         cfg.load_ctas = load_ctas
         cfg.engine_stream = self.stream_handle
+        if memo_entries is not None:
+            cfg.memo_entries = memo_entries
         check(self.L.tkv_connector_create(self.store, self.pages, ct.byref(cfg), ct.byref(self.conn)))
         self._metas: list[ct.c_void_p | None] = []
         self._dev_prompts: dict[int, torch.Tensor] = {}
@@ -323,6 +326,11 @@ class Engine:
     def hash_launches(self) -> int:
         return int(self.L.tkv_connector_hash_launches(self.conn))
 
+    def memo_stats(self) -> dict:
+        out = (ct.c_uint64 * 4)()
+        check(self.L.tkv_connector_memo_stats(self.conn, out))
+        return {"hits": out[0], "misses": out[1], "capacity": out[2], "resets": out[3]}
+
     # --- store ---
     def contains(self, digest: bytes) -> bool:
         d = _u8(digest)
@@ -362,6 +370,37 @@ class Engine:
         stride = ct.c_uint32(0)
         check(self.L.tkv_pages_device_table(self.pages, qid, self.stream_handle, ct.byref(ptr), ct.byref(stride)))
         return ptr.value, stride.value
+
+
+def _codec_launch(fn, srcs, dsts, sizes, with_scratch: bool, stream=None):
+    from ._lib import CodecItemC
+    items = (CodecItemC * len(srcs))(*[CodecItemC(s.data_ptr(), d.data_ptr(), n) for s, d, n in zip(srcs, dsts, sizes)])
+    seg = np.zeros(len(srcs) + 1, np.uint32)
+    check(lib().tkv_codec_plan(ct.cast(items, ct.c_void_p), len(srcs), seg.ctypes.data_as(u32p)))
+    dev = srcs[0].device
+    d_items = torch.frombuffer(bytearray(bytes(items)), dtype=torch.uint8).to(dev)
+    d_seg = torch.from_numpy(seg.view(np.int32)).to(dev)
+    s = stream.cuda_stream if stream is not None else torch.cuda.current_stream(dev).cuda_stream
+    if with_scratch:
+        scratch = torch.zeros(len(srcs), dtype=torch.int32, device=dev)
+        check(fn(d_items.data_ptr(), d_seg.data_ptr(), len(srcs), int(seg[-1]), scratch.data_ptr(), s))
+    else:
+        check(fn(d_items.data_ptr(), d_seg.data_ptr(), len(srcs), int(seg[-1]), s))
+    torch.cuda.synchronize(dev)
+
+
+def q8_encode(payloads: list[torch.Tensor]) -> list[torch.Tensor]:
+    """q8-scale blobs of device uint8 payloads, one batched launch (codec.cpp:27-91)."""
+    blobs = [torch.empty(int(lib().tkv_q8_blob_bytes(p.numel())), dtype=torch.uint8, device=p.device)
+             for p in payloads]
+    _codec_launch(lib().tkv_q8_encode, payloads, blobs, [p.numel() for p in payloads], True)
+    return blobs
+
+
+def q8_decode(blobs: list[torch.Tensor], lengths: list[int]) -> list[torch.Tensor]:
+    outs = [torch.empty(n, dtype=torch.uint8, device=b.device) for b, n in zip(blobs, lengths)]
+    _codec_launch(lib().tkv_q8_decode, blobs, outs, lengths, False)
+    return outs
 
 
 class PdStaging:

@@ -11,6 +11,7 @@
 #include "kernels.hpp"
 #include "paged_store.hpp"
 #include "pd.hpp"
+#include "record.hpp"
 #include "store.hpp"
 #include "tokens.hpp"
 
@@ -212,6 +213,30 @@ int tkv_synth_chunk(const uint32_t* tokens, uint64_t seed, uint32_t start, uint3
     return cuda(launch_synth_chunk(tokens, seed, start, n, n_layers, bpt, out, cudaStream_t(stream)));
 }
 
+// ---- q8 codec -----------------------------------------------------------------
+
+static_assert(sizeof(tkv_codec_item) == sizeof(CodecItem));
+
+uint64_t tkv_q8_blob_bytes(uint64_t payload) { return q8_blob_bytes(payload); }
+
+int tkv_codec_plan(const tkv_codec_item* items, uint32_t n, uint32_t* seg_base) {
+    seg_base[0] = 0;
+    for (uint32_t i = 0; i < n; ++i) seg_base[i + 1] = seg_base[i] + codec_segments(items[i].bytes);
+    return 0;
+}
+
+int tkv_q8_encode(const tkv_codec_item* items, const uint32_t* seg_base, uint32_t n, uint32_t segs,
+                  int* maxabs, void* stream) {
+    return cuda(launch_q8_encode(reinterpret_cast<const CodecItem*>(items), seg_base, n, segs, maxabs,
+                                 cudaStream_t(stream)));
+}
+
+int tkv_q8_decode(const tkv_codec_item* items, const uint32_t* seg_base, uint32_t n, uint32_t segs,
+                  void* stream) {
+    return cuda(launch_q8_decode(reinterpret_cast<const CodecItem*>(items), seg_base, n, segs,
+                                 cudaStream_t(stream)));
+}
+
 // ---- keys -------------------------------------------------------------------
 
 int tkv_chunk_keys(const char* tag, size_t cs, const uint32_t* tokens, size_t n, uint8_t* out,
@@ -411,6 +436,44 @@ int tkv_store_stats(tkv_store* s, size_t out[4]) {
     return 0;
 }
 
+int tkv_model_tag_hash(const char* tag, uint64_t* out) {
+    return guard([&] {
+        const size_t n = std::strlen(tag);
+        PinnedBuffer buf(n + 32 + 16);
+        std::memcpy(buf.host, tag, n);
+        TKV_CUDA(launch_sha256_bytes(buf.dev, uint32_t(n), buf.dev + ((n + 15) & ~size_t(15)), nullptr));
+        TKV_CUDA(cudaStreamSynchronize(nullptr));
+        const uint8_t* d = buf.host + ((n + 15) & ~size_t(15));
+        uint64_t v = 0;
+        for (int i = 7; i >= 0; --i) v = (v << 8) | d[i];
+        *out = v;
+        return 0;
+    });
+}
+int tkv_store_export_record(tkv_store* s, const uint8_t* digest, uint64_t tag_hash, uint8_t* out,
+                            size_t cap, size_t* n) {
+    return guard([&] {
+        auto r = s->s->export_record(to_digest(digest), tag_hash);
+        if (!r.ok()) return st(r.status());
+        *n = r.value().size();
+        if (out && r.value().size() <= cap) std::memcpy(out, r.value().data(), r.value().size());
+        return 0;
+    });
+}
+int tkv_store_import_record(tkv_store* s, const uint8_t* record, size_t n, int pin) {
+    return guard([&] { return st(s->s->import_record(record, n, pin != 0)); });
+}
+int tkv_record_peek(const uint8_t* record, size_t n, uint8_t* digest, uint32_t* geo, uint64_t* tag_hash) {
+    auto r = peek_record(record, n);
+    if (!r.ok()) return st(r.status());
+    std::memcpy(digest, r.value().digest.data(), 32);
+    geo[0] = r.value().token_count;
+    geo[1] = r.value().num_layers;
+    geo[2] = r.value().bytes_per_token;
+    *tag_hash = r.value().model_tag_hash;
+    return 0;
+}
+
 // ---- connector --------------------------------------------------------------
 
 void tkv_connector_config_default(tkv_connector_config* cfg) {
@@ -424,6 +487,7 @@ void tkv_connector_config_default(tkv_connector_config* cfg) {
     cfg->store_ctas = d.store_ctas;
     cfg->load_ctas = d.load_ctas;
     cfg->engine_stream = d.engine_stream;
+    cfg->memo_entries = d.memo_entries;
 }
 
 int tkv_connector_create(tkv_store* s, tkv_pages* p, const tkv_connector_config* cfg,
@@ -440,6 +504,7 @@ int tkv_connector_create(tkv_store* s, tkv_pages* p, const tkv_connector_config*
             c.store_ctas = cfg->store_ctas > 0 ? cfg->store_ctas : c.store_ctas;
             c.load_ctas = cfg->load_ctas;
             c.engine_stream = cudaStream_t(cfg->engine_stream);
+            c.memo_entries = cfg->memo_entries;
         }
         auto* h = new tkv_connector;
         h->c = std::make_unique<Connector>(*s->s, *p->p, c);
@@ -511,6 +576,16 @@ int tkv_connector_finish_query(tkv_connector* c, uint64_t q, uint8_t* out, size_
     });
 }
 size_t tkv_connector_staging_peak(tkv_connector* c) { return c->c->staging_peak_bytes(); }
+int tkv_connector_memo_stats(tkv_connector* c, uint64_t out[4]) {
+    return guard([&] {
+        auto s = c->c->hasher().memo_stats();
+        out[0] = s.hits;
+        out[1] = s.misses;
+        out[2] = s.capacity;
+        out[3] = s.resets;
+        return 0;
+    });
+}
 uint64_t tkv_connector_hash_launches(tkv_connector* c) { return c->c->hasher().launches(); }
 
 // ---- PD -----------------------------------------------------------------------

@@ -184,6 +184,7 @@ Connector::Connector(TieredStore& store, PagedKVStore& pages, Config cfg)
     load_stream_ = Stream::create();
     store_stream_ = Stream::create();
     d2h_stream_ = Stream::create();
+    hasher_.enable_memo(cfg_.memo_entries);
 }
 
 Connector::Connector(TieredStore& store, PagedKVStore& pages) : Connector(store, pages, Config{}) {}

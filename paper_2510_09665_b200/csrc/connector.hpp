@@ -98,6 +98,7 @@ public:
         int store_ctas = 64;             // zero-copy K1 grid (PCIe-bound)
         int load_ctas = 0;               // K2 grid (0 = 2 x SMs)
         cudaStream_t engine_stream = nullptr;
+        size_t memo_entries = 65536;     // prefix-digest memo links on the device (0 = off)
     };
 
     Connector(TieredStore& store, PagedKVStore& pages, Config cfg);

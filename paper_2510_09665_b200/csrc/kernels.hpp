@@ -95,8 +95,44 @@ struct HashParams {
     uint8_t tag[kMaxTagBytes] = {};
 };
 
+// Prefix-digest memo: a device hash table
+// (parent digest, chunk tokens) -> digest. A probe that matches the key is
+// verified exactly — parent words, token count and every token — so a hit
+// returns the digest the SHA chain would have produced; misses are hashed
+// and inserted by the same launch. Slot word = (tag40 << 24) | entry index;
+// entry = parent[8] | digest[8] | n | tokens[chunk_size] (u32 words).
+struct MemoView {
+    unsigned long long* slots = nullptr;  // [slot_mask + 1], 0 = empty
+    uint32_t* entries = nullptr;          // [entry_cap][entry_words]
+    unsigned int* counter = nullptr;      // next free entry
+    uint32_t slot_mask = 0;
+    uint32_t entry_cap = 0;               // <= 2^24
+    uint32_t entry_words = 0;             // 17 + chunk_size
+    unsigned long long* stats = nullptr;  // [0] hits, [1] misses (optional)
+};
+
 cudaError_t launch_hash_chains(const uint32_t* tokens, const ChainDesc* chains, uint32_t n_chains,
-                               const HashParams& params, uint8_t* out, cudaStream_t stream);
+                               const HashParams& params, uint8_t* out, cudaStream_t stream,
+                               const MemoView* memo = nullptr);
+// SHA-256 of n bytes (one thread; for the model tag hash, hash.cpp:41-44).
+cudaError_t launch_sha256_bytes(const uint8_t* data, uint32_t n, uint8_t* out, cudaStream_t stream);
+
+// ---------------------------------------------------------------------------
+// q8-scale codec (src/codec.cpp:27-91) over a batch of chunk payloads.
+// Encode: src = payload, dst = blob (8 + bytes/2 + bytes%2), bytes = payload
+// length. Decode: src = blob, dst = payload, bytes = original length.
+// seg_base = prefix over items of codec_segments(bytes) (n + 1 entries).
+struct CodecItem {
+    const uint8_t* src = nullptr;
+    uint8_t* dst = nullptr;
+    uint64_t bytes = 0;
+};
+uint32_t codec_segments(uint64_t bytes);
+inline uint64_t q8_blob_bytes(uint64_t payload) { return 8 + payload / 2 + (payload & 1); }
+cudaError_t launch_q8_encode(const CodecItem* items, const uint32_t* seg_base, uint32_t n_items,
+                             uint32_t total_segs, int* maxabs, cudaStream_t stream);
+cudaError_t launch_q8_decode(const CodecItem* items, const uint32_t* seg_base, uint32_t n_items,
+                             uint32_t total_segs, cudaStream_t stream);
 
 // ---------------------------------------------------------------------------
 // K4: synthetic KV (synth_token_kv, src/synth.cpp:7-20) written straight into

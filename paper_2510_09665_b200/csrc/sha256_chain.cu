@@ -254,9 +254,78 @@ __device__ __forceinline__ uint32_t smem_msg_byte(const WarpSmem& s, const HashP
     return 0;
 }
 
+// ---- prefix-digest memo helpers (warp-cooperative) --------------------------
+
+__device__ __forceinline__ uint64_t mix64(uint64_t x) {
+    x += 0x9e3779b97f4a7c15ull;
+    x = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ull;
+    x = (x ^ (x >> 27)) * 0x94d049bb133111ebull;
+    return x ^ (x >> 31);
+}
+
+// Same value in every lane: fingerprint of (parent, n, tokens). Only a probe
+// key — a hit is confirmed by comparing parent, n and every token.
+__device__ __forceinline__ uint64_t memo_key(const WarpSmem& s, uint32_t n, uint32_t lane) {
+    uint64_t h = 0;
+    for (uint32_t idx = lane; idx < n; idx += 32) h = mix64(h ^ (uint64_t(s.tok[idx]) << 20) ^ idx);
+    uint64_t v = mix64(h + 0x632be59bd9b4e019ull * (lane + 1));
+#pragma unroll
+    for (int off = 16; off; off >>= 1) v ^= __shfl_xor_sync(0xffffffffu, v, off);
+    v ^= uint64_t(n) * 0xc2b2ae3d27d4eb4full;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) v = mix64(v ^ s.parent[i]);
+    return v;
+}
+
+__device__ __forceinline__ bool memo_probe(const MemoView& M, const WarpSmem& s, uint32_t n,
+                                           uint64_t key, uint32_t lane, uint32_t* digest) {
+    const uint64_t tag = (key >> 24) | 1u;
+    uint32_t slot = uint32_t(key) & M.slot_mask;
+    for (uint32_t p = 0; p <= M.slot_mask; ++p, slot = (slot + 1) & M.slot_mask) {
+        const unsigned long long sv = __ldcg(M.slots + slot);
+        if (sv == 0) return false;
+        if ((sv >> 24) != tag) continue;
+        const uint32_t* ent = M.entries + uint64_t(sv & 0xffffffu) * M.entry_words;
+        bool ok = __ldcg(ent + 16) == n;
+        if (lane < 8) ok = ok && __ldcg(ent + lane) == s.parent[lane];
+        for (uint32_t idx = lane; idx < n; idx += 32) ok = ok && __ldcg(ent + 17 + idx) == s.tok[idx];
+        if (__all_sync(0xffffffffu, ok)) {
+#pragma unroll
+            for (int i = 0; i < 8; ++i) digest[i] = __ldcg(ent + 8 + i);
+            return true;
+        }
+    }
+    return false;
+}
+
+__device__ __forceinline__ void memo_insert(const MemoView& M, const WarpSmem& s, uint32_t n,
+                                            uint64_t key, uint32_t lane, const uint32_t h[8]) {
+    unsigned int e = 0;
+    if (lane == 0) e = atomicAdd(M.counter, 1u);
+    e = __shfl_sync(0xffffffffu, e, 0);
+    if (e >= M.entry_cap) return;  // full: the memo stops growing until reset
+    uint32_t* ent = M.entries + uint64_t(e) * M.entry_words;
+    if (lane < 8) ent[lane] = s.parent[lane];
+    if (lane == 0) {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) ent[8 + i] = h[i];
+        ent[16] = n;
+    }
+    for (uint32_t idx = lane; idx < n; idx += 32) ent[17 + idx] = s.tok[idx];
+    __threadfence();
+    __syncwarp();
+    if (lane == 0) {
+        const unsigned long long packed = (((key >> 24) | 1u) << 24) | e;
+        uint32_t slot = uint32_t(key) & M.slot_mask;
+        for (uint32_t p = 0; p <= M.slot_mask; ++p, slot = (slot + 1) & M.slot_mask)
+            if (atomicCAS(M.slots + slot, 0ull, packed) == 0ull) break;
+    }
+}
+
 __global__ void __launch_bounds__(32 * kWarpsPerCta)
 hash_chains_warp_kernel(const uint32_t* __restrict__ tokens, const ChainDesc* __restrict__ chains,
-                        uint32_t n_chains, const HashParams P, uint8_t* __restrict__ out) {
+                        uint32_t n_chains, const HashParams P, uint8_t* __restrict__ out,
+                        const MemoView M) {
     __shared__ WarpSmem smem[kWarpsPerCta];
     const uint32_t lane = threadIdx.x & 31;
     const uint32_t wid = threadIdx.x >> 5;
@@ -281,6 +350,8 @@ hash_chains_warp_kernel(const uint32_t* __restrict__ tokens, const ChainDesc* __
         }
     }
     uint32_t row = cd.out_first;
+    bool probing = M.slots != nullptr;  // after the first memo miss the parent is novel
+    unsigned long long hits = 0, misses = 0;
     for (uint32_t start = 0; start < cd.n_tokens; start += cs, ++row) {
         const uint32_t n = min(cs, cd.n_tokens - start);
         // 1. stage this chunk's tokens
@@ -301,6 +372,28 @@ hash_chains_warp_kernel(const uint32_t* __restrict__ tokens, const ChainDesc* __
                 pf[j] = idx < nn ? __ldg(base + nstart + idx) : 0u;
             }
         }
+        // 2b. memo: a verified (parent, tokens) hit replaces the SHA chain link
+        uint64_t key = 0;
+        if (M.slots != nullptr) key = memo_key(s, n, lane);
+        if (probing) {
+            uint32_t d[8];
+            if (memo_probe(M, s, n, key, lane, d)) {
+                ++hits;
+                __syncwarp();
+                if (lane == 0) {
+                    uint32_t* o = reinterpret_cast<uint32_t*>(out + 32ull * row);
+#pragma unroll
+                    for (int i = 0; i < 8; ++i) {
+                        s.parent[i] = d[i];
+                        o[i] = __byte_perm(d[i], 0, 0x0123);
+                    }
+                }
+                __syncwarp();
+                continue;
+            }
+            probing = false;
+        }
+        ++misses;
         // 3. every message word of the chunk, in parallel across lanes
         const uint32_t len = hdr + 4 * n;
         const uint32_t nblocks = (len + 9 + 63) / 64;
@@ -331,6 +424,8 @@ hash_chains_warp_kernel(const uint32_t* __restrict__ tokens, const ChainDesc* __
 #pragma unroll 1
         for (uint32_t b = 0; b < nblocks; ++b) compress_kw(h, s.kw + 64 * b);
         __syncwarp();  // all lanes done reading s.w / s.parent of this chunk
+        if (M.slots != nullptr) memo_insert(M, s, n, key, lane, h);  // needs the old parent
+        __syncwarp();
         // 5. digest out; it is the next chunk's parent
         if (lane == 0) {
             uint32_t* o = reinterpret_cast<uint32_t*>(out + 32ull * row);
@@ -342,20 +437,62 @@ hash_chains_warp_kernel(const uint32_t* __restrict__ tokens, const ChainDesc* __
         }
         __syncwarp();
     }
+    if (M.stats != nullptr && lane == 0) {
+        if (hits) atomicAdd(M.stats, hits);
+        if (misses) atomicAdd(M.stats + 1, misses);
+    }
+}
+
+// Plain SHA-256 of a short byte string (model_tag_hash, src/hash.cpp:41-44):
+// one thread, message bytes read from (mapped) memory.
+__global__ void sha256_bytes_kernel(const uint8_t* __restrict__ data, uint32_t n,
+                                    uint8_t* __restrict__ out) {
+    uint32_t h[8] = {0x6a09e667, 0xbb67ae85, 0x3c6ef372, 0xa54ff53a,
+                     0x510e527f, 0x9b05688c, 0x1f83d9ab, 0x5be0cd19};
+    const uint32_t nblocks = (n + 9 + 63) / 64;
+    const uint32_t end = 64 * nblocks;
+    for (uint32_t b = 0; b < nblocks; ++b) {
+        uint32_t w[16];
+        for (int i = 0; i < 16; ++i) {
+            uint32_t word = 0;
+            for (int k = 0; k < 4; ++k) {
+                const uint32_t o = 64 * b + 4 * i + k;
+                uint32_t byte;
+                if (o < n) byte = data[o];
+                else if (o == n) byte = 0x80;
+                else if (o >= end - 8) byte = uint32_t((uint64_t(n) * 8) >> (8 * (end - 1 - o))) & 0xff;
+                else byte = 0;
+                word = (word << 8) | byte;
+            }
+            w[i] = word;
+        }
+        compress(h, w);
+    }
+    for (int i = 0; i < 8; ++i)
+        for (int k = 0; k < 4; ++k) out[4 * i + k] = uint8_t(h[i] >> (24 - 8 * k));
 }
 
 }  // namespace
 
+cudaError_t launch_sha256_bytes(const uint8_t* data, uint32_t n, uint8_t* out, cudaStream_t s) {
+    note_launch();
+    sha256_bytes_kernel<<<1, 1, 0, s>>>(data, n, out);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_hash_chains(const uint32_t* tokens, const ChainDesc* chains, uint32_t n_chains,
-                               const HashParams& params, uint8_t* out, cudaStream_t stream) {
+                               const HashParams& params, uint8_t* out, cudaStream_t stream,
+                               const MemoView* memo) {
     if (n_chains == 0) return cudaSuccess;
     if (params.tag_len > uint32_t(kMaxTagBytes) || params.chunk_size == 0)
         return cudaErrorInvalidValue;
     note_launch();
     if (params.chunk_size <= uint32_t(kWarpChunkMax)) {
         const int blocks = int((n_chains + kWarpsPerCta - 1) / kWarpsPerCta);
+        MemoView m;
+        if (memo && memo->slots && memo->entry_words == 17 + params.chunk_size) m = *memo;
         hash_chains_warp_kernel<<<blocks, 32 * kWarpsPerCta, 0, stream>>>(tokens, chains, n_chains,
-                                                                          params, out);
+                                                                          params, out, m);
     } else {
         const int threads = 128;
         const int blocks = int((n_chains + threads - 1) / threads);

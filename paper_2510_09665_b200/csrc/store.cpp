@@ -3,6 +3,8 @@
 #include <algorithm>
 #include <cstring>
 
+#include "record.hpp"
+
 namespace tkv {
 
 const Status& PutHandle::wait() const {
@@ -222,6 +224,31 @@ ClearResult TieredStore::clear(const std::vector<Digest>& digests) {
         r.removed++;
     }
     return r;
+}
+
+Result<std::vector<uint8_t>> TieredStore::export_record(const Digest& digest, uint64_t tag_hash) {
+    auto r = acquire(digest, 0);
+    if (!r.ok()) return r.status();
+    RecordInfo info;
+    info.digest = digest;
+    info.model_tag_hash = tag_hash;
+    info.token_count = uint16_t(r.value().token_count);
+    info.num_layers = uint16_t(cfg_.model.num_layers);
+    info.bytes_per_token = cfg_.model.bytes_per_token_per_layer;
+    auto rec = encode_record(info, r.value().host, info.payload_bytes());
+    release(digest);
+    return rec;
+}
+
+Status TieredStore::import_record(const uint8_t* record, size_t n, bool pin) {
+    const uint8_t* payload = nullptr;
+    auto info = parse_record(record, n, &payload);
+    if (!info.ok()) return info.status();
+    const auto& i = info.value();
+    if (i.num_layers != cfg_.model.num_layers ||
+        i.bytes_per_token != cfg_.model.bytes_per_token_per_layer || i.token_count > cfg_.chunk_size)
+        return Status{Errc::invalid_argument, "chunk geometry does not match store"};
+    return put(i.digest, i.token_count, payload, i.payload_bytes(), pin).wait();
 }
 
 StoreStats TieredStore::stats() const {

@@ -121,6 +121,12 @@ public:
     size_t evict_until(size_t bytes_needed);
     StoreStats stats() const;
 
+    // LMCK record framing (chunk_file.cpp:7-95) for interop with the
+    // reference's disk / wire format: export a present entry as a record,
+    // or import a record (checksum and geometry verified) into a slot.
+    Result<std::vector<uint8_t>> export_record(const Digest& digest, uint64_t model_tag_hash);
+    Status import_record(const uint8_t* record, size_t n, bool pin = false);
+
 private:
     struct Entry {
         enum class State : uint8_t { writing, present };

@@ -61,9 +61,14 @@ std::vector<std::vector<Digest>> KeyHasher::hash(const std::vector<TokenSpanView
     p.tag_len = uint32_t(tag_.size());
     std::copy(tag_.begin(), tag_.end(), p.tag);
 
+    if (memo_.slots) {
+        if (memo_used_bound_ + total_chunks > memo_.entry_cap) memo_reset_locked();
+        memo_used_bound_ += total_chunks;
+    }
     TKV_CUDA(launch_hash_chains(reinterpret_cast<const uint32_t*>(h_tokens_.dev),
                                 reinterpret_cast<const ChainDesc*>(h_chains_.dev),
-                                uint32_t(seqs.size()), p, h_out_.dev, stream_));
+                                uint32_t(seqs.size()), p, h_out_.dev, stream_,
+                                memo_.slots ? &memo_ : nullptr));
     TKV_CUDA(cudaStreamSynchronize(stream_));
     ++launches_;
     chunks_ += total_chunks;
@@ -76,6 +81,53 @@ std::vector<std::vector<Digest>> KeyHasher::hash(const std::vector<TokenSpanView
             std::copy(h_out_.host + 32 * row, h_out_.host + 32 * row + 32, out[i][c].begin());
     }
     return out;
+}
+
+void KeyHasher::enable_memo(size_t entries) {
+    std::lock_guard lock(mu_);
+    TKV_CUDA(cudaSetDevice(device_));
+    if (entries == 0 || chunk_size_ > 256) {  // the memo lives in the warp-per-chain kernel
+        memo_ = MemoView{};
+        return;
+    }
+    entries = std::min<size_t>(entries, size_t(1) << 24);
+    size_t slots = 1;
+    while (slots < 2 * entries) slots <<= 1;
+    const uint32_t words = uint32_t(17 + chunk_size_);
+    memo_slots_.reserve(slots * sizeof(unsigned long long));
+    memo_entries_.reserve(entries * words * sizeof(uint32_t));
+    memo_meta_.reserve(64);
+    memo_.slots = reinterpret_cast<unsigned long long*>(memo_slots_.ptr);
+    memo_.entries = reinterpret_cast<uint32_t*>(memo_entries_.ptr);
+    memo_.counter = reinterpret_cast<unsigned int*>(memo_meta_.ptr);
+    memo_.stats = reinterpret_cast<unsigned long long*>(memo_meta_.ptr + 16);
+    memo_.slot_mask = uint32_t(slots - 1);
+    memo_.entry_cap = uint32_t(entries);
+    memo_.entry_words = words;
+    TKV_CUDA(cudaMemsetAsync(memo_meta_.ptr, 0, 64, stream_));
+    memo_reset_locked();
+    TKV_CUDA(cudaStreamSynchronize(stream_));
+}
+
+void KeyHasher::memo_reset_locked() {
+    TKV_CUDA(cudaMemsetAsync(memo_.slots, 0, (size_t(memo_.slot_mask) + 1) * 8, stream_));
+    TKV_CUDA(cudaMemsetAsync(memo_.counter, 0, sizeof(unsigned int), stream_));
+    memo_used_bound_ = 0;
+    ++memo_resets_;
+}
+
+KeyHasher::MemoStats KeyHasher::memo_stats() {
+    std::lock_guard lock(mu_);
+    MemoStats s;
+    if (!memo_.slots) return s;
+    unsigned long long st[2] = {0, 0};
+    TKV_CUDA(cudaMemcpyAsync(st, memo_.stats, sizeof st, cudaMemcpyDeviceToHost, stream_));
+    TKV_CUDA(cudaStreamSynchronize(stream_));
+    s.hits = st[0];
+    s.misses = st[1];
+    s.capacity = memo_.entry_cap;
+    s.resets = memo_resets_ - 1;  // the enabling clear is not a reset
+    return s;
 }
 
 std::vector<Digest> KeyHasher::hash_one(TokenSpanView seq, const Digest& parent) {

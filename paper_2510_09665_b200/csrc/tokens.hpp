@@ -53,7 +53,16 @@ public:
     uint64_t launches() const { return launches_; }
     uint64_t chunks_hashed() const { return chunks_; }
 
+    // Prefix-digest memo: `entries` chunk links
+    // kept on the device; 0 disables. Exact: hits are verified token by token.
+    void enable_memo(size_t entries);
+    struct MemoStats {
+        uint64_t hits = 0, misses = 0, capacity = 0, resets = 0;
+    };
+    MemoStats memo_stats();
+
 private:
+    void memo_reset_locked();
     std::string tag_;
     size_t chunk_size_;
     int device_;
@@ -61,6 +70,11 @@ private:
     Stream stream_;
     PinnedBuffer h_tokens_, h_chains_, h_out_;  // mapped: K3 reads/writes them directly
     uint64_t launches_ = 0, chunks_ = 0;
+    // memo (device): slots, entries, counter + stats
+    DeviceBuffer memo_slots_, memo_entries_, memo_meta_;
+    MemoView memo_;
+    size_t memo_used_bound_ = 0;  // host upper bound of inserted entries
+    uint64_t memo_resets_ = 0;
 };
 
 // tokens.cpp:49-57.

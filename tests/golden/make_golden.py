@@ -68,6 +68,17 @@ def main():
         json.dump({"keys": keys, "lpm": lpm, **out}, f)
     with open(os.path.join(HERE, "synth.json"), "w") as f:
         json.dump({"tokens": t, "slabs": synth, **out}, f, indent=1)
+    q8 = []
+    rng = np.random.default_rng(8)
+    for n in (2, 3, 100, 4096, 4097, 70000):
+        p = rng.integers(0, 256, size=n, dtype=np.uint8)
+        blob = R.q8_encode(p)
+        dec, code = R.q8_decode(blob)
+        q8.append({"seed": 8, "n": n, "blob_sha256": hashlib.sha256(blob.tobytes()).hexdigest(),
+                   "decoded_sha256": hashlib.sha256(dec.tobytes()).hexdigest()})
+    with open(os.path.join(HERE, "q8.json"), "w") as f:
+        json.dump({"note": "payloads: np.random.default_rng(8).integers(0, 256, size=n) in order", "cases": q8},
+                  f, indent=1)
     C = oracle.C()
     sc = {fn.__name__: json.loads(json.dumps(fn(oracle.RefEngine, C))) for fn in S.ALL}
     with open(os.path.join(HERE, "scenarios.json"), "w") as f:

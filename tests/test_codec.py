@@ -1,0 +1,80 @@
+"""q8-scale codec (src/codec.cpp:27-94): the C
+oracle against the reference (CPU), and the device codec against the oracle
+byte for byte (GPU). Cases follow test_formats.cpp:137-186 — lengths 2, 100,
+4096, 4097, all-zero, the -32768 lane, truncated blobs — plus large payloads
+that span many CTA segments."""
+import numpy as np
+import pytest
+import torch
+
+LENGTHS = [0, 1, 2, 3, 100, 4096, 4097, 65536 * 2 + 7, (1 << 20) + 1]
+
+
+def _payloads():
+    rng = np.random.default_rng(5)
+    out = [rng.integers(0, 256, size=n, dtype=np.uint8) for n in LENGTHS]
+    out.append(np.zeros(512, np.uint8))
+    edge = np.zeros(64, np.uint8)
+    edge[0], edge[1] = 0x00, 0x80  # lane -32768: |lane| = 32768
+    edge[2], edge[3] = 0xFF, 0x7F  # 32767
+    out.append(edge)
+    small = (rng.integers(-3, 4, size=1000).astype(np.int16)).view(np.uint8)  # tiny scale, many .5 ties
+    out.append(small.copy())
+    return out
+
+
+def test_oracle_q8_matches_reference(C, Ref):
+    for p in _payloads():
+        blob = C.q8_encode(p)
+        assert np.array_equal(blob, Ref.q8_encode(p)), p.size
+        dec, code = Ref.q8_decode(blob)
+        assert code == 0 and np.array_equal(C.q8_decode(blob), dec)
+
+
+def test_oracle_q8_golden(C):
+    import hashlib
+    import json
+    import os
+    with open(os.path.join(os.path.dirname(__file__), "golden", "q8.json")) as f:
+        g = json.load(f)
+    rng = np.random.default_rng(8)
+    for case in g["cases"]:
+        p = rng.integers(0, 256, size=case["n"], dtype=np.uint8)
+        blob = C.q8_encode(p)
+        assert hashlib.sha256(blob.tobytes()).hexdigest() == case["blob_sha256"]
+        assert hashlib.sha256(C.q8_decode(blob).tobytes()).hexdigest() == case["decoded_sha256"]
+
+
+def test_oracle_q8_bounds_and_corruption(C):
+    """test_formats.cpp:137-186: size ratio, per-lane error bound, raw odd tail,
+    exact zeros, truncated / over-long blobs rejected."""
+    rng = np.random.default_rng(5)
+    for n in (2, 100, 4096, 4097):
+        p = rng.integers(0, 256, size=n, dtype=np.uint8)
+        blob = C.q8_encode(p)
+        if n >= 1000:
+            assert 0.45 < blob.size / n < 0.55
+        d = C.q8_decode(blob)
+        lanes_o = p[: n // 2 * 2].view(np.int16).astype(np.int64)
+        lanes_r = d[: n // 2 * 2].view(np.int16).astype(np.int64)
+        scale = np.abs(lanes_o).max() / 127.0
+        assert np.all(np.abs(lanes_o - lanes_r) <= scale / 2 + 1)
+        if n % 2:
+            assert d[-1] == p[-1]
+    z = np.zeros(512, np.uint8)
+    assert np.array_equal(C.q8_decode(C.q8_encode(z)), z)
+    blob = C.q8_encode(np.zeros(100, np.uint8))
+    assert C.q8_decode(blob[:-3]) is None and C.q8_decode(blob[:3]) is None
+
+
+@pytest.mark.gpu
+def test_device_q8_matches_oracle(tkv, C):
+    from paper_2510_09665_b200.api import q8_decode, q8_encode
+    ps = [p for p in _payloads() if p.size > 0]
+    dev = [torch.from_numpy(p.copy()).cuda() for p in ps]
+    blobs = q8_encode(dev)
+    for p, b in zip(ps, blobs):
+        assert np.array_equal(b.cpu().numpy(), C.q8_encode(p)), p.size
+    back = q8_decode(blobs, [p.size for p in ps])
+    for p, b, d in zip(ps, blobs, back):
+        assert np.array_equal(d.cpu().numpy(), C.q8_decode(C.q8_encode(p))), p.size

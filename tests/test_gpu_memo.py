@@ -1,0 +1,64 @@
+"""The device prefix-digest memo never changes a
+key: every digest the connector plans with equals the CPU oracle's chain,
+whether it came from SHA or from a verified memo hit — for repeated prompts,
+shared prefixes, equal chunk contents under different parents, partial tails,
+and a memo small enough to fill up and reset."""
+import numpy as np
+import pytest
+
+import scenarios as S
+
+pytestmark = pytest.mark.gpu
+
+TAG = "memo-test"
+
+
+def _keys_via_connector(e, qid, prompt):
+    """Digests the connector derived for `prompt` (nothing stored -> the store
+    plan lists every chunk with its key)."""
+    e.get_num_new_matched_tokens(qid, prompt)
+    e.bind_pages(qid, len(prompt))
+    e.update_state_after_alloc(qid, (len(prompt) + 15) // 16, 0)
+    m = e.build_connector_meta([(qid, prompt)])
+    sp, _ = e.plan(m, 0, "store")
+    e.drop_meta(m)
+    e.finish_query(qid)
+    e.release_query(qid)
+    return [d for _, _, _, _, d in sp]
+
+
+@pytest.mark.parametrize("entries", [65536, 24])
+def test_memo_keys_equal_oracle(tkv, C, entries):
+    from paper_2510_09665_b200.api import Engine
+    e = Engine(num_layers=2, bpt=64, page_tokens=16, tag=TAG, chunk_size=256, ram_slots=2, num_pages=4096,
+               memo_entries=entries)
+    rng = np.random.default_rng(entries)
+    doc = rng.integers(0, 128256, size=256 * 12, dtype=np.uint32)
+    prompts = [doc, doc.copy(),                                   # repeat: all hits
+               np.concatenate([doc[:256 * 5], rng.integers(0, 128256, 300, dtype=np.uint32)]),  # shared prefix
+               np.concatenate([doc[256:512], doc[:256], doc[512:900]]),  # same chunk bytes, other parents
+               doc[:256 * 3 + 17],                                # partial tail
+               doc]
+    qid = 1
+    for p in prompts:
+        assert _keys_via_connector(e, qid, p) == C.chunk_keys(p, 256, TAG)
+        qid += 1
+    st = e.memo_stats()
+    if entries == 65536:
+        assert st["hits"] >= 12 + 12 + 5 + 3 and st["resets"] == 0
+    else:
+        assert st["resets"] >= 1
+    e.close()
+
+
+def test_memo_does_not_change_connector_outcomes(tkv, C):
+    """The connector scenarios give the reference outcome with the memo on
+    (default) and off."""
+    import json
+
+    from paper_2510_09665_b200.api import Engine
+    for name in ("sc_partial_match", "sc_multi_query_batch"):
+        on = json.loads(json.dumps(getattr(S, name)(Engine, C)))
+        off = json.loads(json.dumps(getattr(S, name)(
+            lambda **kw: Engine(**kw, memo_entries=0), C)))
+        assert on == off
