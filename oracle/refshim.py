@@ -133,7 +133,7 @@ class _Ref:
                       payload: np.ndarray) -> np.ndarray:
         p = np.ascontiguousarray(payload, np.uint8)
         d = np.frombuffer(digest, np.uint8).copy()
-        out = np.zeros(52 + p.size + 8, np.uint8)
+        out = np.zeros(54 + p.size + 8, np.uint8)  # kChunkHeaderBytes = 54 (chunk_file.hpp:18)
         n = self.lib.ref_encode_record(tag.encode(), d.ctypes.data_as(_u8p), token_count, layers, bpt,
                                        p.ctypes.data_as(_u8p), out.ctypes.data_as(_u8p))
         return out[:n]

@@ -266,15 +266,14 @@ __device__ __forceinline__ uint64_t mix64(uint64_t x) {
 // Same value in every lane: fingerprint of (parent, n, tokens). Only a probe
 // key — a hit is confirmed by comparing parent, n and every token.
 __device__ __forceinline__ uint64_t memo_key(const WarpSmem& s, uint32_t n, uint32_t lane) {
+    // Independent per-token / per-word mixes (ILP), xor-combined: no serial chain.
     uint64_t h = 0;
-    for (uint32_t idx = lane; idx < n; idx += 32) h = mix64(h ^ (uint64_t(s.tok[idx]) << 20) ^ idx);
-    uint64_t v = mix64(h + 0x632be59bd9b4e019ull * (lane + 1));
+    for (uint32_t idx = lane; idx < n; idx += 32)
+        h ^= mix64((uint64_t(s.tok[idx]) << 32) | idx);
+    if (lane < 8) h ^= mix64((uint64_t(s.parent[lane]) << 32) | (0x80000000u + lane));
 #pragma unroll
-    for (int off = 16; off; off >>= 1) v ^= __shfl_xor_sync(0xffffffffu, v, off);
-    v ^= uint64_t(n) * 0xc2b2ae3d27d4eb4full;
-#pragma unroll
-    for (int i = 0; i < 8; ++i) v = mix64(v ^ s.parent[i]);
-    return v;
+    for (int off = 16; off; off >>= 1) h ^= __shfl_xor_sync(0xffffffffu, h, off);
+    return mix64(h ^ (uint64_t(n) * 0xc2b2ae3d27d4eb4full));
 }
 
 __device__ __forceinline__ bool memo_probe(const MemoView& M, const WarpSmem& s, uint32_t n,
@@ -286,10 +285,13 @@ __device__ __forceinline__ bool memo_probe(const MemoView& M, const WarpSmem& s,
         if (sv == 0) return false;
         if ((sv >> 24) != tag) continue;
         const uint32_t* ent = M.entries + uint64_t(sv & 0xffffffu) * M.entry_words;
-        bool ok = __ldcg(ent + 16) == n;
-        if (lane < 8) ok = ok && __ldcg(ent + lane) == s.parent[lane];
-        for (uint32_t idx = lane; idx < n; idx += 32) ok = ok && __ldcg(ent + 17 + idx) == s.tok[idx];
-        if (__all_sync(0xffffffffu, ok)) {
+        // Issue every verification load up front (no short-circuit: each
+        // dependent load would cost a full memory round trip).
+        uint32_t bad = __ldcg(ent + 16) ^ n;
+        if (lane < 8) bad |= __ldcg(ent + lane) ^ s.parent[lane];
+#pragma unroll 8
+        for (uint32_t idx = lane; idx < n; idx += 32) bad |= __ldcg(ent + 17 + idx) ^ s.tok[idx];
+        if (__all_sync(0xffffffffu, bad == 0)) {
 #pragma unroll
             for (int i = 0; i < 8; ++i) digest[i] = __ldcg(ent + 8 + i);
             return true;

@@ -66,9 +66,9 @@ def test_export_matches_reference_and_import_roundtrip(tkv, C, Ref):
     bad[4] = 9
     assert lib.tkv_store_import_record(f.store, bad.ctypes.data_as(u8p), bad.size, 0) == 5
     bad = rec.copy()
-    bad[52 + 5] ^= 0x40
+    bad[54 + 5] ^= 0x40  # header is 54 bytes (chunk_file.hpp:18)
     assert lib.tkv_store_import_record(f.store, bad.ctypes.data_as(u8p), bad.size, 0) == 5
-    for keep in (0, 3, 51, 52, rec.size - 9, rec.size - 1):
+    for keep in (0, 3, 53, 54, rec.size - 9, rec.size - 1):
         t = rec[:keep].copy()
         assert lib.tkv_store_import_record(f.store, t.ctypes.data_as(u8p), t.size, 0) == 5
     longer = np.concatenate([rec, np.zeros(1, np.uint8)])
