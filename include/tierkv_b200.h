@@ -280,8 +280,11 @@ int tkv_connector_append_decode(tkv_connector* c, uint64_t query, uint32_t token
 int tkv_connector_finish_query(tkv_connector* c, uint64_t query, uint8_t* digests_out, size_t cap,
                                size_t* n);
 size_t tkv_connector_staging_peak(tkv_connector* c);
-/* Prefix-digest memo counters: hits, misses (chunk links), capacity, resets. */
-int tkv_connector_memo_stats(tkv_connector* c, uint64_t out[4]);
+/* Prefix-digest memo counters: hits, misses (chunk links), capacity, resets,
+ * re-hashed launches (a hit failed verification). */
+int tkv_connector_memo_stats(tkv_connector* c, uint64_t out[5]);
+/* Test hook: corrupt every memo slot's digest (verification must catch it). */
+int tkv_connector_debug_poison_memo(tkv_connector* c);
 uint64_t tkv_connector_hash_launches(tkv_connector* c);
 
 void tkv_meta_destroy(tkv_meta* m);

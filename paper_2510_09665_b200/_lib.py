@@ -131,6 +131,7 @@ SIGNATURES = {
     "tkv_connector_finish_query": (ct.c_int, [vp, ct.c_uint64, u8p, sz, szp]),
     "tkv_connector_staging_peak": (sz, [vp]),
     "tkv_connector_memo_stats": (ct.c_int, [vp, u64p]),
+    "tkv_connector_debug_poison_memo": (ct.c_int, [vp]),
     "tkv_connector_hash_launches": (ct.c_uint64, [vp]),
     "tkv_meta_destroy": (None, [vp]),
     "tkv_meta_layerwise": (ct.c_int, [vp]),

@@ -327,9 +327,12 @@ class Engine:
         return int(self.L.tkv_connector_hash_launches(self.conn))
 
     def memo_stats(self) -> dict:
-        out = (ct.c_uint64 * 4)()
+        out = (ct.c_uint64 * 5)()
         check(self.L.tkv_connector_memo_stats(self.conn, out))
-        return {"hits": out[0], "misses": out[1], "capacity": out[2], "resets": out[3]}
+        return {"hits": out[0], "misses": out[1], "capacity": out[2], "resets": out[3], "rehashes": out[4]}
+
+    def debug_poison_memo(self) -> None:
+        check(self.L.tkv_connector_debug_poison_memo(self.conn))
 
     # --- store ---
     def contains(self, digest: bytes) -> bool:

@@ -576,13 +576,20 @@ int tkv_connector_finish_query(tkv_connector* c, uint64_t q, uint8_t* out, size_
     });
 }
 size_t tkv_connector_staging_peak(tkv_connector* c) { return c->c->staging_peak_bytes(); }
-int tkv_connector_memo_stats(tkv_connector* c, uint64_t out[4]) {
+int tkv_connector_memo_stats(tkv_connector* c, uint64_t out[5]) {
     return guard([&] {
         auto s = c->c->hasher().memo_stats();
         out[0] = s.hits;
         out[1] = s.misses;
         out[2] = s.capacity;
         out[3] = s.resets;
+        out[4] = s.rehashes;
+        return 0;
+    });
+}
+int tkv_connector_debug_poison_memo(tkv_connector* c) {
+    return guard([&] {
+        c->c->hasher().debug_poison_memo();
         return 0;
     });
 }

@@ -102,7 +102,8 @@ struct HashParams {
 // and inserted by the same launch. Slot word = (tag40 << 24) | entry index;
 // entry = parent[8] | digest[8] | n | tokens[chunk_size] (u32 words).
 struct MemoView {
-    unsigned long long* slots = nullptr;  // [slot_mask + 1], 0 = empty
+    unsigned long long* slots = nullptr;  // [slot_mask + 1] x 8 u64: tagword | digest[8 x u32]
+    uint32_t* hit_entry = nullptr;        // per output row: memo entry used, or ~0u
     uint32_t* entries = nullptr;          // [entry_cap][entry_words]
     unsigned int* counter = nullptr;      // next free entry
     uint32_t slot_mask = 0;
@@ -114,6 +115,16 @@ struct MemoView {
 cudaError_t launch_hash_chains(const uint32_t* tokens, const ChainDesc* chains, uint32_t n_chains,
                                const HashParams& params, uint8_t* out, cudaStream_t stream,
                                const MemoView* memo = nullptr);
+// Copies `bytes` (rounded up to 16) from src to dst (mapped host -> HBM staging).
+cudaError_t launch_stage_words(const void* src, void* dst, uint64_t bytes, cudaStream_t stream);
+// Verifies every memo hit of a launch against its entry and publishes all
+// digest rows from dev_out to out; first_bad[chain] = first failed chunk.
+cudaError_t launch_memo_verify(const uint32_t* tokens, const ChainDesc* chains, uint32_t n_chains,
+                               uint32_t total_rows, const HashParams& params, const uint8_t* dev_out,
+                               const MemoView* memo, uint8_t* out, unsigned int* first_bad,
+                               cudaStream_t stream);
+// Test hook: corrupt the digest of every published memo slot.
+cudaError_t launch_memo_poison(const MemoView& memo, cudaStream_t stream);
 // SHA-256 of n bytes (one thread; for the model tag hash, hash.cpp:41-44).
 cudaError_t launch_sha256_bytes(const uint8_t* data, uint32_t n, uint8_t* out, cudaStream_t stream);
 

@@ -276,26 +276,35 @@ __device__ __forceinline__ uint64_t memo_key(const WarpSmem& s, uint32_t n, uint
     return mix64(h ^ (uint64_t(n) * 0xc2b2ae3d27d4eb4full));
 }
 
-__device__ __forceinline__ bool memo_probe(const MemoView& M, const WarpSmem& s, uint32_t n,
-                                           uint64_t key, uint32_t lane, uint32_t* digest) {
+// Slot = 8 u64 (64 B): [0] tagword = (tag40 << 24) | entry, [2..5] digest
+// words (16-byte aligned for vector loads). 0 = empty, kBusy = being published. The digest rides in the slot so
+// a hit is ONE memory round trip on the serial chain; the full comparison
+// against the entry (parent, n, every token, digest) runs afterwards, in
+// parallel over all hit chunks (memo_verify_kernel).
+constexpr unsigned long long kBusy = ~0ull;
+constexpr uint32_t kNoEntry = 0xffffffffu;
+
+__device__ __forceinline__ unsigned long long ld_acquire(const unsigned long long* p) {
+    unsigned long long v;
+    asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+
+__device__ __forceinline__ bool memo_probe(const MemoView& M, uint64_t key, uint32_t* digest,
+                                           uint32_t* entry) {
     const uint64_t tag = (key >> 24) | 1u;
     uint32_t slot = uint32_t(key) & M.slot_mask;
     for (uint32_t p = 0; p <= M.slot_mask; ++p, slot = (slot + 1) & M.slot_mask) {
-        const unsigned long long sv = __ldcg(M.slots + slot);
+        const unsigned long long* sp = M.slots + 8ull * slot;
+        const unsigned long long sv = ld_acquire(sp);
         if (sv == 0) return false;
-        if ((sv >> 24) != tag) continue;
-        const uint32_t* ent = M.entries + uint64_t(sv & 0xffffffu) * M.entry_words;
-        // Issue every verification load up front (no short-circuit: each
-        // dependent load would cost a full memory round trip).
-        uint32_t bad = __ldcg(ent + 16) ^ n;
-        if (lane < 8) bad |= __ldcg(ent + lane) ^ s.parent[lane];
-#pragma unroll 8
-        for (uint32_t idx = lane; idx < n; idx += 32) bad |= __ldcg(ent + 17 + idx) ^ s.tok[idx];
-        if (__all_sync(0xffffffffu, bad == 0)) {
-#pragma unroll
-            for (int i = 0; i < 8; ++i) digest[i] = __ldcg(ent + 8 + i);
-            return true;
-        }
+        if (sv == kBusy || (sv >> 24) != tag) continue;
+        const uint4 d0 = __ldcg(reinterpret_cast<const uint4*>(sp + 2));
+        const uint4 d1 = __ldcg(reinterpret_cast<const uint4*>(sp + 4));
+        digest[0] = d0.x; digest[1] = d0.y; digest[2] = d0.z; digest[3] = d0.w;
+        digest[4] = d1.x; digest[5] = d1.y; digest[6] = d1.z; digest[7] = d1.w;
+        *entry = uint32_t(sv & 0xffffffu);
+        return true;
     }
     return false;
 }
@@ -319,8 +328,16 @@ __device__ __forceinline__ void memo_insert(const MemoView& M, const WarpSmem& s
     if (lane == 0) {
         const unsigned long long packed = (((key >> 24) | 1u) << 24) | e;
         uint32_t slot = uint32_t(key) & M.slot_mask;
-        for (uint32_t p = 0; p <= M.slot_mask; ++p, slot = (slot + 1) & M.slot_mask)
-            if (atomicCAS(M.slots + slot, 0ull, packed) == 0ull) break;
+        for (uint32_t p = 0; p <= M.slot_mask; ++p, slot = (slot + 1) & M.slot_mask) {
+            unsigned long long* sp = M.slots + 8ull * slot;
+            if (atomicCAS(sp, 0ull, kBusy) != 0ull) continue;
+            uint4* d = reinterpret_cast<uint4*>(sp + 2);
+            d[0] = make_uint4(h[0], h[1], h[2], h[3]);
+            d[1] = make_uint4(h[4], h[5], h[6], h[7]);
+            __threadfence();
+            atomicExch(sp, packed);  // publish: readers acquire the tag, then the digest
+            break;
+        }
     }
 }
 
@@ -378,8 +395,8 @@ hash_chains_warp_kernel(const uint32_t* __restrict__ tokens, const ChainDesc* __
         uint64_t key = 0;
         if (M.slots != nullptr) key = memo_key(s, n, lane);
         if (probing) {
-            uint32_t d[8];
-            if (memo_probe(M, s, n, key, lane, d)) {
+            uint32_t d[8], ent = 0;
+            if (memo_probe(M, key, d, &ent)) {
                 ++hits;
                 __syncwarp();
                 if (lane == 0) {
@@ -389,12 +406,14 @@ hash_chains_warp_kernel(const uint32_t* __restrict__ tokens, const ChainDesc* __
                         s.parent[i] = d[i];
                         o[i] = __byte_perm(d[i], 0, 0x0123);
                     }
+                    M.hit_entry[row] = ent;  // verified later, in parallel
                 }
                 __syncwarp();
                 continue;
             }
             probing = false;
         }
+        if (M.hit_entry != nullptr && lane == 0) M.hit_entry[row] = kNoEntry;
         ++misses;
         // 3. every message word of the chunk, in parallel across lanes
         const uint32_t len = hdr + 4 * n;
@@ -445,6 +464,65 @@ hash_chains_warp_kernel(const uint32_t* __restrict__ tokens, const ChainDesc* __
     }
 }
 
+// Copies the packed tokens from mapped host memory into HBM once, in
+// parallel, so the serial chains read them at device latency.
+__global__ void stage_words_kernel(const uint4* __restrict__ src, uint4* __restrict__ dst, uint64_t n16) {
+    for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n16;
+         i += uint64_t(gridDim.x) * blockDim.x)
+        dst[i] = src[i];
+}
+
+// One warp per digest row: a memo hit is checked against its entry (parent,
+// token count, every token, digest); every row's digest is then published to
+// the caller's buffer. A failed check records the first bad row of its chain
+// (the host re-hashes that chain from there without the memo).
+__global__ void __launch_bounds__(128)
+memo_verify_kernel(const uint32_t* __restrict__ tokens, const ChainDesc* __restrict__ chains,
+                   uint32_t n_chains, uint32_t total_rows, const HashParams P,
+                   const uint8_t* __restrict__ dev_out, const MemoView M, uint8_t* __restrict__ out,
+                   unsigned int* __restrict__ first_bad) {
+    const uint32_t lane = threadIdx.x & 31;
+    const uint32_t row = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    if (row >= total_rows) return;
+    const uint32_t dw = lane < 8 ? reinterpret_cast<const uint32_t*>(dev_out + 32ull * row)[lane] : 0u;
+    if (lane < 8) reinterpret_cast<uint32_t*>(out + 32ull * row)[lane] = dw;
+    if (M.hit_entry == nullptr) return;
+    const uint32_t e = M.hit_entry[row];
+    if (e == kNoEntry) return;
+    uint32_t lo = 0, hi = n_chains;  // chain of this row: largest c with out_first <= row
+    while (hi - lo > 1) {
+        const uint32_t mid = (lo + hi) >> 1;
+        if (chains[mid].out_first <= row) lo = mid; else hi = mid;
+    }
+    const ChainDesc& cd = chains[lo];
+    const uint32_t k = row - cd.out_first;
+    const uint32_t start = k * P.chunk_size;
+    const uint32_t n = min(P.chunk_size, cd.n_tokens - start);
+    const uint32_t* ent = M.entries + uint64_t(e) * M.entry_words;
+    const uint32_t* tok = tokens + cd.token_off + start;
+    uint32_t bad = 0;
+    if (lane < 8) {
+        // parent of this row: previous row's digest, or the chain's parent
+        const uint32_t parent = k ? __byte_perm(reinterpret_cast<const uint32_t*>(dev_out + 32ull * (row - 1))[lane], 0, 0x0123)
+                                  : ((uint32_t(cd.parent[4 * lane]) << 24) | (uint32_t(cd.parent[4 * lane + 1]) << 16) |
+                                     (uint32_t(cd.parent[4 * lane + 2]) << 8) | uint32_t(cd.parent[4 * lane + 3]));
+        bad |= ent[lane] ^ parent;
+        bad |= ent[8 + lane] ^ __byte_perm(dw, 0, 0x0123);
+    }
+    if (lane == 0) bad |= ent[16] ^ n;
+    for (uint32_t idx = lane; idx < n; idx += 32) bad |= ent[17 + idx] ^ tok[idx];
+    if (__any_sync(0xffffffffu, bad != 0) && lane == 0) atomicMin(first_bad + lo, k);
+}
+
+// Test hook: corrupt the digest carried by every published slot, so every
+// optimistic memo hit must be caught by memo_verify_kernel.
+__global__ void memo_poison_kernel(unsigned long long* slots, uint32_t n_slots) {
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n_slots; i += gridDim.x * blockDim.x) {
+        unsigned long long* sp = slots + 8ull * i;
+        if (*sp != 0 && *sp != kBusy) sp[2] ^= 0x1ull;
+    }
+}
+
 // Plain SHA-256 of a short byte string (model_tag_hash, src/hash.cpp:41-44):
 // one thread, message bytes read from (mapped) memory.
 __global__ void sha256_bytes_kernel(const uint8_t* __restrict__ data, uint32_t n,
@@ -475,6 +553,37 @@ __global__ void sha256_bytes_kernel(const uint8_t* __restrict__ data, uint32_t n
 }
 
 }  // namespace
+
+cudaError_t launch_stage_words(const void* src, void* dst, uint64_t bytes, cudaStream_t s) {
+    const uint64_t n16 = (bytes + 15) / 16;
+    if (n16 == 0) return cudaSuccess;
+    note_launch();
+    const uint64_t g = (n16 + 255) / 256;
+    stage_words_kernel<<<int(g < 148 * 4 ? g : 148 * 4), 256, 0, s>>>(
+        static_cast<const uint4*>(src), static_cast<uint4*>(dst), n16);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_memo_verify(const uint32_t* tokens, const ChainDesc* chains, uint32_t n_chains,
+                               uint32_t total_rows, const HashParams& params, const uint8_t* dev_out,
+                               const MemoView* memo, uint8_t* out, unsigned int* first_bad,
+                               cudaStream_t s) {
+    if (total_rows == 0) return cudaSuccess;
+    note_launch();
+    MemoView m;
+    if (memo) m = *memo;
+    const uint32_t blocks = (total_rows * 32 + 127) / 128;
+    memo_verify_kernel<<<blocks, 128, 0, s>>>(tokens, chains, n_chains, total_rows, params, dev_out, m,
+                                              out, first_bad);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_memo_poison(const MemoView& m, cudaStream_t s) {
+    if (!m.slots) return cudaSuccess;
+    note_launch();
+    memo_poison_kernel<<<148, 256, 0, s>>>(m.slots, m.slot_mask + 1);
+    return cudaGetLastError();
+}
 
 cudaError_t launch_sha256_bytes(const uint8_t* data, uint32_t n, uint8_t* out, cudaStream_t s) {
     note_launch();

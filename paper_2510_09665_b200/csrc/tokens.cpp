@@ -61,17 +61,60 @@ std::vector<std::vector<Digest>> KeyHasher::hash(const std::vector<TokenSpanView
     p.tag_len = uint32_t(tag_.size());
     std::copy(tag_.begin(), tag_.end(), p.tag);
 
+    // Stage tokens and descriptors into HBM (one parallel read of the mapped
+    // buffers), run the chains writing digests to HBM, then verify memo hits
+    // and publish every digest to the mapped result buffer.
+    const size_t tok_bytes = total_tokens * sizeof(TokenId);
+    const size_t ch_bytes = seqs.size() * sizeof(ChainDesc);
+    d_tokens_.reserve(tok_bytes + 64);
+    d_chains_.reserve(ch_bytes + 64);
+    d_out_.reserve(total_chunks * 32);
+    h_bad_.reserve(seqs.size() * sizeof(unsigned int));
+    auto* bad = reinterpret_cast<unsigned int*>(h_bad_.host);
+    std::fill(bad, bad + seqs.size(), ~0u);
+    MemoView m = memo_;
     if (memo_.slots) {
         if (memo_used_bound_ + total_chunks > memo_.entry_cap) memo_reset_locked();
         memo_used_bound_ += total_chunks;
+        d_hit_.reserve(total_chunks * sizeof(uint32_t));
+        m = memo_;
+        m.hit_entry = reinterpret_cast<uint32_t*>(d_hit_.ptr);
     }
-    TKV_CUDA(launch_hash_chains(reinterpret_cast<const uint32_t*>(h_tokens_.dev),
-                                reinterpret_cast<const ChainDesc*>(h_chains_.dev),
-                                uint32_t(seqs.size()), p, h_out_.dev, stream_,
-                                memo_.slots ? &memo_ : nullptr));
+    const auto* d_tok = reinterpret_cast<const uint32_t*>(d_tokens_.ptr);
+    const auto* d_ch = reinterpret_cast<const ChainDesc*>(d_chains_.ptr);
+    TKV_CUDA(launch_stage_words(h_tokens_.dev, d_tokens_.ptr, tok_bytes, stream_));
+    TKV_CUDA(launch_stage_words(h_chains_.dev, d_chains_.ptr, ch_bytes, stream_));
+    TKV_CUDA(launch_hash_chains(d_tok, d_ch, uint32_t(seqs.size()), p, d_out_.ptr, stream_,
+                                memo_.slots ? &m : nullptr));
+    TKV_CUDA(launch_memo_verify(d_tok, d_ch, uint32_t(seqs.size()), uint32_t(total_chunks), p,
+                                d_out_.ptr, memo_.slots ? &m : nullptr, h_out_.dev,
+                                reinterpret_cast<unsigned int*>(h_bad_.dev), stream_));
     TKV_CUDA(cudaStreamSynchronize(stream_));
     ++launches_;
     chunks_ += total_chunks;
+
+    // A memo hit that failed verification (a 40-bit tag collision): re-hash
+    // those chains from the first bad chunk with plain SHA-256.
+    std::vector<ChainDesc> redo;
+    for (size_t i = 0; i < seqs.size(); ++i) {
+        if (bad[i] == ~0u) continue;
+        ChainDesc d = ch[i];
+        const size_t skip = size_t(bad[i]) * chunk_size_;
+        d.token_off += skip;
+        d.n_tokens -= uint32_t(skip);
+        d.out_first += bad[i];
+        if (bad[i]) std::copy(h_out_.host + 32 * (d.out_first - 1), h_out_.host + 32 * d.out_first, d.parent);
+        redo.push_back(d);
+    }
+    if (!redo.empty()) {
+        ++memo_rehashes_;
+        std::copy(redo.begin(), redo.end(), ch);
+        TKV_CUDA(launch_stage_words(h_chains_.dev, d_chains_.ptr, redo.size() * sizeof(ChainDesc), stream_));
+        TKV_CUDA(launch_hash_chains(d_tok, d_ch, uint32_t(redo.size()), p, d_out_.ptr, stream_, nullptr));
+        TKV_CUDA(launch_memo_verify(d_tok, d_ch, uint32_t(redo.size()), uint32_t(total_chunks), p,
+                                    d_out_.ptr, nullptr, h_out_.dev, nullptr, stream_));
+        TKV_CUDA(cudaStreamSynchronize(stream_));
+    }
 
     row = 0;
     for (size_t i = 0; i < seqs.size(); ++i) {
@@ -94,7 +137,7 @@ void KeyHasher::enable_memo(size_t entries) {
     size_t slots = 1;
     while (slots < 2 * entries) slots <<= 1;
     const uint32_t words = uint32_t(17 + chunk_size_);
-    memo_slots_.reserve(slots * sizeof(unsigned long long));
+    memo_slots_.reserve(slots * 8 * sizeof(unsigned long long));  // 64-byte slots
     memo_entries_.reserve(entries * words * sizeof(uint32_t));
     memo_meta_.reserve(64);
     memo_.slots = reinterpret_cast<unsigned long long*>(memo_slots_.ptr);
@@ -106,11 +149,33 @@ void KeyHasher::enable_memo(size_t entries) {
     memo_.entry_words = words;
     TKV_CUDA(cudaMemsetAsync(memo_meta_.ptr, 0, 64, stream_));
     memo_reset_locked();
+    // Keep the slot table (64 B per slot) resident in L2 for this stream's
+    // kernels: a memo hit is one dependent load per chunk on the serial
+    // chain, and the KV transfers between lookups (streaming loads/stores)
+    // would otherwise evict it to DRAM. Best effort: ignored if unsupported.
+    const size_t slot_bytes = slots * 64;
+    int max_persist = 0;
+    cudaDeviceGetAttribute(&max_persist, cudaDevAttrMaxPersistingL2CacheSize, device_);
+    if (max_persist > 0) {
+        size_t cur = 0;
+        cudaDeviceGetLimit(&cur, cudaLimitPersistingL2CacheSize);
+        const size_t want = std::min<size_t>(size_t(max_persist), std::max(cur, slot_bytes));
+        if (cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, want) == cudaSuccess) {
+            cudaStreamAttrValue attr{};
+            attr.accessPolicyWindow.base_ptr = memo_slots_.ptr;
+            attr.accessPolicyWindow.num_bytes = std::min(slot_bytes, want);
+            attr.accessPolicyWindow.hitRatio = 1.0f;
+            attr.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+            attr.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+            cudaStreamSetAttribute(stream_, cudaStreamAttributeAccessPolicyWindow, &attr);
+        }
+        cudaGetLastError();
+    }
     TKV_CUDA(cudaStreamSynchronize(stream_));
 }
 
 void KeyHasher::memo_reset_locked() {
-    TKV_CUDA(cudaMemsetAsync(memo_.slots, 0, (size_t(memo_.slot_mask) + 1) * 8, stream_));
+    TKV_CUDA(cudaMemsetAsync(memo_.slots, 0, (size_t(memo_.slot_mask) + 1) * 64, stream_));
     TKV_CUDA(cudaMemsetAsync(memo_.counter, 0, sizeof(unsigned int), stream_));
     memo_used_bound_ = 0;
     ++memo_resets_;
@@ -127,7 +192,14 @@ KeyHasher::MemoStats KeyHasher::memo_stats() {
     s.misses = st[1];
     s.capacity = memo_.entry_cap;
     s.resets = memo_resets_ - 1;  // the enabling clear is not a reset
+    s.rehashes = memo_rehashes_;
     return s;
+}
+
+void KeyHasher::debug_poison_memo() {
+    std::lock_guard lock(mu_);
+    TKV_CUDA(launch_memo_poison(memo_, stream_));
+    TKV_CUDA(cudaStreamSynchronize(stream_));
 }
 
 std::vector<Digest> KeyHasher::hash_one(TokenSpanView seq, const Digest& parent) {

@@ -57,9 +57,12 @@ public:
     // kept on the device; 0 disables. Exact: hits are verified token by token.
     void enable_memo(size_t entries);
     struct MemoStats {
-        uint64_t hits = 0, misses = 0, capacity = 0, resets = 0;
+        uint64_t hits = 0, misses = 0, capacity = 0, resets = 0, rehashes = 0;
     };
     MemoStats memo_stats();
+    // Test hook: corrupt every memo slot's digest (hits must then fail
+    // verification and be re-hashed).
+    void debug_poison_memo();
 
 private:
     void memo_reset_locked();
@@ -68,7 +71,9 @@ private:
     int device_;
     std::mutex mu_;
     Stream stream_;
-    PinnedBuffer h_tokens_, h_chains_, h_out_;  // mapped: K3 reads/writes them directly
+    PinnedBuffer h_tokens_, h_chains_, h_out_, h_bad_;  // mapped host side of a launch
+    DeviceBuffer d_tokens_, d_chains_, d_out_, d_hit_;  // HBM copies the kernels work on
+    uint64_t memo_rehashes_ = 0;
     uint64_t launches_ = 0, chunks_ = 0;
     // memo (device): slots, entries, counter + stats
     DeviceBuffer memo_slots_, memo_entries_, memo_meta_;

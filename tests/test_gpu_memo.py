@@ -51,6 +51,22 @@ def test_memo_keys_equal_oracle(tkv, C, entries):
     e.close()
 
 
+def test_memo_false_hit_is_caught_and_rehashed(tkv, C):
+    """Corrupt every memo slot's digest: the optimistic chain then follows a
+    wrong digest, the parallel verification must flag it and the chain must be
+    re-hashed, giving the oracle keys."""
+    from paper_2510_09665_b200.api import Engine
+    e = Engine(num_layers=2, bpt=64, page_tokens=16, tag=TAG, chunk_size=256, ram_slots=2, num_pages=4096)
+    rng = np.random.default_rng(42)
+    doc = rng.integers(0, 128256, size=256 * 9 + 40, dtype=np.uint32)
+    assert _keys_via_connector(e, 1, doc) == C.chunk_keys(doc, 256, TAG)
+    e.debug_poison_memo()
+    before = e.memo_stats()["rehashes"]
+    assert _keys_via_connector(e, 2, doc) == C.chunk_keys(doc, 256, TAG)
+    assert e.memo_stats()["rehashes"] == before + 1
+    e.close()
+
+
 def test_memo_does_not_change_connector_outcomes(tkv, C):
     """The connector scenarios give the reference outcome with the memo on
     (default) and off."""
