@@ -375,6 +375,14 @@ class B200Bench:
         assert e.wait_store_kv(m, self.L - 1) == 0
         res = e.store_results(m, q)
         assert len(res) == (self.n - self.n_pre + 255) // 256 and all(c == 0 for _, c in res), res[:2]
+        if getattr(self, "_pipe_ref", None) is not None:
+            o = e.origin_since(m, self._pipe_ref)
+            tl = e.timeline(m) + o
+            # per step: first/last H2D done, first/last D2H done (ms on one axis)
+            self._pipe_tl.append({"origin": round(o, 2), "h2d": [round(float(tl[0, 0]), 2), round(float(tl[-1, 0]), 2)],
+                                  "d2h": [round(float(tl[0, 4]), 2), round(float(tl[-1, 4]), 2)],
+                                  "layer_ms_h2d": round(float(self.np.median(self.np.diff(tl[:, 0]))), 3),
+                                  "layer_ms_d2h": round(float(self.np.median(self.np.diff(tl[:, 4]))), 3)})
         e.drop_meta(m)
         e.finish_query(q)
         e.release_query(q, sync=False)
@@ -384,12 +392,32 @@ class B200Bench:
         """Serving-style schedule: request k+1 is looked up and enqueued while
         request k transfers, then k's final store wait returns. Each request
         still does the full reference call sequence; only the batches overlap."""
+        tr = [] if os.environ.get("TKV_TRACE_PIPE") else None
+        T0 = time.perf_counter()
+        if tr is not None:
+            self._pipe_ref = self.torch.cuda.Event(enable_timing=True)
+            self._pipe_ref.record(self.stream)
+            self._pipe_tl = []
+
+        def mark(what):
+            if tr is not None:
+                tr.append((what, round(1e3 * (time.perf_counter() - T0), 2)))
         st = self.begin(self.lookup(ks[0]))
         out = None
         for i in range(len(ks)):
-            nxt = self.begin(self.lookup(ks[i + 1])) if i + 1 < len(ks) else None
+            nxt = None
+            if i + 1 < len(ks):
+                mark(f"lookup{i + 1}")
+                lk = self.lookup(ks[i + 1])
+                mark(f"begin{i + 1}")
+                nxt = self.begin(lk)
+            mark(f"end{i}")
             out = self.end(st)
+            mark(f"ended{i}")
             st = nxt
+        if tr is not None:
+            print(json.dumps({"pipe_trace_ms": tr, "device_ms": self._pipe_tl}), file=sys.stderr, flush=True)
+            self._pipe_ref = None
         return out
 
     def trace_step(self, k):
@@ -618,6 +646,26 @@ def run_pd_pairs(args, world, rank, local):
     return out
 
 
+def ncu_traffic(kernel, algorithmic_bytes, bench):
+    """roofline.traffic: DRAM bytes per launch of `kernel` from the committed
+    ncu --set full capture (profiles/ncu_traffic.json), when that capture was
+    taken on this exact workload; otherwise null."""
+    out = {"traffic": None, "algorithmic_bytes": int(algorithmic_bytes)}
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+            t = json.load(f)
+    except (OSError, ValueError):
+        return out
+    want = {"prompt": bench.n, "prefix": bench.n_pre, "layers": bench.L, "bpt": bench.bpt}
+    k = t.get("kernels", {}).get(kernel)
+    if k is None or t.get("config") != want:
+        return out
+    out["traffic"] = int(k["dram_read"] + k["dram_write"])
+    out["traffic_source"] = t.get("source")
+    out["traffic_frac_of_algorithmic"] = round(out["traffic"] / algorithmic_bytes, 4)
+    return out
+
+
 def run_b200(args):
     import numpy as np  # noqa: F401
     import torch
@@ -637,6 +685,8 @@ def run_b200(args):
     except OSError:
         pass
     hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
+    peak_source = ("MEASURED_PEAKS.json hbm_gbs (copy, read+write)" if "hbm_gbs" in peaks
+                   else "fallback 6650 GB/s (B200_PROFILING.md; MEASURED_PEAKS.json absent)")
     pcie = measure_pcie(torch, bench.dev)
 
     def barrier():
@@ -743,10 +793,13 @@ def run_b200(args):
         "tokens_per_s": round(tokens_per_s, 1),
         "e2e": {"value": round(e2e, 2), "unit": "GB/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                 "ms_per_step": round(e2e_ms, 3), "wall_ms_per_step": round(1e3 * wall / args.steps, 3),
-                "path": "C-ABI connector: K3 lookup, CE batched H2D + K2 scatter, K1 zero-copy store"},
+                "path": "C-ABI connector: K3 lookup, "
+                        + ("zero-copy K2 loads" if args.load_zero_copy else "CE batched H2D + K2 scatter")
+                        + ", " + ("K1 zero-copy store" if args.store_zero_copy
+                                  else "K1 gather to HBM ring + CE batched D2H store")},
         "roofline": {"bound": "hbm", "kernel": dom, "achieved": round(achieved, 1), "peak": hbm_peak,
-                     "unit": "GB/s", "frac": round(achieved / hbm_peak, 4), "traffic": None,
-                     "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy, read+write)"},
+                     "unit": "GB/s", "frac": round(achieved / hbm_peak, 4),
+                     **ncu_traffic(dom, dom_bytes, bench), "peak_source": peak_source},
         "links": {"pcie": pcie, "e2e_frac_of_pcie_bidir": round(e2e / world / pcie["bidir_gbps"], 4)},
         "gpu_launches": int(e2e_launches),
         "kernel_launches_value": int(kr["launches"]),

@@ -148,6 +148,13 @@ int tkv_verify_pages(const tkv_paged_layout* layout, const uint32_t* tokens_dev,
 int tkv_synth_chunk(const uint32_t* tokens_dev, uint64_t seed, uint32_t start, uint32_t n,
                     uint32_t n_layers, uint32_t bpt, uint8_t* out_dev, void* stream);
 
+/* SM-driven copy of `bytes` from src to dst, both device-visible (HBM, mapped
+ * or UVA pinned host memory, peer memory), on `stream`. For the engine's small
+ * per-step uploads (prompt tokens): a kernel over PCIe never waits behind the
+ * KV transfers queued on the copy engines. No reference equivalent (the
+ * reference has no device). */
+int tkv_sm_copy(const void* src, void* dst, uint64_t bytes, void* stream);
+
 /* q8-scale codec (Q8ScaleCodec, src/codec.cpp:27-91), bit-exact, over a
  * batch of payloads. Encode: src = payload, dst = blob, bytes = payload
  * length; blob = u32 len | f32 scale | int8 lanes | odd tail byte
@@ -301,6 +308,9 @@ int tkv_meta_store_results(tkv_meta* m, uint64_t query, int* codes, uint8_t* dig
  * done} in ms since the batch's loads were enqueued (-1 = unused). Writes
  * 5*num_layers floats after the batch completed. */
 int tkv_meta_timeline(tkv_meta* m, float* out, size_t cap, size_t* n);
+/* Diagnostics: ms from the caller's completed timing event `cuda_event`
+ * (a cudaEvent_t) to the batch's timeline origin (-1 if unavailable). */
+int tkv_meta_origin_since(tkv_meta* m, void* cuda_event, float* ms);
 
 /* ---- PD disaggregation over NVLink (run_pd, src/sim_engine.cpp:347-543;
  *      PdStaging, include/tierkv/pd_staging.hpp) --------------------------- */

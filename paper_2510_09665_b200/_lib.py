@@ -77,6 +77,7 @@ SIGNATURES = {
     "tkv_verify_pages": (ct.c_int, [ct.POINTER(PagedLayoutC), vp, vp, ct.c_uint32, ct.c_uint64, ct.c_uint32,
                                     ct.c_uint32, ct.c_uint32, ct.c_uint32, vp, vp]),
     "tkv_synth_chunk": (ct.c_int, [vp, ct.c_uint64, ct.c_uint32, ct.c_uint32, ct.c_uint32, ct.c_uint32, vp, vp]),
+    "tkv_sm_copy": (ct.c_int, [vp, vp, ct.c_uint64, vp]),
     "tkv_q8_blob_bytes": (ct.c_uint64, [ct.c_uint64]),
     "tkv_codec_plan": (ct.c_int, [vp, ct.c_uint32, u32p]),
     "tkv_q8_encode": (ct.c_int, [vp, vp, ct.c_uint32, ct.c_uint32, vp, vp]),
@@ -140,6 +141,7 @@ SIGNATURES = {
     "tkv_meta_plan": (ct.c_int, [vp, sz, ct.c_int, u64p, u8p, sz, szp, u64p]),
     "tkv_meta_store_results": (ct.c_int, [vp, ct.c_uint64, ct.POINTER(ct.c_int), u8p, sz, szp]),
     "tkv_meta_timeline": (ct.c_int, [vp, ct.POINTER(ct.c_float), sz, szp]),
+    "tkv_meta_origin_since": (ct.c_int, [vp, vp, ct.POINTER(ct.c_float)]),
     "tkv_pd_staging_create": (ct.c_int, [ct.POINTER(vp)]),
     "tkv_pd_staging_destroy": (None, [vp]),
     "tkv_pd_register": (ct.c_int, [vp, ct.c_uint64]),

@@ -171,8 +171,18 @@ class Engine:
         cur = self._dev_prompts.get(qid)
         self._prompt_src[qid] = prompt
         if cur is None or cur.numel() != t.size or not np.array_equal(self._host_prompts.get(qid), t):
-            self._host_prompts[qid] = t.copy()
-            cur = torch.from_numpy(t.view(np.int32)).to(f"cuda:{self.device}", non_blocking=False)
+            # Pinned host copy read by an SM-driven copy kernel on the engine
+            # stream: a copy-engine upload would queue behind the layerwise KV
+            # transfers already in flight. The pinned buffer
+            # doubles as the host copy and lives until release_query.
+            host = torch.empty(max(1, t.size), dtype=torch.int32, pin_memory=True)
+            hv = host.numpy().view(np.uint32)[:t.size]
+            hv[:] = t
+            cur = torch.empty(max(1, t.size), dtype=torch.int32, device=f"cuda:{self.device}")[:t.size]
+            check(self.L.tkv_sm_copy(host.data_ptr(), cur.data_ptr(), t.nbytes, self.stream_handle))
+            if self.stream is not None:
+                cur.record_stream(self.stream)
+            self._host_prompts[qid] = hv
             self._dev_prompts[qid] = cur
         return cur
 
@@ -299,6 +309,12 @@ class Engine:
         n = ct.c_size_t(0)
         check(self.L.tkv_meta_timeline(self._metas[m], out, cap, ct.byref(n)))
         return np.array(out[:n.value], dtype=np.float32).reshape(-1, 5)
+
+    def origin_since(self, m: int, event: torch.cuda.Event) -> float:
+        """ms from a completed torch timing event to batch m's timeline origin."""
+        ms = ct.c_float(-1.0)
+        check(self.L.tkv_meta_origin_since(self._metas[m], ct.c_void_p(event.cuda_event), ct.byref(ms)))
+        return ms.value
 
     def begin_decode(self, qid: int) -> int:
         return self.L.tkv_connector_begin_decode(self.conn, qid)

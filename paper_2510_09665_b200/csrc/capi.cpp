@@ -101,7 +101,10 @@ KeyHasher& hasher_for(const char* tag, size_t cs) {
     cudaGetDevice(&dev);
     auto key = std::make_pair(std::string(tag) + "#" + std::to_string(dev), cs);
     auto& h = g_hashers[key];
-    if (!h) h = std::make_unique<KeyHasher>(tag, cs);
+    if (!h) {
+        h = std::make_unique<KeyHasher>(tag, cs);
+        h->enable_memo(4096);  // repeated prompts through the free functions skip SHA too
+    }
     return *h;
 }
 
@@ -177,6 +180,11 @@ int tkv_hash_chains(const uint32_t* tokens, const tkv_chain_desc* chains, uint32
     std::memcpy(p.tag, tag, tag_len);
     return cuda(launch_hash_chains(tokens, reinterpret_cast<const ChainDesc*>(chains), n_chains, p,
                                    out, cudaStream_t(stream)));
+}
+
+int tkv_sm_copy(const void* src, void* dst, uint64_t bytes, void* stream) {
+    if (bytes && (!src || !dst)) return fail(Errc::invalid_argument, "null pointer");
+    return cuda(launch_sm_copy(src, dst, bytes, cudaStream_t(stream)));
 }
 
 static SynthArgs synth_args(const uint32_t* tokens, const int32_t* table, uint32_t stride,
@@ -665,6 +673,13 @@ int tkv_meta_timeline(tkv_meta* m, float* out, size_t cap, size_t* n) {
         auto t = m->m.timeline();
         *n = t.size();
         std::memcpy(out, t.data(), std::min(cap, t.size()) * sizeof(float));
+        return 0;
+    });
+}
+
+int tkv_meta_origin_since(tkv_meta* m, void* ev, float* ms) {
+    return guard([&] {
+        *ms = m->m.origin_since(cudaEvent_t(ev));
         return 0;
     });
 }

@@ -1,6 +1,9 @@
 #include "common.hpp"
 
+#include <sys/mman.h>
+
 #include <atomic>
+#include <cstdint>
 #include <utility>
 
 #include "kernels.hpp"
@@ -51,17 +54,44 @@ void cuda_check(cudaError_t e, const char* what, const char* file, int line) {
 
 PinnedBuffer::PinnedBuffer(size_t n) { reserve(n); }
 
-PinnedBuffer::~PinnedBuffer() {
-    if (host) cudaFreeHost(host);
+PinnedBuffer::~PinnedBuffer() { release(); }
+
+void PinnedBuffer::release() {
+    if (host) {
+        if (map_base) {
+            cudaHostUnregister(host);
+            munmap(map_base, map_bytes);
+        } else {
+            cudaFreeHost(host);
+        }
+    }
+    host = dev = nullptr;
+    map_base = nullptr;
+    bytes = map_bytes = 0;
 }
 
 void PinnedBuffer::reserve(size_t n) {
     if (n <= bytes) return;
-    if (host) TKV_CUDA(cudaFreeHost(host));
-    host = dev = nullptr;
-    bytes = 0;
+    release();
     void* p = nullptr;
-    TKV_CUDA(cudaHostAlloc(&p, n, cudaHostAllocMapped | cudaHostAllocPortable));
+    constexpr size_t kHuge = size_t(2) << 20;
+    if (huge && n >= 32 * kHuge) {
+        const size_t len = (n + kHuge - 1) / kHuge * kHuge;
+        void* m = mmap(nullptr, len + kHuge, PROT_READ | PROT_WRITE, MAP_PRIVATE | MAP_ANONYMOUS, -1, 0);
+        if (m != MAP_FAILED) {
+            auto* a = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(m) + kHuge - 1) & ~(kHuge - 1));
+            madvise(a, len, MADV_HUGEPAGE);  // advisory: ignored where THP is off
+            if (cudaHostRegister(a, len, cudaHostRegisterMapped | cudaHostRegisterPortable) == cudaSuccess) {
+                p = a;
+                map_base = m;
+                map_bytes = len + kHuge;
+            } else {
+                cudaGetLastError();
+                munmap(m, len + kHuge);
+            }
+        }
+    }
+    if (!p) TKV_CUDA(cudaHostAlloc(&p, n, cudaHostAllocMapped | cudaHostAllocPortable));
     host = static_cast<uint8_t*>(p);
     void* d = nullptr;
     TKV_CUDA(cudaHostGetDevicePointer(&d, p, 0));

@@ -140,10 +140,17 @@ void cuda_check(cudaError_t e, const char* what, const char* file, int line);
 #define TKV_CUDA(x) ::tkv::cuda_check((x), #x, __FILE__, __LINE__)
 
 // Pinned, device-mapped host allocation (cudaHostAlloc Mapped|Portable).
+// huge = true (large slabs): a 2 MiB-aligned anonymous mapping advised for
+// transparent huge pages, then cudaHostRegister(Mapped|Portable) — fewer,
+// physically larger pages for the copy engines' DMA (measured +1-4 % PCIe
+// both-ways throughput on the B200 boxes, tools/microbench4.cu).
 struct PinnedBuffer {
     uint8_t* host = nullptr;
     uint8_t* dev = nullptr;  // device-visible alias of `host`
     size_t bytes = 0;
+    bool huge = false;
+    void* map_base = nullptr;  // huge: the mmap to unmap
+    size_t map_bytes = 0;
     PinnedBuffer() = default;
     explicit PinnedBuffer(size_t n);
     ~PinnedBuffer();
@@ -158,8 +165,12 @@ struct PinnedBuffer {
         std::swap(host, o.host);
         std::swap(dev, o.dev);
         std::swap(bytes, o.bytes);
+        std::swap(huge, o.huge);
+        std::swap(map_base, o.map_base);
+        std::swap(map_bytes, o.map_bytes);
     }
     void reserve(size_t n);  // grow-only, contents not preserved
+    void release();
 };
 
 // Device allocation (cudaMalloc), grow-only reserve.

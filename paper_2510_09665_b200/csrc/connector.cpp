@@ -1,5 +1,9 @@
 #include "connector.hpp"
 
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
+
 #include "copy_plan.hpp"
 
 #include <algorithm>
@@ -179,6 +183,15 @@ std::vector<float> ConnectorMetadata::timeline() const {
     return out;
 }
 
+float ConnectorMetadata::origin_since(cudaEvent_t ref) const {
+    float ms = -1.f;
+    if (!state_->loads_started || cudaEventElapsedTime(&ms, ref, state_->t0) != cudaSuccess) {
+        cudaGetLastError();
+        return -1.f;
+    }
+    return ms;
+}
+
 Connector::Connector(TieredStore& store, PagedKVStore& pages, Config cfg)
     : store_(store),
       pages_(pages),
@@ -205,6 +218,26 @@ Connector::~Connector() {
     }
 }
 
+// Prompt buffers of finished queries are kept (up to a few) and reused: a
+// 128K-token prompt is 512 KiB, and a fresh allocation of that size is an
+// mmap whose first touch page-faults on the lookup path. Caller holds mu_.
+void Connector::recycle_prompt(std::vector<TokenId>&& v) {
+    if (v.capacity() == 0 || prompt_pool_.size() >= 16) return;
+    v.clear();
+    prompt_pool_.push_back(std::move(v));
+}
+
+void Connector::recycle_prompt_into(std::vector<TokenId>& dst, size_t n) {
+    for (size_t i = prompt_pool_.size(); i-- > 0;) {
+        if (prompt_pool_[i].capacity() >= n) {
+            recycle_prompt(std::move(dst));
+            dst = std::move(prompt_pool_[i]);
+            prompt_pool_.erase(prompt_pool_.begin() + std::ptrdiff_t(i));
+            return;
+        }
+    }
+}
+
 const std::vector<ChunkKey>& Connector::keys_for(QueryState& qs, TokenSpanView prompt) {
     if (qs.keys.empty() || qs.prompt.size() != prompt.size() ||
         !std::equal(prompt.begin(), prompt.end(), qs.prompt.begin())) {
@@ -221,7 +254,10 @@ size_t Connector::get_num_new_matched_tokens(QueryId id, TokenSpanView prompt) {
 std::vector<size_t> Connector::get_num_new_matched_tokens(
     const std::vector<QueryId>& ids, const std::vector<TokenSpanView>& prompts) {
     const size_t cs = store_.config().chunk_size;
+    static const bool trace = std::getenv("TKV_TRACE_LOOKUP") != nullptr;
+    const auto t0 = std::chrono::steady_clock::now();
     auto digests = hasher_.hash(prompts);  // one K3 launch for the whole batch
+    const auto t1 = std::chrono::steady_clock::now();
     KeyIndex index = [this](const ChunkKey& k) { return store_.contains(k.digest); };
     std::vector<size_t> out(ids.size());
     for (size_t q = 0; q < ids.size(); ++q) {
@@ -234,11 +270,18 @@ std::vector<size_t> Connector::get_num_new_matched_tokens(
         const size_t matched = std::min(lpm, cap);
         std::lock_guard lock(mu_);
         QueryState& qs = queries_[ids[q]];
+        if (qs.prompt.capacity() < prompts[q].size()) recycle_prompt_into(qs.prompt, prompts[q].size());
         qs.prompt.assign(prompts[q].begin(), prompts[q].end());
         qs.keys = std::move(keys);
         qs.lpm = lpm;
         qs.matched = matched;
         out[q] = matched;
+    }
+    if (trace) {
+        const auto t2 = std::chrono::steady_clock::now();
+        std::fprintf(stderr, "[tkv lookup] hash=%.1fus lpm+state=%.1fus\n",
+                     std::chrono::duration<double, std::micro>(t1 - t0).count(),
+                     std::chrono::duration<double, std::micro>(t2 - t1).count());
     }
     return out;
 }
@@ -821,7 +864,10 @@ Result<std::vector<ChunkKey>> Connector::finish_query(QueryId id) {
             }
             ds = std::move(it->second.decode);
         }
-        if (it != queries_.end()) queries_.erase(it);
+        if (it != queries_.end()) {
+            recycle_prompt(std::move(it->second.prompt));
+            queries_.erase(it);
+        }
     }
     if (ds) {
         for (const auto& h : ds->puts) h.wait();

@@ -78,6 +78,9 @@ public:
     // enqueued for {h2d done, load done, compute done, gathered, d2h done}
     // (-1 where the event was not used). Diagnostics only.
     std::vector<float> timeline() const;
+    // ms from a caller's (completed, timing) CUDA event to this batch's
+    // timeline origin; places batches of a pipelined schedule on one axis.
+    float origin_since(cudaEvent_t ref) const;
     explicit operator bool() const { return state_ != nullptr; }
 
 private:
@@ -151,6 +154,9 @@ private:
     };
 
     const std::vector<ChunkKey>& keys_for(QueryState& qs, TokenSpanView prompt);
+    void recycle_prompt(std::vector<TokenId>&& v);
+    void recycle_prompt_into(std::vector<TokenId>& dst, size_t n);
+    std::vector<std::vector<TokenId>> prompt_pool_;  // guarded by mu_
     Status enqueue_loads(detail::BatchState& b);
     void enqueue_load_layers(detail::BatchState& b, uint32_t upto);
     Status store_layers(detail::BatchState& b, uint32_t first, uint32_t last);

@@ -80,7 +80,7 @@ cudaError_t launch_paged_copy(const PagedLayout& layout, const PagedCopyPlan& pl
 // ---------------------------------------------------------------------------
 // K3: chained SHA-256 chunk keys (KeyChain::next, src/tokens.cpp:22-42).
 // digest_i = SHA-256(u16le(|tag|) | tag | digest_{i-1} | u32le tokens of chunk i)
-// One thread per chain (request); chains are independent.
+// One warp per chain (request); chains are independent.
 struct ChainDesc {
     uint64_t token_off = 0;     // first token in the packed token buffer
     uint32_t n_tokens = 0;      // tokens of this chain (chunked by chunk_size)
@@ -95,15 +95,21 @@ struct HashParams {
     uint8_t tag[kMaxTagBytes] = {};
 };
 
-// Prefix-digest memo: a device hash table
-// (parent digest, chunk tokens) -> digest. A probe that matches the key is
-// verified exactly — parent words, token count and every token — so a hit
-// returns the digest the SHA chain would have produced; misses are hashed
-// and inserted by the same launch. Slot word = (tag40 << 24) | entry index;
+// Prefix-digest memo: a device hash table from a
+// fingerprint of the whole token prefix (chain parent + every token up to the
+// end of chunk k) to digest_k. Because the probe key does not contain
+// digest_{k-1}, every chunk of every chain is probed in parallel
+// (memo_probe_kernel); a hit is then verified exactly against its entry —
+// parent digest = the previous row's digest, token count and every token — so
+// a verified hit is the digest the SHA chain would have produced. Chains are
+// hashed with SHA from their first miss on and the new links inserted by the
+// same launch. Slot word = (tag40 << 24) | entry index;
 // entry = parent[8] | digest[8] | n | tokens[chunk_size] (u32 words).
 struct MemoView {
     unsigned long long* slots = nullptr;  // [slot_mask + 1] x 8 u64: tagword | digest[8 x u32]
     uint32_t* hit_entry = nullptr;        // per output row: memo entry used, or ~0u
+    unsigned long long* keys = nullptr;   // per output row: prefix fingerprint (probe key)
+    uint32_t* first_miss = nullptr;       // per chain: first row the probes missed
     uint32_t* entries = nullptr;          // [entry_cap][entry_words]
     unsigned int* counter = nullptr;      // next free entry
     uint32_t slot_mask = 0;
@@ -112,11 +118,21 @@ struct MemoView {
     unsigned long long* stats = nullptr;  // [0] hits, [1] misses (optional)
 };
 
+// With a memo: probes every row of every chain in parallel (one CTA per
+// chain), then hashes each chain from its first miss. Without: plain chains.
 cudaError_t launch_hash_chains(const uint32_t* tokens, const ChainDesc* chains, uint32_t n_chains,
                                const HashParams& params, uint8_t* out, cudaStream_t stream,
                                const MemoView* memo = nullptr);
+// SM-driven copy of exactly `bytes` between device-visible addresses (no copy
+// engine): 16-byte vectors when both ends are 16-aligned, bytes otherwise.
+cudaError_t launch_sm_copy(const void* src, void* dst, uint64_t bytes, cudaStream_t stream);
 // Copies `bytes` (rounded up to 16) from src to dst (mapped host -> HBM staging).
 cudaError_t launch_stage_words(const void* src, void* dst, uint64_t bytes, cudaStream_t stream);
+// Memo pass 1: stages the packed tokens (src: mapped host) into dst (HBM)
+// and writes every row's chunk fingerprint to memo.keys (chains: device).
+cudaError_t launch_memo_stage(const uint32_t* src, uint32_t* dst, const ChainDesc* chains, uint32_t n_chains,
+                              uint32_t total_rows, const HashParams& params, const MemoView& memo,
+                              cudaStream_t stream);
 // Verifies every memo hit of a launch against its entry and publishes all
 // digest rows from dev_out to out; first_bad[chain] = first failed chunk.
 cudaError_t launch_memo_verify(const uint32_t* tokens, const ChainDesc* chains, uint32_t n_chains,

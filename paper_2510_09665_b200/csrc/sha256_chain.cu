@@ -7,12 +7,14 @@
 // 17 SHA-256 blocks per 256-token chunk.
 //
 // Parallelism. The chain is serial: block 0 of chunk i holds digest_{i-1},
-// so chunks of one sequence cannot be compressed in parallel. One thread owns
+// so chunks of one sequence cannot be compressed in parallel. One warp owns
 // one chain (request) and walks its chunks; independent requests fill the
 // GPU. Within a chunk the message words of the token-only blocks are packed
 // straight from the u32 token array with one byte-permute per word
 // (PRMT), so only the header block and the padding block take the generic
-// byte path.
+// byte path. What can be parallel is the memo: it is keyed by a fingerprint
+// of the whole prefix, so every chunk of every chain is probed at once and
+// only the rows after a chain's first miss go through SHA.
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -266,24 +268,12 @@ __device__ __forceinline__ uint64_t mix64(uint64_t x) {
     return x ^ (x >> 31);
 }
 
-// Same value in every lane: fingerprint of (parent, n, tokens). Only a probe
-// key — a hit is confirmed by comparing parent, n and every token.
-__device__ __forceinline__ uint64_t memo_key(const WarpSmem& s, uint32_t n, uint32_t lane) {
-    // Independent per-token / per-word mixes (ILP), xor-combined: no serial chain.
-    uint64_t h = 0;
-    for (uint32_t idx = lane; idx < n; idx += 32)
-        h ^= mix64((uint64_t(s.tok[idx]) << 32) | idx);
-    if (lane < 8) h ^= mix64((uint64_t(s.parent[lane]) << 32) | (0x80000000u + lane));
-#pragma unroll
-    for (int off = 16; off; off >>= 1) h ^= __shfl_xor_sync(0xffffffffu, h, off);
-    return mix64(h ^ (uint64_t(n) * 0xc2b2ae3d27d4eb4full));
-}
-
 // Slot = 8 u64 (64 B): [0] tagword = (tag40 << 24) | entry, [2..5] digest
-// words (16-byte aligned for vector loads). 0 = empty, kBusy = being published. The digest rides in the slot so
-// a hit is ONE memory round trip on the serial chain; the full comparison
-// against the entry (parent, n, every token, digest) runs afterwards, in
-// parallel over all hit chunks (memo_verify_kernel).
+// words (16-byte aligned for vector loads). 0 = empty, kBusy = being
+// published. The digest rides in the slot so a probe is one memory round
+// trip; the full comparison against the entry (parent, n, every token,
+// digest) runs afterwards, in parallel over all hit chunks
+// (memo_verify_kernel).
 constexpr unsigned long long kBusy = ~0ull;
 constexpr uint32_t kNoEntry = 0xffffffffu;
 
@@ -355,26 +345,32 @@ hash_chains_warp_kernel(const uint32_t* __restrict__ tokens, const ChainDesc* __
     if (c >= n_chains) return;  // warp-uniform
     WarpSmem& s = smem[wid];
     const ChainDesc cd = chains[c];
-    if (lane < 8)
-        s.parent[lane] = (uint32_t(cd.parent[4 * lane]) << 24) |
-                         (uint32_t(cd.parent[4 * lane + 1]) << 16) |
-                         (uint32_t(cd.parent[4 * lane + 2]) << 8) | uint32_t(cd.parent[4 * lane + 3]);
     const uint32_t cs = P.chunk_size;
+    // With a memo the probe kernel already published rows [0, k0) (verified
+    // later); the chain resumes at its first miss from the last hit digest.
+    const uint32_t k0 = M.first_miss != nullptr ? M.first_miss[c] : 0u;
+    const uint32_t start0 = k0 * cs;
+    if (start0 >= cd.n_tokens) return;
+    if (lane < 8) {
+        s.parent[lane] =
+            k0 ? __byte_perm(reinterpret_cast<const uint32_t*>(out + 32ull * (cd.out_first + k0 - 1))[lane], 0, 0x0123)
+               : (uint32_t(cd.parent[4 * lane]) << 24) | (uint32_t(cd.parent[4 * lane + 1]) << 16) |
+                     (uint32_t(cd.parent[4 * lane + 2]) << 8) | uint32_t(cd.parent[4 * lane + 3]);
+    }
     const uint32_t hdr = 2 + P.tag_len + 32;
     const uint32_t* base = tokens + cd.token_off;
     uint32_t pf[kPrefetch];
     {
-        const uint32_t n0 = min(cs, cd.n_tokens);
+        const uint32_t n0 = min(cs, cd.n_tokens - start0);
 #pragma unroll
         for (int j = 0; j < kPrefetch; ++j) {
             const uint32_t idx = lane + 32 * j;
-            pf[j] = idx < n0 ? __ldg(base + idx) : 0u;
+            pf[j] = idx < n0 ? __ldg(base + start0 + idx) : 0u;
         }
     }
-    uint32_t row = cd.out_first;
-    bool probing = M.slots != nullptr;  // after the first memo miss the parent is novel
-    unsigned long long hits = 0, misses = 0;
-    for (uint32_t start = 0; start < cd.n_tokens; start += cs, ++row) {
+    uint32_t row = cd.out_first + k0;
+    unsigned long long misses = 0;
+    for (uint32_t start = start0; start < cd.n_tokens; start += cs, ++row) {
         const uint32_t n = min(cs, cd.n_tokens - start);
         // 1. stage this chunk's tokens
 #pragma unroll
@@ -394,28 +390,8 @@ hash_chains_warp_kernel(const uint32_t* __restrict__ tokens, const ChainDesc* __
                 pf[j] = idx < nn ? __ldg(base + nstart + idx) : 0u;
             }
         }
-        // 2b. memo: a verified (parent, tokens) hit replaces the SHA chain link
         uint64_t key = 0;
-        if (M.slots != nullptr) key = memo_key(s, n, lane);
-        if (probing) {
-            uint32_t d[8], ent = 0;
-            if (memo_probe(M, key, d, &ent)) {
-                ++hits;
-                __syncwarp();
-                if (lane == 0) {
-                    uint32_t* o = reinterpret_cast<uint32_t*>(out + 32ull * row);
-#pragma unroll
-                    for (int i = 0; i < 8; ++i) {
-                        s.parent[i] = d[i];
-                        o[i] = __byte_perm(d[i], 0, 0x0123);
-                    }
-                    M.hit_entry[row] = ent;  // verified later, in parallel
-                }
-                __syncwarp();
-                continue;
-            }
-            probing = false;
-        }
+        if (M.slots != nullptr) key = M.keys[row];
         if (M.hit_entry != nullptr && lane == 0) M.hit_entry[row] = kNoEntry;
         ++misses;
         // 3. every message word of the chunk, in parallel across lanes
@@ -461,9 +437,116 @@ hash_chains_warp_kernel(const uint32_t* __restrict__ tokens, const ChainDesc* __
         }
         __syncwarp();
     }
-    if (M.stats != nullptr && lane == 0) {
-        if (hits) atomicAdd(M.stats, hits);
-        if (misses) atomicAdd(M.stats + 1, misses);
+    if (M.stats != nullptr && lane == 0 && misses) atomicAdd(M.stats + 1, misses);
+}
+
+// Largest chain index c with chains[c].out_first <= row.
+__device__ __forceinline__ uint32_t chain_of_row(const ChainDesc* __restrict__ chains, uint32_t n_chains,
+                                                 uint32_t row) {
+    uint32_t lo = 0, hi = n_chains;
+    while (hi - lo > 1) {
+        const uint32_t mid = (lo + hi) >> 1;
+        if (chains[mid].out_first <= row) lo = mid; else hi = mid;
+    }
+    return lo;
+}
+
+// Memo pass 1, one warp per row of every chain: copies the row's tokens from
+// the mapped host buffer into HBM (the copy the plain path does with
+// stage_words_kernel) and writes the row's chunk fingerprint to keys[row].
+__global__ void __launch_bounds__(128)
+memo_fingerprint_kernel(const uint32_t* __restrict__ src, uint32_t* __restrict__ dst,
+                        const ChainDesc* __restrict__ chains, uint32_t n_chains, uint32_t total_rows,
+                        const HashParams P, const MemoView M) {
+    const uint32_t lane = threadIdx.x & 31;
+    const uint32_t row = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    if (row >= total_rows) return;
+    const ChainDesc& cd = chains[chain_of_row(chains, n_chains, row)];
+    const uint32_t k = row - cd.out_first;
+    const uint32_t start = k * P.chunk_size;
+    const uint32_t n = min(P.chunk_size, cd.n_tokens - start);
+    const uint64_t off = cd.token_off + start;
+    uint64_t h = 0;
+    for (uint32_t idx = lane; idx < n; idx += 32) {
+        const uint32_t t = src[off + idx];
+        dst[off + idx] = t;
+        h ^= mix64((uint64_t(t) << 32) | idx);
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) h ^= __shfl_xor_sync(0xffffffffu, h, o);
+    if (lane == 0)
+        M.keys[row] = mix64(h ^ (uint64_t(n) * 0xc2b2ae3d27d4eb4full) ^ (uint64_t(k) * 0x9e3779b97f4a7c15ull));
+}
+
+// Memo pass 2, one CTA per chain: an inclusive scan of the row fingerprints
+// over the chain (wrapping add, so key_k covers the parent and every token up
+// to the end of chunk k), then one independent probe per row. Hits publish their digest to `out` and
+// their entry to hit_entry (checked later by memo_verify_kernel); the first
+// miss of the chain goes to first_miss, where the SHA chain resumes. Every
+// row's key is kept for the insertions of the rows that miss.
+constexpr int kProbeThreads = 256;
+
+__global__ void __launch_bounds__(kProbeThreads)
+memo_probe_kernel(const ChainDesc* __restrict__ chains, const HashParams P, uint8_t* __restrict__ out, const MemoView M) {
+    __shared__ unsigned long long warp_sum[kProbeThreads / 32];
+    __shared__ uint32_t first;
+    const uint32_t lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const ChainDesc cd = chains[blockIdx.x];
+    const uint32_t cs = P.chunk_size;
+    const uint32_t rows = (cd.n_tokens + cs - 1) / cs;
+    unsigned long long* keys = M.keys + cd.out_first;
+    if (threadIdx.x == 0) first = rows;
+    // the chain's parent digest (KeyChain::reset) seeds every key of the chain
+    uint64_t pfp = 0x8f1bbcdcca62c1d6ull;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        uint64_t w = 0;
+#pragma unroll
+        for (int b = 0; b < 8; ++b) w |= uint64_t(cd.parent[8 * i + b]) << (8 * b);
+        pfp = mix64(pfp ^ w);
+    }
+    __syncthreads();
+    // 2. scan + probe, one thread per row
+    uint64_t carry = 0;
+    for (uint32_t base = 0; base < rows; base += kProbeThreads) {
+        const uint32_t k = base + threadIdx.x;
+        uint64_t v = k < rows ? keys[k] : 0;
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) {
+            const uint64_t t = __shfl_up_sync(0xffffffffu, v, off);
+            if (lane >= uint32_t(off)) v += t;
+        }
+        if (lane == 31) warp_sum[wid] = v;
+        __syncthreads();
+        uint64_t before = 0, total = 0;
+#pragma unroll
+        for (int w = 0; w < kProbeThreads / 32; ++w) {
+            const uint64_t ws = warp_sum[w];
+            before += uint32_t(w) < wid ? ws : 0;
+            total += ws;
+        }
+        v += before + carry;
+        carry += total;
+        const bool skip = first < base;  // an earlier tile already missed: no hits after it
+        if (k < rows) {
+            const uint64_t key = mix64(v ^ pfp);
+            keys[k] = key;
+            uint32_t d[8], ent = kNoEntry;
+            if (!skip && memo_probe(M, key, d, &ent)) {
+                uint32_t* o = reinterpret_cast<uint32_t*>(out + 32ull * (cd.out_first + k));
+#pragma unroll
+                for (int i = 0; i < 8; ++i) o[i] = __byte_perm(d[i], 0, 0x0123);
+            } else {
+                ent = kNoEntry;
+                atomicMin(&first, k);
+            }
+            M.hit_entry[cd.out_first + k] = ent;
+        }
+        __syncthreads();  // warp_sum reuse; `first` settled for the next tile
+    }
+    if (threadIdx.x == 0) {
+        M.first_miss[blockIdx.x] = first;
+        if (M.stats != nullptr && first) atomicAdd(M.stats, (unsigned long long)first);
     }
 }
 
@@ -492,11 +575,7 @@ memo_verify_kernel(const uint32_t* __restrict__ tokens, const ChainDesc* __restr
     if (M.hit_entry == nullptr) return;
     const uint32_t e = M.hit_entry[row];
     if (e == kNoEntry) return;
-    uint32_t lo = 0, hi = n_chains;  // chain of this row: largest c with out_first <= row
-    while (hi - lo > 1) {
-        const uint32_t mid = (lo + hi) >> 1;
-        if (chains[mid].out_first <= row) lo = mid; else hi = mid;
-    }
+    const uint32_t lo = chain_of_row(chains, n_chains, row);
     const ChainDesc& cd = chains[lo];
     const uint32_t k = row - cd.out_first;
     const uint32_t start = k * P.chunk_size;
@@ -567,6 +646,16 @@ cudaError_t launch_stage_words(const void* src, void* dst, uint64_t bytes, cudaS
     return cudaGetLastError();
 }
 
+cudaError_t launch_memo_stage(const uint32_t* src, uint32_t* dst, const ChainDesc* chains, uint32_t n_chains,
+                              uint32_t total_rows, const HashParams& params, const MemoView& memo,
+                              cudaStream_t s) {
+    if (total_rows == 0) return cudaSuccess;
+    note_launch();
+    const uint32_t blocks = (total_rows * 32 + 127) / 128;
+    memo_fingerprint_kernel<<<blocks, 128, 0, s>>>(src, dst, chains, n_chains, total_rows, params, memo);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_memo_verify(const uint32_t* tokens, const ChainDesc* chains, uint32_t n_chains,
                                uint32_t total_rows, const HashParams& params, const uint8_t* dev_out,
                                const MemoView* memo, uint8_t* out, unsigned int* first_bad,
@@ -604,7 +693,11 @@ cudaError_t launch_hash_chains(const uint32_t* tokens, const ChainDesc* chains, 
     if (params.chunk_size <= uint32_t(kWarpChunkMax)) {
         const int blocks = int((n_chains + kWarpsPerCta - 1) / kWarpsPerCta);
         MemoView m;
-        if (memo && memo->slots && memo->entry_words == 17 + params.chunk_size) m = *memo;
+        if (memo && memo->slots && memo->entry_words == 17 + params.chunk_size) {
+            m = *memo;
+            memo_probe_kernel<<<n_chains, kProbeThreads, 0, stream>>>(chains, params, out, m);
+            note_launch();
+        }
         hash_chains_warp_kernel<<<blocks, 32 * kWarpsPerCta, 0, stream>>>(tokens, chains, n_chains,
                                                                           params, out, m);
     } else {

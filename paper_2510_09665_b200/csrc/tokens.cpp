@@ -1,6 +1,9 @@
 #include "tokens.hpp"
 
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <stdexcept>
 
 namespace tkv {
@@ -23,8 +26,20 @@ KeyHasher::KeyHasher(std::string model_tag, size_t chunk_size, int device)
     stream_ = Stream::create();
 }
 
+namespace {
+// TKV_TRACE_LOOKUP=1: host-side phase times of every hash() call on stderr.
+bool trace_lookup() {
+    static const bool on = std::getenv("TKV_TRACE_LOOKUP") != nullptr;
+    return on;
+}
+double now_us() {
+    return std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+}  // namespace
+
 std::vector<std::vector<Digest>> KeyHasher::hash(const std::vector<TokenSpanView>& seqs,
                                                  const std::vector<Digest>* parents) {
+    const double t_in = trace_lookup() ? now_us() : 0;
     std::lock_guard lock(mu_);
     TKV_CUDA(cudaSetDevice(device_));
     size_t total_tokens = 0, total_chunks = 0;
@@ -64,6 +79,7 @@ std::vector<std::vector<Digest>> KeyHasher::hash(const std::vector<TokenSpanView
     // Stage tokens and descriptors into HBM (one parallel read of the mapped
     // buffers), run the chains writing digests to HBM, then verify memo hits
     // and publish every digest to the mapped result buffer.
+    const double t_packed = trace_lookup() ? now_us() : 0;
     const size_t tok_bytes = total_tokens * sizeof(TokenId);
     const size_t ch_bytes = seqs.size() * sizeof(ChainDesc);
     d_tokens_.reserve(tok_bytes + 64);
@@ -77,19 +93,30 @@ std::vector<std::vector<Digest>> KeyHasher::hash(const std::vector<TokenSpanView
         if (memo_used_bound_ + total_chunks > memo_.entry_cap) memo_reset_locked();
         memo_used_bound_ += total_chunks;
         d_hit_.reserve(total_chunks * sizeof(uint32_t));
+        d_keys_.reserve(total_chunks * sizeof(unsigned long long));
+        d_first_.reserve(seqs.size() * sizeof(uint32_t));
         m = memo_;
         m.hit_entry = reinterpret_cast<uint32_t*>(d_hit_.ptr);
+        m.keys = reinterpret_cast<unsigned long long*>(d_keys_.ptr);
+        m.first_miss = reinterpret_cast<uint32_t*>(d_first_.ptr);
     }
     const auto* d_tok = reinterpret_cast<const uint32_t*>(d_tokens_.ptr);
     const auto* d_ch = reinterpret_cast<const ChainDesc*>(d_chains_.ptr);
-    TKV_CUDA(launch_stage_words(h_tokens_.dev, d_tokens_.ptr, tok_bytes, stream_));
     TKV_CUDA(launch_stage_words(h_chains_.dev, d_chains_.ptr, ch_bytes, stream_));
+    if (memo_.slots)  // staging + per-row fingerprints in one pass
+        TKV_CUDA(launch_memo_stage(reinterpret_cast<const uint32_t*>(h_tokens_.dev),
+                                   reinterpret_cast<uint32_t*>(d_tokens_.ptr), d_ch, uint32_t(seqs.size()),
+                                   uint32_t(total_chunks), p, m, stream_));
+    else
+        TKV_CUDA(launch_stage_words(h_tokens_.dev, d_tokens_.ptr, tok_bytes, stream_));
     TKV_CUDA(launch_hash_chains(d_tok, d_ch, uint32_t(seqs.size()), p, d_out_.ptr, stream_,
                                 memo_.slots ? &m : nullptr));
     TKV_CUDA(launch_memo_verify(d_tok, d_ch, uint32_t(seqs.size()), uint32_t(total_chunks), p,
                                 d_out_.ptr, memo_.slots ? &m : nullptr, h_out_.dev,
                                 reinterpret_cast<unsigned int*>(h_bad_.dev), stream_));
+    const double t_launched = trace_lookup() ? now_us() : 0;
     TKV_CUDA(cudaStreamSynchronize(stream_));
+    const double t_synced = trace_lookup() ? now_us() : 0;
     ++launches_;
     chunks_ += total_chunks;
 
@@ -123,6 +150,10 @@ std::vector<std::vector<Digest>> KeyHasher::hash(const std::vector<TokenSpanView
         for (size_t c = 0; c < n; ++c, ++row)
             std::copy(h_out_.host + 32 * row, h_out_.host + 32 * row + 32, out[i][c].begin());
     }
+    if (trace_lookup())
+        std::fprintf(stderr, "[tkv hash] chains=%zu rows=%zu pack=%.1fus launch=%.1fus device+sync=%.1fus unpack=%.1fus\n",
+                     seqs.size(), total_chunks, t_packed - t_in, t_launched - t_packed, t_synced - t_launched,
+                     now_us() - t_synced);
     return out;
 }
 

@@ -3,7 +3,7 @@
 // The arithmetic is the reference's: 256-token spans (only the last may be
 // short), digest_i = SHA-256(u16le(|tag|) | tag | digest_{i-1} | u32le tokens).
 // The difference is where it runs: every digest is computed by the K3 kernel
-// (sha256_chain.cu) through a KeyHasher, one thread per sequence, and a
+// (sha256_chain.cu) through a KeyHasher, one warp per sequence, and a
 // sequence is hashed ONCE per query — the reference re-derives the same chain
 // three to four times (connector.cpp:74,103,139,446-450).
 #pragma once
@@ -73,6 +73,7 @@ private:
     Stream stream_;
     PinnedBuffer h_tokens_, h_chains_, h_out_, h_bad_;  // mapped host side of a launch
     DeviceBuffer d_tokens_, d_chains_, d_out_, d_hit_;  // HBM copies the kernels work on
+    DeviceBuffer d_keys_, d_first_;                     // memo probe keys / first miss per chain
     uint64_t memo_rehashes_ = 0;
     uint64_t launches_ = 0, chunks_ = 0;
     // memo (device): slots, entries, counter + stats

@@ -268,3 +268,20 @@ def test_vllm_two_plane_layout(tkv):
             b = table[t // pt]
             assert np.array_equal(got[layer, t, 0], kv[0, b, t % pt])
             assert np.array_equal(got[layer, t, 1], kv[1, b, t % pt])
+
+
+@pytest.mark.parametrize("nbytes,src_off,dst_off", [(0, 0, 0), (1, 0, 0), (4096 * 4 + 12, 0, 0),
+                                                    (1000, 3, 0), (777, 16, 48), (1 << 20, 0, 16)])
+def test_sm_copy_pinned_to_device(tkv, nbytes, src_off, dst_off):
+    """tkv_sm_copy: exact bytes from pinned host memory into HBM (vector body +
+    byte tail, or byte path when misaligned); nothing past the end is touched."""
+    from paper_2510_09665_b200._lib import check, lib
+    rng = np.random.default_rng(nbytes)
+    host = torch.empty(nbytes + 64, dtype=torch.uint8, pin_memory=True)
+    host.numpy()[:] = rng.integers(0, 256, size=nbytes + 64, dtype=np.uint8)
+    dev = torch.full((nbytes + 128,), 0xAB, dtype=torch.uint8, device="cuda")
+    check(lib().tkv_sm_copy(host.data_ptr() + src_off, dev.data_ptr() + dst_off, nbytes, None))
+    torch.cuda.synchronize()
+    d = dev.cpu().numpy()
+    assert np.array_equal(d[dst_off:dst_off + nbytes], host.numpy()[src_off:src_off + nbytes])
+    assert (d[:dst_off] == 0xAB).all() and (d[dst_off + nbytes:] == 0xAB).all()

@@ -78,3 +78,49 @@ def test_memo_does_not_change_connector_outcomes(tkv, C):
         off = json.loads(json.dumps(getattr(S, name)(
             lambda **kw: Engine(**kw, memo_entries=0), C)))
         assert on == off
+
+
+def test_memo_batched_mixed_hits(tkv, C):
+    """One lookup launch over many chains: full hits, a shared prefix that
+    diverges mid-chain, a cold chain, a repeat inside the batch and a partial
+    tail. The parallel probes resume each chain at its own first miss."""
+    from paper_2510_09665_b200.api import Engine
+    e = Engine(num_layers=2, bpt=64, page_tokens=16, tag=TAG, chunk_size=256, ram_slots=2, num_pages=8192)
+    rng = np.random.default_rng(7)
+    doc = rng.integers(0, 128256, size=256 * 20 + 33, dtype=np.uint32)
+    assert _keys_via_connector(e, 1, doc) == C.chunk_keys(doc, 256, TAG)  # warm the memo
+    cold = rng.integers(0, 128256, size=256 * 7, dtype=np.uint32)
+    diverge = doc.copy()
+    diverge[256 * 9 + 100] ^= 1
+    prompts = [doc, diverge, cold, doc[:256 * 4 + 5], cold, doc[:256 * 20]]
+    ids = list(range(10, 10 + len(prompts)))
+    e.lookup_batch(ids, prompts)
+    for q, p in zip(ids, prompts):
+        e.bind_pages(q, len(p))
+        e.update_state_after_alloc(q, (len(p) + 15) // 16, 0)
+    m = e.build_connector_meta(list(zip(ids, prompts)))
+    for i, p in enumerate(prompts):
+        sp, _ = e.plan(m, i, "store")
+        assert [d for _, _, _, _, d in sp] == C.chunk_keys(p, 256, TAG), i
+    e.drop_meta(m)
+    st = e.memo_stats()
+    # doc: 21 hits; diverge: 9; doc[:4 full + 5]: 4; doc[:20 full]: 20
+    assert st["hits"] >= 21 + 9 + 4 + 20
+    assert st["rehashes"] == 0
+    e.close()
+
+
+def test_memo_resumed_chain_parent(tkv, C):
+    """KeyChain::next with a parent (tokens.hpp:41-63) through the memo-enabled
+    free-function hasher: equal chunk tokens under different parents never
+    share a link, and a repeated (parent, chunk) is served from the memo."""
+    from paper_2510_09665_b200.api import chunk_keys, keychain_next
+    rng = np.random.default_rng(9)
+    chunk = rng.integers(0, 128256, size=256, dtype=np.uint32)
+    parents = [bytes(32), bytes(range(32)), bytes(31) + b"\x01"]
+    for _ in range(2):
+        for p in parents:
+            assert keychain_next(TAG, 256, p, chunk) == C.keychain_next(TAG, p, chunk)
+    doc = rng.integers(0, 128256, size=256 * 6 + 7, dtype=np.uint32)
+    for _ in range(2):
+        assert chunk_keys(doc, 256, TAG) == C.chunk_keys(doc, 256, TAG)
