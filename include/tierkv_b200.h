@@ -340,6 +340,13 @@ size_t tkv_pd_registered(tkv_pd_staging* s);
 int tkv_pd_send(tkv_pages* src, uint64_t query, size_t n_tokens, size_t chunk_size,
                 uint64_t landing_dev, uint64_t chunk_stride, void* stream, tkv_pd_record* out,
                 size_t cap, size_t* n);
+/* Same contract through the copy engines: K1 gathers groups of chunks into
+ * staging_dev (local HBM, chunk i at staging_dev + i*chunk_stride) while the
+ * copy engine moves each finished group (about group_bytes; 0 = 1 GiB) to
+ * landing_dev with one peer memcpy. Records point into landing_dev. */
+int tkv_pd_send_staged(tkv_pages* src, uint64_t query, size_t n_tokens, size_t chunk_size,
+                       uint64_t landing_dev, uint64_t chunk_stride, uint64_t staging_dev,
+                       uint64_t group_bytes, void* stream, tkv_pd_record* out, size_t cap, size_t* n);
 /* Decoder: K2 of every landed record into the query's pages (one launch). */
 int tkv_pd_land(tkv_pages* dst, uint64_t query, const tkv_pd_record* recs, size_t n, void* stream);
 int tkv_enable_peer_access(int device, int peer);

@@ -151,6 +151,8 @@ SIGNATURES = {
     "tkv_pd_registered": (sz, [vp]),
     "tkv_pd_send": (ct.c_int, [vp, ct.c_uint64, sz, sz, ct.c_uint64, ct.c_uint64, vp, ct.POINTER(PdRecordC), sz,
                                szp]),
+    "tkv_pd_send_staged": (ct.c_int, [vp, ct.c_uint64, sz, sz, ct.c_uint64, ct.c_uint64, ct.c_uint64,
+                                      ct.c_uint64, vp, ct.POINTER(PdRecordC), sz, szp]),
     "tkv_pd_land": (ct.c_int, [vp, ct.c_uint64, ct.POINTER(PdRecordC), sz, vp]),
     "tkv_enable_peer_access": (ct.c_int, [ct.c_int, ct.c_int]),
     "tkv_ipc_get_handle": (ct.c_int, [vp, u8p]),

@@ -475,6 +475,17 @@ def pd_send(engine: "Engine", qid: int, n_tokens: int, landing_ptr: int, chunk_s
     return [out[i] for i in range(n.value)]
 
 
+def pd_send_staged(engine: "Engine", qid: int, n_tokens: int, landing_ptr: int, chunk_stride: int,
+                   staging_ptr: int, group_bytes: int = 0):
+    """Prefiller, copy-engine variant: K1 into local staging, CE peer copies."""
+    cap = 1 << 14
+    out = (PdRecordC * cap)()
+    n = ct.c_size_t(0)
+    check(lib().tkv_pd_send_staged(engine.pages, qid, n_tokens, engine.chunk_size, landing_ptr, chunk_stride,
+                                   staging_ptr, group_bytes, engine.stream_handle, out, cap, ct.byref(n)))
+    return [out[i] for i in range(n.value)]
+
+
 def pd_land(engine: "Engine", qid: int, records) -> None:
     """Decoder: scatter landed chunks into the query's pages (one launch)."""
     arr = (PdRecordC * max(1, len(records)))(*records)

@@ -644,6 +644,22 @@ int tkv_pd_send(tkv_pages* src, uint64_t q, size_t n_tokens, size_t chunk_size, 
         return 0;
     });
 }
+int tkv_pd_send_staged(tkv_pages* src, uint64_t q, size_t n_tokens, size_t chunk_size, uint64_t landing,
+                       uint64_t stride, uint64_t staging, uint64_t group_bytes, void* stream,
+                       tkv_pd_record* out, size_t cap, size_t* n) {
+    return guard([&] {
+        if (!staging) return fail(Errc::invalid_argument, "null staging buffer");
+        auto r = pd_send_chunks_staged(*src->p, q, n_tokens, chunk_size, landing, stride, staging,
+                                       cudaStream_t(stream), group_bytes ? group_bytes : (1ull << 30));
+        if (!r.ok()) return st(r.status());
+        *n = r.value().size();
+        for (size_t i = 0; i < r.value().size() && i < cap; ++i) {
+            const auto& x = r.value()[i];
+            out[i] = tkv_pd_record{x.addr, x.bytes, x.token_count, x.first_token};
+        }
+        return 0;
+    });
+}
 int tkv_pd_land(tkv_pages* dst, uint64_t q, const tkv_pd_record* recs, size_t n, void* stream) {
     return guard([&] {
         std::vector<PdRecord> v(n);

@@ -74,15 +74,16 @@ DualPool& pd_plan_pool() {
 }
 }  // namespace
 
-Result<std::vector<PdRecord>> pd_send_chunks(PagedKVStore& pages, QueryId query, size_t n_tokens,
-                                             size_t chunk_size, uint64_t landing,
-                                             uint64_t chunk_stride, cudaStream_t stream, int ctas) {
+namespace {
+// Records (where each chunk lands) and K1 descriptors writing chunk i at
+// base + i * chunk_stride, after the reference's readability checks.
+Status pd_describe(PagedKVStore& pages, QueryId query, size_t n_tokens, size_t chunk_size,
+                   uint64_t landing, uint64_t base, uint64_t chunk_stride, cudaStream_t stream,
+                   std::vector<PdRecord>& recs, std::vector<XferDesc>& descs) {
     const auto& spec = pages.spec();
     const uint32_t pt = spec.page_tokens;
     const size_t bpt = spec.bytes_per_token_per_layer;
     if (chunk_size == 0 || chunk_size % pt) return Status{Errc::invalid_argument, "chunk size"};
-    std::vector<PdRecord> recs;
-    std::vector<XferDesc> descs;
     auto t = pages.device_table(query, stream);
     if (!t.ok()) return t.status();
     for (size_t start = 0, i = 0; start < n_tokens; start += chunk_size, ++i) {
@@ -93,10 +94,9 @@ Result<std::vector<PdRecord>> pd_send_chunks(PagedKVStore& pages, QueryId query,
         }
         const uint64_t bytes = uint64_t(spec.num_layers) * n * bpt;
         if (bytes > chunk_stride) return Status{Errc::size_mismatch, "landing slot too small"};
-        PdRecord r{landing + i * chunk_stride, bytes, uint32_t(n), uint32_t(start)};
-        recs.push_back(r);
+        recs.push_back(PdRecord{landing + i * chunk_stride, bytes, uint32_t(n), uint32_t(start)});
         XferDesc x;
-        x.chunk = r.addr;
+        x.chunk = base + i * chunk_stride;
         x.layer_stride = uint64_t(n) * bpt;
         x.table = t.value().ptr;
         x.table_stride = t.value().stride;
@@ -104,13 +104,62 @@ Result<std::vector<PdRecord>> pd_send_chunks(PagedKVStore& pages, QueryId query,
         x.n_tokens = uint32_t(n);
         descs.push_back(x);
     }
+    return Status::success();
+}
+}  // namespace
+
+Result<std::vector<PdRecord>> pd_send_chunks(PagedKVStore& pages, QueryId query, size_t n_tokens,
+                                             size_t chunk_size, uint64_t landing,
+                                             uint64_t chunk_stride, cudaStream_t stream, int ctas) {
+    const auto& spec = pages.spec();
+    std::vector<PdRecord> recs;
+    std::vector<XferDesc> descs;
+    Status st = pd_describe(pages, query, n_tokens, chunk_size, landing, landing, chunk_stride, stream, recs, descs);
+    if (!st.ok()) return st;
     if (descs.empty()) return recs;
+    const uint32_t pt = spec.page_tokens;
     const uint32_t ppt = pages_per_tile(pages.page_bytes());
     DevicePlan plan;
     plan.build(pd_plan_pool(), {descs}, pt, ppt, spec.num_layers, stream);
     TKV_CUDA(launch_paged_copy(pages.layout(), plan.plan(0, 0, spec.num_layers, ppt), CopyDir::gather,
                                ctas, stream));
     TKV_CUDA(cudaStreamSynchronize(stream));  // bytes landed before any ordinal is pushed
+    return recs;
+}
+
+Result<std::vector<PdRecord>> pd_send_chunks_staged(PagedKVStore& pages, QueryId query, size_t n_tokens,
+                                                    size_t chunk_size, uint64_t landing,
+                                                    uint64_t chunk_stride, uint64_t staging,
+                                                    cudaStream_t stream, uint64_t group_bytes) {
+    const auto& spec = pages.spec();
+    std::vector<PdRecord> recs;
+    std::vector<XferDesc> descs;
+    Status st = pd_describe(pages, query, n_tokens, chunk_size, landing, staging, chunk_stride, stream, recs, descs);
+    if (!st.ok()) return st;
+    if (descs.empty()) return recs;
+    const uint32_t pt = spec.page_tokens;
+    const uint32_t ppt = pages_per_tile(pages.page_bytes());
+    const size_t per_group = std::max<size_t>(1, group_bytes / chunk_stride);
+    std::vector<std::vector<XferDesc>> groups;
+    for (size_t i = 0; i < descs.size(); i += per_group)
+        groups.emplace_back(descs.begin() + i, descs.begin() + std::min(descs.size(), i + per_group));
+    std::vector<DevicePlan> plans(groups.size());  // group sizes differ: one plan each
+    static thread_local Stream ce = Stream::create();
+    std::vector<Event> done(groups.size());
+    for (size_t g = 0; g < groups.size(); ++g) {
+        plans[g].build(pd_plan_pool(), {groups[g]}, pt, ppt, spec.num_layers, stream);
+        TKV_CUDA(launch_paged_copy(pages.layout(), plans[g].plan(0, 0, spec.num_layers, ppt),
+                                   CopyDir::gather, 0, stream));
+        done[g].record(stream);
+        done[g].wait_on(ce);
+        const size_t first = g * per_group, last = first + groups[g].size() - 1;
+        const uint64_t bytes = (last - first) * chunk_stride + recs[last].bytes;
+        TKV_CUDA(cudaMemcpyAsync(reinterpret_cast<void*>(landing + first * chunk_stride),
+                                 reinterpret_cast<const void*>(staging + first * chunk_stride), bytes,
+                                 cudaMemcpyDefault, ce));
+    }
+    TKV_CUDA(cudaStreamSynchronize(ce));  // bytes landed before any ordinal is pushed
+    TKV_CUDA(cudaStreamSynchronize(stream));
     return recs;
 }
 

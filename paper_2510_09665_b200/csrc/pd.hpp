@@ -70,6 +70,16 @@ Result<std::vector<PdRecord>> pd_send_chunks(PagedKVStore& pages, QueryId query,
                                              uint64_t chunk_stride, cudaStream_t stream,
                                              int ctas = 0);
 
+// Same contract through the copy engines: K1 gathers groups of chunks into
+// `staging` (local HBM, same layout as landing) on `stream` while the copy
+// engine moves each finished group to `landing` with one peer memcpy on a
+// second stream (groups of about `group_bytes`). One extra HBM pass; the
+// NVLink leg is a plain CE peer copy (the measured 770 GB/s path).
+Result<std::vector<PdRecord>> pd_send_chunks_staged(PagedKVStore& pages, QueryId query, size_t n_tokens,
+                                                    size_t chunk_size, uint64_t landing,
+                                                    uint64_t chunk_stride, uint64_t staging,
+                                                    cudaStream_t stream, uint64_t group_bytes = 1ull << 30);
+
 // Decoder side: K2 of every landed record into the query's pages (all
 // layers, one launch), marks the pages populated. Enqueued on `stream`.
 Status pd_land_chunks(PagedKVStore& pages, QueryId query, const std::vector<PdRecord>& records,

@@ -14,8 +14,11 @@ import scenarios as S
 pytestmark = pytest.mark.gpu
 
 
-def test_pd_send_land_byte_exact(tkv, C):
-    from paper_2510_09665_b200.api import Engine, PdStaging, pd_land, pd_send
+@pytest.mark.parametrize("staged", [False, True])
+def test_pd_send_land_byte_exact(tkv, C, staged):
+    """staged: K1 into local staging + copy-engine peer copies in groups (the
+    group size is forced down so the 7 chunks travel as several copies)."""
+    from paper_2510_09665_b200.api import Engine, PdStaging, pd_land, pd_send, pd_send_staged
     spec = dict(num_layers=4, bpt=512, page_tokens=16, tag="pd-test", chunk_size=32)
     pre = Engine(**spec, ram_slots=4, num_pages=256)
     dec = Engine(**spec, ram_slots=4, num_pages=256)
@@ -26,7 +29,11 @@ def test_pd_send_land_byte_exact(tkv, C):
     landing = torch.zeros(7 * stride, dtype=torch.uint8, device="cuda")
     staging = PdStaging()
     assert staging.register_query(10) == 0
-    recs = pd_send(pre, 10, 200, landing.data_ptr(), stride)
+    if staged:
+        buf = torch.zeros(7 * stride, dtype=torch.uint8, device="cuda")
+        recs = pd_send_staged(pre, 10, 200, landing.data_ptr(), stride, buf.data_ptr(), group_bytes=2 * stride)
+    else:
+        recs = pd_send(pre, 10, 200, landing.data_ptr(), stride)
     assert [r.token_count for r in recs] == [32] * 6 + [8]
     for o in [3, 0, 6, 1, 5, 2, 4, 3]:
         assert staging.push(10, o, o == 6, recs[o]) == 0
