@@ -16,4 +16,7 @@ timeout 600 $NCU --set full --clock-control none --import-source on -k regex:pag
   > gpurun_out/prof_paged.log 2>&1
 timeout 600 $NCU --set full --clock-control none --import-source on -k regex:hash_chains -c 1 \
   -o gpurun_out/prof_hash -f python tools/bench_hash.py > gpurun_out/prof_hash.log 2>&1
+# 4. --set full of the memo kernels on a warm 128K-token lookup (config 4)
+timeout 600 $NCU --set full --clock-control none --import-source on -k regex:"memo_|hash_chains" -s 12 -c 4 \
+  -o gpurun_out/prof_memo -f python tools/bench_lookup.py > gpurun_out/prof_memo.log 2>&1
 ls -la gpurun_out
