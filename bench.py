@@ -81,6 +81,25 @@ def dist_env():
     return world, rank, local
 
 
+def bind_to_gpu_numa(local):
+    """Restrict this rank to the CPUs NVML reports as local to its GPU, before
+    any pinned allocation: the pinned host tier is then first-touched on the
+    GPU's own NUMA node and its DMA never crosses the socket interconnect.
+    Returns the CPU count in use (no-op where NVML or affinity is missing)."""
+    try:
+        import pynvml
+        pynvml.nvmlInit()
+        h = pynvml.nvmlDeviceGetHandleByIndex(local)
+        words = pynvml.nvmlDeviceGetCpuAffinity(h, 16)
+        cpus = {64 * i + b for i, w in enumerate(words) for b in range(64) if (int(w) >> b) & 1}
+        avail = os.sched_getaffinity(0)
+        if cpus and cpus & avail and (cpus & avail) != avail:
+            os.sched_setaffinity(0, cpus & avail)
+    except Exception:
+        pass
+    return len(os.sched_getaffinity(0))
+
+
 def backend():
     return os.environ.get("TKV_DIST_BACKEND", "nccl")
 
@@ -683,6 +702,7 @@ def run_b200(args):
     import torch.distributed as dist
 
     world, rank, local = dist_env()
+    bind_to_gpu_numa(local)
     if world > 1:
         if backend() == "nccl":
             dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
@@ -778,7 +798,7 @@ def run_b200(args):
             pd = {"error": repr(ex)[:300]}
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        threads = os.cpu_count() or 1
+        threads = len(os.sched_getaffinity(0))
         r = reference_step_gbps(args, args.cpu_layers, bench.bpt, threads)
         if r is not None:
             cpu = {"value": round(r["gbps"], 4), "unit": "GB/s", "cores": threads, "kind": "reference",

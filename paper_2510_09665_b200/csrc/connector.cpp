@@ -560,12 +560,21 @@ Status Connector::reserve_stores(BatchState& b) {
     const uint32_t ppt = pages_per_tile(pages_.page_bytes());
     std::vector<XferDesc> descs;
     std::unordered_map<QueryId, PagedKVStore::DeviceTable> tables;
+    // Every slot of the batch in one reservation, in the reference's
+    // batch_put order (plans, then chunks), with its eviction outcome.
+    std::vector<TieredStore::WriteSpec> specs;
+    for (const auto& plan : b.plans)
+        for (const auto& d : plan.store_plan) specs.push_back({d.key.digest, d.record_tokens, cfg_.pin_stores});
+    std::unordered_map<Digest, uint32_t, DigestHasher> own_shares;
+    for (const auto& it : b.loads) ++own_shares[it.digest];
+    auto writes = store_.begin_write_batch(specs, own_shares);
+    size_t k = 0;
     for (size_t p = 0; p < b.plans.size(); ++p) {
         const auto& plan = b.plans[p];
         for (size_t i = 0; i < plan.store_plan.size(); ++i) {
             const auto& d = plan.store_plan[i];
             detail::StoreItem item{p, i, Status::success(), {}};
-            auto w = store_.begin_write(d.key.digest, d.record_tokens, cfg_.pin_stores);
+            auto& w = writes[k++];
             if (!w.ok()) {
                 item.status = w.status();
             } else {

@@ -123,6 +123,98 @@ Result<SlotWrite> TieredStore::begin_write(const Digest& digest, uint32_t token_
     return w;
 }
 
+std::vector<Result<SlotWrite>> TieredStore::begin_write_batch(
+    const std::vector<WriteSpec>& specs, const std::unordered_map<Digest, uint32_t, DigestHasher>& own_shares) {
+    std::vector<Result<SlotWrite>> out;
+    out.reserve(specs.size());
+    std::lock_guard lock(mu_);
+    std::unordered_map<Digest, size_t, DigestHasher> batch_new;  // written by this batch -> index in out
+    for (const auto& s : specs) {
+        if (s.token_count == 0 || s.token_count > cfg_.chunk_size) {
+            out.emplace_back(Status{Errc::invalid_argument, "chunk geometry does not match store"});
+            continue;
+        }
+        auto it = index_.find(s.digest);
+        if (it != index_.end()) {
+            Entry& e = it->second;
+            if (e.token_count != s.token_count) {
+                out.emplace_back(Status{Errc::invalid_argument, "digest indexed with other geometry"});
+                continue;
+            }
+            SlotWrite w;
+            if (s.pin) e.pinned = true;
+            if (e.state == Entry::State::present || batch_new.count(s.digest)) {
+                touch(e);  // store.cpp:322-329: idempotent put
+                w.kind = e.state == Entry::State::present ? SlotWrite::Kind::already_present
+                                                          : SlotWrite::Kind::in_flight;
+                w.handle = e.state == Entry::State::present ? PutHandle::immediate(Status::success())
+                                                            : PutHandle(e.writer);
+            } else {
+                w.kind = SlotWrite::Kind::in_flight;  // an earlier batch is writing it
+                w.handle = PutHandle(e.writer);
+            }
+            out.emplace_back(std::move(w));
+            continue;
+        }
+        if (free_slots_.empty()) {
+            const Digest* victim = nullptr;
+            uint64_t oldest = ~uint64_t(0);
+            for (const auto& [d, e] : index_) {
+                if (e.pinned) continue;
+                bool cand;
+                if (e.state == Entry::State::present) {
+                    // An entry this batch is still loading may be overwritten
+                    // layer by layer behind its loads (layer l is loaded before
+                    // layer l is stored) only if the new chunk's layer l lies
+                    // within the old chunk's layers <= l: token_count >= new.
+                    auto own = own_shares.find(d);
+                    const uint32_t mine = own == own_shares.end() ? 0u : own->second;
+                    cand = e.share_count == 0 || (e.share_count <= mine && e.token_count >= s.token_count);
+                } else {
+                    cand = batch_new.count(d) != 0;
+                }
+                if (cand && e.last_touch < oldest) {
+                    oldest = e.last_touch;
+                    victim = &d;
+                }
+            }
+            if (!victim) {
+                out.emplace_back(Status{Errc::tier_full, "ram pool exhausted"});
+                continue;
+            }
+            auto vit = index_.find(*victim);
+            auto bn = batch_new.find(vit->first);
+            if (bn != batch_new.end()) {  // stored, then evicted, within this batch
+                SlotWrite& vw = out[bn->second].value();
+                vw.kind = SlotWrite::Kind::dropped;
+                vw.host = vw.dev = nullptr;
+                finish(vit->second.writer, Status::success());
+                batch_new.erase(bn);
+            }
+            free_slots_.push_back(vit->second.slot);
+            index_.erase(vit);
+        }
+        const uint32_t slot = free_slots_.back();
+        free_slots_.pop_back();
+        Entry e;
+        e.state = Entry::State::writing;
+        e.token_count = uint16_t(s.token_count);
+        e.slot = slot;
+        e.pinned = s.pin;
+        e.writer = std::make_shared<detail::PutState>();
+        touch(e);  // the reference's write order (touched again at commit)
+        SlotWrite w;
+        w.kind = SlotWrite::Kind::write;
+        w.host = slab_.host + size_t(slot) * slot_bytes_;
+        w.dev = slab_.dev + size_t(slot) * slot_bytes_;
+        w.handle = PutHandle(e.writer);
+        batch_new[s.digest] = out.size();
+        index_.emplace(s.digest, std::move(e));
+        out.emplace_back(std::move(w));
+    }
+    return out;
+}
+
 void TieredStore::commit_write(const Digest& digest, const Status& status) {
     std::shared_ptr<detail::PutState> writer;
     {

@@ -71,7 +71,10 @@ private:
 // A reserved slot about to be written by the device.
 struct SlotWrite {
     // none: no slot claimed (reservation failed, or not attempted).
-    enum class Kind { none, write, already_present, in_flight } kind = Kind::none;
+    // dropped: the reference would write this chunk and evict it again before
+    // its batch ends (a later put of the same batch takes the slot); it is
+    // reported stored and no bytes move (begin_write_batch).
+    enum class Kind { none, write, already_present, in_flight, dropped } kind = Kind::none;
     uint8_t* host = nullptr;   // slot base (host address)
     uint8_t* dev = nullptr;    // slot base (device-visible alias)
     PutHandle handle;          // completes when the bytes are present
@@ -99,6 +102,26 @@ public:
     // invalid_argument for geometry mismatch, tier_full when no slot can be
     // freed. The entry stays invisible to contains() until commit_write.
     Result<SlotWrite> begin_write(const Digest& digest, uint32_t token_count, bool pin);
+    // The slots of one store batch, claimed up front with the outcome of the
+    // reference's sequential batch_put (store.cpp:332-357, 500-506): puts are
+    // applied in order, and a put that finds no free slot evicts the least
+    // recently touched entry that is present, unpinned and unshared — where
+    // chunks this same batch is loading count as unshared (their loads finish
+    // before the reference seals the batch) and the batch's own earlier
+    // writes count as present (the reference has written them by then; such a
+    // victim comes back as Kind::dropped). `own_shares`: digest -> shares this
+    // batch holds through acquire(). One deliberate difference: a chunk this
+    // batch loads is only evictable by a put of at most its token count (the
+    // new bytes land behind the loads layer by layer); the reference, which
+    // seals after the loads, could also pick it for a longer chunk.
+    struct WriteSpec {
+        Digest digest;
+        uint32_t token_count = 0;
+        bool pin = false;
+    };
+    std::vector<Result<SlotWrite>> begin_write_batch(
+        const std::vector<WriteSpec>& specs,
+        const std::unordered_map<Digest, uint32_t, DigestHasher>& own_shares);
     // Marks the entry present (ok) or drops the claim (error). Safe to call
     // from a CUDA host callback (no CUDA API calls inside).
     void commit_write(const Digest& digest, const Status& status);

@@ -297,3 +297,81 @@ def sc_multi_query_batch(factory, C):
 
 ALL = [sc_match_cap, sc_load_plan_clip, sc_inconsistent_alloc, sc_partial_match, sc_layerwise_vs_blocking,
        sc_vanishing_chunk, sc_tier_full, sc_degrade_blocking, sc_multi_query_batch]
+
+
+def _random_trace(factory, C, seed: int, slots: int, **cfg):
+    """Randomised serving trace: shared document prefixes cut at arbitrary
+    (non chunk- or page-aligned) points plus fresh tails, 1-3 queries per
+    scheduling iteration, a RAM tier of `slots` chunks (small -> LRU evictions
+    between iterations). Records every observable per query."""
+    rng = np.random.default_rng(seed)
+    e = factory(**CONN, ram_slots=slots, num_pages=1024, **cfg)
+    docs = [make_prompt(int(rng.integers(40, 200)), 1000 + 10 * seed + i) for i in range(4)]
+    out = []
+    qid = 100
+    for _ in range(8):
+        batch = []
+        for _ in range(int(rng.integers(1, 4))):
+            d = docs[int(rng.integers(0, len(docs)))]
+            cut = int(rng.integers(1, len(d) + 1))
+            tail = make_prompt(int(rng.integers(0, 40)), int(rng.integers(0, 1 << 30)))
+            batch.append((qid, np.concatenate([d[:cut], tail]).astype(np.uint32)))
+            qid += 1
+        rec = {"matched": [e.get_num_new_matched_tokens(q, p) for q, p in batch]}
+        for (q, p), mt in zip(batch, rec["matched"]):
+            e.bind_pages(q, len(p))
+            assert e.update_state_after_alloc(q, (len(p) + 15) // 16, (mt + 15) // 16) == 0
+        m = e.build_connector_meta(batch)
+        rec["plans"] = [plan_view(e, m, i) for i in range(len(batch))]
+        assert e.start_load_kv(m) == 0
+        layerwise = e.meta_layerwise(m)
+        for layer in range(e.num_layers):
+            if layerwise:
+                assert e.wait_load_kv(m, layer) == 0
+            for q, p in batch:
+                lo = e.loaded_tokens(m, q)
+                if hasattr(e, "stream_handle"):
+                    e.compute_range(q, p, lo, len(p), layers=(layer, layer + 1))
+                else:
+                    e.compute_range(q, p, lo, len(p))
+            if layerwise:
+                if layer > 0:
+                    assert e.wait_store_kv(m, layer - 1) == 0
+                assert e.start_store_kv(m) == 0
+        if layerwise:
+            assert e.wait_store_kv(m, e.num_layers - 1) == 0
+        else:  # blocking: one store of every layer after the compute (sim_engine.cpp:150-160)
+            assert e.start_store_kv(m) == 0
+        rec["loaded"] = [e.loaded_tokens(m, q) for q, _ in batch]
+        rec["pages_ok"] = [pages_equal_synth(e, q, p, len(p), C) for q, p in batch]
+        rec["results"] = [[(d.hex(), c) for d, c in e.store_results(m, q)] for q, _ in batch]
+        for q, _ in batch:
+            e.finish_query(q)
+            e.release_query(q)
+        rec["entries"] = e.store_entries()
+        out.append(rec)
+    e.close()
+    return out
+
+
+def sc_random_trace_roomy(factory, C):
+    """Random trace, tier large enough to keep everything."""
+    return [_random_trace(factory, C, seed, 256) for seed in (1, 2, 3)]
+
+
+def sc_random_trace_evicting(factory, C):
+    """Random trace, 6-chunk tier: LRU evictions decide later hits."""
+    return [_random_trace(factory, C, seed, 6) for seed in (4, 5, 6)]
+
+
+def sc_random_trace_pinned(factory, C):
+    """Random trace, pinned stores into an 8-chunk tier: fills, then tier_full."""
+    return [_random_trace(factory, C, seed, 8, pin_stores=True) for seed in (7, 8)]
+
+
+def sc_random_trace_blocking(factory, C):
+    """Random trace in blocking (non-layerwise) mode with evictions."""
+    return [_random_trace(factory, C, seed, 5, layerwise=False) for seed in (9, 10)]
+
+
+ALL += [sc_random_trace_roomy, sc_random_trace_evicting, sc_random_trace_pinned, sc_random_trace_blocking]
