@@ -298,6 +298,34 @@ int ref_finish_query(void* h, uint64_t id) {
     return int(r.code());
 }
 
+// Decode storing (connector.hpp:116-119): the engine hands each generated
+// token's per-layer KV to append_decode; here those bytes are the synth KV of
+// `token` at absolute position `pos` (what the engine computed).
+int ref_begin_decode(void* h, uint64_t id) {
+    return int(static_cast<RefEngine*>(h)->conn->begin_decode(id).code);
+}
+int ref_append_decode(void* h, uint64_t id, uint32_t token, size_t pos) {
+    auto* e = static_cast<RefEngine*>(h);
+    const auto& sp = e->pages->spec();
+    const uint32_t bpt = uint32_t(sp.bytes_per_token_per_layer);
+    std::vector<std::vector<uint8_t>> bufs(sp.num_layers, std::vector<uint8_t>(bpt));
+    std::vector<ByteSpan> spans;
+    for (uint32_t l = 0; l < sp.num_layers; ++l) {
+        synth_layer_kv(model_seed_of(sp), TokenSpanView(&token, 1), l, pos, bpt,
+                       MutByteSpan(bufs[l].data(), bpt));
+        spans.emplace_back(bufs[l].data(), bpt);
+    }
+    return int(e->conn->append_decode(id, token, spans).code);
+}
+size_t ref_finish_query_keys(void* h, uint64_t id, uint8_t* digests, size_t cap, int* code) {
+    auto r = static_cast<RefEngine*>(h)->conn->finish_query(id);
+    *code = int(r.code());
+    if (!r.ok()) return 0;
+    const auto& keys = r.value();
+    for (size_t i = 0; i < keys.size() && i < cap; ++i) std::memcpy(digests + 32 * i, keys[i].digest.data(), 32);
+    return keys.size();
+}
+
 // --- store (store.hpp:153-171) ----------------------------------------------
 
 int ref_store_contains(void* h, const uint8_t* digest) {

@@ -65,6 +65,9 @@ class _Ref:
             "ref_meta_plan": (_sz, [_vp, ct.c_int, _sz, ct.c_int, _u64p, _u8p, _sz, _u64p]),
             "ref_meta_store_results": (_sz, [_vp, ct.c_int, ct.c_uint64, ct.POINTER(ct.c_int), _u8p, _sz]),
             "ref_finish_query": (ct.c_int, [_vp, ct.c_uint64]),
+            "ref_begin_decode": (ct.c_int, [_vp, ct.c_uint64]),
+            "ref_append_decode": (ct.c_int, [_vp, ct.c_uint64, ct.c_uint32, _sz]),
+            "ref_finish_query_keys": (_sz, [_vp, ct.c_uint64, _u8p, _sz, ct.POINTER(ct.c_int)]),
             "ref_store_contains": (ct.c_int, [_vp, _u8p]),
             "ref_store_get": (_sz, [_vp, _u8p, _u8p, _sz]),
             "ref_store_clear": (_sz, [_vp, _u8p]),
@@ -186,6 +189,8 @@ class RefEngine:
                                             store_io_threads, num_pages, int(layerwise), staging_budget,
                                             io_threads, int(pin_stores))
         self._keep = []
+        self._prompt_len: dict[int, int] = {}
+        self._decode_pos: dict[int, int] = {}
 
     def close(self):
         if self.h:
@@ -232,6 +237,8 @@ class RefEngine:
         ids = (ct.c_uint64 * len(queries))(*[q for q, _ in queries])
         arrs = [_tokens(p) for _, p in queries]
         self._keep.append(arrs)
+        for (q, _), a in zip(queries, arrs):
+            self._prompt_len[q] = a.size
         ptrs = (_u32p * len(queries))(*[a.ctypes.data_as(_u32p) for a in arrs])
         lens = (_sz * len(queries))(*[a.size for a in arrs])
         return self.lib.ref_build_meta(self.h, len(queries), ids, ptrs, lens)
@@ -275,7 +282,30 @@ class RefEngine:
         return [(dig[32 * i:32 * i + 32].tobytes(), int(codes[i])) for i in range(n)]
 
     def finish_query(self, qid: int) -> int:
+        self._decode_pos.pop(qid, None)
         return self.lib.ref_finish_query(self.h, qid)
+
+    # --- decode storing (connector.hpp:116-119) ---
+    def begin_decode(self, qid: int) -> int:
+        rc = self.lib.ref_begin_decode(self.h, qid)
+        if rc == 0:
+            self._decode_pos[qid] = self._prompt_len.get(qid, 0)
+        return rc
+
+    def append_decode(self, qid: int, token: int) -> int:
+        pos = self._decode_pos.get(qid, 0)
+        rc = self.lib.ref_append_decode(self.h, qid, token, pos)
+        if rc == 0:
+            self._decode_pos[qid] = pos + 1
+        return rc
+
+    def finish_query_keys(self, qid: int):
+        cap = 4096
+        dig = np.zeros(32 * cap, np.uint8)
+        code = ct.c_int(0)
+        n = self.lib.ref_finish_query_keys(self.h, qid, dig.ctypes.data_as(_u8p), cap, ct.byref(code))
+        self._decode_pos.pop(qid, None)
+        return [dig[32 * i:32 * i + 32].tobytes() for i in range(n)], code.value
 
     def drop_meta(self, m: int) -> None:
         self.lib.ref_meta_drop(self.h, m)

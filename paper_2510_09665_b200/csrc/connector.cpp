@@ -44,10 +44,12 @@ struct CommitCtx {
     TieredStore* store;
     std::vector<Digest> digests;
     std::atomic<bool>* committed;
+    std::vector<Digest> touches;  // the reference's LRU touch order for the batch
 };
 void CUDART_CB commit_cb(void* p) {
     auto* c = static_cast<CommitCtx*>(p);
     for (const auto& d : c->digests) c->store->commit_write(d, Status::success());
+    if (!c->touches.empty()) c->store->touch_in_order(c->touches);
     if (c->committed) c->committed->store(true);
     delete c;
 }
@@ -106,6 +108,7 @@ struct BatchState {
     std::vector<bool> store_done;
     bool stores_sealed = false, stores_waited = false;
     std::vector<StoreItem> stores;
+    std::vector<Digest> store_touches;  // LRU touch order of the batch's puts (begin_write_batch)
     std::vector<Event> compute_done, gathered, d2h_done;
     Event store_complete;
     Event t0{true};  // timeline origin (recorded when loads are enqueued)
@@ -567,7 +570,7 @@ Status Connector::reserve_stores(BatchState& b) {
         for (const auto& d : plan.store_plan) specs.push_back({d.key.digest, d.record_tokens, cfg_.pin_stores});
     std::unordered_map<Digest, uint32_t, DigestHasher> own_shares;
     for (const auto& it : b.loads) ++own_shares[it.digest];
-    auto writes = store_.begin_write_batch(specs, own_shares);
+    auto writes = store_.begin_write_batch(specs, own_shares, &b.store_touches);
     size_t k = 0;
     for (size_t p = 0; p < b.plans.size(); ++p) {
         const auto& plan = b.plans[p];
@@ -731,7 +734,7 @@ Status Connector::start_store_kv(ConnectorMetadata& meta) {
                 store_ring_used_ = true;
             }
             if (b.any_store_writes) {
-                auto* ctx = new CommitCtx{&store_, {}, &b.committed};
+                auto* ctx = new CommitCtx{&store_, {}, &b.committed, std::move(b.store_touches)};
                 for (const auto& s : b.stores)
                     if (s.w.kind == SlotWrite::Kind::write)
                         ctx->digests.push_back(b.plans[s.plan].store_plan[s.desc].key.digest);

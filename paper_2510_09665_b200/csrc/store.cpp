@@ -124,12 +124,19 @@ Result<SlotWrite> TieredStore::begin_write(const Digest& digest, uint32_t token_
 }
 
 std::vector<Result<SlotWrite>> TieredStore::begin_write_batch(
-    const std::vector<WriteSpec>& specs, const std::unordered_map<Digest, uint32_t, DigestHasher>& own_shares) {
+    const std::vector<WriteSpec>& specs, const std::unordered_map<Digest, uint32_t, DigestHasher>& own_shares,
+    std::vector<Digest>* touch_order) {
     std::vector<Result<SlotWrite>> out;
     out.reserve(specs.size());
     std::lock_guard lock(mu_);
     std::unordered_map<Digest, size_t, DigestHasher> batch_new;  // written by this batch -> index in out
+    // batch_put registers every put (share_count++) before any write runs, so
+    // a chunk this batch puts again later stays unevictable until that later
+    // put has been applied (store.cpp:455-460).
+    std::unordered_map<Digest, uint32_t, DigestHasher> pending;
+    for (const auto& s : specs) ++pending[s.digest];
     for (const auto& s : specs) {
+        --pending[s.digest];
         if (s.token_count == 0 || s.token_count > cfg_.chunk_size) {
             out.emplace_back(Status{Errc::invalid_argument, "chunk geometry does not match store"});
             continue;
@@ -145,6 +152,7 @@ std::vector<Result<SlotWrite>> TieredStore::begin_write_batch(
             if (s.pin) e.pinned = true;
             if (e.state == Entry::State::present || batch_new.count(s.digest)) {
                 touch(e);  // store.cpp:322-329: idempotent put
+                if (touch_order) touch_order->push_back(s.digest);
                 w.kind = e.state == Entry::State::present ? SlotWrite::Kind::already_present
                                                           : SlotWrite::Kind::in_flight;
                 w.handle = e.state == Entry::State::present ? PutHandle::immediate(Status::success())
@@ -172,6 +180,10 @@ std::vector<Result<SlotWrite>> TieredStore::begin_write_batch(
                     cand = e.share_count == 0 || (e.share_count <= mine && e.token_count >= s.token_count);
                 } else {
                     cand = batch_new.count(d) != 0;
+                }
+                if (cand) {
+                    auto pd = pending.find(d);
+                    cand = pd == pending.end() || pd->second == 0;
                 }
                 if (cand && e.last_touch < oldest) {
                     oldest = e.last_touch;
@@ -202,7 +214,8 @@ std::vector<Result<SlotWrite>> TieredStore::begin_write_batch(
         e.slot = slot;
         e.pinned = s.pin;
         e.writer = std::make_shared<detail::PutState>();
-        touch(e);  // the reference's write order (touched again at commit)
+        touch(e);  // the reference's write order (replayed at commit)
+        if (touch_order) touch_order->push_back(s.digest);
         SlotWrite w;
         w.kind = SlotWrite::Kind::write;
         w.host = slab_.host + size_t(slot) * slot_bytes_;
@@ -213,6 +226,14 @@ std::vector<Result<SlotWrite>> TieredStore::begin_write_batch(
         out.emplace_back(std::move(w));
     }
     return out;
+}
+
+void TieredStore::touch_in_order(const std::vector<Digest>& digests) {
+    std::lock_guard lock(mu_);
+    for (const auto& d : digests) {
+        auto it = index_.find(d);
+        if (it != index_.end()) touch(it->second);
+    }
 }
 
 void TieredStore::commit_write(const Digest& digest, const Status& status) {

@@ -299,7 +299,7 @@ ALL = [sc_match_cap, sc_load_plan_clip, sc_inconsistent_alloc, sc_partial_match,
        sc_vanishing_chunk, sc_tier_full, sc_degrade_blocking, sc_multi_query_batch]
 
 
-def _random_trace(factory, C, seed: int, slots: int, **cfg):
+def _random_trace(factory, C, seed: int, slots: int, decode: bool = False, probe: bool = False, **cfg):
     """Randomised serving trace: shared document prefixes cut at arbitrary
     (non chunk- or page-aligned) points plus fresh tails, 1-3 queries per
     scheduling iteration, a RAM tier of `slots` chunks (small -> LRU evictions
@@ -309,6 +309,7 @@ def _random_trace(factory, C, seed: int, slots: int, **cfg):
     docs = [make_prompt(int(rng.integers(40, 200)), 1000 + 10 * seed + i) for i in range(4)]
     out = []
     qid = 100
+    seen: set[str] = set()
     for _ in range(8):
         batch = []
         for _ in range(int(rng.integers(1, 4))):
@@ -317,10 +318,12 @@ def _random_trace(factory, C, seed: int, slots: int, **cfg):
             tail = make_prompt(int(rng.integers(0, 40)), int(rng.integers(0, 1 << 30)))
             batch.append((qid, np.concatenate([d[:cut], tail]).astype(np.uint32)))
             qid += 1
+        n_dec = {q: int(rng.integers(0, 70)) if decode and rng.random() < 0.6 else 0 for q, _ in batch}
         rec = {"matched": [e.get_num_new_matched_tokens(q, p) for q, p in batch]}
         for (q, p), mt in zip(batch, rec["matched"]):
-            e.bind_pages(q, len(p))
-            assert e.update_state_after_alloc(q, (len(p) + 15) // 16, (mt + 15) // 16) == 0
+            n_all = len(p) + n_dec[q]
+            e.bind_pages(q, n_all)
+            assert e.update_state_after_alloc(q, (n_all + 15) // 16, (mt + 15) // 16) == 0
         m = e.build_connector_meta(batch)
         rec["plans"] = [plan_view(e, m, i) for i in range(len(batch))]
         assert e.start_load_kv(m) == 0
@@ -345,6 +348,28 @@ def _random_trace(factory, C, seed: int, slots: int, **cfg):
         rec["loaded"] = [e.loaded_tokens(m, q) for q, _ in batch]
         rec["pages_ok"] = [pages_equal_synth(e, q, p, len(p), C) for q, p in batch]
         rec["results"] = [[(d.hex(), c) for d, c in e.store_results(m, q)] for q, _ in batch]
+        seen = {d for r in rec["results"] for d, _ in r} | seen
+        if probe:  # diagnostics: which chunks the tier holds after the batch
+            rec["present_after_batch"] = sorted(d[:8] for d in seen if e.contains(bytes.fromhex(d)))
+            # decode storing (connector.cpp:434-497): generated tokens' KV
+            # computed one at a time, full chunks flushed as they complete,
+            # the tail at finish_query
+            rec["decode"] = []
+            for q, p in batch:
+                if not n_dec[q]:
+                    rec["decode"].append(None)
+                    continue
+                gen = make_prompt(n_dec[q], int(rng.integers(0, 1 << 30)))
+                full = np.concatenate([p, gen]).astype(np.uint32)
+                rcs = [e.begin_decode(q)]
+                for i, tok in enumerate(gen):
+                    e.compute_range(q, full, len(p) + i, len(p) + i + 1)
+                    rcs.append(e.append_decode(q, int(tok)))
+                keys, rc = e.finish_query_keys(q)
+                rec["decode"].append({"rcs": rcs, "keys": [k.hex() for k in keys], "rc": rc})
+                if probe:
+                    seen |= {k.hex() for k in keys}
+                    rec["decode"][-1]["present"] = sorted(d[:8] for d in seen if e.contains(bytes.fromhex(d)))
         for q, _ in batch:
             e.finish_query(q)
             e.release_query(q)
@@ -374,4 +399,10 @@ def sc_random_trace_blocking(factory, C):
     return [_random_trace(factory, C, seed, 5, layerwise=False) for seed in (9, 10)]
 
 
-ALL += [sc_random_trace_roomy, sc_random_trace_evicting, sc_random_trace_pinned, sc_random_trace_blocking]
+def sc_random_trace_decode(factory, C):
+    """Random trace with decode storing after each prefill, roomy and evicting tiers."""
+    return [_random_trace(factory, C, 11, 256, decode=True), _random_trace(factory, C, 12, 7, decode=True)]
+
+
+ALL += [sc_random_trace_roomy, sc_random_trace_evicting, sc_random_trace_pinned, sc_random_trace_blocking,
+        sc_random_trace_decode]

@@ -4,7 +4,7 @@ import scenarios as S, oracle
 from paper_2510_09665_b200.api import Engine
 C = oracle.C()
 for fn in (S.sc_random_trace_roomy, S.sc_random_trace_evicting, S.sc_random_trace_pinned,
-           S.sc_random_trace_blocking):
+           S.sc_random_trace_blocking, S.sc_random_trace_decode):
     ref = json.loads(json.dumps(fn(oracle.RefEngine, C)))
     got = json.loads(json.dumps(fn(Engine, C)))
     print(fn.__name__, "equal:", ref == got)
