@@ -216,8 +216,12 @@ __device__ __forceinline__ void expand_block(const uint32_t* in, uint32_t* out) 
 
 // The 64 rounds with K+W precomputed: only the state recurrence is serial.
 // (Measured: forcing the additions onto the FMA pipe with mad.lo to relieve
-// the ALU pipe made a chunk slower, 20.5 vs 19.4 us — the longer cross-pipe
-// latency lands on the critical path — so ptxas' own pipe mix is kept.)
+// the ALU pipe made a chunk slower, 20.5 vs 19.4 us, and so did computing
+// Sigma0's rotates on the FMA pipe as IMAD(x, 2^(32-n), IMAD.HI(x, 2^(32-n)))
+// with the multipliers hidden in constant memory, 27.4 vs 19.8 us — the
+// round is dependency-latency bound (ncu: 0.44 issue/cycle, "wait" stalls
+// ~1 cycle per instruction), so longer-latency pipes only lengthen the
+// chain. ptxas' own pipe mix is kept.)
 __device__ __forceinline__ void compress_kw(uint32_t h[8], const uint32_t* kw) {
     uint32_t a = h[0], b = h[1], c = h[2], d = h[3], e = h[4], f = h[5], g = h[6], hh = h[7];
 #pragma unroll
