@@ -638,15 +638,23 @@ def run_pd_pairs(args, world, rank, local):
         # decoder verifies come from the direct K1 writes.
         t_ce, _ = timed(lambda: pd_send_staged(e, qid, n, peer_ptr.value, stride, staging.data_ptr()))
         t_sm, recs = timed(lambda: pd_send(e, qid, n, peer_ptr.value, stride))
-        del staging
+        # link probe: one plain copy-engine peer copy of 1 GiB (all pairs at once)
+        probe = min(1 << 30, chunks * stride)
+
+        def raw():
+            check(lib().tkv_ce_copy(ct.c_void_p(staging.data_ptr()), ct.c_void_p(peer_ptr.value), probe, None))
+            torch.cuda.synchronize(dev)
+        t_link, _ = timed(raw)
         meta = torch.tensor([[r.addr - peer_ptr.value, r.bytes, r.token_count, r.first_token] for r in recs],
                             dtype=torch.int64, device=coll_device(dev))
         dist.send(meta, dst=peer)
         lib().tkv_ipc_close(peer_ptr)
+        del staging
         moved = sum(r.bytes for r in recs)
         best = min(t_sm, t_ce)
         result = {"pair": f"{rank}->{peer}", "gbps": moved / best / 1e9, "bytes": moved,
-                  "ms": 1e3 * best, "sm_direct_gbps": moved / t_sm / 1e9, "ce_staged_gbps": moved / t_ce / 1e9}
+                  "ms": 1e3 * best, "sm_direct_gbps": moved / t_sm / 1e9, "ce_staged_gbps": moved / t_ce / 1e9,
+                  "link_gbps": probe / t_link / 1e9}
     else:
         meta = torch.zeros((chunks, 4), dtype=torch.int64, device=coll_device(dev))
         dist.recv(meta, src=peer)
@@ -789,8 +797,10 @@ def run_b200(args):
                   "aggregate_gbps": round(agg, 1), "bytes_per_pair": sends[0]["bytes"],
                   "land_ms": [round(r["land_ms"], 3) for r in lands],
                   "mismatch_words": sum(r["mismatch_words"] for r in lands),
+                  "link_probe_gbps": [round(r["link_gbps"], 1) for r in sends],
                   "nvlink_peak_gbps_per_direction": 770.0,
                   "frac_of_peak": round(min(r["gbps"] for r in sends) / 770.0, 4),
+                  "frac_of_measured_link": round(min(r["gbps"] / r["link_gbps"] for r in sends), 4),
                   "path": "per pair the faster of: K1 gather straight into the peer decoder's landing buffer "
                           "(CUDA IPC, SM writes over NVLink) | K1 into local staging + copy-engine peer copies "
                           "per 1 GiB group; PdStaging ordinal contract, one K2 land, bytes verified on device"}

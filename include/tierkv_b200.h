@@ -154,6 +154,10 @@ int tkv_synth_chunk(const uint32_t* tokens_dev, uint64_t seed, uint32_t start, u
  * KV transfers queued on the copy engines. No reference equivalent (the
  * reference has no device). */
 int tkv_sm_copy(const void* src, void* dst, uint64_t bytes, void* stream);
+/* Copy-engine copy of `bytes` between any two device-visible addresses
+ * (cudaMemcpyAsync, kind Default) on `stream`: the link probes (PCIe, NVLink
+ * peer copy) the bench reports its rooflines against. */
+int tkv_ce_copy(const void* src, void* dst, uint64_t bytes, void* stream);
 
 /* q8-scale codec (Q8ScaleCodec, src/codec.cpp:27-91), bit-exact, over a
  * batch of payloads. Encode: src = payload, dst = blob, bytes = payload

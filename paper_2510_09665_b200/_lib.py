@@ -78,6 +78,7 @@ SIGNATURES = {
                                     ct.c_uint32, ct.c_uint32, ct.c_uint32, vp, vp]),
     "tkv_synth_chunk": (ct.c_int, [vp, ct.c_uint64, ct.c_uint32, ct.c_uint32, ct.c_uint32, ct.c_uint32, vp, vp]),
     "tkv_sm_copy": (ct.c_int, [vp, vp, ct.c_uint64, vp]),
+    "tkv_ce_copy": (ct.c_int, [vp, vp, ct.c_uint64, vp]),
     "tkv_q8_blob_bytes": (ct.c_uint64, [ct.c_uint64]),
     "tkv_codec_plan": (ct.c_int, [vp, ct.c_uint32, u32p]),
     "tkv_q8_encode": (ct.c_int, [vp, vp, ct.c_uint32, ct.c_uint32, vp, vp]),

@@ -187,6 +187,11 @@ int tkv_sm_copy(const void* src, void* dst, uint64_t bytes, void* stream) {
     return cuda(launch_sm_copy(src, dst, bytes, cudaStream_t(stream)));
 }
 
+int tkv_ce_copy(const void* src, void* dst, uint64_t bytes, void* stream) {
+    if (bytes && (!src || !dst)) return fail(Errc::invalid_argument, "null pointer");
+    return cuda(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, cudaStream_t(stream)));
+}
+
 static SynthArgs synth_args(const uint32_t* tokens, const int32_t* table, uint32_t stride,
                             uint64_t seed, uint32_t p0, uint32_t p1, uint32_t l0, uint32_t l1) {
     SynthArgs a;
