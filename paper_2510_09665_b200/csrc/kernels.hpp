@@ -126,8 +126,6 @@ cudaError_t launch_hash_chains(const uint32_t* tokens, const ChainDesc* chains, 
 // SM-driven copy of exactly `bytes` between device-visible addresses (no copy
 // engine): 16-byte vectors when both ends are 16-aligned, bytes otherwise.
 cudaError_t launch_sm_copy(const void* src, void* dst, uint64_t bytes, cudaStream_t stream);
-// Copies `bytes` (rounded up to 16) from src to dst (mapped host -> HBM staging).
-cudaError_t launch_stage_words(const void* src, void* dst, uint64_t bytes, cudaStream_t stream);
 // Memo pass 1: stages the packed tokens (src: mapped host) into dst (HBM)
 // and writes every row's chunk fingerprint to memo.keys (chains: device).
 cudaError_t launch_memo_stage(const uint32_t* src, uint32_t* dst, const ChainDesc* chains, uint32_t n_chains,

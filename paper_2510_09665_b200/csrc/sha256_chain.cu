@@ -554,14 +554,6 @@ memo_probe_kernel(const ChainDesc* __restrict__ chains, const HashParams P, uint
     }
 }
 
-// Copies the packed tokens from mapped host memory into HBM once, in
-// parallel, so the serial chains read them at device latency.
-__global__ void stage_words_kernel(const uint4* __restrict__ src, uint4* __restrict__ dst, uint64_t n16) {
-    for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n16;
-         i += uint64_t(gridDim.x) * blockDim.x)
-        dst[i] = src[i];
-}
-
 // One warp per digest row: a memo hit is checked against its entry (parent,
 // token count, every token, digest); every row's digest is then published to
 // the caller's buffer. A failed check records the first bad row of its chain
@@ -639,16 +631,6 @@ __global__ void sha256_bytes_kernel(const uint8_t* __restrict__ data, uint32_t n
 }
 
 }  // namespace
-
-cudaError_t launch_stage_words(const void* src, void* dst, uint64_t bytes, cudaStream_t s) {
-    const uint64_t n16 = (bytes + 15) / 16;
-    if (n16 == 0) return cudaSuccess;
-    note_launch();
-    const uint64_t g = (n16 + 255) / 256;
-    stage_words_kernel<<<int(g < 148 * 4 ? g : 148 * 4), 256, 0, s>>>(
-        static_cast<const uint4*>(src), static_cast<uint4*>(dst), n16);
-    return cudaGetLastError();
-}
 
 cudaError_t launch_memo_stage(const uint32_t* src, uint32_t* dst, const ChainDesc* chains, uint32_t n_chains,
                               uint32_t total_rows, const HashParams& params, const MemoView& memo,

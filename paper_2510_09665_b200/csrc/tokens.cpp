@@ -102,13 +102,13 @@ std::vector<std::vector<Digest>> KeyHasher::hash(const std::vector<TokenSpanView
     }
     const auto* d_tok = reinterpret_cast<const uint32_t*>(d_tokens_.ptr);
     const auto* d_ch = reinterpret_cast<const ChainDesc*>(d_chains_.ptr);
-    TKV_CUDA(launch_stage_words(h_chains_.dev, d_chains_.ptr, ch_bytes, stream_));
+    TKV_CUDA(launch_sm_copy(h_chains_.dev, d_chains_.ptr, ch_bytes, stream_));
     if (memo_.slots)  // staging + per-row fingerprints in one pass
         TKV_CUDA(launch_memo_stage(reinterpret_cast<const uint32_t*>(h_tokens_.dev),
                                    reinterpret_cast<uint32_t*>(d_tokens_.ptr), d_ch, uint32_t(seqs.size()),
                                    uint32_t(total_chunks), p, m, stream_));
     else
-        TKV_CUDA(launch_stage_words(h_tokens_.dev, d_tokens_.ptr, tok_bytes, stream_));
+        TKV_CUDA(launch_sm_copy(h_tokens_.dev, d_tokens_.ptr, tok_bytes, stream_));
     TKV_CUDA(launch_hash_chains(d_tok, d_ch, uint32_t(seqs.size()), p, d_out_.ptr, stream_,
                                 memo_.slots ? &m : nullptr));
     TKV_CUDA(launch_memo_verify(d_tok, d_ch, uint32_t(seqs.size()), uint32_t(total_chunks), p,
@@ -136,7 +136,7 @@ std::vector<std::vector<Digest>> KeyHasher::hash(const std::vector<TokenSpanView
     if (!redo.empty()) {
         ++memo_rehashes_;
         std::copy(redo.begin(), redo.end(), ch);
-        TKV_CUDA(launch_stage_words(h_chains_.dev, d_chains_.ptr, redo.size() * sizeof(ChainDesc), stream_));
+        TKV_CUDA(launch_sm_copy(h_chains_.dev, d_chains_.ptr, redo.size() * sizeof(ChainDesc), stream_));
         TKV_CUDA(launch_hash_chains(d_tok, d_ch, uint32_t(redo.size()), p, d_out_.ptr, stream_, nullptr));
         TKV_CUDA(launch_memo_verify(d_tok, d_ch, uint32_t(redo.size()), uint32_t(total_chunks), p,
                                     d_out_.ptr, nullptr, h_out_.dev, nullptr, stream_));
