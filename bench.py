@@ -608,16 +608,19 @@ def run_pd_pairs(args, world, rank, local):
     qid = 5000
     landing = None
     handle = np.zeros(64, np.uint8)
+    offset = ct.c_uint64(0)
     if not prefill:
         landing = torch.empty(chunks * stride, dtype=torch.uint8, device=dev)
-        check(lib().tkv_ipc_get_handle(landing.data_ptr(), handle.ctypes.data_as(ct.POINTER(ct.c_uint8))))
+        check(lib().tkv_ipc_get_handle(landing.data_ptr(), handle.ctypes.data_as(ct.POINTER(ct.c_uint8)),
+                                       ct.byref(offset)))
     handles = [None] * world
-    dist.all_gather_object(handles, handle.tobytes())
+    dist.all_gather_object(handles, (handle.tobytes(), offset.value))
     result = {}
     if prefill:
         peer_ptr = ct.c_void_p()
-        h = np.frombuffer(handles[peer], np.uint8).copy()
-        check(lib().tkv_ipc_open_handle(h.ctypes.data_as(ct.POINTER(ct.c_uint8)), ct.byref(peer_ptr)))
+        h = np.frombuffer(handles[peer][0], np.uint8).copy()
+        peer_off = handles[peer][1]
+        check(lib().tkv_ipc_open_handle(h.ctypes.data_as(ct.POINTER(ct.c_uint8)), peer_off, ct.byref(peer_ptr)))
         e.bind_pages(qid, n)
         e.compute_range(qid, prompt, 0, n)  # prefill compute stand-in
         staging = torch.empty(chunks * stride, dtype=torch.uint8, device=dev)
@@ -648,7 +651,7 @@ def run_pd_pairs(args, world, rank, local):
         meta = torch.tensor([[r.addr - peer_ptr.value, r.bytes, r.token_count, r.first_token] for r in recs],
                             dtype=torch.int64, device=coll_device(dev))
         dist.send(meta, dst=peer)
-        lib().tkv_ipc_close(peer_ptr)
+        lib().tkv_ipc_close(peer_ptr, peer_off)
         del staging
         moved = sum(r.bytes for r in recs)
         best = min(t_sm, t_ce)

@@ -355,9 +355,12 @@ int tkv_pd_send_staged(tkv_pages* src, uint64_t query, size_t n_tokens, size_t c
 int tkv_pd_land(tkv_pages* dst, uint64_t query, const tkv_pd_record* recs, size_t n, void* stream);
 int tkv_enable_peer_access(int device, int peer);
 /* CUDA IPC for cross-process landing buffers (one process per GPU). */
-int tkv_ipc_get_handle(void* dev_ptr, uint8_t* handle64);
-int tkv_ipc_open_handle(const uint8_t* handle64, void** dev_ptr_out);
-int tkv_ipc_close(void* dev_ptr);
+/* A handle names the whole allocation that contains dev_ptr; offset_out is
+ * dev_ptr's offset in it (non-zero for sub-allocations of a caching
+ * allocator). open maps the allocation and returns base + offset. */
+int tkv_ipc_get_handle(void* dev_ptr, uint8_t* handle64, uint64_t* offset_out);
+int tkv_ipc_open_handle(const uint8_t* handle64, uint64_t offset, void** dev_ptr_out);
+int tkv_ipc_close(void* dev_ptr, uint64_t offset);
 
 #ifdef __cplusplus
 }

@@ -156,9 +156,9 @@ SIGNATURES = {
                                       ct.c_uint64, vp, ct.POINTER(PdRecordC), sz, szp]),
     "tkv_pd_land": (ct.c_int, [vp, ct.c_uint64, ct.POINTER(PdRecordC), sz, vp]),
     "tkv_enable_peer_access": (ct.c_int, [ct.c_int, ct.c_int]),
-    "tkv_ipc_get_handle": (ct.c_int, [vp, u8p]),
-    "tkv_ipc_open_handle": (ct.c_int, [u8p, ct.POINTER(vp)]),
-    "tkv_ipc_close": (ct.c_int, [vp]),
+    "tkv_ipc_get_handle": (ct.c_int, [vp, u8p, ct.POINTER(ct.c_uint64)]),
+    "tkv_ipc_open_handle": (ct.c_int, [u8p, ct.c_uint64, ct.POINTER(vp)]),
+    "tkv_ipc_close": (ct.c_int, [vp, ct.c_uint64]),
 }
 
 _lib = None

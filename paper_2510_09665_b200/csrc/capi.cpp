@@ -676,18 +676,42 @@ int tkv_pd_land(tkv_pages* dst, uint64_t q, const tkv_pd_record* recs, size_t n,
 int tkv_enable_peer_access(int device, int peer) {
     return guard([&] { return st(enable_peer_access(device, peer)); });
 }
-int tkv_ipc_get_handle(void* ptr, uint8_t* handle64) {
+// An IPC handle names the whole cudaMalloc allocation and maps at its base,
+// so a buffer carved out of a larger allocation (a caching allocator's
+// segment) travels as handle + offset from the allocation base. The base
+// comes from the driver's cuMemGetAddressRange, reached through the runtime
+// (no link-time libcuda dependency).
+int tkv_ipc_get_handle(void* ptr, uint8_t* handle64, uint64_t* offset) {
+    using GetRange = int (*)(unsigned long long*, size_t*, unsigned long long);
+    static GetRange get_range = [] {
+        void* fn = nullptr;
+        cudaDriverEntryPointQueryResult q{};
+        if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &fn, cudaEnableDefault, &q) != cudaSuccess)
+            fn = nullptr;
+        return reinterpret_cast<GetRange>(fn);
+    }();
     cudaIpcMemHandle_t h;
     int rc = cuda(cudaIpcGetMemHandle(&h, ptr));
-    if (rc == 0) std::memcpy(handle64, &h, sizeof h);
-    return rc;
+    if (rc != 0) return rc;
+    unsigned long long base = 0;
+    size_t size = 0;
+    if (!get_range || get_range(&base, &size, reinterpret_cast<unsigned long long>(ptr)) != 0)
+        return fail(Errc::cuda_error, "cuMemGetAddressRange failed");
+    std::memcpy(handle64, &h, sizeof h);
+    *offset = reinterpret_cast<unsigned long long>(ptr) - base;
+    return 0;
 }
-int tkv_ipc_open_handle(const uint8_t* handle64, void** out) {
+int tkv_ipc_open_handle(const uint8_t* handle64, uint64_t offset, void** out) {
     cudaIpcMemHandle_t h;
     std::memcpy(&h, handle64, sizeof h);
-    return cuda(cudaIpcOpenMemHandle(out, h, cudaIpcMemLazyEnablePeerAccess));
+    void* base = nullptr;
+    int rc = cuda(cudaIpcOpenMemHandle(&base, h, cudaIpcMemLazyEnablePeerAccess));
+    if (rc == 0) *out = static_cast<uint8_t*>(base) + offset;
+    return rc;
 }
-int tkv_ipc_close(void* ptr) { return cuda(cudaIpcCloseMemHandle(ptr)); }
+int tkv_ipc_close(void* ptr, uint64_t offset) {
+    return cuda(cudaIpcCloseMemHandle(static_cast<uint8_t*>(ptr) - offset));
+}
 
 int tkv_meta_timeline(tkv_meta* m, float* out, size_t cap, size_t* n) {
     return guard([&] {

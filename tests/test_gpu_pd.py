@@ -68,13 +68,45 @@ def test_pd_land_rejects_bad_records(tkv):
     dec.close()
 
 
-def test_pd_ipc_handle_roundtrip(tkv):
-    """The cross-process landing path: export a landing buffer with CUDA IPC
-    and map it back (same process here: cudaIpcOpenMemHandle refuses the
-    exporting process, which is the documented behaviour we assert)."""
+def _ipc_child(handle: bytes, offset: int, n: int, q):
+    """Second process: map the exported buffer and write a pattern into it."""
     import ctypes as ct
+    import torch
     from paper_2510_09665_b200._lib import lib
-    buf = torch.zeros(1 << 20, dtype=torch.uint8, device="cuda")
+    torch.cuda.set_device(0)
+    h = (ct.c_uint8 * 64).from_buffer_copy(handle)
+    ptr = ct.c_void_p()
+    rc = lib().tkv_ipc_open_handle(h, offset, ct.byref(ptr))
+    if rc == 0:
+        src = torch.arange(n, dtype=torch.int64, device="cuda").to(torch.uint8) ^ 0x5A
+        rc = lib().tkv_ce_copy(ct.c_void_p(src.data_ptr()), ptr, n, None)
+        torch.cuda.synchronize()
+        lib().tkv_ipc_close(ptr, offset)
+    q.put(rc)
+
+
+def test_pd_ipc_handle_suballocation(tkv):
+    """The cross-process landing path with a buffer carved out of a larger
+    allocation (what a caching allocator hands out): the handle maps the
+    allocation base, the offset travels beside it, and the other process's
+    writes land exactly in the sub-buffer."""
+    import ctypes as ct
+    import multiprocessing as mp
+    from paper_2510_09665_b200._lib import lib
+    big = torch.zeros(4 << 20, dtype=torch.uint8, device="cuda")
+    off0, n = 3 * 4096 + 256, 1 << 20
+    buf = big[off0:off0 + n]
     h = (ct.c_uint8 * 64)()
-    assert lib().tkv_ipc_get_handle(buf.data_ptr(), h) == 0
-    assert any(h[i] for i in range(64))
+    offset = ct.c_uint64(0)
+    assert lib().tkv_ipc_get_handle(ct.c_void_p(buf.data_ptr()), h, ct.byref(offset)) == 0
+    assert offset.value >= off0  # at least the carve-out; more if torch's segment is shared
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    p = ctx.Process(target=_ipc_child, args=(bytes(h), offset.value, n, q))
+    p.start()
+    rc = q.get(timeout=120)
+    p.join(timeout=60)
+    assert rc == 0
+    want = (torch.arange(n, dtype=torch.int64, device="cuda").to(torch.uint8) ^ 0x5A)
+    assert torch.equal(buf, want)
+    assert int(big[:off0].count_nonzero()) == 0 and int(big[off0 + n:].count_nonzero()) == 0
