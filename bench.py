@@ -730,6 +730,10 @@ def run_b200(args):
     peak_source = ("MEASURED_PEAKS.json hbm_gbs (copy, read+write)" if "hbm_gbs" in peaks
                    else "fallback 6650 GB/s (B200_PROFILING.md; MEASURED_PEAKS.json absent)")
     pcie = measure_pcie(torch, bench.dev)
+    pcie_all = [pcie]
+    if world > 1:  # every rank's own link, for the per-GPU and aggregate roofline
+        pcie_all = [None] * world
+        dist.all_gather_object(pcie_all, pcie)
 
     def barrier():
         if world > 1:
@@ -847,7 +851,9 @@ def run_b200(args):
         "roofline": {"bound": "hbm", "kernel": dom, "achieved": round(achieved, 1), "peak": hbm_peak,
                      "unit": "GB/s", "frac": round(achieved / hbm_peak, 4),
                      **ncu_traffic(dom, dom_bytes, bench), "peak_source": peak_source},
-        "links": {"pcie": pcie, "e2e_frac_of_pcie_bidir": round(e2e / world / pcie["bidir_gbps"], 4)},
+        "links": {"pcie": pcie, "pcie_bidir_per_rank": [p["bidir_gbps"] for p in pcie_all],
+                  "pcie_bidir_aggregate": round(sum(p["bidir_gbps"] for p in pcie_all), 2),
+                  "e2e_frac_of_pcie_bidir": round(e2e / sum(p["bidir_gbps"] for p in pcie_all), 4)},
         "gpu_launches": int(e2e_launches),
         "kernel_launches_value": int(kr["launches"]),
         "parity": {"value_pages_mismatch_words": kr["mismatch_words"]},
