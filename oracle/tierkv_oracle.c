@@ -252,8 +252,10 @@ size_t tkvo_q8_decode(const uint8_t* blob, size_t n, uint8_t* payload) {
     if (n != 8 + lanes + (len & 1)) return 0;
     for (size_t i = 0; i < lanes; ++i) {
         double v = round((double)(int8_t)blob[8 + i] * (double)scale);
-        if (v > 32767.0) v = 32767.0;
-        if (v < -32768.0) v = -32768.0;
+        /* std::max(-32768.0, v) then std::min(32767.0, v) (codec.cpp:65): the
+           comparisons are false for NaN, so a NaN product becomes -32768 */
+        v = (-32768.0 < v) ? v : -32768.0;
+        v = (v < 32767.0) ? v : 32767.0;
         uint16_t lane = (uint16_t)(int16_t)v;
         payload[2 * i] = (uint8_t)(lane & 0xff);
         payload[2 * i + 1] = (uint8_t)(lane >> 8);

@@ -20,6 +20,8 @@ namespace {
 
 constexpr int kThreads = 256;
 constexpr uint64_t kSeg = 64 * 1024;  // payload bytes per CTA work item
+constexpr int kUnroll = 4;            // 16-byte vectors in flight per thread
+constexpr uint64_t kStride = 16 * kThreads;
 
 __device__ __forceinline__ int32_t lane16(uint32_t w, int half) {
     return int32_t(int16_t(uint16_t(w >> (16 * half))));
@@ -41,15 +43,25 @@ q8_absmax_kernel(const CodecItem* __restrict__ items, const uint32_t* __restrict
         const uint64_t lanes_end = it.bytes & ~uint64_t(1);
         const uint64_t b1 = min(b0 + kSeg, lanes_end);
         int m = 0;
-        if ((reinterpret_cast<uint64_t>(it.src) & 3) == 0) {
-            for (uint64_t b = b0 + 4 * threadIdx.x; b + 4 <= b1; b += 4 * kThreads) {
-                const uint32_t w = __ldcs(reinterpret_cast<const unsigned int*>(it.src + b));
-                m = max(m, max(abs(lane16(w, 0)), abs(lane16(w, 1))));
+        if ((reinterpret_cast<uint64_t>(it.src) & 15) == 0) {
+            // 16-byte loads, 8 lanes each: per-halfword |lane| (non-saturating,
+            // so -32768 -> 0x8000 = 32768 unsigned) folded with unsigned max
+            const uint64_t vend = b0 + ((b1 - b0) & ~uint64_t(15));
+            uint32_t m2 = 0;
+            for (uint64_t b = b0 + 16 * threadIdx.x; b < vend; b += kStride * kUnroll) {
+                uint4 v[kUnroll];
+#pragma unroll
+                for (int u = 0; u < kUnroll; ++u)
+                    v[u] = b + u * kStride < vend ? __ldcs(reinterpret_cast<const uint4*>(it.src + b + u * kStride))
+                                                  : make_uint4(0, 0, 0, 0);
+#pragma unroll
+                for (int u = 0; u < kUnroll; ++u)
+                    m2 = __vmaxu2(m2, __vmaxu2(__vmaxu2(__vabs2(v[u].x), __vabs2(v[u].y)),
+                                               __vmaxu2(__vabs2(v[u].z), __vabs2(v[u].w))));
             }
-            // a 2-byte lane left over when (b1 - b0) % 4 == 2
-            const uint64_t tail = b0 + ((b1 - b0) & ~uint64_t(3));
-            if (threadIdx.x == 0 && tail + 2 <= b1)
-                m = max(m, abs(int32_t(int16_t(uint16_t(it.src[tail] | (it.src[tail + 1] << 8))))));
+            m = int(max(m2 & 0xffffu, m2 >> 16));
+            for (uint64_t b = vend + 2 * threadIdx.x; b + 2 <= b1; b += 2 * kThreads)
+                m = max(m, abs(int32_t(int16_t(uint16_t(it.src[b] | (it.src[b + 1] << 8))))));
         } else {
             for (uint64_t b = b0 + 2 * threadIdx.x; b + 2 <= b1; b += 2 * kThreads)
                 m = max(m, abs(int32_t(int16_t(uint16_t(it.src[b] | (it.src[b + 1] << 8))))));
@@ -67,10 +79,21 @@ q8_absmax_kernel(const CodecItem* __restrict__ items, const uint32_t* __restrict
     }
 }
 
-__device__ __forceinline__ uint32_t quant(int32_t lane, float scale) {
-    double q = scale > 0.f ? round(double(lane) / double(scale)) : 0.0;
-    q = fmin(127.0, fmax(-127.0, q));
-    return uint32_t(uint8_t(int8_t(q)));
+// round(double(lane) / double(scale)) without the division (codec.cpp:42-44).
+// scale is a float (24-bit significand M) and |lane| <= 32768, so a quotient
+// that is not exactly k + 1/2 lies at least 1/(2M) >= 2^-25 away from every
+// half-integer, while lane * (1/scale) in double is within ~6e-14 of the
+// quotient: rounding the product gives the quotient's rounding, except at an
+// exact tie, recognised by a fractional part within 1e-10 of 1/2, where
+// round-half-away-from-zero gives floor(|q|) + 1. (The reference's correctly
+// rounded double quotient rounds the same way for the same reason.)
+__device__ __forceinline__ uint32_t quant(int32_t lane, double inv) {
+    const double y = double(lane) * inv;
+    const double a = fabs(y);
+    const double fl = floor(a);
+    double q = fabs(a - fl - 0.5) < 1e-10 ? fl + 1.0 : round(a);
+    q = fmin(127.0, q);
+    return uint32_t(uint8_t(int8_t(int32_t(y < 0.0 ? -q : q))));
 }
 
 __global__ void __launch_bounds__(kThreads)
@@ -84,6 +107,7 @@ q8_encode_kernel(const CodecItem* __restrict__ items, const uint32_t* __restrict
         }
         const CodecItem it = items[lo];
         const float scale = float(double(maxabs[lo]) / 127.0);
+        const double inv = scale > 0.f ? 1.0 / double(scale) : 0.0;  // scale 0: every lane is 0
         const uint32_t local = seg - seg_base[lo];
         if (local == 0 && threadIdx.x == 0) {
             const uint32_t len = uint32_t(it.bytes);
@@ -99,11 +123,43 @@ q8_encode_kernel(const CodecItem* __restrict__ items, const uint32_t* __restrict
         const uint64_t lanes_end = it.bytes & ~uint64_t(1);
         const uint64_t b1 = min(b0 + kSeg, lanes_end);
         uint8_t* out = it.dst + 8;
-        for (uint64_t b = b0 + 2 * threadIdx.x; b + 2 <= b1; b += 2 * kThreads) {
+        uint64_t vend = b0;
+        if (((reinterpret_cast<uint64_t>(it.src) & 15) | (reinterpret_cast<uint64_t>(out) & 7)) == 0) {
+            vend = b0 + ((b1 - b0) & ~uint64_t(15));
+            for (uint64_t b = b0 + 16 * threadIdx.x; b < vend; b += kStride * kUnroll) {
+                uint4 v[kUnroll];
+#pragma unroll
+                for (int u = 0; u < kUnroll; ++u)
+                    if (b + u * kStride < vend) v[u] = __ldcs(reinterpret_cast<const uint4*>(it.src + b + u * kStride));
+#pragma unroll
+                for (int u = 0; u < kUnroll; ++u) {
+                    if (b + u * kStride >= vend) break;
+                    const uint32_t w[4] = {v[u].x, v[u].y, v[u].z, v[u].w};
+                    uint32_t o[2];
+#pragma unroll
+                    for (int k = 0; k < 2; ++k)
+                        o[k] = quant(lane16(w[2 * k], 0), inv) | (quant(lane16(w[2 * k], 1), inv) << 8) |
+                               (quant(lane16(w[2 * k + 1], 0), inv) << 16) |
+                               (quant(lane16(w[2 * k + 1], 1), inv) << 24);
+                    __stcs(reinterpret_cast<uint2*>(out + (b + u * kStride) / 2), make_uint2(o[0], o[1]));
+                }
+            }
+        }
+        for (uint64_t b = vend + 2 * threadIdx.x; b + 2 <= b1; b += 2 * kThreads) {
             const int32_t lane = int32_t(int16_t(uint16_t(it.src[b] | (it.src[b + 1] << 8))));
-            out[b / 2] = uint8_t(quant(lane, scale));
+            out[b / 2] = uint8_t(quant(lane, inv));
         }
     }
+}
+
+// round(double(q) * double(scale)) clamped to int16 (codec.cpp:62-68): the
+// product of an 8-bit and a 24-bit significand is exact in double, and the
+// formula holds for any scale bit pattern the blob carries (0, subnormal,
+// negative, inf, NaN: fmax(-32768, NaN) = -32768 like std::max's order).
+__device__ __forceinline__ uint32_t dequant(int8_t q, double sc) {
+    double v = round(double(q) * sc);
+    v = fmin(32767.0, fmax(-32768.0, v));
+    return uint32_t(uint16_t(int16_t(v)));
 }
 
 __global__ void __launch_bounds__(kThreads)
@@ -125,11 +181,32 @@ q8_decode_kernel(const CodecItem* __restrict__ items, const uint32_t* __restrict
             it.dst[it.bytes - 1] = it.src[8 + it.bytes / 2];
         const uint64_t b0 = uint64_t(local) * kSeg;
         const uint64_t b1 = min(b0 + kSeg, it.bytes & ~uint64_t(1));
-        for (uint64_t b = b0 + 2 * threadIdx.x; b + 2 <= b1; b += 2 * kThreads) {
-            const int8_t q = int8_t(it.src[8 + b / 2]);
-            double v = round(double(q) * double(scale));
-            v = fmin(32767.0, fmax(-32768.0, v));
-            const uint16_t lane = uint16_t(int16_t(v));
+        const double sc = double(scale);
+        uint64_t vend = b0;
+        if (((reinterpret_cast<uint64_t>(it.src + 8) & 7) | (reinterpret_cast<uint64_t>(it.dst) & 15)) == 0) {
+            vend = b0 + ((b1 - b0) & ~uint64_t(15));
+            for (uint64_t b = b0 + 16 * threadIdx.x; b < vend; b += kStride * kUnroll) {
+                uint2 qv[kUnroll];
+#pragma unroll
+                for (int u = 0; u < kUnroll; ++u)
+                    if (b + u * kStride < vend)
+                        qv[u] = __ldcs(reinterpret_cast<const uint2*>(it.src + 8 + (b + u * kStride) / 2));
+#pragma unroll
+                for (int u = 0; u < kUnroll; ++u) {
+                    if (b + u * kStride >= vend) break;
+                    uint32_t o[4];
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) {
+                        const uint32_t w = k < 2 ? qv[u].x : qv[u].y;
+                        o[k] = dequant(int8_t(w >> (16 * (k & 1))), sc) |
+                               (dequant(int8_t(w >> (16 * (k & 1) + 8)), sc) << 16);
+                    }
+                    __stcs(reinterpret_cast<uint4*>(it.dst + b + u * kStride), make_uint4(o[0], o[1], o[2], o[3]));
+                }
+            }
+        }
+        for (uint64_t b = vend + 2 * threadIdx.x; b + 2 <= b1; b += 2 * kThreads) {
+            const uint32_t lane = dequant(int8_t(it.src[8 + b / 2]), sc);
             it.dst[b] = uint8_t(lane & 0xff);
             it.dst[b + 1] = uint8_t(lane >> 8);
         }

@@ -23,12 +23,30 @@ def _payloads():
     return out
 
 
+SPECIAL_SCALES = [1.0, 0.5, 1 / 127, 258.0157480314961, 3.0e-5, 1.0e-30, 7.0e5, 8388608.0, 3.0e38,
+                  1.0e-40, 0.0, -0.0, -2.5, float("inf"), float("-inf"), float("nan")]
+
+
+def _scale_blobs():
+    """Blobs carrying every int8 code under arbitrary scale bit patterns."""
+    q = np.arange(256, dtype=np.uint8)
+    scales = SPECIAL_SCALES + list(np.random.default_rng(11).uniform(0.001, 300.0, size=24))
+    n = 2 * q.size + 1
+    return scales, [np.concatenate([np.frombuffer(np.uint32(n).tobytes(), np.uint8),
+                                    np.frombuffer(np.float32(s).tobytes(), np.uint8), q, [0x5A]]).astype(np.uint8)
+                    for s in scales], n
+
+
 def test_oracle_q8_matches_reference(C, Ref):
     for p in _payloads():
         blob = C.q8_encode(p)
         assert np.array_equal(blob, Ref.q8_encode(p)), p.size
         dec, code = Ref.q8_decode(blob)
         assert code == 0 and np.array_equal(C.q8_decode(blob), dec)
+    scales, blobs, _ = _scale_blobs()
+    for s, b in zip(scales, blobs):
+        dec, code = Ref.q8_decode(b)
+        assert code == 0 and np.array_equal(C.q8_decode(b), dec), s
 
 
 def test_oracle_q8_golden(C):
@@ -78,3 +96,33 @@ def test_device_q8_matches_oracle(tkv, C):
     back = q8_decode(blobs, [p.size for p in ps])
     for p, b, d in zip(ps, blobs, back):
         assert np.array_equal(d.cpu().numpy(), C.q8_decode(C.q8_encode(p))), p.size
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("maxabs", [1, 2, 3, 5, 127, 128, 254, 255, 1000, 4097, 12345, 32767, 32768])
+def test_device_q8_encode_every_lane(tkv, C, maxabs):
+    """Every lane value in [-maxabs, maxabs] (including the exact .5 ties the
+    scale produces) quantises to the reference's byte: the device's integer
+    rounding against the oracle's double division."""
+    from paper_2510_09665_b200.api import q8_decode, q8_encode
+    rng = np.random.default_rng(maxabs)
+    lanes = np.arange(-maxabs, min(maxabs, 32767) + 1, dtype=np.int64)
+    lanes = np.concatenate([lanes, [-maxabs if maxabs == 32768 else maxabs]])
+    rng.shuffle(lanes)
+    p = lanes.astype(np.int16).view(np.uint8)
+    blob = q8_encode([torch.from_numpy(p.copy()).cuda()])[0].cpu().numpy()
+    assert np.array_equal(blob, C.q8_encode(p))
+    back = q8_decode([torch.from_numpy(blob.copy()).cuda()], [p.size])[0].cpu().numpy()
+    assert np.array_equal(back, C.q8_decode(blob))
+
+
+@pytest.mark.gpu
+def test_device_q8_decode_any_scale_bits(tkv, C):
+    """Decode takes the scale from the blob: every int8 code under scales that
+    are normal, tiny, huge, subnormal, zero, negative, infinite and NaN equals
+    the reference's double formula."""
+    from paper_2510_09665_b200.api import q8_decode
+    scales, blobs, n = _scale_blobs()
+    outs = q8_decode([torch.from_numpy(b.copy()).cuda() for b in blobs], [n] * len(blobs))
+    for s, b, o in zip(scales, blobs, outs):
+        assert np.array_equal(o.cpu().numpy(), C.q8_decode(b)), s

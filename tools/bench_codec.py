@@ -1,0 +1,84 @@
+"""q8-scale codec kernels on the B200: encode and
+decode of 16 chunk payloads of the 8B model (32 layers x 256 tokens x 4096 B
+= 32 MiB each, 512 MiB per launch), device time by CUDA events, HBM GB/s of
+the algorithmic bytes (encode: read payload twice — absmax, quantise — and
+write half of it; decode: read the blob, write the payload), bytes checked
+against the reference codec (oracle/_ref Q8ScaleCodec) on one chunk; the
+reference's own encode/decode timed on one core for the same chunk."""
+import ctypes as ct
+import json
+import os
+import sys
+import time
+
+import numpy as np
+import torch
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+from paper_2510_09665_b200._lib import CodecItemC, check, lib, u32p  # noqa: E402
+
+
+def main(n_items=16, nbytes=32 << 20, reps=5):
+    g = torch.Generator(device="cuda").manual_seed(3)
+    # KV-like lanes: normal-ish int16 values
+    pay = [(torch.randn(nbytes // 2, device="cuda", generator=g) * 3000).clamp(-32768, 32767).to(torch.int16)
+           .view(torch.uint8) for _ in range(n_items)]
+    blob_b = int(lib().tkv_q8_blob_bytes(nbytes))
+    blobs = [torch.empty(blob_b, dtype=torch.uint8, device="cuda") for _ in range(n_items)]
+    outs = [torch.empty(nbytes, dtype=torch.uint8, device="cuda") for _ in range(n_items)]
+
+    def plan(srcs, dsts):
+        items = (CodecItemC * n_items)(*[CodecItemC(s.data_ptr(), d.data_ptr(), nbytes) for s, d in zip(srcs, dsts)])
+        seg = np.zeros(n_items + 1, np.uint32)
+        check(lib().tkv_codec_plan(ct.cast(items, ct.c_void_p), n_items, seg.ctypes.data_as(u32p)))
+        return (torch.frombuffer(bytearray(bytes(items)), dtype=torch.uint8).cuda(),
+                torch.from_numpy(seg.view(np.int32)).cuda(), int(seg[-1]))
+    ei, es, en = plan(pay, blobs)
+    di, ds, dn = plan(blobs, outs)
+    scratch = torch.zeros(n_items, dtype=torch.int32, device="cuda")
+    s = torch.cuda.current_stream().cuda_stream
+
+    def enc():
+        check(lib().tkv_q8_encode(ei.data_ptr(), es.data_ptr(), n_items, en, scratch.data_ptr(), s))
+
+    def dec():
+        check(lib().tkv_q8_decode(di.data_ptr(), ds.data_ptr(), n_items, dn, s))
+
+    def timed(fn):
+        fn()
+        torch.cuda.synchronize()
+        ts = []
+        for _ in range(reps):
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            fn()
+            b.record()
+            torch.cuda.synchronize()
+            ts.append(a.elapsed_time(b))
+        return min(ts)
+    te, td = timed(enc), timed(dec)
+    payload = n_items * nbytes
+    res = {"codec": "q8-scale", "items": n_items, "payload_bytes_per_item": nbytes,
+           "encode_ms": round(te, 4), "decode_ms": round(td, 4),
+           "encode_hbm_gbps": round(2.5 * payload / te / 1e6, 1),
+           "decode_hbm_gbps": round(1.5 * payload / td / 1e6, 1),
+           "encode_payload_gbps": round(payload / te / 1e6, 1), "decode_payload_gbps": round(payload / td / 1e6, 1)}
+    import oracle
+    if oracle.ref_available():
+        R = oracle.Ref()
+        p0 = pay[0].cpu().numpy()
+        t0 = time.perf_counter()
+        want = R.q8_encode(p0)
+        t1 = time.perf_counter()
+        back, _ = R.q8_decode(want)
+        t2 = time.perf_counter()
+        res["bytes_equal_reference"] = bool(np.array_equal(blobs[0].cpu().numpy(), want)
+                                            and np.array_equal(outs[0].cpu().numpy(), back))
+        res["ref_cpu_encode_gbps_1core"] = round(nbytes / (t1 - t0) / 1e9, 3)
+        res["ref_cpu_decode_gbps_1core"] = round(nbytes / (t2 - t1) / 1e9, 3)
+    print(json.dumps(res))
+
+
+if __name__ == "__main__":
+    main()
