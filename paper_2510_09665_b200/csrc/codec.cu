@@ -83,17 +83,17 @@ q8_absmax_kernel(const CodecItem* __restrict__ items, const uint32_t* __restrict
 // scale is a float (24-bit significand M) and |lane| <= 32768, so a quotient
 // that is not exactly k + 1/2 lies at least 1/(2M) >= 2^-25 away from every
 // half-integer, while lane * (1/scale) in double is within ~6e-14 of the
-// quotient: rounding the product gives the quotient's rounding, except at an
-// exact tie, recognised by a fractional part within 1e-10 of 1/2, where
-// round-half-away-from-zero gives floor(|q|) + 1. (The reference's correctly
-// rounded double quotient rounds the same way for the same reason.)
+// quotient. So round-half-away-from-zero of the quotient is
+// floor(|product| + 1/2 + 1e-10): the 1e-10 lifts an exact tie that the
+// product missed by ~1e-13 over the half-integer, and is far too small to
+// move any other quotient across one. (The reference's correctly rounded
+// double quotient rounds the same way for the same reason.) One DMUL, one
+// DADD and a truncating conversion per lane.
 __device__ __forceinline__ uint32_t quant(int32_t lane, double inv) {
-    const double y = double(lane) * inv;
-    const double a = fabs(y);
-    const double fl = floor(a);
-    double q = fabs(a - fl - 0.5) < 1e-10 ? fl + 1.0 : round(a);
-    q = fmin(127.0, q);
-    return uint32_t(uint8_t(int8_t(int32_t(y < 0.0 ? -q : q))));
+    const double a = fabs(double(lane) * inv);
+    int32_t q = __double2int_rz(a + (0.5 + 1e-10));
+    q = min(q, 127);
+    return uint32_t(uint8_t(int8_t(lane < 0 ? -q : q)));
 }
 
 __global__ void __launch_bounds__(kThreads)
@@ -152,19 +152,27 @@ q8_encode_kernel(const CodecItem* __restrict__ items, const uint32_t* __restrict
     }
 }
 
-// round(double(q) * double(scale)) clamped to int16 (codec.cpp:62-68): the
-// product of an 8-bit and a 24-bit significand is exact in double, and the
-// formula holds for any scale bit pattern the blob carries (0, subnormal,
-// negative, inf, NaN: fmax(-32768, NaN) = -32768 like std::max's order).
+// round(double(q) * double(scale)) clamped to int16 (codec.cpp:62-68), for
+// any scale bit pattern the blob carries. The product v of an 8-bit and a
+// 24-bit significand is exact; v +- 1/2 is exact too wherever it can matter
+// (|v| < 2^15 with no bits below 2^-38 — a scale small enough to have them
+// gives |v| < 1/2), so truncating v +- 1/2 rounds half away from zero. The
+// truncating conversion saturates +-inf; a NaN product (0 * inf, NaN scale)
+// is -32768, as std::max(-32768.0, NaN) returns its first argument.
 __device__ __forceinline__ uint32_t dequant(int8_t q, double sc) {
-    double v = round(double(q) * sc);
-    v = fmin(32767.0, fmax(-32768.0, v));
-    return uint32_t(uint16_t(int16_t(v)));
+    const double v = double(q) * sc;
+    if (v != v) return 0x8000u;
+    int32_t r = __double2int_rz(v + (v < 0.0 ? -0.5 : 0.5));
+    r = max(-32768, min(32767, r));
+    return uint32_t(uint16_t(int16_t(r)));
 }
 
 __global__ void __launch_bounds__(kThreads)
 q8_decode_kernel(const CodecItem* __restrict__ items, const uint32_t* __restrict__ seg_base,
                  uint32_t n_items, uint32_t total_segs) {
+    // An item has one scale, so its 256 possible codes decode through a
+    // 256-entry table built per segment: one shared-memory load per lane.
+    __shared__ uint16_t table[256];
     for (uint32_t seg = blockIdx.x; seg < total_segs; seg += gridDim.x) {
         uint32_t lo = 0, hi = n_items;
         while (hi - lo > 1) {
@@ -182,6 +190,9 @@ q8_decode_kernel(const CodecItem* __restrict__ items, const uint32_t* __restrict
         const uint64_t b0 = uint64_t(local) * kSeg;
         const uint64_t b1 = min(b0 + kSeg, it.bytes & ~uint64_t(1));
         const double sc = double(scale);
+        __syncthreads();  // previous segment done with the table
+        for (uint32_t c = threadIdx.x; c < 256; c += kThreads) table[c] = uint16_t(dequant(int8_t(uint8_t(c)), sc));
+        __syncthreads();
         uint64_t vend = b0;
         if (((reinterpret_cast<uint64_t>(it.src + 8) & 7) | (reinterpret_cast<uint64_t>(it.dst) & 15)) == 0) {
             vend = b0 + ((b1 - b0) & ~uint64_t(15));
@@ -198,15 +209,15 @@ q8_decode_kernel(const CodecItem* __restrict__ items, const uint32_t* __restrict
 #pragma unroll
                     for (int k = 0; k < 4; ++k) {
                         const uint32_t w = k < 2 ? qv[u].x : qv[u].y;
-                        o[k] = dequant(int8_t(w >> (16 * (k & 1))), sc) |
-                               (dequant(int8_t(w >> (16 * (k & 1) + 8)), sc) << 16);
+                        o[k] = uint32_t(table[(w >> (16 * (k & 1))) & 0xff]) |
+                               (uint32_t(table[(w >> (16 * (k & 1) + 8)) & 0xff]) << 16);
                     }
                     __stcs(reinterpret_cast<uint4*>(it.dst + b + u * kStride), make_uint4(o[0], o[1], o[2], o[3]));
                 }
             }
         }
         for (uint64_t b = vend + 2 * threadIdx.x; b + 2 <= b1; b += 2 * kThreads) {
-            const uint32_t lane = dequant(int8_t(it.src[8 + b / 2]), sc);
+            const uint32_t lane = table[it.src[8 + b / 2]];
             it.dst[b] = uint8_t(lane & 0xff);
             it.dst[b + 1] = uint8_t(lane >> 8);
         }
