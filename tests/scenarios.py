@@ -406,3 +406,33 @@ def sc_random_trace_decode(factory, C):
 
 ALL += [sc_random_trace_roomy, sc_random_trace_evicting, sc_random_trace_pinned, sc_random_trace_blocking,
         sc_random_trace_decode]
+
+
+def sc_degenerate_prompts(factory, C):
+    """Edge lengths through the whole connector sequence: 1 token, exactly one
+    chunk, one chunk + 1, a chunk minus 1, a page exactly, and an empty
+    lookup (cap min(lpm, len - 1), connector.cpp:75-76)."""
+    e = factory(**CONN, ram_slots=32, num_pages=256)
+    out = {"empty": e.get_num_new_matched_tokens(1, np.zeros(0, np.uint32))}
+    qid = 10
+    for n in (1, 32, 33, 31, 16):
+        p = make_prompt(n, 500 + n)
+        for rnd in range(2):  # cold store, then warm retrieve of the same prompt
+            mt = e.get_num_new_matched_tokens(qid, p)
+            e.bind_pages(qid, n)
+            upd = e.update_state_after_alloc(qid, (n + 15) // 16, (mt + 15) // 16)
+            m = e.build_connector_meta([(qid, p)])
+            transfer(e, m, qid, p)
+            out[f"n{n}_r{rnd}"] = {"matched": mt, "upd": upd, "plan": plan_view(e, m, 0),
+                                   "loaded": e.loaded_tokens(m, qid),
+                                   "ok": pages_equal_synth(e, qid, p, n, C),
+                                   "res": [(d.hex(), c) for d, c in e.store_results(m, qid)]}
+            e.finish_query(qid)
+            e.release_query(qid)
+            qid += 1
+    out["entries"] = e.store_entries()
+    e.close()
+    return out
+
+
+ALL += [sc_degenerate_prompts]
