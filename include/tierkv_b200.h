@@ -286,6 +286,11 @@ int tkv_connector_start_load_kv(tkv_connector* c, tkv_meta* m);
 int tkv_connector_wait_load_kv(tkv_connector* c, tkv_meta* m, uint32_t layer);
 int tkv_connector_start_store_kv(tkv_connector* c, tkv_meta* m);
 int tkv_connector_wait_store_kv(tkv_connector* c, tkv_meta* m, uint32_t layer);
+/* Connector::prefetch / drain_prefetch (connector.hpp:96-99): promote
+ * matched chunks from slower tiers; the pinned RAM tier is the only tier
+ * here, so both return at once (kept for API parity). */
+int tkv_connector_prefetch(tkv_connector* c, const uint32_t* tokens, size_t n);
+int tkv_connector_drain_prefetch(tkv_connector* c);
 int tkv_connector_begin_decode(tkv_connector* c, uint64_t query);
 int tkv_connector_append_decode(tkv_connector* c, uint64_t query, uint32_t token);
 int tkv_connector_finish_query(tkv_connector* c, uint64_t query, uint8_t* digests_out, size_t cap,

@@ -128,6 +128,8 @@ SIGNATURES = {
     "tkv_connector_wait_load_kv": (ct.c_int, [vp, vp, ct.c_uint32]),
     "tkv_connector_start_store_kv": (ct.c_int, [vp, vp]),
     "tkv_connector_wait_store_kv": (ct.c_int, [vp, vp, ct.c_uint32]),
+    "tkv_connector_prefetch": (ct.c_int, [vp, u32p, sz]),
+    "tkv_connector_drain_prefetch": (ct.c_int, [vp]),
     "tkv_connector_begin_decode": (ct.c_int, [vp, ct.c_uint64]),
     "tkv_connector_append_decode": (ct.c_int, [vp, ct.c_uint64, ct.c_uint32]),
     "tkv_connector_finish_query": (ct.c_int, [vp, ct.c_uint64, u8p, sz, szp]),

@@ -572,6 +572,18 @@ int tkv_connector_start_store_kv(tkv_connector* c, tkv_meta* m) {
 int tkv_connector_wait_store_kv(tkv_connector* c, tkv_meta* m, uint32_t layer) {
     return guard([&] { return st(c->c->wait_store_kv(m->m, layer)); });
 }
+int tkv_connector_prefetch(tkv_connector* c, const uint32_t* tokens, size_t n) {
+    return guard([&] {
+        c->c->prefetch(TokenSpanView(tokens, n));
+        return 0;
+    });
+}
+int tkv_connector_drain_prefetch(tkv_connector* c) {
+    return guard([&] {
+        c->c->drain_prefetch();
+        return 0;
+    });
+}
 int tkv_connector_begin_decode(tkv_connector* c, uint64_t q) {
     return guard([&] { return st(c->c->begin_decode(q)); });
 }

@@ -121,6 +121,14 @@ public:
     Status start_store_kv(ConnectorMetadata& meta);
     Status wait_store_kv(ConnectorMetadata& meta, uint32_t layer);
 
+    // Prefetch (connector.cpp:393-431) promotes matched chunks that sit only
+    // in slower tiers (disk, remote) into the prefetch tiers. The pinned RAM
+    // tier is the only tier on this path, so every present chunk is already
+    // in the fastest one and both calls have nothing to do — kept so the API
+    // is the reference's.
+    void prefetch(TokenSpanView) {}
+    void drain_prefetch() {}
+
     // Delayed decode storing (connector.cpp:434-497): the decode tokens' KV
     // lives in the query's pages; full chunks are gathered straight from the
     // pages into pinned slots (K1) as they complete.
