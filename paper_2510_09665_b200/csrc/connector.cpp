@@ -261,14 +261,16 @@ std::vector<size_t> Connector::get_num_new_matched_tokens(
     const auto t0 = std::chrono::steady_clock::now();
     auto digests = hasher_.hash(prompts);  // one K3 launch for the whole batch
     const auto t1 = std::chrono::steady_clock::now();
-    KeyIndex index = [this](const ChunkKey& k) { return store_.contains(k.digest); };
+    // LPM (tokens.cpp:59-69) over the hashed chain: the leading present
+    // chunks, probed under one store lock per query.
     std::vector<size_t> out(ids.size());
     for (size_t q = 0; q < ids.size(); ++q) {
         std::vector<ChunkKey> keys(digests[q].size());
         for (size_t i = 0; i < keys.size(); ++i)
             keys[i] = ChunkKey{digests[q][i], store_.config().model.model_tag, uint32_t(i)};
         const size_t n = prompts[q].size();
-        const size_t lpm = longest_prefix_match(keys, n, cs, index);
+        const size_t present = store_.present_prefix(digests[q]);
+        const size_t lpm = present == 0 ? 0 : std::min(n, present * cs);
         const size_t cap = n == 0 ? 0 : n - 1;  // connector.cpp:75-76
         const size_t matched = std::min(lpm, cap);
         std::lock_guard lock(mu_);

@@ -314,6 +314,16 @@ bool TieredStore::contains(const Digest& digest) const {
     return it != index_.end() && it->second.state == Entry::State::present;
 }
 
+size_t TieredStore::present_prefix(const std::vector<Digest>& digests) const {
+    std::lock_guard lock(mu_);
+    size_t k = 0;
+    for (; k < digests.size(); ++k) {
+        auto it = index_.find(digests[k]);
+        if (it == index_.end() || it->second.state != Entry::State::present) break;
+    }
+    return k;
+}
+
 Status TieredStore::pin(const Digest& digest, bool on) {
     std::lock_guard lock(mu_);
     auto it = index_.find(digest);

@@ -146,6 +146,9 @@ public:
     Result<std::vector<uint8_t>> get(const Digest& digest);
     Result<std::vector<uint8_t>> get_layer(const Digest& digest, uint32_t layer);
     bool contains(const Digest& digest) const;
+    // Leading entries of `digests` that are present, under one lock (the
+    // reference probes contains() once per chunk, store.cpp:797-806).
+    size_t present_prefix(const std::vector<Digest>& digests) const;
     Status pin(const Digest& digest, bool on);
     ClearResult clear(const std::vector<Digest>& digests);
     size_t evict_until(size_t bytes_needed);
