@@ -20,6 +20,14 @@ using namespace tkv;
 static_assert(sizeof(tkv_paged_layout) == sizeof(PagedLayout));
 static_assert(sizeof(tkv_xfer_desc) == sizeof(XferDesc));
 static_assert(sizeof(tkv_chain_desc) == sizeof(ChainDesc));
+// Device arrays of these cross the ABI by pointer: the field offsets must agree.
+static_assert(offsetof(tkv_xfer_desc, layer_stride) == offsetof(XferDesc, layer_stride));
+static_assert(offsetof(tkv_xfer_desc, table_dev) == offsetof(XferDesc, table));
+static_assert(offsetof(tkv_xfer_desc, first_page) == offsetof(XferDesc, first_page));
+static_assert(offsetof(tkv_xfer_desc, n_tokens) == offsetof(XferDesc, n_tokens));
+static_assert(offsetof(tkv_chain_desc, n_tokens) == offsetof(ChainDesc, n_tokens));
+static_assert(offsetof(tkv_chain_desc, out_first) == offsetof(ChainDesc, out_first));
+static_assert(offsetof(tkv_chain_desc, parent) == offsetof(ChainDesc, parent));
 
 struct tkv_pages {
     std::unique_ptr<PagedKVStore> p;
@@ -89,7 +97,16 @@ Digest to_digest(const uint8_t* p) {
 
 PagedLayout to_layout(const tkv_paged_layout* l) {
     PagedLayout L;
-    std::memcpy(&L, l, sizeof L);
+    L.base = l->base;
+    L.layer_base = l->layer_base_dev;
+    L.page_stride = l->page_stride;
+    L.plane_stride = l->plane_stride;
+    L.token_stride = l->token_stride;
+    L.plane_bytes = l->plane_bytes;
+    L.n_planes = l->n_planes;
+    L.page_tokens = l->page_tokens;
+    L.bpt = l->bpt;
+    L.shared_table = l->shared_table;
     return L;
 }
 
@@ -338,8 +355,17 @@ int tkv_pages_scatter(tkv_pages* p, const uint8_t* buf, size_t bytes, const uint
     });
 }
 int tkv_pages_layout(tkv_pages* p, tkv_paged_layout* out) {
-    PagedLayout L = p->p->layout();
-    std::memcpy(out, &L, sizeof L);
+    const PagedLayout L = p->p->layout();
+    out->base = L.base;
+    out->layer_base_dev = L.layer_base;
+    out->page_stride = L.page_stride;
+    out->plane_stride = L.plane_stride;
+    out->token_stride = L.token_stride;
+    out->plane_bytes = L.plane_bytes;
+    out->n_planes = L.n_planes;
+    out->page_tokens = L.page_tokens;
+    out->bpt = L.bpt;
+    out->shared_table = L.shared_table;
     return 0;
 }
 int tkv_pages_device_table(tkv_pages* p, uint64_t q, void* stream, const int32_t** table,
