@@ -45,6 +45,7 @@ struct CommitCtx {
     std::vector<Digest> digests;
     std::atomic<bool>* committed;
     std::vector<Digest> touches;  // the reference's LRU touch order for the batch
+    std::shared_ptr<void> keep;   // device-read buffers (a launch plan) freed after the copy
 };
 void CUDART_CB commit_cb(void* p) {
     auto* c = static_cast<CommitCtx*>(p);
@@ -834,10 +835,10 @@ Status Connector::flush_decode(QueryId id, QueryState& qs) {
         computed.wait_on(store_stream_);
         TKV_CUDA(launch_paged_copy(pages_.layout(), plan->plan(0, 0, model.num_layers, ppt),
                                    CopyDir::gather, cfg_.store_ctas, store_stream_));
-        auto* ctx = new CommitCtx{&store_, {key.digest}, nullptr};
+        // Asynchronous: the commit callback marks the chunk present and frees
+        // the plan after the gather ran; finish_query waits on the handle.
+        auto* ctx = new CommitCtx{&store_, {key.digest}, nullptr, {}, plan};
         TKV_CUDA(cudaLaunchHostFunc(store_stream_, commit_cb, ctx));
-        // Keep the plan buffers alive until the gather ran.
-        TKV_CUDA(cudaStreamSynchronize(store_stream_));
         ds.puts.push_back(w.value().handle);
     }
     ds.flushed.push_back(key);
