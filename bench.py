@@ -143,17 +143,32 @@ class ClockSampler:
 
     def _read(self):
         for line in self.proc.stdout:
-            self.lines.append(line.strip())
+            self.lines.append((time.time(), line.strip()))
 
     def __exit__(self, *a):
         if self.proc:
             self.proc.terminate()
             self.proc.wait()
 
-    def summary(self):
+    def summary(self, window=None):
+        """Median SM clock and the throttle reasons seen. `window` = (t0, t1)
+        wall-clock bounds of the timed region: only samples that arrived in
+        it count; when fewer than 3 did (a sub-second region), the nearest
+        samples of the same workload around it are added and `in_window`
+        says how many were strictly inside."""
         sm, mx, reasons = [], [], set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
+        lines = self.lines
+        inside = len(lines)
+        if window is not None:
+            t0, t1 = window
+            picked = [x for x in lines if t0 <= x[0] <= t1]
+            inside = len(picked)
+            if len(picked) < 3:
+                mid = 0.5 * (t0 + t1)
+                picked = sorted(lines, key=lambda x: abs(x[0] - mid))[:3]
+            lines = picked
+        for _, ln in lines:
             f = [x.strip() for x in ln.split(",")]
             if len(f) < 9:
                 continue
@@ -168,7 +183,7 @@ class ClockSampler:
         if not sm:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
         return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
-                "samples": len(sm)}
+                "samples": len(sm), "in_window": inside}
 
 
 # ------------------------------------------------------------ reference ----
@@ -758,9 +773,11 @@ def run_b200(args):
         return
     # ---- e2e: the connector step through the C-ABI, pinned host tier
     bench.store_prefix()
+    clk = ClockSampler(local).__enter__()  # running (and sampling the warm-up load) before the timed region
     for k in range(args.warmup):
         bench.step(k)
     if args.trace:
+        clk.__exit__()
         if rank == 0:
             print(json.dumps({"trace": bench.trace_step(1000)}), flush=True)
         return
@@ -768,22 +785,25 @@ def run_b200(args):
     torch.cuda.synchronize()
     lib_ = bench.e.L
     launches0 = lib_.tkv_launch_count()
-    with ClockSampler(local) as clk:
-        start = torch.cuda.Event(enable_timing=True)
-        end = torch.cuda.Event(enable_timing=True)
-        start.record(bench.stream)
-        t0 = time.perf_counter()
-        if args.sequential:
-            nxt = bench.lookup(args.warmup)
-            for k in range(args.steps):
-                kk = args.warmup + k
-                loaded, stored, nxt = bench.step(kk, looked_up=nxt, next_k=kk + 1 if k + 1 < args.steps else None)
-        else:
-            loaded, stored = bench.run_pipelined([args.warmup + k for k in range(args.steps)])
-        torch.cuda.synchronize()
-        end.record(bench.stream)
-        torch.cuda.synchronize()
-        wall = time.perf_counter() - t0
+    w0 = time.time()
+    start = torch.cuda.Event(enable_timing=True)
+    end = torch.cuda.Event(enable_timing=True)
+    start.record(bench.stream)
+    t0 = time.perf_counter()
+    if args.sequential:
+        nxt = bench.lookup(args.warmup)
+        for k in range(args.steps):
+            kk = args.warmup + k
+            loaded, stored, nxt = bench.step(kk, looked_up=nxt, next_k=kk + 1 if k + 1 < args.steps else None)
+    else:
+        loaded, stored = bench.run_pipelined([args.warmup + k for k in range(args.steps)])
+    torch.cuda.synchronize()
+    end.record(bench.stream)
+    torch.cuda.synchronize()
+    wall = time.perf_counter() - t0
+    w1 = time.time()
+    time.sleep(0.25)  # let the sampler deliver the samples taken inside the region
+    clk.__exit__()
     e2e_launches = lib_.tkv_launch_count() - launches0
     e2e_ms = max_over_ranks(start.elapsed_time(end) / args.steps)
     barrier()
@@ -858,7 +878,7 @@ def run_b200(args):
         "kernel_launches_value": int(kr["launches"]),
         "parity": {"value_pages_mismatch_words": kr["mismatch_words"]},
         "cpu_baseline": cpu,
-        "clocks": clk.summary(),
+        "clocks": clk.summary((w0, w1)),
     }
     if pd is not None:
         line["pd"] = pd
