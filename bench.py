@@ -702,6 +702,34 @@ def run_pd_pairs(args, world, rank, local):
     return out
 
 
+def reference_pd_gbps(L, bpt, n_chunks=4):
+    """CPU work of the reference's PD transfer per chunk (run_pd,
+    src/sim_engine.cpp:389-397 and 441-455): LMCK encode of the prefilled
+    chunk (payload copy + FNV-1a) and parse on the decoder (FNV check +
+    copy), on a bounded sample of chunks of the pair's geometry. TCP is left
+    out, so this is the reference's best case."""
+    import oracle
+    if not oracle.ref_available():
+        return None
+    import numpy as np
+    C, R = oracle.C(), oracle.Ref()
+    toks = prompt_tokens(256 * n_chunks, 0, 999)
+    seed = C.model_seed(TAG)
+    keys = C.chunk_keys(toks, 256, TAG)
+    t = 0.0
+    for i in range(n_chunks):
+        pay = C.synth_chunk(seed, toks, 256 * i, 256, L, bpt)
+        t0 = time.perf_counter()
+        rec = R.encode_record(TAG, keys[i], 256, L, bpt, pay)
+        code, back = R.parse_record(rec, pay.size)
+        t += time.perf_counter() - t0
+        assert code == 0 and np.array_equal(back, pay)
+    moved = n_chunks * 256 * L * bpt
+    return {"value": round(moved / t / 1e9, 4), "unit": "GB/s", "cores": 1, "kind": "reference",
+            "sample": f"{n_chunks} chunks of {L} layers x 256 tokens x {bpt} B: LMCK encode + parse "
+                      f"(run_pd's CPU work, TCP excluded)"}
+
+
 def ncu_traffic(kernel, algorithmic_bytes, bench):
     """roofline.traffic: DRAM bytes per launch of `kernel` from the committed
     ncu --set full capture (profiles/ncu_traffic.json), when that capture was
@@ -828,6 +856,8 @@ def run_b200(args):
                   "nvlink_peak_gbps_per_direction": 770.0,
                   "frac_of_peak": round(min(r["gbps"] for r in sends) / 770.0, 4),
                   "frac_of_measured_link": round(min(r["gbps"] / r["link_gbps"] for r in sends), 4),
+                  "cpu_baseline": (reference_pd_gbps(args.layers, args.bpt_full // (world // 2))
+                                   if rank == 0 and not args.no_cpu_baseline else None),
                   "path": "per pair the faster of: K1 gather straight into the peer decoder's landing buffer "
                           "(CUDA IPC, SM writes over NVLink) | K1 into local staging + copy-engine peer copies "
                           "per 1 GiB group; PdStaging ordinal contract, one K2 land, bytes verified on device"}
