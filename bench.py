@@ -762,6 +762,10 @@ def run_b200(args):
             dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
         else:
             dist.init_process_group(backend())
+    # nvidia-smi (NVML init) takes a second or more to come up and perturbs the
+    # device while it does: start the clock sampler now, seconds before the
+    # timed region; only the samples that arrive inside it are summarised.
+    clk = ClockSampler(local).__enter__()
     bench = B200Bench(args, world, rank, local)
     peaks = {}
     try:
@@ -796,12 +800,12 @@ def run_b200(args):
     step_bytes_rank = kr["pre_bytes"] + kr["suf_bytes"]
     value = step_bytes_rank * world / (k_ms / 1e3) / 1e9
     if args.profile_kernels:
+        clk.__exit__()
         if rank == 0:
             print(json.dumps({"kernels": kr}), flush=True)
         return
     # ---- e2e: the connector step through the C-ABI, pinned host tier
     bench.store_prefix()
-    clk = ClockSampler(local).__enter__()  # running (and sampling the warm-up load) before the timed region
     for k in range(args.warmup):
         bench.step(k)
     if args.trace:
