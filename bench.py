@@ -131,6 +131,8 @@ class ClockSampler:
         self.lines: list[str] = []
 
     def __enter__(self):
+        if os.environ.get("TKV_NO_CLOCKS"):  # diagnostics: run without the sampler
+            return self
         try:
             self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
                                           "--format=csv,noheader,nounits", "-lms", "100"],
@@ -806,8 +808,14 @@ def run_b200(args):
         return
     # ---- e2e: the connector step through the C-ABI, pinned host tier
     bench.store_prefix()
-    for k in range(args.warmup):
-        bench.step(k)
+    # Warm-up runs the same schedule as the timed region: the pipelined one
+    # keeps two requests in flight, and its first steps grow the launch-plan
+    # and page-table pools (pinned + device allocations) to that depth.
+    if args.sequential or args.trace:
+        for k in range(args.warmup):
+            bench.step(k)
+    elif args.warmup:
+        bench.run_pipelined(list(range(args.warmup)))
     if args.trace:
         clk.__exit__()
         if rank == 0:
