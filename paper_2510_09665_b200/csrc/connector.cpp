@@ -338,8 +338,11 @@ ConnectorMetadata Connector::build_connector_meta(const SchedulerOutput& out) {
             plan.load_plan.push_back({keys[i], span, record_tokens});
         }
         // Store descriptors: chunks absent at build time (connector.cpp:100-110).
+        std::vector<Digest> digests(keys.size());
+        for (size_t i = 0; i < keys.size(); ++i) digests[i] = keys[i].digest;
+        const std::vector<bool> present = store_.present_mask(digests);
         for (size_t i = 0; i < spans.size(); ++i) {
-            if (store_.contains(keys[i].digest)) continue;
+            if (present[i]) continue;
             plan.store_plan.push_back({keys[i], spans[i], uint32_t(spans[i].length())});
         }
         detail::PerQueryState pq;

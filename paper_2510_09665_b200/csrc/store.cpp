@@ -324,6 +324,16 @@ size_t TieredStore::present_prefix(const std::vector<Digest>& digests) const {
     return k;
 }
 
+std::vector<bool> TieredStore::present_mask(const std::vector<Digest>& digests) const {
+    std::vector<bool> out(digests.size());
+    std::lock_guard lock(mu_);
+    for (size_t i = 0; i < digests.size(); ++i) {
+        auto it = index_.find(digests[i]);
+        out[i] = it != index_.end() && it->second.state == Entry::State::present;
+    }
+    return out;
+}
+
 Status TieredStore::pin(const Digest& digest, bool on) {
     std::lock_guard lock(mu_);
     auto it = index_.find(digest);

@@ -149,6 +149,8 @@ public:
     // Leading entries of `digests` that are present, under one lock (the
     // reference probes contains() once per chunk, store.cpp:797-806).
     size_t present_prefix(const std::vector<Digest>& digests) const;
+    // present[i] = contains(digests[i]) for every digest, under one lock.
+    std::vector<bool> present_mask(const std::vector<Digest>& digests) const;
     Status pin(const Digest& digest, bool on);
     ClearResult clear(const std::vector<Digest>& digests);
     size_t evict_until(size_t bytes_needed);
