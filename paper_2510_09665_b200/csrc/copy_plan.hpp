@@ -67,7 +67,9 @@ struct DevicePlan {
         }
         std::memcpy(h + off_tb1, tb1.data(), tb1.size() * 4);
         std::memcpy(h + off_tball, tball.data(), tball.size() * 4);
-        TKV_CUDA(cudaMemcpyAsync(buf->dev.ptr, h, total, cudaMemcpyHostToDevice, s));
+        // SM copy from the mapped pinned side: a copy-engine upload would queue
+        // behind the layer transfers already in flight.
+        TKV_CUDA(launch_sm_copy(buf->host.dev, buf->dev.ptr, total, s));
     }
 
     PagedCopyPlan plan(size_t variant, uint32_t layer_begin, uint32_t n_layers, uint32_t ppt) const {

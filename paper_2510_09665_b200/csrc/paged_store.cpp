@@ -139,7 +139,8 @@ Result<PagedKVStore::DeviceTable> PagedKVStore::device_table(QueryId query, cuda
         std::fill(h, h + rows * stride, -1);
         for (size_t l = 0; l < t.layers.size(); ++l)
             std::copy(t.layers[l].begin(), t.layers[l].end(), h + l * stride);
-        TKV_CUDA(cudaMemcpyAsync(t.buf->dev.ptr, h, bytes, cudaMemcpyHostToDevice, stream));
+        // SM copy from the mapped pinned side (not behind in-flight CE transfers)
+        TKV_CUDA(launch_sm_copy(t.buf->host.dev, t.buf->dev.ptr, bytes, stream));
         t.stride = uint32_t(stride);
         t.dirty = false;
     }
