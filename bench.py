@@ -321,7 +321,8 @@ class B200Bench:
                         staging_budget=1 << 34, staging_depth=args.staging_depth,
                         load_zero_copy=args.load_zero_copy, store_zero_copy=args.store_zero_copy,
                         store_ctas=args.store_ctas, device=local,
-                        stream=self.stream, memo_entries=args.memo_entries)
+                        stream=self.stream, memo_entries=args.memo_entries,
+                        shard_offset=rank * self.bpt)  # this rank's heads: its slice of every row
         self.qid = 100
 
     def store_prefix(self):
@@ -620,7 +621,7 @@ def run_pd_pairs(args, world, rank, local):
     prefill = rank < half
     peer = rank + half if prefill else rank - half
     e = Engine(num_layers=L, bpt=bpt, page_tokens=16, tag=TAG, chunk_size=256, ram_slots=2,
-               num_pages=(n // 16 + 16) * L, device=local)
+               num_pages=(n // 16 + 16) * L, device=local, shard_offset=(rank % half) * bpt)
     prompt = prompt_tokens(n, 0, 999)
     qid = 5000
     landing = None

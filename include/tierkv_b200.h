@@ -216,6 +216,10 @@ int tkv_pages_scatter(tkv_pages* p, const uint8_t* buf, size_t buf_bytes, const 
 int tkv_pages_layout(tkv_pages* p, tkv_paged_layout* out);
 int tkv_pages_device_table(tkv_pages* p, uint64_t query, void* stream, const int32_t** table_dev,
                            uint32_t* stride);
+/* Tensor parallelism: this pool holds bytes [byte_offset, byte_offset + bpt)
+ * of every full KV row (a head shard); the compute stand-in and its verifier
+ * then produce / check exactly that slice of synth_token_kv's row. */
+int tkv_pages_set_shard(tkv_pages* p, uint64_t byte_offset);
 /* Engine compute stand-in (SimEngine::write_tokens, src/sim_engine.cpp:43-64):
  * K4 into the query's pages for positions [from, to), layers [l0, l1), and
  * marks them populated. tokens_dev holds the whole prompt. */

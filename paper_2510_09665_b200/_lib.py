@@ -101,6 +101,7 @@ SIGNATURES = {
     "tkv_pages_scatter": (ct.c_int, [vp, u8p, sz, u32p, sz, ct.c_uint32, sz]),
     "tkv_pages_layout": (ct.c_int, [vp, ct.POINTER(PagedLayoutC)]),
     "tkv_pages_device_table": (ct.c_int, [vp, ct.c_uint64, vp, ct.POINTER(vp), u32p]),
+    "tkv_pages_set_shard": (ct.c_int, [vp, ct.c_uint64]),
     "tkv_pages_compute": (ct.c_int, [vp, ct.c_uint64, vp, ct.c_uint32, ct.c_uint32, ct.c_uint32, ct.c_uint32, vp]),
     "tkv_pages_verify": (ct.c_int, [vp, ct.c_uint64, vp, ct.c_uint32, ct.c_uint32, ct.c_uint32, ct.c_uint32,
                                     vp, vp]),

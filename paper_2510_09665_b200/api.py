@@ -81,7 +81,7 @@ class Engine:
                  staging_depth: int = 2, load_zero_copy: bool = False, store_zero_copy: bool = False,
                  store_ctas: int = 0,
                  load_ctas: int = 0, device: int = 0, stream: torch.cuda.Stream | None = None,
-                 memo_entries: int | None = None):
+                 memo_entries: int | None = None, shard_offset: int = 0):
         del io_threads, store_io_threads  # host thread pools do not exist on this path
         self.L = lib()
         self.num_layers, self.bpt, self.page_tokens = num_layers, bpt, page_tokens
@@ -95,6 +95,8 @@ class Engine:
         self.store = ct.c_void_p()
         self.conn = ct.c_void_p()
         check(self.L.tkv_pages_create(ct.byref(spec), num_pages, device, ct.byref(self.pages)))
+        if shard_offset:  # TP head shard: compute/verify produce this slice of the full row
+            check(self.L.tkv_pages_set_shard(self.pages, shard_offset))
         ram = ram_slots * num_layers * chunk_size * bpt
         check(self.L.tkv_store_create(ct.byref(spec), chunk_size, ram, ct.byref(self.store)))
         cfg = ConnectorConfigC()

@@ -31,6 +31,7 @@ static_assert(offsetof(tkv_chain_desc, parent) == offsetof(ChainDesc, parent));
 
 struct tkv_pages {
     std::unique_ptr<PagedKVStore> p;
+    uint64_t shard_offset = 0;  // bytes of the full KV row before this TP shard
 };
 struct tkv_store {
     std::unique_ptr<TieredStore> s;
@@ -392,6 +393,7 @@ static int pages_synth(tkv_pages* p, uint64_t q, const uint32_t* tokens, uint32_
         auto t = p->p->device_table(q, cudaStream_t(stream));
         if (!t.ok()) return st(t.status());
         SynthArgs a = synth_args(tokens, t.value().ptr, t.value().stride, sp.model_seed(), from, to, l0, l1);
+        a.row_offset = p->shard_offset;
         if (mism) return cuda(launch_verify_pages(p->p->layout(), a, mism, cudaStream_t(stream)));
         int rc = cuda(launch_synth_pages(p->p->layout(), a, cudaStream_t(stream)));
         if (rc) return rc;
@@ -406,6 +408,11 @@ static int pages_synth(tkv_pages* p, uint64_t q, const uint32_t* tokens, uint32_
     });
 }
 
+int tkv_pages_set_shard(tkv_pages* p, uint64_t byte_offset) {
+    if (byte_offset % 8) return fail(Errc::invalid_argument, "shard offset must be a multiple of 8");
+    p->shard_offset = byte_offset;
+    return 0;
+}
 int tkv_pages_compute(tkv_pages* p, uint64_t q, const uint32_t* tokens, uint32_t from, uint32_t to,
                       uint32_t l0, uint32_t l1, void* stream) {
     return pages_synth(p, q, tokens, from, to, l0, l1, nullptr, stream);

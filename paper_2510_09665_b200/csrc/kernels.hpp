@@ -171,6 +171,7 @@ struct SynthArgs {
     uint64_t seed = 0;
     uint32_t pos_begin = 0, pos_end = 0;
     uint32_t layer_begin = 0, layer_end = 0;
+    uint64_t row_offset = 0;  // byte offset of this row slice in the full row (TP head shard)
 };
 cudaError_t launch_synth_pages(const PagedLayout& layout, const SynthArgs& args,
                                cudaStream_t stream);

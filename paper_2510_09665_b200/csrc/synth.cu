@@ -59,7 +59,7 @@ __global__ void synth_pages_kernel(const PagedLayout L, const SynthArgs A,
         const uint32_t w = uint32_t(idx - row * wpr);
         const uint32_t layer = A.layer_begin + uint32_t(row / ntok);
         const uint32_t pos = A.pos_begin + uint32_t(row % ntok);
-        const uint64_t word = splitmix64(row_base(A.seed, A.tokens[pos], layer, pos) + 8ull * w);
+        const uint64_t word = splitmix64(row_base(A.seed, A.tokens[pos], layer, pos) + A.row_offset + 8ull * w);
         const uint32_t i0 = 8 * w;
         const uint32_t nb = min(8u, L.bpt - i0);
         if (aligned8 && nb == 8) {
@@ -104,7 +104,7 @@ synth_rows_kernel(const PagedLayout L, const SynthArgs A, unsigned long long* mi
          row += warps) {
         const uint32_t layer = A.layer_begin + uint32_t(row / ntok);
         const uint32_t pos = A.pos_begin + uint32_t(row % ntok);
-        const uint64_t base = row_base(A.seed, A.tokens[pos], layer, pos);
+        const uint64_t base = row_base(A.seed, A.tokens[pos], layer, pos) + A.row_offset;
         for (uint32_t p = lane; p < pairs; p += 32) {
             const uint32_t i0 = 16 * p;
             const uint64_t w0 = splitmix64(base + i0), w1 = splitmix64(base + i0 + 8);

@@ -285,3 +285,49 @@ def test_sm_copy_pinned_to_device(tkv, nbytes, src_off, dst_off):
     d = dev.cpu().numpy()
     assert np.array_equal(d[dst_off:dst_off + nbytes], host.numpy()[src_off:src_off + nbytes])
     assert (d[:dst_off] == 0xAB).all() and (d[dst_off + nbytes:] == 0xAB).all()
+
+
+@pytest.mark.parametrize("tp", [2, 4])
+def test_tp_shards_are_head_slices(tkv, C, tp):
+    """TP head sharding (a18): rank r's pool holds bytes [r*S, (r+1)*S) of
+    every full KV row, S = bpt/tp. Each rank's compute + store + retrieve
+    through its own connector; concatenating the ranks' retrieved rows gives
+    the full-model rows of the oracle (synth_token_kv at bpt)."""
+    from paper_2510_09665_b200.api import Engine
+    full, L, n = 512, 3, 300
+    S = full // tp
+    prompt = rand_tokens(np.random.default_rng(40 + tp), n)
+    rows = []
+    for r in range(tp):
+        e = Engine(num_layers=L, bpt=S, page_tokens=16, tag="tp-test", chunk_size=64, ram_slots=16,
+                   num_pages=256, shard_offset=r * S)
+        e.get_num_new_matched_tokens(1, prompt)
+        e.bind_pages(1, n)
+        e.update_state_after_alloc(1, (n + 15) // 16, 0)
+        m = e.build_connector_meta([(1, prompt)])
+        assert e.start_load_kv(m) == 0
+        for layer in range(L):
+            e.wait_load_kv(m, layer)
+            e.compute_range(1, prompt, 0, n, layers=(layer, layer + 1))
+            if layer:
+                e.wait_store_kv(m, layer - 1)
+            e.start_store_kv(m)
+        assert e.wait_store_kv(m, L - 1) == 0
+        e.finish_query(1)
+        e.release_query(1)
+        assert e.get_num_new_matched_tokens(2, prompt) == n - 1  # keys are rank-independent
+        e.bind_pages(2, n)
+        e.update_state_after_alloc(2, (n + 15) // 16, (n - 1 + 15) // 16)
+        m = e.build_connector_meta([(2, prompt)])
+        assert e.start_load_kv(m) == 0
+        for layer in range(L):
+            e.wait_load_kv(m, layer)
+        e.synchronize()
+        assert e.verify_range(2, prompt, 0, n - 1) == 0
+        rows.append([e.gather_layer(2, layer, n - 1).reshape(n - 1, S) for layer in range(L)])
+        e.close()
+    seed = C.model_seed("tp-test")
+    for layer in range(L):
+        want = C.synth_layer_kv(seed, prompt[:n - 1], layer, 0, full).reshape(n - 1, full)
+        got = np.concatenate([rows[r][layer] for r in range(tp)], axis=1)
+        assert np.array_equal(got, want), layer
