@@ -800,6 +800,11 @@ def run_b200(args):
     barrier()
     kr = kernel_loop(bench, args.steps, args.warmup)
     k_ms = max_over_ranks(kr["total_ms"] / args.steps)
+    mism_all = kr["mismatch_words"]
+    if world > 1:  # every rank's page image, not rank 0's alone
+        t = torch.tensor([float(mism_all)], dtype=torch.float64, device=coll_device(bench.dev))
+        dist.all_reduce(t, op=dist.ReduceOp.SUM)
+        mism_all = int(t.item())
     step_bytes_rank = kr["pre_bytes"] + kr["suf_bytes"]
     value = step_bytes_rank * world / (k_ms / 1e3) / 1e9
     if args.profile_kernels:
@@ -919,7 +924,7 @@ def run_b200(args):
                   "e2e_frac_of_pcie_bidir": round(e2e / sum(p["bidir_gbps"] for p in pcie_all), 4)},
         "gpu_launches": int(e2e_launches),
         "kernel_launches_value": int(kr["launches"]),
-        "parity": {"value_pages_mismatch_words": kr["mismatch_words"]},
+        "parity": {"value_pages_mismatch_words": mism_all, "ranks_checked": world},
         "cpu_baseline": cpu,
         "clocks": clk.summary((w0, w1)),
     }
