@@ -357,6 +357,30 @@ class B200Bench:
         assert matched == min(self.n_pre, self.n - 1), matched
         return q, prompt, matched
 
+    def verified_step(self, k):
+        """One untimed step through the connector whose retrieved prefix and
+        computed suffix are then checked word by word on the device against
+        synth (the full-size e2e parity property)."""
+        e, L, n = self.e, self.L, self.n
+        q, prompt, matched = self.lookup(k)
+        assert e.bind_pages(q, n) == 0
+        assert e.update_state_after_alloc(q, (n + 15) // 16, (matched + 15) // 16) == 0
+        m = e.build_connector_meta([(q, prompt)])
+        assert e.start_load_kv(m) == 0
+        loaded = e.loaded_tokens(m, q)
+        for layer in range(L):
+            e.wait_load_kv(m, layer)
+            e.compute_range(q, prompt, loaded, n, layers=(layer, layer + 1))
+            if layer:
+                e.wait_store_kv(m, layer - 1)
+            assert e.start_store_kv(m) == 0
+        assert e.wait_store_kv(m, L - 1) == 0
+        mism = e.verify_range(q, prompt, 0, n)
+        e.drop_meta(m)
+        e.finish_query(q)
+        e.release_query(q)
+        return mism, loaded
+
     def step(self, k, looked_up=None, next_k=None):
         """One scheduling iteration: retrieve the prefix, store the new suffix.
 
@@ -851,6 +875,11 @@ def run_b200(args):
     time.sleep(0.25)  # let the sampler deliver the samples taken inside the region
     clk.__exit__()
     e2e_launches = lib_.tkv_launch_count() - launches0
+    e2e_mism, e2e_loaded = bench.verified_step(args.warmup + args.steps)  # untimed parity step
+    if world > 1:
+        t = torch.tensor([float(e2e_mism)], dtype=torch.float64, device=coll_device(bench.dev))
+        dist.all_reduce(t, op=dist.ReduceOp.SUM)
+        e2e_mism = int(t.item())
     e2e_ms = max_over_ranks(start.elapsed_time(end) / args.steps)
     barrier()
     e2e_bytes_rank = (loaded + stored) * bench.L * bench.bpt
@@ -924,7 +953,11 @@ def run_b200(args):
                   "e2e_frac_of_pcie_bidir": round(e2e / sum(p["bidir_gbps"] for p in pcie_all), 4)},
         "gpu_launches": int(e2e_launches),
         "kernel_launches_value": int(kr["launches"]),
-        "parity": {"value_pages_mismatch_words": mism_all, "ranks_checked": world},
+        "parity": {"value_pages_mismatch_words": mism_all, "ranks_checked": world,
+                   "e2e_pages_mismatch_words": e2e_mism,
+                   "e2e_check": f"one more connector step after the timed region: {e2e_loaded}-token prefix "
+                                f"retrieved from the pinned tier + {bench.n - e2e_loaded} computed tokens, "
+                                f"every page word of all {bench.L} layers against synth on the device"},
         "cpu_baseline": cpu,
         "clocks": clk.summary((w0, w1)),
     }
