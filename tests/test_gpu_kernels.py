@@ -331,3 +331,42 @@ def test_tp_shards_are_head_slices(tkv, C, tp):
         want = C.synth_layer_kv(seed, prompt[:n - 1], layer, 0, full).reshape(n - 1, full)
         got = np.concatenate([rows[r][layer] for r in range(tp)], axis=1)
         assert np.array_equal(got, want), layer
+
+
+@pytest.mark.parametrize("direction", ["gather", "scatter"])
+def test_vllm_slot_mapping(tkv, direction):
+    """Per-token slot_mapping (vLLM: slot = block * block_size + offset, or any
+    token -> slot map) is the paged layout with page_tokens = 1: the table is
+    the slot mapping and a "page" is one token row. K/V planes per layer,
+    scattered slots; gather (store) and scatter (retrieve) against numpy."""
+    from paper_2510_09665_b200.api import XferDescC, plan_tiles
+    from paper_2510_09665_b200._lib import check, lib
+    rng = np.random.default_rng(13)
+    L, n_slots, hd, n_tok = 3, 400, 128, 300  # hd = plane bytes per token (H*D*elt)
+    kv = [torch.from_numpy(rng.integers(0, 256, size=2 * n_slots * hd, dtype=np.uint8)).cuda() for _ in range(L)]
+    bases = torch.tensor([t.data_ptr() for t in kv], dtype=torch.int64).cuda()
+    slots = rng.permutation(n_slots)[:n_tok].astype(np.int32)  # arbitrary, non-contiguous
+    tab = torch.from_numpy(slots).cuda()
+    ch = torch.from_numpy(rng.integers(0, 256, size=L * n_tok * 2 * hd, dtype=np.uint8)).cuda()
+    d = XferDescC(chunk=ch.data_ptr(), layer_stride=n_tok * 2 * hd, table_dev=tab.data_ptr(),
+                  table_stride=n_tok, first_page=0, n_tokens=n_tok)
+    tb, ppt = plan_tiles([d], 1, hd, L)
+    d_descs = torch.frombuffer(bytearray(bytes(d)), dtype=torch.uint8).cuda()
+    d_tb = torch.from_numpy(tb.view(np.int32)).cuda()
+    layout = tkv.api.PagedLayoutC(base=0, layer_base_dev=bases.data_ptr(), page_stride=hd,
+                                  plane_stride=n_slots * hd, token_stride=hd, plane_bytes=hd, n_planes=2,
+                                  page_tokens=1, bpt=2 * hd, shared_table=1)
+    before = [t.cpu().numpy().reshape(2, n_slots, hd).copy() for t in kv]
+    chunk_before = ch.cpu().numpy().reshape(L, n_tok, 2, hd).copy()
+    fn = lib().tkv_gather_layers if direction == "gather" else lib().tkv_scatter_layers
+    check(fn(ct.byref(layout), d_descs.data_ptr(), d_tb.data_ptr(), 1, int(tb[-1]), 0, L, ppt,
+             d.chunk | d.layer_stride, 0, None))
+    torch.cuda.synchronize()
+    for layer in range(L):
+        if direction == "gather":
+            got = ch.cpu().numpy().reshape(L, n_tok, 2, hd)[layer]
+            assert np.array_equal(got, before[layer][:, slots].transpose(1, 0, 2))
+        else:
+            want = before[layer].copy()
+            want[:, slots] = chunk_before[layer].transpose(1, 0, 2)
+            assert np.array_equal(kv[layer].cpu().numpy().reshape(2, n_slots, hd), want)
