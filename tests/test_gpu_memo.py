@@ -124,3 +124,31 @@ def test_memo_resumed_chain_parent(tkv, C):
     doc = rng.integers(0, 128256, size=256 * 6 + 7, dtype=np.uint32)
     for _ in range(2):
         assert chunk_keys(doc, 256, TAG) == C.chunk_keys(doc, 256, TAG)
+
+
+def test_memo_batch_with_empty_and_single_token_prompts(tkv, C):
+    """Empty and one-token prompts in the same lookup launch as long ones
+    (zero-row chains next to multi-row chains in the probe and hash kernels)."""
+    from paper_2510_09665_b200.api import Engine
+    e = Engine(num_layers=2, bpt=64, page_tokens=16, tag=TAG, chunk_size=256, ram_slots=2, num_pages=4096)
+    rng = np.random.default_rng(3)
+    doc = rng.integers(0, 128256, size=256 * 3 + 9, dtype=np.uint32)
+    one = doc[:1].copy()
+    empty = np.zeros(0, np.uint32)
+    for rnd in range(2):  # cold memo, then warm
+        got = e.lookup_batch([10 * rnd + 1, 10 * rnd + 2, 10 * rnd + 3, 10 * rnd + 4], [empty, doc, one, empty])
+        assert got == [0, 0, 0, 0]  # nothing stored: no hits
+        keys = []
+        for q, p in zip([10 * rnd + 2, 10 * rnd + 3], [doc, one]):
+            e.bind_pages(q, len(p))
+            e.update_state_after_alloc(q, (len(p) + 15) // 16, 0)
+            m = e.build_connector_meta([(q, p)])
+            sp, _ = e.plan(m, 0, "store")
+            keys.append([d for _, _, _, _, d in sp])
+            e.drop_meta(m)
+        assert keys == [C.chunk_keys(doc, 256, TAG), C.chunk_keys(one, 256, TAG)]
+        for q in range(10 * rnd + 1, 10 * rnd + 5):
+            e.finish_query(q)
+            e.release_query(q)
+    assert e.memo_stats()["rehashes"] == 0
+    e.close()
