@@ -98,3 +98,18 @@ def test_decode_chunks_chain_correct(tkv, C):
         assert np.array_equal(e.store_get(want[c]), C.synth_chunk(seed, full, start, cnt, 4, 64))
     e.release_query(12)
     e.close()
+
+
+@pytest.mark.parametrize("name", ["sc_partial_match", "sc_layerwise_vs_blocking", "sc_multi_query_batch",
+                                  "sc_random_trace_evicting", "sc_random_trace_decode", "sc_degenerate_prompts"])
+@pytest.mark.parametrize("mode", ["load_zero_copy", "store_zero_copy", "both_zero_copy", "depth1", "depth4"])
+def test_transfer_modes_match_reference(tkv, C, name, mode):
+    """The non-default host-tier paths give the reference outcome too: K2
+    reading pinned slots directly (no HBM ring), K1 writing them directly (no
+    copy-engine D2H), both, and staging rings of depth 1 and 4."""
+    from paper_2510_09665_b200.api import Engine
+    kw = {"load_zero_copy": dict(load_zero_copy=True), "store_zero_copy": dict(store_zero_copy=True),
+          "both_zero_copy": dict(load_zero_copy=True, store_zero_copy=True),
+          "depth1": dict(staging_depth=1), "depth4": dict(staging_depth=4)}[mode]
+    got = json.loads(json.dumps(getattr(S, name)(lambda **a: Engine(**a, **kw), C)))
+    assert got == _ref_outcome(name, C)
