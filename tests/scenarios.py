@@ -299,14 +299,16 @@ ALL = [sc_match_cap, sc_load_plan_clip, sc_inconsistent_alloc, sc_partial_match,
        sc_vanishing_chunk, sc_tier_full, sc_degrade_blocking, sc_multi_query_batch]
 
 
-def _random_trace(factory, C, seed: int, slots: int, decode: bool = False, probe: bool = False, **cfg):
+def _random_trace(factory, C, seed: int, slots: int, decode: bool = False, probe: bool = False,
+                  chunk_size: int = 32, scale: int = 1, num_pages: int = 1024, **cfg):
     """Randomised serving trace: shared document prefixes cut at arbitrary
     (non chunk- or page-aligned) points plus fresh tails, 1-3 queries per
     scheduling iteration, a RAM tier of `slots` chunks (small -> LRU evictions
     between iterations). Records every observable per query."""
     rng = np.random.default_rng(seed)
-    e = factory(**CONN, ram_slots=slots, num_pages=1024, **cfg)
-    docs = [make_prompt(int(rng.integers(40, 200)), 1000 + 10 * seed + i) for i in range(4)]
+    geom = dict(CONN, chunk_size=chunk_size)
+    e = factory(**geom, ram_slots=slots, num_pages=num_pages, **cfg)
+    docs = [make_prompt(int(rng.integers(40, 200)) * scale, 1000 + 10 * seed + i) for i in range(4)]
     out = []
     qid = 100
     seen: set[str] = set()
@@ -404,8 +406,14 @@ def sc_random_trace_decode(factory, C):
     return [_random_trace(factory, C, 11, 256, decode=True), _random_trace(factory, C, 12, 7, decode=True)]
 
 
+def sc_random_trace_big_chunks(factory, C):
+    """Random trace with 512-token chunks (the thread-per-chain K3 variant and
+    32-page chunk spans) and 1K-3K-token documents, evicting tier."""
+    return [_random_trace(factory, C, 13, 10, chunk_size=512, scale=16, num_pages=12000)]
+
+
 ALL += [sc_random_trace_roomy, sc_random_trace_evicting, sc_random_trace_pinned, sc_random_trace_blocking,
-        sc_random_trace_decode]
+        sc_random_trace_decode, sc_random_trace_big_chunks]
 
 
 def sc_degenerate_prompts(factory, C):
