@@ -300,13 +300,14 @@ ALL = [sc_match_cap, sc_load_plan_clip, sc_inconsistent_alloc, sc_partial_match,
 
 
 def _random_trace(factory, C, seed: int, slots: int, decode: bool = False, probe: bool = False,
-                  chunk_size: int = 32, scale: int = 1, num_pages: int = 1024, **cfg):
+                  chunk_size: int = 32, scale: int = 1, num_pages: int = 1024, bpt: int = 64, layers: int = 4,
+                  **cfg):
     """Randomised serving trace: shared document prefixes cut at arbitrary
     (non chunk- or page-aligned) points plus fresh tails, 1-3 queries per
     scheduling iteration, a RAM tier of `slots` chunks (small -> LRU evictions
     between iterations). Records every observable per query."""
     rng = np.random.default_rng(seed)
-    geom = dict(CONN, chunk_size=chunk_size)
+    geom = dict(CONN, chunk_size=chunk_size, bpt=bpt, num_layers=layers)
     e = factory(**geom, ram_slots=slots, num_pages=num_pages, **cfg)
     docs = [make_prompt(int(rng.integers(40, 200)) * scale, 1000 + 10 * seed + i) for i in range(4)]
     out = []
@@ -412,8 +413,14 @@ def sc_random_trace_big_chunks(factory, C):
     return [_random_trace(factory, C, 13, 10, chunk_size=512, scale=16, num_pages=12000)]
 
 
+def sc_random_trace_odd_rows(factory, C):
+    """Random trace with 12- and 40-byte rows (4- and 8-byte vector paths of
+    K1/K2, byte tails in synth) and 3 / 5 layers, evicting tier."""
+    return [_random_trace(factory, C, 14, 6, bpt=12, layers=3), _random_trace(factory, C, 15, 6, bpt=40, layers=5)]
+
+
 ALL += [sc_random_trace_roomy, sc_random_trace_evicting, sc_random_trace_pinned, sc_random_trace_blocking,
-        sc_random_trace_decode, sc_random_trace_big_chunks]
+        sc_random_trace_decode, sc_random_trace_big_chunks, sc_random_trace_odd_rows]
 
 
 def sc_degenerate_prompts(factory, C):
