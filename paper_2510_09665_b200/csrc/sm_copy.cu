@@ -12,11 +12,14 @@
 namespace tkv {
 namespace {
 
+// 16-byte body plus the (< 16 byte) tail in the same launch.
 __global__ void __launch_bounds__(256)
-sm_copy16_kernel(const uint4* __restrict__ src, uint4* __restrict__ dst, uint64_t n16) {
+sm_copy16_kernel(const uint4* __restrict__ src, uint4* __restrict__ dst, uint64_t n16, uint32_t tail) {
     for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n16;
          i += uint64_t(gridDim.x) * blockDim.x)
         dst[i] = src[i];
+    if (blockIdx.x == 0 && threadIdx.x < tail)
+        reinterpret_cast<uint8_t*>(dst + n16)[threadIdx.x] = reinterpret_cast<const uint8_t*>(src + n16)[threadIdx.x];
 }
 
 __global__ void __launch_bounds__(256)
@@ -39,12 +42,11 @@ cudaError_t launch_sm_copy(const void* src, void* dst, uint64_t bytes, cudaStrea
     auto* d8 = static_cast<uint8_t*>(dst);
     uint64_t body = 0;
     if (((reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(dst)) & 15) == 0) {
-        body = bytes & ~uint64_t(15);
-        if (body) {
-            note_launch();
-            sm_copy16_kernel<<<grid_for(body / 16), 256, 0, s>>>(reinterpret_cast<const uint4*>(s8),
-                                                                  reinterpret_cast<uint4*>(d8), body / 16);
-        }
+        note_launch();
+        sm_copy16_kernel<<<grid_for(bytes / 16), 256, 0, s>>>(reinterpret_cast<const uint4*>(s8),
+                                                               reinterpret_cast<uint4*>(d8), bytes / 16,
+                                                               uint32_t(bytes & 15));
+        return cudaGetLastError();
     }
     if (bytes > body) {
         note_launch();
