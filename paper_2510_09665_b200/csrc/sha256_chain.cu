@@ -221,7 +221,8 @@ __device__ __forceinline__ void expand_block(const uint32_t* in, uint32_t* out) 
 // with the multipliers hidden in constant memory, 27.4 vs 19.8 us — the
 // round is dependency-latency bound (ncu: 0.44 issue/cycle, "wait" stalls
 // ~1 cycle per instruction), so longer-latency pipes only lengthen the
-// chain. ptxas' own pipe mix is kept.)
+// chain. Hoisting d + h + K + W off the e-chain so the new e is one IADD3
+// after Sigma1/Ch also measured slower (20.9 us). ptxas' own schedule is kept.)
 __device__ __forceinline__ void compress_kw(uint32_t h[8], const uint32_t* kw) {
     uint32_t a = h[0], b = h[1], c = h[2], d = h[3], e = h[4], f = h[5], g = h[6], hh = h[7];
 #pragma unroll
