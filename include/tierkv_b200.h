@@ -297,6 +297,10 @@ int tkv_connector_prefetch(tkv_connector* c, const uint32_t* tokens, size_t n);
 int tkv_connector_drain_prefetch(tkv_connector* c);
 int tkv_connector_begin_decode(tkv_connector* c, uint64_t query);
 int tkv_connector_append_decode(tkv_connector* c, uint64_t query, uint32_t token);
+/* One decode step of many queries: tokens[i] appended to queries[i];
+ * statuses[i] = what tkv_connector_append_decode would return. */
+int tkv_connector_append_decode_batch(tkv_connector* c, size_t n, const uint64_t* queries,
+                                      const uint32_t* tokens, int* statuses);
 int tkv_connector_finish_query(tkv_connector* c, uint64_t query, uint8_t* digests_out, size_t cap,
                                size_t* n);
 size_t tkv_connector_staging_peak(tkv_connector* c);

@@ -133,6 +133,7 @@ SIGNATURES = {
     "tkv_connector_drain_prefetch": (ct.c_int, [vp]),
     "tkv_connector_begin_decode": (ct.c_int, [vp, ct.c_uint64]),
     "tkv_connector_append_decode": (ct.c_int, [vp, ct.c_uint64, ct.c_uint32]),
+    "tkv_connector_append_decode_batch": (ct.c_int, [vp, sz, u64p, u32p, ct.POINTER(ct.c_int)]),
     "tkv_connector_finish_query": (ct.c_int, [vp, ct.c_uint64, u8p, sz, szp]),
     "tkv_connector_staging_peak": (sz, [vp]),
     "tkv_connector_memo_stats": (ct.c_int, [vp, u64p]),

@@ -324,6 +324,15 @@ class Engine:
     def append_decode(self, qid: int, token: int) -> int:
         return self.L.tkv_connector_append_decode(self.conn, qid, token)
 
+    def append_decode_batch(self, qids, tokens) -> list[int]:
+        """One decode step for many queries in one call."""
+        n = len(qids)
+        q = (ct.c_uint64 * n)(*qids)
+        t = (ct.c_uint32 * n)(*[int(x) for x in tokens])
+        out = (ct.c_int * n)()
+        check(self.L.tkv_connector_append_decode_batch(self.conn, n, q, t, out))
+        return list(out)
+
     def finish_query(self, qid: int) -> int:
         keys, rc = self.finish_query_keys(qid)
         return rc

@@ -623,6 +623,15 @@ int tkv_connector_begin_decode(tkv_connector* c, uint64_t q) {
 int tkv_connector_append_decode(tkv_connector* c, uint64_t q, uint32_t token) {
     return guard([&] { return st(c->c->append_decode(q, token)); });
 }
+int tkv_connector_append_decode_batch(tkv_connector* c, size_t n, const uint64_t* queries,
+                                      const uint32_t* tokens, int* statuses) {
+    return guard([&] {
+        std::vector<Status> st_(n);
+        c->c->append_decode_batch(queries, tokens, n, st_.data());
+        for (size_t i = 0; i < n; ++i) statuses[i] = int(st_[i].code);
+        return 0;
+    });
+}
 int tkv_connector_finish_query(tkv_connector* c, uint64_t q, uint8_t* out, size_t cap, size_t* n) {
     return guard([&] {
         auto r = c->c->finish_query(q);

@@ -867,6 +867,10 @@ Status Connector::append_decode(QueryId id, TokenId token) {
     return Status::success();
 }
 
+void Connector::append_decode_batch(const QueryId* ids, const TokenId* tokens, size_t n, Status* statuses) {
+    for (size_t i = 0; i < n; ++i) statuses[i] = append_decode(ids[i], tokens[i]);
+}
+
 Result<std::vector<ChunkKey>> Connector::finish_query(QueryId id) {
     std::vector<ChunkKey> keys;
     std::unique_ptr<DecodeState> ds;

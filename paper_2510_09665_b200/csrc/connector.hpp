@@ -134,6 +134,9 @@ public:
     // pages into pinned slots (K1) as they complete.
     Status begin_decode(QueryId id);
     Status append_decode(QueryId id, TokenId token);
+    // One generated token for each of many decoding queries (an engine's
+    // decode step), one call; statuses[i] is append_decode's result.
+    void append_decode_batch(const QueryId* ids, const TokenId* tokens, size_t n, Status* statuses);
     Result<std::vector<ChunkKey>> finish_query(QueryId id);
 
     const Config& config() const { return cfg_; }

@@ -113,3 +113,43 @@ def test_transfer_modes_match_reference(tkv, C, name, mode):
           "depth1": dict(staging_depth=1), "depth4": dict(staging_depth=4)}[mode]
     got = json.loads(json.dumps(getattr(S, name)(lambda **a: Engine(**a, **kw), C)))
     assert got == _ref_outcome(name, C)
+
+
+def test_decode_batch_matches_oracle(tkv, C):
+    """append_decode_batch: one decode step for four queries per call (an
+    engine's decode loop); every query's flushed chunk keys equal the chain
+    keys of its prompt + generated tokens, and the stored payloads equal the
+    oracle's synthetic chunks."""
+    import numpy as np
+    from paper_2510_09665_b200.api import Engine
+    e = Engine(**S.CONN, ram_slots=64, num_pages=512)
+    rng = np.random.default_rng(77)
+    qs = [21, 22, 23, 24]
+    prompts = {q: S.make_prompt(int(rng.integers(5, 60)), 100 + q) for q in qs}
+    gen = {q: S.make_prompt(70, 200 + q) for q in qs}
+    full = {q: np.concatenate([prompts[q], gen[q]]) for q in qs}
+    for q in qs:
+        e.get_num_new_matched_tokens(q, prompts[q])
+        e.bind_pages(q, len(full[q]))
+        e.compute_range(q, full[q], 0, len(prompts[q]))
+    m = e.build_connector_meta([(q, prompts[q]) for q in qs])
+    e.drop_meta(m)
+    for q in qs:
+        assert e.begin_decode(q) == 0
+    for i in range(70):
+        for q in qs:
+            e.compute_range(q, full[q], len(prompts[q]) + i, len(prompts[q]) + i + 1)
+        assert e.append_decode_batch(qs, [int(gen[q][i]) for q in qs]) == [0] * len(qs)
+    seed = C.model_seed(S.CONN["tag"])
+    for q in qs:
+        keys, rc = e.finish_query_keys(q)
+        assert rc == 0
+        want = C.chunk_keys(full[q], 32, S.CONN["tag"])
+        first = len(prompts[q]) // 32
+        assert keys == want[first:]
+        for c in range(first, len(want)):
+            cnt = min(32, len(full[q]) - 32 * c)
+            assert np.array_equal(e.store_get(want[c]), C.synth_chunk(seed, full[q], 32 * c, cnt, 4, 64))
+        e.release_query(q)
+    assert e.append_decode_batch([99], [1]) == [10]  # unknown_query for a query with no open decode
+    e.close()
