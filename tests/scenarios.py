@@ -301,7 +301,7 @@ ALL = [sc_match_cap, sc_load_plan_clip, sc_inconsistent_alloc, sc_partial_match,
 
 def _random_trace(factory, C, seed: int, slots: int, decode: bool = False, probe: bool = False,
                   chunk_size: int = 32, scale: int = 1, num_pages: int = 1024, bpt: int = 64, layers: int = 4,
-                  **cfg):
+                  width: tuple = (1, 4), **cfg):
     """Randomised serving trace: shared document prefixes cut at arbitrary
     (non chunk- or page-aligned) points plus fresh tails, 1-3 queries per
     scheduling iteration, a RAM tier of `slots` chunks (small -> LRU evictions
@@ -315,7 +315,7 @@ def _random_trace(factory, C, seed: int, slots: int, decode: bool = False, probe
     seen: set[str] = set()
     for _ in range(8):
         batch = []
-        for _ in range(int(rng.integers(1, 4))):
+        for _ in range(int(rng.integers(*width))):
             d = docs[int(rng.integers(0, len(docs)))]
             cut = int(rng.integers(1, len(d) + 1))
             tail = make_prompt(int(rng.integers(0, 40)), int(rng.integers(0, 1 << 30)))
@@ -419,8 +419,15 @@ def sc_random_trace_odd_rows(factory, C):
     return [_random_trace(factory, C, 14, 6, bpt=12, layers=3), _random_trace(factory, C, 15, 6, bpt=40, layers=5)]
 
 
+def sc_random_trace_wide(factory, C):
+    """Random trace with 5-12 queries per scheduling iteration (many plans,
+    shared chunks across queries of one batch), roomy and evicting tiers."""
+    return [_random_trace(factory, C, 16, 256, width=(5, 13), num_pages=4096),
+            _random_trace(factory, C, 17, 12, width=(5, 13), num_pages=4096)]
+
+
 ALL += [sc_random_trace_roomy, sc_random_trace_evicting, sc_random_trace_pinned, sc_random_trace_blocking,
-        sc_random_trace_decode, sc_random_trace_big_chunks, sc_random_trace_odd_rows]
+        sc_random_trace_decode, sc_random_trace_big_chunks, sc_random_trace_odd_rows, sc_random_trace_wide]
 
 
 def sc_degenerate_prompts(factory, C):
