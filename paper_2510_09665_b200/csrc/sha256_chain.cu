@@ -18,6 +18,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdlib>
 
 #include "kernels.hpp"
 
@@ -170,28 +171,18 @@ hash_chains_kernel(const uint32_t* __restrict__ tokens, const ChainDesc* __restr
     }
 }
 
-// ---- warp-per-chain variant (chunk_size <= kWarpChunkMax) -----------------
+// ---- warp-cooperative chains (chunk_size <= kWarpChunkMax) ----------------
 //
 // The compression is inherently serial, so its latency is the floor; what the
 // thread-per-chain kernel adds on top is memory latency: each block's 16
-// token loads sit on the critical path between compressions. Here a warp
-// owns a chain: the lanes stage the chunk's tokens (prefetched into
-// registers while the previous chunk compresses), build every message word
-// of the chunk in shared memory in parallel, and then all lanes run the same
-// compression (SIMT: the cost of one) reading W by broadcast.
+// token loads sit on the critical path between compressions. Here warps own
+// a chain: lanes stage the chunk's tokens, build every message word in shared
+// memory in parallel and expand the schedules one block per lane, and then
+// all lanes of the compressing warp run the same rounds (SIMT: the cost of
+// one) reading K+W by broadcast.
 constexpr int kWarpChunkMax = 256;  // the reference chunk size; larger chunks use the kernel above
-constexpr int kWarpsPerCta = 4;
-constexpr int kPrefetch = kWarpChunkMax / 32;
 constexpr int kMaxWords = ((2 + kMaxTagBytes + 32 + 4 * kWarpChunkMax + 9 + 63) / 64) * 16;
-
 constexpr int kMaxBlocks = kMaxWords / 16;
-
-struct WarpSmem {
-    uint32_t tok[kWarpChunkMax + 4];
-    uint32_t w[kMaxWords];
-    uint32_t kw[kMaxBlocks * 64];  // K[t] + W[t] of every block, expanded in parallel
-    uint32_t parent[8];
-};
 
 // Message schedule of one block (FIPS 180-4 §6.2.2 step 1) folded with the
 // round constants: out[t] = K[t] + W[t]. Independent of the chaining state,
@@ -245,25 +236,6 @@ __device__ __forceinline__ void compress_kw(uint32_t h[8], const uint32_t* kw) {
     h[4] += e; h[5] += f; h[6] += g; h[7] += hh;
 }
 
-__device__ __forceinline__ uint32_t smem_msg_byte(const WarpSmem& s, const HashParams& P,
-                                                  uint32_t hdr, uint32_t len, uint32_t end,
-                                                  uint32_t o) {
-    const uint32_t tl = P.tag_len;
-    if (o < 2) return (tl >> (8 * o)) & 0xff;
-    if (o < 2 + tl) return P.tag[o - 2];
-    if (o < hdr) {
-        const uint32_t j = o - 2 - tl;
-        return (s.parent[j >> 2] >> (24 - 8 * (j & 3))) & 0xff;
-    }
-    if (o < len) {
-        const uint32_t k = o - hdr;
-        return (s.tok[k >> 2] >> (8 * (k & 3))) & 0xff;
-    }
-    if (o == len) return 0x80;
-    if (o >= end - 8) return uint32_t((uint64_t(len) * 8) >> (8 * (end - 1 - o))) & 0xff;
-    return 0;
-}
-
 // ---- prefix-digest memo helpers (warp-cooperative) --------------------------
 
 __device__ __forceinline__ uint64_t mix64(uint64_t x) {
@@ -307,20 +279,20 @@ __device__ __forceinline__ bool memo_probe(const MemoView& M, uint64_t key, uint
     return false;
 }
 
-__device__ __forceinline__ void memo_insert(const MemoView& M, const WarpSmem& s, uint32_t n,
-                                            uint64_t key, uint32_t lane, const uint32_t h[8]) {
+__device__ __forceinline__ void memo_insert(const MemoView& M, const uint32_t* s_parent, const uint32_t* s_tok,
+                                            uint32_t n, uint64_t key, uint32_t lane, const uint32_t h[8]) {
     unsigned int e = 0;
     if (lane == 0) e = atomicAdd(M.counter, 1u);
     e = __shfl_sync(0xffffffffu, e, 0);
     if (e >= M.entry_cap) return;  // full: the memo stops growing until reset
     uint32_t* ent = M.entries + uint64_t(e) * M.entry_words;
-    if (lane < 8) ent[lane] = s.parent[lane];
+    if (lane < 8) ent[lane] = s_parent[lane];
     if (lane == 0) {
 #pragma unroll
         for (int i = 0; i < 8; ++i) ent[8 + i] = h[i];
         ent[16] = n;
     }
-    for (uint32_t idx = lane; idx < n; idx += 32) ent[17 + idx] = s.tok[idx];
+    for (uint32_t idx = lane; idx < n; idx += 32) ent[17 + idx] = s_tok[idx];
     __threadfence();
     __syncwarp();
     if (lane == 0) {
@@ -339,99 +311,142 @@ __device__ __forceinline__ void memo_insert(const MemoView& M, const WarpSmem& s
     }
 }
 
-__global__ void __launch_bounds__(32 * kWarpsPerCta)
-hash_chains_warp_kernel(const uint32_t* __restrict__ tokens, const ChainDesc* __restrict__ chains,
-                        uint32_t n_chains, const HashParams P, uint8_t* __restrict__ out,
-                        const MemoView M) {
-    __shared__ WarpSmem smem[kWarpsPerCta];
+// ---- producer / consumer variant: two warps per chain ----------------------
+//
+// The serial compression is ~83 % of a chunk (ncu source samples); the rest —
+// staging tokens, building message words, expanding the message schedules —
+// does not depend on the chaining state except for the block(s) holding the
+// parent digest. So a second warp prepares chunk i+1 (tokens, words, K+W of
+// every parent-free block) in a double buffer while the first compresses
+// chunk i; the consumer only builds and expands the parent block(s) itself.
+constexpr int kPairsPerCta = 2;
+
+struct PairSmem {
+    uint32_t tok[2][kWarpChunkMax + 4];
+    uint32_t w[2][kMaxWords];
+    uint32_t kw[2][kMaxBlocks * 64];
+    uint32_t parent[8];
+};
+
+__device__ __forceinline__ void named_barrier(uint32_t id, uint32_t threads) {
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(threads) : "memory");
+}
+
+// Message byte o of a chunk (header, parent, token, padding or length byte).
+__device__ __forceinline__ uint32_t pair_msg_byte(const uint32_t* tok, const uint32_t* parent, const HashParams& P,
+                                                  uint32_t hdr, uint32_t len, uint32_t end, uint32_t o) {
+    const uint32_t tl = P.tag_len;
+    if (o < 2) return (tl >> (8 * o)) & 0xff;
+    if (o < 2 + tl) return P.tag[o - 2];
+    if (o < hdr) {
+        const uint32_t j = o - 2 - tl;
+        return (parent[j >> 2] >> (24 - 8 * (j & 3))) & 0xff;
+    }
+    if (o < len) {
+        const uint32_t k = o - hdr;
+        return (tok[k >> 2] >> (8 * (k & 3))) & 0xff;
+    }
+    if (o == len) return 0x80;
+    if (o >= end - 8) return uint32_t((uint64_t(len) * 8) >> (8 * (end - 1 - o))) & 0xff;
+    return 0;
+}
+
+// Word j (4 message bytes, big-endian) of a chunk; token-only words by PRMT.
+__device__ __forceinline__ uint32_t pair_msg_word(const uint32_t* tok, const uint32_t* parent, const HashParams& P,
+                                                  uint32_t hdr, uint32_t len, uint32_t end, uint32_t j) {
+    const uint32_t o = 4 * j;
+    if (o >= hdr && o + 4 <= len) {
+        const uint32_t k = o - hdr;
+        const uint32_t kk = k & 3;
+        const uint32_t sl = (kk + 3) | ((kk + 2) << 4) | ((kk + 1) << 8) | (kk << 12);
+        return __byte_perm(tok[k >> 2], kk ? tok[(k >> 2) + 1] : 0u, sl);
+    }
+    return (pair_msg_byte(tok, parent, P, hdr, len, end, o) << 24) |
+           (pair_msg_byte(tok, parent, P, hdr, len, end, o + 1) << 16) |
+           (pair_msg_byte(tok, parent, P, hdr, len, end, o + 2) << 8) |
+           pair_msg_byte(tok, parent, P, hdr, len, end, o + 3);
+}
+
+__global__ void __launch_bounds__(64 * kPairsPerCta)
+hash_chains_pair_kernel(const uint32_t* __restrict__ tokens, const ChainDesc* __restrict__ chains,
+                        uint32_t n_chains, const HashParams P, uint8_t* __restrict__ out, const MemoView M) {
+    __shared__ PairSmem smem[kPairsPerCta];
     const uint32_t lane = threadIdx.x & 31;
-    const uint32_t wid = threadIdx.x >> 5;
-    const uint32_t c = blockIdx.x * kWarpsPerCta + wid;
-    if (c >= n_chains) return;  // warp-uniform
-    WarpSmem& s = smem[wid];
+    const uint32_t pair = threadIdx.x >> 6;
+    const bool producer = (threadIdx.x >> 5) & 1;
+    const uint32_t c = blockIdx.x * kPairsPerCta + pair;
+    if (c >= n_chains) return;  // both warps of the pair
+    PairSmem& s = smem[pair];
     const ChainDesc cd = chains[c];
     const uint32_t cs = P.chunk_size;
-    // With a memo the probe kernel already published rows [0, k0) (verified
-    // later); the chain resumes at its first miss from the last hit digest.
     const uint32_t k0 = M.first_miss != nullptr ? M.first_miss[c] : 0u;
     const uint32_t start0 = k0 * cs;
-    if (start0 >= cd.n_tokens) return;
-    if (lane < 8) {
+    if (start0 >= cd.n_tokens) return;  // both warps
+    const uint32_t nchunks = (cd.n_tokens - start0 + cs - 1) / cs;
+    const uint32_t hdr = 2 + P.tag_len + 32;
+    const uint32_t pb0 = (2 + P.tag_len) / 64, pb1 = (hdr - 1) / 64;  // blocks holding the parent
+    const uint32_t bar_id = 1 + pair;
+    const uint32_t* base = tokens + cd.token_off;
+
+    auto produce = [&](uint32_t j) {
+        const uint32_t b = j & 1;
+        const uint32_t start = start0 + j * cs;
+        const uint32_t n = min(cs, cd.n_tokens - start);
+        for (uint32_t idx = lane; idx < n; idx += 32) s.tok[b][idx] = __ldg(base + start + idx);
+        if (lane == 0) s.tok[b][n] = 0;
+        __syncwarp();
+        const uint32_t len = hdr + 4 * n;
+        const uint32_t nblocks = (len + 9 + 63) / 64;
+        const uint32_t end = 64 * nblocks;
+        for (uint32_t jw = lane; jw < 16 * nblocks; jw += 32) {
+            const uint32_t blk = jw >> 4;
+            if (blk >= pb0 && blk <= pb1) continue;  // parent block(s): the consumer's
+            s.w[b][jw] = pair_msg_word(s.tok[b], nullptr, P, hdr, len, end, jw);
+        }
+        __syncwarp();
+        for (uint32_t blk = lane; blk < nblocks; blk += 32)
+            if (blk < pb0 || blk > pb1) expand_block(s.w[b] + 16 * blk, s.kw[b] + 64 * blk);
+        __syncwarp();
+    };
+
+    if (producer) {
+        produce(0);
+    } else if (lane < 8) {
         s.parent[lane] =
             k0 ? __byte_perm(reinterpret_cast<const uint32_t*>(out + 32ull * (cd.out_first + k0 - 1))[lane], 0, 0x0123)
                : (uint32_t(cd.parent[4 * lane]) << 24) | (uint32_t(cd.parent[4 * lane + 1]) << 16) |
                      (uint32_t(cd.parent[4 * lane + 2]) << 8) | uint32_t(cd.parent[4 * lane + 3]);
     }
-    const uint32_t hdr = 2 + P.tag_len + 32;
-    const uint32_t* base = tokens + cd.token_off;
-    uint32_t pf[kPrefetch];
-    {
-        const uint32_t n0 = min(cs, cd.n_tokens - start0);
-#pragma unroll
-        for (int j = 0; j < kPrefetch; ++j) {
-            const uint32_t idx = lane + 32 * j;
-            pf[j] = idx < n0 ? __ldg(base + start0 + idx) : 0u;
-        }
-    }
-    uint32_t row = cd.out_first + k0;
     unsigned long long misses = 0;
-    for (uint32_t start = start0; start < cd.n_tokens; start += cs, ++row) {
+    for (uint32_t j = 0; j < nchunks; ++j) {
+        named_barrier(bar_id, 64);  // chunk j prepared; the other buffer is free
+        if (producer) {
+            if (j + 1 < nchunks) produce(j + 1);
+            continue;
+        }
+        const uint32_t b = j & 1;
+        const uint32_t start = start0 + j * cs;
         const uint32_t n = min(cs, cd.n_tokens - start);
-        // 1. stage this chunk's tokens
-#pragma unroll
-        for (int j = 0; j < kPrefetch; ++j) {
-            const uint32_t idx = lane + 32 * j;
-            if (idx < n) s.tok[idx] = pf[j];
-        }
-        if (lane == 0) s.tok[n] = 0;
-        __syncwarp();
-        // 2. prefetch the next chunk (lands while this one compresses)
-        const uint32_t nstart = start + cs;
-        if (nstart < cd.n_tokens) {
-            const uint32_t nn = min(cs, cd.n_tokens - nstart);
-#pragma unroll
-            for (int j = 0; j < kPrefetch; ++j) {
-                const uint32_t idx = lane + 32 * j;
-                pf[j] = idx < nn ? __ldg(base + nstart + idx) : 0u;
-            }
-        }
-        uint64_t key = 0;
-        if (M.slots != nullptr) key = M.keys[row];
-        if (M.hit_entry != nullptr && lane == 0) M.hit_entry[row] = kNoEntry;
-        ++misses;
-        // 3. every message word of the chunk, in parallel across lanes
         const uint32_t len = hdr + 4 * n;
         const uint32_t nblocks = (len + 9 + 63) / 64;
         const uint32_t end = 64 * nblocks;
-        for (uint32_t j = lane; j < 16 * nblocks; j += 32) {
-            const uint32_t o = 4 * j;
-            uint32_t word;
-            if (o >= hdr && o + 4 <= len) {
-                const uint32_t k = o - hdr;
-                const uint32_t kk = k & 3;
-                const uint32_t sl = (kk + 3) | ((kk + 2) << 4) | ((kk + 1) << 8) | (kk << 12);
-                word = __byte_perm(s.tok[k >> 2], kk ? s.tok[(k >> 2) + 1] : 0u, sl);
-            } else {
-                word = (smem_msg_byte(s, P, hdr, len, end, o) << 24) |
-                       (smem_msg_byte(s, P, hdr, len, end, o + 1) << 16) |
-                       (smem_msg_byte(s, P, hdr, len, end, o + 2) << 8) |
-                       smem_msg_byte(s, P, hdr, len, end, o + 3);
-            }
-            s.w[j] = word;
-        }
+        const uint32_t row = cd.out_first + k0 + j;
+        const uint64_t key = M.slots != nullptr ? M.keys[row] : 0;
+        if (M.hit_entry != nullptr && lane == 0) M.hit_entry[row] = kNoEntry;
+        ++misses;
+        // parent block(s): words, then their schedules
+        for (uint32_t jw = 16 * pb0 + lane; jw < 16 * (pb1 + 1); jw += 32)
+            s.w[b][jw] = pair_msg_word(s.tok[b], s.parent, P, hdr, len, end, jw);
         __syncwarp();
-        // 3b. message schedules of all blocks, one lane per block
-        for (uint32_t b = lane; b < nblocks; b += 32) expand_block(s.w + 16 * b, s.kw + 64 * b);
+        if (lane <= pb1 - pb0) expand_block(s.w[b] + 16 * (pb0 + lane), s.kw[b] + 64 * (pb0 + lane));
         __syncwarp();
-        // 4. the serial part: every lane runs the same rounds
         uint32_t h[8] = {0x6a09e667, 0xbb67ae85, 0x3c6ef372, 0xa54ff53a,
                          0x510e527f, 0x9b05688c, 0x1f83d9ab, 0x5be0cd19};
 #pragma unroll 1
-        for (uint32_t b = 0; b < nblocks; ++b) compress_kw(h, s.kw + 64 * b);
-        __syncwarp();  // all lanes done reading s.w / s.parent of this chunk
-        if (M.slots != nullptr) memo_insert(M, s, n, key, lane, h);  // needs the old parent
+        for (uint32_t blk = 0; blk < nblocks; ++blk) compress_kw(h, s.kw[b] + 64 * blk);
         __syncwarp();
-        // 5. digest out; it is the next chunk's parent
+        if (M.slots != nullptr) memo_insert(M, s.parent, s.tok[b], n, key, lane, h);  // needs the old parent
+        __syncwarp();
         if (lane == 0) {
             uint32_t* o = reinterpret_cast<uint32_t*>(out + 32ull * row);
 #pragma unroll
@@ -442,7 +457,7 @@ hash_chains_warp_kernel(const uint32_t* __restrict__ tokens, const ChainDesc* __
         }
         __syncwarp();
     }
-    if (M.stats != nullptr && lane == 0 && misses) atomicAdd(M.stats + 1, misses);
+    if (!producer && M.stats != nullptr && lane == 0 && misses) atomicAdd(M.stats + 1, misses);
 }
 
 // Largest chain index c with chains[c].out_first <= row.
@@ -678,15 +693,15 @@ cudaError_t launch_hash_chains(const uint32_t* tokens, const ChainDesc* chains, 
         return cudaErrorInvalidValue;
     note_launch();
     if (params.chunk_size <= uint32_t(kWarpChunkMax)) {
-        const int blocks = int((n_chains + kWarpsPerCta - 1) / kWarpsPerCta);
         MemoView m;
         if (memo && memo->slots && memo->entry_words == 17 + params.chunk_size) {
             m = *memo;
             memo_probe_kernel<<<n_chains, kProbeThreads, 0, stream>>>(chains, params, out, m);
             note_launch();
         }
-        hash_chains_warp_kernel<<<blocks, 32 * kWarpsPerCta, 0, stream>>>(tokens, chains, n_chains,
-                                                                          params, out, m);
+        const int pblocks = int((n_chains + kPairsPerCta - 1) / kPairsPerCta);
+        hash_chains_pair_kernel<<<pblocks, 64 * kPairsPerCta, 0, stream>>>(tokens, chains, n_chains, params,
+                                                                         out, m);
     } else {
         const int threads = 128;
         const int blocks = int((n_chains + threads - 1) / threads);

@@ -160,7 +160,7 @@ std::vector<std::vector<Digest>> KeyHasher::hash(const std::vector<TokenSpanView
 void KeyHasher::enable_memo(size_t entries) {
     std::lock_guard lock(mu_);
     TKV_CUDA(cudaSetDevice(device_));
-    if (entries == 0 || chunk_size_ > 256) {  // the memo lives in the warp-per-chain kernel
+    if (entries == 0 || chunk_size_ > 256) {  // the memo lives in the warp-cooperative kernel
         memo_ = MemoView{};
         return;
     }
