@@ -1,13 +1,12 @@
 #include "connector.hpp"
 
+#include <algorithm>
 #include <chrono>
 #include <cstdio>
 #include <cstdlib>
+#include <cstring>
 
 #include "copy_plan.hpp"
-
-#include <algorithm>
-#include <cstring>
 
 namespace tkv {
 

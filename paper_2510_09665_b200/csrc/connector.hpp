@@ -1,21 +1,27 @@
 // Engine-facing connector (mirror of include/tierkv/connector.hpp:14-152):
-// the seven Table-1 functions plus decode storing, with
-// the reference's names, argument meaning and error behaviour.
+// the seven scheduler/worker calls (get_num_new_matched_tokens,
+// update_state_after_alloc, build_connector_meta, start/wait_load_kv,
+// start/wait_store_kv) plus decode storing and prefetch, with the
+// reference's names, argument meaning and error behaviour.
 //
 // What changes is the execution model. The reference runs every byte on host
 // threads: a TaskPool task per layer for loads (connector.cpp:179-237) and
 // inline memcpys plus a record encode per chunk for stores (:281-358). Here
-//   * lookup hashes each prompt once on the GPU (K3) and caches the keys;
-//   * loads are enqueued at start_load_kv for ALL layers: per layer one
-//     batched copy-engine H2D of every chunk-layer slice from the pinned
-//     slots into a device staging ring, then one K2 scatter launch into the
-//     pages; wait_load_kv(l) makes the engine stream wait on layer l's event
-//     instead of blocking the host;
-//   * stores run K1 per layer on a side stream ordered after the engine's
-//     compute of that layer, writing each chunk straight into its pinned
-//     slot (zero-copy over PCIe, no staging, no full-size assembly
-//     buffers); a stream callback marks the chunks present when the last
-//     layer landed.
+//   * lookup hashes each prompt once on the GPU (K3, with the prefix memo)
+//     and caches the keys for planning;
+//   * loads (copy-engine path, default): per layer one batched H2D of every
+//     chunk-layer slice from the pinned slots into a device staging ring,
+//     then one K2 scatter launch into the pages, enqueued a `staging_depth`
+//     window ahead of the engine; wait_load_kv(l) makes the engine stream
+//     wait on layer l's event instead of blocking the host;
+//   * stores (copy-engine path, default): per layer K1 on a side stream,
+//     ordered after the engine's compute of that layer, gathers every chunk
+//     into an HBM staging ring and one batched D2H copies the slices into
+//     their pinned slots; a stream callback marks the chunks present after
+//     the last layer landed. Slots are claimed up front with the outcome of
+//     the reference's sequential batch_put (TieredStore::begin_write_batch);
+//   * zero-copy variants (K2 reading / K1 writing the pinned slots directly)
+//     are selectable per connector.
 // Blocking mode (configured, or a batch whose one-layer staging exceeds the
 // budget, connector.cpp:244-256) moves all layers in one launch and returns
 // only after the bytes are in place, like the reference.
