@@ -20,9 +20,15 @@ Reported (one JSON line, rank 0):
   e2e      the connector step above through the C-ABI with the pinned host
            tier (H2D/D2H inside the timed region), payload GB/s, whole job.
   roofline K1/K2 kernel: algorithmic HBM bytes (2 x payload) / launch time vs
-           MEASURED_PEAKS.json hbm_gbs; links: PCIe measured in-run.
+           MEASURED_PEAKS.json hbm_gbs (fallback 6650); traffic from the
+           committed ncu capture; links: PCIe measured in-run per rank.
   cpu_baseline  the unmodified reference Connector (oracle/_ref) on the
            same step, bounded to 8 of the 80 layers, rank 0 / N=1 only.
+  parity   the 10 GiB page image after the kernel loop, and after one more
+           (untimed) connector step, checked word by word on the device.
+  pd       (N >= 2) prefill rank r -> decode rank r + N/2 chunk sends over
+           NVLink, both send variants, an in-run peer-copy probe, and the
+           reference's PD CPU work on a bounded sample.
 
 --impl reference runs only the reference CPU path (rank 0) and prints its
 line. Inputs (64 + 64 chunks of 5 GiB each at N=1) exceed L2 (126 MB), so no
