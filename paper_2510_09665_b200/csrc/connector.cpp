@@ -242,7 +242,10 @@ void Connector::recycle_prompt_into(std::vector<TokenId>& dst, size_t n) {
 }
 
 const std::vector<ChunkKey>& Connector::keys_for(QueryState& qs, TokenSpanView prompt) {
-    if (qs.keys.empty() || qs.prompt.size() != prompt.size() ||
+    const size_t rows = (prompt.size() + store_.config().chunk_size - 1) / store_.config().chunk_size;
+    // Recompute when the prompt differs or the lookup stopped at the first
+    // absent chunk (the memo serves the part it already hashed).
+    if (qs.keys.size() != rows || qs.prompt.size() != prompt.size() ||
         !std::equal(prompt.begin(), prompt.end(), qs.prompt.begin())) {
         qs.prompt.assign(prompt.begin(), prompt.end());
         qs.keys = chunk_keys(hasher_, prompt);
@@ -259,10 +262,13 @@ std::vector<size_t> Connector::get_num_new_matched_tokens(
     const size_t cs = store_.config().chunk_size;
     static const bool trace = std::getenv("TKV_TRACE_LOOKUP") != nullptr;
     const auto t0 = std::chrono::steady_clock::now();
-    auto digests = hasher_.hash(prompts);  // one K3 launch for the whole batch
+    // LPM (tokens.cpp:59-69): the chain only as far as the first absent
+    // chunk, like the reference's lookup; the leading present chunks are
+    // probed under one store lock per query. Planning completes the chain.
+    auto digests = hasher_.hash_prefix(prompts, [this](const std::vector<Digest>& d) {
+        return store_.present_prefix(d);
+    });
     const auto t1 = std::chrono::steady_clock::now();
-    // LPM (tokens.cpp:59-69) over the hashed chain: the leading present
-    // chunks, probed under one store lock per query.
     std::vector<size_t> out(ids.size());
     for (size_t q = 0; q < ids.size(); ++q) {
         std::vector<ChunkKey> keys(digests[q].size());

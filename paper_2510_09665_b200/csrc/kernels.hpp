@@ -116,13 +116,19 @@ struct MemoView {
     uint32_t entry_cap = 0;               // <= 2^24
     uint32_t entry_words = 0;             // 17 + chunk_size
     unsigned long long* stats = nullptr;  // [0] hits, [1] misses (optional)
+    uint32_t max_rows = 0;                // hash at most this many rows per chain (0 = all)
 };
 
-// With a memo: probes every row of every chain in parallel (one CTA per
-// chain), then hashes each chain from its first miss. Without: plain chains.
+// With a memo whose first_miss is set: probes every row of every chain in
+// parallel (one CTA per chain), then hashes each chain from its first miss.
+// With first_miss unset: hashes every row of each chain, inserting the links
+// under memo.keys[row]. Without a memo: plain chains.
 cudaError_t launch_hash_chains(const uint32_t* tokens, const ChainDesc* chains, uint32_t n_chains,
                                const HashParams& params, uint8_t* out, cudaStream_t stream,
                                const MemoView* memo = nullptr);
+// The memo probe pass alone (fills out / hit_entry / first_miss).
+cudaError_t launch_memo_probe(const ChainDesc* chains, uint32_t n_chains, const HashParams& params,
+                              uint8_t* out, const MemoView& memo, cudaStream_t stream);
 // SM-driven copy of exactly `bytes` between device-visible addresses (no copy
 // engine): 16-byte vectors when both ends are 16-aligned, bytes otherwise.
 cudaError_t launch_sm_copy(const void* src, void* dst, uint64_t bytes, cudaStream_t stream);

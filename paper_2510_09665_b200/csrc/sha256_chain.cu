@@ -382,7 +382,8 @@ hash_chains_pair_kernel(const uint32_t* __restrict__ tokens, const ChainDesc* __
     const uint32_t k0 = M.first_miss != nullptr ? M.first_miss[c] : 0u;
     const uint32_t start0 = k0 * cs;
     if (start0 >= cd.n_tokens) return;  // both warps
-    const uint32_t nchunks = (cd.n_tokens - start0 + cs - 1) / cs;
+    uint32_t nchunks = (cd.n_tokens - start0 + cs - 1) / cs;
+    if (M.max_rows) nchunks = min(nchunks, M.max_rows);
     const uint32_t hdr = 2 + P.tag_len + 32;
     const uint32_t pb0 = (2 + P.tag_len) / 64, pb1 = (hdr - 1) / 64;  // blocks holding the parent
     const uint32_t bar_id = 1 + pair;
@@ -658,6 +659,14 @@ cudaError_t launch_memo_stage(const uint32_t* src, uint32_t* dst, const ChainDes
     return cudaGetLastError();
 }
 
+cudaError_t launch_memo_probe(const ChainDesc* chains, uint32_t n_chains, const HashParams& params,
+                              uint8_t* out, const MemoView& memo, cudaStream_t s) {
+    if (n_chains == 0 || !memo.slots || !memo.first_miss) return cudaSuccess;
+    note_launch();
+    memo_probe_kernel<<<n_chains, kProbeThreads, 0, s>>>(chains, params, out, memo);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_memo_verify(const uint32_t* tokens, const ChainDesc* chains, uint32_t n_chains,
                                uint32_t total_rows, const HashParams& params, const uint8_t* dev_out,
                                const MemoView* memo, uint8_t* out, unsigned int* first_bad,
@@ -694,10 +703,13 @@ cudaError_t launch_hash_chains(const uint32_t* tokens, const ChainDesc* chains, 
     note_launch();
     if (params.chunk_size <= uint32_t(kWarpChunkMax)) {
         MemoView m;
+        if (memo) m.max_rows = memo->max_rows;
         if (memo && memo->slots && memo->entry_words == 17 + params.chunk_size) {
             m = *memo;
-            memo_probe_kernel<<<n_chains, kProbeThreads, 0, stream>>>(chains, params, out, m);
-            note_launch();
+            if (m.first_miss != nullptr) {
+                memo_probe_kernel<<<n_chains, kProbeThreads, 0, stream>>>(chains, params, out, m);
+                note_launch();
+            }
         }
         const int pblocks = int((n_chains + kPairsPerCta - 1) / kPairsPerCta);
         hash_chains_pair_kernel<<<pblocks, 64 * kPairsPerCta, 0, stream>>>(tokens, chains, n_chains, params,

@@ -37,26 +37,18 @@ double now_us() {
 }
 }  // namespace
 
-std::vector<std::vector<Digest>> KeyHasher::hash(const std::vector<TokenSpanView>& seqs,
-                                                 const std::vector<Digest>* parents) {
-    const double t_in = trace_lookup() ? now_us() : 0;
-    std::lock_guard lock(mu_);
-    TKV_CUDA(cudaSetDevice(device_));
-    size_t total_tokens = 0, total_chunks = 0;
-    for (const auto& s : seqs) {
-        total_tokens += s.size();
-        total_chunks += (s.size() + chunk_size_ - 1) / chunk_size_;
-    }
-    std::vector<std::vector<Digest>> out(seqs.size());
-    if (total_chunks == 0) return out;
-
-    // Tokens, chain descriptors and digests live in mapped pinned memory: K3
-    // reads and writes them over PCIe directly (a few KiB per chain), so a
-    // lookup never queues on the copy engines behind in-flight KV transfers.
+// Packs the sequences into the mapped buffers and stages them into HBM on the
+// hasher stream (with the memo: the fingerprint pass does the staging).
+// Caller holds mu_. Returns the memo view for this launch (slots == nullptr
+// without a memo).
+MemoView KeyHasher::stage_locked(const std::vector<TokenSpanView>& seqs, const std::vector<Digest>* parents,
+                                 size_t total_tokens, size_t total_chunks, HashParams& p) {
+    // Tokens, chain descriptors and digests live in mapped pinned memory and
+    // move by SM loads/stores, so a lookup never queues on the copy engines
+    // behind in-flight KV transfers.
     h_tokens_.reserve(total_tokens * sizeof(TokenId) + 64);
     h_chains_.reserve(seqs.size() * sizeof(ChainDesc));
     h_out_.reserve(total_chunks * 32);
-
     auto* tok = reinterpret_cast<TokenId*>(h_tokens_.host);
     auto* ch = reinterpret_cast<ChainDesc*>(h_chains_.host);
     size_t toff = 0, row = 0;
@@ -71,21 +63,17 @@ std::vector<std::vector<Digest>> KeyHasher::hash(const std::vector<TokenSpanView
         toff += seqs[i].size();
         row += (seqs[i].size() + chunk_size_ - 1) / chunk_size_;
     }
-    HashParams p;
     p.chunk_size = uint32_t(chunk_size_);
     p.tag_len = uint32_t(tag_.size());
     std::copy(tag_.begin(), tag_.end(), p.tag);
 
-    // Stage tokens and descriptors into HBM (one parallel read of the mapped
-    // buffers), run the chains writing digests to HBM, then verify memo hits
-    // and publish every digest to the mapped result buffer.
-    const double t_packed = trace_lookup() ? now_us() : 0;
     const size_t tok_bytes = total_tokens * sizeof(TokenId);
     const size_t ch_bytes = seqs.size() * sizeof(ChainDesc);
     d_tokens_.reserve(tok_bytes + 64);
     d_chains_.reserve(ch_bytes + 64);
     d_out_.reserve(total_chunks * 32);
     h_bad_.reserve(seqs.size() * sizeof(unsigned int));
+    h_first_.reserve(seqs.size() * sizeof(uint32_t));
     auto* bad = reinterpret_cast<unsigned int*>(h_bad_.host);
     std::fill(bad, bad + seqs.size(), ~0u);
     MemoView m = memo_;
@@ -100,15 +88,72 @@ std::vector<std::vector<Digest>> KeyHasher::hash(const std::vector<TokenSpanView
         m.keys = reinterpret_cast<unsigned long long*>(d_keys_.ptr);
         m.first_miss = reinterpret_cast<uint32_t*>(d_first_.ptr);
     }
-    const auto* d_tok = reinterpret_cast<const uint32_t*>(d_tokens_.ptr);
-    const auto* d_ch = reinterpret_cast<const ChainDesc*>(d_chains_.ptr);
     TKV_CUDA(launch_sm_copy(h_chains_.dev, d_chains_.ptr, ch_bytes, stream_));
     if (memo_.slots)  // staging + per-row fingerprints in one pass
         TKV_CUDA(launch_memo_stage(reinterpret_cast<const uint32_t*>(h_tokens_.dev),
-                                   reinterpret_cast<uint32_t*>(d_tokens_.ptr), d_ch, uint32_t(seqs.size()),
+                                   reinterpret_cast<uint32_t*>(d_tokens_.ptr),
+                                   reinterpret_cast<const ChainDesc*>(d_chains_.ptr), uint32_t(seqs.size()),
                                    uint32_t(total_chunks), p, m, stream_));
     else
         TKV_CUDA(launch_sm_copy(h_tokens_.dev, d_tokens_.ptr, tok_bytes, stream_));
+    return m;
+}
+
+// Re-hashes, without the memo, the chains whose memo hits failed
+// verification (first_bad != ~0: a 40-bit tag collision), from the first bad
+// chunk on, and republishes every row. Caller holds mu_.
+void KeyHasher::rehash_bad_locked(size_t n_chains, size_t total_chunks, const HashParams& p) {
+    auto* bad = reinterpret_cast<unsigned int*>(h_bad_.host);
+    auto* ch = reinterpret_cast<ChainDesc*>(h_chains_.host);
+    std::vector<ChainDesc> redo;
+    for (size_t i = 0; i < n_chains; ++i) {
+        if (bad[i] == ~0u) continue;
+        ChainDesc d = ch[i];
+        const size_t skip = size_t(bad[i]) * chunk_size_;
+        d.token_off += skip;
+        d.n_tokens -= uint32_t(skip);
+        d.out_first += bad[i];
+        if (bad[i]) std::copy(h_out_.host + 32 * (d.out_first - 1), h_out_.host + 32 * d.out_first, d.parent);
+        redo.push_back(d);
+        bad[i] = ~0u;
+    }
+    if (redo.empty()) return;
+    ++memo_rehashes_;
+    // the redo descriptors go after the launch's own (d_chains_ keeps those)
+    std::vector<ChainDesc> all(ch, ch + n_chains);
+    all.insert(all.end(), redo.begin(), redo.end());
+    h_chains_.reserve(all.size() * sizeof(ChainDesc));
+    d_chains_.reserve(all.size() * sizeof(ChainDesc) + 64);
+    ch = reinterpret_cast<ChainDesc*>(h_chains_.host);
+    std::copy(all.begin(), all.end(), ch);
+    TKV_CUDA(launch_sm_copy(h_chains_.dev, d_chains_.ptr, all.size() * sizeof(ChainDesc), stream_));
+    const auto* d_tok = reinterpret_cast<const uint32_t*>(d_tokens_.ptr);
+    const auto* d_ch = reinterpret_cast<const ChainDesc*>(d_chains_.ptr);
+    TKV_CUDA(launch_hash_chains(d_tok, d_ch + n_chains, uint32_t(redo.size()), p, d_out_.ptr, stream_, nullptr));
+    TKV_CUDA(launch_memo_verify(d_tok, d_ch, uint32_t(n_chains), uint32_t(total_chunks), p, d_out_.ptr, nullptr,
+                                h_out_.dev, nullptr, stream_));
+    TKV_CUDA(cudaStreamSynchronize(stream_));
+}
+
+std::vector<std::vector<Digest>> KeyHasher::hash(const std::vector<TokenSpanView>& seqs,
+                                                 const std::vector<Digest>* parents) {
+    const double t_in = trace_lookup() ? now_us() : 0;
+    std::lock_guard lock(mu_);
+    TKV_CUDA(cudaSetDevice(device_));
+    size_t total_tokens = 0, total_chunks = 0;
+    for (const auto& s : seqs) {
+        total_tokens += s.size();
+        total_chunks += (s.size() + chunk_size_ - 1) / chunk_size_;
+    }
+    std::vector<std::vector<Digest>> out(seqs.size());
+    if (total_chunks == 0) return out;
+    HashParams p;
+    MemoView m = stage_locked(seqs, parents, total_tokens, total_chunks, p);
+    const double t_packed = trace_lookup() ? now_us() : 0;
+    // Run the chains writing digests to HBM, then verify memo hits and
+    // publish every digest to the mapped result buffer.
+    const auto* d_tok = reinterpret_cast<const uint32_t*>(d_tokens_.ptr);
+    const auto* d_ch = reinterpret_cast<const ChainDesc*>(d_chains_.ptr);
     TKV_CUDA(launch_hash_chains(d_tok, d_ch, uint32_t(seqs.size()), p, d_out_.ptr, stream_,
                                 memo_.slots ? &m : nullptr));
     TKV_CUDA(launch_memo_verify(d_tok, d_ch, uint32_t(seqs.size()), uint32_t(total_chunks), p,
@@ -119,31 +164,9 @@ std::vector<std::vector<Digest>> KeyHasher::hash(const std::vector<TokenSpanView
     const double t_synced = trace_lookup() ? now_us() : 0;
     ++launches_;
     chunks_ += total_chunks;
+    rehash_bad_locked(seqs.size(), total_chunks, p);
 
-    // A memo hit that failed verification (a 40-bit tag collision): re-hash
-    // those chains from the first bad chunk with plain SHA-256.
-    std::vector<ChainDesc> redo;
-    for (size_t i = 0; i < seqs.size(); ++i) {
-        if (bad[i] == ~0u) continue;
-        ChainDesc d = ch[i];
-        const size_t skip = size_t(bad[i]) * chunk_size_;
-        d.token_off += skip;
-        d.n_tokens -= uint32_t(skip);
-        d.out_first += bad[i];
-        if (bad[i]) std::copy(h_out_.host + 32 * (d.out_first - 1), h_out_.host + 32 * d.out_first, d.parent);
-        redo.push_back(d);
-    }
-    if (!redo.empty()) {
-        ++memo_rehashes_;
-        std::copy(redo.begin(), redo.end(), ch);
-        TKV_CUDA(launch_sm_copy(h_chains_.dev, d_chains_.ptr, redo.size() * sizeof(ChainDesc), stream_));
-        TKV_CUDA(launch_hash_chains(d_tok, d_ch, uint32_t(redo.size()), p, d_out_.ptr, stream_, nullptr));
-        TKV_CUDA(launch_memo_verify(d_tok, d_ch, uint32_t(redo.size()), uint32_t(total_chunks), p,
-                                    d_out_.ptr, nullptr, h_out_.dev, nullptr, stream_));
-        TKV_CUDA(cudaStreamSynchronize(stream_));
-    }
-
-    row = 0;
+    size_t row = 0;
     for (size_t i = 0; i < seqs.size(); ++i) {
         size_t n = (seqs[i].size() + chunk_size_ - 1) / chunk_size_;
         out[i].resize(n);
@@ -154,6 +177,102 @@ std::vector<std::vector<Digest>> KeyHasher::hash(const std::vector<TokenSpanView
         std::fprintf(stderr, "[tkv hash] chains=%zu rows=%zu pack=%.1fus launch=%.1fus device+sync=%.1fus unpack=%.1fus\n",
                      seqs.size(), total_chunks, t_packed - t_in, t_launched - t_packed, t_synced - t_launched,
                      now_us() - t_synced);
+    return out;
+}
+
+std::vector<std::vector<Digest>> KeyHasher::hash_prefix(const std::vector<TokenSpanView>& seqs,
+                                                        const PresentPrefix& present) {
+    std::lock_guard lock(mu_);
+    TKV_CUDA(cudaSetDevice(device_));
+    const size_t n_chains = seqs.size();
+    size_t total_tokens = 0, total_chunks = 0;
+    std::vector<size_t> rows(n_chains), first_row(n_chains);
+    for (size_t i = 0; i < n_chains; ++i) {
+        first_row[i] = total_chunks;
+        rows[i] = (seqs[i].size() + chunk_size_ - 1) / chunk_size_;
+        total_tokens += seqs[i].size();
+        total_chunks += rows[i];
+    }
+    std::vector<std::vector<Digest>> out(n_chains);
+    if (total_chunks == 0) return out;
+    HashParams p;
+    MemoView m = stage_locked(seqs, nullptr, total_tokens, total_chunks, p);
+    const auto* d_tok = reinterpret_cast<const uint32_t*>(d_tokens_.ptr);
+    const auto* d_ch = reinterpret_cast<const ChainDesc*>(d_chains_.ptr);
+    auto* first = reinterpret_cast<uint32_t*>(h_first_.host);
+    auto* bad = reinterpret_cast<unsigned int*>(h_bad_.host);
+    std::vector<size_t> known(n_chains, 0);
+    ++launches_;
+    // 1. every row probed at once (memo), the first row past the hits of
+    //    every chain hashed (one SHA chunk: the reference's
+    //    longest_prefix_match also stops at the first absent chunk,
+    //    tokens.cpp:59-69), the hits verified exactly, all in one round trip.
+    m.max_rows = 1;
+    TKV_CUDA(launch_hash_chains(d_tok, d_ch, uint32_t(n_chains), p, d_out_.ptr, stream_, &m));
+    TKV_CUDA(launch_memo_verify(d_tok, d_ch, uint32_t(n_chains), uint32_t(total_chunks), p, d_out_.ptr,
+                                memo_.slots ? &m : nullptr, h_out_.dev,
+                                reinterpret_cast<unsigned int*>(h_bad_.dev), stream_));
+    if (memo_.slots) TKV_CUDA(launch_sm_copy(d_first_.ptr, h_first_.dev, n_chains * sizeof(uint32_t), stream_));
+    TKV_CUDA(cudaStreamSynchronize(stream_));
+    for (size_t i = 0; i < n_chains; ++i) {
+        const size_t f = memo_.slots ? size_t(first[i]) : 0;
+        known[i] = std::min(rows[i], f + 1);
+        if (memo_.slots && bad[i] != ~0u) known[i] = std::min<size_t>(known[i], bad[i]);
+    }
+    // 2. the leading present chunks: a chain whose known chunks are all
+    //    present (a memo that lost its links, or a failed hit) continues —
+    //    one chunk at a time is the reference's order; here the first pass
+    //    adds one chunk and the second hashes the rest in one launch.
+    auto digests_of = [&](size_t i, size_t n) {
+        std::vector<Digest> d(n);
+        for (size_t c = 0; c < n; ++c)
+            std::copy(h_out_.host + 32 * (first_row[i] + c), h_out_.host + 32 * (first_row[i] + c) + 32,
+                      d[c].begin());
+        return d;
+    };
+    auto ch = reinterpret_cast<const ChainDesc*>(h_chains_.host);
+    for (int pass = 0; pass < 2; ++pass) {
+        // (a chain with a failed memo hit re-enters here one chunk at a time)
+        std::vector<ChainDesc> more;
+        std::vector<size_t> which;
+        for (size_t i = 0; i < n_chains; ++i) {
+            if (known[i] >= rows[i]) continue;
+            const auto d = digests_of(i, known[i]);
+            if (present(d) < known[i]) continue;  // the LPM ended inside the hits
+            ChainDesc x = ch[i];
+            const size_t skip = known[i] * chunk_size_;
+            x.token_off += skip;
+            x.n_tokens = pass == 0 ? uint32_t(std::min(chunk_size_, seqs[i].size() - skip))
+                                   : uint32_t(seqs[i].size() - skip);
+            x.out_first = uint32_t(first_row[i] + known[i]);
+            if (known[i]) std::copy(d[known[i] - 1].begin(), d[known[i] - 1].end(), x.parent);
+            more.push_back(x);
+            which.push_back(i);
+        }
+        if (more.empty()) break;
+        std::vector<ChainDesc> all(ch, ch + n_chains);
+        all.insert(all.end(), more.begin(), more.end());
+        h_chains_.reserve(all.size() * sizeof(ChainDesc));
+        d_chains_.reserve(all.size() * sizeof(ChainDesc) + 64);
+        std::copy(all.begin(), all.end(), reinterpret_cast<ChainDesc*>(h_chains_.host));
+        ch = reinterpret_cast<const ChainDesc*>(h_chains_.host);
+        d_ch = reinterpret_cast<const ChainDesc*>(d_chains_.ptr);
+        TKV_CUDA(launch_sm_copy(h_chains_.dev, d_chains_.ptr, all.size() * sizeof(ChainDesc), stream_));
+        MemoView ins = m;  // insert the new links under their full-prefix keys
+        ins.first_miss = nullptr;
+        ins.max_rows = 0;  // the descriptors bound the rows
+        TKV_CUDA(launch_hash_chains(d_tok, d_ch + n_chains, uint32_t(more.size()), p, d_out_.ptr, stream_,
+                                    memo_.slots ? &ins : nullptr));
+        TKV_CUDA(launch_memo_verify(d_tok, d_ch, uint32_t(n_chains), uint32_t(total_chunks), p, d_out_.ptr,
+                                    nullptr, h_out_.dev, nullptr, stream_));
+        TKV_CUDA(cudaStreamSynchronize(stream_));
+        for (size_t k = 0; k < which.size(); ++k) {
+            const size_t i = which[k];
+            chunks_ += more[k].n_tokens ? (more[k].n_tokens + chunk_size_ - 1) / chunk_size_ : 0;
+            known[i] = pass == 0 ? known[i] + 1 : rows[i];
+        }
+    }
+    for (size_t i = 0; i < n_chains; ++i) out[i] = digests_of(i, known[i]);
     return out;
 }
 

@@ -49,6 +49,16 @@ public:
                                           const std::vector<Digest>* parents = nullptr);
     std::vector<Digest> hash_one(TokenSpanView seq, const Digest& parent = kZeroDigest);
 
+    // Lookup form: the leading digests of each sequence, just far enough to
+    // decide its longest stored prefix — like the reference's
+    // longest_prefix_match (tokens.cpp:59-69), which stops at the first
+    // absent chunk. `present(d)` returns how many leading digests of d are
+    // stored. Memo hits come from the parallel probe (verified); past them
+    // one SHA chunk decides, and only a present one continues the chain.
+    using PresentPrefix = std::function<size_t(const std::vector<Digest>&)>;
+    std::vector<std::vector<Digest>> hash_prefix(const std::vector<TokenSpanView>& seqs,
+                                                 const PresentPrefix& present);
+
     // Launch counters (tests assert the once-per-query property).
     uint64_t launches() const { return launches_; }
     uint64_t chunks_hashed() const { return chunks_; }
@@ -66,12 +76,15 @@ public:
 
 private:
     void memo_reset_locked();
+    MemoView stage_locked(const std::vector<TokenSpanView>& seqs, const std::vector<Digest>* parents,
+                          size_t total_tokens, size_t total_chunks, HashParams& p);
+    void rehash_bad_locked(size_t n_chains, size_t total_chunks, const HashParams& p);
     std::string tag_;
     size_t chunk_size_;
     int device_;
     std::mutex mu_;
     Stream stream_;
-    PinnedBuffer h_tokens_, h_chains_, h_out_, h_bad_;  // mapped host side of a launch
+    PinnedBuffer h_tokens_, h_chains_, h_out_, h_bad_, h_first_;  // mapped host side of a launch
     DeviceBuffer d_tokens_, d_chains_, d_out_, d_hit_;  // HBM copies the kernels work on
     DeviceBuffer d_keys_, d_first_;                     // memo probe keys / first miss per chain
     uint64_t memo_rehashes_ = 0;

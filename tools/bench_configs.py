@@ -211,11 +211,19 @@ def c4(queries, reuse):
     import oracle
     ref_lookup = None
     if oracle.ref_available():
-        R = oracle.Ref()
-        prompt = np.concatenate([docs[0], toks(60, 1)])
-        t0 = time.perf_counter()
-        R.chunk_keys(prompt, 256, TAG8)  # the reference lookup's cost: the full SHA-NI chain
-        ref_lookup = round(1e3 * (time.perf_counter() - t0), 3)
+        # The reference Connector's own lookup on the same prompts (hashing up
+        # to the first absent chunk); the lookup does not depend on the KV
+        # geometry, so the reference stack holds the document in 64-byte rows.
+        r = oracle.RefEngine(num_layers=1, bpt=64, page_tokens=16, tag=TAG8, chunk_size=256,
+                             ram_slots=n_doc // 256 + 8, num_pages=64)
+        r.seed_store(docs[0], n_doc)
+        ref_lookup = {}
+        for kind, p in (("hit", np.concatenate([docs[0], toks(60, 1)])), ("miss", docs[1])):
+            t0 = time.perf_counter()
+            r.get_num_new_matched_tokens(1, p)
+            ref_lookup[kind] = round(1e3 * (time.perf_counter() - t0), 3)
+            r.finish_query(1)
+        r.close()
     memo = e.memo_stats()
     e.close()
     return {"config": f"c4: 8B KV, {n_docs} shared 128K docs + question, reuse {reuse:.0%}, {queries} queries",
@@ -224,7 +232,7 @@ def c4(queries, reuse):
             "lookup_ms_hit": round(1e3 * float(np.median([t for t, h in zip(t_lookup, hit_flags) if h] or [0])), 3),
             "lookup_ms_miss": round(1e3 * float(np.median([t for t, h in zip(t_lookup, hit_flags) if not h] or [0])), 3),
             "lookup_tokens_per_s": round((n_doc + 60) / float(np.median(t_lookup)), 1),
-            "memo": memo, "ref_cpu_lookup_ms_1core": ref_lookup}
+            "memo": memo, "ref_cpu_lookup_ms": ref_lookup}
 
 
 if __name__ == "__main__":

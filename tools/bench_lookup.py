@@ -1,7 +1,15 @@
-"""Config-4 lookup latency: get_num_new_matched_tokens of a 128K-token
-document + question through the C-ABI connector, memo cold (first lookup:
-SHA of every chunk) and warm (every chunk a memo hit), vs the reference's own
-chunk_keys (oracle/_ref, OpenSSL SHA-NI, one core). One JSON line."""
+"""Config-4 lookup latency, B200 connector vs the reference Connector, on the
+same prompts (get_num_new_matched_tokens through each C-ABI / shim):
+
+  hit   a stored 128K-token document + a 60-token question: the reference
+        hashes every chunk up to the first absent one (the question), so 513
+        SHA-256 chunks; the B200 path probes the prefix memo (warm after the
+        first lookup) and hashes the one new chunk.
+  miss  a cold 128K-token document: both stop at the first chunk.
+
+The lookup does not depend on the KV geometry, so both engines use one layer
+of 64-byte rows (the stored chunks' bytes are irrelevant to the lookup).
+One JSON line."""
 import json
 import os
 import sys
@@ -12,45 +20,56 @@ import torch
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
+import oracle  # noqa: E402
 from paper_2510_09665_b200.api import Engine  # noqa: E402
 
+TAG, N_DOC = "llama-3.1-8b", 131072
+GEOM = dict(num_layers=1, bpt=64, page_tokens=16, tag=TAG, chunk_size=256, ram_slots=N_DOC // 256 + 8,
+            num_pages=64)
 
-def main():
-    n_doc, reps = 131072, 20
-    rng = np.random.default_rng(5)
-    doc = rng.integers(0, 128256, size=n_doc, dtype=np.uint32)
-    e = Engine(num_layers=32, bpt=4096, page_tokens=16, tag="llama-3.1-8b", chunk_size=256,
-               ram_slots=4, num_pages=256)
-    prompts = [np.concatenate([doc, rng.integers(0, 128256, size=60, dtype=np.uint32)]) for _ in range(reps + 1)]
-    e.dev_prompt(1, prompts[0])
-    torch.cuda.synchronize()
-    t0 = time.perf_counter()
-    e.get_num_new_matched_tokens(1, prompts[0])
-    cold = time.perf_counter() - t0
-    warm = []
-    for i in range(reps):
-        e.dev_prompt(2 + i, prompts[1 + i])  # the engine's own prompt upload, not part of the lookup
-        torch.cuda.synchronize()
+
+def toks(n, seed):
+    return np.random.default_rng(seed).integers(0, 128256, size=n, dtype=np.uint32)
+
+
+def timed_lookups(e, prompts, qid0, prepare=None):
+    ts = []
+    for i, p in enumerate(prompts):
+        if prepare:
+            prepare(qid0 + i, p)
         t0 = time.perf_counter()
-        e.get_num_new_matched_tokens(2 + i, prompts[1 + i])
-        warm.append(time.perf_counter() - t0)
-        e.finish_query(2 + i)
-        e.release_query(2 + i)
-    st = e.memo_stats()
+        m = e.get_num_new_matched_tokens(qid0 + i, p)
+        ts.append(time.perf_counter() - t0)
+        e.finish_query(qid0 + i)
+    return ts, m
+
+
+def main(reps=20):
+    doc = toks(N_DOC, 5)
+    hits = [np.concatenate([doc, toks(60, 100 + i)]) for i in range(reps + 1)]
+    misses = [toks(N_DOC, 1000 + i) for i in range(reps)]
+    e = Engine(**GEOM)
+    e.seed_store(doc, N_DOC)
+    prep = (lambda q, p: (e.dev_prompt(q, p), torch.cuda.synchronize()))
+    t_first, _ = timed_lookups(e, hits[:1], 1, prep)  # memo cold: every chunk through SHA
+    t_hit, m_hit = timed_lookups(e, hits[1:], 100, prep)
+    t_miss, m_miss = timed_lookups(e, misses, 1000, prep)
+    assert m_hit == N_DOC and m_miss == 0
+    out = {"lookup": "c4: 128K-token document (+ 60-token question)", "tokens_hit": len(hits[0]),
+           "b200_hit_first_ms": round(1e3 * t_first[0], 3),
+           "b200_hit_ms_median": round(1e3 * float(np.median(t_hit)), 3),
+           "b200_miss_ms_median": round(1e3 * float(np.median(t_miss)), 3), "memo": e.memo_stats()}
     e.close()
-    ref = None
-    import oracle
     if oracle.ref_available():
-        R = oracle.Ref()
-        ts = []
-        for _ in range(5):
-            t0 = time.perf_counter()
-            R.chunk_keys(prompts[0], 256, "llama-3.1-8b")
-            ts.append(time.perf_counter() - t0)
-        ref = round(1e3 * min(ts), 3)
-    print(json.dumps({"lookup": "c4 128K doc + 60-token question", "tokens": len(prompts[0]),
-                      "cold_ms": round(1e3 * cold, 3), "warm_ms_median": round(1e3 * float(np.median(warm)), 3),
-                      "warm_ms_min": round(1e3 * min(warm), 3), "memo": st, "ref_cpu_chunk_keys_ms_1core": ref}))
+        r = oracle.RefEngine(**GEOM)
+        r.seed_store(doc, N_DOC)
+        rh, rm_hit = timed_lookups(r, hits[:5], 1)
+        rm, rm_miss = timed_lookups(r, misses[:5], 100)
+        assert rm_hit == N_DOC and rm_miss == 0
+        out.update({"ref_hit_ms_median": round(1e3 * float(np.median(rh)), 3),
+                    "ref_miss_ms_median": round(1e3 * float(np.median(rm)), 3), "ref_cores": 1})
+        r.close()
+    print(json.dumps(out))
 
 
 if __name__ == "__main__":
