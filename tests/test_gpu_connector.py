@@ -55,17 +55,30 @@ def test_expectations_from_reference_tests(tkv, C):
 
 def test_lookup_hashes_once_per_query(tkv, C):
     """The reference re-derives the chain 3-4x per query
-    (connector.cpp:74,103,139); here lookup hashes once and planning reuses it."""
+    (connector.cpp:74,103,139). Here the lookup hashes up to the first absent
+    chunk (like the reference's longest_prefix_match); when that already
+    covers the prompt, planning reuses the keys (one hash call per query),
+    otherwise planning completes the chain once (two calls)."""
     from paper_2510_09665_b200.api import Engine
     e = Engine(**S.CONN, ram_slots=16, num_pages=64)
     prompt = S.make_prompt(96, 5)
-    e.seed_store(prompt, 64)
+    e.seed_store(prompt, 96)  # whole prompt stored: the lookup derives every key
     before = e.hash_launches()
-    e.get_num_new_matched_tokens(1, prompt)
+    assert e.get_num_new_matched_tokens(1, prompt) == 95
     e.bind_pages(1, 96)
-    e.update_state_after_alloc(1, 6, 4)
+    e.update_state_after_alloc(1, 6, 6)
     e.build_connector_meta([(1, prompt)])
     assert e.hash_launches() - before == 1
+    prompt2 = S.make_prompt(96, 6)
+    e.seed_store(prompt2, 32)  # first chunk stored: the lookup stops after chunk 2
+    before = e.hash_launches()
+    assert e.get_num_new_matched_tokens(2, prompt2) == 32
+    e.bind_pages(2, 96)
+    e.update_state_after_alloc(2, 6, 2)
+    m = e.build_connector_meta([(2, prompt2)])
+    assert e.hash_launches() - before == 2
+    sp, _ = e.plan(m, 0, "store")
+    assert [d for _, _, _, _, d in sp] == C.chunk_keys(prompt2, 32, S.CONN["tag"])[1:]
     e.close()
 
 
