@@ -360,6 +360,15 @@ ConnectorMetadata Connector::build_connector_meta(const SchedulerOutput& out) {
     return meta;
 }
 
+// Size for a staging ring that must grow: at least `need`, and at least twice
+// the current size up to the depth x budget bound, so batches of varying
+// size stop reallocating (each growth synchronizes the ring's streams and
+// calls cudaMalloc, which must not recur inside a serving loop).
+size_t Connector::ring_growth(size_t need, size_t current, uint32_t depth) const {
+    const size_t cap = size_t(depth) * cfg_.staging_budget_bytes;
+    return std::max(need, std::min(2 * current, cap));
+}
+
 // --- loads -----------------------------------------------------------------
 
 Status Connector::enqueue_loads(BatchState& b) {
@@ -422,7 +431,7 @@ Status Connector::enqueue_loads(BatchState& b) {
         if (size_t(depth) * layer_bytes > staging_.bytes) {
             TKV_CUDA(cudaStreamSynchronize(h2d_stream_));  // previous batch may use the ring
             TKV_CUDA(cudaStreamSynchronize(load_stream_));
-            staging_.reserve(size_t(depth) * layer_bytes);
+            staging_.reserve(ring_growth(size_t(depth) * layer_bytes, staging_.bytes, depth));
         }
         staging_peak_ = std::max(staging_peak_, size_t(depth) * layer_bytes);
     }
@@ -639,7 +648,7 @@ Status Connector::reserve_stores(BatchState& b) {
     if (need > store_staging_.bytes) {
         TKV_CUDA(cudaStreamSynchronize(store_stream_));  // previous batch may use the ring
         TKV_CUDA(cudaStreamSynchronize(d2h_stream_));
-        store_staging_.reserve(need);
+        store_staging_.reserve(ring_growth(need, store_staging_.bytes, b.store_depth));
     }
     staging_peak_ = std::max(staging_peak_, need);
     std::vector<std::vector<XferDesc>> vars(b.store_depth, descs);

@@ -171,6 +171,7 @@ private:
     };
 
     const std::vector<ChunkKey>& keys_for(QueryState& qs, TokenSpanView prompt);
+    size_t ring_growth(size_t need, size_t current, uint32_t depth) const;
     void recycle_prompt(std::vector<TokenId>&& v);
     void recycle_prompt_into(std::vector<TokenId>& dst, size_t n);
     std::vector<std::vector<TokenId>> prompt_pool_;  // guarded by mu_

@@ -166,6 +166,9 @@ def c2(wave):
         assert so == 0 and lo == sum(len(p) - 1 for _, p in batch)
         total_loaded += lo
         total_t += t
+        if os.environ.get("TKV_C2_WAVES"):
+            print(json.dumps({"wave": w0 // wave, "gbps": round(lo * L8 * BPT8 / t / 1e9, 2), "s": round(t, 3)}),
+                  file=sys.stderr, flush=True)
     gb = total_loaded * L8 * BPT8
     small = [(1, toks(lens[0], 5000))]
     ref = ref_batch_gbps(small, 8, BPT8, TAG8, lambda p: len(p))
