@@ -2,6 +2,7 @@
 
 #include <sys/mman.h>
 
+#include <algorithm>
 #include <atomic>
 #include <cstdint>
 #include <utility>
@@ -72,6 +73,7 @@ void PinnedBuffer::release() {
 
 void PinnedBuffer::reserve(size_t n) {
     if (n <= bytes) return;
+    if (bytes) n = std::max(n, bytes + bytes / 2);  // regrow rarely: pinning is slow and synchronizes
     release();
     void* p = nullptr;
     constexpr size_t kHuge = size_t(2) << 20;
@@ -107,6 +109,7 @@ DeviceBuffer::~DeviceBuffer() {
 
 void DeviceBuffer::reserve(size_t n) {
     if (n <= bytes) return;
+    if (bytes) n = std::max(n, bytes + bytes / 2);  // regrow rarely: cudaFree/cudaMalloc synchronize
     if (ptr) TKV_CUDA(cudaFree(ptr));
     ptr = nullptr;
     bytes = 0;
