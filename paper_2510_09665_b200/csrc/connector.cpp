@@ -29,13 +29,31 @@ float elapsed(const Event& a, const Event& b) {
     return ms;
 }
 
+// Set once a batch's load shares are released (after its last scatter).
+struct ReleaseState {
+    std::mutex m;
+    std::condition_variable cv;
+    bool done = false;
+    void wait() {
+        std::unique_lock lock(m);
+        cv.wait(lock, [&] { return done; });
+    }
+};
 struct ReleaseCtx {
     TieredStore* store;
     std::vector<Digest> digests;
+    std::shared_ptr<ReleaseState> state;
 };
 void CUDART_CB release_cb(void* p) {
     auto* c = static_cast<ReleaseCtx*>(p);
     for (const auto& d : c->digests) c->store->release(d);
+    if (c->state) {
+        {
+            std::lock_guard lock(c->state->m);
+            c->state->done = true;
+        }
+        c->state->cv.notify_all();
+    }
     delete c;
 }
 
@@ -48,8 +66,7 @@ struct CommitCtx {
 };
 void CUDART_CB commit_cb(void* p) {
     auto* c = static_cast<CommitCtx*>(p);
-    for (const auto& d : c->digests) c->store->commit_write(d, Status::success());
-    if (!c->touches.empty()) c->store->touch_in_order(c->touches);
+    c->store->commit_batch(c->digests, c->touches);
     if (c->committed) c->committed->store(true);
     delete c;
 }
@@ -109,6 +126,7 @@ struct BatchState {
     bool stores_sealed = false, stores_waited = false;
     std::vector<StoreItem> stores;
     std::vector<Digest> store_touches;  // LRU touch order of the batch's puts (begin_write_batch)
+    std::shared_ptr<ReleaseState> loads_released;  // set by the load release callback
     std::vector<Event> compute_done, gathered, d2h_done;
     Event store_complete;
     Event t0{true};  // timeline origin (recorded when loads are enqueued)
@@ -485,7 +503,8 @@ Status Connector::enqueue_loads(BatchState& b) {
         for (uint32_t l = 0; l < L; ++l)
             pages_.mark_span_populated(it.id, l, it.span.start / pt, it.span.length());
     if (!b.loads_ce) {  // the lazy CE pipeline releases after its last layer
-        auto* ctx = new ReleaseCtx{&store_, {}};
+        b.loads_released = std::make_shared<ReleaseState>();
+        auto* ctx = new ReleaseCtx{&store_, {}, b.loads_released};
         for (const auto& it : b.loads) ctx->digests.push_back(it.digest);
         TKV_CUDA(cudaLaunchHostFunc(load_stream_, release_cb, ctx));
     }
@@ -528,7 +547,8 @@ void Connector::enqueue_load_layers(BatchState& b, uint32_t upto) {
         b.loads_finalized = true;
         ring_free_.record(load_stream_);
         ring_used_ = true;
-        auto* ctx = new ReleaseCtx{&store_, {}};
+        b.loads_released = std::make_shared<ReleaseState>();
+        auto* ctx = new ReleaseCtx{&store_, {}, b.loads_released};
         for (const auto& it : b.loads) ctx->digests.push_back(it.digest);
         TKV_CUDA(cudaLaunchHostFunc(load_stream_, release_cb, ctx));
     }
@@ -785,6 +805,10 @@ Status Connector::wait_store_kv(ConnectorMetadata& meta, uint32_t layer) {
     } catch (const CudaError& e) {
         return Status{Errc::cuda_error, e.what()};
     }
+    // The reference's loads have released their shares by the time its
+    // stores are sealed; so do ours by the time this returns (the next
+    // batch's slot reservation must see the same evictable set).
+    if (b.loads_released) b.loads_released->wait();
     std::unordered_map<QueryId, std::vector<std::pair<ChunkKey, Status>>> results;
     for (auto& s : b.stores) {
         const auto& plan = b.plans[s.plan];

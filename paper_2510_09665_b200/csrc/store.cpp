@@ -228,12 +228,26 @@ std::vector<Result<SlotWrite>> TieredStore::begin_write_batch(
     return out;
 }
 
-void TieredStore::touch_in_order(const std::vector<Digest>& digests) {
-    std::lock_guard lock(mu_);
-    for (const auto& d : digests) {
-        auto it = index_.find(d);
-        if (it != index_.end()) touch(it->second);
+void TieredStore::commit_batch(const std::vector<Digest>& digests, const std::vector<Digest>& touches) {
+    // Everything under one lock, and the writers finished only afterwards:
+    // whoever waits on a put handle then sees the batch's final LRU order.
+    std::vector<std::shared_ptr<detail::PutState>> writers;
+    {
+        std::lock_guard lock(mu_);
+        for (const auto& d : digests) {
+            auto it = index_.find(d);
+            if (it == index_.end() || it->second.state != Entry::State::writing) continue;
+            writers.push_back(std::move(it->second.writer));
+            it->second.state = Entry::State::present;
+            touch(it->second);
+        }
+        for (const auto& d : touches) {
+            auto it = index_.find(d);
+            if (it != index_.end()) touch(it->second);
+        }
     }
+    for (auto& w : writers)
+        if (w) finish(w, Status::success());
 }
 
 void TieredStore::commit_write(const Digest& digest, const Status& status) {

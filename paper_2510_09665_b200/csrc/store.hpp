@@ -121,14 +121,15 @@ public:
     };
     // `touch_order` receives the digests in the order the reference's writes
     // touch them (new writes, repeated puts, already-present puts); replay it
-    // with touch_in_order() once the batch's bytes landed.
+    // with commit_batch() once the batch's bytes landed.
     std::vector<Result<SlotWrite>> begin_write_batch(
         const std::vector<WriteSpec>& specs,
         const std::unordered_map<Digest, uint32_t, DigestHasher>& own_shares,
         std::vector<Digest>* touch_order = nullptr);
-    // LRU touch of every listed entry still indexed, in order. Safe to call
-    // from a CUDA host callback.
-    void touch_in_order(const std::vector<Digest>& digests);
+    // A whole store batch landed: every written entry becomes present, the
+    // touch order is replayed, and only then are the put handles finished.
+    // Safe to call from a CUDA host callback.
+    void commit_batch(const std::vector<Digest>& digests, const std::vector<Digest>& touches);
     // Marks the entry present (ok) or drops the claim (error). Safe to call
     // from a CUDA host callback (no CUDA API calls inside).
     void commit_write(const Digest& digest, const Status& status);

@@ -458,3 +458,44 @@ def sc_degenerate_prompts(factory, C):
 
 
 ALL += [sc_degenerate_prompts]
+
+
+def sc_api_errors(factory, C):
+    """Error behaviour of the connector calls (connector.cpp:239-392,
+    434-497): layer out of range, a store wait before its start, surplus
+    store starts, decode on an unplanned query, finish of an unknown query."""
+    e = factory(**CONN, ram_slots=16, num_pages=64)
+    prompt = make_prompt(70, 31)
+    e.seed_store(prompt, 32)
+    out = {"match": e.get_num_new_matched_tokens(7, prompt)}
+    e.bind_pages(7, 70)
+    out["upd"] = e.update_state_after_alloc(7, 5, 2)
+    m = e.build_connector_meta([(7, prompt)])
+    out["start_load"] = e.start_load_kv(m)
+    out["wait_load_out_of_range"] = e.wait_load_kv(m, e.num_layers)
+    out["wait_store_out_of_range"] = e.wait_store_kv(m, e.num_layers)
+    out["wait_store_not_started"] = e.wait_store_kv(m, 0)
+    loaded = e.loaded_tokens(m, 7)
+    starts = []
+    for layer in range(e.num_layers):
+        assert e.wait_load_kv(m, layer) == 0
+        if hasattr(e, "stream_handle"):
+            e.compute_range(7, prompt, loaded, 70, layers=(layer, layer + 1))
+        else:
+            e.compute_range(7, prompt, loaded, 70)
+        starts.append(e.start_store_kv(m))
+    starts.append(e.start_store_kv(m))  # one more than there are layers
+    out["starts"] = starts
+    out["final_wait"] = e.wait_store_kv(m, e.num_layers - 1)
+    out["final_wait_again"] = e.wait_store_kv(m, e.num_layers - 1)
+    out["results"] = [(d.hex(), c) for d, c in e.store_results(m, 7)]
+    out["pages_ok"] = pages_equal_synth(e, 7, prompt, 70, C)
+    out["decode_unplanned"] = e.begin_decode(12345)
+    out["finish_unknown"] = e.finish_query(999)
+    out["finish"] = e.finish_query(7)
+    e.release_query(7)
+    e.close()
+    return out
+
+
+ALL += [sc_api_errors]
