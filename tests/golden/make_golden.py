@@ -80,7 +80,7 @@ def main():
         json.dump({"note": "payloads: np.random.default_rng(8).integers(0, 256, size=n) in order", "cases": q8},
                   f, indent=1)
     C = oracle.C()
-    sc = {fn.__name__: json.loads(json.dumps(fn(oracle.RefEngine, C))) for fn in S.ALL}
+    sc = {fn.__name__: json.loads(json.dumps(fn(S.ref_factory, C))) for fn in S.ALL}
     with open(os.path.join(HERE, "scenarios.json"), "w") as f:
         json.dump(sc, f, indent=1)
     print("wrote keys.json synth.json scenarios.json")

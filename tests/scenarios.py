@@ -15,6 +15,16 @@ import numpy as np
 CONN = dict(num_layers=4, bpt=64, page_tokens=16, tag="conn-test", chunk_size=32)
 
 
+def ref_factory(**kw):
+    """The reference engine as the parity oracle: one store I/O thread and one
+    connector I/O thread, so its puts apply in batch_put order. With several
+    threads its write_tier tasks race for slots and the LRU victims of an
+    overfull batch vary from run to run (observed on a 16-core host); the
+    sequential order is the one its code states (store.cpp:500-506)."""
+    import oracle
+    return oracle.RefEngine(**kw, io_threads=1, store_io_threads=1)
+
+
 def make_prompt(n: int, seed: int, vocab: int = 32000) -> np.ndarray:
     rng = np.random.default_rng(seed)
     return rng.integers(0, vocab, size=n, dtype=np.uint32)

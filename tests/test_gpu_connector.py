@@ -19,7 +19,7 @@ GOLDEN = os.path.join(os.path.dirname(__file__), "golden", "scenarios.json")
 def _ref_outcome(name, C):
     import oracle
     if oracle.ref_available():
-        return json.loads(json.dumps(getattr(S, name)(oracle.RefEngine, C)))
+        return json.loads(json.dumps(getattr(S, name)(S.ref_factory, C)))
     with open(GOLDEN) as f:
         return json.load(f)[name]
 

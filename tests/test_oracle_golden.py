@@ -139,7 +139,7 @@ def test_fixtures_regenerate_identically(Ref, name):
             g = json.load(f)
         C = oracle.C()
         for fn in S.ALL:
-            assert json.loads(json.dumps(fn(oracle.RefEngine, C))) == g[fn.__name__], fn.__name__
+            assert json.loads(json.dumps(fn(S.ref_factory, C))) == g[fn.__name__], fn.__name__
     else:
         with open(os.path.join(GOLDEN, "keys.json")) as f:
             g = json.load(f)
