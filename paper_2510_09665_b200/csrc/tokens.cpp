@@ -42,7 +42,7 @@ double now_us() {
 // Caller holds mu_. Returns the memo view for this launch (slots == nullptr
 // without a memo).
 MemoView KeyHasher::stage_locked(const std::vector<TokenSpanView>& seqs, const std::vector<Digest>* parents,
-                                 size_t total_tokens, size_t total_chunks, HashParams& p) {
+                                 size_t total_tokens, size_t total_chunks, size_t max_inserts, HashParams& p) {
     // Tokens, chain descriptors and digests live in mapped pinned memory and
     // move by SM loads/stores, so a lookup never queues on the copy engines
     // behind in-flight KV transfers.
@@ -78,8 +78,10 @@ MemoView KeyHasher::stage_locked(const std::vector<TokenSpanView>& seqs, const s
     std::fill(bad, bad + seqs.size(), ~0u);
     MemoView m = memo_;
     if (memo_.slots) {
-        if (memo_used_bound_ + total_chunks > memo_.entry_cap) memo_reset_locked();
-        memo_used_bound_ += total_chunks;
+        // memo_used_bound_ bounds the links inserted so far; resetting here,
+        // before the probe, never invalidates a hit this call relies on.
+        if (memo_used_bound_ + max_inserts > memo_.entry_cap) memo_reset_locked();
+        memo_used_bound_ += max_inserts;
         d_hit_.reserve(total_chunks * sizeof(uint32_t));
         d_keys_.reserve(total_chunks * sizeof(unsigned long long));
         d_first_.reserve(seqs.size() * sizeof(uint32_t));
@@ -148,7 +150,7 @@ std::vector<std::vector<Digest>> KeyHasher::hash(const std::vector<TokenSpanView
     std::vector<std::vector<Digest>> out(seqs.size());
     if (total_chunks == 0) return out;
     HashParams p;
-    MemoView m = stage_locked(seqs, parents, total_tokens, total_chunks, p);
+    MemoView m = stage_locked(seqs, parents, total_tokens, total_chunks, total_chunks, p);
     const double t_packed = trace_lookup() ? now_us() : 0;
     // Run the chains writing digests to HBM, then verify memo hits and
     // publish every digest to the mapped result buffer.
@@ -196,7 +198,8 @@ std::vector<std::vector<Digest>> KeyHasher::hash_prefix(const std::vector<TokenS
     std::vector<std::vector<Digest>> out(n_chains);
     if (total_chunks == 0) return out;
     HashParams p;
-    MemoView m = stage_locked(seqs, nullptr, total_tokens, total_chunks, p);
+    // the first launch inserts at most one link per chain
+    MemoView m = stage_locked(seqs, nullptr, total_tokens, total_chunks, n_chains, p);
     const auto* d_tok = reinterpret_cast<const uint32_t*>(d_tokens_.ptr);
     const auto* d_ch = reinterpret_cast<const ChainDesc*>(d_chains_.ptr);
     auto* first = reinterpret_cast<uint32_t*>(h_first_.host);
@@ -261,6 +264,9 @@ std::vector<std::vector<Digest>> KeyHasher::hash_prefix(const std::vector<TokenS
         MemoView ins = m;  // insert the new links under their full-prefix keys
         ins.first_miss = nullptr;
         ins.max_rows = 0;  // the descriptors bound the rows
+        // no reset mid-call (the hits above point into the memo): links past
+        // the capacity are simply not inserted (memo_insert checks it)
+        for (const auto& x : more) memo_used_bound_ += (x.n_tokens + chunk_size_ - 1) / chunk_size_;
         TKV_CUDA(launch_hash_chains(d_tok, d_ch + n_chains, uint32_t(more.size()), p, d_out_.ptr, stream_,
                                     memo_.slots ? &ins : nullptr));
         TKV_CUDA(launch_memo_verify(d_tok, d_ch, uint32_t(n_chains), uint32_t(total_chunks), p, d_out_.ptr,

@@ -77,7 +77,7 @@ public:
 private:
     void memo_reset_locked();
     MemoView stage_locked(const std::vector<TokenSpanView>& seqs, const std::vector<Digest>* parents,
-                          size_t total_tokens, size_t total_chunks, HashParams& p);
+                          size_t total_tokens, size_t total_chunks, size_t max_inserts, HashParams& p);
     void rehash_bad_locked(size_t n_chains, size_t total_chunks, const HashParams& p);
     std::string tag_;
     size_t chunk_size_;

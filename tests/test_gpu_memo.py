@@ -152,3 +152,22 @@ def test_memo_batch_with_empty_and_single_token_prompts(tkv, C):
             e.release_query(q)
     assert e.memo_stats()["rehashes"] == 0
     e.close()
+
+
+def test_prefix_lookups_do_not_fill_the_memo(tkv, C):
+    """A lookup inserts at most one link per chain (the first absent chunk),
+    so many lookups of one stored document under new questions keep the memo
+    warm: no reset, and every lookup still matches the whole document."""
+    from paper_2510_09665_b200.api import Engine
+    e = Engine(num_layers=1, bpt=64, page_tokens=16, tag=TAG, chunk_size=256, ram_slots=48, num_pages=64,
+               memo_entries=256)
+    rng = np.random.default_rng(9)
+    doc = rng.integers(0, 128256, size=256 * 40, dtype=np.uint32)
+    e.seed_store(doc, len(doc))
+    for q in range(100):  # 100 lookups x 41 chunks would overflow a 256-entry bound 16 times
+        p = np.concatenate([doc, rng.integers(0, 128256, 60, dtype=np.uint32)])
+        assert e.get_num_new_matched_tokens(q + 1, p) == len(doc)
+        e.finish_query(q + 1)
+    st = e.memo_stats()
+    assert st["resets"] == 0 and st["hits"] >= 99 * 40
+    e.close()
