@@ -184,6 +184,7 @@ std::vector<std::vector<Digest>> KeyHasher::hash(const std::vector<TokenSpanView
 
 std::vector<std::vector<Digest>> KeyHasher::hash_prefix(const std::vector<TokenSpanView>& seqs,
                                                         const PresentPrefix& present) {
+    const double t_in = trace_lookup() ? now_us() : 0;
     std::lock_guard lock(mu_);
     TKV_CUDA(cudaSetDevice(device_));
     const size_t n_chains = seqs.size();
@@ -200,6 +201,7 @@ std::vector<std::vector<Digest>> KeyHasher::hash_prefix(const std::vector<TokenS
     HashParams p;
     // the first launch inserts at most one link per chain
     MemoView m = stage_locked(seqs, nullptr, total_tokens, total_chunks, n_chains, p);
+    const double t_packed = trace_lookup() ? now_us() : 0;
     const auto* d_tok = reinterpret_cast<const uint32_t*>(d_tokens_.ptr);
     const auto* d_ch = reinterpret_cast<const ChainDesc*>(d_chains_.ptr);
     auto* first = reinterpret_cast<uint32_t*>(h_first_.host);
@@ -216,7 +218,10 @@ std::vector<std::vector<Digest>> KeyHasher::hash_prefix(const std::vector<TokenS
                                 memo_.slots ? &m : nullptr, h_out_.dev,
                                 reinterpret_cast<unsigned int*>(h_bad_.dev), stream_));
     if (memo_.slots) TKV_CUDA(launch_sm_copy(d_first_.ptr, h_first_.dev, n_chains * sizeof(uint32_t), stream_));
+    const double t_launched = trace_lookup() ? now_us() : 0;
     TKV_CUDA(cudaStreamSynchronize(stream_));
+    const double t_synced = trace_lookup() ? now_us() : 0;
+    int passes = 0;
     for (size_t i = 0; i < n_chains; ++i) {
         const size_t f = memo_.slots ? size_t(first[i]) : 0;
         known[i] = std::min(rows[i], f + 1);
@@ -253,6 +258,7 @@ std::vector<std::vector<Digest>> KeyHasher::hash_prefix(const std::vector<TokenS
             which.push_back(i);
         }
         if (more.empty()) break;
+        ++passes;
         std::vector<ChainDesc> all(ch, ch + n_chains);
         all.insert(all.end(), more.begin(), more.end());
         h_chains_.reserve(all.size() * sizeof(ChainDesc));
@@ -279,6 +285,10 @@ std::vector<std::vector<Digest>> KeyHasher::hash_prefix(const std::vector<TokenS
         }
     }
     for (size_t i = 0; i < n_chains; ++i) out[i] = digests_of(i, known[i]);
+    if (trace_lookup())
+        std::fprintf(stderr, "[tkv prefix] chains=%zu rows=%zu pack=%.1fus launch=%.1fus device+sync=%.1fus "
+                     "passes=%d rest=%.1fus\n", n_chains, total_chunks, t_packed - t_in, t_launched - t_packed,
+                     t_synced - t_launched, passes, now_us() - t_synced);
     return out;
 }
 
