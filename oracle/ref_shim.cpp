@@ -353,6 +353,60 @@ size_t ref_store_clear(void* h, const uint8_t* digest) {
 
 size_t ref_store_entries(void* h) { return static_cast<RefEngine*>(h)->store->stats().entries; }
 
+// Direct RAM-tier operations (store.hpp:153-171) for the store op-soup
+// parity test: put of a caller payload ([L][T][bpt]), pin, get_layer, clear
+// with its refused count, and the RAM slot statistics.
+int ref_store_put(void* h, const uint8_t* digest, uint32_t token_count, const uint8_t* payload, size_t n,
+                  int pin) {
+    auto* e = static_cast<RefEngine*>(h);
+    const auto& m = e->store->config().model;
+    ChunkKey key;
+    std::memcpy(key.digest.data(), digest, 32);
+    key.model_tag = m.model_tag;
+    KVChunkBuilder b(key, token_count, m.num_layers, m.bytes_per_token_per_layer);
+    const size_t lb = size_t(token_count) * m.bytes_per_token_per_layer;
+    if (n != lb * m.num_layers) return int(Errc::size_mismatch);
+    for (uint32_t l = 0; l < m.num_layers; ++l) b.set_layer(l, ByteSpan(payload + l * lb, lb));
+    const auto& r = e->store->put(std::move(b).seal(), {TierId::ram()}, pin != 0).wait();
+    for (const auto& t : r.tiers)
+        if (!t.status.ok()) return int(t.status.code);
+    return 0;
+}
+
+int ref_store_pin(void* h, const uint8_t* digest, int on) {
+    Digest d;
+    std::memcpy(d.data(), digest, 32);
+    return int(static_cast<RefEngine*>(h)->store->pin(d, TierId::ram(), on != 0).code);
+}
+
+int ref_store_get_layer(void* h, const uint8_t* digest, uint32_t layer, uint8_t* out, size_t cap, size_t* n) {
+    Digest d;
+    std::memcpy(d.data(), digest, 32);
+    auto r = static_cast<RefEngine*>(h)->store->get_layer(d, layer);
+    *n = 0;
+    if (!r.ok()) return int(r.code());
+    *n = r.value().size();
+    if (out && r.value().size() <= cap) std::memcpy(out, r.value().data(), r.value().size());
+    return 0;
+}
+
+int ref_store_clear_n(void* h, const uint8_t* digest, size_t* removed, size_t* refused) {
+    Digest d;
+    std::memcpy(d.data(), digest, 32);
+    const auto r = static_cast<RefEngine*>(h)->store->clear({d});
+    *removed = r.removed;
+    *refused = r.refused;
+    return 0;
+}
+
+void ref_store_stats(void* h, size_t out[4]) {
+    const auto s = static_cast<RefEngine*>(h)->store->stats();
+    out[0] = s.entries;
+    out[1] = s.ram_slots_total;
+    out[2] = s.ram_slots_used;
+    out[3] = s.ram_entries;
+}
+
 // Store chunk payloads synthesized for prompt[0, n) (test_connector.cpp:71-99).
 int ref_seed_store(void* h, const uint32_t* prompt, size_t n) {
     auto* e = static_cast<RefEngine*>(h);

@@ -72,6 +72,11 @@ class _Ref:
             "ref_store_get": (_sz, [_vp, _u8p, _u8p, _sz]),
             "ref_store_clear": (_sz, [_vp, _u8p]),
             "ref_store_entries": (_sz, [_vp]),
+            "ref_store_put": (ct.c_int, [_vp, _u8p, ct.c_uint32, _u8p, _sz, ct.c_int]),
+            "ref_store_pin": (ct.c_int, [_vp, _u8p, ct.c_int]),
+            "ref_store_get_layer": (ct.c_int, [_vp, _u8p, ct.c_uint32, _u8p, _sz, ct.POINTER(_sz)]),
+            "ref_store_clear_n": (ct.c_int, [_vp, _u8p, ct.POINTER(_sz), ct.POINTER(_sz)]),
+            "ref_store_stats": (None, [_vp, ct.POINTER(_sz)]),
             "ref_seed_store": (ct.c_int, [_vp, _u32p, _sz]),
             "ref_staging_peak": (ct.c_int64, [_vp]),
             "ref_staging_refs": (ct.c_int64, [_vp]),
@@ -330,6 +335,37 @@ class RefEngine:
 
     def store_entries(self) -> int:
         return int(self.lib.ref_store_entries(self.h))
+
+    def store_put(self, digest: bytes, token_count: int, payload: np.ndarray, pin: bool = False) -> int:
+        d, p = np.frombuffer(digest, np.uint8).copy(), np.ascontiguousarray(payload, dtype=np.uint8)
+        return int(self.lib.ref_store_put(self.h, d.ctypes.data_as(_u8p), token_count, p.ctypes.data_as(_u8p),
+                                          p.size, int(pin)))
+
+    def store_pin(self, digest: bytes, on: bool) -> int:
+        d = np.frombuffer(digest, np.uint8).copy()
+        return int(self.lib.ref_store_pin(self.h, d.ctypes.data_as(_u8p), int(on)))
+
+    def store_get_layer(self, digest: bytes, layer: int):
+        d = np.frombuffer(digest, np.uint8).copy()
+        n = _sz(0)
+        rc = self.lib.ref_store_get_layer(self.h, d.ctypes.data_as(_u8p), layer, None, 0, ct.byref(n))
+        if rc:
+            return int(rc), None
+        out = np.zeros(n.value, np.uint8)
+        self.lib.ref_store_get_layer(self.h, d.ctypes.data_as(_u8p), layer, out.ctypes.data_as(_u8p), n.value,
+                                     ct.byref(n))
+        return 0, out
+
+    def store_clear_n(self, digest: bytes):
+        d = np.frombuffer(digest, np.uint8).copy()
+        removed, refused = _sz(0), _sz(0)
+        self.lib.ref_store_clear_n(self.h, d.ctypes.data_as(_u8p), ct.byref(removed), ct.byref(refused))
+        return removed.value, refused.value
+
+    def store_stats(self):
+        out = (_sz * 4)()
+        self.lib.ref_store_stats(self.h, out)
+        return tuple(int(x) for x in out)
 
     def staging_peak(self) -> int:
         return int(self.lib.ref_staging_peak(self.h))

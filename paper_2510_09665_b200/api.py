@@ -389,9 +389,42 @@ class Engine:
         return removed.value
 
     def store_entries(self) -> int:
+        return self.store_stats()[0]
+
+    # direct RAM-tier operations (same names and returns as oracle.RefEngine)
+    def store_put(self, digest: bytes, token_count: int, payload: np.ndarray, pin: bool = False) -> int:
+        d, p = _u8(digest), np.ascontiguousarray(payload, dtype=np.uint8)
+        return int(self.L.tkv_store_put(self.store, d.ctypes.data_as(u8p), token_count, p.ctypes.data_as(u8p),
+                                        p.size, int(pin)))
+
+    def store_pin(self, digest: bytes, on: bool) -> int:
+        return int(self.L.tkv_store_pin(self.store, _u8(digest).ctypes.data_as(u8p), int(on)))
+
+    def store_get_layer(self, digest: bytes, layer: int):
+        """(code, layer bytes or None)."""
+        self.synchronize()
+        d = _u8(digest)
+        n = ct.c_size_t(0)
+        rc = self.L.tkv_store_get_layer(self.store, d.ctypes.data_as(u8p), layer, None, 0, ct.byref(n))
+        if rc:
+            return int(rc), None
+        out = np.zeros(n.value, np.uint8)
+        check(self.L.tkv_store_get_layer(self.store, d.ctypes.data_as(u8p), layer, out.ctypes.data_as(u8p),
+                                         n.value, ct.byref(n)))
+        return 0, out
+
+    def store_clear_n(self, digest: bytes):
+        """(removed, refused)."""
+        d = _u8(digest)
+        removed, refused = ct.c_size_t(0), ct.c_size_t(0)
+        check(self.L.tkv_store_clear(self.store, d.ctypes.data_as(u8p), 1, ct.byref(removed), ct.byref(refused)))
+        return removed.value, refused.value
+
+    def store_stats(self):
+        """(entries, ram_slots_total, ram_slots_used, ram_entries)."""
         out = (ct.c_size_t * 4)()
         check(self.L.tkv_store_stats(self.store, out))
-        return int(out[0])
+        return tuple(int(x) for x in out)
 
     def layout(self) -> PagedLayoutC:
         L = PagedLayoutC()

@@ -312,7 +312,11 @@ Result<std::vector<uint8_t>> TieredStore::get(const Digest& digest) {
 }
 
 Result<std::vector<uint8_t>> TieredStore::get_layer(const Digest& digest, uint32_t layer) {
-    if (layer >= cfg_.model.num_layers) return Status{Errc::invalid_argument, "layer out of range"};
+    // store.cpp:654-680: an absent chunk is not_found before the layer is
+    // checked; a present one with a bad layer is invalid_argument (untouched)
+    if (layer >= cfg_.model.num_layers)
+        return contains(digest) ? Status{Errc::invalid_argument, "layer out of range"}
+                                : Status{Errc::not_found, "no such chunk"};
     auto r = acquire(digest, 0);
     if (!r.ok()) return r.status();
     const size_t lb = size_t(r.value().token_count) * cfg_.model.bytes_per_token_per_layer;

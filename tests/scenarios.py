@@ -509,3 +509,51 @@ def sc_api_errors(factory, C):
 
 
 ALL += [sc_api_errors]
+
+
+def _store_op_soup(factory, seed: int, n_ops: int, ram_slots: int, n_keys: int):
+    """Sequential random RAM-tier operations straight on the store
+    (test_store.cpp: put/get round trips, duplicate puts, LRU eviction that
+    spares pinned entries and reports tier_full when stuck, clear refusing
+    pinned copies, pin of an absent key, per-layer reads). Every result is
+    logged; payloads by digest."""
+    import hashlib
+    e = factory(num_layers=3, bpt=24, page_tokens=16, tag="soup", chunk_size=32, ram_slots=ram_slots,
+                num_pages=16)
+    rng = np.random.default_rng(seed)
+    keys = [rng.integers(0, 256, 32, dtype=np.uint8).tobytes() for _ in range(n_keys)]
+    h = (lambda b: None if b is None else hashlib.sha256(b.tobytes()).hexdigest()[:16])
+    log = []
+    for _ in range(n_ops):
+        k = keys[int(rng.integers(n_keys))]
+        op = int(rng.integers(8))
+        if op <= 2:
+            tc = int(rng.choice([32, 32, 32, 17, 1]))
+            pay = rng.integers(0, 256, 3 * tc * 24, dtype=np.uint8)
+            log.append(("put", tc, e.store_put(k, tc, pay, bool(rng.random() < 0.15))))
+        elif op == 3:
+            log.append(("get", h(e.store_get(k))))
+        elif op == 4:
+            layer = int(rng.integers(4))  # 3 = out of range
+            code, b = e.store_get_layer(k, layer)
+            log.append(("get_layer", layer, code, h(b)))
+        elif op == 5:
+            log.append(("pin", e.store_pin(k, bool(rng.random() < 0.6))))
+        elif op == 6:
+            log.append(("clear", *e.store_clear_n(k)))
+        else:
+            log.append(("contains", e.contains(k), *e.store_stats()))
+    log.append(("final", *e.store_stats()))
+    e.close()
+    return log
+
+
+def sc_store_op_soup(factory, C):
+    """RAM-tier op soup: 6 and 3 slots over 12 and 8 keys (evictions, pinned
+    slots, tier_full), one and two slots, and a roomy tier."""
+    return [_store_op_soup(factory, 1, 400, 6, 12), _store_op_soup(factory, 2, 400, 3, 8),
+            _store_op_soup(factory, 3, 300, 64, 12), _store_op_soup(factory, 4, 300, 1, 5),
+            _store_op_soup(factory, 5, 300, 2, 6)]
+
+
+ALL += [sc_store_op_soup]

@@ -159,6 +159,53 @@ def test_gather_checks(tkv):
     e.close()
 
 
+def test_alloc_pages_atomic_and_conserving(tkv):
+    """test_kv_core.cpp:98-133 — a failed allocation hands out nothing, the
+    pool is conserved across alloc/release, concurrent holders get distinct
+    page ids."""
+    from paper_2510_09665_b200._lib import u32p
+    e = _engine(tkv, 4, 64, 10)
+    L = e.L
+    assert L.tkv_pages_free_count(e.pages) == 10
+    a = np.zeros(6, np.uint32)
+    assert L.tkv_pages_alloc(e.pages, 1, 6, a.ctypes.data_as(u32p)) == 0
+    assert L.tkv_pages_free_count(e.pages) == 4 and L.tkv_pages_allocated_count(e.pages) == 6
+    big = np.zeros(5, np.uint32)
+    assert L.tkv_pages_alloc(e.pages, 2, 5, big.ctypes.data_as(u32p)) == 3  # out_of_pages
+    assert L.tkv_pages_free_count(e.pages) == 4  # nothing handed out on failure
+    b = np.zeros(4, np.uint32)
+    assert L.tkv_pages_alloc(e.pages, 2, 4, b.ctypes.data_as(u32p)) == 0
+    assert L.tkv_pages_free_count(e.pages) == 0
+    assert L.tkv_pages_release(e.pages, 1) == 6 and L.tkv_pages_free_count(e.pages) == 6
+    L.tkv_pages_release(e.pages, 2)
+    assert L.tkv_pages_free_count(e.pages) == 10 and L.tkv_pages_allocated_count(e.pages) == 0
+    c, d = np.zeros(5, np.uint32), np.zeros(5, np.uint32)
+    assert L.tkv_pages_alloc(e.pages, 3, 5, c.ctypes.data_as(u32p)) == 0
+    assert L.tkv_pages_alloc(e.pages, 4, 5, d.ctypes.data_as(u32p)) == 0
+    assert len(set(c.tolist()) | set(d.tolist())) == 10
+    # admit (SimEngine::admit) is all-or-nothing too
+    assert e.bind_pages(5, 16) == 3 and L.tkv_pages_free_count(e.pages) == 0
+    e.close()
+
+
+def test_layer_page_table_roundtrip(tkv):
+    """test_kv_core.cpp:191-205 — bind_layer / layer_pages per (query, layer);
+    unbound layers and unknown queries are empty; release clears them."""
+    from paper_2510_09665_b200._lib import u32p
+    e = _engine(tkv, 4, 64, 32)
+    L = e.L
+    ids = np.zeros(8, np.uint32)
+    assert L.tkv_pages_alloc(e.pages, 5, 8, ids.ctypes.data_as(u32p)) == 0
+    l0, l1 = ids[:4].copy(), ids[4:].copy()
+    assert L.tkv_pages_bind_layer(e.pages, 5, 0, l0.ctypes.data_as(u32p), 4) == 0
+    assert L.tkv_pages_bind_layer(e.pages, 5, 1, l1.ctypes.data_as(u32p), 4) == 0
+    assert np.array_equal(e.layer_pages(5, 0), l0) and np.array_equal(e.layer_pages(5, 1), l1)
+    assert e.layer_pages(5, 3).size == 0 and e.layer_pages(6, 0).size == 0
+    L.tkv_pages_release(e.pages, 5)
+    assert e.layer_pages(5, 0).size == 0
+    e.close()
+
+
 def _multi_layer_case(tkv, C, bpt, L, spans, seed, ppt=0):
     """K1 then K2 over random page tables for several chunk descriptors and
     all layers in ONE launch each, checked against the oracle's per-page
