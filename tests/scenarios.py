@@ -557,3 +557,87 @@ def sc_store_op_soup(factory, C):
 
 
 ALL += [sc_store_op_soup]
+
+
+def _protocol_fuzz(factory, C, seed: int):
+    """Serving iterations with protocol slips mixed in, every return code
+    logged (connector.cpp:71-164, 239-392): allocation updates with wrong
+    block counts before the right one, a second lookup of a query with a
+    different prompt, queries planned without a lookup or without an
+    allocation update, out-of-range and early waits, surplus store starts,
+    finish of unknown queries."""
+    rng = np.random.default_rng(seed)
+    e = factory(**CONN, ram_slots=12, num_pages=1024)
+    docs = [make_prompt(int(rng.integers(40, 160)), 3000 + 10 * seed + i) for i in range(3)]
+    log = []
+    qid = 500
+    for _ in range(10):
+        batch = []
+        for _ in range(int(rng.integers(1, 4))):
+            d = docs[int(rng.integers(0, len(docs)))]
+            cut = int(rng.integers(1, len(d) + 1))
+            p = np.concatenate([d[:cut], make_prompt(int(rng.integers(0, 30)), int(rng.integers(1 << 30)))])
+            batch.append((qid, p.astype(np.uint32)))
+            qid += 1
+        rec = {}
+        slip = {q: int(rng.integers(0, 6)) for q, _ in batch}
+        matched = {}
+        for q, p in batch:
+            if slip[q] == 1:  # looked up once with another prompt first
+                rec[f"pre{q}"] = e.get_num_new_matched_tokens(q, make_prompt(len(p) + 7, q))
+            matched[q] = e.get_num_new_matched_tokens(q, p) if slip[q] != 2 else None
+        for q, p in batch:
+            e.bind_pages(q, len(p))
+            ext = (matched[q] or 0) + 15
+            ext //= 16
+            blocks = (len(p) + 15) // 16
+            if slip[q] == 3:  # wrong counts first
+                rec[f"bad_ext{q}"] = e.update_state_after_alloc(q, blocks, ext + 1)
+                if blocks:
+                    rec[f"bad_blocks{q}"] = e.update_state_after_alloc(q, max(0, ext - 1), ext)
+            if slip[q] != 4:
+                rec[f"upd{q}"] = e.update_state_after_alloc(q, blocks, ext)
+        m = e.build_connector_meta(batch)
+        rec["plans"] = [plan_view(e, m, i) for i in range(len(batch))]
+        rec["start_load"] = e.start_load_kv(m)
+        layerwise = e.meta_layerwise(m)
+        rec["early_store_wait"] = e.wait_store_kv(m, 0)
+        rec["wait_load_oob"] = e.wait_load_kv(m, e.num_layers + int(rng.integers(0, 3)))
+        for layer in range(e.num_layers):
+            if layerwise:
+                rec[f"wl{layer}"] = e.wait_load_kv(m, layer)
+            for q, p in batch:
+                lo = e.loaded_tokens(m, q)
+                if hasattr(e, "stream_handle"):
+                    e.compute_range(q, p, lo, len(p), layers=(layer, layer + 1))
+                else:
+                    e.compute_range(q, p, lo, len(p))
+            if layerwise:
+                if layer > 0:
+                    rec[f"ws{layer - 1}"] = e.wait_store_kv(m, layer - 1)
+                rec[f"ss{layer}"] = e.start_store_kv(m)
+        if layerwise:
+            if rng.random() < 0.3:
+                rec["surplus_start"] = e.start_store_kv(m)
+            rec["final"] = e.wait_store_kv(m, e.num_layers - 1)
+        else:
+            rec["blocking_store"] = e.start_store_kv(m)
+        rec["loaded"] = [e.loaded_tokens(m, q) for q, _ in batch]
+        rec["pages_ok"] = [pages_equal_synth(e, q, p, len(p), C) for q, p in batch]
+        rec["results"] = [[(d.hex(), c) for d, c in e.store_results(m, q)] for q, _ in batch]
+        rec["finish_unknown"] = e.finish_query(qid + 1000)
+        rec["finish"] = [e.finish_query(q) for q, _ in batch]
+        rec["finish_again"] = [e.finish_query(q) for q, _ in batch]
+        for q, _ in batch:
+            e.release_query(q)
+        rec["entries"] = e.store_entries()
+        log.append(rec)
+    e.close()
+    return log
+
+
+def sc_protocol_fuzz(factory, C):
+    return [_protocol_fuzz(factory, C, seed) for seed in (1, 2, 3, 4)]
+
+
+ALL += [sc_protocol_fuzz]
