@@ -77,3 +77,39 @@ def test_export_matches_reference_and_import_roundtrip(tkv, C, Ref):
     g = Engine(num_layers=2, bpt=64, page_tokens=16, tag=TAG, chunk_size=32, ram_slots=8, num_pages=64)
     assert lib.tkv_store_import_record(g.store, rec.ctypes.data_as(u8p), rec.size, 0) == 16
     g.close()
+
+
+def test_record_bit_flips_match_reference_parse(tkv, C, Ref):
+    """Every single-bit flip of the header, the trailing checksum and sampled
+    payload bytes: import into the tier fails exactly when the reference's
+    parse_chunk_record (chunk_file.cpp:47-95) rejects the record, with the
+    same Errc; an accepted record stores the payload the reference parsed."""
+    from paper_2510_09665_b200._lib import u8p
+    from paper_2510_09665_b200.api import Engine
+    lib = tkv.lib()
+    prompt = S.make_prompt(40, 9)
+    keys = C.chunk_keys(prompt, 32, TAG)
+    payload = C.synth_chunk(C.model_seed(TAG), prompt, 32, 8, 4, 64)  # the 8-token tail chunk
+    rec = Ref.encode_record(TAG, keys[1], 8, 4, 64, payload)
+    rng = np.random.default_rng(5)
+    positions = list(range(54)) + list(range(rec.size - 8, rec.size)) + \
+        sorted(rng.choice(np.arange(54, rec.size - 8), 40, replace=False).tolist())
+    e = Engine(num_layers=4, bpt=64, page_tokens=16, tag=TAG, chunk_size=32, ram_slots=4, num_pages=64)
+    accepted = 0
+    for pos in positions:
+        for bit in (0, 3, 7):
+            bad = rec.copy()
+            bad[pos] ^= np.uint8(1 << bit)
+            want, back = Ref.parse_record(bad, payload.size)
+            got = lib.tkv_store_import_record(e.store, bad.ctypes.data_as(u8p), bad.size, 0)
+            assert got == want, (pos, bit, got, want)
+            if got == 0:  # accepted: stored under the record's digest, bytes as parsed
+                dig = np.zeros(32, np.uint8)
+                geo = (ct.c_uint32 * 3)()
+                th = ct.c_uint64(0)
+                assert lib.tkv_record_peek(bad.ctypes.data_as(u8p), bad.size, dig.ctypes.data_as(u8p), geo,
+                                           ct.byref(th)) == 0
+                assert np.array_equal(e.store_get(dig.tobytes()), back)
+                e.store_clear(dig.tobytes())
+                accepted += 1
+    e.close()
