@@ -641,3 +641,79 @@ def sc_protocol_fuzz(factory, C):
 
 
 ALL += [sc_protocol_fuzz]
+
+
+def _prefill(e, C, q, p, extra):
+    """One query through a full layerwise (or blocking) iteration, pages for
+    len(p) + extra tokens."""
+    mt = e.get_num_new_matched_tokens(q, p)
+    n_all = len(p) + extra
+    e.bind_pages(q, n_all)
+    rc = e.update_state_after_alloc(q, (n_all + 15) // 16, (mt + 15) // 16)
+    m = e.build_connector_meta([(q, p)])
+    transfer(e, m, q, p)
+    out = {"matched": mt, "upd": rc, "loaded": e.loaded_tokens(m, q),
+           "res": [(d.hex(), c) for d, c in e.store_results(m, q)]}
+    e.drop_meta(m)
+    return out
+
+
+def _decode_fuzz(factory, C, seed: int):
+    """Decode storing (connector.cpp:434-497) with several queries decoding
+    interleaved and protocol slips: begin twice, append before begin or
+    after finish, finish twice. Logs every code, the flushed keys and the
+    stored bytes of every flushed chunk."""
+    import hashlib
+    rng = np.random.default_rng(seed)
+    e = factory(**CONN, ram_slots=32, num_pages=2048)
+    log = []
+    qs = {}
+    for i in range(4):
+        q = 900 + i
+        p = make_prompt(int(rng.integers(1, 100)), 4000 + 10 * seed + i)
+        log.append(("prefill", q, _prefill(e, C, q, p, 90)))
+        qs[q] = {"p": p, "gen": [], "state": "prefilled"}
+    for _ in range(260):
+        q = 900 + int(rng.integers(0, 4))
+        s = qs[q]
+        r = rng.random()
+        if s["state"] == "prefilled" and r > 0.3:
+            r = 0.0  # mostly begin a prefilled query; sometimes slip an append first
+        if r < 0.06:
+            log.append(("begin", q, e.begin_decode(q)))
+            if s["state"] == "prefilled":
+                s["state"] = "decoding"
+        elif r < 0.09:
+            keys, rc = e.finish_query_keys(q)
+            log.append(("finish", q, rc, [k.hex() for k in keys]))
+            s["state"] = "finished"
+        else:
+            tok = int(rng.integers(0, 32000))
+            if s["state"] == "decoding" and len(s["gen"]) < 90:
+                full = np.concatenate([s["p"], np.array(s["gen"] + [tok], np.uint32)]).astype(np.uint32)
+                pos = len(full) - 1
+                e.compute_range(q, full, pos, pos + 1)
+                rc = e.append_decode(q, tok)
+                if rc == 0:
+                    s["gen"].append(tok)
+                log.append(("append", q, rc))
+            elif s["state"] != "decoding":
+                log.append(("append_slip", q, e.append_decode(q, tok)))
+    for q, s in qs.items():
+        keys, rc = e.finish_query_keys(q)
+        log.append(("final_finish", q, rc, [k.hex() for k in keys]))
+    # every chunk the decode flushed: its bytes in the tier
+    h = (lambda b: None if b is None else hashlib.sha256(b.tobytes()).hexdigest()[:16])
+    flushed = sorted({k for x in log if x[0] in ("finish", "final_finish") for k in x[-1]})
+    log.append(("stored", [(k[:16], h(e.store_get(bytes.fromhex(k)))) for k in flushed]))
+    for q in qs:
+        e.release_query(q)
+    e.close()
+    return log
+
+
+def sc_decode_fuzz(factory, C):
+    return [_decode_fuzz(factory, C, seed) for seed in (1, 2, 3)]
+
+
+ALL += [sc_decode_fuzz]
