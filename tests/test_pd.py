@@ -151,3 +151,40 @@ def test_pd_two_process_gloo(tkv):
     assert rc == 0
     assert firsts == [256 * i for i in range(9)]
     assert addrs == [4096 * i for i in range(9)]
+
+
+def _random_pd_sequence(rng):
+    """Registrations (sometimes twice), pushes of shuffled ordinals with
+    duplicates, several or no final flags, ordinals past the final, pushes
+    for unknown queries; every query is cancelled before it is awaited (an
+    incomplete await blocks by contract), and some are re-registered after."""
+    seq = []
+    qs = [int(q) for q in rng.choice(50, size=int(rng.integers(1, 4)), replace=False)]
+    for q in qs:
+        seq.append(("reg", q))
+        if rng.random() < 0.2:
+            seq.append(("reg", q))
+    for _ in range(int(rng.integers(0, 14))):
+        q = qs[int(rng.integers(len(qs)))] if rng.random() < 0.9 else 100 + int(rng.integers(5))
+        seq.append(("push", q, int(rng.integers(0, 8)), bool(rng.random() < 0.2)))
+    for q in qs:
+        seq.append(("cancel", q))
+        seq.append(("await", q))
+        if rng.random() < 0.3:
+            seq += [("reg", q), ("push", q, 0, True), ("await", q)]
+    return seq
+
+
+def test_pd_staging_random_sequences_match_reference(tkv):
+    """300 random push/cancel sequences through both PdStaging
+    implementations, every return code and every awaited ordinal list equal."""
+    import numpy as np
+    if _ref_pd() is None:
+        pytest.skip("oracle/_ref not built")
+    rng = np.random.default_rng(2510)
+    for i in range(300):
+        seq = _random_pd_sequence(rng)
+        s, *ours = _ours()
+        h, *ref = _reference()
+        assert _run_sequence(*ours, seq) == _run_sequence(*ref, seq), (i, seq)
+        _ref_pd().ref_pd_destroy(h)
