@@ -280,12 +280,21 @@ std::vector<size_t> Connector::get_num_new_matched_tokens(
     const size_t cs = store_.config().chunk_size;
     static const bool trace = std::getenv("TKV_TRACE_LOOKUP") != nullptr;
     const auto t0 = std::chrono::steady_clock::now();
+    // The query state keeps a copy of each prompt; it is made while the
+    // lookup's first launch runs (pooled buffers, swapped in below).
+    std::vector<std::vector<TokenId>> staged(ids.size());
+    {
+        std::lock_guard lock(mu_);
+        for (size_t q = 0; q < ids.size(); ++q) recycle_prompt_into(staged[q], prompts[q].size());
+    }
     // LPM (tokens.cpp:59-69): the chain only as far as the first absent
     // chunk, like the reference's lookup; the leading present chunks are
     // probed under one store lock per query. Planning completes the chain.
-    auto digests = hasher_.hash_prefix(prompts, [this](const std::vector<Digest>& d) {
-        return store_.present_prefix(d);
-    });
+    auto digests = hasher_.hash_prefix(
+        prompts, [this](const std::vector<Digest>& d) { return store_.present_prefix(d); },
+        [&] {
+            for (size_t q = 0; q < ids.size(); ++q) staged[q].assign(prompts[q].begin(), prompts[q].end());
+        });
     const auto t1 = std::chrono::steady_clock::now();
     std::vector<size_t> out(ids.size());
     for (size_t q = 0; q < ids.size(); ++q) {
@@ -299,8 +308,8 @@ std::vector<size_t> Connector::get_num_new_matched_tokens(
         const size_t matched = std::min(lpm, cap);
         std::lock_guard lock(mu_);
         QueryState& qs = queries_[ids[q]];
-        if (qs.prompt.capacity() < prompts[q].size()) recycle_prompt_into(qs.prompt, prompts[q].size());
-        qs.prompt.assign(prompts[q].begin(), prompts[q].end());
+        std::swap(qs.prompt, staged[q]);
+        recycle_prompt(std::move(staged[q]));
         qs.keys = std::move(keys);
         qs.lpm = lpm;
         qs.matched = matched;

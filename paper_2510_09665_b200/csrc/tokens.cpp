@@ -183,7 +183,8 @@ std::vector<std::vector<Digest>> KeyHasher::hash(const std::vector<TokenSpanView
 }
 
 std::vector<std::vector<Digest>> KeyHasher::hash_prefix(const std::vector<TokenSpanView>& seqs,
-                                                        const PresentPrefix& present) {
+                                                        const PresentPrefix& present,
+                                                        const std::function<void()>& while_waiting) {
     const double t_in = trace_lookup() ? now_us() : 0;
     std::lock_guard lock(mu_);
     TKV_CUDA(cudaSetDevice(device_));
@@ -197,7 +198,10 @@ std::vector<std::vector<Digest>> KeyHasher::hash_prefix(const std::vector<TokenS
         total_chunks += rows[i];
     }
     std::vector<std::vector<Digest>> out(n_chains);
-    if (total_chunks == 0) return out;
+    if (total_chunks == 0) {
+        if (while_waiting) while_waiting();
+        return out;
+    }
     HashParams p;
     // the first launch inserts at most one link per chain
     MemoView m = stage_locked(seqs, nullptr, total_tokens, total_chunks, n_chains, p);
@@ -218,6 +222,7 @@ std::vector<std::vector<Digest>> KeyHasher::hash_prefix(const std::vector<TokenS
                                 memo_.slots ? &m : nullptr, h_out_.dev,
                                 reinterpret_cast<unsigned int*>(h_bad_.dev), stream_));
     if (memo_.slots) TKV_CUDA(launch_sm_copy(d_first_.ptr, h_first_.dev, n_chains * sizeof(uint32_t), stream_));
+    if (while_waiting) while_waiting();
     const double t_launched = trace_lookup() ? now_us() : 0;
     TKV_CUDA(cudaStreamSynchronize(stream_));
     const double t_synced = trace_lookup() ? now_us() : 0;

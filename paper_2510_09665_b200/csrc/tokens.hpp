@@ -55,9 +55,12 @@ public:
     // absent chunk. `present(d)` returns how many leading digests of d are
     // stored. Memo hits come from the parallel probe (verified); past them
     // one SHA chunk decides, and only a present one continues the chain.
+    // `while_waiting` (optional) runs on the calling thread while the first
+    // launch is in flight (the caller's own host work, off the critical path).
     using PresentPrefix = std::function<size_t(const std::vector<Digest>&)>;
     std::vector<std::vector<Digest>> hash_prefix(const std::vector<TokenSpanView>& seqs,
-                                                 const PresentPrefix& present);
+                                                 const PresentPrefix& present,
+                                                 const std::function<void()>& while_waiting = {});
 
     // Launch counters (tests assert the once-per-query property).
     uint64_t launches() const { return launches_; }
