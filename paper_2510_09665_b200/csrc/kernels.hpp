@@ -117,6 +117,7 @@ struct MemoView {
     uint32_t entry_words = 0;             // 17 + chunk_size
     unsigned long long* stats = nullptr;  // [0] hits, [1] misses (optional)
     uint32_t max_rows = 0;                // hash at most this many rows per chain (0 = all)
+    uint32_t* first_miss_out = nullptr;   // verify also publishes first_miss here (mapped host)
 };
 
 // With a memo whose first_miss is set: probes every row of every chain in

@@ -582,6 +582,9 @@ memo_verify_kernel(const uint32_t* __restrict__ tokens, const ChainDesc* __restr
                    unsigned int* __restrict__ first_bad) {
     const uint32_t lane = threadIdx.x & 31;
     const uint32_t row = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    if (M.first_miss_out != nullptr)  // publish the probe's first misses (saves a copy launch)
+        for (uint32_t c = blockIdx.x * blockDim.x + threadIdx.x; c < n_chains; c += gridDim.x * blockDim.x)
+            M.first_miss_out[c] = M.first_miss[c];
     if (row >= total_rows) return;
     const uint32_t dw = lane < 8 ? reinterpret_cast<const uint32_t*>(dev_out + 32ull * row)[lane] : 0u;
     if (lane < 8) reinterpret_cast<uint32_t*>(out + 32ull * row)[lane] = dw;

@@ -218,10 +218,11 @@ std::vector<std::vector<Digest>> KeyHasher::hash_prefix(const std::vector<TokenS
     //    tokens.cpp:59-69), the hits verified exactly, all in one round trip.
     m.max_rows = 1;
     TKV_CUDA(launch_hash_chains(d_tok, d_ch, uint32_t(n_chains), p, d_out_.ptr, stream_, &m));
+    MemoView vm = m;
+    vm.first_miss_out = reinterpret_cast<uint32_t*>(h_first_.dev);
     TKV_CUDA(launch_memo_verify(d_tok, d_ch, uint32_t(n_chains), uint32_t(total_chunks), p, d_out_.ptr,
-                                memo_.slots ? &m : nullptr, h_out_.dev,
+                                memo_.slots ? &vm : nullptr, h_out_.dev,
                                 reinterpret_cast<unsigned int*>(h_bad_.dev), stream_));
-    if (memo_.slots) TKV_CUDA(launch_sm_copy(d_first_.ptr, h_first_.dev, n_chains * sizeof(uint32_t), stream_));
     if (while_waiting) while_waiting();
     const double t_launched = trace_lookup() ? now_us() : 0;
     TKV_CUDA(cudaStreamSynchronize(stream_));
