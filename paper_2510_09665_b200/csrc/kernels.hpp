@@ -138,6 +138,11 @@ cudaError_t launch_sm_copy(const void* src, void* dst, uint64_t bytes, cudaStrea
 cudaError_t launch_memo_stage(const uint32_t* src, uint32_t* dst, const ChainDesc* chains, uint32_t n_chains,
                               uint32_t total_rows, const HashParams& params, const MemoView& memo,
                               cudaStream_t stream);
+// Same, taking the descriptors from mapped host memory and staging them into
+// chains_dev in the same launch (a separate copy only for > 128 chains).
+cudaError_t launch_memo_stage_chains(const uint32_t* src, uint32_t* dst, const ChainDesc* chains_host,
+                                     ChainDesc* chains_dev, uint32_t n_chains, uint32_t total_rows,
+                                     const HashParams& params, const MemoView& memo, cudaStream_t stream);
 // Verifies every memo hit of a launch against its entry and publishes all
 // digest rows from dev_out to out; first_bad[chain] = first failed chunk.
 cudaError_t launch_memo_verify(const uint32_t* tokens, const ChainDesc* chains, uint32_t n_chains,

@@ -475,12 +475,32 @@ __device__ __forceinline__ uint32_t chain_of_row(const ChainDesc* __restrict__ c
 // Memo pass 1, one warp per row of every chain: copies the row's tokens from
 // the mapped host buffer into HBM (the copy the plain path does with
 // stage_words_kernel) and writes the row's chunk fingerprint to keys[row].
+// With chains_dst set, `chains` is the mapped host copy of at most
+// kStageChains descriptors: every block reads them once into shared memory
+// and block 0 also stages them into chains_dst for the later passes (one
+// copy launch fewer per lookup).
+constexpr uint32_t kStageChains = 128;
+
 __global__ void __launch_bounds__(128)
 memo_fingerprint_kernel(const uint32_t* __restrict__ src, uint32_t* __restrict__ dst,
                         const ChainDesc* __restrict__ chains, uint32_t n_chains, uint32_t total_rows,
-                        const HashParams P, const MemoView M) {
+                        const HashParams P, const MemoView M, ChainDesc* __restrict__ chains_dst) {
+    __shared__ ChainDesc s_chains[kStageChains];
     const uint32_t lane = threadIdx.x & 31;
     const uint32_t row = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    if (chains_dst != nullptr) {
+        const uint32_t words = n_chains * uint32_t(sizeof(ChainDesc) / 4);
+        const uint32_t* cs = reinterpret_cast<const uint32_t*>(chains);
+        uint32_t* sm = reinterpret_cast<uint32_t*>(s_chains);
+        uint32_t* gd = reinterpret_cast<uint32_t*>(chains_dst);
+        for (uint32_t i = threadIdx.x; i < words; i += blockDim.x) {
+            const uint32_t w = cs[i];
+            sm[i] = w;
+            if (blockIdx.x == 0) gd[i] = w;
+        }
+        __syncthreads();
+        chains = s_chains;
+    }
     if (row >= total_rows) return;
     const ChainDesc& cd = chains[chain_of_row(chains, n_chains, row)];
     const uint32_t k = row - cd.out_first;
@@ -658,7 +678,23 @@ cudaError_t launch_memo_stage(const uint32_t* src, uint32_t* dst, const ChainDes
     if (total_rows == 0) return cudaSuccess;
     note_launch();
     const uint32_t blocks = (total_rows * 32 + 127) / 128;
-    memo_fingerprint_kernel<<<blocks, 128, 0, s>>>(src, dst, chains, n_chains, total_rows, params, memo);
+    memo_fingerprint_kernel<<<blocks, 128, 0, s>>>(src, dst, chains, n_chains, total_rows, params, memo, nullptr);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_memo_stage_chains(const uint32_t* src, uint32_t* dst, const ChainDesc* chains_host,
+                                     ChainDesc* chains_dev, uint32_t n_chains, uint32_t total_rows,
+                                     const HashParams& params, const MemoView& memo, cudaStream_t s) {
+    if (n_chains > kStageChains) {  // too many to stage per block: copy them first
+        cudaError_t e = launch_sm_copy(chains_host, chains_dev, n_chains * sizeof(ChainDesc), s);
+        if (e != cudaSuccess) return e;
+        return launch_memo_stage(src, dst, chains_dev, n_chains, total_rows, params, memo, s);
+    }
+    if (total_rows == 0) return launch_sm_copy(chains_host, chains_dev, n_chains * sizeof(ChainDesc), s);
+    note_launch();
+    const uint32_t blocks = (total_rows * 32 + 127) / 128;
+    memo_fingerprint_kernel<<<blocks, 128, 0, s>>>(src, dst, chains_host, n_chains, total_rows, params, memo,
+                                                    chains_dev);
     return cudaGetLastError();
 }
 

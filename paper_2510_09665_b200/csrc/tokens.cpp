@@ -90,14 +90,16 @@ MemoView KeyHasher::stage_locked(const std::vector<TokenSpanView>& seqs, const s
         m.keys = reinterpret_cast<unsigned long long*>(d_keys_.ptr);
         m.first_miss = reinterpret_cast<uint32_t*>(d_first_.ptr);
     }
-    TKV_CUDA(launch_sm_copy(h_chains_.dev, d_chains_.ptr, ch_bytes, stream_));
-    if (memo_.slots)  // staging + per-row fingerprints in one pass
-        TKV_CUDA(launch_memo_stage(reinterpret_cast<const uint32_t*>(h_tokens_.dev),
-                                   reinterpret_cast<uint32_t*>(d_tokens_.ptr),
-                                   reinterpret_cast<const ChainDesc*>(d_chains_.ptr), uint32_t(seqs.size()),
-                                   uint32_t(total_chunks), p, m, stream_));
-    else
+    if (memo_.slots) {  // descriptors + token staging + per-row fingerprints in one pass
+        TKV_CUDA(launch_memo_stage_chains(reinterpret_cast<const uint32_t*>(h_tokens_.dev),
+                                          reinterpret_cast<uint32_t*>(d_tokens_.ptr),
+                                          reinterpret_cast<const ChainDesc*>(h_chains_.dev),
+                                          reinterpret_cast<ChainDesc*>(d_chains_.ptr), uint32_t(seqs.size()),
+                                          uint32_t(total_chunks), p, m, stream_));
+    } else {
+        TKV_CUDA(launch_sm_copy(h_chains_.dev, d_chains_.ptr, ch_bytes, stream_));
         TKV_CUDA(launch_sm_copy(h_tokens_.dev, d_tokens_.ptr, tok_bytes, stream_));
+    }
     return m;
 }
 

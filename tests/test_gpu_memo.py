@@ -171,3 +171,28 @@ def test_prefix_lookups_do_not_fill_the_memo(tkv, C):
     st = e.memo_stats()
     assert st["resets"] == 0 and st["hits"] >= 99 * 40
     e.close()
+
+
+@pytest.mark.parametrize("n_queries", [127, 129, 300])
+def test_memo_many_chains_one_launch(tkv, C, n_queries):
+    """Lookups and planning over more chains than the fingerprint pass stages
+    per block (128): descriptors come through the separate copy, keys still
+    equal the oracle's; below the limit they are staged in the same launch."""
+    from paper_2510_09665_b200.api import Engine
+    e = Engine(num_layers=1, bpt=16, page_tokens=16, tag=TAG, chunk_size=32, ram_slots=4, num_pages=20000)
+    rng = np.random.default_rng(n_queries)
+    doc = rng.integers(0, 128256, size=32 * 6, dtype=np.uint32)
+    prompts = [np.concatenate([doc[:int(rng.integers(0, len(doc)))],
+                               rng.integers(0, 128256, size=int(rng.integers(0, 70)), dtype=np.uint32)])
+               for _ in range(n_queries)]
+    ids = list(range(1, n_queries + 1))
+    e.lookup_batch(ids, prompts)
+    for q, p in zip(ids, prompts):
+        e.bind_pages(q, max(1, len(p)))
+        e.update_state_after_alloc(q, (len(p) + 15) // 16, 0)
+    m = e.build_connector_meta(list(zip(ids, prompts)))
+    for i, p in enumerate(prompts):
+        sp, _ = e.plan(m, i, "store")
+        assert [d for _, _, _, _, d in sp] == C.chunk_keys(p, 32, TAG), i
+    e.drop_meta(m)
+    e.close()
