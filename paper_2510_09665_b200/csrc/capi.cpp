@@ -499,11 +499,7 @@ int tkv_model_tag_hash(const char* tag, uint64_t* out) {
 int tkv_store_export_record(tkv_store* s, const uint8_t* digest, uint64_t tag_hash, uint8_t* out,
                             size_t cap, size_t* n) {
     return guard([&] {
-        auto r = s->s->export_record(to_digest(digest), tag_hash);
-        if (!r.ok()) return st(r.status());
-        *n = r.value().size();
-        if (out && r.value().size() <= cap) std::memcpy(out, r.value().data(), r.value().size());
-        return 0;
+        return st(s->s->export_record_into(to_digest(digest), tag_hash, out, cap, n));
     });
 }
 int tkv_store_import_record(tkv_store* s, const uint8_t* record, size_t n, int pin) {

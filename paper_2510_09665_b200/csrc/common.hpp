@@ -102,6 +102,27 @@ inline uint64_t fnv1a64(const uint8_t* p, size_t n, uint64_t h = 0xcbf29ce484222
     return h;
 }
 
+// fnv1a64 of src while copying it to dst: the checksum is a serial chain of
+// one multiply per byte, so the 8-byte loads and stores ride under it for free.
+inline uint64_t fnv1a64_copy(uint8_t* dst, const uint8_t* src, size_t n, uint64_t h = 0xcbf29ce484222325ull) {
+    size_t i = 0;
+    for (; i + 8 <= n; i += 8) {
+        uint64_t w;
+        std::memcpy(&w, src + i, 8);
+        std::memcpy(dst + i, &w, 8);
+        for (int b = 0; b < 8; ++b) {
+            h ^= (w >> (8 * b)) & 0xffu;
+            h *= 0x100000001b3ull;
+        }
+    }
+    for (; i < n; ++i) {
+        dst[i] = src[i];
+        h ^= src[i];
+        h *= 0x100000001b3ull;
+    }
+    return h;
+}
+
 // Layout of the KV a model produces (model.hpp:11-33).
 struct ModelSpec {
     uint32_t num_layers = 8;

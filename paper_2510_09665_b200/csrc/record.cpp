@@ -35,6 +35,21 @@ std::vector<uint8_t> encode_record(const RecordInfo& info, const uint8_t* payloa
     return out;
 }
 
+size_t encode_record_into(const RecordInfo& info, const uint8_t* payload, size_t n, uint8_t* out) {
+    auto le = [&](size_t off, uint64_t v, size_t bytes) {
+        for (size_t i = 0; i < bytes; ++i) out[off + i] = uint8_t(v >> (8 * i));
+    };
+    std::memcpy(out, "LMCK", 4);
+    le(4, kRecordVersion, 2);
+    le(6, info.model_tag_hash, 8);
+    std::memcpy(out + 14, info.digest.data(), 32);
+    le(46, info.token_count, 2);
+    le(48, info.num_layers, 2);
+    le(50, info.bytes_per_token, 4);
+    le(kRecordHeaderBytes + n, fnv1a64_copy(out + kRecordHeaderBytes, payload, n), 8);
+    return record_bytes(n);
+}
+
 Result<RecordInfo> peek_record(const uint8_t* b, size_t n) {
     if (n < kRecordHeaderBytes) return Status{Errc::corrupt_chunk, "record shorter than header"};
     if (std::memcmp(b, "LMCK", 4) != 0) return Status{Errc::corrupt_chunk, "bad magic"};

@@ -31,6 +31,10 @@ struct RecordInfo {
 };
 
 std::vector<uint8_t> encode_record(const RecordInfo& info, const uint8_t* payload, size_t n);
+// Record bytes for an n-byte payload, and the encoder writing straight into
+// a caller buffer of at least that size (payload copy fused with the checksum).
+inline size_t record_bytes(size_t n) { return kRecordHeaderBytes + n + 8; }
+size_t encode_record_into(const RecordInfo& info, const uint8_t* payload, size_t n, uint8_t* out);
 // Header only (chunk_file.cpp:27-50): corrupt_chunk on short / bad magic /
 // bad version / empty geometry.
 Result<RecordInfo> peek_record(const uint8_t* bytes, size_t n);

@@ -392,6 +392,22 @@ Result<std::vector<uint8_t>> TieredStore::export_record(const Digest& digest, ui
     return rec;
 }
 
+Status TieredStore::export_record_into(const Digest& digest, uint64_t tag_hash, uint8_t* out, size_t cap,
+                                      size_t* n) {
+    auto r = acquire(digest, 0);
+    if (!r.ok()) return r.status();
+    RecordInfo info;
+    info.digest = digest;
+    info.model_tag_hash = tag_hash;
+    info.token_count = uint16_t(r.value().token_count);
+    info.num_layers = uint16_t(cfg_.model.num_layers);
+    info.bytes_per_token = cfg_.model.bytes_per_token_per_layer;
+    *n = record_bytes(info.payload_bytes());
+    if (out && cap >= *n) encode_record_into(info, r.value().host, info.payload_bytes(), out);
+    release(digest);
+    return Status::success();
+}
+
 Status TieredStore::import_record(const uint8_t* record, size_t n, bool pin) {
     const uint8_t* payload = nullptr;
     auto info = parse_record(record, n, &payload);

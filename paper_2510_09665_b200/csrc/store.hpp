@@ -161,6 +161,10 @@ public:
     // reference's disk / wire format: export a present entry as a record,
     // or import a record (checksum and geometry verified) into a slot.
     Result<std::vector<uint8_t>> export_record(const Digest& digest, uint64_t model_tag_hash);
+    // Into a caller buffer: *n = record bytes always; bytes written only when
+    // out != nullptr and cap >= *n (a size query costs no copy or checksum).
+    Status export_record_into(const Digest& digest, uint64_t model_tag_hash, uint8_t* out, size_t cap,
+                              size_t* n);
     Status import_record(const uint8_t* record, size_t n, bool pin = false);
 
 private:
