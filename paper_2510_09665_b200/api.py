@@ -118,6 +118,8 @@ class Engine:
         self._dev_prompts: dict[int, torch.Tensor] = {}
         self._host_prompts: dict[int, np.ndarray] = {}
         self._prompt_src: dict[int, object] = {}
+        self._host_tensors: dict[int, torch.Tensor] = {}
+        self._retired_hosts: list = []
         self._mism = torch.zeros(1, dtype=torch.int64, device=f"cuda:{device}")
 
     @property
@@ -161,6 +163,7 @@ class Engine:
         self._dev_prompts.pop(qid, None)
         self._host_prompts.pop(qid, None)
         self._prompt_src.pop(qid, None)
+        self._retire_host(qid)
         return self.L.tkv_pages_release(self.pages, qid)
 
     def free_page_count(self) -> int:
@@ -176,7 +179,12 @@ class Engine:
             # Pinned host copy read by an SM-driven copy kernel on the engine
             # stream: a copy-engine upload would queue behind the layerwise KV
             # transfers already in flight. The pinned buffer
-            # doubles as the host copy and lives until release_query.
+            # doubles as the host copy. A replaced buffer is retired with an
+            # event and only returned to torch's pinned cache once the copy
+            # reading it ran: torch records no use for a kernel's reads, and a
+            # recycled block refilled by the host under a pending copy would
+            # hand the engine another prompt's tokens.
+            self._retire_host(qid)
             host = torch.empty(max(1, t.size), dtype=torch.int32, pin_memory=True)
             hv = host.numpy().view(np.uint32)[:t.size]
             hv[:] = t
@@ -185,8 +193,17 @@ class Engine:
             if self.stream is not None:
                 cur.record_stream(self.stream)
             self._host_prompts[qid] = hv
+            self._host_tensors[qid] = host
             self._dev_prompts[qid] = cur
         return cur
+
+    def _retire_host(self, qid: int) -> None:
+        old = self._host_tensors.pop(qid, None)
+        if old is not None:
+            ev = torch.cuda.Event()
+            ev.record(self.stream if self.stream is not None else torch.cuda.default_stream(self.device))
+            self._retired_hosts.append((ev, old))
+        self._retired_hosts = [(e, h) for e, h in self._retired_hosts if not e.query()]
 
     def compute_range(self, qid: int, prompt, start: int, end: int, layers=None) -> None:
         """Engine compute stand-in: synth KV for [start, end) into pages (K4)."""
