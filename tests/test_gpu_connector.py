@@ -114,7 +114,8 @@ def test_decode_chunks_chain_correct(tkv, C):
 
 
 @pytest.mark.parametrize("name", ["sc_partial_match", "sc_layerwise_vs_blocking", "sc_multi_query_batch",
-                                  "sc_random_trace_evicting", "sc_random_trace_decode", "sc_degenerate_prompts"])
+                                  "sc_random_trace_evicting", "sc_random_trace_decode", "sc_degenerate_prompts",
+                                  "sc_protocol_fuzz", "sc_decode_fuzz"])
 @pytest.mark.parametrize("mode", ["load_zero_copy", "store_zero_copy", "both_zero_copy", "depth1", "depth4"])
 def test_transfer_modes_match_reference(tkv, C, name, mode):
     """The non-default host-tier paths give the reference outcome too: K2
