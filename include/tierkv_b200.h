@@ -250,7 +250,9 @@ int tkv_store_stats(tkv_store* s, size_t out[4]);
  * record (checksum + geometry verified; corrupt_chunk / invalid_argument as
  * the reference). tkv_model_tag_hash = first 8 LE bytes of SHA-256(tag)
  * (hash.cpp:41-44), computed on the device. tkv_record_peek reads the
- * header: digest, {token_count, num_layers, bytes_per_token}, tag hash. */
+ * header: digest, {token_count, num_layers, bytes_per_token}, tag hash.
+ * Export always sets *n to the record size; it writes the record only when
+ * out != NULL and cap >= *n (a size query costs no copy or checksum). */
 int tkv_model_tag_hash(const char* tag, uint64_t* out);
 int tkv_store_export_record(tkv_store* s, const uint8_t* digest, uint64_t model_tag_hash,
                             uint8_t* out, size_t cap, size_t* n);
