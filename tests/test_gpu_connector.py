@@ -167,3 +167,23 @@ def test_decode_batch_matches_oracle(tkv, C):
         e.release_query(q)
     assert e.append_decode_batch([99], [1]) == [10]  # unknown_query for a query with no open decode
     e.close()
+
+
+@pytest.mark.parametrize("name", ["sc_decode_fuzz", "sc_protocol_fuzz", "sc_random_trace_evicting"])
+def test_scenarios_with_a_late_engine_stream(tkv, C, name):
+    """The same outcomes when the engine stream runs ~1 ms behind the host
+    before every compute (a spin kernel queued ahead of the token upload and
+    the KV writes): host-side lifetime races — a buffer recycled while a
+    queued copy or kernel still reads it — show up here instead of hiding
+    behind a fast GPU (racecheck found one this way)."""
+    import torch
+    from paper_2510_09665_b200.api import Engine
+
+    class LateEngine(Engine):
+        def compute_range(self, qid, prompt, start, end, layers=None):
+            with torch.cuda.stream(self.stream if self.stream is not None else torch.cuda.default_stream()):
+                torch.cuda._sleep(2_000_000)  # ~1 ms of spinning: the GPU falls behind the host
+            super().compute_range(qid, prompt, start, end, layers)
+
+    got = json.loads(json.dumps(getattr(S, name)(LateEngine, C)))
+    assert got == _ref_outcome(name, C)
