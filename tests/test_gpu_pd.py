@@ -14,16 +14,22 @@ import scenarios as S
 pytestmark = pytest.mark.gpu
 
 
+@pytest.mark.parametrize("late", [False, True])
 @pytest.mark.parametrize("staged", [False, True])
-def test_pd_send_land_byte_exact(tkv, C, staged):
+def test_pd_send_land_byte_exact(tkv, C, staged, late):
     """staged: K1 into local staging + copy-engine peer copies in groups (the
-    group size is forced down so the 7 chunks travel as several copies)."""
+    group size is forced down so the 7 chunks travel as several copies).
+    late: the engine stream runs ~1 ms behind the host before the compute,
+    so the send, the await and the land must all be ordered by the streams,
+    not by luck."""
     from paper_2510_09665_b200.api import Engine, PdStaging, pd_land, pd_send, pd_send_staged
     spec = dict(num_layers=4, bpt=512, page_tokens=16, tag="pd-test", chunk_size=32)
     pre = Engine(**spec, ram_slots=4, num_pages=256)
     dec = Engine(**spec, ram_slots=4, num_pages=256)
     prompt = S.make_prompt(200, 71)  # 7 chunks, the last one partial (8 tokens)
     pre.bind_pages(10, 200)
+    if late:
+        torch.cuda._sleep(2_000_000)
     pre.compute_range(10, prompt, 0, 200)
     stride = 4 * 32 * 512
     landing = torch.zeros(7 * stride, dtype=torch.uint8, device="cuda")
