@@ -22,17 +22,27 @@ Reported (one JSON line, rank 0):
   roofline K1/K2 kernel: algorithmic HBM bytes (2 x payload) / launch time vs
            MEASURED_PEAKS.json hbm_gbs (fallback 6650); traffic from the
            committed ncu capture; links: PCIe measured in-run per rank.
-  cpu_baseline  the unmodified reference Connector (oracle/_ref) on the
-           same step, bounded to 8 of the 80 layers, rank 0 / N=1 only.
-  parity   the 10 GiB page image after the kernel loop, and after one more
-           (untimed) connector step, checked word by word on the device.
+  cpu_baseline  the unmodified reference Connector (oracle/_ref) on one
+           step of the same workload (all 80 layers, the full-model rows: the
+           reference has no TP, so at N GPUs it does the whole job), rank 0,
+           every N, all host cores.
+  parity   the 10 GiB page image after the kernel loop; every suffix chunk
+           the timed steps stored that is still in the tier (read from its
+           pinned slot by the SMs) against synth; and one more (untimed)
+           connector step's page image — all checked word by word on device.
+  configs  (N = 1) BASELINE.json configs 1, 2 and 4 through the same C-ABI
+           connector (tools/bench_configs.py): e2e GB/s and tokens/s, PCIe
+           fractions, device byte verification, the reference beside each.
   pd       (N >= 2) prefill rank r -> decode rank r + N/2 chunk sends over
-           NVLink, both send variants, an in-run peer-copy probe, and the
+           NVLink: SM-direct, CE-staged and NCCL send/recv variants, in-run
+           peer-copy probes (each pair alone, all pairs at once), and the
            reference's PD CPU work on a bounded sample.
 
---impl reference runs only the reference CPU path (rank 0) and prints its
-line. Inputs (64 + 64 chunks of 5 GiB each at N=1) exceed L2 (126 MB), so no
-L2 flush is needed between timed steps.
+--impl reference runs only the reference CPU path (rank 0): the unmodified
+reference Connector on the same step (all layers, full rows), one engine
+seeded once and reused across steps, with the same config dict. Inputs (64 +
+64 chunks of 5 GiB each at N=1) exceed L2 (126 MB), so no L2 flush is needed
+between timed steps.
 """
 from __future__ import annotations
 
@@ -62,8 +72,8 @@ def parse():
     ap.add_argument("--prefix", type=int, default=16384)
     ap.add_argument("--layers", type=int, default=80)
     ap.add_argument("--bpt-full", type=int, default=4096)
-    ap.add_argument("--cpu-layers", type=int, default=8, help="layers in the bounded CPU sample")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-configs", action="store_true", help="skip the configs 1/2/4 object (N=1)")
     ap.add_argument("--load-zero-copy", action="store_true")
     ap.add_argument("--store-zero-copy", action="store_true")
     ap.add_argument("--store-ctas", type=int, default=0)
@@ -113,6 +123,11 @@ def backend():
 def coll_device(dev):
     """Where collective tensors live: the GPU for NCCL, the host for gloo."""
     return dev if backend() == "nccl" else "cpu"
+
+
+def agree_loaded(loaded, device):
+    from paper_2510_09665_b200.tp import agree_loaded as agree
+    return agree(loaded, device)
 
 
 def prompt_tokens(n_prefix, n_suffix, step, vocab=128256):
@@ -196,75 +211,132 @@ class ClockSampler:
 
 # ------------------------------------------------------------ reference ----
 
-def reference_step_gbps(args, n_layers, bpt, threads):
-    """The unmodified reference Connector (oracle/_ref) on the bench step,
-    bounded to n_layers. Times only the connector calls."""
-    import oracle
-    from oracle import RefEngine
-    if not oracle.ref_available():
-        return None
-    n_pre, n = args.prefix, args.prompt
-    chunks = (n + 255) // 256
-    e = RefEngine(num_layers=n_layers, bpt=bpt, page_tokens=16, tag=TAG, chunk_size=256,
-                  ram_slots=chunks + 8, num_pages=(n // 16 + 16) * n_layers, layerwise=True,
-                  staging_budget=1 << 40, io_threads=threads, store_io_threads=threads)
-    pre = prompt_tokens(n_pre, 0, 0)
-    e.seed_store(pre, n_pre)  # prefix in the RAM tier (setup, untimed)
-    prompt = prompt_tokens(n_pre, n - n_pre, 0)
-    qid = 1
-    e.bind_pages(qid, n)
-    e.compute_range(qid, prompt, n_pre, n)  # engine compute of the new tokens (untimed)
-    t = 0.0
-    t0 = time.perf_counter()
-    matched = e.get_num_new_matched_tokens(qid, prompt)
-    blocks = (n + 15) // 16
-    e.update_state_after_alloc(qid, blocks, (matched + 15) // 16)
-    m = e.build_connector_meta([(qid, prompt)])
-    assert e.start_load_kv(m) == 0
-    for layer in range(n_layers):
-        assert e.wait_load_kv(m, layer) == 0
-        if layer:
-            assert e.wait_store_kv(m, layer - 1) == 0
-        assert e.start_store_kv(m) == 0
-    assert e.wait_store_kv(m, n_layers - 1) == 0
-    t = time.perf_counter() - t0
-    loaded = e.loaded_tokens(m, qid)
-    assert loaded == n_pre, loaded
-    stored = sum(min(256, n - s) for s in range(n_pre, n, 256))
-    moved = (loaded + stored) * n_layers * bpt
-    e.finish_query(qid)
-    e.close()
-    return {"gbps": moved / t / 1e9, "seconds": t, "bytes": moved, "tokens": loaded + stored}
+def config_dict(args, world):
+    """The workload both arms report (identical dict: same config)."""
+    bpt = args.bpt_full // world
+    return {"workload": "c3: Llama-3.1-70B KV, 80 layers, TP=N head-sharded, 32K prompt: "
+                        "16K prefix retrieve + 16K suffix store per step",
+            "prompt": args.prompt, "prefix": args.prefix, "layers": args.layers, "tp": world, "bpt": bpt,
+            "chunk": 256, "page": 16, "parallelism": f"tp{world} head-sharded, no data-path collective",
+            "l2": "inputs 10 GiB/N >> 126 MB L2, no flush"}
+
+
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return None
+
+
+class RefStep:
+    """The unmodified reference Connector (oracle/_ref, src/connector.cpp:
+    71-392) on the bench step: lookup -> update_state_after_alloc ->
+    build_connector_meta -> start_load_kv -> per layer {wait_load_kv,
+    wait_store_kv(l-1), start_store_kv} -> final wait_store_kv, timed around
+    the connector calls only. One engine is seeded once (the stored prefix)
+    and reused: the query's pages stay bound with the suffix KV computed once
+    (engine compute, untimed), and after each step the suffix chunks are
+    cleared from the tier (untimed) so the next step stores them again. Every
+    step therefore retrieves the 16K prefix and stores the 16K suffix, all
+    layers, full rows — the B200 step's bytes."""
+
+    def __init__(self, args, n_layers, bpt, threads):
+        import oracle
+        from oracle import RefEngine
+        self.ok = oracle.ref_available()
+        if not self.ok:
+            return
+        n, n_pre = args.prompt, args.prefix
+        self.n, self.n_pre, self.L, self.bpt = n, n_pre, n_layers, bpt
+        chunks = (n + 255) // 256
+        self.e = RefEngine(num_layers=n_layers, bpt=bpt, page_tokens=16, tag=TAG, chunk_size=256,
+                           ram_slots=chunks + 8, num_pages=(n // 16 + 16) * n_layers, layerwise=True,
+                           staging_budget=1 << 40, io_threads=threads, store_io_threads=threads)
+        t0 = time.perf_counter()
+        self.e.seed_store(prompt_tokens(n_pre, 0, 0), n_pre)  # the stored prefix (setup)
+        self.prompt = prompt_tokens(n_pre, n - n_pre, 0)
+        self.q = 1
+        assert self.e.bind_pages(self.q, n) == 0
+        self.e.compute_range(self.q, self.prompt, n_pre, n)  # engine compute of the new tokens
+        self.suffix_keys = oracle.C().chunk_keys(self.prompt, 256, TAG)[n_pre // 256:]
+        self.setup_s = time.perf_counter() - t0
+
+    def step(self):
+        e, q, n, L = self.e, self.q, self.n, self.L
+        t0 = time.perf_counter()
+        matched = e.get_num_new_matched_tokens(q, self.prompt)
+        assert e.update_state_after_alloc(q, (n + 15) // 16, (matched + 15) // 16) == 0
+        m = e.build_connector_meta([(q, self.prompt)])
+        assert e.start_load_kv(m) == 0
+        for layer in range(L):
+            assert e.wait_load_kv(m, layer) == 0
+            if layer:
+                assert e.wait_store_kv(m, layer - 1) == 0
+            assert e.start_store_kv(m) == 0
+        assert e.wait_store_kv(m, L - 1) == 0
+        t = time.perf_counter() - t0
+        loaded = e.loaded_tokens(m, q)
+        res = e.store_results(m, q)
+        assert loaded == self.n_pre, loaded
+        assert len(res) == len(self.suffix_keys) and all(c == 0 for _, c in res), res[:2]
+        e.drop_meta(m)
+        e.finish_query(q)
+        for k in self.suffix_keys:  # the next step stores them again
+            e.store_clear(k)
+        moved = n * L * self.bpt
+        return {"gbps": moved / t / 1e9, "seconds": t, "bytes": moved, "tokens": n}
+
+    def close(self):
+        if self.ok:
+            self.e.close()
+
+
+def all_cpus():
+    """Every CPU of the host (the reference gets all of them, whatever this
+    rank's NUMA binding)."""
+    try:
+        return set(range(os.cpu_count() or 1))
+    except Exception:
+        return os.sched_getaffinity(0)
 
 
 def run_reference(args):
     world, rank, _ = dist_env()
     if rank != 0:
         return
-    threads = os.cpu_count() or 1
-    bpt = args.bpt_full // world
-    vals, secs, bytes_ = [], [], 0
+    try:
+        os.sched_setaffinity(0, all_cpus())
+    except OSError:
+        pass
+    threads = len(os.sched_getaffinity(0))
+    ref = RefStep(args, args.layers, args.bpt_full, threads)
+    if not ref.ok:
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libtierkv_ref.so not built"}))
+        return
+    vals, secs = [], []
     for i in range(args.warmup + args.steps):
-        r = reference_step_gbps(args, args.cpu_layers, bpt, threads)
-        if r is None:
-            print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libtierkv_ref.so not built"}))
-            return
+        r = ref.step()
         if i >= args.warmup:
             vals.append(r["gbps"])
             secs.append(r["seconds"])
-            bytes_ = r["bytes"]
+    ref.close()
     v = statistics.median(vals)
-    sample = (f"{args.prompt}-token prompt ({args.prefix} stored prefix loaded + {args.prompt - args.prefix} "
-              f"new tokens stored), {args.cpu_layers} of {args.layers} layers, bpt {bpt}")
+    ms = 1e3 * statistics.median(secs)
+    sample = (f"every step the full workload: {args.prompt}-token prompt, {args.prefix}-token stored prefix "
+              f"retrieved + {args.prompt - args.prefix} tokens stored, all {args.layers} layers, full rows "
+              f"(bpt {args.bpt_full}: the reference has no TP, it does the whole {world}-GPU job); one engine "
+              f"seeded once ({ref.setup_s:.1f} s setup, untimed), suffix chunks cleared between steps")
     line = {"metric": METRIC, "value": round(v, 4), "unit": "GB/s", "impl": "reference", "n_gpus": world,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(1e3 * statistics.median(secs), 3),
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 3),
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "u8",
-            "data": "synthetic (splitmix64 KV, seeded tokens)",
-            "config": {"workload": "c3: Llama-3.1-70B KV, 80 layers, TP=N head-sharded, 32K prompt, "
-                                   "16K prefix retrieve + 16K suffix store", "prompt": args.prompt,
-                       "prefix": args.prefix, "tp": world, "bpt": bpt, "chunk": 256, "page": 16},
-            "cpu_baseline": {"value": round(v, 4), "unit": "GB/s", "cores": threads, "kind": "reference",
-                             "sample": sample},
+            "data": "synthetic (splitmix64 KV from seeded tokens)", "config": config_dict(args, world),
+            "tokens_per_s": round(args.prompt / (ms / 1e3), 1),
+            "cpu_baseline": {"value": round(v, 4), "unit": "GB/s", "cores": threads, "cpu": cpu_model(),
+                             "kind": "reference", "sample": sample},
             "e2e": {"value": round(v, 4), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -426,6 +498,8 @@ class B200Bench:
         m = e.build_connector_meta([(q, prompt)])
         assert e.start_load_kv(m) == 0
         loaded = e.loaded_tokens(m, q)
+        if self.world > 1:  # one hit length for the TP forward pass: MIN over ranks (the TP exchange)
+            loaded = agree_loaded({q: loaded}, coll_device(self.dev))[q]
         assert loaded == matched
         for layer in range(L):
             e.wait_load_kv(m, layer)
@@ -530,10 +604,25 @@ class B200Bench:
     def step_bytes(self):
         return (self.n_pre + (self.n - self.n_pre)) * self.L * self.bpt
 
-    def verify_last(self, prompt):
-        """Full-size parity: pages of the last step vs the synth oracle on
-        device, plus the stored suffix slots against the CPU oracle sample."""
-        return None
+    def verify_stored_steps(self, ks):
+        """Every suffix chunk that the steps `ks` stored and the tier still
+        holds, read from its pinned slot by the SMs and compared word by word
+        with synth of that step's tokens (this rank's row slice). Returns
+        (mismatching words, chunks verified, chunks no longer present)."""
+        from paper_2510_09665_b200.api import chunk_keys
+        mism = verified = gone = 0
+        first = self.n_pre // 256
+        for k in ks:
+            prompt = prompt_tokens(self.n_pre, self.n - self.n_pre, k + 1)
+            keys = chunk_keys(prompt, 256, TAG)
+            for i in range(first, len(keys)):
+                r = self.e.verify_stored(keys[i], prompt, 256 * i, shard_offset=self.rank * self.bpt)
+                if r is None:
+                    gone += 1
+                else:
+                    mism += r
+                    verified += 1
+        return mism, verified, gone
 
 
 def kernel_loop(bench, steps, warmup):
@@ -629,11 +718,21 @@ def kernel_loop(bench, steps, warmup):
 
 def run_pd_pairs(args, world, rank, local):
     """Config 5 (N >= 2): prefill ranks [0, N/2) send a 32K-token prompt's KV
-    (70B, TP = N/2 head shards) to decode ranks r + N/2. The prefiller's K1
-    gathers every chunk straight into the decoder's landing buffer (CUDA IPC
-    mapping -> NVLink writes); ordinals go over the process group; the decoder
-    checks the PdStaging contract, lands with one K2 and verifies the bytes
-    on device. Returns per-pair NVLink GB/s (rank 0 aggregates)."""
+    (70B, TP = N/2 head shards) to decode ranks r + N/2 (run_pd's transfer,
+    src/sim_engine.cpp:374-472, at chunk granularity). Every rank runs the
+    same phases (barriers and NCCL calls are collective):
+      1. CE-staged: K1 into local staging, copy-engine peer copies per group;
+      2. NCCL: K1 into local staging, ncclSend / ncclRecv of the payload
+         (one batch_isend_irecv group per pair; NCCL backend only);
+      3. SM-direct: K1 gathers straight into the decoder's landing buffer
+         (CUDA IPC mapping: NVLink writes by the SMs) — last, so the landed
+         bytes the decoder verifies come from it;
+      4. link probes: one plain copy-engine peer copy of 1 GiB per pair, all
+         pairs at once and each pair alone;
+      5. ordinals over the process group; the decoder checks the PdStaging
+         contract (out of order + a duplicate), lands with one K2 and
+         verifies every landed byte on device.
+    Returns every rank's result dict (rank 0 aggregates)."""
     import ctypes as ct
 
     import numpy as np
@@ -654,6 +753,7 @@ def run_pd_pairs(args, world, rank, local):
                num_pages=(n // 16 + 16) * L, device=local, shard_offset=(rank % half) * bpt)
     prompt = prompt_tokens(n, 0, 999)
     qid = 5000
+    payload = n * L * bpt  # bytes per pair
     landing = None
     handle = np.zeros(64, np.uint8)
     offset = ct.c_uint64(0)
@@ -664,6 +764,7 @@ def run_pd_pairs(args, world, rank, local):
     handles = [None] * world
     dist.all_gather_object(handles, (handle.tobytes(), offset.value))
     result = {}
+    staging = peer_ptr = None
     if prefill:
         peer_ptr = ct.c_void_p()
         h = np.frombuffer(handles[peer][0], np.uint8).copy()
@@ -673,39 +774,84 @@ def run_pd_pairs(args, world, rank, local):
         e.compute_range(qid, prompt, 0, n)  # prefill compute stand-in
         staging = torch.empty(chunks * stride, dtype=torch.uint8, device=dev)
         torch.cuda.synchronize(dev)
+    reps = 1 + args.steps
 
-        def timed(send):
-            # each send returns after its bytes landed (it synchronizes)
-            times, recs = [], None
-            for it in range(1 + args.steps):
-                torch.cuda.synchronize(dev)
-                t0 = time.perf_counter()
-                recs = send()
-                dt = time.perf_counter() - t0
-                if it:
-                    times.append(dt)
-            return min(times), recs
-        # staged (CE peer copy) first, SM-direct last: the landed bytes the
-        # decoder verifies come from the direct K1 writes.
-        t_ce, _ = timed(lambda: pd_send_staged(e, qid, n, peer_ptr.value, stride, staging.data_ptr()))
-        t_sm, recs = timed(lambda: pd_send(e, qid, n, peer_ptr.value, stride))
-        # link probe: one plain copy-engine peer copy of 1 GiB (all pairs at once)
-        probe = min(1 << 30, chunks * stride)
-
-        def raw():
-            check(lib().tkv_ce_copy(ct.c_void_p(staging.data_ptr()), ct.c_void_p(peer_ptr.value), probe, None))
+    def timed(fn):
+        """min over reps of one synchronizing call (the first is a warm-up)."""
+        times, out = [], None
+        for it in range(reps):
             torch.cuda.synchronize(dev)
-        t_link, _ = timed(raw)
+            t0 = time.perf_counter()
+            out = fn()
+            torch.cuda.synchronize(dev)
+            if it:
+                times.append(time.perf_counter() - t0)
+        return min(times), out
+
+    # 1. CE-staged (prefill ranks only; each send returns after its bytes landed)
+    if prefill:
+        result["t_ce"], _ = timed(lambda: pd_send_staged(e, qid, n, peer_ptr.value, stride, staging.data_ptr()))
+    dist.barrier()
+    # 2. NCCL send/recv of the gathered payload
+    nccl = backend() == "nccl"
+    if nccl:
+        recv_t = landing[:payload] if landing is not None else None
+        if prefill:
+            def nccl_send():
+                recs = pd_send(e, qid, n, staging.data_ptr(), stride)  # K1 into local staging
+                # staging holds chunk i at i * stride; the tail chunks are
+                # contiguous up to the last record's end
+                nbytes = (len(recs) - 1) * stride + recs[-1].bytes
+                for w in dist.batch_isend_irecv([dist.P2POp(dist.isend, staging[:nbytes], peer)]):
+                    w.wait()
+            result["t_nccl"], _ = timed(nccl_send)
+        else:
+            nbytes = (chunks - 1) * stride + (n - 256 * (chunks - 1)) * L * bpt
+            recv_t = landing[:nbytes]
+
+            def nccl_recv():
+                for w in dist.batch_isend_irecv([dist.P2POp(dist.irecv, recv_t, peer)]):
+                    w.wait()
+            timed(nccl_recv)
+    dist.barrier()
+    # 3. SM-direct (its landed bytes are the ones verified)
+    recs = None
+    if prefill:
+        result["t_sm"], recs = timed(lambda: pd_send(e, qid, n, peer_ptr.value, stride))
+    dist.barrier()
+    # 4. link probes: a plain CE peer copy of 1 GiB per pair
+    probe = min(1 << 30, chunks * stride)
+
+    def raw():
+        check(lib().tkv_ce_copy(ct.c_void_p(staging.data_ptr()), ct.c_void_p(peer_ptr.value), probe, None))
+        torch.cuda.synchronize(dev)
+    best_all = best_alone = 1e9
+    for _ in range(3):  # all pairs at once
+        dist.barrier()
+        if prefill:
+            t0 = time.perf_counter()
+            raw()
+            best_all = min(best_all, time.perf_counter() - t0)
+    for p in range(half):  # each pair alone
+        for _ in range(3):
+            dist.barrier()
+            if prefill and rank == p:
+                t0 = time.perf_counter()
+                raw()
+                best_alone = min(best_alone, time.perf_counter() - t0)
+    dist.barrier()
+    # 5. ordinals, PdStaging contract, land, verify
+    if prefill:
         meta = torch.tensor([[r.addr - peer_ptr.value, r.bytes, r.token_count, r.first_token] for r in recs],
                             dtype=torch.int64, device=coll_device(dev))
         dist.send(meta, dst=peer)
         lib().tkv_ipc_close(peer_ptr, peer_off)
-        del staging
         moved = sum(r.bytes for r in recs)
-        best = min(t_sm, t_ce)
-        result = {"pair": f"{rank}->{peer}", "gbps": moved / best / 1e9, "bytes": moved,
-                  "ms": 1e3 * best, "sm_direct_gbps": moved / t_sm / 1e9, "ce_staged_gbps": moved / t_ce / 1e9,
-                  "link_gbps": probe / t_link / 1e9}
+        best = min(result["t_sm"], result["t_ce"], result.get("t_nccl", 1e9))
+        result = {"pair": f"{rank}->{peer}", "gbps": moved / best / 1e9, "bytes": moved, "ms": 1e3 * best,
+                  "sm_direct_gbps": moved / result["t_sm"] / 1e9, "ce_staged_gbps": moved / result["t_ce"] / 1e9,
+                  "nccl_gbps": moved / result["t_nccl"] / 1e9 if "t_nccl" in result else None,
+                  "link_all_pairs_gbps": probe / best_all / 1e9, "link_alone_gbps": probe / best_alone / 1e9}
     else:
         meta = torch.zeros((chunks, 4), dtype=torch.int64, device=coll_device(dev))
         dist.recv(meta, src=peer)
@@ -730,7 +876,7 @@ def run_pd_pairs(args, world, rank, local):
     out = [None] * world
     dist.all_gather_object(out, result)
     e.close()
-    del landing
+    del landing, staging
     torch.cuda.empty_cache()
     return out
 
@@ -881,11 +1027,15 @@ def run_b200(args):
     time.sleep(0.25)  # let the sampler deliver the samples taken inside the region
     clk.__exit__()
     e2e_launches = lib_.tkv_launch_count() - launches0
+    # parity of the timed schedule itself: every suffix chunk the timed steps
+    # stored that the tier still holds, read back from its slot on device
+    ts_mism, ts_ok, ts_gone = bench.verify_stored_steps([args.warmup + k for k in range(args.steps)])
     e2e_mism, e2e_loaded = bench.verified_step(args.warmup + args.steps)  # untimed parity step
     if world > 1:
-        t = torch.tensor([float(e2e_mism)], dtype=torch.float64, device=coll_device(bench.dev))
+        t = torch.tensor([float(e2e_mism), float(ts_mism), float(ts_ok), float(ts_gone)], dtype=torch.float64,
+                         device=coll_device(bench.dev))
         dist.all_reduce(t, op=dist.ReduceOp.SUM)
-        e2e_mism = int(t.item())
+        e2e_mism, ts_mism, ts_ok, ts_gone = (int(x) for x in t.tolist())
     e2e_ms = max_over_ranks(start.elapsed_time(end) / args.steps)
     barrier()
     e2e_bytes_rank = (loaded + stored) * bench.L * bench.bpt
@@ -893,38 +1043,68 @@ def run_b200(args):
     tokens_per_s = (loaded + stored) / (e2e_ms / 1e3)
 
     pd = None
+    pd_failed = False
     if world >= 2 and world % 2 == 0 and not args.no_pd:
         try:
             res = run_pd_pairs(args, world, rank, local)
             sends = [r for r in res if "gbps" in r]
             lands = [r for r in res if "land_ms" in r]
             agg = sum(r["gbps"] for r in sends)
-            pd = {"pairs": len(sends), "per_pair_gbps": [round(r["gbps"], 1) for r in sends],
+            mism = sum(r["mismatch_words"] for r in lands)
+            nccl = [r["nccl_gbps"] for r in sends]
+            pd = {"ok": mism == 0, "pairs": len(sends), "per_pair_gbps": [round(r["gbps"], 1) for r in sends],
                   "sm_direct_gbps": [round(r["sm_direct_gbps"], 1) for r in sends],
                   "ce_staged_gbps": [round(r["ce_staged_gbps"], 1) for r in sends],
+                  "nccl_gbps": [round(x, 1) for x in nccl] if all(x is not None for x in nccl) else None,
                   "aggregate_gbps": round(agg, 1), "bytes_per_pair": sends[0]["bytes"],
-                  "land_ms": [round(r["land_ms"], 3) for r in lands],
-                  "mismatch_words": sum(r["mismatch_words"] for r in lands),
-                  "link_probe_gbps": [round(r["link_gbps"], 1) for r in sends],
-                  "nvlink_peak_gbps_per_direction": 770.0,
-                  "frac_of_peak": round(min(r["gbps"] for r in sends) / 770.0, 4),
-                  "frac_of_measured_link": round(min(r["gbps"] / r["link_gbps"] for r in sends), 4),
+                  "land_ms": [round(r["land_ms"], 3) for r in lands], "mismatch_words": mism,
+                  "link_alone_gbps": [round(r["link_alone_gbps"], 1) for r in sends],
+                  "link_all_pairs_gbps": [round(r["link_all_pairs_gbps"], 1) for r in sends],
+                  "frac_of_link_alone": round(min(r["gbps"] / r["link_alone_gbps"] for r in sends), 4),
+                  "frac_of_link_all_pairs": round(min(r["gbps"] / r["link_all_pairs_gbps"] for r in sends), 4),
+                  "link_probe": "in-run copy-engine peer copy of 1 GiB per pair (cudaMemcpyAsync over NVLink), "
+                                "best of 3, each pair alone and all pairs at once",
                   "cpu_baseline": (reference_pd_gbps(args.layers, args.bpt_full // (world // 2))
                                    if rank == 0 and not args.no_cpu_baseline else None),
-                  "path": "per pair the faster of: K1 gather straight into the peer decoder's landing buffer "
+                  "path": "per pair the fastest of: K1 gather straight into the peer decoder's landing buffer "
                           "(CUDA IPC, SM writes over NVLink) | K1 into local staging + copy-engine peer copies "
-                          "per 1 GiB group; PdStaging ordinal contract, one K2 land, bytes verified on device"}
-        except Exception as ex:  # keep the headline line even if PD fails
-            pd = {"error": repr(ex)[:300]}
+                          "per 1 GiB group | K1 into local staging + ncclSend/ncclRecv; PdStaging ordinal "
+                          "contract, one K2 land, bytes verified on device"}
+            pd_failed = mism != 0
+        except Exception as ex:  # the headline line still prints; the run then fails (rc 3)
+            pd = {"ok": False, "error": repr(ex)[:300]}
+            pd_failed = True
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+    if rank == 0 and not args.no_cpu_baseline:
+        # the reference on one step of the whole job (full rows: it has no TP),
+        # on every host core; after every timed region, rank 0 only
+        aff = os.sched_getaffinity(0)
+        try:
+            os.sched_setaffinity(0, all_cpus())
+        except OSError:
+            pass
         threads = len(os.sched_getaffinity(0))
-        r = reference_step_gbps(args, args.cpu_layers, bench.bpt, threads)
-        if r is not None:
-            cpu = {"value": round(r["gbps"], 4), "unit": "GB/s", "cores": threads, "kind": "reference",
-                   "sample": f"one step ({args.prefix}-token prefix load + {args.prompt - args.prefix}-token "
-                             f"suffix store), {args.cpu_layers} of {args.layers} layers, bpt {bench.bpt}, "
-                             f"{r['seconds']:.2f} s"}
+        ref = RefStep(args, args.layers, args.bpt_full, threads)
+        if ref.ok:
+            r = ref.step()
+            ref.close()
+            cpu = {"value": round(r["gbps"], 4), "unit": "GB/s", "cores": threads, "cpu": cpu_model(),
+                   "kind": "reference",
+                   "sample": f"one step of the same workload: {args.prefix}-token prefix retrieved + "
+                             f"{args.prompt - args.prefix} tokens stored, all {args.layers} layers, full rows "
+                             f"(bpt {args.bpt_full}, the whole {world}-GPU job), {r['seconds']:.2f} s "
+                             f"(setup {ref.setup_s:.1f} s untimed)"}
+        try:
+            os.sched_setaffinity(0, aff)
+        except OSError:
+            pass
+    configs = None
+    if world == 1 and not args.no_configs:
+        bench.e.close()  # its pinned tier and pages are not needed any more
+        torch.cuda.empty_cache()
+        sys.path.insert(0, os.path.join(ROOT, "tools"))
+        import bench_configs
+        configs = bench_configs.run_all(pcie, cpu=not args.no_cpu_baseline)
     if rank != 0:
         return
     dom_ms = max(kr["scatter_ms"], kr["gather_ms"])
@@ -937,11 +1117,7 @@ def run_b200(args):
         "metric": METRIC, "value": round(value, 2), "unit": "GB/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(e2e_ms, 3), "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "u8", "data": "synthetic (splitmix64 KV from seeded tokens, device-generated)",
-        "config": {"workload": "c3: Llama-3.1-70B KV, 80 layers, TP=N head-sharded, 32K prompt: "
-                               "16K prefix retrieve + 16K suffix store per step",
-                   "prompt": bench.n, "prefix": bench.n_pre, "layers": bench.L, "tp": world, "bpt": bench.bpt,
-                   "chunk": 256, "page": 16, "parallelism": f"tp{world} head-sharded, no data-path collective",
-                   "l2": "inputs 10 GiB/N >> 126 MB L2, no flush"},
+        "config": config_dict(args, world),
         "value_kind": "device-resident K2+K1 payload GB/s (chunk side in HBM)",
         "kernel_ms_per_step": round(k_ms, 3),
         "tokens_per_s": round(tokens_per_s, 1),
@@ -960,6 +1136,11 @@ def run_b200(args):
         "gpu_launches": int(e2e_launches),
         "kernel_launches_value": int(kr["launches"]),
         "parity": {"value_pages_mismatch_words": mism_all, "ranks_checked": world,
+                   "timed_store_mismatch_words": ts_mism, "timed_store_chunks_verified": ts_ok,
+                   "timed_store_chunks_evicted": ts_gone,
+                   "timed_store_check": "after the timed loop: every suffix chunk the timed steps stored that "
+                                        "the tier still holds (LRU evicted the rest), read from its pinned slot "
+                                        "by the SMs and compared word by word with synth of that step's tokens",
                    "e2e_pages_mismatch_words": e2e_mism,
                    "e2e_check": f"one more connector step after the timed region: {e2e_loaded}-token prefix "
                                 f"retrieved from the pinned tier + {bench.n - e2e_loaded} computed tokens, "
@@ -969,9 +1150,13 @@ def run_b200(args):
     }
     if pd is not None:
         line["pd"] = pd
+    if configs is not None:
+        line["configs"] = configs
     print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
+    if pd_failed or ts_mism or e2e_mism or mism_all:
+        sys.exit(3)  # a parity or PD failure fails the run (the line above says which)
 
 
 def main():

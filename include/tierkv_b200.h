@@ -244,6 +244,15 @@ int tkv_store_contains(tkv_store* s, const uint8_t* digest);
 int tkv_store_pin(tkv_store* s, const uint8_t* digest, int on);
 int tkv_store_clear(tkv_store* s, const uint8_t* digests, size_t n, size_t* removed,
                     size_t* refused);
+/* Device byte oracle over one tier entry (test / bench verification, not a
+ * reference API): the SMs read the chunk's pinned slot ([L][T][bpt]) over
+ * PCIe and compare it with synth for tokens [start, start + T) of tokens_dev
+ * (row slice at row_offset of the full row, TP shard), adding mismatching
+ * 8-byte words to *mismatches_dev. Returns not_found for an absent chunk;
+ * synchronizes `stream` before returning. */
+int tkv_store_verify_synth(tkv_store* s, const uint8_t* digest, const uint32_t* tokens_dev, uint64_t seed,
+                           uint32_t start, uint64_t row_offset, unsigned long long* mismatches_dev,
+                           void* stream);
 /* entries, ram_slots_total, ram_slots_used, ram_entries */
 int tkv_store_stats(tkv_store* s, size_t out[4]);
 /* LMCK records (chunk_file.hpp:12-56): export a present chunk / import a
@@ -278,6 +287,9 @@ typedef struct tkv_connector_config {
 void tkv_connector_config_default(tkv_connector_config* cfg);
 int tkv_connector_create(tkv_store* s, tkv_pages* p, const tkv_connector_config* cfg,
                          tkv_connector** out);
+/* Handles are reference-counted: a connector keeps its store and pages alive
+   and a tkv_meta keeps its connector alive, so destroy calls may come in any
+   order; the objects go when their last handle does. */
 void tkv_connector_destroy(tkv_connector* c);
 int tkv_connector_get_num_new_matched_tokens(tkv_connector* c, uint64_t query,
                                              const uint32_t* tokens, size_t n, size_t* matched);

@@ -114,6 +114,7 @@ SIGNATURES = {
     "tkv_store_pin": (ct.c_int, [vp, u8p, ct.c_int]),
     "tkv_store_clear": (ct.c_int, [vp, u8p, sz, szp, szp]),
     "tkv_store_stats": (ct.c_int, [vp, szp]),
+    "tkv_store_verify_synth": (ct.c_int, [vp, u8p, vp, ct.c_uint64, ct.c_uint32, ct.c_uint64, vp, vp]),
     "tkv_model_tag_hash": (ct.c_int, [ct.c_char_p, u64p]),
     "tkv_store_export_record": (ct.c_int, [vp, u8p, ct.c_uint64, u8p, sz, szp]),
     "tkv_store_import_record": (ct.c_int, [vp, u8p, sz, ct.c_int]),

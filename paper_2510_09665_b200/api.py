@@ -437,6 +437,22 @@ class Engine:
         check(self.L.tkv_store_clear(self.store, d.ctypes.data_as(u8p), 1, ct.byref(removed), ct.byref(refused)))
         return removed.value, refused.value
 
+    def verify_stored(self, digest: bytes, prompt, start: int, shard_offset: int = 0) -> int | None:
+        """Device byte oracle over one tier entry: mismatching 8-byte words of
+        its pinned slot against synth for tokens [start, start + T) of
+        `prompt` (the SMs read the slot over PCIe); None if absent."""
+        t = _tokens(prompt)
+        dev = torch.from_numpy(t.view(np.int32)).to(f"cuda:{self.device}")
+        d = _u8(digest)
+        self._mism.zero_()
+        self.synchronize()
+        rc = self.L.tkv_store_verify_synth(self.store, d.ctypes.data_as(u8p), dev.data_ptr(), _model_seed(self.tag),
+                                           start, shard_offset, self._mism.data_ptr(), self.stream_handle)
+        if rc == 1:  # not_found
+            return None
+        check(rc)
+        return int(self._mism.item())
+
     def store_stats(self):
         """(entries, ram_slots_total, ram_slots_used, ram_entries)."""
         out = (ct.c_size_t * 4)()

@@ -8,6 +8,7 @@
 #include <string>
 
 #include "connector.hpp"
+#include "copy_plan.hpp"
 #include "kernels.hpp"
 #include "paged_store.hpp"
 #include "pd.hpp"
@@ -29,17 +30,21 @@ static_assert(offsetof(tkv_chain_desc, n_tokens) == offsetof(ChainDesc, n_tokens
 static_assert(offsetof(tkv_chain_desc, out_first) == offsetof(ChainDesc, out_first));
 static_assert(offsetof(tkv_chain_desc, parent) == offsetof(ChainDesc, parent));
 
+// Objects are shared: a connector keeps its store and pages alive, and a
+// metadata handle keeps its connector alive, so the C caller may destroy
+// handles in any order (each destroy drops one reference).
 struct tkv_pages {
-    std::unique_ptr<PagedKVStore> p;
+    std::shared_ptr<PagedKVStore> p;
     uint64_t shard_offset = 0;  // bytes of the full KV row before this TP shard
 };
 struct tkv_store {
-    std::unique_ptr<TieredStore> s;
+    std::shared_ptr<TieredStore> s;
 };
 struct tkv_connector {
-    std::unique_ptr<Connector> c;
+    std::shared_ptr<Connector> c;
 };
 struct tkv_meta {
+    std::shared_ptr<Connector> keep;  // destroyed after m (members in reverse order)
     ConnectorMetadata m;
 };
 struct tkv_pd_staging {
@@ -148,10 +153,7 @@ int tkv_plan_tiles(const tkv_xfer_desc* descs, uint32_t n, uint32_t page_tokens,
                    uint32_t page_bytes, uint32_t ppt, uint32_t n_layers, uint32_t* tb,
                    uint32_t* ppt_out) {
     if (!page_tokens) return fail(Errc::invalid_argument, "page_tokens == 0");
-    if (ppt == 0) {
-        size_t p = 65536 / (page_bytes ? page_bytes : 1);
-        ppt = uint32_t(p < 1 ? 1 : (p > 64 ? 64 : p));
-    }
+    if (ppt == 0) ppt = pages_per_tile(page_bytes);
     tb[0] = 0;
     for (uint32_t i = 0; i < n; ++i)
         tb[i + 1] = tb[i] + tiles_for(descs[i].n_tokens, page_tokens, ppt, n_layers);
@@ -297,7 +299,7 @@ int tkv_pages_create(const tkv_model_spec* spec, uint32_t num_pages, int device,
     return guard([&] {
         if (device >= 0) TKV_CUDA(cudaSetDevice(device));
         auto* p = new tkv_pages;
-        p->p = std::make_unique<PagedKVStore>(to_spec(spec), num_pages, device);
+        p->p = std::make_shared<PagedKVStore>(to_spec(spec), num_pages, device);
         *out = p;
         return 0;
     });
@@ -432,12 +434,29 @@ int tkv_store_create(const tkv_model_spec* spec, size_t chunk_size, size_t ram_b
         cfg.chunk_size = chunk_size;
         cfg.ram_pool_bytes = ram_bytes;
         auto* s = new tkv_store;
-        s->s = std::make_unique<TieredStore>(cfg);
+        s->s = std::make_shared<TieredStore>(cfg);
         *out = s;
         return 0;
     });
 }
 void tkv_store_destroy(tkv_store* s) { delete s; }
+int tkv_store_verify_synth(tkv_store* s, const uint8_t* digest, const uint32_t* tokens_dev, uint64_t seed,
+                           uint32_t start, uint64_t row_offset, unsigned long long* mismatches_dev,
+                           void* stream) {
+    return guard([&] {
+        Digest d;
+        std::memcpy(d.data(), digest, 32);
+        auto r = s->s->acquire(d, 0);
+        if (!r.ok()) return st(r.status());
+        const auto& m = s->s->config().model;
+        cudaError_t e = launch_verify_chunk(tokens_dev, seed, start, r.value().token_count, m.num_layers,
+                                            uint32_t(m.bytes_per_token_per_layer), row_offset, r.value().dev,
+                                            mismatches_dev, cudaStream_t(stream));
+        if (e == cudaSuccess) e = cudaStreamSynchronize(cudaStream_t(stream));
+        s->s->release(d);
+        return cuda(e);
+    });
+}
 int tkv_store_put(tkv_store* s, const uint8_t* digest, uint32_t tokens, const uint8_t* payload,
                   size_t bytes, int pin) {
     return guard([&] { return st(s->s->put(to_digest(digest), tokens, payload, bytes, pin != 0).wait()); });
@@ -549,7 +568,11 @@ int tkv_connector_create(tkv_store* s, tkv_pages* p, const tkv_connector_config*
             c.memo_entries = cfg->memo_entries;
         }
         auto* h = new tkv_connector;
-        h->c = std::make_unique<Connector>(*s->s, *p->p, c);
+        // the deleter's captures release the store and pages after the connector
+        std::shared_ptr<TieredStore> store = s->s;
+        std::shared_ptr<PagedKVStore> pages = p->p;
+        h->c = std::shared_ptr<Connector>(new Connector(*store, *pages, c),
+                                          [store, pages](Connector* x) { delete x; });
         *out = h;
         return 0;
     });
@@ -584,6 +607,7 @@ int tkv_connector_build_meta(tkv_connector* c, size_t nq, const uint64_t* ids,
         auto qs = to_queries(nq, prompts, lens);
         for (size_t i = 0; i < nq; ++i) so.queries.push_back({ids[i], std::move(qs[i])});
         auto* m = new tkv_meta;
+        m->keep = c->c;
         m->m = c->c->build_connector_meta(so);
         *out = m;
         return 0;

@@ -136,6 +136,7 @@ struct BatchState {
     bool store_ce = false;         // copy-engine store path for this batch
     uint32_t store_depth = 1;
     size_t store_layer_bytes = 0;  // one staging layer
+    Connector::StagingRing* store_ring = nullptr;  // held until the stores are sealed
 
     ~BatchState() {
         // Device buffers above may still feed in-flight work: drain first.
@@ -149,7 +150,7 @@ struct BatchState {
                 // This batch's own completion only: later batches may already
                 // be queued on the same streams.
                 if (stores_sealed) {
-                    store_complete.sync();
+                    store_complete.sync();  // recorded after the commit callback: `committed` is final
                 } else {
                     TKV_CUDA(cudaStreamSynchronize(conn->store_stream_));
                     TKV_CUDA(cudaStreamSynchronize(conn->d2h_stream_));
@@ -163,6 +164,11 @@ struct BatchState {
                 }
             }
         } catch (...) {
+        }
+        if (store_ring != nullptr) {  // never sealed: the streams were drained above
+            std::lock_guard io(conn->io_mu_);
+            store_ring->owner = nullptr;
+            store_ring->used = false;
         }
     }
 };
@@ -403,7 +409,6 @@ Status Connector::enqueue_loads(BatchState& b) {
     const uint32_t L = b.num_layers;
     const uint32_t pt = model.page_tokens;
     const size_t bpt = model.bytes_per_token_per_layer;
-    const uint32_t ppt = pages_per_tile(pages_.page_bytes());
 
     // Safe prefix per query (connector.cpp:196-216): a chunk that vanished, a
     // record whose geometry differs from the plan, or pages that cannot take
@@ -455,10 +460,16 @@ Status Connector::enqueue_loads(BatchState& b) {
     std::vector<std::vector<XferDesc>> vars(zero_copy ? 1 : depth);
     if (!zero_copy) {
         b.ring_slot_bytes = layer_bytes;
-        if (size_t(depth) * layer_bytes > staging_.bytes) {
-            TKV_CUDA(cudaStreamSynchronize(h2d_stream_));  // previous batch may use the ring
-            TKV_CUDA(cudaStreamSynchronize(load_stream_));
-            staging_.reserve(ring_growth(size_t(depth) * layer_bytes, staging_.bytes, depth));
+        // One load ring: an earlier batch still holding it (its engine has
+        // not waited on every layer yet) enqueues its remaining layers first,
+        // so no two batches ever interleave in the ring.
+        if (load_ring_.owner != nullptr && load_ring_.owner != &b)
+            enqueue_load_layers(*load_ring_.owner, load_ring_.owner->num_layers);
+        if (size_t(depth) * layer_bytes > load_ring_.buf.bytes) {
+            // every earlier batch has enqueued all its layers: once the ring's
+            // last use finished, nothing reads the old buffer any more
+            if (load_ring_.used) load_ring_.free.sync();
+            load_ring_.buf.reserve(ring_growth(size_t(depth) * layer_bytes, load_ring_.buf.bytes, depth));
         }
         staging_peak_ = std::max(staging_peak_, size_t(depth) * layer_bytes);
     }
@@ -474,22 +485,22 @@ Status Connector::enqueue_loads(BatchState& b) {
                 d.chunk = reinterpret_cast<uint64_t>(it.slot.dev);
                 d.layer_stride = uint64_t(it.record_tokens) * bpt;
             } else {
-                d.chunk = reinterpret_cast<uint64_t>(staging_.ptr + v * layer_bytes + it.staging_off);
+                d.chunk = reinterpret_cast<uint64_t>(load_ring_.buf.ptr + v * layer_bytes + it.staging_off);
                 d.layer_stride = 0;
             }
             vars[v].push_back(d);
         }
     }
-    b.load_plan.build(plan_pool_, vars, pt, ppt, L, load_stream_);
+    b.load_plan.build(plan_pool_, vars, pt, pages_.page_bytes(), L, load_stream_);
     const PagedLayout layout = pages_.layout();
 
     if (zero_copy && blocking) {
-        TKV_CUDA(launch_paged_copy(layout, b.load_plan.plan(0, 0, L, ppt), CopyDir::scatter,
+        TKV_CUDA(launch_paged_copy(layout, b.load_plan.plan(0, 0, L), CopyDir::scatter,
                                    cfg_.load_ctas, load_stream_));
         for (uint32_t l = 0; l < L; ++l) b.load_done[l].record(load_stream_);
     } else if (zero_copy) {
         for (uint32_t l = 0; l < L; ++l) {
-            TKV_CUDA(launch_paged_copy(layout, b.load_plan.plan(0, l, 1, ppt), CopyDir::scatter,
+            TKV_CUDA(launch_paged_copy(layout, b.load_plan.plan(0, l, 1), CopyDir::scatter,
                                        cfg_.load_ctas, load_stream_));
             b.load_done[l].record(load_stream_);
         }
@@ -499,7 +510,8 @@ Status Connector::enqueue_loads(BatchState& b) {
         // launches layer l+1 when the engine waits for l, connector.cpp:268-279):
         // the copy engines are shared with the engine's own transfers, which
         // must not queue behind a whole prompt of loads.
-        if (ring_used_) ring_free_.wait_on(h2d_stream_);  // previous batch done with the ring
+        if (load_ring_.used) load_ring_.free.wait_on(h2d_stream_);  // previous batch done with the ring
+        load_ring_.owner = &b;
         b.loads_ce = true;
         b.load_depth = depth;
         b.load_layer_bytes = layer_bytes;
@@ -525,7 +537,6 @@ void Connector::enqueue_load_layers(BatchState& b, uint32_t upto) {
     if (!b.loads_ce) return;
     const auto& model = store_.config().model;
     const size_t bpt = model.bytes_per_token_per_layer;
-    const uint32_t ppt = pages_per_tile(pages_.page_bytes());
     const PagedLayout layout = pages_.layout();
     const size_t n = b.loads.size();
     std::vector<void*> dst(n), src(n);
@@ -540,22 +551,23 @@ void Connector::enqueue_load_layers(BatchState& b, uint32_t upto) {
         for (size_t i = 0; i < n; ++i) {
             const auto& it = b.loads[i];
             src[i] = it.slot.host + size_t(l) * it.record_tokens * bpt;
-            dst[i] = staging_.ptr + size_t(r) * b.load_layer_bytes + it.staging_off;
+            dst[i] = load_ring_.buf.ptr + size_t(r) * b.load_layer_bytes + it.staging_off;
             sizes[i] = it.span.length() * bpt;
         }
         TKV_CUDA(cudaMemcpyBatchAsync(dst.data(), src.data(), sizes.data(), n, &attr, &attr_idx, 1,
                                       &fail_idx, h2d_stream_));
         b.h2d_done[l].record(h2d_stream_);
         b.h2d_done[l].wait_on(load_stream_);
-        TKV_CUDA(launch_paged_copy(layout, b.load_plan.plan(r, l, 1, ppt), CopyDir::scatter,
+        TKV_CUDA(launch_paged_copy(layout, b.load_plan.plan(r, l, 1), CopyDir::scatter,
                                    cfg_.load_ctas, load_stream_));
         b.load_done[l].record(load_stream_);
     }
     if (upto > b.next_load) b.next_load = upto;
     if (b.next_load == b.num_layers && !b.loads_finalized) {
         b.loads_finalized = true;
-        ring_free_.record(load_stream_);
-        ring_used_ = true;
+        load_ring_.free.record(load_stream_);
+        load_ring_.used = true;
+        load_ring_.owner = nullptr;
         b.loads_released = std::make_shared<ReleaseState>();
         auto* ctx = new ReleaseCtx{&store_, {}, b.loads_released};
         for (const auto& it : b.loads) ctx->digests.push_back(it.digest);
@@ -609,7 +621,6 @@ Status Connector::reserve_stores(BatchState& b) {
     const auto& model = store_.config().model;
     const uint32_t pt = model.page_tokens;
     const size_t bpt = model.bytes_per_token_per_layer;
-    const uint32_t ppt = pages_per_tile(pages_.page_bytes());
     std::vector<XferDesc> descs;
     std::unordered_map<QueryId, PagedKVStore::DeviceTable> tables;
     // Every slot of the batch in one reservation, in the reference's
@@ -659,7 +670,7 @@ Status Connector::reserve_stores(BatchState& b) {
     b.store_ce = cfg_.store_path == StorePath::copy_engine &&
                  b.mode == TransferMode::layerwise && b.any_store_writes;
     if (!b.store_ce) {
-        b.store_plan.build(plan_pool_, {descs}, pt, ppt, b.num_layers, store_stream_);
+        b.store_plan.build(plan_pool_, {descs}, pt, pages_.page_bytes(), b.num_layers, store_stream_);
         return Status::success();
     }
     size_t off = 0;
@@ -674,33 +685,57 @@ Status Connector::reserve_stores(BatchState& b) {
     b.store_layer_bytes = off;
     b.store_depth = std::min<uint32_t>(std::max<uint32_t>(cfg_.staging_depth, 1), b.num_layers);
     const size_t need = size_t(b.store_depth) * off;
-    if (need > store_staging_.bytes) {
-        TKV_CUDA(cudaStreamSynchronize(store_stream_));  // previous batch may use the ring
-        TKV_CUDA(cudaStreamSynchronize(d2h_stream_));
-        store_staging_.reserve(ring_growth(need, store_staging_.bytes, b.store_depth));
-    }
+    StagingRing* ring = acquire_store_ring(b, need, b.store_depth);
     staging_peak_ = std::max(staging_peak_, need);
     std::vector<std::vector<XferDesc>> vars(b.store_depth, descs);
     for (uint32_t r = 0; r < b.store_depth; ++r) {
         size_t k = 0;
         for (const auto& s : b.stores) {
             if (s.w.kind != SlotWrite::Kind::write) continue;
-            vars[r][k].chunk = reinterpret_cast<uint64_t>(store_staging_.ptr + r * off + s.staging_off);
+            vars[r][k].chunk = reinterpret_cast<uint64_t>(ring->buf.ptr + r * off + s.staging_off);
             vars[r][k].layer_stride = 0;
             ++k;
         }
     }
-    b.store_plan.build(plan_pool_, vars, pt, ppt, b.num_layers, store_stream_);
+    b.store_plan.build(plan_pool_, vars, pt, pages_.page_bytes(), b.num_layers, store_stream_);
     make_events(b.gathered, b.num_layers);
     make_events(b.d2h_done, b.num_layers);
-    if (store_ring_used_) store_ring_free_.wait_on(store_stream_);
+    if (ring->used) ring->free.wait_on(store_stream_);  // the ring's previous batch finished its copies
     return Status::success();
+}
+
+// A store ring for batch b: a free one large enough, else a free one grown
+// (after its last use finished), else a new one. A ring stays with its batch
+// until the batch's last layer is enqueued (start_store_kv seals it), so two
+// batches whose stores overlap never share one. Caller holds io_mu_.
+Connector::StagingRing* Connector::acquire_store_ring(BatchState& b, size_t need, uint32_t depth) {
+    StagingRing* pick = nullptr;
+    for (auto& r : store_rings_)
+        if (r->owner == nullptr && r->buf.bytes >= need) {
+            pick = r.get();
+            break;
+        }
+    if (pick == nullptr) {
+        for (auto& r : store_rings_)
+            if (r->owner == nullptr) {
+                pick = r.get();
+                break;
+            }
+        if (pick == nullptr) {
+            store_rings_.push_back(std::make_unique<StagingRing>());
+            pick = store_rings_.back().get();
+        }
+        if (pick->used) pick->free.sync();  // its last batch's copies have finished
+        pick->buf.reserve(ring_growth(need, pick->buf.bytes, depth));
+    }
+    pick->owner = &b;
+    b.store_ring = pick;
+    return pick;
 }
 
 Status Connector::store_layers(BatchState& b, uint32_t first, uint32_t last) {
     const auto& model = store_.config().model;
     const uint32_t pt = model.page_tokens;
-    const uint32_t ppt = pages_per_tile(pages_.page_bytes());
     // Gather readability (check_readable, paged_store.cpp:94-111) per layer.
     for (uint32_t l = first; l < last; ++l)
         for (const auto& s : b.stores) {
@@ -715,8 +750,18 @@ Status Connector::store_layers(BatchState& b, uint32_t first, uint32_t last) {
     // K1 for these layers, ordered after the engine's compute of them.
     b.compute_done[first].record(cfg_.engine_stream);
     b.compute_done[first].wait_on(store_stream_);
+    // ... and after this batch's own loads of them: a slot this batch evicts
+    // may be one it is still loading (begin_write_batch), and layer l of the
+    // new chunk must not land before layer l of the old one was read. An
+    // engine that waited on wait_load_kv(l) before computing l already
+    // implies this; one that did not (or a lazy pipeline not yet enqueued
+    // that far) gets the order here.
+    if (b.loads_started && !b.loads.empty()) {
+        if (b.loads_ce && b.next_load < last) enqueue_load_layers(b, last);
+        b.load_done[last - 1].wait_on(store_stream_);
+    }
     if (!b.store_ce) {
-        TKV_CUDA(launch_paged_copy(layout, b.store_plan.plan(0, first, last - first, ppt),
+        TKV_CUDA(launch_paged_copy(layout, b.store_plan.plan(0, first, last - first),
                                    CopyDir::gather, cfg_.store_ctas, store_stream_));
         return Status::success();
     }
@@ -724,7 +769,7 @@ Status Connector::store_layers(BatchState& b, uint32_t first, uint32_t last) {
     for (uint32_t l = first; l < last; ++l) {
         const uint32_t r = l % b.store_depth;
         if (l >= b.store_depth) b.d2h_done[l - b.store_depth].wait_on(store_stream_);
-        TKV_CUDA(launch_paged_copy(layout, b.store_plan.plan(r, l, 1, ppt), CopyDir::gather,
+        TKV_CUDA(launch_paged_copy(layout, b.store_plan.plan(r, l, 1), CopyDir::gather,
                                    cfg_.load_ctas, store_stream_));
         b.gathered[l].record(store_stream_);
         b.gathered[l].wait_on(d2h_stream_);
@@ -733,7 +778,7 @@ Status Connector::store_layers(BatchState& b, uint32_t first, uint32_t last) {
         for (const auto& s : b.stores) {
             if (s.w.kind != SlotWrite::Kind::write) continue;
             dst.push_back(s.w.host + size_t(l) * s.record_tokens * bpt);
-            src.push_back(store_staging_.ptr + size_t(r) * b.store_layer_bytes + s.staging_off);
+            src.push_back(b.store_ring->buf.ptr + size_t(r) * b.store_layer_bytes + s.staging_off);
             sizes.push_back(s.rows * bpt);
         }
         cudaMemcpyAttributes attr{};
@@ -777,10 +822,11 @@ Status Connector::start_store_kv(ConnectorMetadata& meta) {
         if (last == b.num_layers && !b.stores_sealed) {
             b.stores_sealed = true;
             cudaStream_t done_stream = b.store_ce ? d2h_stream_.s : store_stream_.s;
-            b.store_complete.record(done_stream);
-            if (b.store_ce) {
-                store_ring_free_.record(d2h_stream_);
-                store_ring_used_ = true;
+            if (b.store_ring != nullptr) {
+                b.store_ring->free.record(d2h_stream_);
+                b.store_ring->used = true;
+                b.store_ring->owner = nullptr;
+                b.store_ring = nullptr;
             }
             if (b.any_store_writes) {
                 auto* ctx = new CommitCtx{&store_, {}, &b.committed, std::move(b.store_touches)};
@@ -791,6 +837,11 @@ Status Connector::start_store_kv(ConnectorMetadata& meta) {
             } else {
                 b.committed.store(true);
             }
+            // Recorded after the commit callback: a stream does not pass a host
+            // function until it returned, so whoever syncs this event (the
+            // final wait, ~BatchState) sees the batch committed and the
+            // callback done with the batch's memory.
+            b.store_complete.record(done_stream);
         }
     } catch (const CudaError& e) {
         return Status{Errc::cuda_error, e.what()};
@@ -855,12 +906,15 @@ Status Connector::flush_decode(QueryId id, QueryState& qs) {
     const auto& model = store_.config().model;
     const uint32_t pt = model.page_tokens;
     const size_t n = ds.tokens.size();
-    ChunkKey key = ds.chain.next(ds.tokens);
-    key.model_tag = model.model_tag;
+    // Nothing changes (chain, buffered tokens, tier) unless the flush goes
+    // through: the readability checks run first, the chain advances last.
     for (uint32_t l = 0; l < model.num_layers; ++l) {
         Status st = pages_.check_readable_span(id, l, ds.chunk_start / pt, n);
         if (!st.ok()) return st;
     }
+    KeyChain chain = ds.chain;
+    ChunkKey key = chain.next(ds.tokens);
+    key.model_tag = model.model_tag;
     auto w = store_.begin_write(key.digest, uint32_t(n), cfg_.pin_stores);
     if (!w.ok()) {
         ds.puts.push_back(PutHandle::immediate(w.status()));
@@ -869,7 +923,10 @@ Status Connector::flush_decode(QueryId id, QueryState& qs) {
     } else {
         std::lock_guard io(io_mu_);
         auto t = pages_.device_table(id, store_stream_);
-        if (!t.ok()) return t.status();
+        if (!t.ok()) {
+            store_.commit_write(key.digest, t.status());  // drop the claim
+            return t.status();
+        }
         XferDesc x;
         x.chunk = reinterpret_cast<uint64_t>(w.value().dev);
         x.layer_stride = uint64_t(n) * model.bytes_per_token_per_layer;
@@ -878,12 +935,11 @@ Status Connector::flush_decode(QueryId id, QueryState& qs) {
         x.first_page = uint32_t(ds.chunk_start / pt);
         x.n_tokens = uint32_t(n);
         auto plan = std::make_shared<DevicePlan>();
-        const uint32_t ppt = pages_per_tile(pages_.page_bytes());
-        plan->build(plan_pool_, {{x}}, pt, ppt, model.num_layers, store_stream_);
+            plan->build(plan_pool_, {{x}}, pt, pages_.page_bytes(), model.num_layers, store_stream_);
         Event computed;
         computed.record(cfg_.engine_stream);
         computed.wait_on(store_stream_);
-        TKV_CUDA(launch_paged_copy(pages_.layout(), plan->plan(0, 0, model.num_layers, ppt),
+        TKV_CUDA(launch_paged_copy(pages_.layout(), plan->plan(0, 0, model.num_layers),
                                    CopyDir::gather, cfg_.store_ctas, store_stream_));
         // Asynchronous: the commit callback marks the chunk present and frees
         // the plan after the gather ran; finish_query waits on the handle.
@@ -891,6 +947,7 @@ Status Connector::flush_decode(QueryId id, QueryState& qs) {
         TKV_CUDA(cudaLaunchHostFunc(store_stream_, commit_cb, ctx));
         ds.puts.push_back(w.value().handle);
     }
+    ds.chain = chain;
     ds.flushed.push_back(key);
     ds.chunk_start += n;
     ds.tokens.clear();
@@ -905,11 +962,19 @@ Status Connector::append_decode(QueryId id, TokenId token) {
     DecodeState& ds = *it->second.decode;
     ds.tokens.push_back(token);
     if (ds.tokens.size() == store_.config().chunk_size) {
+        Status st;
         try {
-            return flush_decode(id, it->second);
+            st = flush_decode(id, it->second);
         } catch (const CudaError& e) {
-            return Status{Errc::cuda_error, e.what()};
+            st = Status{Errc::cuda_error, e.what()};
+        } catch (const std::exception& e) {
+            st = Status{Errc::invalid_argument, e.what()};
         }
+        // A chunk that could not be flushed (its KV not written yet) rejects
+        // this append: the token is not taken, the buffer stays one short of
+        // a chunk, and the engine may append it again.
+        if (!st.ok()) ds.tokens.pop_back();
+        return st;
     }
     return Status::success();
 }
@@ -930,6 +995,8 @@ Result<std::vector<ChunkKey>> Connector::finish_query(QueryId id) {
                 if (!st.ok()) return st;
             } catch (const CudaError& e) {
                 return Status{Errc::cuda_error, e.what()};
+            } catch (const std::exception& e) {
+                return Status{Errc::invalid_argument, e.what()};
             }
             ds = std::move(it->second.decode);
         }

@@ -146,6 +146,12 @@ public:
     Result<std::vector<ChunkKey>> finish_query(QueryId id);
 
     const Config& config() const { return cfg_; }
+    // Several batches may be in flight at once (a serving loop begins batch
+    // k+1 before batch k's final wait_store_kv). The load staging ring is
+    // held by one batch at a time: a batch that needs it while an earlier
+    // one still has layers to enqueue first enqueues the earlier batch's
+    // remaining layers. Store staging comes from a pool of rings, one per
+    // batch whose stores are not yet sealed (normally one).
     TieredStore& store() { return store_; }
     PagedKVStore& pages() { return pages_; }
     KeyHasher& hasher() { return hasher_; }
@@ -187,9 +193,17 @@ private:
     KeyHasher hasher_;
     DualPool plan_pool_;  // per-batch launch plans (outlives every BatchState)
     Stream h2d_stream_, load_stream_, store_stream_, d2h_stream_;
-    DeviceBuffer staging_, store_staging_;
-    Event ring_free_, store_ring_free_;
-    bool ring_used_ = false, store_ring_used_ = false;
+    // A device staging ring; `owner` is the batch still enqueueing into it,
+    // `free` (valid once `used`) marks the end of the last owner's device use.
+    struct StagingRing {
+        DeviceBuffer buf;
+        Event free;
+        bool used = false;
+        detail::BatchState* owner = nullptr;
+    };
+    StagingRing* acquire_store_ring(detail::BatchState& b, size_t need, uint32_t depth);
+    StagingRing load_ring_;
+    std::vector<std::unique_ptr<StagingRing>> store_rings_;
     size_t staging_peak_ = 0;
     std::mutex io_mu_;  // one batch enqueues at a time
 

@@ -13,6 +13,7 @@
 
 namespace tkv {
 
+// Pages per tile of the tile kernel: ~64 KiB tiles.
 inline uint32_t pages_per_tile(size_t page_bytes) {
     size_t p = 65536 / (page_bytes ? page_bytes : 1);
     return uint32_t(p < 1 ? 1 : (p > 64 ? 64 : p));
@@ -26,9 +27,17 @@ inline std::vector<uint32_t> tile_prefix(const std::vector<XferDesc>& d, uint32_
     return tb;
 }
 
+// One-layer launches (the layerwise connector: 8-64 MiB each) use one page
+// per tile when rows are 16-byte multiples, so they can run the unit kernel
+// (paged_copy.cu); all-layer launches keep the tile kernel's ~64 KiB tiles.
+inline uint32_t pages_per_tile_one_layer(size_t page_bytes) {
+    return page_bytes % 256 == 0 ? 1u : pages_per_tile(page_bytes);
+}
+
 struct DevicePlan {
     size_t n_desc = 0;
     size_t variants = 0;
+    uint32_t ppt_1 = 1, ppt_all = 1;
     uint32_t tiles_1 = 0, tiles_all = 0;
     uint64_t addr_or = 0;
     size_t off_tb1 = 0, off_tball = 0;
@@ -44,12 +53,14 @@ struct DevicePlan {
     }
 
     void build(DualPool& p, const std::vector<std::vector<XferDesc>>& vars, uint32_t page_tokens,
-               uint32_t ppt, uint32_t n_layers, cudaStream_t s) {
+               size_t page_bytes, uint32_t n_layers, cudaStream_t s) {
         variants = vars.size();
         n_desc = vars.empty() ? 0 : vars[0].size();
         if (n_desc == 0) return;
-        auto tb1 = tile_prefix(vars[0], page_tokens, ppt, 1);
-        auto tball = tile_prefix(vars[0], page_tokens, ppt, n_layers);
+        ppt_1 = pages_per_tile_one_layer(page_bytes);
+        ppt_all = pages_per_tile(page_bytes);
+        auto tb1 = tile_prefix(vars[0], page_tokens, ppt_1, 1);
+        auto tball = tile_prefix(vars[0], page_tokens, ppt_all, n_layers);
         tiles_1 = tb1.back();
         tiles_all = tball.back();
         const size_t desc_bytes = variants * n_desc * sizeof(XferDesc);
@@ -72,7 +83,10 @@ struct DevicePlan {
         TKV_CUDA(launch_sm_copy(buf->host.dev, buf->dev.ptr, total, s));
     }
 
-    PagedCopyPlan plan(size_t variant, uint32_t layer_begin, uint32_t n_layers, uint32_t ppt) const {
+    // Launch plan over [layer_begin, layer_begin + n_layers): the one-layer
+    // tile prefix for n_layers == 1, the all-layer one otherwise (which must
+    // then cover every layer of the build).
+    PagedCopyPlan plan(size_t variant, uint32_t layer_begin, uint32_t n_layers) const {
         PagedCopyPlan p;
         p.descs = reinterpret_cast<const XferDesc*>(buf->dev.ptr) + variant * n_desc;
         const bool one = n_layers == 1;
@@ -81,7 +95,7 @@ struct DevicePlan {
         p.total_tiles = one ? tiles_1 : tiles_all;
         p.layer_begin = layer_begin;
         p.n_layers = n_layers;
-        p.pages_per_tile = ppt;
+        p.pages_per_tile = one ? ppt_1 : ppt_all;
         p.addr_or = addr_or;
         return p;
     }

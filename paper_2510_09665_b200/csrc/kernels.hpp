@@ -190,6 +190,12 @@ cudaError_t launch_synth_pages(const PagedLayout& layout, const SynthArgs& args,
 // Counts rows (layer, token) whose page bytes differ from synth; adds to *mismatches.
 cudaError_t launch_verify_pages(const PagedLayout& layout, const SynthArgs& args,
                                 unsigned long long* mismatches, cudaStream_t stream);
+// Adds to *mismatches the 8-byte words of a chunk payload [n_layers][n][bpt]
+// (any device-visible address: HBM or a mapped pinned tier slot) that differ
+// from synth for tokens [start, start + n), row slice at row_offset.
+cudaError_t launch_verify_chunk(const uint32_t* tokens, uint64_t seed, uint32_t start, uint32_t n,
+                                uint32_t n_layers, uint32_t bpt, uint64_t row_offset, const uint8_t* chunk,
+                                unsigned long long* mismatches, cudaStream_t stream);
 // Synthetic chunk payload [n_layers][n][bpt] into a flat device buffer.
 cudaError_t launch_synth_chunk(const uint32_t* tokens, uint64_t seed, uint32_t start, uint32_t n,
                                uint32_t n_layers, uint32_t bpt, uint8_t* out,

@@ -19,6 +19,8 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdlib>
+#include <cstring>
 
 #include "kernels.hpp"
 
@@ -165,10 +167,127 @@ paged_copy_kernel(const PagedLayout L, const PagedCopyPlan P, const int dir) {
     }
 }
 
+// ---- unit kernel: the launch as a flat list of <= 4 KiB page pieces ----------
+//
+// The tile kernel above resolves a tile with one thread (binary search over
+// the descriptor prefix, then the page-table reads) while the CTA waits, and
+// hands out work in ~64 KiB tiles. Over a whole prompt (80 layers, 5 GiB per
+// launch) that is hidden behind the other CTA on the SM; at the launch sizes
+// the layerwise connector issues (one layer: 8-64 MiB) it is not: a 64 MiB
+// launch measured 0.68 of the HBM peak and an 8 MiB one 0.21-0.25
+// (profiles/r02_k12_layers.jsonl), i.e. a ~10 us fixed cost per launch made
+// of the serial resolve chains and of 1024 tiles quantised over 296 CTAs.
+//
+// Here every warp is independent. A unit is (layer, descriptor, page, part):
+// at most 4 KiB of one page run, contiguous on both sides. Warp w takes units
+// w, w + warps, ...; it finds the descriptor by binary search over the
+// one-layer page prefix held in shared memory (loaded once per CTA), reads the
+// descriptor and ONE page-table entry, and its 32 lanes move the piece with up
+// to 8 x 16-byte loads in flight each. No block-wide barrier after the
+// prefix load, no idle threads during a resolve, and 4 KiB granularity keeps
+// the tail short. Requires one page per tile (the plan's tile prefix is then
+// a page prefix, times n_layers), a contiguous row layout and 16-byte
+// alignment; other launches use the tile kernel.
+constexpr int kUnitBytes = 4096;
+constexpr int kUnitVecs = kUnitBytes / 16 / 32;  // vectors per lane per unit
+constexpr uint32_t kSmemDescs = 4096;
+constexpr uint64_t kUnitMaxBytes = 512ull << 20;
+
+__global__ void __launch_bounds__(kThreads, 2)
+paged_copy_units_kernel(const PagedLayout L, const PagedCopyPlan P, const int dir, const uint32_t parts,
+                        const uint32_t part_bytes) {
+    __shared__ uint32_t s_pb[kSmemDescs + 1];
+    const uint32_t nl = P.n_layers;
+    const bool smem = P.n_desc <= kSmemDescs;
+    if (smem)
+        for (uint32_t i = threadIdx.x; i <= P.n_desc; i += kThreads) s_pb[i] = __ldg(P.tile_base + i) / nl;
+    __syncthreads();
+    auto prefix = [&](uint32_t d) { return smem ? s_pb[d] : __ldg(P.tile_base + d) / nl; };
+    const uint32_t pages1 = __ldg(P.tile_base + P.n_desc) / nl;  // pages of one layer over all descriptors
+    const uint32_t total = pages1 * nl * parts;
+    const uint32_t lane = threadIdx.x & 31;
+    const uint32_t warps = gridDim.x * (kThreads / 32);
+    const uint32_t w = blockIdx.x * (kThreads / 32) + (threadIdx.x >> 5);
+    // Warp w owns the contiguous unit range [u0, u1): consecutive units are the
+    // parts of one page, then the next page of the same descriptor, so after
+    // the first unit the warp resolves by stepping (no search) and re-reads
+    // the descriptor / page-table entry from L1.
+    const uint32_t u0 = uint32_t(uint64_t(total) * w / warps);
+    const uint32_t u1 = uint32_t(uint64_t(total) * (w + 1) / warps);
+    if (u0 >= u1) return;
+    uint32_t g = u0 / parts;
+    uint32_t q = u0 - g * parts;
+    uint32_t ll = g / pages1;
+    uint32_t g1 = g - ll * pages1;
+    uint32_t lo = 0, hi = P.n_desc;  // largest d with prefix[d] <= g1
+    while (hi - lo > 1) {
+        const uint32_t mid = (lo + hi) >> 1;
+        if (prefix(mid) <= g1) lo = mid; else hi = mid;
+    }
+    uint32_t next_base = prefix(lo + 1);  // first page of descriptor lo + 1
+    const uint8_t* page_p = nullptr;
+    uint64_t chunk = 0;
+    uint32_t page_valid = 0;  // bytes of the current page run
+    bool fresh = true;        // page addresses need resolving
+    for (uint32_t u = u0; u < u1; ++u) {
+        if (fresh) {
+            const XferDesc* dp = P.descs + lo;
+            const uint32_t j = g1 - prefix(lo);
+            const uint32_t n_tokens = __ldg(&dp->n_tokens);
+            page_valid = min(L.page_tokens, n_tokens - j * L.page_tokens) * L.bpt;
+            const uint32_t layer = P.layer_begin + ll;
+            const int32_t* table =
+                reinterpret_cast<const int32_t*>(__ldg(reinterpret_cast<const unsigned long long*>(&dp->table)));
+            const uint32_t page = uint32_t(__ldg(table + uint64_t(L.shared_table ? 0 : layer) * __ldg(&dp->table_stride) +
+                                                 __ldg(&dp->first_page) + j));
+            const uint64_t pbase =
+                L.layer_base ? __ldg(reinterpret_cast<const unsigned long long*>(L.layer_base) + layer) : L.base;
+            page_p = reinterpret_cast<const uint8_t*>(pbase + uint64_t(page) * L.page_stride);
+            chunk = __ldg(reinterpret_cast<const unsigned long long*>(&dp->chunk)) +
+                    uint64_t(layer) * __ldg(reinterpret_cast<const unsigned long long*>(&dp->layer_stride)) +
+                    uint64_t(j) * L.page_tokens * L.bpt;
+            fresh = false;
+        }
+        const uint32_t begin = q * part_bytes;
+        const uint32_t end = min(begin + part_bytes, page_valid);
+        if (begin < end) {  // (empty: a part past the short last page of a descriptor)
+            const uint8_t* src = dir == int(CopyDir::gather) ? page_p + begin
+                                                             : reinterpret_cast<const uint8_t*>(chunk + begin);
+            uint8_t* dst = dir == int(CopyDir::gather) ? reinterpret_cast<uint8_t*>(chunk + begin)
+                                                       : const_cast<uint8_t*>(page_p + begin);
+            const uint32_t nv = (end - begin) >> 4;
+            int4 v[kUnitVecs];
+#pragma unroll
+            for (int k = 0; k < kUnitVecs; ++k) {
+                const uint32_t i = lane + 32u * k;
+                if (i < nv) v[k] = __ldcs(reinterpret_cast<const int4*>(src) + i);
+            }
+#pragma unroll
+            for (int k = 0; k < kUnitVecs; ++k) {
+                const uint32_t i = lane + 32u * k;
+                if (i < nv) __stcs(reinterpret_cast<int4*>(dst) + i, v[k]);
+            }
+        }
+        // step to unit u + 1
+        if (++q == parts) {
+            q = 0;
+            fresh = true;
+            if (++g1 == pages1) {  // next layer: descriptors from the start
+                g1 = 0;
+                ++ll;
+                lo = 0;
+                next_base = prefix(1);
+            }
+            while (g1 >= next_base) next_base = prefix(++lo + 1);
+        }
+    }
+}
+
 template <int W, bool CONTIG>
 cudaError_t launch_w(const PagedLayout& L, const PagedCopyPlan& P, CopyDir dir, int ctas,
                      cudaStream_t s) {
     constexpr int U = W >= 8 ? 4 : 8;
+    if (uint32_t(ctas) > P.total_tiles) ctas = int(P.total_tiles);
     note_launch();
     paged_copy_kernel<W, CONTIG, U><<<ctas, kThreads, 0, s>>>(L, P, int(dir));
     return cudaGetLastError();
@@ -191,11 +310,33 @@ cudaError_t launch_paged_copy(const PagedLayout& L, const PagedCopyPlan& P, Copy
     if (P.total_tiles == 0 || P.n_desc == 0) return cudaSuccess;
     if (P.pages_per_tile == 0 || P.pages_per_tile > kMaxPagesPerTile) return cudaErrorInvalidValue;
     if (ctas <= 0) ctas = 2 * sm_count();
-    if (uint32_t(ctas) > P.total_tiles) ctas = int(P.total_tiles);
     // Vector width: the largest of 16/8/4/1 dividing every stride and base.
     uint64_t a = L.bpt | L.plane_bytes | L.token_stride | L.page_stride | L.plane_stride | L.base |
                  P.addr_or;
     const bool contig = L.n_planes == 1 && L.token_stride == L.bpt;
+    const uint64_t page_bytes = uint64_t(L.page_tokens) * L.bpt;
+    // TKV_PAGED_KERNEL=tile forces the tile kernel (A/B measurements only).
+    static const bool force_tile = [] {
+        const char* v = std::getenv("TKV_PAGED_KERNEL");
+        return v != nullptr && std::strcmp(v, "tile") == 0;
+    }();
+    // Unit kernel for launches up to kUnitMaxBytes (one layer of a batch);
+    // bigger ones (all layers at once) keep the tile kernel, whose sweep over
+    // consecutive tiles measured faster at that size (1.04 vs 0.95 of peak
+    // at 5 GiB, profiles/r02_k12_layers.jsonl).
+    const uint64_t launch_bytes = uint64_t(P.total_tiles) * page_bytes;
+    if ((a & 15) == 0 && contig && P.pages_per_tile == 1 && launch_bytes <= kUnitMaxBytes && !force_tile) {
+        const uint32_t parts = uint32_t((page_bytes + kUnitBytes - 1) / kUnitBytes);
+        const uint32_t part_bytes = uint32_t(((page_bytes + parts - 1) / parts + 15) & ~uint64_t(15));
+        if (uint64_t(P.total_tiles) * parts < (1ull << 32)) {
+            const uint64_t units = uint64_t(P.total_tiles) * parts;
+            const uint64_t want = (units + kThreads / 32 - 1) / (kThreads / 32);  // at least one unit per warp
+            if (uint64_t(ctas) > want) ctas = int(want);
+            note_launch();
+            paged_copy_units_kernel<<<ctas, kThreads, 0, stream>>>(L, P, int(dir), parts, part_bytes);
+            return cudaGetLastError();
+        }
+    }
     if ((a & 15) == 0) return contig ? launch_w<16, true>(L, P, dir, ctas, stream)
                                      : launch_w<16, false>(L, P, dir, ctas, stream);
     if ((a & 7) == 0) return contig ? launch_w<8, true>(L, P, dir, ctas, stream)

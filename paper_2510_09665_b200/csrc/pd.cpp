@@ -1,6 +1,8 @@
 #include "pd.hpp"
 
 #include <algorithm>
+#include <map>
+#include <memory>
 
 #include "copy_plan.hpp"
 
@@ -68,9 +70,26 @@ size_t PdStaging::registered() const {
 // --- data plane ------------------------------------------------------------
 
 namespace {
+// Plan buffers and the copy-engine stream are per device: a process may drive
+// several GPUs (one engine per device), and a pooled buffer or a stream
+// belongs to the device that was current when it was created.
 DualPool& pd_plan_pool() {
-    static DualPool pool;
-    return pool;
+    static std::mutex mu;
+    static std::map<int, std::unique_ptr<DualPool>> pools;
+    int dev = 0;
+    TKV_CUDA(cudaGetDevice(&dev));
+    std::lock_guard lock(mu);
+    auto& p = pools[dev];
+    if (!p) p = std::make_unique<DualPool>();
+    return *p;
+}
+cudaStream_t pd_ce_stream() {
+    thread_local std::map<int, Stream> streams;
+    int dev = 0;
+    TKV_CUDA(cudaGetDevice(&dev));
+    auto it = streams.find(dev);
+    if (it == streams.end()) it = streams.emplace(dev, Stream::create()).first;
+    return it->second;
 }
 }  // namespace
 
@@ -80,6 +99,7 @@ namespace {
 Status pd_describe(PagedKVStore& pages, QueryId query, size_t n_tokens, size_t chunk_size,
                    uint64_t landing, uint64_t base, uint64_t chunk_stride, cudaStream_t stream,
                    std::vector<PdRecord>& recs, std::vector<XferDesc>& descs) {
+    TKV_CUDA(cudaSetDevice(pages.device()));
     const auto& spec = pages.spec();
     const uint32_t pt = spec.page_tokens;
     const size_t bpt = spec.bytes_per_token_per_layer;
@@ -118,10 +138,9 @@ Result<std::vector<PdRecord>> pd_send_chunks(PagedKVStore& pages, QueryId query,
     if (!st.ok()) return st;
     if (descs.empty()) return recs;
     const uint32_t pt = spec.page_tokens;
-    const uint32_t ppt = pages_per_tile(pages.page_bytes());
     DevicePlan plan;
-    plan.build(pd_plan_pool(), {descs}, pt, ppt, spec.num_layers, stream);
-    TKV_CUDA(launch_paged_copy(pages.layout(), plan.plan(0, 0, spec.num_layers, ppt), CopyDir::gather,
+    plan.build(pd_plan_pool(), {descs}, pt, pages.page_bytes(), spec.num_layers, stream);
+    TKV_CUDA(launch_paged_copy(pages.layout(), plan.plan(0, 0, spec.num_layers), CopyDir::gather,
                                ctas, stream));
     TKV_CUDA(cudaStreamSynchronize(stream));  // bytes landed before any ordinal is pushed
     return recs;
@@ -138,17 +157,16 @@ Result<std::vector<PdRecord>> pd_send_chunks_staged(PagedKVStore& pages, QueryId
     if (!st.ok()) return st;
     if (descs.empty()) return recs;
     const uint32_t pt = spec.page_tokens;
-    const uint32_t ppt = pages_per_tile(pages.page_bytes());
     const size_t per_group = std::max<size_t>(1, group_bytes / chunk_stride);
     std::vector<std::vector<XferDesc>> groups;
     for (size_t i = 0; i < descs.size(); i += per_group)
         groups.emplace_back(descs.begin() + i, descs.begin() + std::min(descs.size(), i + per_group));
     std::vector<DevicePlan> plans(groups.size());  // group sizes differ: one plan each
-    static thread_local Stream ce = Stream::create();
+    cudaStream_t ce = pd_ce_stream();
     std::vector<Event> done(groups.size());
     for (size_t g = 0; g < groups.size(); ++g) {
-        plans[g].build(pd_plan_pool(), {groups[g]}, pt, ppt, spec.num_layers, stream);
-        TKV_CUDA(launch_paged_copy(pages.layout(), plans[g].plan(0, 0, spec.num_layers, ppt),
+        plans[g].build(pd_plan_pool(), {groups[g]}, pt, pages.page_bytes(), spec.num_layers, stream);
+        TKV_CUDA(launch_paged_copy(pages.layout(), plans[g].plan(0, 0, spec.num_layers),
                                    CopyDir::gather, 0, stream));
         done[g].record(stream);
         done[g].wait_on(ce);
@@ -165,6 +183,7 @@ Result<std::vector<PdRecord>> pd_send_chunks_staged(PagedKVStore& pages, QueryId
 
 Status pd_land_chunks(PagedKVStore& pages, QueryId query, const std::vector<PdRecord>& records,
                       cudaStream_t stream, int ctas) {
+    TKV_CUDA(cudaSetDevice(pages.device()));
     const auto& spec = pages.spec();
     const uint32_t pt = spec.page_tokens;
     const size_t bpt = spec.bytes_per_token_per_layer;
@@ -189,10 +208,9 @@ Status pd_land_chunks(PagedKVStore& pages, QueryId query, const std::vector<PdRe
         descs.push_back(x);
     }
     if (descs.empty()) return Status::success();
-    const uint32_t ppt = pages_per_tile(pages.page_bytes());
     DevicePlan plan;
-    plan.build(pd_plan_pool(), {descs}, pt, ppt, spec.num_layers, stream);
-    TKV_CUDA(launch_paged_copy(pages.layout(), plan.plan(0, 0, spec.num_layers, ppt),
+    plan.build(pd_plan_pool(), {descs}, pt, pages.page_bytes(), spec.num_layers, stream);
+    TKV_CUDA(launch_paged_copy(pages.layout(), plan.plan(0, 0, spec.num_layers),
                                CopyDir::scatter, ctas, stream));
     for (const auto& r : records)
         for (uint32_t l = 0; l < spec.num_layers; ++l)

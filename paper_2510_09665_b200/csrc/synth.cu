@@ -150,6 +150,38 @@ __global__ void synth_chunk_kernel(const uint32_t* __restrict__ tokens, uint64_t
     }
 }
 
+// Checks a chunk payload [n_layers][n][bpt] (e.g. a pinned tier slot read
+// over PCIe) against synth; row_offset = this TP shard's byte offset in the
+// full row. One warp per (layer, token) row, 8-byte words.
+__global__ void __launch_bounds__(256)
+verify_chunk_kernel(const uint32_t* __restrict__ tokens, uint64_t seed, uint32_t start, uint32_t n,
+                    uint32_t n_layers, uint32_t bpt, uint64_t row_offset, const uint8_t* __restrict__ chunk,
+                    unsigned long long* mismatches) {
+    const uint32_t lane = threadIdx.x & 31;
+    const uint64_t rows = uint64_t(n_layers) * n;
+    const uint64_t warps = uint64_t(gridDim.x) * (blockDim.x >> 5);
+    const uint32_t wpr = (bpt + 7) / 8;
+    unsigned long long bad = 0;
+    for (uint64_t row = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; row < rows; row += warps) {
+        const uint32_t layer = uint32_t(row / n);
+        const uint32_t t = uint32_t(row - uint64_t(layer) * n);
+        const uint64_t base = row_base(seed, tokens[start + t], layer, start + t) + row_offset;
+        const uint8_t* r = chunk + row * bpt;
+        for (uint32_t w = lane; w < wpr; w += 32) {
+            const uint64_t word = splitmix64(base + 8ull * w);
+            const uint32_t nb = min(8u, bpt - 8 * w);
+            uint32_t diff = 0;
+            if (nb == 8 && bpt % 8 == 0) {
+                diff = *reinterpret_cast<const uint64_t*>(r + 8ull * w) != word;
+            } else {
+                for (uint32_t b = 0; b < nb; ++b) diff |= r[8 * w + b] != uint8_t(word >> (8 * b));
+            }
+            bad += diff;
+        }
+    }
+    if (bad) atomicAdd(mismatches, bad);
+}
+
 int grid_for(uint64_t total) {
     uint64_t g = (total + 255) / 256;
     return int(g < 148 * 16 ? (g ? g : 1) : 148 * 16);
@@ -183,6 +215,16 @@ cudaError_t launch_verify_pages(const PagedLayout& L, const SynthArgs& A,
     } else {
         synth_pages_kernel<true><<<grid_for(total), 256, 0, s>>>(L, A, mismatches);
     }
+    return cudaGetLastError();
+}
+
+cudaError_t launch_verify_chunk(const uint32_t* tokens, uint64_t seed, uint32_t start, uint32_t n,
+                                uint32_t n_layers, uint32_t bpt, uint64_t row_offset, const uint8_t* chunk,
+                                unsigned long long* mismatches, cudaStream_t s) {
+    if (n == 0 || n_layers == 0) return cudaSuccess;
+    note_launch();
+    verify_chunk_kernel<<<grid_for(uint64_t(n_layers) * n * 32), 256, 0, s>>>(tokens, seed, start, n, n_layers,
+                                                                             bpt, row_offset, chunk, mismatches);
     return cudaGetLastError();
 }
 

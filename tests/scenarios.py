@@ -717,3 +717,113 @@ def sc_decode_fuzz(factory, C):
 
 
 ALL += [sc_decode_fuzz]
+
+
+def _pipelined(factory, C, seed: int, n_req: int = 6, batch: int = 1):
+    """Serving schedule with two scheduling iterations in flight (bench.py's
+    run_pipelined): the B200 engine looks up and begins iteration k+1 — bind,
+    plan, start_load_kv and every layer's wait_load / compute / start_store —
+    before iteration k's final wait_store_kv; the reference runs the same
+    iterations one after another (its sequential order, connector.cpp:239-392).
+    Every iteration retrieves a shared stored document prefix and stores fresh
+    suffixes of 3 chunks per query (ragged tails); the tier holds the prefix
+    plus two iterations' suffixes, so each iteration's stores evict the
+    suffixes of the iteration two back (LRU), while its predecessor's are still
+    being written. Records every hit length, plan, loaded count, store status,
+    page image and the payload of every chunk left in the tier."""
+    rng = np.random.default_rng(seed)
+    cs = CONN["chunk_size"]
+    doc = make_prompt(3 * cs, 7000 + seed)  # 3 chunks, stored up front
+    S = 3 * batch
+    e = factory(**CONN, ram_slots=3 + 2 * S, num_pages=4096)
+    e.seed_store(doc, len(doc))
+    pipelined = hasattr(e, "stream_handle")
+    iters = []
+    for k in range(n_req):
+        qs = []
+        for b in range(batch):
+            tail = make_prompt(2 * cs + int(rng.integers(1, cs + 1)), int(rng.integers(0, 1 << 30)))
+            qs.append((1000 + batch * k + b, np.concatenate([doc, tail]).astype(np.uint32)))
+        iters.append(qs)
+    out = {"iters": []}
+
+    def lookup(qs):
+        return [e.get_num_new_matched_tokens(q, p) for q, p in qs]
+
+    def begin(qs, matched):
+        for (q, p), mt in zip(qs, matched):
+            assert e.bind_pages(q, len(p)) == 0
+            assert e.update_state_after_alloc(q, (len(p) + 15) // 16, (mt + 15) // 16) == 0
+        m = e.build_connector_meta(qs)
+        assert e.start_load_kv(m) == 0
+        for layer in range(e.num_layers):
+            assert e.wait_load_kv(m, layer) == 0
+            for q, p in qs:
+                lo = e.loaded_tokens(m, q)
+                if pipelined:
+                    e.compute_range(q, p, lo, len(p), layers=(layer, layer + 1))
+                else:
+                    e.compute_range(q, p, lo, len(p))
+            if layer:
+                assert e.wait_store_kv(m, layer - 1) == 0
+            assert e.start_store_kv(m) == 0
+        return m
+
+    def end(qs, matched, m):
+        assert e.wait_store_kv(m, e.num_layers - 1) == 0
+        rec = {"matched": matched, "plans": [plan_view(e, m, i) for i in range(len(qs))],
+               "loaded": [e.loaded_tokens(m, q) for q, _ in qs],
+               "pages_ok": [pages_equal_synth(e, q, p, len(p), C) for q, p in qs],
+               "image": [page_image(e, q, len(p)) for q, p in qs],
+               "results": [[(d.hex(), c) for d, c in e.store_results(m, q)] for q, _ in qs]}
+        e.drop_meta(m)
+        for q, _ in qs:
+            e.finish_query(q)
+            if pipelined:
+                e.release_query(q, sync=False)  # the next iteration stays in flight
+            else:
+                e.release_query(q)
+        out["iters"].append(rec)
+
+    if pipelined:
+        mt = lookup(iters[0])
+        cur = (iters[0], mt, begin(iters[0], mt))
+        for k in range(n_req):
+            nxt = None
+            if k + 1 < n_req:
+                mt = lookup(iters[k + 1])
+                nxt = (iters[k + 1], mt, begin(iters[k + 1], mt))
+            end(*cur)
+            cur = nxt
+    else:
+        for qs in iters:
+            mt = lookup(qs)
+            end(qs, mt, begin(qs, mt))
+    # every chunk any iteration stored: still in the tier? its bytes
+    seed_m = C.model_seed(e.tag)
+    tier = []
+    for qs in iters:
+        for q, p in qs:
+            keys = C.chunk_keys(p, cs, e.tag)
+            for i in range(3, len(keys)):
+                got = e.store_get(keys[i])
+                if got is None:
+                    tier.append((keys[i].hex()[:16], None))
+                else:
+                    cnt = min(cs, len(p) - cs * i)
+                    want = C.synth_chunk(seed_m, p, cs * i, cnt, e.num_layers, e.bpt)
+                    tier.append((keys[i].hex()[:16], bool(np.array_equal(got, want))))
+    out["tier"] = tier
+    out["entries"] = e.store_entries()
+    e.close()
+    return out
+
+
+def sc_pipelined_two_in_flight(factory, C):
+    """Two iterations in flight (B200) vs sequential (reference): one query per
+    iteration, and three queries per iteration (one plan per query, 9 suffix
+    chunks per iteration)."""
+    return [_pipelined(factory, C, 1), _pipelined(factory, C, 2, n_req=5, batch=3)]
+
+
+ALL += [sc_pipelined_two_in_flight]

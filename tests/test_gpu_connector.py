@@ -171,7 +171,7 @@ def test_decode_batch_matches_oracle(tkv, C):
 
 @pytest.mark.parametrize("name", ["sc_decode_fuzz", "sc_protocol_fuzz", "sc_random_trace_evicting",
                                   "sc_random_trace_decode", "sc_random_trace_blocking", "sc_multi_query_batch",
-                                  "sc_vanishing_chunk", "sc_degrade_blocking"])
+                                  "sc_vanishing_chunk", "sc_degrade_blocking", "sc_pipelined_two_in_flight"])
 def test_scenarios_with_a_late_engine_stream(tkv, C, name):
     """The same outcomes when the engine stream runs ~1 ms behind the host
     before every compute (a spin kernel queued ahead of the token upload and

@@ -206,9 +206,10 @@ def test_layer_page_table_roundtrip(tkv):
     e.close()
 
 
-def _multi_layer_case(tkv, C, bpt, L, spans, seed, ppt=0):
+def _multi_layer_case(tkv, C, bpt, L, spans, seed, ppt=0, per_layer=False):
     """K1 then K2 over random page tables for several chunk descriptors and
-    all layers in ONE launch each, checked against the oracle's per-page
+    all layers in ONE launch each (per_layer: one launch per layer, the
+    layerwise connector's shape), checked against the oracle's per-page
     memcpy restatement (paged_store.cpp:123-175)."""
     from paper_2510_09665_b200.api import XferDescC, plan_tiles
     from paper_2510_09665_b200._lib import check, lib
@@ -238,7 +239,7 @@ def _multi_layer_case(tkv, C, bpt, L, spans, seed, ppt=0):
         d.first_page = start // pt
         d.n_tokens = end - start
         descs.append(d)
-    tb, ppt_used = plan_tiles(descs, pt, page_bytes, L, ppt)
+    tb, ppt_used = plan_tiles(descs, pt, page_bytes, 1 if per_layer else L, ppt)
     arr = (XferDescC * len(descs))(*descs)
     d_descs = torch.frombuffer(bytearray(bytes(arr)), dtype=torch.uint8).cuda()
     d_tb = torch.from_numpy(tb.view(np.int32)).cuda()
@@ -248,8 +249,12 @@ def _multi_layer_case(tkv, C, bpt, L, spans, seed, ppt=0):
     addr_or = 0
     for d in descs:
         addr_or |= d.chunk | d.layer_stride
-    check(lib().tkv_gather_layers(ct.byref(layout), d_descs.data_ptr(), d_tb.data_ptr(), len(descs),
-                                  int(tb[-1]), 0, L, ppt_used, addr_or, 0, None))
+    def launch(fn):
+        for l0, nl in ([(layer, 1) for layer in range(L)] if per_layer else [(0, L)]):
+            check(fn(ct.byref(layout), d_descs.data_ptr(), d_tb.data_ptr(), len(descs), int(tb[-1]), l0, nl,
+                     ppt_used, addr_or, 0, None))
+
+    launch(lib().tkv_gather_layers)
     torch.cuda.synchronize()
     for (start, end, rec), tab, ch in zip(spans, tables, chunks):
         got = ch.cpu().numpy()
@@ -267,8 +272,7 @@ def _multi_layer_case(tkv, C, bpt, L, spans, seed, ppt=0):
         for layer in range(L):
             C.scatter_tokens(ref_pool, page_bytes, t[layer, start // pt:], bpt, end - start,
                              src[layer * rec * bpt: layer * rec * bpt + (end - start) * bpt])
-    check(lib().tkv_scatter_layers(ct.byref(layout), d_descs.data_ptr(), d_tb.data_ptr(), len(descs),
-                                   int(tb[-1]), 0, L, ppt_used, addr_or, 0, None))
+    launch(lib().tkv_scatter_layers)
     torch.cuda.synchronize()
     assert np.array_equal(pool.cpu().numpy(), ref_pool)
 
@@ -277,6 +281,16 @@ def _multi_layer_case(tkv, C, bpt, L, spans, seed, ppt=0):
 def test_multilayer_gather_scatter(tkv, C, bpt):
     spans = [(0, 256, 256), (256, 512, 256), (512, 600, 88), (768, 1000, 256)]  # last clips a record
     _multi_layer_case(tkv, C, bpt, 5, spans, seed=bpt)
+
+
+@pytest.mark.parametrize("per_layer", [False, True])
+@pytest.mark.parametrize("bpt", [16, 48, 64, 512, 4096])
+def test_unit_kernel_gather_scatter(tkv, C, bpt, per_layer):
+    """One page per tile with 16-byte rows: the unit kernel (<= 4 KiB page
+    pieces, one warp each), launched over all layers and per layer; ragged
+    spans, a clipped record, an empty descriptor between others."""
+    spans = [(0, 256, 256), (256, 256, 256), (256, 512, 256), (512, 600, 88), (768, 1000, 256), (1024, 1031, 7)]
+    _multi_layer_case(tkv, C, bpt, 5, spans, seed=100 + bpt, ppt=1, per_layer=per_layer)
 
 
 def test_multilayer_small_tiles(tkv, C):
