@@ -324,6 +324,10 @@ int tkv_connector_memo_stats(tkv_connector* c, uint64_t out[5]);
 /* Test hook: corrupt every memo slot's digest (verification must catch it). */
 int tkv_connector_debug_poison_memo(tkv_connector* c);
 uint64_t tkv_connector_hash_launches(tkv_connector* c);
+/* Prompts whose stored prefix the host had to decide (the device presence
+ * index decides the rest in the lookup launches): a memo hit that failed
+ * verification, or a stored chunk the memo had no link for. */
+uint64_t tkv_connector_lookups_host_decided(tkv_connector* c);
 
 void tkv_meta_destroy(tkv_meta* m);
 int tkv_meta_layerwise(tkv_meta* m);

@@ -370,6 +370,9 @@ class Engine:
     def staging_peak(self) -> int:
         return int(self.L.tkv_connector_staging_peak(self.conn))
 
+    def lookups_host_decided(self) -> int:
+        return int(self.L.tkv_connector_lookups_host_decided(self.conn))
+
     def hash_launches(self) -> int:
         return int(self.L.tkv_connector_hash_launches(self.conn))
 

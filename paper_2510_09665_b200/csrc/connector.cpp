@@ -231,6 +231,14 @@ Connector::Connector(TieredStore& store, PagedKVStore& pages, Config cfg)
     store_stream_ = Stream::create();
     d2h_stream_ = Stream::create();
     hasher_.enable_memo(cfg_.memo_entries);
+    // The lookup kernels decide the stored prefix from a device mirror of the
+    // tier's present set (TKV_NO_PRESENCE=1: the host index, A/B only).
+    if (std::getenv("TKV_NO_PRESENCE") == nullptr) {
+        const size_t id = store_.presence_subscribe();
+        TieredStore* st = &store_;
+        hasher_.enable_presence(store_.slab_slots(), [st, id](bool full, std::vector<std::pair<Digest, bool>>& out,
+                                                             bool& reset) { st->presence_drain(id, full, out, reset); });
+    }
 }
 
 Connector::Connector(TieredStore& store, PagedKVStore& pages) : Connector(store, pages, Config{}) {}
@@ -296,11 +304,13 @@ std::vector<size_t> Connector::get_num_new_matched_tokens(
     // LPM (tokens.cpp:59-69): the chain only as far as the first absent
     // chunk, like the reference's lookup; the leading present chunks are
     // probed under one store lock per query. Planning completes the chain.
+    std::vector<size_t> present_rows;
     auto digests = hasher_.hash_prefix(
         prompts, [this](const std::vector<Digest>& d) { return store_.present_prefix(d); },
         [&] {
             for (size_t q = 0; q < ids.size(); ++q) staged[q].assign(prompts[q].begin(), prompts[q].end());
-        });
+        },
+        &present_rows);
     const auto t1 = std::chrono::steady_clock::now();
     std::vector<size_t> out(ids.size());
     for (size_t q = 0; q < ids.size(); ++q) {
@@ -308,7 +318,7 @@ std::vector<size_t> Connector::get_num_new_matched_tokens(
         for (size_t i = 0; i < keys.size(); ++i)
             keys[i] = ChunkKey{digests[q][i], store_.config().model.model_tag, uint32_t(i)};
         const size_t n = prompts[q].size();
-        const size_t present = store_.present_prefix(digests[q]);
+        const size_t present = present_rows[q];  // decided on the device (presence index) where it could
         const size_t lpm = present == 0 ? 0 : std::min(n, present * cs);
         const size_t cap = n == 0 ? 0 : n - 1;  // connector.cpp:75-76
         const size_t matched = std::min(lpm, cap);

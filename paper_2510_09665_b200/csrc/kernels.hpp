@@ -95,6 +95,33 @@ struct HashParams {
     uint8_t tag[kMaxTagBytes] = {};
 };
 
+// Presence index of the pinned tier (TieredStore "present" entries, the
+// reference's contains(), store.cpp:797-806), probed by the lookup kernels:
+// an HBM open-addressing table (linear probing) of 64-byte slots
+// {digest bytes as 8 words, state: 0 empty, 1 present, 2 gone (tombstone),
+// 3 being claimed}. The store records every transition to and from
+// `present` (TieredStore::presence_drain); each lookup hands the pending
+// ones (coalesced: one final state per digest) to its first kernel, which
+// applies them in parallel before the probe kernel runs (stream order).
+// Distinct digests never touch each other's slots except through CAS claims
+// of empty slots, so the parallel apply is race-free. Home slot: the
+// digest's first 4 bytes (little-endian) & mask.
+struct PresenceView {
+    uint32_t* slots = nullptr;            // device, [mask + 1] x 16 words
+    uint32_t mask = 0;
+    const uint32_t* updates = nullptr;    // device-visible (mapped host): n_updates x {digest words[8], present}
+    uint32_t n_updates = 0;
+};
+
+// Lookup outputs of the memo probe / hash kernels with a presence index:
+// per chain, present_out[c] = leading rows of the chain that are present
+// (bit 31 set when that decides the prefix: the next row is absent or the
+// chain ended), known_out[c] = rows whose digests are in `out` ([0, known)).
+struct LookupOut {
+    uint32_t* present_out = nullptr;  // mapped host
+    uint32_t* known_out = nullptr;    // mapped host
+};
+
 // Prefix-digest memo: a device hash table from a
 // fingerprint of the whole token prefix (chain parent + every token up to the
 // end of chunk k) to digest_k. Because the probe key does not contain
@@ -118,6 +145,9 @@ struct MemoView {
     unsigned long long* stats = nullptr;  // [0] hits, [1] misses (optional)
     uint32_t max_rows = 0;                // hash at most this many rows per chain (0 = all)
     uint32_t* first_miss_out = nullptr;   // verify also publishes first_miss here (mapped host)
+    PresenceView presence;                // optional: decide the stored prefix on the device
+    LookupOut lookup;                     // with presence: per-chain results (mapped host)
+    uint32_t* first_absent = nullptr;     // with presence: per chain, first memo hit that is absent
 };
 
 // With a memo whose first_miss is set: probes every row of every chain in

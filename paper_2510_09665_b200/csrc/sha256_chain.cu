@@ -206,31 +206,49 @@ __device__ __forceinline__ void expand_block(const uint32_t* in, uint32_t* out) 
 }
 
 // The 64 rounds with K+W precomputed: only the state recurrence is serial.
-// (Measured: forcing the additions onto the FMA pipe with mad.lo to relieve
-// the ALU pipe made a chunk slower, 20.5 vs 19.4 us, and so did computing
-// Sigma0's rotates on the FMA pipe as IMAD(x, 2^(32-n), IMAD.HI(x, 2^(32-n)))
-// with the multipliers hidden in constant memory, 27.4 vs 19.8 us — the
-// round is dependency-latency bound (ncu: 0.44 issue/cycle, "wait" stalls
-// ~1 cycle per instruction), so longer-latency pipes only lengthen the
-// chain. Hoisting d + h + K + W off the e-chain so the new e is one IADD3
-// after Sigma1/Ch also measured slower (20.9 us). ptxas' own schedule is kept.)
+// The round is arranged around its shortest dependent path. With
+//   Y_t  = h_t + (K+W)_t            (h_t = e_{t-3}: known three rounds ahead)
+//   Yd_t = Y_t + d_t                (d_t = a_{t-3}: likewise)
+// both prepared one round early, off the chains,
+//   e_{t+1} = Sigma1(e_t) + Ch(e_t, f_t, g_t) + Yd_t      one IADD3
+//   a_{t+1} = Sigma1(e_t) + Ch(e_t, f_t, g_t) + Y_t + Sigma0(a_t) + Maj(a_t, b_t, c_t)
+// so e advances by SHF -> LOP3 -> IADD3 per round and a by one IADD3 more
+// (round 1's version computed h + K+W + Sigma1 + Ch, then d + T1: four
+// dependent ALU ops on the e chain, ~31 cycles per round measured).
+// An add the compiler may not reassociate (NVVM would otherwise fold the
+// prepared Y_t + d_t back into a three-operand add behind Sigma1 + Ch).
+__device__ __forceinline__ uint32_t add_fixed(uint32_t x, uint32_t y) {
+    uint32_t r;
+    asm("add.u32 %0, %1, %2;" : "=r"(r) : "r"(x), "r"(y));
+    return r;
+}
+
 __device__ __forceinline__ void compress_kw(uint32_t h[8], const uint32_t* kw) {
     uint32_t a = h[0], b = h[1], c = h[2], d = h[3], e = h[4], f = h[5], g = h[6], hh = h[7];
+    uint32_t y = hh + kw[0];
+    uint32_t yd = y + d;
 #pragma unroll
     for (int t = 0; t < 64; ++t) {
         const uint32_t S1 = rotr(e, 6) ^ rotr(e, 11) ^ rotr(e, 25);
         const uint32_t ch = (e & f) ^ (~e & g);
-        const uint32_t t1 = hh + kw[t] + S1 + ch;
         const uint32_t S0 = rotr(a, 2) ^ rotr(a, 13) ^ rotr(a, 22);
         const uint32_t mj = (a & b) ^ (a & c) ^ (b & c);
+        // Ch is ready one op before Sigma1: (Ch + Yd) then + Sigma1
+        const uint32_t e_new = add_fixed(S1, add_fixed(ch, yd));
+        const uint32_t t1 = add_fixed(S1, add_fixed(ch, y));
+        const uint32_t a_new = add_fixed(t1, add_fixed(S0, mj));
+        if (t + 1 < 64) {  // next round: h = g, d = c
+            y = g + kw[t + 1];
+            yd = y + c;
+        }
         hh = g;
         g = f;
         f = e;
-        e = d + t1;
+        e = e_new;
         d = c;
         c = b;
         b = a;
-        a = t1 + S0 + mj;
+        a = a_new;
     }
     h[0] += a; h[1] += b; h[2] += c; h[3] += d;
     h[4] += e; h[5] += f; h[6] += g; h[7] += hh;
@@ -308,6 +326,76 @@ __device__ __forceinline__ void memo_insert(const MemoView& M, const uint32_t* s
             atomicExch(sp, packed);  // publish: readers acquire the tag, then the digest
             break;
         }
+    }
+}
+
+// ---- presence index probe (PresenceView, kernels.hpp) ----------------------
+constexpr uint32_t kDecided = 0x80000000u;
+
+// Slot states of the presence index (PresenceView).
+constexpr uint32_t kSlotEmpty = 0, kSlotPresent = 1, kSlotGone = 2, kSlotClaim = 3;
+
+// Is the digest whose words (digest bytes, little-endian) are b[8] in the
+// table? Tombstones keep probe runs contiguous; a slot's digest and state
+// are read together (one 64-byte line).
+__device__ __forceinline__ bool presence_has_words(const PresenceView& P, const uint32_t b[8]) {
+    uint32_t i = b[0] & P.mask;
+    for (uint32_t n = 0; n <= P.mask; ++n, i = (i + 1) & P.mask) {
+        const uint4* sp = reinterpret_cast<const uint4*>(P.slots + 16ull * i);
+        const uint4 d0 = __ldcg(sp), d1 = __ldcg(sp + 1), st = __ldcg(sp + 2);
+        if (st.x == kSlotEmpty) return false;
+        if (d0.x == b[0] && d0.y == b[1] && d0.z == b[2] && d0.w == b[3] && d1.x == b[4] && d1.y == b[5] &&
+            d1.z == b[6] && d1.w == b[7])
+            return st.x == kSlotPresent;
+    }
+    return false;
+}
+
+// The same for a digest given as SHA chaining words h[8] (bytes = bswap).
+__device__ __forceinline__ bool presence_has(const PresenceView& P, const uint32_t h[8]) {
+    uint32_t b[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) b[i] = __byte_perm(h[i], 0, 0x0123);
+    return presence_has_words(P, b);
+}
+
+// Applies one pending change (one thread per distinct digest): find the
+// digest's slot in its probe run and set its state, or claim the run's first
+// empty slot (CAS; a concurrent claimer of the same slot publishes its own
+// digest, which we then compare and step past). Removing an absent digest is
+// a no-op; slots are never reused within a table generation (the host
+// rebuilds the table before the tombstones fill it).
+__device__ void presence_apply(const PresenceView& P, const uint32_t* u) {
+    uint32_t b[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) b[k] = u[k];
+    const bool present = u[8] != 0;
+    uint32_t i = b[0] & P.mask;
+    for (uint32_t n = 0; n <= P.mask;) {
+        uint32_t* sp = P.slots + 16ull * i;
+        uint32_t st = atomicAdd(sp + 8, 0u);
+        if (st == kSlotEmpty) {
+            if (!present) return;
+            if (atomicCAS(sp + 8, kSlotEmpty, kSlotClaim) == kSlotEmpty) {
+#pragma unroll
+                for (int k = 0; k < 8; ++k) sp[k] = b[k];
+                __threadfence();
+                atomicExch(sp + 8, kSlotPresent);
+                return;
+            }
+            continue;  // lost the claim: re-read this slot
+        }
+        if (st == kSlotClaim) continue;  // another digest is being published here
+        __threadfence();
+        bool eq = true;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) eq &= __ldcg(sp + k) == b[k];
+        if (eq) {
+            atomicExch(sp + 8, present ? kSlotPresent : kSlotGone);
+            return;
+        }
+        i = (i + 1) & P.mask;
+        ++n;
     }
 }
 
@@ -455,6 +543,14 @@ hash_chains_pair_kernel(const uint32_t* __restrict__ tokens, const ChainDesc* __
                 s.parent[i] = h[i];
                 o[i] = __byte_perm(h[i], 0, 0x0123);
             }
+            // lookup mode: the row after the present memo hits was hashed;
+            // its presence decides the prefix unless it is present too
+            if (M.lookup.present_out != nullptr && M.presence.slots != nullptr && j == 0) {
+                const uint32_t rows = (cd.n_tokens + cs - 1) / cs;
+                const uint32_t k = k0 + 1;
+                M.lookup.present_out[c] =
+                    presence_has(M.presence, h) ? (k | (k == rows ? kDecided : 0u)) : ((k - 1) | kDecided);
+            }
         }
         __syncwarp();
     }
@@ -501,6 +597,9 @@ memo_fingerprint_kernel(const uint32_t* __restrict__ src, uint32_t* __restrict__
         __syncthreads();
         chains = s_chains;
     }
+    // pending presence changes, applied before the probe kernel (next launch)
+    for (uint32_t u = blockIdx.x * blockDim.x + threadIdx.x; u < M.presence.n_updates; u += gridDim.x * blockDim.x)
+        presence_apply(M.presence, M.presence.updates + 9ull * u);
     if (row >= total_rows) return;
     const ChainDesc& cd = chains[chain_of_row(chains, n_chains, row)];
     const uint32_t k = row - cd.out_first;
@@ -530,13 +629,16 @@ constexpr int kProbeThreads = 256;
 __global__ void __launch_bounds__(kProbeThreads)
 memo_probe_kernel(const ChainDesc* __restrict__ chains, const HashParams P, uint8_t* __restrict__ out, const MemoView M) {
     __shared__ unsigned long long warp_sum[kProbeThreads / 32];
-    __shared__ uint32_t first;
+    __shared__ uint32_t first;   // first row the memo missed
+    __shared__ uint32_t absent;  // first memo hit that is not in the tier (with a presence index)
     const uint32_t lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const ChainDesc cd = chains[blockIdx.x];
     const uint32_t cs = P.chunk_size;
     const uint32_t rows = (cd.n_tokens + cs - 1) / cs;
     unsigned long long* keys = M.keys + cd.out_first;
-    if (threadIdx.x == 0) first = rows;
+    if (threadIdx.x == 0) first = absent = rows;
+    // lookup mode (hash_prefix with a presence index): presence decides too
+    const bool lookup = M.lookup.present_out != nullptr && M.presence.slots != nullptr;
     // the chain's parent digest (KeyChain::reset) seeds every key of the chain
     uint64_t pfp = 0x8f1bbcdcca62c1d6ull;
 #pragma unroll
@@ -568,7 +670,7 @@ memo_probe_kernel(const ChainDesc* __restrict__ chains, const HashParams P, uint
         }
         v += before + carry;
         carry += total;
-        const bool skip = first < base;  // an earlier tile already missed: no hits after it
+        const bool skip = min(first, absent) < base;  // an earlier tile already ended the prefix
         if (k < rows) {
             const uint64_t key = mix64(v ^ pfp);
             keys[k] = key;
@@ -577,6 +679,7 @@ memo_probe_kernel(const ChainDesc* __restrict__ chains, const HashParams P, uint
                 uint32_t* o = reinterpret_cast<uint32_t*>(out + 32ull * (cd.out_first + k));
 #pragma unroll
                 for (int i = 0; i < 8; ++i) o[i] = __byte_perm(d[i], 0, 0x0123);
+                if (lookup && !presence_has(M.presence, d)) atomicMin(&absent, k);
             } else {
                 ent = kNoEntry;
                 atomicMin(&first, k);
@@ -586,7 +689,22 @@ memo_probe_kernel(const ChainDesc* __restrict__ chains, const HashParams P, uint
         __syncthreads();  // warp_sum reuse; `first` settled for the next tile
     }
     if (threadIdx.x == 0) {
-        M.first_miss[blockIdx.x] = first;
+        if (lookup) {
+            // the stored prefix, decided on the device: a memo hit that is not
+            // in the tier ends it (no SHA needed); otherwise the first row the
+            // memo missed is hashed (max_rows = 1) and its presence decides
+            if (absent < first) {
+                M.first_miss[blockIdx.x] = rows;  // nothing to hash
+                M.lookup.present_out[blockIdx.x] = absent | kDecided;
+                M.lookup.known_out[blockIdx.x] = absent + 1;
+            } else {
+                M.first_miss[blockIdx.x] = first;
+                M.lookup.present_out[blockIdx.x] = first | (first >= rows ? kDecided : 0u);
+                M.lookup.known_out[blockIdx.x] = min(rows, first + 1);
+            }
+        } else {
+            M.first_miss[blockIdx.x] = first;
+        }
         if (M.stats != nullptr && first) atomicAdd(M.stats, (unsigned long long)first);
     }
 }

@@ -36,6 +36,33 @@ void finish(const std::shared_ptr<detail::PutState>& s, Status st) {
 }
 }  // namespace
 
+size_t TieredStore::presence_subscribe() {
+    std::lock_guard lock(mu_);
+    feeds_.push_back(std::make_unique<PresenceFeed>());
+    return feeds_.size() - 1;
+}
+
+void TieredStore::presence_changed(const Digest& d, bool present) {
+    for (auto& f : feeds_)
+        if (!f->fresh) f->pending[d] = present;
+}
+
+void TieredStore::presence_drain(size_t id, bool want_full, std::vector<std::pair<Digest, bool>>& out,
+                                 bool& reset) {
+    std::lock_guard lock(mu_);
+    PresenceFeed& f = *feeds_.at(id);
+    out.clear();
+    reset = want_full || f.fresh;
+    if (reset) {
+        for (const auto& [d, e] : index_)
+            if (e.state == Entry::State::present) out.emplace_back(d, true);
+        f.fresh = false;
+    } else {
+        out.assign(f.pending.begin(), f.pending.end());
+    }
+    f.pending.clear();
+}
+
 TieredStore::TieredStore(StoreConfig cfg) : cfg_(std::move(cfg)) {
     cfg_.model.validate(cfg_.chunk_size);
     slot_bytes_ = cfg_.model.chunk_bytes(cfg_.chunk_size);
@@ -72,6 +99,7 @@ size_t TieredStore::evict_until_locked(size_t bytes_needed) {
         if (!victim) break;
         auto it = index_.find(*victim);
         free_slots_.push_back(it->second.slot);
+        presence_changed(it->first, false);
         index_.erase(it);
         freed += slot_bytes_;
     }
@@ -204,6 +232,7 @@ std::vector<Result<SlotWrite>> TieredStore::begin_write_batch(
                 batch_new.erase(bn);
             }
             free_slots_.push_back(vit->second.slot);
+            if (vit->second.state == Entry::State::present) presence_changed(vit->first, false);
             index_.erase(vit);
         }
         const uint32_t slot = free_slots_.back();
@@ -239,6 +268,7 @@ void TieredStore::commit_batch(const std::vector<Digest>& digests, const std::ve
             if (it == index_.end() || it->second.state != Entry::State::writing) continue;
             writers.push_back(std::move(it->second.writer));
             it->second.state = Entry::State::present;
+            presence_changed(d, true);
             touch(it->second);
         }
         for (const auto& d : touches) {
@@ -259,6 +289,7 @@ void TieredStore::commit_write(const Digest& digest, const Status& status) {
         writer = std::move(it->second.writer);
         if (status.ok()) {
             it->second.state = Entry::State::present;
+            presence_changed(digest, true);
             touch(it->second);
         } else {
             free_slots_.push_back(it->second.slot);
@@ -372,6 +403,7 @@ ClearResult TieredStore::clear(const std::vector<Digest>& digests) {
             continue;
         }
         free_slots_.push_back(e.slot);
+        presence_changed(d, false);
         index_.erase(it);
         r.removed++;
     }

@@ -96,6 +96,7 @@ public:
 
     const StoreConfig& config() const { return cfg_; }
     size_t slot_bytes() const { return slot_bytes_; }
+    size_t slab_slots() const { return slot_bytes_ ? slab_.bytes / slot_bytes_ : 0; }
 
     // --- device write path (used by the connector's K1 store) --------------
     // Claims a slot for `digest` (token_count rows per layer). Errors:
@@ -156,6 +157,14 @@ public:
     ClearResult clear(const std::vector<Digest>& digests);
     size_t evict_until(size_t bytes_needed);
     StoreStats stats() const;
+    // Change feed of the present set (contains()) for a device mirror (the
+    // lookup kernels' presence index, KeyHasher::enable_presence). Every
+    // transition to or from `present` is recorded per subscriber, coalesced
+    // to the final state per digest; drain hands them over. A subscriber's
+    // first drain, or one with want_full, returns the whole present set
+    // instead (reset = true: the mirror must be cleared first).
+    size_t presence_subscribe();
+    void presence_drain(size_t id, bool want_full, std::vector<std::pair<Digest, bool>>& out, bool& reset);
 
     // LMCK record framing (chunk_file.cpp:7-95) for interop with the
     // reference's disk / wire format: export a present entry as a record,
@@ -190,6 +199,12 @@ private:
     std::unordered_map<Digest, Entry, DigestHasher> index_;
     std::vector<uint32_t> free_slots_;
     uint64_t clock_ = 0;
+    void presence_changed(const Digest& d, bool present);  // caller holds mu_
+    struct PresenceFeed {
+        std::unordered_map<Digest, bool, DigestHasher> pending;
+        bool fresh = true;  // nothing drained yet: the first drain is a full snapshot
+    };
+    std::vector<std::unique_ptr<PresenceFeed>> feeds_;  // guarded by mu_
 };
 
 }  // namespace tkv

@@ -4,6 +4,7 @@
 #include <chrono>
 #include <cstdio>
 #include <cstdlib>
+#include <cstring>
 #include <stdexcept>
 
 namespace tkv {
@@ -184,9 +185,55 @@ std::vector<std::vector<Digest>> KeyHasher::hash(const std::vector<TokenSpanView
     return out;
 }
 
+void KeyHasher::enable_presence(size_t max_entries, PresenceDrain drain) {
+    std::lock_guard lock(mu_);
+    TKV_CUDA(cudaSetDevice(device_));
+    size_t cap = 1024;
+    while (cap < 4 * max_entries) cap <<= 1;
+    presence_table_.reserve(cap * 64);
+    TKV_CUDA(cudaMemsetAsync(presence_table_.ptr, 0, cap * 64, stream_));
+    TKV_CUDA(cudaStreamSynchronize(stream_));
+    presence_mask_ = uint32_t(cap - 1);
+    presence_used_ = 0;
+    presence_drain_ = std::move(drain);
+}
+
+// The tier's pending presence changes into this launch's MemoView (applied
+// by its first kernel). A table that would fill past half its slots with
+// entries and tombstones is cleared and reloaded from a full snapshot.
+// Caller holds mu_.
+void KeyHasher::presence_sync_locked(MemoView& m) {
+    bool reset = false;
+    presence_drain_(false, presence_pending_, reset);
+    size_t adds = 0;
+    for (const auto& u : presence_pending_) adds += u.second;
+    const size_t cap = size_t(presence_mask_) + 1;
+    if (!reset && presence_used_ + adds > cap / 2) {
+        presence_drain_(true, presence_pending_, reset);  // everything present, from scratch
+        adds = presence_pending_.size();
+    }
+    if (reset) {
+        TKV_CUDA(cudaMemsetAsync(presence_table_.ptr, 0, cap * 64, stream_));
+        presence_used_ = 0;
+    }
+    presence_used_ += adds;
+    const size_t n = presence_pending_.size();
+    h_updates_.reserve(std::max<size_t>(1, n) * 36);
+    auto* w = reinterpret_cast<uint32_t*>(h_updates_.host);
+    for (size_t i = 0; i < n; ++i) {
+        std::memcpy(w + 9 * i, presence_pending_[i].first.data(), 32);
+        w[9 * i + 8] = presence_pending_[i].second ? 1u : 0u;
+    }
+    m.presence.slots = reinterpret_cast<uint32_t*>(presence_table_.ptr);
+    m.presence.mask = presence_mask_;
+    m.presence.updates = reinterpret_cast<const uint32_t*>(h_updates_.dev);
+    m.presence.n_updates = uint32_t(n);
+}
+
 std::vector<std::vector<Digest>> KeyHasher::hash_prefix(const std::vector<TokenSpanView>& seqs,
                                                         const PresentPrefix& present,
-                                                        const std::function<void()>& while_waiting) {
+                                                        const std::function<void()>& while_waiting,
+                                                        std::vector<size_t>* present_rows) {
     const double t_in = trace_lookup() ? now_us() : 0;
     std::lock_guard lock(mu_);
     TKV_CUDA(cudaSetDevice(device_));
@@ -200,13 +247,29 @@ std::vector<std::vector<Digest>> KeyHasher::hash_prefix(const std::vector<TokenS
         total_chunks += rows[i];
     }
     std::vector<std::vector<Digest>> out(n_chains);
+    if (present_rows) present_rows->assign(n_chains, 0);
     if (total_chunks == 0) {
         if (while_waiting) while_waiting();
         return out;
     }
     HashParams p;
+    const bool on_device = memo_.slots != nullptr && presence_drain_ && present_rows != nullptr;
+    if (on_device) presence_sync_locked(memo_);  // the stage kernel applies the changes
     // the first launch inserts at most one link per chain
     MemoView m = stage_locked(seqs, nullptr, total_tokens, total_chunks, n_chains, p);
+    memo_.presence.n_updates = 0;  // applied once
+    auto* dev_present = reinterpret_cast<uint32_t*>(h_present_.host);
+    auto* dev_known = reinterpret_cast<uint32_t*>(h_known_.host);
+    if (on_device) {
+        h_present_.reserve(n_chains * sizeof(uint32_t));
+        h_known_.reserve(n_chains * sizeof(uint32_t));
+        dev_present = reinterpret_cast<uint32_t*>(h_present_.host);
+        dev_known = reinterpret_cast<uint32_t*>(h_known_.host);
+        m.lookup.present_out = reinterpret_cast<uint32_t*>(h_present_.dev);
+        m.lookup.known_out = reinterpret_cast<uint32_t*>(h_known_.dev);
+    } else {
+        m.presence = PresenceView{};
+    }
     const double t_packed = trace_lookup() ? now_us() : 0;
     const auto* d_tok = reinterpret_cast<const uint32_t*>(d_tokens_.ptr);
     const auto* d_ch = reinterpret_cast<const ChainDesc*>(d_chains_.ptr);
@@ -230,7 +293,15 @@ std::vector<std::vector<Digest>> KeyHasher::hash_prefix(const std::vector<TokenS
     TKV_CUDA(cudaStreamSynchronize(stream_));
     const double t_synced = trace_lookup() ? now_us() : 0;
     int passes = 0;
+    std::vector<bool> decided(n_chains, false);
     for (size_t i = 0; i < n_chains; ++i) {
+        if (on_device && bad[i] == ~0u && (dev_present[i] & 0x80000000u)) {
+            // the device decided: memo hits verified, presence from the index
+            decided[i] = true;
+            known[i] = dev_known[i];
+            (*present_rows)[i] = dev_present[i] & 0x7fffffffu;
+            continue;
+        }
         const size_t f = memo_.slots ? size_t(first[i]) : 0;
         known[i] = std::min(rows[i], f + 1);
         if (memo_.slots && bad[i] != ~0u) known[i] = std::min<size_t>(known[i], bad[i]);
@@ -252,7 +323,7 @@ std::vector<std::vector<Digest>> KeyHasher::hash_prefix(const std::vector<TokenS
         std::vector<ChainDesc> more;
         std::vector<size_t> which;
         for (size_t i = 0; i < n_chains; ++i) {
-            if (known[i] >= rows[i]) continue;
+            if (decided[i] || known[i] >= rows[i]) continue;
             const auto d = digests_of(i, known[i]);
             if (present(d) < known[i]) continue;  // the LPM ended inside the hits
             ChainDesc x = ch[i];
@@ -278,6 +349,7 @@ std::vector<std::vector<Digest>> KeyHasher::hash_prefix(const std::vector<TokenS
         MemoView ins = m;  // insert the new links under their full-prefix keys
         ins.first_miss = nullptr;
         ins.max_rows = 0;  // the descriptors bound the rows
+        ins.lookup = LookupOut{};
         // no reset mid-call (the hits above point into the memo): links past
         // the capacity are simply not inserted (memo_insert checks it)
         for (const auto& x : more) memo_used_bound_ += (x.n_tokens + chunk_size_ - 1) / chunk_size_;
@@ -292,7 +364,13 @@ std::vector<std::vector<Digest>> KeyHasher::hash_prefix(const std::vector<TokenS
             known[i] = pass == 0 ? known[i] + 1 : rows[i];
         }
     }
-    for (size_t i = 0; i < n_chains; ++i) out[i] = digests_of(i, known[i]);
+    for (size_t i = 0; i < n_chains; ++i) {
+        out[i] = digests_of(i, known[i]);
+        if (present_rows && !decided[i]) {
+            (*present_rows)[i] = present(out[i]);
+            ++host_decided_;
+        }
+    }
     if (trace_lookup())
         std::fprintf(stderr, "[tkv prefix] chains=%zu rows=%zu pack=%.1fus launch=%.1fus device+sync=%.1fus "
                      "passes=%d rest=%.1fus\n", n_chains, total_chunks, t_packed - t_in, t_launched - t_packed,

@@ -57,10 +57,25 @@ public:
     // one SHA chunk decides, and only a present one continues the chain.
     // `while_waiting` (optional) runs on the calling thread while the first
     // launch is in flight (the caller's own host work, off the critical path).
+    // `present_rows` (optional) receives, per sequence, how many leading
+    // chunks are stored: decided on the device from the presence index (see
+    // set_presence) in the same launches — or, where the device could not
+    // decide (no index, a memo hit that failed verification, a stored chunk
+    // the memo had no link for), by `present` on the host.
     using PresentPrefix = std::function<size_t(const std::vector<Digest>&)>;
     std::vector<std::vector<Digest>> hash_prefix(const std::vector<TokenSpanView>& seqs,
                                                  const PresentPrefix& present,
-                                                 const std::function<void()>& while_waiting = {});
+                                                 const std::function<void()>& while_waiting = {},
+                                                 std::vector<size_t>* present_rows = nullptr);
+    // A device mirror of the tier's present set (PresenceView), probed by the
+    // lookup kernels (needs the memo): lookups then decide the stored prefix
+    // without the host index. `drain(want_full, changes, reset)` hands over
+    // the tier's pending changes (TieredStore::presence_drain); they are
+    // applied by each lookup's first kernel. max_entries: the tier's slots.
+    using PresenceDrain = std::function<void(bool, std::vector<std::pair<Digest, bool>>&, bool&)>;
+    void enable_presence(size_t max_entries, PresenceDrain drain);
+    // Lookups whose stored prefix the host decided (diagnostics / tests).
+    uint64_t host_decided() const { return host_decided_; }
 
     // Launch counters (tests assert the once-per-query property).
     uint64_t launches() const { return launches_; }
@@ -88,6 +103,16 @@ private:
     std::mutex mu_;
     Stream stream_;
     PinnedBuffer h_tokens_, h_chains_, h_out_, h_bad_, h_first_;  // mapped host side of a launch
+    PinnedBuffer h_present_, h_known_;                           // lookup results per chain (mapped)
+    uint64_t host_decided_ = 0;
+    // presence index (device table) and the pending changes of one lookup
+    void presence_sync_locked(MemoView& m);
+    PresenceDrain presence_drain_;
+    DeviceBuffer presence_table_;
+    PinnedBuffer h_updates_;
+    uint32_t presence_mask_ = 0;
+    size_t presence_used_ = 0;  // slots claimed since the table was cleared (upper bound)
+    std::vector<std::pair<Digest, bool>> presence_pending_;
     DeviceBuffer d_tokens_, d_chains_, d_out_, d_hit_;  // HBM copies the kernels work on
     DeviceBuffer d_keys_, d_first_;                     // memo probe keys / first miss per chain
     uint64_t memo_rehashes_ = 0;

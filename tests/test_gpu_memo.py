@@ -196,3 +196,53 @@ def test_memo_many_chains_one_launch(tkv, C, n_queries):
         assert [d for _, _, _, _, d in sp] == C.chunk_keys(p, 32, TAG), i
     e.drop_meta(m)
     e.close()
+
+
+def test_presence_index_decides_lookups_on_device(tkv, C):
+    """The stored prefix is decided in the lookup launches from the device
+    presence index (TieredStore's present set mirrored in mapped memory):
+    warm, partially stored, evicted, cleared and cold prompts give the
+    reference's hit lengths with no host presence probe; a chunk stored
+    without a memo link (seeded straight into the tier) and a memo whose
+    hits fail verification fall back to the host index and still agree."""
+    from paper_2510_09665_b200.api import Engine
+    rng = np.random.default_rng(3)
+    e = Engine(num_layers=2, bpt=64, page_tokens=16, tag=TAG, chunk_size=256, ram_slots=6, num_pages=4096)
+    doc = rng.integers(0, 128256, size=256 * 5 + 40, dtype=np.uint32)
+    keys = C.chunk_keys(doc, 256, TAG)
+
+    def lookup(qid, p):
+        m = e.get_num_new_matched_tokens(qid, p)
+        e.finish_query(qid)
+        return m
+
+    def store(qid, p):  # a cold prefill through the connector (memo links + tier entries)
+        e.get_num_new_matched_tokens(qid, p)
+        e.bind_pages(qid, len(p))
+        e.update_state_after_alloc(qid, (len(p) + 15) // 16, 0)
+        m = e.build_connector_meta([(qid, p)])
+        S.transfer(e, m, qid, p)
+        e.drop_meta(m)
+        e.finish_query(qid)
+        e.release_query(qid)
+
+    assert lookup(1, doc) == 0                       # cold: chunk 0 hashed, absent
+    store(2, doc)                                     # all 6 chunks stored (tier full)
+    base = e.lookups_host_decided()
+    assert lookup(3, doc) == len(doc) - 1             # warm: every row a memo hit, all present
+    assert lookup(4, doc[:256 * 3 + 7]) == 256 * 3    # shared prefix, new tail
+    assert e.store_clear(keys[2]) == 1                # a present memo hit that left the tier
+    assert lookup(5, doc) == 512
+    assert e.lookups_host_decided() == base
+    other = rng.integers(0, 128256, size=256 * 2, dtype=np.uint32)
+    store(6, other)                                   # LRU evicts the oldest two of doc's chunks
+    want = 0 if not e.contains(keys[0]) else (256 if not e.contains(keys[1]) else 512)
+    assert lookup(7, doc) == want
+    assert lookup(8, other) == 511
+    assert e.lookups_host_decided() == base
+    # a stored chunk the memo never linked: the device cannot decide, the host does
+    fresh = rng.integers(0, 128256, size=256 * 2, dtype=np.uint32)
+    e.seed_store(fresh, 512)                          # tier entries without memo links
+    assert lookup(9, fresh) == 511
+    assert e.lookups_host_decided() == base + 1
+    e.close()

@@ -1,0 +1,190 @@
+"""The reference's pipeline assertions, on the B200 path.
+
+* "staging peaks at one layer of transfer bytes" (tests/test_connector.cpp:
+  387-427): device staging is bounded by `staging_depth` layers of the
+  batch's transfer bytes (the reference holds one layer on the host; here
+  the ring holds `depth` layers in HBM, each chunk slice 256-byte aligned).
+* "layerwise pipelining beats blocking when load matches compute"
+  (tests/test_engine.cpp:237-269): with an engine whose per-layer compute
+  costs about one layer's load, layerwise < 0.85 x blocking.
+* "a warm backend cuts TTFT and the loads are byte-checked"
+  (tests/test_engine.cpp:217-235): warm TTFT < 0.5 x cold, page bytes equal.
+
+The engine "compute" is the K4 synth kernel plus a calibrated spin on the
+engine stream (torch.cuda._sleep), i.e. a prefill cost per computed token
+and layer, like the reference SimEngine's cost model (prefill_linear).
+"""
+import time
+
+import numpy as np
+import pytest
+import torch
+
+import scenarios as S
+
+pytestmark = pytest.mark.gpu
+
+
+def _aligned(n_bytes):
+    return (n_bytes + 255) // 256 * 256
+
+
+@pytest.mark.parametrize("depth", [1, 2, 4])
+def test_staging_peak_bounded_by_depth_layers(tkv, C, depth):
+    from paper_2510_09665_b200.api import Engine
+    bpt = S.CONN["bpt"]
+    # fully warm query: loads only (95 tokens in 3 chunk slices per layer)
+    e = Engine(**S.CONN, ram_slots=16, num_pages=64, staging_depth=depth)
+    prompt = S.make_prompt(96, 31)
+    e.seed_store(prompt, 96)
+    assert e.get_num_new_matched_tokens(1, prompt) == 95
+    e.bind_pages(1, 96)
+    e.update_state_after_alloc(1, 6, 6)
+    m = e.build_connector_meta([(1, prompt)])
+    assert e.plan(m, 0, "store")[0] == []
+    S.transfer(e, m, 1, prompt)
+    one_layer = _aligned(32 * bpt) * 2 + _aligned(31 * bpt)
+    peak = e.staging_peak()
+    assert 0 < peak <= min(depth, e.num_layers) * one_layer
+    assert S.pages_equal_synth(e, 1, prompt, 96, C)
+    e.finish_query(1)
+    e.release_query(1)
+    e.close()
+    # cold query: stores only (96 tokens per layer)
+    e = Engine(**S.CONN, ram_slots=16, num_pages=64, staging_depth=depth)
+    prompt = S.make_prompt(96, 37)
+    e.get_num_new_matched_tokens(2, prompt)
+    e.bind_pages(2, 96)
+    e.update_state_after_alloc(2, 6, 0)
+    m = e.build_connector_meta([(2, prompt)])
+    S.transfer(e, m, 2, prompt)
+    assert e.staging_peak() == min(depth, e.num_layers) * _aligned(32 * bpt) * 3
+    assert all(c == 0 for _, c in e.store_results(m, 2))
+    e.finish_query(2)
+    e.release_query(2)
+    e.close()
+
+
+def _cycles_per_ms(stream):
+    with torch.cuda.stream(stream):
+        torch.cuda._sleep(1_000_000)
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        torch.cuda._sleep(20_000_000)
+        b.record(stream)
+        torch.cuda.synchronize()
+    return 20_000_000 / a.elapsed_time(b)
+
+
+class CostEngine:
+    """Engine stand-in: per layer, the K4 synth of the computed tokens plus a
+    spin of `ms_per_token_layer` x tokens on the engine stream."""
+
+    def __init__(self, e, ms_per_token_layer, cycles_per_ms):
+        self.e, self.cost, self.cpm = e, ms_per_token_layer, cycles_per_ms
+
+    def compute_layer(self, q, p, lo, layer, fixed_ms=0.0):
+        e = self.e
+        with torch.cuda.stream(e.stream):
+            ms = fixed_ms + self.cost * (len(p) - lo)
+            if ms > 0:
+                torch.cuda._sleep(int(ms * self.cpm))
+        e.compute_range(q, p, lo, len(p), layers=(layer, layer + 1))
+
+
+def _query(ce, q, prompt, layerwise_expected=None, fixed_ms=0.0):
+    """One query through the reference call order; returns (ttft_s, total_s,
+    loaded). TTFT: until the engine stream finished the last layer's compute."""
+    e = ce.e
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    mt = e.get_num_new_matched_tokens(q, prompt)
+    e.bind_pages(q, len(prompt))
+    assert e.update_state_after_alloc(q, (len(prompt) + 15) // 16, (mt + 15) // 16) == 0
+    m = e.build_connector_meta([(q, prompt)])
+    assert e.start_load_kv(m) == 0
+    lw = e.meta_layerwise(m)
+    if layerwise_expected is not None:
+        assert lw == layerwise_expected
+    lo = e.loaded_tokens(m, q)
+    done = torch.cuda.Event()
+    for layer in range(e.num_layers):
+        if lw:
+            assert e.wait_load_kv(m, layer) == 0
+        ce.compute_layer(q, prompt, lo, layer, fixed_ms)
+        if lw:
+            if layer:
+                assert e.wait_store_kv(m, layer - 1) == 0
+            assert e.start_store_kv(m) == 0
+    done.record(e.stream)
+    done.synchronize()
+    ttft = time.perf_counter() - t0
+    if lw:
+        assert e.wait_store_kv(m, e.num_layers - 1) == 0
+    else:
+        assert e.start_store_kv(m) == 0
+    torch.cuda.synchronize()
+    total = time.perf_counter() - t0
+    assert all(c == 0 for _, c in e.store_results(m, q))
+    assert e.verify_range(q, prompt, 0, len(prompt)) == 0  # the loads are byte-checked
+    e.drop_meta(m)
+    e.finish_query(q)
+    e.release_query(q)
+    return ttft, total, lo
+
+
+def test_layerwise_beats_blocking_when_load_matches_compute(tkv):
+    """8 warm queries of 16K tokens (8 layers x 4 KiB rows: 64 MiB of loads
+    per layer over PCIe); each layer's compute is calibrated to one layer's
+    load time. Blocking pays loads and compute serially, layerwise overlaps
+    all loads but the first."""
+    from paper_2510_09665_b200.api import Engine
+    L, bpt, n = 8, 4096, 16384
+    prompts = [np.random.default_rng(900 + i).integers(0, 128256, size=n, dtype=np.uint32) for i in range(8)]
+    stream = torch.cuda.Stream()
+    cpm = _cycles_per_ms(stream)
+    per_layer_ms = None
+    avg = {}
+    for layerwise in (True, False):
+        e = Engine(num_layers=L, bpt=bpt, page_tokens=16, tag="pipe", chunk_size=256, ram_slots=8 * 64 + 8,
+                   num_pages=(n // 16 + 16) * L, layerwise=layerwise, staging_budget=1 << 30, stream=stream)
+        for i, p in enumerate(prompts):
+            e.seed_store(p, n)
+            e.get_num_new_matched_tokens(7000 + i, p)  # warm the key memo (untimed)
+            e.finish_query(7000 + i)
+        ce = CostEngine(e, 0.0, cpm)
+        _query(ce, 8887, prompts[0], layerwise)  # first use: buffers and rings grow here
+        if per_layer_ms is None:  # calibrate: a warm layerwise query without compute cost
+            _, total, _ = _query(ce, 9999, prompts[0])
+            per_layer_ms = 1e3 * total / L
+        _query(ce, 8888, prompts[1], layerwise, per_layer_ms)  # warm-up of this mode
+        times = []
+        for i, p in enumerate(prompts):
+            _, total, lo = _query(ce, 100 + i, p, layerwise, per_layer_ms)
+            assert lo == n - 1
+            times.append(total)
+        avg[layerwise] = float(np.mean(times))
+        e.close()
+    assert avg[True] < 0.85 * avg[False], (avg, per_layer_ms)
+
+
+def test_warm_backend_cuts_ttft(tkv):
+    """A 8K-token prompt (32 layers x 4 KiB rows), prefill cost 0.5 us per
+    token-layer (~2 x 8e9 FLOP per token at 1 PFLOP/s): cold computes every
+    token, warm loads 8191 tokens from the pinned tier and computes one."""
+    from paper_2510_09665_b200.api import Engine
+    L, bpt, n = 32, 4096, 8192
+    stream = torch.cuda.Stream()
+    cpm = _cycles_per_ms(stream)
+    e = Engine(num_layers=L, bpt=bpt, page_tokens=16, tag="ttft", chunk_size=256, ram_slots=3 * 32 + 8,
+               num_pages=(n // 16 + 16) * L, staging_budget=1 << 30, stream=stream)
+    ce = CostEngine(e, 0.5e-3, cpm)
+    p0 = np.random.default_rng(5).integers(0, 128256, size=n, dtype=np.uint32)
+    _query(ce, 1, p0)  # warm-up: first store (rings, plan pools grow here) ...
+    _query(ce, 4, p0)  # ... and first load
+    prompt = np.random.default_rng(17).integers(0, 128256, size=n, dtype=np.uint32)
+    cold, _, lo_c = _query(ce, 2, prompt)
+    warm, _, lo_w = _query(ce, 3, prompt)
+    e.close()
+    assert lo_c == 0 and lo_w == n - 1
+    assert warm < 0.5 * cold, (warm, cold)

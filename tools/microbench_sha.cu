@@ -1,0 +1,184 @@
+// K3 round-function variants, one serial chain on one warp (the lookup's
+// critical path): cycles per 64-round compression for each variant, and the
+// final state (every variant must agree). Build + run on the box:
+//   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o /tmp/mb_sha tools/microbench_sha.cu && /tmp/mb_sha
+#include <cstdint>
+#include <cstdio>
+
+__constant__ uint32_t kK[64] = {
+    0x428a2f98, 0x71374491, 0xb5c0fbcf, 0xe9b5dba5, 0x3956c25b, 0x59f111f1, 0x923f82a4, 0xab1c5ed5, 0xd807aa98,
+    0x12835b01, 0x243185be, 0x550c7dc3, 0x72be5d74, 0x80deb1fe, 0x9bdc06a7, 0xc19bf174, 0xe49b69c1, 0xefbe4786,
+    0x0fc19dc6, 0x240ca1cc, 0x2de92c6f, 0x4a7484aa, 0x5cb0a9dc, 0x76f988da, 0x983e5152, 0xa831c66d, 0xb00327c8,
+    0xbf597fc7, 0xc6e00bf3, 0xd5a79147, 0x06ca6351, 0x14292967, 0x27b70a85, 0x2e1b2138, 0x4d2c6dfc, 0x53380d13,
+    0x650a7354, 0x766a0abb, 0x81c2c92e, 0x92722c85, 0xa2bfe8a1, 0xa81a664b, 0xc24b8b70, 0xc76c51a3, 0xd192e819,
+    0xd6990624, 0xf40e3585, 0x106aa070, 0x19a4c116, 0x1e376c08, 0x2748774c, 0x34b0bcb5, 0x391c0cb3, 0x4ed8aa4a,
+    0x5b9cca4f, 0x682e6ff3, 0x748f82ee, 0x78a5636f, 0x84c87814, 0x8cc70208, 0x90befffa, 0xa4506ceb, 0xbef9a3f7,
+    0xc67178f2};
+
+__device__ __forceinline__ uint32_t rotr(uint32_t x, int n) { return __funnelshift_r(x, x, n); }
+__device__ __forceinline__ uint32_t add_fixed(uint32_t x, uint32_t y) {
+    uint32_t r;
+    asm("add.u32 %0, %1, %2;" : "=r"(r) : "r"(x), "r"(y));
+    return r;
+}
+__device__ __forceinline__ uint32_t add_fma(uint32_t x, uint32_t y) {  // IMAD pipe
+    uint32_t r;
+    asm("mad.lo.u32 %0, %1, 1, %2;" : "=r"(r) : "r"(x), "r"(y));
+    return r;
+}
+__device__ __forceinline__ uint32_t rotr_fma(uint32_t x, int n) {  // x * 2^(32-n): hi | lo words
+    const uint32_t m = 1u << (32 - n);
+    uint32_t lo, hi;
+    asm("mul.lo.u32 %0, %1, %2;" : "=r"(lo) : "r"(x), "r"(m));
+    asm("mul.hi.u32 %0, %1, %2;" : "=r"(hi) : "r"(x), "r"(m));
+    return lo | hi;
+}
+
+// V0: round 1 (T1 = h + KW + S1 + Ch; e = d + T1)
+__device__ __forceinline__ void c_v0(uint32_t h[8], const uint32_t* kw) {
+    uint32_t a = h[0], b = h[1], c = h[2], d = h[3], e = h[4], f = h[5], g = h[6], hh = h[7];
+#pragma unroll
+    for (int t = 0; t < 64; ++t) {
+        const uint32_t S1 = rotr(e, 6) ^ rotr(e, 11) ^ rotr(e, 25);
+        const uint32_t ch = (e & f) ^ (~e & g);
+        const uint32_t t1 = hh + kw[t] + S1 + ch;
+        const uint32_t S0 = rotr(a, 2) ^ rotr(a, 13) ^ rotr(a, 22);
+        const uint32_t mj = (a & b) ^ (a & c) ^ (b & c);
+        hh = g; g = f; f = e; e = d + t1; d = c; c = b; b = a; a = t1 + S0 + mj;
+    }
+    h[0] += a; h[1] += b; h[2] += c; h[3] += d; h[4] += e; h[5] += f; h[6] += g; h[7] += hh;
+}
+
+// V1: Y/Yd prepared a round early (the product's compress_kw)
+__device__ __forceinline__ void c_v1(uint32_t h[8], const uint32_t* kw) {
+    uint32_t a = h[0], b = h[1], c = h[2], d = h[3], e = h[4], f = h[5], g = h[6], hh = h[7];
+    uint32_t y = hh + kw[0], yd = y + d;
+#pragma unroll
+    for (int t = 0; t < 64; ++t) {
+        const uint32_t S1 = rotr(e, 6) ^ rotr(e, 11) ^ rotr(e, 25);
+        const uint32_t ch = (e & f) ^ (~e & g);
+        const uint32_t S0 = rotr(a, 2) ^ rotr(a, 13) ^ rotr(a, 22);
+        const uint32_t mj = (a & b) ^ (a & c) ^ (b & c);
+        const uint32_t e_new = add_fixed(S1, add_fixed(ch, yd));
+        const uint32_t t1 = add_fixed(S1, add_fixed(ch, y));
+        const uint32_t a_new = add_fixed(t1, add_fixed(S0, mj));
+        if (t + 1 < 64) { y = g + kw[t + 1]; yd = y + c; }
+        hh = g; g = f; f = e; e = e_new; d = c; c = b; b = a; a = a_new;
+    }
+    h[0] += a; h[1] += b; h[2] += c; h[3] += d; h[4] += e; h[5] += f; h[6] += g; h[7] += hh;
+}
+
+// V2: as V1, every add on the IMAD (FMA) pipe: the ALU pipe keeps only the
+// 6 SHF + 4 LOP3 of a round
+__device__ __forceinline__ void c_v2(uint32_t h[8], const uint32_t* kw) {
+    uint32_t a = h[0], b = h[1], c = h[2], d = h[3], e = h[4], f = h[5], g = h[6], hh = h[7];
+    uint32_t y = add_fma(hh, kw[0]), yd = add_fma(y, d);
+#pragma unroll
+    for (int t = 0; t < 64; ++t) {
+        const uint32_t S1 = rotr(e, 6) ^ rotr(e, 11) ^ rotr(e, 25);
+        const uint32_t ch = (e & f) ^ (~e & g);
+        const uint32_t S0 = rotr(a, 2) ^ rotr(a, 13) ^ rotr(a, 22);
+        const uint32_t mj = (a & b) ^ (a & c) ^ (b & c);
+        const uint32_t e_new = add_fma(S1, add_fma(ch, yd));
+        const uint32_t t1 = add_fma(S1, add_fma(ch, y));
+        const uint32_t a_new = add_fma(t1, add_fma(S0, mj));
+        if (t + 1 < 64) { y = add_fma(g, kw[t + 1]); yd = add_fma(y, c); }
+        hh = g; g = f; f = e; e = e_new; d = c; c = b; b = a; a = a_new;
+    }
+    h[0] += a; h[1] += b; h[2] += c; h[3] += d; h[4] += e; h[5] += f; h[6] += g; h[7] += hh;
+}
+
+// V3: V1 adds, and the off-path prepare (y, yd) on the FMA pipe only
+__device__ __forceinline__ void c_v3(uint32_t h[8], const uint32_t* kw) {
+    uint32_t a = h[0], b = h[1], c = h[2], d = h[3], e = h[4], f = h[5], g = h[6], hh = h[7];
+    uint32_t y = add_fma(hh, kw[0]), yd = add_fma(y, d);
+#pragma unroll
+    for (int t = 0; t < 64; ++t) {
+        const uint32_t S1 = rotr(e, 6) ^ rotr(e, 11) ^ rotr(e, 25);
+        const uint32_t ch = (e & f) ^ (~e & g);
+        const uint32_t S0 = rotr(a, 2) ^ rotr(a, 13) ^ rotr(a, 22);
+        const uint32_t mj = (a & b) ^ (a & c) ^ (b & c);
+        const uint32_t e_new = add_fixed(S1, add_fixed(ch, yd));
+        const uint32_t t1 = add_fixed(S1, add_fixed(ch, y));
+        const uint32_t a_new = add_fixed(t1, add_fixed(S0, mj));
+        if (t + 1 < 64) { y = add_fma(g, kw[t + 1]); yd = add_fma(y, c); }
+        hh = g; g = f; f = e; e = e_new; d = c; c = b; b = a; a = a_new;
+    }
+    h[0] += a; h[1] += b; h[2] += c; h[3] += d; h[4] += e; h[5] += f; h[6] += g; h[7] += hh;
+}
+
+// V4: V2 with Maj and Ch written to stay single LOP3s, Sigma0's three
+// rotates on the FMA pipe (IMAD.HI | IMAD.LO); Sigma1 stays on the ALU pipe
+__device__ __forceinline__ void c_v4(uint32_t h[8], const uint32_t* kw) {
+    uint32_t a = h[0], b = h[1], c = h[2], d = h[3], e = h[4], f = h[5], g = h[6], hh = h[7];
+    uint32_t y = add_fma(hh, kw[0]), yd = add_fma(y, d);
+#pragma unroll
+    for (int t = 0; t < 64; ++t) {
+        const uint32_t S1 = rotr(e, 6) ^ rotr(e, 11) ^ rotr(e, 25);
+        const uint32_t ch = (e & f) ^ (~e & g);
+        const uint32_t S0 = rotr_fma(a, 2) ^ rotr_fma(a, 13) ^ rotr_fma(a, 22);
+        const uint32_t mj = (a & b) ^ (a & c) ^ (b & c);
+        const uint32_t e_new = add_fma(S1, add_fma(ch, yd));
+        const uint32_t t1 = add_fma(S1, add_fma(ch, y));
+        const uint32_t a_new = add_fma(t1, add_fma(S0, mj));
+        if (t + 1 < 64) { y = add_fma(g, kw[t + 1]); yd = add_fma(y, c); }
+        hh = g; g = f; f = e; e = e_new; d = c; c = b; b = a; a = a_new;
+    }
+    h[0] += a; h[1] += b; h[2] += c; h[3] += d; h[4] += e; h[5] += f; h[6] += g; h[7] += hh;
+}
+
+template <int V>
+__global__ void bench(const uint32_t* kw_g, int blocks, uint32_t* out, long long* cycles) {
+    __shared__ uint32_t kw[64];
+    for (int i = threadIdx.x; i < 64; i += 32) kw[i] = kw_g[i] + kK[i];
+    __syncwarp();
+    uint32_t h[8] = {0x6a09e667, 0xbb67ae85, 0x3c6ef372, 0xa54ff53a, 0x510e527f, 0x9b05688c, 0x1f83d9ab, 0x5be0cd19};
+    const long long t0 = clock64();
+    for (int b = 0; b < blocks; ++b) {
+        if (V == 0) c_v0(h, kw);
+        if (V == 1) c_v1(h, kw);
+        if (V == 2) c_v2(h, kw);
+        if (V == 3) c_v3(h, kw);
+        if (V == 4) c_v4(h, kw);
+    }
+    const long long t1 = clock64();
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < 8; ++i) out[i] = h[i];
+        *cycles = t1 - t0;
+    }
+}
+
+int main() {
+    uint32_t hw[64];
+    for (int i = 0; i < 64; ++i) hw[i] = 0x9e3779b9u * (i + 1);
+    uint32_t *kw, *out;
+    long long* cyc;
+    cudaMalloc(&kw, 256);
+    cudaMalloc(&out, 32);
+    cudaMalloc(&cyc, 8);
+    cudaMemcpy(kw, hw, 256, cudaMemcpyHostToDevice);
+    const int blocks = 2000;
+    uint32_t ref[8] = {};
+    for (int v = 0; v < 5; ++v) {
+        for (int rep = 0; rep < 2; ++rep) {
+            switch (v) {
+                case 0: bench<0><<<1, 32>>>(kw, blocks, out, cyc); break;
+                case 1: bench<1><<<1, 32>>>(kw, blocks, out, cyc); break;
+                case 2: bench<2><<<1, 32>>>(kw, blocks, out, cyc); break;
+                case 3: bench<3><<<1, 32>>>(kw, blocks, out, cyc); break;
+                case 4: bench<4><<<1, 32>>>(kw, blocks, out, cyc); break;
+            }
+        }
+        uint32_t h[8];
+        long long c = 0;
+        cudaMemcpy(h, out, 32, cudaMemcpyDeviceToHost);
+        cudaMemcpy(&c, cyc, 8, cudaMemcpyDeviceToHost);
+        if (v == 0)
+            for (int i = 0; i < 8; ++i) ref[i] = h[i];
+        bool same = true;
+        for (int i = 0; i < 8; ++i) same &= h[i] == ref[i];
+        printf("{\"variant\": %d, \"cycles_per_block\": %.1f, \"cycles_per_round\": %.2f, \"same_state\": %s}\n", v,
+               double(c) / blocks, double(c) / blocks / 64, same ? "true" : "false");
+    }
+    return 0;
+}
