@@ -814,6 +814,22 @@ def run_pd_pairs(args, world, rank, local):
                     w.wait()
             timed(nccl_recv)
     dist.barrier()
+    # 3a. layer-streamed at page granularity: one K1 per layer into 16-token
+    #     window records (run_pd's PdGranularity::page), as a prefill would
+    #     issue it layer by layer (here without the compute in between)
+    if prefill:
+        from paper_2510_09665_b200.api import PdLayerSender
+
+        def streamed():
+            snd = PdLayerSender(e, qid, n, 16, peer_ptr.value, L * 16 * bpt)
+            for layer in range(L):
+                assert snd.layer(layer) == 0
+            r = snd.finish()
+            snd.close()
+            return r
+        result["t_layers"], wrecs = timed(streamed)
+        assert len(wrecs) == (n + 15) // 16
+    dist.barrier()
     # 3. SM-direct (its landed bytes are the ones verified)
     recs = None
     if prefill:
@@ -850,6 +866,7 @@ def run_pd_pairs(args, world, rank, local):
         best = min(result["t_sm"], result["t_ce"], result.get("t_nccl", 1e9))
         result = {"pair": f"{rank}->{peer}", "gbps": moved / best / 1e9, "bytes": moved, "ms": 1e3 * best,
                   "sm_direct_gbps": moved / result["t_sm"] / 1e9, "ce_staged_gbps": moved / result["t_ce"] / 1e9,
+                  "layer_streamed_page_gbps": moved / result["t_layers"] / 1e9,
                   "nccl_gbps": moved / result["t_nccl"] / 1e9 if "t_nccl" in result else None,
                   "link_all_pairs_gbps": probe / best_all / 1e9, "link_alone_gbps": probe / best_alone / 1e9}
     else:
@@ -1055,6 +1072,7 @@ def run_b200(args):
             pd = {"ok": mism == 0, "pairs": len(sends), "per_pair_gbps": [round(r["gbps"], 1) for r in sends],
                   "sm_direct_gbps": [round(r["sm_direct_gbps"], 1) for r in sends],
                   "ce_staged_gbps": [round(r["ce_staged_gbps"], 1) for r in sends],
+                  "layer_streamed_page_gbps": [round(r["layer_streamed_page_gbps"], 1) for r in sends],
                   "nccl_gbps": [round(x, 1) for x in nccl] if all(x is not None for x in nccl) else None,
                   "aggregate_gbps": round(agg, 1), "bytes_per_pair": sends[0]["bytes"],
                   "land_ms": [round(r["land_ms"], 3) for r in lands], "mismatch_words": mism,

@@ -379,6 +379,20 @@ int tkv_pd_send(tkv_pages* src, uint64_t query, size_t n_tokens, size_t chunk_si
  * staging_dev (local HBM, chunk i at staging_dev + i*chunk_stride) while the
  * copy engine moves each finished group (about group_bytes; 0 = 1 GiB) to
  * landing_dev with one peer memcpy. Records point into landing_dev. */
+/* Layer-streamed PD send (run_pd, src/sim_engine.cpp:389-424): one record
+ * per unit of unit_tokens tokens — chunk_size (PdGranularity::chunk) or
+ * page_tokens (PdGranularity::page) — at landing + i * unit_stride, laid out
+ * [L][T_unit][bpt]. tkv_pd_sender_layer(l) gathers layer l of every unit into
+ * the landing buffer, ordered after the work already queued on
+ * engine_stream (the prefill's compute of layer l), on the sender's own
+ * stream; finish waits for every layer (invalid_argument if one was not
+ * sent) and returns the records to push to the decoder's PdStaging. */
+typedef struct tkv_pd_sender tkv_pd_sender;
+int tkv_pd_sender_begin(tkv_pages* src, uint64_t query, size_t n_tokens, size_t unit_tokens, uint64_t landing,
+                        uint64_t unit_stride, tkv_pd_sender** out);
+int tkv_pd_sender_layer(tkv_pd_sender* s, uint32_t layer, void* engine_stream);
+int tkv_pd_sender_finish(tkv_pd_sender* s, tkv_pd_record* out, size_t cap, size_t* n);
+void tkv_pd_sender_destroy(tkv_pd_sender* s);
 int tkv_pd_send_staged(tkv_pages* src, uint64_t query, size_t n_tokens, size_t chunk_size,
                        uint64_t landing_dev, uint64_t chunk_stride, uint64_t staging_dev,
                        uint64_t group_bytes, void* stream, tkv_pd_record* out, size_t cap, size_t* n);

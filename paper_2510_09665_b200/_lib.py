@@ -158,6 +158,10 @@ SIGNATURES = {
     "tkv_pd_registered": (sz, [vp]),
     "tkv_pd_send": (ct.c_int, [vp, ct.c_uint64, sz, sz, ct.c_uint64, ct.c_uint64, vp, ct.POINTER(PdRecordC), sz,
                                szp]),
+    "tkv_pd_sender_begin": (ct.c_int, [vp, ct.c_uint64, sz, sz, ct.c_uint64, ct.c_uint64, ct.POINTER(vp)]),
+    "tkv_pd_sender_layer": (ct.c_int, [vp, ct.c_uint32, vp]),
+    "tkv_pd_sender_finish": (ct.c_int, [vp, ct.POINTER(PdRecordC), sz, szp]),
+    "tkv_pd_sender_destroy": (None, [vp]),
     "tkv_pd_send_staged": (ct.c_int, [vp, ct.c_uint64, sz, sz, ct.c_uint64, ct.c_uint64, ct.c_uint64,
                                       ct.c_uint64, vp, ct.POINTER(PdRecordC), sz, szp]),
     "tkv_pd_land": (ct.c_int, [vp, ct.c_uint64, ct.POINTER(PdRecordC), sz, vp]),

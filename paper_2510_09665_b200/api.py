@@ -566,6 +566,40 @@ def pd_send_staged(engine: "Engine", qid: int, n_tokens: int, landing_ptr: int, 
     return [out[i] for i in range(n.value)]
 
 
+class PdLayerSender:
+    """Layer-streamed PD send (chunk or page granularity): layer(l) after the
+    engine computed layer l, finish() -> records, one per unit."""
+
+    def __init__(self, engine: "Engine", qid: int, n_tokens: int, unit_tokens: int, landing_ptr: int,
+                 unit_stride: int):
+        self.L = lib()
+        self.e = engine
+        self.h = ct.c_void_p()
+        check(self.L.tkv_pd_sender_begin(engine.pages, qid, n_tokens, unit_tokens, landing_ptr, unit_stride,
+                                         ct.byref(self.h)))
+
+    def layer(self, layer: int) -> int:
+        return self.L.tkv_pd_sender_layer(self.h, layer, self.e.stream_handle)
+
+    def finish(self):
+        cap = 1 << 16
+        out = (PdRecordC * cap)()
+        n = ct.c_size_t(0)
+        check(self.L.tkv_pd_sender_finish(self.h, out, cap, ct.byref(n)))
+        return [out[i] for i in range(n.value)]
+
+    def close(self):
+        if self.h:
+            self.L.tkv_pd_sender_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
 def pd_land(engine: "Engine", qid: int, records) -> None:
     """Decoder: scatter landed chunks into the query's pages (one launch)."""
     arr = (PdRecordC * max(1, len(records)))(*records)

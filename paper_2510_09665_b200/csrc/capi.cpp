@@ -50,6 +50,10 @@ struct tkv_meta {
 struct tkv_pd_staging {
     PdStaging s;
 };
+struct tkv_pd_sender {
+    std::shared_ptr<PagedKVStore> pages;  // kept alive while layers are in flight
+    std::unique_ptr<PdLayerSender> s;
+};
 
 static_assert(sizeof(tkv_pd_record) == sizeof(PdRecord));
 static_assert(sizeof(cudaIpcMemHandle_t) == 64);
@@ -724,6 +728,34 @@ int tkv_pd_send(tkv_pages* src, uint64_t q, size_t n_tokens, size_t chunk_size, 
         return 0;
     });
 }
+int tkv_pd_sender_begin(tkv_pages* src, uint64_t q, size_t n_tokens, size_t unit_tokens, uint64_t landing,
+                        uint64_t unit_stride, tkv_pd_sender** out) {
+    return guard([&] {
+        auto h = std::make_unique<tkv_pd_sender>();
+        h->pages = src->p;
+        h->s = std::make_unique<PdLayerSender>(*src->p, q, n_tokens, unit_tokens, landing, unit_stride);
+        if (!h->s->status().ok()) return st(h->s->status());
+        *out = h.release();
+        return 0;
+    });
+}
+int tkv_pd_sender_layer(tkv_pd_sender* s, uint32_t layer, void* engine_stream) {
+    return guard([&] { return st(s->s->send_layer(layer, cudaStream_t(engine_stream))); });
+}
+int tkv_pd_sender_finish(tkv_pd_sender* s, tkv_pd_record* out, size_t cap, size_t* n) {
+    return guard([&] {
+        auto r = s->s->finish();
+        if (!r.ok()) return st(r.status());
+        *n = r.value().size();
+        for (size_t i = 0; i < r.value().size() && i < cap; ++i) {
+            const auto& x = r.value()[i];
+            out[i] = tkv_pd_record{x.addr, x.bytes, x.token_count, x.first_token};
+        }
+        return 0;
+    });
+}
+void tkv_pd_sender_destroy(tkv_pd_sender* s) { delete s; }
+
 int tkv_pd_send_staged(tkv_pages* src, uint64_t q, size_t n_tokens, size_t chunk_size, uint64_t landing,
                        uint64_t stride, uint64_t staging, uint64_t group_bytes, void* stream,
                        tkv_pd_record* out, size_t cap, size_t* n) {

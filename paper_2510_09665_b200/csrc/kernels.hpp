@@ -157,6 +157,15 @@ struct MemoView {
 cudaError_t launch_hash_chains(const uint32_t* tokens, const ChainDesc* chains, uint32_t n_chains,
                                const HashParams& params, uint8_t* out, cudaStream_t stream,
                                const MemoView* memo = nullptr);
+// Cold-lookup fast path: row 0 of every chain decided in one launch (tokens
+// and descriptors may be mapped host memory): memo hit (verified) or SHA,
+// memo insert, presence probe. digests_out[8 c..8 c+8) = digest bytes,
+// flags_out[c] = 1 | 2 * present, stored last with a system-scope release.
+cudaError_t launch_first_row(const uint32_t* tokens, const ChainDesc* chains, uint32_t n_chains,
+                             const HashParams& params, const MemoView& memo, uint32_t* digests_out,
+                             uint32_t* flags_out, cudaStream_t stream);
+// Applies a presence view's pending changes (before the lookup kernels).
+cudaError_t launch_presence_apply(const PresenceView& view, cudaStream_t stream);
 // The memo probe pass alone (fills out / hit_entry / first_miss).
 cudaError_t launch_memo_probe(const ChainDesc* chains, uint32_t n_chains, const HashParams& params,
                               uint8_t* out, const MemoView& memo, cudaStream_t stream);

@@ -98,7 +98,7 @@ namespace {
 // base + i * chunk_stride, after the reference's readability checks.
 Status pd_describe(PagedKVStore& pages, QueryId query, size_t n_tokens, size_t chunk_size,
                    uint64_t landing, uint64_t base, uint64_t chunk_stride, cudaStream_t stream,
-                   std::vector<PdRecord>& recs, std::vector<XferDesc>& descs) {
+                   std::vector<PdRecord>& recs, std::vector<XferDesc>& descs, bool check_layers = true) {
     TKV_CUDA(cudaSetDevice(pages.device()));
     const auto& spec = pages.spec();
     const uint32_t pt = spec.page_tokens;
@@ -108,7 +108,7 @@ Status pd_describe(PagedKVStore& pages, QueryId query, size_t n_tokens, size_t c
     if (!t.ok()) return t.status();
     for (size_t start = 0, i = 0; start < n_tokens; start += chunk_size, ++i) {
         const size_t n = std::min(chunk_size, n_tokens - start);
-        for (uint32_t l = 0; l < spec.num_layers; ++l) {
+        for (uint32_t l = 0; check_layers && l < spec.num_layers; ++l) {
             Status st = pages.check_readable_span(query, l, start / pt, n);
             if (!st.ok()) return st;
         }
@@ -179,6 +179,56 @@ Result<std::vector<PdRecord>> pd_send_chunks_staged(PagedKVStore& pages, QueryId
     TKV_CUDA(cudaStreamSynchronize(ce));  // bytes landed before any ordinal is pushed
     TKV_CUDA(cudaStreamSynchronize(stream));
     return recs;
+}
+
+PdLayerSender::PdLayerSender(PagedKVStore& pages, QueryId query, size_t n_tokens, size_t unit_tokens,
+                             uint64_t landing, uint64_t unit_stride)
+    : pages_(pages), query_(query), n_tokens_(n_tokens), unit_tokens_(unit_tokens) {
+    TKV_CUDA(cudaSetDevice(pages.device()));
+    stream_ = Stream::create();
+    const auto& spec = pages.spec();
+    sent_.assign(spec.num_layers, false);
+    std::vector<XferDesc> descs;
+    status_ = pd_describe(pages, query, n_tokens, unit_tokens, landing, landing, unit_stride, stream_, recs_, descs,
+                          /*check_layers=*/false);
+    if (!status_.ok() || descs.empty()) return;
+    plan_ = std::make_unique<DevicePlan>();
+    plan_->build(pd_plan_pool(), {descs}, spec.page_tokens, pages.page_bytes(), spec.num_layers, stream_);
+}
+
+PdLayerSender::~PdLayerSender() {
+    try {
+        TKV_CUDA(cudaStreamSynchronize(stream_));  // the plan is read by launches in flight
+    } catch (...) {
+    }
+}
+
+Status PdLayerSender::send_layer(uint32_t layer, cudaStream_t engine_stream) {
+    if (!status_.ok()) return status_;
+    const auto& spec = pages_.spec();
+    if (layer >= spec.num_layers) return Status{Errc::invalid_argument, "layer out of range"};
+    if (sent_[layer]) return Status{Errc::duplicate_key, "layer already sent"};
+    const uint32_t pt = spec.page_tokens;
+    for (const auto& r : recs_) {  // the engine computed this layer (check_readable)
+        Status st = pages_.check_readable_span(query_, layer, r.first_token / pt, r.token_count);
+        if (!st.ok()) return st;
+    }
+    sent_[layer] = true;
+    if (!plan_) return Status::success();
+    TKV_CUDA(cudaSetDevice(pages_.device()));
+    Event computed;
+    computed.record(engine_stream);
+    computed.wait_on(stream_);
+    TKV_CUDA(launch_paged_copy(pages_.layout(), plan_->plan(0, layer, 1), CopyDir::gather, 0, stream_));
+    return Status::success();
+}
+
+Result<std::vector<PdRecord>> PdLayerSender::finish() {
+    if (!status_.ok()) return status_;
+    for (bool s : sent_)
+        if (!s) return Status{Errc::invalid_argument, "a layer was not sent"};
+    TKV_CUDA(cudaStreamSynchronize(stream_));  // every layer landed before any ordinal is pushed
+    return recs_;
 }
 
 Status pd_land_chunks(PagedKVStore& pages, QueryId query, const std::vector<PdRecord>& records,

@@ -20,6 +20,7 @@
 
 #include <condition_variable>
 #include <map>
+#include <memory>
 #include <mutex>
 #include <vector>
 
@@ -28,6 +29,8 @@
 #include "paged_store.hpp"
 
 namespace tkv {
+
+struct DevicePlan;  // copy_plan.hpp
 
 struct PdRecord {
     uint64_t addr = 0;          // device address of the landed chunk payload (decoder GPU)
@@ -79,6 +82,37 @@ Result<std::vector<PdRecord>> pd_send_chunks_staged(PagedKVStore& pages, QueryId
                                                     size_t chunk_size, uint64_t landing,
                                                     uint64_t chunk_stride, uint64_t staging,
                                                     cudaStream_t stream, uint64_t group_bytes = 1ull << 30);
+
+// Layer-streamed send at chunk or page granularity (run_pd's PdGranularity,
+// src/sim_engine.cpp:389-424: unit_tokens = chunk_size or page_tokens; one
+// record per unit, [L][T_unit][bpt] at landing + i * unit_stride). The K1 plan
+// is built once; send_layer(l) gathers layer l of every unit straight into
+// the landing buffer on the sender's own stream, ordered after an event on
+// the engine stream, so the NVLink transfer of layer l overlaps the prefill
+// compute of the layers after it (the reference ships only after the whole
+// prefill). finish() waits for the last layer and returns the records, which
+// the caller then pushes (ordinals per unit) to the decoder's PdStaging.
+class PdLayerSender {
+public:
+    PdLayerSender(PagedKVStore& pages, QueryId query, size_t n_tokens, size_t unit_tokens, uint64_t landing,
+                  uint64_t unit_stride);
+    ~PdLayerSender();
+    PdLayerSender(const PdLayerSender&) = delete;
+    PdLayerSender& operator=(const PdLayerSender&) = delete;
+    const Status& status() const { return status_; }  // construction outcome
+    Status send_layer(uint32_t layer, cudaStream_t engine_stream);
+    Result<std::vector<PdRecord>> finish();
+
+private:
+    PagedKVStore& pages_;
+    QueryId query_;
+    size_t n_tokens_, unit_tokens_;
+    Status status_;
+    std::vector<PdRecord> recs_;
+    std::unique_ptr<DevicePlan> plan_;
+    Stream stream_;
+    std::vector<bool> sent_;
+};
 
 // Decoder side: K2 of every landed record into the query's pages (all
 // layers, one launch), marks the pages populated. Enqueued on `stream`.

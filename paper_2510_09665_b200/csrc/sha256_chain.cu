@@ -17,6 +17,7 @@
 // only the rows after a chain's first miss go through SHA.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdint>
 #include <cstdlib>
 
@@ -750,6 +751,131 @@ memo_verify_kernel(const uint32_t* __restrict__ tokens, const ChainDesc* __restr
     if (__any_sync(0xffffffffu, bad != 0) && lane == 0) atomicMin(first_bad + lo, k);
 }
 
+// ---- cold-lookup fast path: the first row of every chain, in one launch ----
+//
+// A lookup's stored prefix is empty when its first chunk is absent — the
+// usual case for a new document. The full lookup stages the whole prompt and
+// probes every row (four launches, ~0.1 ms for 128K tokens); this kernel
+// decides row 0 alone from its 256 tokens: memo probe of the row's prefix
+// key (verified against the entry), else the chunk's SHA-256 by one warp
+// (inserting the link), then the presence index. Per chain it publishes the
+// digest and a flag (bit 0: done, bit 1: present) to mapped memory with a
+// system-scope release, so the host can poll instead of synchronizing and
+// return at once when every chain's first chunk is absent.
+constexpr int kFirstRowWarps = 2;
+
+struct FirstRowSmem {
+    uint32_t tok[kWarpChunkMax + 4];
+    uint32_t w[kMaxWords];
+    uint32_t kw[kMaxBlocks * 64];
+    uint32_t parent[8];
+};
+
+__device__ __forceinline__ uint64_t parent_fingerprint(const uint8_t parent[32]) {
+    uint64_t pfp = 0x8f1bbcdcca62c1d6ull;  // as memo_probe_kernel
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        uint64_t w = 0;
+#pragma unroll
+        for (int b = 0; b < 8; ++b) w |= uint64_t(parent[8 * i + b]) << (8 * b);
+        pfp = mix64(pfp ^ w);
+    }
+    return pfp;
+}
+
+__global__ void __launch_bounds__(32 * kFirstRowWarps)
+first_row_kernel(const uint32_t* __restrict__ tokens, const ChainDesc* __restrict__ chains, uint32_t n_chains,
+                 const HashParams P, const MemoView M, uint32_t* __restrict__ digests_out,
+                 uint32_t* __restrict__ flags_out) {
+    __shared__ FirstRowSmem smem[kFirstRowWarps];
+    const uint32_t lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const uint32_t c = blockIdx.x * kFirstRowWarps + wid;
+    if (c >= n_chains) return;
+    FirstRowSmem& s = smem[wid];
+    const ChainDesc cd = chains[c];
+    const uint32_t n = min(P.chunk_size, cd.n_tokens);
+    uint32_t flag = 1;  // done, absent
+    uint32_t h[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    if (n > 0) {
+        // stage the row's tokens and its fingerprint (memo_fingerprint_kernel's)
+        uint64_t fp = 0;
+        for (uint32_t i = lane; i < n; i += 32) {
+            const uint32_t t = tokens[cd.token_off + i];
+            s.tok[i] = t;
+            fp ^= mix64((uint64_t(t) << 32) | i);
+        }
+        if (lane == 0) s.tok[n] = 0;
+        if (lane < 8)
+            s.parent[lane] = (uint32_t(cd.parent[4 * lane]) << 24) | (uint32_t(cd.parent[4 * lane + 1]) << 16) |
+                             (uint32_t(cd.parent[4 * lane + 2]) << 8) | uint32_t(cd.parent[4 * lane + 3]);
+#pragma unroll
+        for (int o = 16; o; o >>= 1) fp ^= __shfl_xor_sync(0xffffffffu, fp, o);
+        __syncwarp();
+        const uint64_t row_fp = mix64(fp ^ (uint64_t(n) * 0xc2b2ae3d27d4eb4full));  // k = 0
+        const uint64_t key = mix64(row_fp ^ parent_fingerprint(cd.parent));
+        // memo probe + exact verification of a hit (memo_verify_kernel's check)
+        uint32_t d[8], ent = kNoEntry;
+        bool hit = false;
+        if (M.slots != nullptr) {
+            if (lane == 0) hit = memo_probe(M, key, d, &ent);
+            hit = __shfl_sync(0xffffffffu, hit, 0);
+            if (hit) {
+                ent = __shfl_sync(0xffffffffu, ent, 0);
+#pragma unroll
+                for (int i = 0; i < 8; ++i) d[i] = __shfl_sync(0xffffffffu, d[i], 0);
+                const uint32_t* e = M.entries + uint64_t(ent) * M.entry_words;
+                uint32_t dl = 0;  // d[lane] without a dynamically indexed (local-memory) array
+#pragma unroll
+                for (int i = 0; i < 8; ++i) dl = lane == uint32_t(i) ? d[i] : dl;
+                uint32_t bad = 0;
+                if (lane < 8) bad |= (e[lane] ^ s.parent[lane]) | (e[8 + lane] ^ dl);
+                if (lane == 0) bad |= e[16] ^ n;
+                for (uint32_t i = lane; i < n; i += 32) bad |= e[17 + i] ^ s.tok[i];
+                hit = !__any_sync(0xffffffffu, bad != 0);
+            }
+        }
+        if (hit) {
+#pragma unroll
+            for (int i = 0; i < 8; ++i) h[i] = d[i];
+        } else {
+            // SHA-256 of the chunk: words and schedules lane-parallel, rounds serial
+            const uint32_t hdr = 2 + P.tag_len + 32;
+            const uint32_t len = hdr + 4 * n;
+            const uint32_t nblocks = (len + 9 + 63) / 64;
+            const uint32_t end = 64 * nblocks;
+            for (uint32_t jw = lane; jw < 16 * nblocks; jw += 32)
+                s.w[jw] = pair_msg_word(s.tok, s.parent, P, hdr, len, end, jw);
+            __syncwarp();
+            for (uint32_t blk = lane; blk < nblocks; blk += 32) expand_block(s.w + 16 * blk, s.kw + 64 * blk);
+            __syncwarp();
+            uint32_t st[8] = {0x6a09e667, 0xbb67ae85, 0x3c6ef372, 0xa54ff53a,
+                              0x510e527f, 0x9b05688c, 0x1f83d9ab, 0x5be0cd19};
+#pragma unroll 1
+            for (uint32_t blk = 0; blk < nblocks; ++blk) compress_kw(st, s.kw + 64 * blk);
+#pragma unroll
+            for (int i = 0; i < 8; ++i) h[i] = st[i];
+            __syncwarp();
+            if (M.slots != nullptr) memo_insert(M, s.parent, s.tok, n, key, lane, h);
+        }
+        if (lane == 0 && M.presence.slots != nullptr && presence_has(M.presence, h)) flag |= 2u;
+    }
+    uint32_t hl = 0;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) hl = lane == uint32_t(i) ? h[i] : hl;
+    if (lane < 8) digests_out[8 * c + lane] = __byte_perm(hl, 0, 0x0123);
+    __syncwarp();
+    if (lane == 0) {
+        __threadfence_system();
+        asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(flags_out + c), "r"(flag) : "memory");
+    }
+}
+
+// The pending presence changes alone (one thread each), before a lookup.
+__global__ void presence_apply_kernel(const PresenceView P) {
+    for (uint32_t u = blockIdx.x * blockDim.x + threadIdx.x; u < P.n_updates; u += gridDim.x * blockDim.x)
+        presence_apply(P, P.updates + 9ull * u);
+}
+
 // Test hook: corrupt the digest carried by every published slot, so every
 // optimistic memo hit must be caught by memo_verify_kernel.
 __global__ void memo_poison_kernel(unsigned long long* slots, uint32_t n_slots) {
@@ -813,6 +939,26 @@ cudaError_t launch_memo_stage_chains(const uint32_t* src, uint32_t* dst, const C
     const uint32_t blocks = (total_rows * 32 + 127) / 128;
     memo_fingerprint_kernel<<<blocks, 128, 0, s>>>(src, dst, chains_host, n_chains, total_rows, params, memo,
                                                     chains_dev);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_first_row(const uint32_t* tokens, const ChainDesc* chains, uint32_t n_chains,
+                             const HashParams& params, const MemoView& memo, uint32_t* digests_out,
+                             uint32_t* flags_out, cudaStream_t s) {
+    if (n_chains == 0) return cudaSuccess;
+    if (params.chunk_size > uint32_t(kWarpChunkMax)) return cudaErrorInvalidValue;
+    note_launch();
+    const uint32_t blocks = (n_chains + kFirstRowWarps - 1) / kFirstRowWarps;
+    first_row_kernel<<<blocks, 32 * kFirstRowWarps, 0, s>>>(tokens, chains, n_chains, params, memo, digests_out,
+                                                             flags_out);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_presence_apply(const PresenceView& v, cudaStream_t s) {
+    if (v.n_updates == 0 || v.slots == nullptr) return cudaSuccess;
+    note_launch();
+    const uint32_t blocks = std::min<uint32_t>((v.n_updates + 255) / 256, 148);
+    presence_apply_kernel<<<blocks, 256, 0, s>>>(v);
     return cudaGetLastError();
 }
 

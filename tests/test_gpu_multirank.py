@@ -42,7 +42,7 @@ def test_bench_two_ranks_on_one_gpu():
     assert par["timed_store_mismatch_words"] == 0 and par["timed_store_chunks_verified"] > 0
     pd = line["pd"]
     assert pd["ok"] and pd["pairs"] == 1 and pd["mismatch_words"] == 0, pd
-    assert pd["sm_direct_gbps"][0] > 0 and pd["ce_staged_gbps"][0] > 0
+    assert pd["sm_direct_gbps"][0] > 0 and pd["ce_staged_gbps"][0] > 0 and pd["layer_streamed_page_gbps"][0] > 0
     assert pd["nccl_gbps"] is None  # gloo: the NCCL variant runs only under NCCL
     assert pd["link_alone_gbps"][0] > 0 and pd["link_all_pairs_gbps"][0] > 0
     assert line["e2e"]["value"] > 0 and line["gpu_launches"] > 0

@@ -116,3 +116,69 @@ def test_pd_ipc_handle_suballocation(tkv):
     want = (torch.arange(n, dtype=torch.int64, device="cuda").to(torch.uint8) ^ 0x5A)
     assert torch.equal(buf, want)
     assert int(big[:off0].count_nonzero()) == 0 and int(big[off0 + n:].count_nonzero()) == 0
+
+
+@pytest.mark.parametrize("late", [False, True])
+def test_pd_layer_streamed_page_and_chunk_granularity(tkv, C, late):
+    """run_pd at page granularity (one record per 16-token window,
+    src/sim_engine.cpp:398-424, landed per window :457-472) and at chunk
+    granularity, both sent layer by layer while the prefill computes (each
+    layer's K1 ordered after the engine stream's compute of it): the decoder
+    pages equal the recomputation (the reference's PD byte oracle,
+    sim_engine.cpp:474-490) and each other — the disaggregated run equals the
+    monolithic one (tests/test_engine.cpp:412-456) — with ceil(len/16) and
+    ceil(len/32) messages. late: the engine stream runs ~1 ms behind the host
+    before every layer, so only the events order the sends."""
+    from paper_2510_09665_b200.api import Engine, PdLayerSender, PdStaging, pd_land
+    L, bpt, pt, cs, n = 4, 512, 16, 32, 200
+    spec = dict(num_layers=L, bpt=bpt, page_tokens=pt, tag="pd-test", chunk_size=cs)
+    stream = torch.cuda.Stream()
+    pre = Engine(**spec, ram_slots=4, num_pages=256, stream=stream)
+    prompt = S.make_prompt(n, 73)
+    pre.bind_pages(20, n)
+    images = {}
+    for unit in (pt, cs):
+        stride = L * unit * bpt
+        n_units = (n + unit - 1) // unit
+        landing = torch.zeros(n_units * stride, dtype=torch.uint8, device="cuda")
+        snd = PdLayerSender(pre, 20, n, unit, landing.data_ptr(), stride)
+        for layer in range(L):
+            if late:
+                with torch.cuda.stream(stream):
+                    torch.cuda._sleep(2_000_000)
+            pre.compute_range(20, prompt, 0, n, layers=(layer, layer + 1))
+            assert snd.layer(layer) == 0
+        assert snd.layer(0) == 4  # duplicate_key: a layer goes once
+        recs = snd.finish()
+        snd.close()
+        assert len(recs) == n_units  # messages: 13 windows, 7 chunks
+        assert [r.first_token for r in recs] == [unit * i for i in range(n_units)]
+        assert [r.token_count for r in recs] == [min(unit, n - unit * i) for i in range(n_units)]
+        staging = PdStaging()
+        assert staging.register_query(20) == 0
+        order = list(range(n_units))[::-1] + [n_units // 2]  # out of order + a duplicate
+        for o in order:
+            assert staging.push(20, o, o == n_units - 1, recs[o]) == 0
+        rc, landed = staging.await_(20)
+        assert rc == 0 and len(landed) == n_units
+        dec = Engine(**spec, ram_slots=4, num_pages=256)
+        dec.bind_pages(20, n)
+        pd_land(dec, 20, landed)
+        assert S.pages_equal_synth(dec, 20, prompt, n, C)
+        images[unit] = S.page_image(dec, 20, n)
+        # a window record is the layer-major slice of its window [L][T][bpt]
+        host = landing.cpu().numpy()
+        seed = C.model_seed("pd-test")
+        for i in (0, n_units - 1):
+            want = C.synth_chunk(seed, prompt, unit * i, recs[i].token_count, L, bpt)
+            assert np.array_equal(host[i * stride: i * stride + want.size], want)
+        dec.close()
+    assert images[pt] == images[cs]
+    # sending a layer the engine has not computed is refused (check_readable)
+    pre.bind_pages(21, n)
+    buf = torch.zeros(L * n * bpt, dtype=torch.uint8, device="cuda")
+    snd = PdLayerSender(pre, 21, n, pt, buf.data_ptr(), L * pt * bpt)
+    assert snd.layer(0) == 7  # unpopulated_page
+    assert snd.layer(L) == 16  # invalid_argument: out of range
+    snd.close()
+    pre.close()

@@ -127,6 +127,106 @@ __device__ __forceinline__ void c_v4(uint32_t h[8], const uint32_t* kw) {
     h[0] += a; h[1] += b; h[2] += c; h[3] += d; h[4] += e; h[5] += f; h[6] += g; h[7] += hh;
 }
 
+template <int N>
+__device__ __forceinline__ uint32_t shr_(uint32_t x) {
+    uint32_t r;
+    asm("shr.b32 %0, %1, %2;" : "=r"(r) : "r"(x), "n"(N));
+    return r;
+}
+template <int N>
+__device__ __forceinline__ uint32_t shl_(uint32_t x) {
+    uint32_t r;
+    asm("shl.b32 %0, %1, %2;" : "=r"(r) : "r"(x), "n"(N));
+    return r;
+}
+template <int N>
+__device__ __forceinline__ uint32_t shl_fma(uint32_t x) {  // x * 2^N on the FMA pipe
+    uint32_t r;
+    asm("mul.lo.u32 %0, %1, %2;" : "=r"(r) : "r"(x), "n"(1u << N));
+    return r;
+}
+__device__ __forceinline__ uint32_t xor3(uint32_t a, uint32_t b, uint32_t c) {
+    uint32_t r;
+    asm("lop3.b32 %0, %1, %2, %3, 0x96;" : "=r"(r) : "r"(a), "r"(b), "r"(c));
+    return r;
+}
+// Sigma from six disjoint shifted halves: the halves of each rotate share no
+// bits, so the whole Sigma is the XOR of the six shifts.
+template <int A, int B, int C, bool FMA>
+__device__ __forceinline__ uint32_t sigma_shifts(uint32_t x) {
+    const uint32_t l0 = FMA ? shl_fma<32 - A>(x) : shl_<32 - A>(x);
+    const uint32_t l1 = FMA ? shl_fma<32 - B>(x) : shl_<32 - B>(x);
+    const uint32_t l2 = FMA ? shl_fma<32 - C>(x) : shl_<32 - C>(x);
+    return xor3(xor3(shr_<A>(x), shr_<B>(x), shr_<C>(x)), l0, l1 ^ l2);
+}
+
+template <bool FMA>
+__device__ __forceinline__ void c_v56(uint32_t h[8], const uint32_t* kw) {
+    uint32_t a = h[0], b = h[1], c = h[2], d = h[3], e = h[4], f = h[5], g = h[6], hh = h[7];
+    uint32_t y = add_fma(hh, kw[0]), yd = add_fma(y, d);
+#pragma unroll
+    for (int t = 0; t < 64; ++t) {
+        const uint32_t S1 = sigma_shifts<6, 11, 25, FMA>(e);
+        const uint32_t ch = (e & f) ^ (~e & g);
+        const uint32_t S0 = sigma_shifts<2, 13, 22, FMA>(a);
+        const uint32_t mj = (a & b) ^ (a & c) ^ (b & c);
+        const uint32_t e_new = add_fixed(S1, add_fixed(ch, yd));
+        const uint32_t t1 = add_fixed(S1, add_fixed(ch, y));
+        const uint32_t a_new = add_fixed(t1, add_fixed(S0, mj));
+        if (t + 1 < 64) { y = add_fma(g, kw[t + 1]); yd = add_fma(y, c); }
+        hh = g; g = f; f = e; e = e_new; d = c; c = b; b = a; a = a_new;
+    }
+    h[0] += a; h[1] += b; h[2] += c; h[3] += d; h[4] += e; h[5] += f; h[6] += g; h[7] += hh;
+}
+
+// V7: V1 with Sigma1 on funnel shifts and Sigma0 from shifts (left halves on
+// the FMA pipe): splits the rotate work across both pipes
+__device__ __forceinline__ void c_v7(uint32_t h[8], const uint32_t* kw) {
+    uint32_t a = h[0], b = h[1], c = h[2], d = h[3], e = h[4], f = h[5], g = h[6], hh = h[7];
+    uint32_t y = add_fma(hh, kw[0]), yd = add_fma(y, d);
+#pragma unroll
+    for (int t = 0; t < 64; ++t) {
+        const uint32_t S1 = rotr(e, 6) ^ rotr(e, 11) ^ rotr(e, 25);
+        const uint32_t ch = (e & f) ^ (~e & g);
+        const uint32_t S0 = sigma_shifts<2, 13, 22, true>(a);
+        const uint32_t mj = (a & b) ^ (a & c) ^ (b & c);
+        const uint32_t e_new = add_fixed(S1, add_fixed(ch, yd));
+        const uint32_t t1 = add_fixed(S1, add_fixed(ch, y));
+        const uint32_t a_new = add_fixed(t1, add_fixed(S0, mj));
+        if (t + 1 < 64) { y = add_fma(g, kw[t + 1]); yd = add_fma(y, c); }
+        hh = g; g = f; f = e; e = e_new; d = c; c = b; b = a; a = a_new;
+    }
+    h[0] += a; h[1] += b; h[2] += c; h[3] += d; h[4] += e; h[5] += f; h[6] += g; h[7] += hh;
+}
+
+// op throughput / latency probes (one warp): 8 independent chains (rt) or
+// one dependent chain (lat) of the same op
+template <int OP, bool DEP>
+__global__ void opbench(uint32_t seed, int iters, uint32_t* out, long long* cycles) {
+    uint32_t x[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) x[i] = seed * (i + 3) + threadIdx.x;
+    const long long t0 = clock64();
+    for (int it = 0; it < iters; ++it) {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            const int j = DEP ? 0 : i;
+            if (OP == 0) x[j] = __funnelshift_r(x[j], x[j], 7);
+            if (OP == 1) x[j] = shr_<7>(x[j]) ^ seed;
+            if (OP == 2) x[j] = xor3(x[j], seed, 0x1234567u);
+            if (OP == 3) x[j] = add_fixed(x[j], seed);
+            if (OP == 4) x[j] = add_fma(x[j], seed);
+            if (OP == 5) x[j] = shl_fma<7>(x[j]) ^ seed;
+        }
+    }
+    const long long t1 = clock64();
+    uint32_t r = 0;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) r ^= x[i];
+    out[threadIdx.x] = r;
+    if (threadIdx.x == 0) *cycles = t1 - t0;
+}
+
 template <int V>
 __global__ void bench(const uint32_t* kw_g, int blocks, uint32_t* out, long long* cycles) {
     __shared__ uint32_t kw[64];
@@ -140,6 +240,9 @@ __global__ void bench(const uint32_t* kw_g, int blocks, uint32_t* out, long long
         if (V == 2) c_v2(h, kw);
         if (V == 3) c_v3(h, kw);
         if (V == 4) c_v4(h, kw);
+        if (V == 5) c_v56<false>(h, kw);
+        if (V == 6) c_v56<true>(h, kw);
+        if (V == 7) c_v7(h, kw);
     }
     const long long t1 = clock64();
     if (threadIdx.x == 0) {
@@ -159,7 +262,7 @@ int main() {
     cudaMemcpy(kw, hw, 256, cudaMemcpyHostToDevice);
     const int blocks = 2000;
     uint32_t ref[8] = {};
-    for (int v = 0; v < 5; ++v) {
+    for (int v = 0; v < 8; ++v) {
         for (int rep = 0; rep < 2; ++rep) {
             switch (v) {
                 case 0: bench<0><<<1, 32>>>(kw, blocks, out, cyc); break;
@@ -167,6 +270,9 @@ int main() {
                 case 2: bench<2><<<1, 32>>>(kw, blocks, out, cyc); break;
                 case 3: bench<3><<<1, 32>>>(kw, blocks, out, cyc); break;
                 case 4: bench<4><<<1, 32>>>(kw, blocks, out, cyc); break;
+                case 5: bench<5><<<1, 32>>>(kw, blocks, out, cyc); break;
+                case 6: bench<6><<<1, 32>>>(kw, blocks, out, cyc); break;
+                case 7: bench<7><<<1, 32>>>(kw, blocks, out, cyc); break;
             }
         }
         uint32_t h[8];
@@ -180,5 +286,23 @@ int main() {
         printf("{\"variant\": %d, \"cycles_per_block\": %.1f, \"cycles_per_round\": %.2f, \"same_state\": %s}\n", v,
                double(c) / blocks, double(c) / blocks / 64, same ? "true" : "false");
     }
+    const char* names[] = {"SHF.R.W funnel", "SHR+xor", "LOP3", "add (IADD)", "mad.lo (IMAD)", "mul.lo shl+xor"};
+    uint32_t* o2;
+    cudaMalloc(&o2, 128);
+    const int iters = 4096;
+    auto run = [&](auto kern, int op, bool dep) {
+        kern<<<1, 32>>>(12345u, iters, o2, cyc);
+        kern<<<1, 32>>>(12345u, iters, o2, cyc);
+        long long c = 0;
+        cudaMemcpy(&c, cyc, 8, cudaMemcpyDeviceToHost);
+        printf("{\"op\": \"%s\", \"%s\": %.2f}\n", names[op], dep ? "cycles_dependent" : "cycles_per_instr_8way",
+               double(c) / (iters * 8.0));
+    };
+    run(opbench<0, false>, 0, false); run(opbench<0, true>, 0, true);
+    run(opbench<1, false>, 1, false); run(opbench<1, true>, 1, true);
+    run(opbench<2, false>, 2, false); run(opbench<2, true>, 2, true);
+    run(opbench<3, false>, 3, false); run(opbench<3, true>, 3, true);
+    run(opbench<4, false>, 4, false); run(opbench<4, true>, 4, true);
+    run(opbench<5, false>, 5, false); run(opbench<5, true>, 5, true);
     return 0;
 }
