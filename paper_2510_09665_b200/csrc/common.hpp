@@ -7,6 +7,7 @@
 
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <array>
 #include <cstdint>
 #include <cstring>
@@ -195,6 +196,27 @@ struct PinnedBuffer {
 };
 
 // Device allocation (cudaMalloc), grow-only reserve.
+// Allocator of mapped pinned host memory (cudaHostAlloc Mapped|Portable): a
+// container's data() is then also a device address (UVA), so kernels read it
+// over PCIe without a staging copy. Allocation and release are slow and can
+// synchronize the device: such containers are pooled, not churned.
+template <typename T>
+struct PinnedAllocator {
+    using value_type = T;
+    PinnedAllocator() = default;
+    template <typename U>
+    PinnedAllocator(const PinnedAllocator<U>&) {}
+    T* allocate(size_t n) {
+        void* p = nullptr;
+        TKV_CUDA(cudaHostAlloc(&p, std::max<size_t>(1, n) * sizeof(T), cudaHostAllocMapped | cudaHostAllocPortable));
+        return static_cast<T*>(p);
+    }
+    void deallocate(T* p, size_t) { cudaFreeHost(p); }
+    template <typename U>
+    bool operator==(const PinnedAllocator<U>&) const { return true; }
+};
+using PinnedTokens = std::vector<TokenId, PinnedAllocator<TokenId>>;
+
 struct DeviceBuffer {
     uint8_t* ptr = nullptr;
     size_t bytes = 0;

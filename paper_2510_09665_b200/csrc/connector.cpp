@@ -253,16 +253,17 @@ Connector::~Connector() {
     }
 }
 
-// Prompt buffers of finished queries are kept (up to a few) and reused: a
-// 128K-token prompt is 512 KiB, and a fresh allocation of that size is an
-// mmap whose first touch page-faults on the lookup path. Caller holds mu_.
-void Connector::recycle_prompt(std::vector<TokenId>&& v) {
-    if (v.capacity() == 0 || prompt_pool_.size() >= 16) return;
+// Prompt buffers of finished queries are kept and reused: they are mapped
+// pinned memory (the lookup kernels read the prompt from the query state
+// itself, no second staging copy), whose allocation and release are slow and
+// can synchronize the device. Caller holds mu_.
+void Connector::recycle_prompt(PinnedTokens&& v) {
+    if (v.capacity() == 0 || prompt_pool_.size() >= 256) return;
     v.clear();
     prompt_pool_.push_back(std::move(v));
 }
 
-void Connector::recycle_prompt_into(std::vector<TokenId>& dst, size_t n) {
+void Connector::recycle_prompt_into(PinnedTokens& dst, size_t n) {
     for (size_t i = prompt_pool_.size(); i-- > 0;) {
         if (prompt_pool_[i].capacity() >= n) {
             recycle_prompt(std::move(dst));
@@ -296,10 +297,15 @@ std::vector<size_t> Connector::get_num_new_matched_tokens(
     const auto t0 = std::chrono::steady_clock::now();
     // The query state keeps a copy of each prompt; it is made while the
     // lookup's first launch runs (pooled buffers, swapped in below).
-    std::vector<std::vector<TokenId>> staged(ids.size());
+    std::vector<PinnedTokens> staged(ids.size());
+    std::vector<const TokenId*> mapped(ids.size());
     {
         std::lock_guard lock(mu_);
-        for (size_t q = 0; q < ids.size(); ++q) recycle_prompt_into(staged[q], prompts[q].size());
+        for (size_t q = 0; q < ids.size(); ++q) {
+            recycle_prompt_into(staged[q], prompts[q].size());
+            staged[q].reserve(prompts[q].size());  // assign() below keeps this buffer
+            mapped[q] = staged[q].data();
+        }
     }
     // LPM (tokens.cpp:59-69): the chain only as far as the first absent
     // chunk, like the reference's lookup; the leading present chunks are
@@ -310,7 +316,7 @@ std::vector<size_t> Connector::get_num_new_matched_tokens(
         [&] {
             for (size_t q = 0; q < ids.size(); ++q) staged[q].assign(prompts[q].begin(), prompts[q].end());
         },
-        &present_rows);
+        &present_rows, &mapped);
     const auto t1 = std::chrono::steady_clock::now();
     std::vector<size_t> out(ids.size());
     for (size_t q = 0; q < ids.size(); ++q) {

@@ -168,7 +168,7 @@ private:
         std::vector<ChunkKey> flushed;
     };
     struct QueryState {
-        std::vector<TokenId> prompt;
+        PinnedTokens prompt;  // mapped pinned: the lookup kernels read it in place
         std::vector<ChunkKey> keys;  // chain of the whole prompt, hashed once
         size_t lpm = 0;
         size_t matched = 0;
@@ -178,9 +178,9 @@ private:
 
     const std::vector<ChunkKey>& keys_for(QueryState& qs, TokenSpanView prompt);
     size_t ring_growth(size_t need, size_t current, uint32_t depth) const;
-    void recycle_prompt(std::vector<TokenId>&& v);
-    void recycle_prompt_into(std::vector<TokenId>& dst, size_t n);
-    std::vector<std::vector<TokenId>> prompt_pool_;  // guarded by mu_
+    void recycle_prompt(PinnedTokens&& v);
+    void recycle_prompt_into(PinnedTokens& dst, size_t n);
+    std::vector<PinnedTokens> prompt_pool_;  // guarded by mu_
     Status enqueue_loads(detail::BatchState& b);
     void enqueue_load_layers(detail::BatchState& b, uint32_t upto);
     Status store_layers(detail::BatchState& b, uint32_t first, uint32_t last);

@@ -161,9 +161,15 @@ cudaError_t launch_hash_chains(const uint32_t* tokens, const ChainDesc* chains, 
 // and descriptors may be mapped host memory): memo hit (verified) or SHA,
 // memo insert, presence probe. digests_out[8 c..8 c+8) = digest bytes,
 // flags_out[c] = 1 | 2 * present, stored last with a system-scope release.
+// one (optional, n_chains == 1, fresh chain): the row's tokens by value.
+struct FirstRowInline {
+    uint32_t n = ~0u;      // tokens in row 0 (~0u: not used)
+    uint32_t tok[256] = {};
+};
 cudaError_t launch_first_row(const uint32_t* tokens, const ChainDesc* chains, uint32_t n_chains,
                              const HashParams& params, const MemoView& memo, uint32_t* digests_out,
-                             uint32_t* flags_out, cudaStream_t stream);
+                             uint32_t* flags_out, cudaStream_t stream, unsigned long long* trace = nullptr,
+                             const FirstRowInline* one = nullptr);
 // Applies a presence view's pending changes (before the lookup kernels).
 cudaError_t launch_presence_apply(const PresenceView& view, cudaStream_t stream);
 // The memo probe pass alone (fills out / hit_entry / first_miss).
@@ -174,14 +180,17 @@ cudaError_t launch_memo_probe(const ChainDesc* chains, uint32_t n_chains, const 
 cudaError_t launch_sm_copy(const void* src, void* dst, uint64_t bytes, cudaStream_t stream);
 // Memo pass 1: stages the packed tokens (src: mapped host) into dst (HBM)
 // and writes every row's chunk fingerprint to memo.keys (chains: device).
+// chain_src (optional, device-visible): per chain, the address its tokens
+// are read from instead of src + token_off (prompts already in mapped memory).
 cudaError_t launch_memo_stage(const uint32_t* src, uint32_t* dst, const ChainDesc* chains, uint32_t n_chains,
                               uint32_t total_rows, const HashParams& params, const MemoView& memo,
-                              cudaStream_t stream);
+                              cudaStream_t stream, const unsigned long long* chain_src = nullptr);
 // Same, taking the descriptors from mapped host memory and staging them into
 // chains_dev in the same launch (a separate copy only for > 128 chains).
 cudaError_t launch_memo_stage_chains(const uint32_t* src, uint32_t* dst, const ChainDesc* chains_host,
                                      ChainDesc* chains_dev, uint32_t n_chains, uint32_t total_rows,
-                                     const HashParams& params, const MemoView& memo, cudaStream_t stream);
+                                     const HashParams& params, const MemoView& memo, cudaStream_t stream,
+                                     const unsigned long long* chain_src = nullptr);
 // Verifies every memo hit of a launch against its entry and publishes all
 // digest rows from dev_out to out; first_bad[chain] = first failed chunk.
 cudaError_t launch_memo_verify(const uint32_t* tokens, const ChainDesc* chains, uint32_t n_chains,

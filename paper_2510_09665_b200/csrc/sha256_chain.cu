@@ -581,7 +581,8 @@ constexpr uint32_t kStageChains = 128;
 __global__ void __launch_bounds__(128)
 memo_fingerprint_kernel(const uint32_t* __restrict__ src, uint32_t* __restrict__ dst,
                         const ChainDesc* __restrict__ chains, uint32_t n_chains, uint32_t total_rows,
-                        const HashParams P, const MemoView M, ChainDesc* __restrict__ chains_dst) {
+                        const HashParams P, const MemoView M, ChainDesc* __restrict__ chains_dst,
+                        const unsigned long long* __restrict__ chain_src) {
     __shared__ ChainDesc s_chains[kStageChains];
     const uint32_t lane = threadIdx.x & 31;
     const uint32_t row = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -602,14 +603,16 @@ memo_fingerprint_kernel(const uint32_t* __restrict__ src, uint32_t* __restrict__
     for (uint32_t u = blockIdx.x * blockDim.x + threadIdx.x; u < M.presence.n_updates; u += gridDim.x * blockDim.x)
         presence_apply(M.presence, M.presence.updates + 9ull * u);
     if (row >= total_rows) return;
-    const ChainDesc& cd = chains[chain_of_row(chains, n_chains, row)];
+    const uint32_t ci = chain_of_row(chains, n_chains, row);
+    const ChainDesc& cd = chains[ci];
     const uint32_t k = row - cd.out_first;
     const uint32_t start = k * P.chunk_size;
     const uint32_t n = min(P.chunk_size, cd.n_tokens - start);
     const uint64_t off = cd.token_off + start;
+    const uint32_t* s = chain_src != nullptr ? reinterpret_cast<const uint32_t*>(chain_src[ci]) + start : src + off;
     uint64_t h = 0;
     for (uint32_t idx = lane; idx < n; idx += 32) {
-        const uint32_t t = src[off + idx];
+        const uint32_t t = s[idx];
         dst[off + idx] = t;
         h ^= mix64((uint64_t(t) << 32) | idx);
     }
@@ -752,6 +755,7 @@ memo_verify_kernel(const uint32_t* __restrict__ tokens, const ChainDesc* __restr
 }
 
 // ---- cold-lookup fast path: the first row of every chain, in one launch ----
+// (FirstRowInline, kernels.hpp: a single chain's row-0 tokens as parameters)
 //
 // A lookup's stored prefix is empty when its first chunk is absent — the
 // usual case for a new document. The full lookup stages the whole prompt and
@@ -786,21 +790,29 @@ __device__ __forceinline__ uint64_t parent_fingerprint(const uint8_t parent[32])
 __global__ void __launch_bounds__(32 * kFirstRowWarps)
 first_row_kernel(const uint32_t* __restrict__ tokens, const ChainDesc* __restrict__ chains, uint32_t n_chains,
                  const HashParams P, const MemoView M, uint32_t* __restrict__ digests_out,
-                 uint32_t* __restrict__ flags_out) {
+                 uint32_t* __restrict__ flags_out, unsigned long long* __restrict__ trace, const FirstRowInline one) {
     __shared__ FirstRowSmem smem[kFirstRowWarps];
+    unsigned long long t_start = 0, t_staged = 0, t_hashed = 0;
+    if (trace != nullptr) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
     const uint32_t lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const uint32_t c = blockIdx.x * kFirstRowWarps + wid;
     if (c >= n_chains) return;
     FirstRowSmem& s = smem[wid];
-    const ChainDesc cd = chains[c];
-    const uint32_t n = min(P.chunk_size, cd.n_tokens);
+    // one chain: its row-0 tokens came in the kernel parameters (no PCIe
+    // round trips for the descriptor and the tokens); else mapped memory
+    const bool inl = one.n != ~0u;
+    ChainDesc cd;
+    if (!inl) cd = chains[c];
+    const uint32_t n = inl ? one.n : min(P.chunk_size, cd.n_tokens);
     uint32_t flag = 1;  // done, absent
     uint32_t h[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    bool row_was_hit = false;
+    uint64_t row_key = 0;
     if (n > 0) {
         // stage the row's tokens and its fingerprint (memo_fingerprint_kernel's)
         uint64_t fp = 0;
         for (uint32_t i = lane; i < n; i += 32) {
-            const uint32_t t = tokens[cd.token_off + i];
+            const uint32_t t = inl ? one.tok[i] : tokens[cd.token_off + i];
             s.tok[i] = t;
             fp ^= mix64((uint64_t(t) << 32) | i);
         }
@@ -811,8 +823,10 @@ first_row_kernel(const uint32_t* __restrict__ tokens, const ChainDesc* __restric
 #pragma unroll
         for (int o = 16; o; o >>= 1) fp ^= __shfl_xor_sync(0xffffffffu, fp, o);
         __syncwarp();
+        if (trace != nullptr) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_staged));
         const uint64_t row_fp = mix64(fp ^ (uint64_t(n) * 0xc2b2ae3d27d4eb4full));  // k = 0
         const uint64_t key = mix64(row_fp ^ parent_fingerprint(cd.parent));
+        row_key = key;
         // memo probe + exact verification of a hit (memo_verify_kernel's check)
         uint32_t d[8], ent = kNoEntry;
         bool hit = false;
@@ -834,6 +848,8 @@ first_row_kernel(const uint32_t* __restrict__ tokens, const ChainDesc* __restric
                 hit = !__any_sync(0xffffffffu, bad != 0);
             }
         }
+        if (M.stats != nullptr && lane == 0) atomicAdd(M.stats + (hit ? 0 : 1), 1ull);
+        row_was_hit = hit;
         if (hit) {
 #pragma unroll
             for (int i = 0; i < 8; ++i) h[i] = d[i];
@@ -854,9 +870,8 @@ first_row_kernel(const uint32_t* __restrict__ tokens, const ChainDesc* __restric
             for (uint32_t blk = 0; blk < nblocks; ++blk) compress_kw(st, s.kw + 64 * blk);
 #pragma unroll
             for (int i = 0; i < 8; ++i) h[i] = st[i];
-            __syncwarp();
-            if (M.slots != nullptr) memo_insert(M, s.parent, s.tok, n, key, lane, h);
         }
+        if (trace != nullptr) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_hashed));
         if (lane == 0 && M.presence.slots != nullptr && presence_has(M.presence, h)) flag |= 2u;
     }
     uint32_t hl = 0;
@@ -864,10 +879,21 @@ first_row_kernel(const uint32_t* __restrict__ tokens, const ChainDesc* __restric
     for (int i = 0; i < 8; ++i) hl = lane == uint32_t(i) ? h[i] : hl;
     if (lane < 8) digests_out[8 * c + lane] = __byte_perm(hl, 0, 0x0123);
     __syncwarp();
-    if (lane == 0) {
+    if (lane == 0 && trace != nullptr) {
+        unsigned long long t_end;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_end));
+        trace[4 * c] = t_start;
+        trace[4 * c + 1] = t_staged;
+        trace[4 * c + 2] = t_hashed;
+        trace[4 * c + 3] = t_end;
+    }
+    if (lane == 0) {  // the result first (the host is spinning on it) ...
         __threadfence_system();
         asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(flags_out + c), "r"(flag) : "memory");
     }
+    // ... then the memo link of a hashed row (the host syncs the stream
+    // before the next launch reads the memo)
+    if (n > 0 && M.slots != nullptr && !row_was_hit) memo_insert(M, s.parent, s.tok, n, row_key, lane, h);
 }
 
 // The pending presence changes alone (one thread each), before a lookup.
@@ -918,39 +944,44 @@ __global__ void sha256_bytes_kernel(const uint8_t* __restrict__ data, uint32_t n
 
 cudaError_t launch_memo_stage(const uint32_t* src, uint32_t* dst, const ChainDesc* chains, uint32_t n_chains,
                               uint32_t total_rows, const HashParams& params, const MemoView& memo,
-                              cudaStream_t s) {
+                              cudaStream_t s, const unsigned long long* chain_src) {
     if (total_rows == 0) return cudaSuccess;
     note_launch();
     const uint32_t blocks = (total_rows * 32 + 127) / 128;
-    memo_fingerprint_kernel<<<blocks, 128, 0, s>>>(src, dst, chains, n_chains, total_rows, params, memo, nullptr);
+    memo_fingerprint_kernel<<<blocks, 128, 0, s>>>(src, dst, chains, n_chains, total_rows, params, memo, nullptr,
+                                                    chain_src);
     return cudaGetLastError();
 }
 
 cudaError_t launch_memo_stage_chains(const uint32_t* src, uint32_t* dst, const ChainDesc* chains_host,
                                      ChainDesc* chains_dev, uint32_t n_chains, uint32_t total_rows,
-                                     const HashParams& params, const MemoView& memo, cudaStream_t s) {
+                                     const HashParams& params, const MemoView& memo, cudaStream_t s,
+                                     const unsigned long long* chain_src) {
     if (n_chains > kStageChains) {  // too many to stage per block: copy them first
         cudaError_t e = launch_sm_copy(chains_host, chains_dev, n_chains * sizeof(ChainDesc), s);
         if (e != cudaSuccess) return e;
-        return launch_memo_stage(src, dst, chains_dev, n_chains, total_rows, params, memo, s);
+        return launch_memo_stage(src, dst, chains_dev, n_chains, total_rows, params, memo, s, chain_src);
     }
     if (total_rows == 0) return launch_sm_copy(chains_host, chains_dev, n_chains * sizeof(ChainDesc), s);
     note_launch();
     const uint32_t blocks = (total_rows * 32 + 127) / 128;
     memo_fingerprint_kernel<<<blocks, 128, 0, s>>>(src, dst, chains_host, n_chains, total_rows, params, memo,
-                                                    chains_dev);
+                                                    chains_dev, chain_src);
     return cudaGetLastError();
 }
 
 cudaError_t launch_first_row(const uint32_t* tokens, const ChainDesc* chains, uint32_t n_chains,
                              const HashParams& params, const MemoView& memo, uint32_t* digests_out,
-                             uint32_t* flags_out, cudaStream_t s) {
+                             uint32_t* flags_out, cudaStream_t s, unsigned long long* trace,
+                             const FirstRowInline* one) {
     if (n_chains == 0) return cudaSuccess;
     if (params.chunk_size > uint32_t(kWarpChunkMax)) return cudaErrorInvalidValue;
     note_launch();
     const uint32_t blocks = (n_chains + kFirstRowWarps - 1) / kFirstRowWarps;
+    FirstRowInline none;
+    none.n = ~0u;
     first_row_kernel<<<blocks, 32 * kFirstRowWarps, 0, s>>>(tokens, chains, n_chains, params, memo, digests_out,
-                                                             flags_out);
+                                                             flags_out, trace, one ? *one : none);
     return cudaGetLastError();
 }
 

@@ -1,6 +1,7 @@
 #include "tokens.hpp"
 
 #include <algorithm>
+#include <atomic>
 #include <chrono>
 #include <cstdio>
 #include <cstdlib>
@@ -43,7 +44,9 @@ double now_us() {
 // Caller holds mu_. Returns the memo view for this launch (slots == nullptr
 // without a memo).
 MemoView KeyHasher::stage_locked(const std::vector<TokenSpanView>& seqs, const std::vector<Digest>* parents,
-                                 size_t total_tokens, size_t total_chunks, size_t max_inserts, HashParams& p) {
+                                 size_t total_tokens, size_t total_chunks, size_t max_inserts, HashParams& p,
+                                 const std::vector<const TokenId*>* mapped) {
+    if (!memo_.slots) mapped = nullptr;  // the plain path stages with copy kernels
     // Tokens, chain descriptors and digests live in mapped pinned memory and
     // move by SM loads/stores, so a lookup never queues on the copy engines
     // behind in-flight KV transfers.
@@ -53,8 +56,16 @@ MemoView KeyHasher::stage_locked(const std::vector<TokenSpanView>& seqs, const s
     auto* tok = reinterpret_cast<TokenId*>(h_tokens_.host);
     auto* ch = reinterpret_cast<ChainDesc*>(h_chains_.host);
     size_t toff = 0, row = 0;
+    unsigned long long* srcs = nullptr;
+    if (mapped) {  // the fingerprint pass reads each prompt where it already is
+        h_srcs_.reserve(seqs.size() * sizeof(unsigned long long));
+        srcs = reinterpret_cast<unsigned long long*>(h_srcs_.host);
+    }
     for (size_t i = 0; i < seqs.size(); ++i) {
-        std::copy(seqs[i].begin(), seqs[i].end(), tok + toff);
+        if (mapped)
+            srcs[i] = reinterpret_cast<unsigned long long>((*mapped)[i]);
+        else
+            std::copy(seqs[i].begin(), seqs[i].end(), tok + toff);
         ChainDesc d;
         d.token_off = toff;
         d.n_tokens = uint32_t(seqs[i].size());
@@ -96,7 +107,9 @@ MemoView KeyHasher::stage_locked(const std::vector<TokenSpanView>& seqs, const s
                                           reinterpret_cast<uint32_t*>(d_tokens_.ptr),
                                           reinterpret_cast<const ChainDesc*>(h_chains_.dev),
                                           reinterpret_cast<ChainDesc*>(d_chains_.ptr), uint32_t(seqs.size()),
-                                          uint32_t(total_chunks), p, m, stream_));
+                                          uint32_t(total_chunks), p, m, stream_,
+                                          mapped ? reinterpret_cast<const unsigned long long*>(h_srcs_.dev)
+                                                 : nullptr));
     } else {
         TKV_CUDA(launch_sm_copy(h_chains_.dev, d_chains_.ptr, ch_bytes, stream_));
         TKV_CUDA(launch_sm_copy(h_tokens_.dev, d_tokens_.ptr, tok_bytes, stream_));
@@ -230,10 +243,102 @@ void KeyHasher::presence_sync_locked(MemoView& m) {
     m.presence.n_updates = uint32_t(n);
 }
 
+// Cold-lookup fast path: row 0 of every chain in one launch (first_row
+// kernel) reading its tokens from mapped memory; the host spins on the
+// published flags. True (and `out` / `present_rows` filled) when every
+// chain's first chunk is absent: the stored prefix is then empty everywhere
+// and nothing else needs hashing. Caller holds mu_.
+bool KeyHasher::first_row_lookup(const std::vector<TokenSpanView>& seqs, const std::vector<size_t>& rows,
+                                 std::vector<std::vector<Digest>>& out, std::vector<size_t>& present_rows,
+                                 const std::function<void()>& while_waiting, bool& waited) {
+    static const bool off = std::getenv("TKV_NO_FIRST_ROW") != nullptr;  // A/B only
+    const size_t n_chains = seqs.size();
+    if (off || chunk_size_ > 256) return false;
+    const double t_pack0 = trace_lookup() ? now_us() : 0;
+    h_row0_tok_.reserve(n_chains * chunk_size_ * sizeof(TokenId) + 64);
+    h_row0_ch_.reserve(n_chains * sizeof(ChainDesc));
+    h_row0_out_.reserve(n_chains * 36 + n_chains * 32 + 64);
+    auto* tok = reinterpret_cast<TokenId*>(h_row0_tok_.host);
+    auto* ch = reinterpret_cast<ChainDesc*>(h_row0_ch_.host);
+    auto* dig = reinterpret_cast<uint32_t*>(h_row0_out_.host);
+    auto* flags = dig + 8 * n_chains;
+    for (size_t i = 0; i < n_chains; ++i) {
+        const size_t n = std::min(chunk_size_, seqs[i].size());
+        std::copy(seqs[i].begin(), seqs[i].begin() + n, tok + i * chunk_size_);
+        ChainDesc d;
+        d.token_off = i * chunk_size_;
+        d.n_tokens = uint32_t(n);
+        d.out_first = uint32_t(i);
+        ch[i] = d;
+        std::atomic_ref<uint32_t>(flags[i]).store(0, std::memory_order_relaxed);
+    }
+    HashParams p;
+    p.chunk_size = uint32_t(chunk_size_);
+    p.tag_len = uint32_t(tag_.size());
+    std::copy(tag_.begin(), tag_.end(), p.tag);
+    if (memo_used_bound_ + n_chains > memo_.entry_cap) memo_reset_locked();
+    memo_used_bound_ += n_chains;  // one link per chain at most
+    FirstRowInline one;
+    const bool inline_one = n_chains == 1;
+    if (inline_one) {
+        one.n = uint32_t(std::min(chunk_size_, seqs[0].size()));
+        std::copy(seqs[0].begin(), seqs[0].begin() + one.n, one.tok);
+    }
+    TKV_CUDA(launch_first_row(reinterpret_cast<const uint32_t*>(h_row0_tok_.dev),
+                              reinterpret_cast<const ChainDesc*>(h_row0_ch_.dev), uint32_t(n_chains), p, memo_,
+                              reinterpret_cast<uint32_t*>(h_row0_out_.dev), reinterpret_cast<uint32_t*>(h_row0_out_.dev) +
+                              8 * n_chains, stream_,
+                              trace_lookup() ? reinterpret_cast<unsigned long long*>(
+                                                   h_row0_out_.dev + ((n_chains * 36 + 7) / 8) * 8)
+                                             : nullptr,
+                              inline_one ? &one : nullptr));
+    const double t_launched = trace_lookup() ? now_us() : 0;
+    if (while_waiting) {  // the caller's host work runs under the kernel
+        while_waiting();
+        waited = true;
+    }
+    const double t_waited = trace_lookup() ? now_us() : 0;
+    // spin on the flags (a few tens of microseconds); a synchronize surfaces
+    // a failed launch instead of spinning forever
+    const double t0 = now_us();
+    for (size_t i = 0; i < n_chains;) {
+        if (std::atomic_ref<uint32_t>(flags[i]).load(std::memory_order_acquire) != 0) {
+            ++i;
+        } else if (now_us() - t0 > 2000.0) {
+            TKV_CUDA(cudaStreamSynchronize(stream_));
+            for (size_t j = i; j < n_chains; ++j)
+                if (std::atomic_ref<uint32_t>(flags[j]).load(std::memory_order_acquire) == 0)
+                    throw CudaError("first-row lookup kernel published no result");
+            break;
+        }
+    }
+    chunks_ += n_chains;
+    if (trace_lookup()) {
+        TKV_CUDA(cudaStreamSynchronize(stream_));
+        const auto* tr = reinterpret_cast<const unsigned long long*>(h_row0_out_.host + ((n_chains * 36 + 7) / 8) * 8);
+        std::fprintf(stderr, "[tkv first-row] pack+launch=%.1fus host-work=%.1fus spin=%.1fus | device: staged %.1fus "
+                     "hashed %.1fus published %.1fus\n", t_launched - t_pack0, t_waited - t_launched,
+                     now_us() - t_waited, (tr[1] - tr[0]) / 1e3, (tr[2] - tr[1]) / 1e3, (tr[3] - tr[2]) / 1e3);
+    }
+    for (size_t i = 0; i < n_chains; ++i)
+        if (rows[i] > 0 && (flags[i] & 2u)) return false;  // a first chunk is stored: the full lookup
+    ++launches_;  // the lookup's one hash pass (a fall-through counts the full pass instead)
+    for (size_t i = 0; i < n_chains; ++i) {
+        present_rows[i] = 0;
+        out[i].clear();
+        if (rows[i] == 0) continue;
+        Digest d;
+        std::memcpy(d.data(), dig + 8 * i, 32);
+        out[i].push_back(d);
+    }
+    return true;
+}
+
 std::vector<std::vector<Digest>> KeyHasher::hash_prefix(const std::vector<TokenSpanView>& seqs,
                                                         const PresentPrefix& present,
                                                         const std::function<void()>& while_waiting,
-                                                        std::vector<size_t>* present_rows) {
+                                                        std::vector<size_t>* present_rows,
+                                                        const std::vector<const TokenId*>* mapped) {
     const double t_in = trace_lookup() ? now_us() : 0;
     std::lock_guard lock(mu_);
     TKV_CUDA(cudaSetDevice(device_));
@@ -254,10 +359,36 @@ std::vector<std::vector<Digest>> KeyHasher::hash_prefix(const std::vector<TokenS
     }
     HashParams p;
     const bool on_device = memo_.slots != nullptr && presence_drain_ && present_rows != nullptr;
-    if (on_device) presence_sync_locked(memo_);  // the stage kernel applies the changes
-    // the first launch inserts at most one link per chain
-    MemoView m = stage_locked(seqs, nullptr, total_tokens, total_chunks, n_chains, p);
-    memo_.presence.n_updates = 0;  // applied once
+    if (on_device) {  // the tier's changes since the last lookup, applied first
+        presence_sync_locked(memo_);
+        TKV_CUDA(launch_presence_apply(memo_.presence, stream_));
+        memo_.presence.n_updates = 0;
+    }
+    bool waited = false;  // while_waiting already ran (during the first-row kernel)
+    // Route: a prompt whose first chunk this hasher has seen before (a host
+    // hint set of row-0 token hashes) goes straight to the full lookup — its
+    // prefix is most likely stored; a new one first asks the first-row kernel,
+    // which answers a cold prompt in one launch. Either route gives the same
+    // result; the hint only picks the faster one.
+    bool novel = false;
+    std::vector<uint64_t> row0(n_chains);
+    for (size_t i = 0; i < n_chains; ++i) {
+        uint64_t h = 0x9e3779b97f4a7c15ull ^ seqs[i].size();
+        const size_t m = std::min(chunk_size_, seqs[i].size());
+        for (size_t j = 0; j < m; ++j) h = (h ^ seqs[i][j]) * 0x100000001b3ull;
+        row0[i] = h ^ (h >> 29);
+        novel |= rows[i] > 0 && seen_row0_.count(row0[i]) == 0;
+    }
+    if (seen_row0_.size() > (1u << 20)) seen_row0_.clear();
+    for (uint64_t h : row0) seen_row0_.insert(h);
+    if (on_device && novel && first_row_lookup(seqs, rows, out, *present_rows, while_waiting, waited)) {
+        if (trace_lookup())
+            std::fprintf(stderr, "[tkv prefix] chains=%zu first-row decided in %.1fus\n", n_chains, now_us() - t_in);
+        return out;  // every first chunk absent: decided without staging the prompts
+    }
+    // the first launch inserts at most one link per chain; the prompts are
+    // read in place when the caller's mapped copies are already filled
+    MemoView m = stage_locked(seqs, nullptr, total_tokens, total_chunks, n_chains, p, waited ? mapped : nullptr);
     auto* dev_present = reinterpret_cast<uint32_t*>(h_present_.host);
     auto* dev_known = reinterpret_cast<uint32_t*>(h_known_.host);
     if (on_device) {
@@ -288,7 +419,7 @@ std::vector<std::vector<Digest>> KeyHasher::hash_prefix(const std::vector<TokenS
     TKV_CUDA(launch_memo_verify(d_tok, d_ch, uint32_t(n_chains), uint32_t(total_chunks), p, d_out_.ptr,
                                 memo_.slots ? &vm : nullptr, h_out_.dev,
                                 reinterpret_cast<unsigned int*>(h_bad_.dev), stream_));
-    if (while_waiting) while_waiting();
+    if (while_waiting && !waited) while_waiting();
     const double t_launched = trace_lookup() ? now_us() : 0;
     TKV_CUDA(cudaStreamSynchronize(stream_));
     const double t_synced = trace_lookup() ? now_us() : 0;

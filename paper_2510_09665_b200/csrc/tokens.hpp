@@ -11,6 +11,7 @@
 #include <functional>
 #include <mutex>
 #include <string>
+#include <unordered_set>
 #include <vector>
 
 #include "common.hpp"
@@ -63,10 +64,15 @@ public:
     // decide (no index, a memo hit that failed verification, a stored chunk
     // the memo had no link for), by `present` on the host.
     using PresentPrefix = std::function<size_t(const std::vector<Digest>&)>;
+    // `mapped` (optional): per sequence, a mapped pinned buffer that
+    // `while_waiting` fills with that sequence's tokens; when the lookup runs
+    // its kernels after while_waiting, they read the tokens there (no
+    // staging copy of the prompts).
     std::vector<std::vector<Digest>> hash_prefix(const std::vector<TokenSpanView>& seqs,
                                                  const PresentPrefix& present,
                                                  const std::function<void()>& while_waiting = {},
-                                                 std::vector<size_t>* present_rows = nullptr);
+                                                 std::vector<size_t>* present_rows = nullptr,
+                                                 const std::vector<const TokenId*>* mapped = nullptr);
     // A device mirror of the tier's present set (PresenceView), probed by the
     // lookup kernels (needs the memo): lookups then decide the stored prefix
     // without the host index. `drain(want_full, changes, reset)` hands over
@@ -95,7 +101,8 @@ public:
 private:
     void memo_reset_locked();
     MemoView stage_locked(const std::vector<TokenSpanView>& seqs, const std::vector<Digest>* parents,
-                          size_t total_tokens, size_t total_chunks, size_t max_inserts, HashParams& p);
+                          size_t total_tokens, size_t total_chunks, size_t max_inserts, HashParams& p,
+                          const std::vector<const TokenId*>* mapped = nullptr);
     void rehash_bad_locked(size_t n_chains, size_t total_chunks, const HashParams& p);
     std::string tag_;
     size_t chunk_size_;
@@ -107,6 +114,12 @@ private:
     uint64_t host_decided_ = 0;
     // presence index (device table) and the pending changes of one lookup
     void presence_sync_locked(MemoView& m);
+    bool first_row_lookup(const std::vector<TokenSpanView>& seqs, const std::vector<size_t>& rows,
+                          std::vector<std::vector<Digest>>& out, std::vector<size_t>& present_rows,
+                          const std::function<void()>& while_waiting, bool& waited);
+    PinnedBuffer h_row0_tok_, h_row0_ch_, h_row0_out_;  // first-row fast path (mapped)
+    PinnedBuffer h_srcs_;                               // per-chain token sources (mapped prompts)
+    std::unordered_set<uint64_t> seen_row0_;            // route hint: first chunks looked up before
     PresenceDrain presence_drain_;
     DeviceBuffer presence_table_;
     PinnedBuffer h_updates_;

@@ -189,3 +189,128 @@ def test_scenarios_with_a_late_engine_stream(tkv, C, name):
 
     got = json.loads(json.dumps(getattr(S, name)(LateEngine, C)))
     assert got == _ref_outcome(name, C)
+
+
+@pytest.mark.parametrize("late", [False, True])
+def test_two_batches_interleaved_layer_by_layer(tkv, C, late):
+    """Two scheduling iterations driven layer by layer in lockstep — batch B
+    starts loading while A still has layers to enqueue (the load ring passes
+    from A to B only after A's remaining layers are enqueued) and both store
+    at once (each takes its own store ring) — and a third that stores each
+    layer BEFORE waiting for that layer's loads, into a tier so small that it
+    evicts the very chunks it is loading (its stores must wait for those
+    loads). Every page image and every stored payload equals synth."""
+    import numpy as np
+    import torch
+    from paper_2510_09665_b200.api import Engine
+
+    class LateEngine(Engine):
+        def compute_range(self, qid, prompt, start, end, layers=None):
+            if late:
+                with torch.cuda.stream(self.stream if self.stream is not None else torch.cuda.default_stream()):
+                    torch.cuda._sleep(1_000_000)
+            super().compute_range(qid, prompt, start, end, layers)
+
+    geom = dict(S.CONN)
+    L, cs = geom["num_layers"], geom["chunk_size"]
+    seed = C.model_seed(geom["tag"])
+    e = LateEngine(**geom, ram_slots=16, num_pages=1024)
+    doc_a, doc_b = S.make_prompt(64, 501), S.make_prompt(96, 502)
+    e.seed_store(doc_a, 64)
+    e.seed_store(doc_b, 64)
+    pa = np.concatenate([doc_a, S.make_prompt(50, 503)]).astype(np.uint32)
+    pb = np.concatenate([doc_b, S.make_prompt(40, 504)]).astype(np.uint32)
+    metas = {}
+    for q, p in ((1, pa), (2, pb)):
+        mt = e.get_num_new_matched_tokens(q, p)
+        assert mt == 64
+        e.bind_pages(q, len(p))
+        assert e.update_state_after_alloc(q, (len(p) + 15) // 16, 4) == 0
+        metas[q] = e.build_connector_meta([(q, p)])
+    assert e.start_load_kv(metas[1]) == 0
+    assert e.wait_load_kv(metas[1], 0) == 0
+    assert e.start_load_kv(metas[2]) == 0  # A has layers left to enqueue
+    for layer in range(L):
+        for q, p in ((1, pa), (2, pb)):
+            assert e.wait_load_kv(metas[q], layer) == 0
+            e.compute_range(q, p, 64, len(p), layers=(layer, layer + 1))
+        for q in (1, 2):
+            if layer:
+                assert e.wait_store_kv(metas[q], layer - 1) == 0
+            assert e.start_store_kv(metas[q]) == 0  # two batches storing at once
+    for q, p in ((1, pa), (2, pb)):
+        assert e.wait_store_kv(metas[q], L - 1) == 0
+        assert e.loaded_tokens(metas[q], q) == 64
+        assert S.pages_equal_synth(e, q, p, len(p), C)
+        keys = C.chunk_keys(p, cs, geom["tag"])
+        res = e.store_results(metas[q], q)
+        assert [d for d, _ in res] == keys[2:] and all(c == 0 for _, c in res)
+        for i in range(2, len(keys)):
+            cnt = min(cs, len(p) - cs * i)
+            assert np.array_equal(e.store_get(keys[i]), C.synth_chunk(seed, p, cs * i, cnt, L, geom["bpt"]))
+        e.drop_meta(metas[q])
+        e.finish_query(q)
+        e.release_query(q)
+    e.close()
+    # a batch whose stores evict the chunks it loads, storing before waiting
+    e = LateEngine(**geom, ram_slots=2, num_pages=1024)
+    doc = S.make_prompt(64, 601)
+    e.seed_store(doc, 64)  # the tier is full: both slots hold doc's chunks
+    p = np.concatenate([doc, S.make_prompt(64, 602)]).astype(np.uint32)
+    assert e.get_num_new_matched_tokens(7, p) == 64
+    e.bind_pages(7, len(p))
+    assert e.update_state_after_alloc(7, 8, 4) == 0
+    m = e.build_connector_meta([(7, p)])
+    assert e.start_load_kv(m) == 0
+    for layer in range(L):
+        e.compute_range(7, p, 64, len(p), layers=(layer, layer + 1))
+        if layer:
+            assert e.wait_store_kv(m, layer - 1) == 0
+        assert e.start_store_kv(m) == 0  # before wait_load_kv(layer)
+        assert e.wait_load_kv(m, layer) == 0
+    assert e.wait_store_kv(m, L - 1) == 0
+    assert e.loaded_tokens(m, 7) == 64
+    assert S.pages_equal_synth(e, 7, p, len(p), C)
+    keys = C.chunk_keys(p, cs, geom["tag"])
+    assert [c for _, c in e.store_results(m, 7)] == [0, 0]
+    for i in (2, 3):
+        assert np.array_equal(e.store_get(keys[i]), C.synth_chunk(seed, p, cs * i, cs, L, geom["bpt"]))
+    assert not e.contains(keys[0]) and not e.contains(keys[1])  # the loaded chunks were evicted
+    e.drop_meta(m)
+    e.finish_query(7)
+    e.release_query(7)
+    e.close()
+
+
+def test_handles_destroyed_in_any_order(tkv, C):
+    """C-ABI handles are reference-counted: a metadata handle keeps its
+    connector (and the connector its store and pages) alive, so a caller may
+    destroy the connector, the store and the pages before a batch's metadata
+    — even with the batch's transfers still queued — without a use-after-free."""
+    from paper_2510_09665_b200.api import Engine
+    for order in ("conn_first", "pages_first"):
+        e = Engine(**S.CONN, ram_slots=16, num_pages=64)
+        prompt = S.make_prompt(96, 91)
+        e.seed_store(prompt, 64)
+        assert e.get_num_new_matched_tokens(1, prompt) == 64
+        e.bind_pages(1, 96)
+        e.update_state_after_alloc(1, 6, 4)
+        m = e.build_connector_meta([(1, prompt)])
+        assert e.start_load_kv(m) == 0
+        assert e.wait_load_kv(m, 0) == 0  # layers 1.. still to enqueue
+        e.compute_range(1, prompt, 64, 96, layers=(0, 1))
+        assert e.start_store_kv(m) == 0   # layer 0's store in flight, unsealed
+        meta = e._metas[m]
+        e._metas[m] = None  # the engine wrapper no longer owns it
+        lib_ = e.L
+        if order == "conn_first":
+            lib_.tkv_connector_destroy(e.conn)
+            lib_.tkv_store_destroy(e.store)
+            lib_.tkv_pages_destroy(e.pages)
+        else:
+            lib_.tkv_pages_destroy(e.pages)
+            lib_.tkv_store_destroy(e.store)
+            lib_.tkv_connector_destroy(e.conn)
+        e.conn = None
+        lib_.tkv_meta_destroy(meta)  # drains the batch, then frees everything
+        assert lib_.tkv_launch_count() > 0

@@ -240,9 +240,11 @@ def test_presence_index_decides_lookups_on_device(tkv, C):
     assert lookup(7, doc) == want
     assert lookup(8, other) == 511
     assert e.lookups_host_decided() == base
-    # a stored chunk the memo never linked: the device cannot decide, the host does
-    fresh = rng.integers(0, 128256, size=256 * 2, dtype=np.uint32)
-    e.seed_store(fresh, 512)                          # tier entries without memo links
-    assert lookup(9, fresh) == 511
+    # stored chunks the memo never linked: the first-row kernel links chunk 0,
+    # chunk 1 is hashed and present too, so the device cannot decide chunk 2
+    # and the host continues the chain
+    fresh = rng.integers(0, 128256, size=256 * 3, dtype=np.uint32)
+    e.seed_store(fresh, 768)                          # tier entries without memo links
+    assert lookup(9, fresh) == 767
     assert e.lookups_host_decided() == base + 1
     e.close()
