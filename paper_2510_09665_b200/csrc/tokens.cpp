@@ -388,6 +388,7 @@ std::vector<std::vector<Digest>> KeyHasher::hash_prefix(const std::vector<TokenS
     }
     // the first launch inserts at most one link per chain; the prompts are
     // read in place when the caller's mapped copies are already filled
+    const double t_routed = trace_lookup() ? now_us() : 0;
     MemoView m = stage_locked(seqs, nullptr, total_tokens, total_chunks, n_chains, p, waited ? mapped : nullptr);
     auto* dev_present = reinterpret_cast<uint32_t*>(h_present_.host);
     auto* dev_known = reinterpret_cast<uint32_t*>(h_known_.host);
@@ -503,9 +504,9 @@ std::vector<std::vector<Digest>> KeyHasher::hash_prefix(const std::vector<TokenS
         }
     }
     if (trace_lookup())
-        std::fprintf(stderr, "[tkv prefix] chains=%zu rows=%zu pack=%.1fus launch=%.1fus device+sync=%.1fus "
-                     "passes=%d rest=%.1fus\n", n_chains, total_chunks, t_packed - t_in, t_launched - t_packed,
-                     t_synced - t_launched, passes, now_us() - t_synced);
+        std::fprintf(stderr, "[tkv prefix] chains=%zu rows=%zu pre=%.1fus pack=%.1fus launch=%.1fus "
+                     "device+sync=%.1fus passes=%d rest=%.1fus\n", n_chains, total_chunks, t_routed - t_in,
+                     t_packed - t_routed, t_launched - t_packed, t_synced - t_launched, passes, now_us() - t_synced);
     return out;
 }
 
