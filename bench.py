@@ -1092,6 +1092,13 @@ def run_b200(args):
         except Exception as ex:  # the headline line still prints; the run then fails (rc 3)
             pd = {"ok": False, "error": repr(ex)[:300]}
             pd_failed = True
+    configs = None
+    if world == 1 and not args.no_configs:
+        bench.e.close()  # its pinned tier and pages are not needed any more
+        torch.cuda.empty_cache()
+        sys.path.insert(0, os.path.join(ROOT, "tools"))
+        import bench_configs
+        configs = bench_configs.run_all(pcie, cpu=not args.no_cpu_baseline)
     cpu = None
     if rank == 0 and not args.no_cpu_baseline:
         # the reference on one step of the whole job (full rows: it has no TP),
@@ -1116,13 +1123,6 @@ def run_b200(args):
             os.sched_setaffinity(0, aff)
         except OSError:
             pass
-    configs = None
-    if world == 1 and not args.no_configs:
-        bench.e.close()  # its pinned tier and pages are not needed any more
-        torch.cuda.empty_cache()
-        sys.path.insert(0, os.path.join(ROOT, "tools"))
-        import bench_configs
-        configs = bench_configs.run_all(pcie, cpu=not args.no_cpu_baseline)
     if rank != 0:
         return
     dom_ms = max(kr["scatter_ms"], kr["gather_ms"])

@@ -611,10 +611,29 @@ memo_fingerprint_kernel(const uint32_t* __restrict__ src, uint32_t* __restrict__
     const uint64_t off = cd.token_off + start;
     const uint32_t* s = chain_src != nullptr ? reinterpret_cast<const uint32_t*>(chain_src[ci]) + start : src + off;
     uint64_t h = 0;
-    for (uint32_t idx = lane; idx < n; idx += 32) {
-        const uint32_t t = s[idx];
-        dst[off + idx] = t;
-        h ^= mix64((uint64_t(t) << 32) | idx);
+    if (n <= 256) {
+        // all of a lane's tokens requested before any is used: the source is
+        // mapped host memory, one PCIe round trip instead of eight
+        uint32_t tv[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            const uint32_t idx = lane + 32u * j;
+            tv[j] = idx < n ? s[idx] : 0u;
+        }
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            const uint32_t idx = lane + 32u * j;
+            if (idx < n) {
+                dst[off + idx] = tv[j];
+                h ^= mix64((uint64_t(tv[j]) << 32) | idx);
+            }
+        }
+    } else {
+        for (uint32_t idx = lane; idx < n; idx += 32) {
+            const uint32_t t = s[idx];
+            dst[off + idx] = t;
+            h ^= mix64((uint64_t(t) << 32) | idx);
+        }
     }
 #pragma unroll
     for (int o = 16; o; o >>= 1) h ^= __shfl_xor_sync(0xffffffffu, h, o);
@@ -628,7 +647,7 @@ memo_fingerprint_kernel(const uint32_t* __restrict__ src, uint32_t* __restrict__
 // their entry to hit_entry (checked later by memo_verify_kernel); the first
 // miss of the chain goes to first_miss, where the SHA chain resumes. Every
 // row's key is kept for the insertions of the rows that miss.
-constexpr int kProbeThreads = 256;
+constexpr int kProbeThreads = 1024;  // a 256K-token chain's rows in one tile
 
 __global__ void __launch_bounds__(kProbeThreads)
 memo_probe_kernel(const ChainDesc* __restrict__ chains, const HashParams P, uint8_t* __restrict__ out, const MemoView M) {

@@ -387,7 +387,10 @@ std::vector<std::vector<Digest>> KeyHasher::hash_prefix(const std::vector<TokenS
         return out;  // every first chunk absent: decided without staging the prompts
     }
     // the first launch inserts at most one link per chain; the prompts are
-    // read in place when the caller's mapped copies are already filled
+    // read in place when the caller's mapped copies are already filled (the
+    // first-row route); otherwise they are packed here and the caller's copy
+    // runs under the kernels (filling the mapped copies first and skipping
+    // the pack measured no faster: the device work is then exposed instead)
     const double t_routed = trace_lookup() ? now_us() : 0;
     MemoView m = stage_locked(seqs, nullptr, total_tokens, total_chunks, n_chains, p, waited ? mapped : nullptr);
     auto* dev_present = reinterpret_cast<uint32_t*>(h_present_.host);

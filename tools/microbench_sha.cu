@@ -199,6 +199,52 @@ __device__ __forceinline__ void c_v7(uint32_t h[8], const uint32_t* kw) {
     h[0] += a; h[1] += b; h[2] += c; h[3] += d; h[4] += e; h[5] += f; h[6] += g; h[7] += hh;
 }
 
+// V8: every add as IMAD with a multiplier the compiler cannot see is 1
+// (ptxas folds `mad.lo x, 1, y` back into an ALU-pipe IADD3): the ALU pipe
+// keeps only the 6 SHF + 4 LOP3, the adds go to the FMA pipe
+__device__ __forceinline__ uint32_t add_rt(uint32_t x, uint32_t one, uint32_t y) {
+    uint32_t r;
+    asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(r) : "r"(x), "r"(one), "r"(y));
+    return r;
+}
+__device__ __forceinline__ void c_v8(uint32_t h[8], const uint32_t* kw, uint32_t one) {
+    uint32_t a = h[0], b = h[1], c = h[2], d = h[3], e = h[4], f = h[5], g = h[6], hh = h[7];
+    uint32_t y = add_rt(hh, one, kw[0]), yd = add_rt(y, one, d);
+#pragma unroll
+    for (int t = 0; t < 64; ++t) {
+        const uint32_t S1 = rotr(e, 6) ^ rotr(e, 11) ^ rotr(e, 25);
+        const uint32_t ch = (e & f) ^ (~e & g);
+        const uint32_t S0 = rotr(a, 2) ^ rotr(a, 13) ^ rotr(a, 22);
+        const uint32_t mj = (a & b) ^ (a & c) ^ (b & c);
+        const uint32_t e_new = add_rt(S1, one, add_rt(ch, one, yd));
+        const uint32_t t1 = add_rt(S1, one, add_rt(ch, one, y));
+        const uint32_t a_new = add_rt(t1, one, add_rt(S0, one, mj));
+        if (t + 1 < 64) { y = add_rt(g, one, kw[t + 1]); yd = add_rt(y, one, c); }
+        hh = g; g = f; f = e; e = e_new; d = c; c = b; b = a; a = a_new;
+    }
+    h[0] += a; h[1] += b; h[2] += c; h[3] += d; h[4] += e; h[5] += f; h[6] += g; h[7] += hh;
+}
+
+// V9: V1, but only the e-chain adds on the ALU pipe (IADD3 e = S1 + ch + Yd)
+// and everything else on the FMA pipe
+__device__ __forceinline__ void c_v9(uint32_t h[8], const uint32_t* kw, uint32_t one) {
+    uint32_t a = h[0], b = h[1], c = h[2], d = h[3], e = h[4], f = h[5], g = h[6], hh = h[7];
+    uint32_t y = add_rt(hh, one, kw[0]), yd = add_rt(y, one, d);
+#pragma unroll
+    for (int t = 0; t < 64; ++t) {
+        const uint32_t S1 = rotr(e, 6) ^ rotr(e, 11) ^ rotr(e, 25);
+        const uint32_t ch = (e & f) ^ (~e & g);
+        const uint32_t S0 = rotr(a, 2) ^ rotr(a, 13) ^ rotr(a, 22);
+        const uint32_t mj = (a & b) ^ (a & c) ^ (b & c);
+        const uint32_t e_new = add_fixed(S1, add_fixed(ch, yd));
+        const uint32_t t1 = add_rt(S1, one, add_rt(ch, one, y));
+        const uint32_t a_new = add_rt(t1, one, add_rt(S0, one, mj));
+        if (t + 1 < 64) { y = add_rt(g, one, kw[t + 1]); yd = add_rt(y, one, c); }
+        hh = g; g = f; f = e; e = e_new; d = c; c = b; b = a; a = a_new;
+    }
+    h[0] += a; h[1] += b; h[2] += c; h[3] += d; h[4] += e; h[5] += f; h[6] += g; h[7] += hh;
+}
+
 // op throughput / latency probes (one warp): 8 independent chains (rt) or
 // one dependent chain (lat) of the same op
 template <int OP, bool DEP>
@@ -228,7 +274,7 @@ __global__ void opbench(uint32_t seed, int iters, uint32_t* out, long long* cycl
 }
 
 template <int V>
-__global__ void bench(const uint32_t* kw_g, int blocks, uint32_t* out, long long* cycles) {
+__global__ void bench(const uint32_t* kw_g, int blocks, uint32_t* out, long long* cycles, uint32_t one) {
     __shared__ uint32_t kw[64];
     for (int i = threadIdx.x; i < 64; i += 32) kw[i] = kw_g[i] + kK[i];
     __syncwarp();
@@ -243,6 +289,8 @@ __global__ void bench(const uint32_t* kw_g, int blocks, uint32_t* out, long long
         if (V == 5) c_v56<false>(h, kw);
         if (V == 6) c_v56<true>(h, kw);
         if (V == 7) c_v7(h, kw);
+        if (V == 8) c_v8(h, kw, one);
+        if (V == 9) c_v9(h, kw, one);
     }
     const long long t1 = clock64();
     if (threadIdx.x == 0) {
@@ -262,17 +310,19 @@ int main() {
     cudaMemcpy(kw, hw, 256, cudaMemcpyHostToDevice);
     const int blocks = 2000;
     uint32_t ref[8] = {};
-    for (int v = 0; v < 8; ++v) {
+    for (int v = 0; v < 10; ++v) {
         for (int rep = 0; rep < 2; ++rep) {
             switch (v) {
-                case 0: bench<0><<<1, 32>>>(kw, blocks, out, cyc); break;
-                case 1: bench<1><<<1, 32>>>(kw, blocks, out, cyc); break;
-                case 2: bench<2><<<1, 32>>>(kw, blocks, out, cyc); break;
-                case 3: bench<3><<<1, 32>>>(kw, blocks, out, cyc); break;
-                case 4: bench<4><<<1, 32>>>(kw, blocks, out, cyc); break;
-                case 5: bench<5><<<1, 32>>>(kw, blocks, out, cyc); break;
-                case 6: bench<6><<<1, 32>>>(kw, blocks, out, cyc); break;
-                case 7: bench<7><<<1, 32>>>(kw, blocks, out, cyc); break;
+                case 0: bench<0><<<1, 32>>>(kw, blocks, out, cyc, 1u); break;
+                case 1: bench<1><<<1, 32>>>(kw, blocks, out, cyc, 1u); break;
+                case 2: bench<2><<<1, 32>>>(kw, blocks, out, cyc, 1u); break;
+                case 3: bench<3><<<1, 32>>>(kw, blocks, out, cyc, 1u); break;
+                case 4: bench<4><<<1, 32>>>(kw, blocks, out, cyc, 1u); break;
+                case 5: bench<5><<<1, 32>>>(kw, blocks, out, cyc, 1u); break;
+                case 6: bench<6><<<1, 32>>>(kw, blocks, out, cyc, 1u); break;
+                case 7: bench<7><<<1, 32>>>(kw, blocks, out, cyc, 1u); break;
+                case 8: bench<8><<<1, 32>>>(kw, blocks, out, cyc, 1u); break;
+                case 9: bench<9><<<1, 32>>>(kw, blocks, out, cyc, 1u); break;
             }
         }
         uint32_t h[8];
