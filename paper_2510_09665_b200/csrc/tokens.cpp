@@ -50,7 +50,8 @@ MemoView KeyHasher::stage_locked(const std::vector<TokenSpanView>& seqs, const s
     // Tokens, chain descriptors and digests live in mapped pinned memory and
     // move by SM loads/stores, so a lookup never queues on the copy engines
     // behind in-flight KV transfers.
-    h_tokens_.reserve(total_tokens * sizeof(TokenId) + 64);
+    // each chain starts on a 16-byte boundary (vector loads of full rows)
+    h_tokens_.reserve((total_tokens + 4 * seqs.size()) * sizeof(TokenId) + 64);
     h_chains_.reserve(seqs.size() * sizeof(ChainDesc));
     h_out_.reserve(total_chunks * 32);
     auto* tok = reinterpret_cast<TokenId*>(h_tokens_.host);
@@ -62,6 +63,7 @@ MemoView KeyHasher::stage_locked(const std::vector<TokenSpanView>& seqs, const s
         srcs = reinterpret_cast<unsigned long long*>(h_srcs_.host);
     }
     for (size_t i = 0; i < seqs.size(); ++i) {
+        toff = (toff + 3) & ~size_t(3);
         if (mapped)
             srcs[i] = reinterpret_cast<unsigned long long>((*mapped)[i]);
         else
@@ -79,7 +81,7 @@ MemoView KeyHasher::stage_locked(const std::vector<TokenSpanView>& seqs, const s
     p.tag_len = uint32_t(tag_.size());
     std::copy(tag_.begin(), tag_.end(), p.tag);
 
-    const size_t tok_bytes = total_tokens * sizeof(TokenId);
+    const size_t tok_bytes = toff * sizeof(TokenId);
     const size_t ch_bytes = seqs.size() * sizeof(ChainDesc);
     d_tokens_.reserve(tok_bytes + 64);
     d_chains_.reserve(ch_bytes + 64);
