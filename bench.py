@@ -63,6 +63,10 @@ TAG = "llama-3.1-70b"
 
 
 def parse():
+    return parse_args_list(None)
+
+
+def parse_args_list(argv):
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=10)
@@ -84,7 +88,7 @@ def parse():
     ap.add_argument("--memo-entries", type=int, default=None, help="K3 prefix memo links (0 = off)")
     ap.add_argument("--sequential", action="store_true",
                     help="one request at a time (no overlap of consecutive steps)")
-    return ap.parse_args()
+    return ap.parse_args(argv)
 
 
 def dist_env():

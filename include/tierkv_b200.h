@@ -386,7 +386,9 @@ int tkv_pd_send(tkv_pages* src, uint64_t query, size_t n_tokens, size_t chunk_si
  * the landing buffer, ordered after the work already queued on
  * engine_stream (the prefill's compute of layer l), on the sender's own
  * stream; finish waits for every layer (invalid_argument if one was not
- * sent) and returns the records to push to the decoder's PdStaging. */
+ * sent) and returns the records to push to the decoder's PdStaging. The
+ * landing memory must be ready before the first layer (the sender's stream
+ * is ordered only after engine_stream). */
 typedef struct tkv_pd_sender tkv_pd_sender;
 int tkv_pd_sender_begin(tkv_pages* src, uint64_t query, size_t n_tokens, size_t unit_tokens, uint64_t landing,
                         uint64_t unit_stride, tkv_pd_sender** out);

@@ -43,8 +43,15 @@ size_t TieredStore::presence_subscribe() {
 }
 
 void TieredStore::presence_changed(const Digest& d, bool present) {
-    for (auto& f : feeds_)
-        if (!f->fresh) f->pending[d] = present;
+    const size_t cap = 4 * std::max<size_t>(256, slab_slots());
+    for (auto& f : feeds_) {
+        if (f->fresh) continue;
+        f->pending[d] = present;
+        if (f->pending.size() > cap) {  // a subscriber that stopped draining: resync from a snapshot
+            f->pending.clear();
+            f->fresh = true;
+        }
+    }
 }
 
 void TieredStore::presence_drain(size_t id, bool want_full, std::vector<std::pair<Digest, bool>>& out,

@@ -141,6 +141,7 @@ def test_pd_layer_streamed_page_and_chunk_granularity(tkv, C, late):
         stride = L * unit * bpt
         n_units = (n + unit - 1) // unit
         landing = torch.zeros(n_units * stride, dtype=torch.uint8, device="cuda")
+        torch.cuda.synchronize()  # the sender's own stream is not ordered after torch's fill
         snd = PdLayerSender(pre, 20, n, unit, landing.data_ptr(), stride)
         for layer in range(L):
             if late:
@@ -177,6 +178,7 @@ def test_pd_layer_streamed_page_and_chunk_granularity(tkv, C, late):
     # sending a layer the engine has not computed is refused (check_readable)
     pre.bind_pages(21, n)
     buf = torch.zeros(L * n * bpt, dtype=torch.uint8, device="cuda")
+    torch.cuda.synchronize()
     snd = PdLayerSender(pre, 21, n, pt, buf.data_ptr(), L * pt * bpt)
     assert snd.layer(0) == 7  # unpopulated_page
     assert snd.layer(L) == 16  # invalid_argument: out of range
