@@ -165,6 +165,7 @@ def test_layerwise_beats_blocking_when_load_matches_compute(tkv):
             times.append(total)
         avg[layerwise] = float(np.mean(times))
         e.close()
+    print(f"layerwise / blocking = {avg[True] / avg[False]:.3f} (per-layer load {per_layer_ms:.2f} ms)")
     assert avg[True] < 0.85 * avg[False], (avg, per_layer_ms)
 
 
@@ -187,4 +188,5 @@ def test_warm_backend_cuts_ttft(tkv):
     warm, _, lo_w = _query(ce, 3, prompt)
     e.close()
     assert lo_c == 0 and lo_w == n - 1
+    print(f"warm / cold TTFT = {warm / cold:.3f} ({1e3 * warm:.1f} / {1e3 * cold:.1f} ms)")
     assert warm < 0.5 * cold, (warm, cold)
