@@ -18,6 +18,7 @@
 // device-visible address.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdint>
 #include <cstdlib>
 #include <cstring>
@@ -283,6 +284,150 @@ paged_copy_units_kernel(const PagedLayout L, const PagedCopyPlan P, const int di
     }
 }
 
+// ---- bulk-copy (TMA) variant of the unit kernel ------------------------------
+//
+// Same units and per-warp ranges as paged_copy_units_kernel, but the bytes
+// move through the copy engine of the SM (cp.async.bulk): lane 0 of each warp
+// keeps kBulkStages units in flight — a bulk load global -> shared (completion
+// on an mbarrier with the byte count), then a bulk store shared -> global —
+// and no thread touches the data. Selected with TKV_PAGED_KERNEL=bulk (A/B,
+// profiles/r02_k12_layers_bulk.jsonl); the LSU version is the default.
+constexpr int kBulkWarps = 4;
+constexpr int kBulkStages = 4;
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__global__ void __launch_bounds__(32 * kBulkWarps)
+paged_copy_bulk_kernel(const PagedLayout L, const PagedCopyPlan P, const int dir, const uint32_t parts,
+                       const uint32_t part_bytes) {
+    extern __shared__ __align__(128) uint8_t bulk_smem[];
+    const uint32_t lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    if (lane != 0) return;  // one issuing thread per warp; the SM's bulk-copy unit moves the bytes
+    uint8_t* buf = bulk_smem + size_t(wid) * kBulkStages * kUnitBytes;
+    __shared__ __align__(8) unsigned long long bars[kBulkWarps][kBulkStages];
+    for (int st = 0; st < kBulkStages; ++st)
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&bars[wid][st])) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+
+    const uint32_t nl = P.n_layers;
+    auto prefix = [&](uint32_t d) { return __ldg(P.tile_base + d) / nl; };
+    const uint32_t pages1 = __ldg(P.tile_base + P.n_desc) / nl;
+    const uint32_t total = pages1 * nl * parts;
+    const uint32_t warps = gridDim.x * kBulkWarps;
+    const uint32_t w = blockIdx.x * kBulkWarps + wid;
+    const uint32_t u0 = uint32_t(uint64_t(total) * w / warps);
+    const uint32_t u1 = uint32_t(uint64_t(total) * (w + 1) / warps);
+    if (u0 >= u1) return;
+    // unit -> (src, dst, bytes), stepping like the unit kernel
+    uint32_t g = u0 / parts, q = u0 - (u0 / parts) * parts;
+    uint32_t ll = g / pages1, g1 = g - ll * pages1;
+    uint32_t lo = 0, hi = P.n_desc;
+    while (hi - lo > 1) {
+        const uint32_t mid = (lo + hi) >> 1;
+        if (prefix(mid) <= g1) lo = mid; else hi = mid;
+    }
+    uint32_t next_base = prefix(lo + 1);
+    const uint8_t* page_p = nullptr;
+    uint64_t chunk = 0;
+    uint32_t page_valid = 0;
+    bool fresh = true;
+    auto next = [&](const uint8_t*& src, uint8_t*& dst, uint32_t& bytes) {
+        for (;;) {
+            if (fresh) {
+                const XferDesc* dp = P.descs + lo;
+                const uint32_t j = g1 - prefix(lo);
+                page_valid = min(L.page_tokens, __ldg(&dp->n_tokens) - j * L.page_tokens) * L.bpt;
+                const uint32_t layer = P.layer_begin + ll;
+                const int32_t* table = reinterpret_cast<const int32_t*>(
+                    __ldg(reinterpret_cast<const unsigned long long*>(&dp->table)));
+                const uint32_t page = uint32_t(__ldg(table + uint64_t(L.shared_table ? 0 : layer) * __ldg(&dp->table_stride) +
+                                                     __ldg(&dp->first_page) + j));
+                const uint64_t pbase =
+                    L.layer_base ? __ldg(reinterpret_cast<const unsigned long long*>(L.layer_base) + layer) : L.base;
+                page_p = reinterpret_cast<const uint8_t*>(pbase + uint64_t(page) * L.page_stride);
+                chunk = __ldg(reinterpret_cast<const unsigned long long*>(&dp->chunk)) +
+                        uint64_t(layer) * __ldg(reinterpret_cast<const unsigned long long*>(&dp->layer_stride)) +
+                        uint64_t(j) * L.page_tokens * L.bpt;
+                fresh = false;
+            }
+            const uint32_t begin = q * part_bytes;
+            const uint32_t end = min(begin + part_bytes, page_valid);
+            const bool have = begin < end;
+            if (have) {
+                src = dir == int(CopyDir::gather) ? page_p + begin : reinterpret_cast<const uint8_t*>(chunk + begin);
+                dst = dir == int(CopyDir::gather) ? reinterpret_cast<uint8_t*>(chunk + begin)
+                                                  : const_cast<uint8_t*>(page_p + begin);
+                bytes = end - begin;
+            }
+            if (++q == parts) {
+                q = 0;
+                fresh = true;
+                if (++g1 == pages1) {
+                    g1 = 0;
+                    ++ll;
+                    lo = 0;
+                    next_base = ll < nl ? prefix(1) : 0;
+                }
+                while (ll < nl && g1 >= next_base) next_base = prefix(++lo + 1);
+            }
+            if (have) return true;
+            if (ll >= nl) return false;
+        }
+    };
+    uint32_t limit = u1 - u0;  // units of this warp (a trailing empty part ends it early)
+    uint8_t* dsts[kBulkStages];
+    uint32_t sizes[kBulkStages];
+    uint32_t issued = 0;
+    auto issue_load = [&](uint32_t i) -> bool {
+        const uint8_t* src;
+        uint8_t* dst;
+        uint32_t bytes;
+        if (!next(src, dst, bytes)) return false;
+        const int st = int(i % kBulkStages);
+        dsts[st] = dst;
+        sizes[st] = bytes;
+        const uint32_t bar = smem_u32(&bars[wid][st]);
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+        asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                         smem_u32(buf + size_t(st) * kUnitBytes)),
+                     "l"(src), "r"(bytes), "r"(bar)
+                     : "memory");
+        return true;
+    };
+    // prologue: up to kBulkStages loads in flight
+    while (issued < kBulkStages && issued < limit) {
+        if (!issue_load(issued)) {
+            limit = issued;
+            break;
+        }
+        ++issued;
+    }
+    for (uint32_t done = 0; done < issued; ++done) {
+        const int st = int(done % kBulkStages);
+        const uint32_t phase = (done / kBulkStages) & 1;
+        const uint32_t bar = smem_u32(&bars[wid][st]);
+        uint32_t ok = 0;
+        while (!ok)
+            asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+                         : "=r"(ok) : "r"(bar), "r"(phase) : "memory");
+        asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dsts[st]),
+                     "r"(smem_u32(buf + size_t(st) * kUnitBytes)), "r"(sizes[st])
+                     : "memory");
+        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+        if (issued < limit) {
+            // the stage is reused once its store has read it
+            asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+            if (issue_load(issued))
+                ++issued;
+            else
+                limit = issued;
+        }
+    }
+    asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+
 template <int W, bool CONTIG>
 cudaError_t launch_w(const PagedLayout& L, const PagedCopyPlan& P, CopyDir dir, int ctas,
                      cudaStream_t s) {
@@ -320,6 +465,10 @@ cudaError_t launch_paged_copy(const PagedLayout& L, const PagedCopyPlan& P, Copy
         const char* v = std::getenv("TKV_PAGED_KERNEL");
         return v != nullptr && std::strcmp(v, "tile") == 0;
     }();
+    static const bool use_bulk = [] {
+        const char* v = std::getenv("TKV_PAGED_KERNEL");
+        return v != nullptr && std::strcmp(v, "bulk") == 0;
+    }();
     // Unit kernel for launches up to kUnitMaxBytes (one layer of a batch);
     // bigger ones (all layers at once) keep the tile kernel, whose sweep over
     // consecutive tiles measured faster at that size (1.04 vs 0.95 of peak
@@ -333,6 +482,16 @@ cudaError_t launch_paged_copy(const PagedLayout& L, const PagedCopyPlan& P, Copy
             const uint64_t want = (units + kThreads / 32 - 1) / (kThreads / 32);  // at least one unit per warp
             if (uint64_t(ctas) > want) ctas = int(want);
             note_launch();
+            if (use_bulk) {
+                const size_t smem = size_t(kBulkWarps) * kBulkStages * kUnitBytes;
+                static const cudaError_t attr = cudaFuncSetAttribute(
+                    paged_copy_bulk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+                if (attr != cudaSuccess) return attr;
+                const uint64_t bwant = (units + kBulkWarps - 1) / kBulkWarps;
+                const int bctas = int(std::min<uint64_t>(bwant, uint64_t(3 * sm_count())));
+                paged_copy_bulk_kernel<<<bctas, 32 * kBulkWarps, smem, stream>>>(L, P, int(dir), parts, part_bytes);
+                return cudaGetLastError();
+            }
             paged_copy_units_kernel<<<ctas, kThreads, 0, stream>>>(L, P, int(dir), parts, part_bytes);
             return cudaGetLastError();
         }

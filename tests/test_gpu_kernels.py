@@ -431,3 +431,19 @@ def test_vllm_slot_mapping(tkv, direction):
             want = before[layer].copy()
             want[:, slots] = chunk_before[layer].transpose(1, 0, 2)
             assert np.array_equal(kv[layer].cpu().numpy().reshape(2, n_slots, hd), want)
+
+
+def test_bulk_variant_gather_scatter_subprocess():
+    """The bulk-copy (cp.async.bulk) variant of the unit kernel is selected
+    by an environment switch read once per process: run the unit-kernel
+    parity cases in a child process with TKV_PAGED_KERNEL=bulk."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, TKV_PAGED_KERNEL="bulk")
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-m", "gpu",
+                        "tests/test_gpu_kernels.py::test_unit_kernel_gather_scatter",
+                        "tests/test_gpu_kernels.py::test_vllm_slot_mapping"],
+                       cwd=root, env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
