@@ -447,3 +447,12 @@ def test_bulk_variant_gather_scatter_subprocess():
                         "tests/test_gpu_kernels.py::test_vllm_slot_mapping"],
                        cwd=root, env=env, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
+
+
+def test_unit_kernel_many_descriptors(tkv, C):
+    """More descriptors than the unit kernel keeps in shared memory (4096):
+    the descriptor search runs on the global prefix. 4500 one-page
+    descriptors (ragged: 1-16 tokens), one-layer launches per layer."""
+    rng = np.random.default_rng(4500)
+    spans = [(0, int(rng.integers(1, 17)), 16) for _ in range(4500)]  # each its own one-page table
+    _multi_layer_case(tkv, C, 64, 2, spans, seed=4501, ppt=1, per_layer=True)
