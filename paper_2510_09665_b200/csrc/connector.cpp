@@ -257,6 +257,12 @@ Connector::~Connector() {
 // pinned memory (the lookup kernels read the prompt from the query state
 // itself, no second staging copy), whose allocation and release are slow and
 // can synchronize the device. Caller holds mu_.
+size_t Connector::prompt_capacity(size_t n) {
+    size_t c = 4096;
+    while (c < n) c <<= 1;
+    return c;
+}
+
 void Connector::recycle_prompt(PinnedTokens&& v) {
     if (v.capacity() == 0 || prompt_pool_.size() >= 256) return;
     v.clear();
@@ -280,6 +286,7 @@ const std::vector<ChunkKey>& Connector::keys_for(QueryState& qs, TokenSpanView p
     // absent chunk (the memo serves the part it already hashed).
     if (qs.keys.size() != rows || qs.prompt.size() != prompt.size() ||
         !std::equal(prompt.begin(), prompt.end(), qs.prompt.begin())) {
+        if (qs.prompt.capacity() < prompt.size()) qs.prompt.reserve(prompt_capacity(prompt.size()));
         qs.prompt.assign(prompt.begin(), prompt.end());
         qs.keys = chunk_keys(hasher_, prompt);
     }
@@ -303,7 +310,10 @@ std::vector<size_t> Connector::get_num_new_matched_tokens(
         std::lock_guard lock(mu_);
         for (size_t q = 0; q < ids.size(); ++q) {
             recycle_prompt_into(staged[q], prompts[q].size());
-            staged[q].reserve(prompts[q].size());  // assign() below keeps this buffer
+            // power-of-two capacity: prompts of varying length reuse pooled
+            // buffers instead of allocating pinned memory (which waits for the
+            // device) on the lookup path; assign() below keeps this buffer
+            staged[q].reserve(prompt_capacity(prompts[q].size()));
             mapped[q] = staged[q].data();
         }
     }

@@ -178,6 +178,7 @@ private:
 
     const std::vector<ChunkKey>& keys_for(QueryState& qs, TokenSpanView prompt);
     size_t ring_growth(size_t need, size_t current, uint32_t depth) const;
+    static size_t prompt_capacity(size_t n);  // pooled prompt buffers: power-of-two tokens
     void recycle_prompt(PinnedTokens&& v);
     void recycle_prompt_into(PinnedTokens& dst, size_t n);
     std::vector<PinnedTokens> prompt_pool_;  // guarded by mu_

@@ -29,6 +29,16 @@ KeyHasher::KeyHasher(std::string model_tag, size_t chunk_size, int device)
 }
 
 namespace {
+// Size for a per-call buffer: the next power of two (64 KiB at least), so
+// prompts of varying length do not regrow it — a regrowth calls cudaMalloc /
+// cudaHostAlloc, which wait for the device (behind whatever KV transfers are
+// in flight: a 120 ms stall was traced in config 4 before this).
+size_t grow(size_t n) {
+    size_t p = size_t(64) << 10;
+    while (p < n) p <<= 1;
+    return p;
+}
+
 // TKV_TRACE_LOOKUP=1: host-side phase times of every hash() call on stderr.
 bool trace_lookup() {
     static const bool on = std::getenv("TKV_TRACE_LOOKUP") != nullptr;
@@ -51,15 +61,15 @@ MemoView KeyHasher::stage_locked(const std::vector<TokenSpanView>& seqs, const s
     // move by SM loads/stores, so a lookup never queues on the copy engines
     // behind in-flight KV transfers.
     // each chain starts on a 16-byte boundary (vector loads of full rows)
-    h_tokens_.reserve((total_tokens + 4 * seqs.size()) * sizeof(TokenId) + 64);
-    h_chains_.reserve(seqs.size() * sizeof(ChainDesc));
-    h_out_.reserve(total_chunks * 32);
+    h_tokens_.reserve(grow((total_tokens + 4 * seqs.size()) * sizeof(TokenId) + 64));
+    h_chains_.reserve(grow(seqs.size() * sizeof(ChainDesc)));
+    h_out_.reserve(grow(total_chunks * 32));
     auto* tok = reinterpret_cast<TokenId*>(h_tokens_.host);
     auto* ch = reinterpret_cast<ChainDesc*>(h_chains_.host);
     size_t toff = 0, row = 0;
     unsigned long long* srcs = nullptr;
     if (mapped) {  // the fingerprint pass reads each prompt where it already is
-        h_srcs_.reserve(seqs.size() * sizeof(unsigned long long));
+        h_srcs_.reserve(grow(seqs.size() * sizeof(unsigned long long)));
         srcs = reinterpret_cast<unsigned long long*>(h_srcs_.host);
     }
     for (size_t i = 0; i < seqs.size(); ++i) {
@@ -83,11 +93,11 @@ MemoView KeyHasher::stage_locked(const std::vector<TokenSpanView>& seqs, const s
 
     const size_t tok_bytes = toff * sizeof(TokenId);
     const size_t ch_bytes = seqs.size() * sizeof(ChainDesc);
-    d_tokens_.reserve(tok_bytes + 64);
-    d_chains_.reserve(ch_bytes + 64);
-    d_out_.reserve(total_chunks * 32);
-    h_bad_.reserve(seqs.size() * sizeof(unsigned int));
-    h_first_.reserve(seqs.size() * sizeof(uint32_t));
+    d_tokens_.reserve(grow(tok_bytes + 64));
+    d_chains_.reserve(grow(ch_bytes + 64));
+    d_out_.reserve(grow(total_chunks * 32));
+    h_bad_.reserve(grow(seqs.size() * sizeof(unsigned int)));
+    h_first_.reserve(grow(seqs.size() * sizeof(uint32_t)));
     auto* bad = reinterpret_cast<unsigned int*>(h_bad_.host);
     std::fill(bad, bad + seqs.size(), ~0u);
     MemoView m = memo_;
@@ -96,9 +106,9 @@ MemoView KeyHasher::stage_locked(const std::vector<TokenSpanView>& seqs, const s
         // before the probe, never invalidates a hit this call relies on.
         if (memo_used_bound_ + max_inserts > memo_.entry_cap) memo_reset_locked();
         memo_used_bound_ += max_inserts;
-        d_hit_.reserve(total_chunks * sizeof(uint32_t));
-        d_keys_.reserve(total_chunks * sizeof(unsigned long long));
-        d_first_.reserve(seqs.size() * sizeof(uint32_t));
+        d_hit_.reserve(grow(total_chunks * sizeof(uint32_t)));
+        d_keys_.reserve(grow(total_chunks * sizeof(unsigned long long)));
+        d_first_.reserve(grow(seqs.size() * sizeof(uint32_t)));
         m = memo_;
         m.hit_entry = reinterpret_cast<uint32_t*>(d_hit_.ptr);
         m.keys = reinterpret_cast<unsigned long long*>(d_keys_.ptr);
@@ -142,8 +152,8 @@ void KeyHasher::rehash_bad_locked(size_t n_chains, size_t total_chunks, const Ha
     // the redo descriptors go after the launch's own (d_chains_ keeps those)
     std::vector<ChainDesc> all(ch, ch + n_chains);
     all.insert(all.end(), redo.begin(), redo.end());
-    h_chains_.reserve(all.size() * sizeof(ChainDesc));
-    d_chains_.reserve(all.size() * sizeof(ChainDesc) + 64);
+    h_chains_.reserve(grow(all.size() * sizeof(ChainDesc)));
+    d_chains_.reserve(grow(all.size() * sizeof(ChainDesc) + 64));
     ch = reinterpret_cast<ChainDesc*>(h_chains_.host);
     std::copy(all.begin(), all.end(), ch);
     TKV_CUDA(launch_sm_copy(h_chains_.dev, d_chains_.ptr, all.size() * sizeof(ChainDesc), stream_));
@@ -233,7 +243,7 @@ void KeyHasher::presence_sync_locked(MemoView& m) {
     }
     presence_used_ += adds;
     const size_t n = presence_pending_.size();
-    h_updates_.reserve(std::max<size_t>(1, n) * 36);
+    h_updates_.reserve(grow(std::max<size_t>(1, n) * 36));
     auto* w = reinterpret_cast<uint32_t*>(h_updates_.host);
     for (size_t i = 0; i < n; ++i) {
         std::memcpy(w + 9 * i, presence_pending_[i].first.data(), 32);
@@ -257,9 +267,9 @@ bool KeyHasher::first_row_lookup(const std::vector<TokenSpanView>& seqs, const s
     const size_t n_chains = seqs.size();
     if (off || chunk_size_ > 256) return false;
     const double t_pack0 = trace_lookup() ? now_us() : 0;
-    h_row0_tok_.reserve(n_chains * chunk_size_ * sizeof(TokenId) + 64);
-    h_row0_ch_.reserve(n_chains * sizeof(ChainDesc));
-    h_row0_out_.reserve(n_chains * 36 + n_chains * 32 + 64);
+    h_row0_tok_.reserve(grow(n_chains * chunk_size_ * sizeof(TokenId) + 64));
+    h_row0_ch_.reserve(grow(n_chains * sizeof(ChainDesc)));
+    h_row0_out_.reserve(grow(n_chains * 36 + n_chains * 32 + 64));
     auto* tok = reinterpret_cast<TokenId*>(h_row0_tok_.host);
     auto* ch = reinterpret_cast<ChainDesc*>(h_row0_ch_.host);
     auto* dig = reinterpret_cast<uint32_t*>(h_row0_out_.host);
@@ -375,8 +385,9 @@ std::vector<std::vector<Digest>> KeyHasher::hash_prefix(const std::vector<TokenS
     bool novel = false;
     std::vector<uint64_t> row0(n_chains);
     for (size_t i = 0; i < n_chains; ++i) {
-        uint64_t h = 0x9e3779b97f4a7c15ull ^ seqs[i].size();
+        // the first chunk's tokens only (prompts sharing a document differ after it)
         const size_t m = std::min(chunk_size_, seqs[i].size());
+        uint64_t h = 0x9e3779b97f4a7c15ull ^ m;
         for (size_t j = 0; j < m; ++j) h = (h ^ seqs[i][j]) * 0x100000001b3ull;
         row0[i] = h ^ (h >> 29);
         novel |= rows[i] > 0 && seen_row0_.count(row0[i]) == 0;
@@ -398,8 +409,8 @@ std::vector<std::vector<Digest>> KeyHasher::hash_prefix(const std::vector<TokenS
     auto* dev_present = reinterpret_cast<uint32_t*>(h_present_.host);
     auto* dev_known = reinterpret_cast<uint32_t*>(h_known_.host);
     if (on_device) {
-        h_present_.reserve(n_chains * sizeof(uint32_t));
-        h_known_.reserve(n_chains * sizeof(uint32_t));
+        h_present_.reserve(grow(n_chains * sizeof(uint32_t)));
+        h_known_.reserve(grow(n_chains * sizeof(uint32_t)));
         dev_present = reinterpret_cast<uint32_t*>(h_present_.host);
         dev_known = reinterpret_cast<uint32_t*>(h_known_.host);
         m.lookup.present_out = reinterpret_cast<uint32_t*>(h_present_.dev);
@@ -477,8 +488,8 @@ std::vector<std::vector<Digest>> KeyHasher::hash_prefix(const std::vector<TokenS
         ++passes;
         std::vector<ChainDesc> all(ch, ch + n_chains);
         all.insert(all.end(), more.begin(), more.end());
-        h_chains_.reserve(all.size() * sizeof(ChainDesc));
-        d_chains_.reserve(all.size() * sizeof(ChainDesc) + 64);
+        h_chains_.reserve(grow(all.size() * sizeof(ChainDesc)));
+        d_chains_.reserve(grow(all.size() * sizeof(ChainDesc) + 64));
         std::copy(all.begin(), all.end(), reinterpret_cast<ChainDesc*>(h_chains_.host));
         ch = reinterpret_cast<const ChainDesc*>(h_chains_.host);
         d_ch = reinterpret_cast<const ChainDesc*>(d_chains_.ptr);
