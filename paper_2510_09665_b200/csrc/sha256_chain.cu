@@ -825,6 +825,14 @@ first_row_kernel(const uint32_t* __restrict__ tokens, const ChainDesc* __restric
     __shared__ FirstRowSmem smem[kFirstRowWarps];
     unsigned long long t_start = 0, t_staged = 0, t_hashed = 0;
     if (trace != nullptr) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
+    // pending presence changes (only when the launch is one CTA: the host
+    // launches presence_apply_kernel first otherwise)
+    if (M.presence.n_updates != 0) {
+        for (uint32_t u = threadIdx.x; u < M.presence.n_updates; u += blockDim.x)
+            presence_apply(M.presence, M.presence.updates + 9ull * u);
+        __threadfence_block();
+        __syncthreads();
+    }
     const uint32_t lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const uint32_t c = blockIdx.x * kFirstRowWarps + wid;
     if (c >= n_chains) return;

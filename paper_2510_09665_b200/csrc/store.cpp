@@ -42,13 +42,48 @@ size_t TieredStore::presence_subscribe() {
     return feeds_.size() - 1;
 }
 
+void TieredStore::PresenceFeed::note(const Digest& d, bool present) {
+    if (index.size() < 2 * (pending.size() + 1)) {  // grow (a power of two) and re-index
+        size_t cap = 1024;
+        while (cap < 4 * (pending.size() + 1)) cap <<= 1;
+        index.assign(cap, -1);
+        const size_t mask = index.size() - 1;
+        for (size_t k = 0; k < pending.size(); ++k) {
+            uint64_t h;
+            std::memcpy(&h, pending[k].first.data(), 8);
+            size_t i = h & mask;
+            while (index[i] >= 0) i = (i + 1) & mask;
+            index[i] = int32_t(k);
+        }
+    }
+    const size_t mask = index.size() - 1;
+    uint64_t h;
+    std::memcpy(&h, d.data(), 8);
+    for (size_t i = h & mask;; i = (i + 1) & mask) {
+        if (index[i] < 0) {
+            index[i] = int32_t(pending.size());
+            pending.emplace_back(d, present);
+            return;
+        }
+        if (pending[index[i]].first == d) {
+            pending[index[i]].second = present;
+            return;
+        }
+    }
+}
+
+void TieredStore::PresenceFeed::clear() {
+    pending.clear();
+    std::fill(index.begin(), index.end(), -1);
+}
+
 void TieredStore::presence_changed(const Digest& d, bool present) {
     const size_t cap = 4 * std::max<size_t>(256, slab_slots());
     for (auto& f : feeds_) {
         if (f->fresh) continue;
-        f->pending[d] = present;
+        f->note(d, present);
         if (f->pending.size() > cap) {  // a subscriber that stopped draining: resync from a snapshot
-            f->pending.clear();
+            f->clear();
             f->fresh = true;
         }
     }
@@ -65,9 +100,9 @@ void TieredStore::presence_drain(size_t id, bool want_full, std::vector<std::pai
             if (e.state == Entry::State::present) out.emplace_back(d, true);
         f.fresh = false;
     } else {
-        out.assign(f.pending.begin(), f.pending.end());
+        out.swap(f.pending);
     }
-    f.pending.clear();
+    f.clear();
 }
 
 TieredStore::TieredStore(StoreConfig cfg) : cfg_(std::move(cfg)) {

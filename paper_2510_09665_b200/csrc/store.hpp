@@ -200,9 +200,16 @@ private:
     std::vector<uint32_t> free_slots_;
     uint64_t clock_ = 0;
     void presence_changed(const Digest& d, bool present);  // caller holds mu_
+    // Pending changes of one subscriber, one final state per digest: a
+    // contiguous vector (drained by a swap) indexed by a flat open-addressing
+    // table (the drain is on the lookup path; a node-based map measured ~75 ns
+    // per entry to walk there).
     struct PresenceFeed {
-        std::unordered_map<Digest, bool, DigestHasher> pending;
-        bool fresh = true;  // nothing drained yet: the first drain is a full snapshot
+        std::vector<std::pair<Digest, bool>> pending;
+        std::vector<int32_t> index;  // power of two, -1 = empty; >= 2 x pending
+        bool fresh = true;           // nothing drained yet: the first drain is a full snapshot
+        void note(const Digest& d, bool present);
+        void clear();
     };
     std::vector<std::unique_ptr<PresenceFeed>> feeds_;  // guarded by mu_
 };

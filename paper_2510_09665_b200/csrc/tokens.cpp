@@ -263,9 +263,7 @@ void KeyHasher::presence_sync_locked(MemoView& m) {
 bool KeyHasher::first_row_lookup(const std::vector<TokenSpanView>& seqs, const std::vector<size_t>& rows,
                                  std::vector<std::vector<Digest>>& out, std::vector<size_t>& present_rows,
                                  const std::function<void()>& while_waiting, bool& waited) {
-    static const bool off = std::getenv("TKV_NO_FIRST_ROW") != nullptr;  // A/B only
     const size_t n_chains = seqs.size();
-    if (off || chunk_size_ > 256) return false;
     const double t_pack0 = trace_lookup() ? now_us() : 0;
     h_row0_tok_.reserve(grow(n_chains * chunk_size_ * sizeof(TokenId) + 64));
     h_row0_ch_.reserve(grow(n_chains * sizeof(ChainDesc)));
@@ -304,6 +302,7 @@ bool KeyHasher::first_row_lookup(const std::vector<TokenSpanView>& seqs, const s
                                                    h_row0_out_.dev + ((n_chains * 36 + 7) / 8) * 8)
                                              : nullptr,
                               inline_one ? &one : nullptr));
+    memo_.presence.n_updates = 0;  // applied by that launch (one CTA) or the separate launch before it
     const double t_launched = trace_lookup() ? now_us() : 0;
     if (while_waiting) {  // the caller's host work runs under the kernel
         while_waiting();
@@ -371,11 +370,6 @@ std::vector<std::vector<Digest>> KeyHasher::hash_prefix(const std::vector<TokenS
     }
     HashParams p;
     const bool on_device = memo_.slots != nullptr && presence_drain_ && present_rows != nullptr;
-    if (on_device) {  // the tier's changes since the last lookup, applied first
-        presence_sync_locked(memo_);
-        TKV_CUDA(launch_presence_apply(memo_.presence, stream_));
-        memo_.presence.n_updates = 0;
-    }
     bool waited = false;  // while_waiting already ran (during the first-row kernel)
     // Route: a prompt whose first chunk this hasher has seen before (a host
     // hint set of row-0 token hashes) goes straight to the full lookup — its
@@ -394,7 +388,23 @@ std::vector<std::vector<Digest>> KeyHasher::hash_prefix(const std::vector<TokenS
     }
     if (seen_row0_.size() > (1u << 20)) seen_row0_.clear();
     for (uint64_t h : row0) seen_row0_.insert(h);
-    if (on_device && novel && first_row_lookup(seqs, rows, out, *present_rows, while_waiting, waited)) {
+    const bool use_first_row = on_device && novel && chunk_size_ <= 256 && std::getenv("TKV_NO_FIRST_ROW") == nullptr;
+    if (on_device) {
+        // The tier's changes since the last lookup, applied by this lookup's
+        // first kernel (the first-row kernel when it is one CTA, else the
+        // fingerprint pass) or, for a multi-CTA first-row launch, by a
+        // separate launch before it.
+        const double ts0 = trace_lookup() ? now_us() : 0;
+        presence_sync_locked(memo_);
+        const uint32_t n_upd = memo_.presence.n_updates;
+        if (use_first_row && n_chains > 2) {
+            TKV_CUDA(launch_presence_apply(memo_.presence, stream_));
+            memo_.presence.n_updates = 0;
+        }
+        if (trace_lookup() && n_upd)
+            std::fprintf(stderr, "[tkv presence] changes=%u sync=%.1fus\n", n_upd, now_us() - ts0);
+    }
+    if (use_first_row && first_row_lookup(seqs, rows, out, *present_rows, while_waiting, waited)) {
         if (trace_lookup())
             std::fprintf(stderr, "[tkv prefix] chains=%zu first-row decided in %.1fus\n", n_chains, now_us() - t_in);
         return out;  // every first chunk absent: decided without staging the prompts
@@ -406,6 +416,7 @@ std::vector<std::vector<Digest>> KeyHasher::hash_prefix(const std::vector<TokenS
     // the pack measured no faster: the device work is then exposed instead)
     const double t_routed = trace_lookup() ? now_us() : 0;
     MemoView m = stage_locked(seqs, nullptr, total_tokens, total_chunks, n_chains, p, waited ? mapped : nullptr);
+    memo_.presence.n_updates = 0;  // applied by the fingerprint pass (or the first-row kernel)
     auto* dev_present = reinterpret_cast<uint32_t*>(h_present_.host);
     auto* dev_known = reinterpret_cast<uint32_t*>(h_known_.host);
     if (on_device) {

@@ -248,3 +248,32 @@ def test_presence_index_decides_lookups_on_device(tkv, C):
     assert lookup(9, fresh) == 767
     assert e.lookups_host_decided() == base + 1
     e.close()
+
+
+def test_presence_many_changes_between_lookups(tkv, C):
+    """Thousands of presence changes between two lookups (a tier filled by
+    one large store, then an evicting one): the change feed grows its index,
+    coalesces, and the next lookups — cold (first-row kernel, the changes
+    applied in that launch) and warm (the fingerprint pass applies them) —
+    still equal the host index."""
+    from paper_2510_09665_b200.api import Engine
+    rng = np.random.default_rng(11)
+    e = Engine(num_layers=1, bpt=16, page_tokens=16, tag=TAG, chunk_size=256, ram_slots=1500, num_pages=8192)
+    big = rng.integers(0, 128256, size=256 * 1400, dtype=np.uint32)
+    e.seed_store(big, len(big))                     # 1400 adds
+    cold = rng.integers(0, 128256, size=256 * 3, dtype=np.uint32)
+    assert e.get_num_new_matched_tokens(1, cold) == 0
+    e.finish_query(1)
+    other = rng.integers(0, 128256, size=256 * 300, dtype=np.uint32)
+    e.seed_store(other, len(other))                 # 300 adds, 200 evictions
+    assert e.get_num_new_matched_tokens(2, rng.integers(0, 128256, size=600, dtype=np.uint32)) == 0
+    e.finish_query(2)
+    keys = C.chunk_keys(big, 256, TAG)
+    want = 0
+    while want < len(keys) and e.contains(keys[want]):
+        want += 1
+    assert e.get_num_new_matched_tokens(3, big) == min(len(big) - 1, 256 * want)
+    e.finish_query(3)
+    assert e.get_num_new_matched_tokens(4, other) == len(other) - 1
+    e.finish_query(4)
+    e.close()
