@@ -16,6 +16,7 @@
 #include <span>
 #include <stdexcept>
 #include <string>
+#include <utility>
 #include <variant>
 #include <vector>
 
@@ -212,6 +213,15 @@ struct PinnedAllocator {
         return static_cast<T*>(p);
     }
     void deallocate(T* p, size_t) { cudaFreeHost(p); }
+    // resize() default-initialises (no zero fill: the buffer is overwritten)
+    template <typename U>
+    void construct(U* p) noexcept {
+        ::new (static_cast<void*>(p)) U;
+    }
+    template <typename U, typename... A>
+    void construct(U* p, A&&... a) {
+        ::new (static_cast<void*>(p)) U(std::forward<A>(a)...);
+    }
     template <typename U>
     bool operator==(const PinnedAllocator<U>&) const { return true; }
 };

@@ -7,6 +7,7 @@
 #include <cstring>
 
 #include "copy_plan.hpp"
+#include "host_copy.hpp"
 
 namespace tkv {
 
@@ -287,7 +288,8 @@ const std::vector<ChunkKey>& Connector::keys_for(QueryState& qs, TokenSpanView p
     if (qs.keys.size() != rows || qs.prompt.size() != prompt.size() ||
         !std::equal(prompt.begin(), prompt.end(), qs.prompt.begin())) {
         if (qs.prompt.capacity() < prompt.size()) qs.prompt.reserve(prompt_capacity(prompt.size()));
-        qs.prompt.assign(prompt.begin(), prompt.end());
+        qs.prompt.resize(prompt.size());
+        host_copy(qs.prompt.data(), prompt.data(), prompt.size() * sizeof(TokenId));
         qs.keys = chunk_keys(hasher_, prompt);
     }
     return qs.keys;
@@ -324,7 +326,10 @@ std::vector<size_t> Connector::get_num_new_matched_tokens(
     auto digests = hasher_.hash_prefix(
         prompts, [this](const std::vector<Digest>& d) { return store_.present_prefix(d); },
         [&] {
-            for (size_t q = 0; q < ids.size(); ++q) staged[q].assign(prompts[q].begin(), prompts[q].end());
+            for (size_t q = 0; q < ids.size(); ++q) {
+                staged[q].resize(prompts[q].size());
+                host_copy(staged[q].data(), prompts[q].data(), prompts[q].size() * sizeof(TokenId));
+            }
         },
         &present_rows, &mapped);
     const auto t1 = std::chrono::steady_clock::now();

@@ -1,0 +1,17 @@
+// Host copies of prompt-sized buffers (lookup packing and the query state's
+// prompt copy: 512 KiB for a 128K-token document) split over a few
+// persistent helper threads with streaming stores. One thread moves ~10-28
+// GB/s into pinned memory; four move 60-110 GB/s on the B200 hosts
+// (tools/microbench_promptcopy.cpp, profiles/r02_promptcopy.jsonl).
+#pragma once
+#include <cstddef>
+
+namespace tkv {
+
+// memcpy semantics (no overlap). Small copies, and copies issued while
+// another thread's parallel copy is running, run on the calling thread alone;
+// the caller always works on its own pieces too, so a helper that wakes late
+// costs nothing but its share.
+void host_copy(void* dst, const void* src, size_t n);
+
+}  // namespace tkv

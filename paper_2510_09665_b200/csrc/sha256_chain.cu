@@ -798,6 +798,7 @@ memo_verify_kernel(const uint32_t* __restrict__ tokens, const ChainDesc* __restr
 // system-scope release, so the host can poll instead of synchronizing and
 // return at once when every chain's first chunk is absent.
 constexpr int kFirstRowWarps = 2;
+constexpr int kFirstRowMaxThreads = 256;  // chain warps + presence-apply warps
 
 struct FirstRowSmem {
     uint32_t tok[kWarpChunkMax + 4];
@@ -818,22 +819,39 @@ __device__ __forceinline__ uint64_t parent_fingerprint(const uint8_t parent[32])
     return pfp;
 }
 
-__global__ void __launch_bounds__(32 * kFirstRowWarps)
+__global__ void __launch_bounds__(kFirstRowMaxThreads)
 first_row_kernel(const uint32_t* __restrict__ tokens, const ChainDesc* __restrict__ chains, uint32_t n_chains,
                  const HashParams P, const MemoView M, uint32_t* __restrict__ digests_out,
                  uint32_t* __restrict__ flags_out, unsigned long long* __restrict__ trace, const FirstRowInline one) {
     __shared__ FirstRowSmem smem[kFirstRowWarps];
+    __shared__ uint32_t applied_warps;
     unsigned long long t_start = 0, t_staged = 0, t_hashed = 0;
     if (trace != nullptr) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
-    // pending presence changes (only when the launch is one CTA: the host
-    // launches presence_apply_kernel first otherwise)
-    if (M.presence.n_updates != 0) {
+    const uint32_t lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    // Pending presence changes (only in a one-CTA launch: the host launches
+    // presence_apply_kernel first otherwise). Warps past the chain warps
+    // apply them while the chain warps stage and hash; a chain warp waits for
+    // them (shared counter) only before its presence test.
+    const uint32_t apply_warps = blockDim.x / 32 - kFirstRowWarps;
+    if (M.presence.n_updates != 0 && apply_warps == 0 && gridDim.x == 1) {
         for (uint32_t u = threadIdx.x; u < M.presence.n_updates; u += blockDim.x)
             presence_apply(M.presence, M.presence.updates + 9ull * u);
         __threadfence_block();
         __syncthreads();
     }
-    const uint32_t lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    if (apply_warps != 0) {
+        if (threadIdx.x == 0) applied_warps = 0;
+        __syncthreads();
+        if (wid >= uint32_t(kFirstRowWarps)) {
+            const uint32_t stride = 32 * apply_warps;
+            for (uint32_t u = threadIdx.x - 32 * kFirstRowWarps; u < M.presence.n_updates; u += stride)
+                presence_apply(M.presence, M.presence.updates + 9ull * u);
+            __threadfence();
+            __syncwarp();
+            if (lane == 0) atomicAdd(&applied_warps, 1u);
+            return;
+        }
+    }
     const uint32_t c = blockIdx.x * kFirstRowWarps + wid;
     if (c >= n_chains) return;
     FirstRowSmem& s = smem[wid];
@@ -911,6 +929,11 @@ first_row_kernel(const uint32_t* __restrict__ tokens, const ChainDesc* __restric
             for (int i = 0; i < 8; ++i) h[i] = st[i];
         }
         if (trace != nullptr) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_hashed));
+        if (lane == 0 && apply_warps != 0) {
+            while (atomicAdd(&applied_warps, 0u) < apply_warps) {
+            }
+            __threadfence();
+        }
         if (lane == 0 && M.presence.slots != nullptr && presence_has(M.presence, h)) flag |= 2u;
     }
     uint32_t hl = 0;
@@ -1019,7 +1042,10 @@ cudaError_t launch_first_row(const uint32_t* tokens, const ChainDesc* chains, ui
     const uint32_t blocks = (n_chains + kFirstRowWarps - 1) / kFirstRowWarps;
     FirstRowInline none;
     none.n = ~0u;
-    first_row_kernel<<<blocks, 32 * kFirstRowWarps, 0, s>>>(tokens, chains, n_chains, params, memo, digests_out,
+    uint32_t threads = 32 * kFirstRowWarps;
+    if (blocks == 1 && memo.presence.n_updates != 0)  // + warps applying the presence changes
+        threads += std::min<uint32_t>(kFirstRowMaxThreads - 32 * kFirstRowWarps, (memo.presence.n_updates + 31) / 32 * 32);
+    first_row_kernel<<<blocks, threads, 0, s>>>(tokens, chains, n_chains, params, memo, digests_out,
                                                              flags_out, trace, one ? *one : none);
     return cudaGetLastError();
 }

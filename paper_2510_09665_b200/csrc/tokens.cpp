@@ -8,6 +8,8 @@
 #include <cstring>
 #include <stdexcept>
 
+#include "host_copy.hpp"
+
 namespace tkv {
 
 std::vector<ChunkSpan> chunk_tokens(size_t n, size_t chunk_size) {
@@ -77,7 +79,7 @@ MemoView KeyHasher::stage_locked(const std::vector<TokenSpanView>& seqs, const s
         if (mapped)
             srcs[i] = reinterpret_cast<unsigned long long>((*mapped)[i]);
         else
-            std::copy(seqs[i].begin(), seqs[i].end(), tok + toff);
+            host_copy(tok + toff, seqs[i].data(), seqs[i].size() * sizeof(TokenId));
         ChainDesc d;
         d.token_off = toff;
         d.n_tokens = uint32_t(seqs[i].size());
@@ -352,6 +354,7 @@ std::vector<std::vector<Digest>> KeyHasher::hash_prefix(const std::vector<TokenS
                                                         const std::vector<const TokenId*>* mapped) {
     const double t_in = trace_lookup() ? now_us() : 0;
     std::lock_guard lock(mu_);
+    const double t_locked = trace_lookup() ? now_us() : 0;
     TKV_CUDA(cudaSetDevice(device_));
     const size_t n_chains = seqs.size();
     size_t total_tokens = 0, total_chunks = 0;
@@ -389,6 +392,7 @@ std::vector<std::vector<Digest>> KeyHasher::hash_prefix(const std::vector<TokenS
     if (seen_row0_.size() > (1u << 20)) seen_row0_.clear();
     for (uint64_t h : row0) seen_row0_.insert(h);
     const bool use_first_row = on_device && novel && chunk_size_ <= 256 && std::getenv("TKV_NO_FIRST_ROW") == nullptr;
+    const double t_hinted = trace_lookup() ? now_us() : 0;
     if (on_device) {
         // The tier's changes since the last lookup, applied by this lookup's
         // first kernel (the first-row kernel when it is one CTA, else the
@@ -401,8 +405,9 @@ std::vector<std::vector<Digest>> KeyHasher::hash_prefix(const std::vector<TokenS
             TKV_CUDA(launch_presence_apply(memo_.presence, stream_));
             memo_.presence.n_updates = 0;
         }
-        if (trace_lookup() && n_upd)
-            std::fprintf(stderr, "[tkv presence] changes=%u sync=%.1fus\n", n_upd, now_us() - ts0);
+        if (trace_lookup())
+            std::fprintf(stderr, "[tkv presence] changes=%u sync=%.1fus | lock=%.1fus route=%.1fus\n", n_upd,
+                         now_us() - ts0, t_locked - t_in, t_hinted - t_locked);
     }
     if (use_first_row && first_row_lookup(seqs, rows, out, *present_rows, while_waiting, waited)) {
         if (trace_lookup())
