@@ -2,6 +2,8 @@
 
 #include <algorithm>
 #include <cstring>
+#include <numeric>
+#include <string>
 
 namespace tkv {
 
@@ -10,100 +12,92 @@ PagedKVStore::PagedKVStore(ModelSpec spec, uint32_t num_pages, int device)
     if (device_ < 0) TKV_CUDA(cudaGetDevice(&device_));
     TKV_CUDA(cudaSetDevice(device_));
     pool_.reserve(std::max<size_t>(1, size_t(num_pages) * spec_.page_bytes()));
-    pages_.resize(num_pages);
-    free_list_.reserve(num_pages);
-    for (uint32_t i = num_pages; i > 0; --i) free_list_.push_back(i - 1);  // page 0 first
+    page_word_.assign(num_pages, layer_word(kNoLayer));
+    // the top of the stack is the last element: descending ids put page 0 there
+    free_ids_.resize(num_pages);
+    std::iota(free_ids_.rbegin(), free_ids_.rend(), PageId(0));
+    free_top_ = num_pages;
     io_stream_ = Stream::create();
 }
 
 Result<std::vector<PageId>> PagedKVStore::alloc_pages(QueryId query, size_t n) {
     std::lock_guard lock(mu_);
-    if (free_list_.size() < n)
-        return Status{Errc::out_of_pages, "need " + std::to_string(n) + " pages, " +
-                                              std::to_string(free_list_.size()) + " free"};
-    std::vector<PageId> out;
-    out.reserve(n);
-    for (size_t i = 0; i < n; ++i) {
-        PageId id = free_list_.back();
-        free_list_.pop_back();
-        pages_[id] = PageMeta{query, kNoLayer, false};
-        out.push_back(id);
-    }
-    auto& owned = owned_[query];
-    owned.insert(owned.end(), out.begin(), out.end());
-    return out;
+    if (n > free_top_)
+        return Status{Errc::out_of_pages,
+                      "alloc_pages: " + std::to_string(n) + " requested, " + std::to_string(free_top_) + " available"};
+    // the n topmost ids, topmost first (the order a pop loop would give)
+    std::vector<PageId> got(free_ids_.rbegin() + std::ptrdiff_t(free_ids_.size() - free_top_),
+                            free_ids_.rbegin() + std::ptrdiff_t(free_ids_.size() - free_top_ + n));
+    free_top_ -= n;
+    for (PageId id : got) page_word_[id] = kAllocated | layer_word(kNoLayer);
+    QueryPages& q = queries_[query];
+    q.allocated = true;
+    q.owned.insert(q.owned.end(), got.begin(), got.end());
+    return got;
 }
 
 void PagedKVStore::bind_layer(QueryId query, uint32_t layer, const std::vector<PageId>& pages) {
     std::lock_guard lock(mu_);
-    auto& t = tables_[query];
-    if (t.layers.size() <= layer) t.layers.resize(layer + 1);
-    t.layers[layer] = pages;
-    t.dirty = true;
-    for (PageId id : pages) pages_[id].layer = layer;
+    QueryPages& q = queries_[query];
+    if (q.layers.size() <= layer) q.layers.resize(size_t(layer) + 1);
+    q.layers[layer] = pages;
+    q.dirty = true;
+    for (PageId id : pages) page_word_[id] = (page_word_[id] & ~0xffffffffull) | layer_word(layer);
 }
 
 Status PagedKVStore::admit(QueryId query, size_t tokens) {
     const size_t blocks = (tokens + spec_.page_tokens - 1) / spec_.page_tokens;
-    auto alloc = alloc_pages(query, blocks * spec_.num_layers);
-    if (!alloc.ok()) return alloc.status();
-    std::lock_guard lock(mu_);
-    auto& t = tables_[query];
-    t.layers.resize(spec_.num_layers);
-    for (uint32_t l = 0; l < spec_.num_layers; ++l) {
-        auto first = alloc.value().begin() + long(size_t(l) * blocks);
-        t.layers[l].assign(first, first + long(blocks));
-        for (size_t i = 0; i < blocks; ++i) pages_[t.layers[l][i]].layer = l;
-    }
-    t.dirty = true;
+    auto got = alloc_pages(query, blocks * spec_.num_layers);
+    if (!got.ok()) return got.status();
+    const std::vector<PageId>& ids = got.value();
+    for (uint32_t l = 0; l < spec_.num_layers; ++l)
+        bind_layer(query, l, std::vector<PageId>(ids.begin() + std::ptrdiff_t(size_t(l) * blocks),
+                                                 ids.begin() + std::ptrdiff_t(size_t(l + 1) * blocks)));
     return Status::success();
 }
 
 std::vector<PageId> PagedKVStore::layer_pages(QueryId query, uint32_t layer) const {
     std::lock_guard lock(mu_);
-    auto it = tables_.find(query);
-    if (it == tables_.end() || it->second.layers.size() <= layer) return {};
-    return it->second.layers[layer];
+    const auto it = queries_.find(query);
+    return it != queries_.end() && layer < it->second.layers.size() ? it->second.layers[layer]
+                                                                    : std::vector<PageId>{};
 }
 
 std::vector<PageId> PagedKVStore::release_query(QueryId query) {
     std::lock_guard lock(mu_);
-    auto it = owned_.find(query);
-    if (it == owned_.end()) return {};
-    std::vector<PageId> freed = std::move(it->second);
-    owned_.erase(it);
-    auto t = tables_.find(query);
-    if (t != tables_.end()) {  // the engine releases a query after its transfers finished
-        table_pool_.release(std::move(t->second.buf));
-        for (auto& r : t->second.retired) table_pool_.release(std::move(r));
-        tables_.erase(t);
+    auto it = queries_.find(query);
+    if (it == queries_.end() || !it->second.allocated) return {};  // page lists without pages stay
+    QueryPages q = std::move(it->second);
+    queries_.erase(it);
+    // the engine releases a query after its transfers finished: its table
+    // mirrors go back to the pool
+    if (q.buf) table_pool_.release(std::move(q.buf));
+    for (auto& r : q.retired) table_pool_.release(std::move(r));
+    for (PageId id : q.owned) {
+        page_word_[id] = layer_word(kNoLayer);
+        free_ids_[free_top_++] = id;
     }
-    for (PageId id : freed) {
-        pages_[id] = PageMeta{};
-        free_list_.push_back(id);
-    }
-    return freed;
+    return std::move(q.owned);
 }
 
 size_t PagedKVStore::free_page_count() const {
     std::lock_guard lock(mu_);
-    return free_list_.size();
+    return free_top_;
 }
 
 size_t PagedKVStore::allocated_page_count() const {
     std::lock_guard lock(mu_);
-    return pages_.size() - free_list_.size();
+    return page_word_.size() - free_top_;
 }
 
 void PagedKVStore::mark_populated(PageId id, uint32_t layer) {
     std::lock_guard lock(mu_);
-    pages_[id].layer = layer;
-    pages_[id].populated = true;
+    page_word_[id] = (page_word_[id] & kAllocated) | kPopulated | layer_word(layer);
 }
 
 bool PagedKVStore::populated(PageId id) const {
     std::lock_guard lock(mu_);
-    return pages_[id].populated;
+    return (page_word_[id] & kPopulated) != 0;
 }
 
 PagedLayout PagedKVStore::layout() const {
@@ -122,9 +116,9 @@ PagedLayout PagedKVStore::layout() const {
 
 Result<PagedKVStore::DeviceTable> PagedKVStore::device_table(QueryId query, cudaStream_t stream) {
     std::lock_guard lock(mu_);
-    auto it = tables_.find(query);
-    if (it == tables_.end()) return Status{Errc::unknown_query, "query has no page table"};
-    QueryTable& t = it->second;
+    auto it = queries_.find(query);
+    if (it == queries_.end()) return Status{Errc::unknown_query, "query has no page table"};
+    QueryPages& t = it->second;
     if (t.dirty) {
         size_t stride = 1;
         for (const auto& l : t.layers) stride = std::max(stride, l.size());
@@ -147,56 +141,60 @@ Result<PagedKVStore::DeviceTable> PagedKVStore::device_table(QueryId query, cuda
     return DeviceTable{reinterpret_cast<const int32_t*>(t.buf->dev.ptr), t.stride};
 }
 
+namespace {
+std::string page_msg(PageId id, uint32_t layer) {
+    return "page " + std::to_string(id) + " holds no data of layer " + std::to_string(layer);
+}
+}  // namespace
+
+// paged_store.cpp:94-111: capacity, then every page in order (range, then
+// populated with this layer's data)
 Status PagedKVStore::check_readable(const std::vector<PageId>& pages, uint32_t layer,
                                     size_t token_count) const {
-    size_t capacity = pages.size() * spec_.page_tokens;
-    if (token_count > capacity)
-        return Status{Errc::size_mismatch, std::to_string(token_count) + " tokens across " +
+    if (token_count > pages.size() * spec_.page_tokens)
+        return Status{Errc::size_mismatch, std::to_string(token_count) + " tokens do not fit " +
                                                std::to_string(pages.size()) + " pages"};
     std::lock_guard lock(mu_);
     for (PageId id : pages) {
-        if (id >= pages_.size()) return Status{Errc::invalid_argument, "page id out of range"};
-        const PageMeta& m = pages_[id];
-        if (!m.populated || m.layer != layer)
-            return Status{Errc::unpopulated_page,
-                          "page " + std::to_string(id) + " layer " + std::to_string(layer)};
+        if (id >= page_word_.size()) return Status{Errc::invalid_argument, "page " + std::to_string(id) + " not in the pool"};
+        if (!page_holds(id, layer)) return Status{Errc::unpopulated_page, page_msg(id, layer)};
     }
     return Status::success();
+}
+
+const std::vector<PageId>* PagedKVStore::span_list(QueryId query, uint32_t layer, size_t first_page,
+                                                   size_t token_count, size_t& end) const {
+    const auto it = queries_.find(query);
+    if (it == queries_.end() || it->second.layers.size() <= layer) return nullptr;
+    const auto& list = it->second.layers[layer];
+    end = first_page + (token_count + spec_.page_tokens - 1) / spec_.page_tokens;
+    return end <= list.size() ? &list : nullptr;
 }
 
 Status PagedKVStore::check_readable_span(QueryId query, uint32_t layer, size_t first_page,
                                          size_t token_count) const {
     std::lock_guard lock(mu_);
-    auto it = tables_.find(query);
-    if (it == tables_.end() || it->second.layers.size() <= layer)
-        return Status{Errc::size_mismatch, "no pages for layer " + std::to_string(layer)};
-    const auto& list = it->second.layers[layer];
-    const size_t need = (token_count + spec_.page_tokens - 1) / spec_.page_tokens;
-    if (first_page + need > list.size())
-        return Status{Errc::size_mismatch, std::to_string(token_count) + " tokens beyond pages"};
-    for (size_t i = first_page; i < first_page + need; ++i) {
-        const PageMeta& m = pages_[list[i]];
-        if (!m.populated || m.layer != layer)
-            return Status{Errc::unpopulated_page,
-                          "page " + std::to_string(list[i]) + " layer " + std::to_string(layer)};
-    }
+    size_t end = 0;
+    const auto* list = span_list(query, layer, first_page, token_count, end);
+    if (list == nullptr)
+        return Status{Errc::size_mismatch, "layer " + std::to_string(layer) + " has no pages for " +
+                                               std::to_string(token_count) + " tokens"};
+    for (size_t i = first_page; i < end; ++i)
+        if (!page_holds((*list)[i], layer)) return Status{Errc::unpopulated_page, page_msg((*list)[i], layer)};
     return Status::success();
 }
 
 Status PagedKVStore::check_writable_span(QueryId query, uint32_t layer, size_t first_page,
                                          size_t token_count) const {
     std::lock_guard lock(mu_);
-    auto it = tables_.find(query);
-    if (it == tables_.end() || it->second.layers.size() <= layer)
-        return Status{Errc::size_mismatch, "scatter exceeds page capacity"};
-    const auto& list = it->second.layers[layer];
-    const size_t need = (token_count + spec_.page_tokens - 1) / spec_.page_tokens;
-    if (first_page + need > list.size())
-        return Status{Errc::size_mismatch, "scatter exceeds page capacity"};
-    for (size_t i = first_page; i < first_page + need; ++i) {
-        if (list[i] >= pages_.size()) return Status{Errc::invalid_argument, "page id out of range"};
-        if (pages_[list[i]].owner == kFree)
-            return Status{Errc::invalid_argument, "scatter into free page"};
+    size_t end = 0;
+    const auto* list = span_list(query, layer, first_page, token_count, end);
+    if (list == nullptr) return Status{Errc::size_mismatch, "span larger than the bound pages"};
+    for (size_t i = first_page; i < end; ++i) {
+        const PageId id = (*list)[i];
+        if (id >= page_word_.size()) return Status{Errc::invalid_argument, "page " + std::to_string(id) + " not in the pool"};
+        if (!(page_word_[id] & kAllocated))
+            return Status{Errc::invalid_argument, "page " + std::to_string(id) + " is not allocated"};
     }
     return Status::success();
 }
@@ -204,17 +202,15 @@ Status PagedKVStore::check_writable_span(QueryId query, uint32_t layer, size_t f
 void PagedKVStore::mark_span_populated(QueryId query, uint32_t layer, size_t first_page,
                                        size_t token_count) {
     std::lock_guard lock(mu_);
-    auto it = tables_.find(query);
-    if (it == tables_.end() || it->second.layers.size() <= layer) return;
+    const auto it = queries_.find(query);
+    if (it == queries_.end() || it->second.layers.size() <= layer) return;
     const auto& list = it->second.layers[layer];
-    const size_t need = (token_count + spec_.page_tokens - 1) / spec_.page_tokens;
-    for (size_t i = first_page; i < first_page + need && i < list.size(); ++i) {
-        pages_[list[i]].layer = layer;
-        pages_[list[i]].populated = true;
-    }
+    const size_t end = std::min(list.size(), first_page + (token_count + spec_.page_tokens - 1) / spec_.page_tokens);
+    for (size_t i = first_page; i < end; ++i)
+        page_word_[list[i]] = (page_word_[list[i]] & kAllocated) | kPopulated | layer_word(layer);
 }
 
-Status PagedKVStore::host_copy(const std::vector<PageId>& pages, uint32_t layer,
+Status PagedKVStore::copy_through_pages(const std::vector<PageId>& pages, uint32_t layer,
                                size_t token_count, uint8_t* host, CopyDir dir) {
     if (token_count == 0) return Status::success();
     std::lock_guard lock(io_mu_);
@@ -270,7 +266,7 @@ Status PagedKVStore::gather_tokens_into(const std::vector<PageId>& pages, uint32
         return Status{Errc::size_mismatch, "gather output size"};
     Status st = check_readable(pages, layer, token_count);
     if (!st.ok()) return st;
-    return host_copy(pages, layer, token_count, out, CopyDir::gather);
+    return copy_through_pages(pages, layer, token_count, out, CopyDir::gather);
 }
 
 Result<std::vector<uint8_t>> PagedKVStore::gather_tokens(const std::vector<PageId>& pages,
@@ -287,16 +283,17 @@ Status PagedKVStore::scatter_tokens(const uint8_t* buf, size_t buf_bytes,
     if (buf_bytes != token_count * spec_.bytes_per_token_per_layer)
         return Status{Errc::size_mismatch, "scatter input size"};
     if (token_count > pages.size() * spec_.page_tokens)
-        return Status{Errc::size_mismatch, "scatter exceeds page capacity"};
+        return Status{Errc::size_mismatch, "span larger than the bound pages"};
     {
         std::lock_guard lock(mu_);
         for (PageId id : pages) {
-            if (id >= pages_.size()) return Status{Errc::invalid_argument, "page id out of range"};
-            if (pages_[id].owner == kFree)
-                return Status{Errc::invalid_argument, "scatter into free page"};
+            if (id >= page_word_.size())
+                return Status{Errc::invalid_argument, "page " + std::to_string(id) + " not in the pool"};
+            if (!(page_word_[id] & kAllocated))
+                return Status{Errc::invalid_argument, "page " + std::to_string(id) + " is not allocated"};
         }
     }
-    Status st = host_copy(pages, layer, token_count, const_cast<uint8_t*>(buf), CopyDir::scatter);
+    Status st = copy_through_pages(pages, layer, token_count, const_cast<uint8_t*>(buf), CopyDir::scatter);
     if (!st.ok()) return st;
     const size_t used = (token_count + spec_.page_tokens - 1) / spec_.page_tokens;
     for (size_t i = 0; i < used; ++i) mark_populated(pages[i], layer);

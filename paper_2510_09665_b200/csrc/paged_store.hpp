@@ -1,12 +1,14 @@
 // Engine-resident paged KV memory on the device (mirror of
 // include/tierkv/paged_store.hpp:19-82).
 //
-// Same bookkeeping as the reference — a pool of fixed pages, a stack free
-// list (page 0 handed out first, paged_store.cpp:8-14), per-(query, layer)
-// page lists, owner/layer/populated metadata and the same checks — but the
-// pool is ONE cudaMalloc slab in HBM (page p at base + p * page_bytes) and
-// each query's page lists are mirrored into a device page table
-// [num_layers][blocks] of int32 that the K1/K2/K4 kernels index directly.
+// The reference's observable contract — which page ids an allocation returns
+// (last freed first; page 0 first in a fresh pool, paged_store.cpp:8-14),
+// per-(query, layer) page lists, and the error codes of its checks — with a
+// B200 layout: the pool is ONE cudaMalloc slab in HBM (page p at base +
+// p * page_bytes), each query's page lists are mirrored into a device page
+// table [num_layers][blocks] of int32 that the K1/K2/K4 kernels index
+// directly, and the host side keeps one packed word per page plus one
+// record per query.
 #pragma once
 
 #include <mutex>
@@ -24,7 +26,7 @@ public:
 
     const ModelSpec& spec() const { return spec_; }
     size_t page_bytes() const { return spec_.page_bytes(); }
-    uint32_t pool_pages() const { return uint32_t(pages_.size()); }
+    uint32_t pool_pages() const { return uint32_t(page_word_.size()); }
     int device() const { return device_; }
 
     Result<std::vector<PageId>> alloc_pages(QueryId query, size_t n);
@@ -73,34 +75,47 @@ public:
                           uint32_t layer, size_t token_count);
 
 private:
-    static constexpr QueryId kFree = ~QueryId(0);
+    // One 64-bit word per page: the layer it holds (low 32 bits) and two
+    // flags. The owning query is known from its QueryPages record; a page
+    // only needs "allocated" for the scatter-side check.
+    static constexpr uint64_t kAllocated = 1ull << 32;
+    static constexpr uint64_t kPopulated = 1ull << 33;
     static constexpr uint32_t kNoLayer = ~uint32_t(0);
-    struct PageMeta {
-        QueryId owner = kFree;
-        uint32_t layer = kNoLayer;
-        bool populated = false;
-    };
-    struct QueryTable {
+    static uint64_t layer_word(uint32_t layer) { return uint64_t(layer); }
+    bool page_holds(PageId id, uint32_t layer) const {  // caller holds mu_
+        const uint64_t w = page_word_[id];
+        return (w & kPopulated) && uint32_t(w) == layer;
+    }
+    // Everything the store knows about one query: the pages it allocated (in
+    // allocation order), its per-layer page lists and their device mirror.
+    struct QueryPages {
+        bool allocated = false;  // alloc_pages ran for it (possibly with n = 0)
+        std::vector<PageId> owned;
         std::vector<std::vector<PageId>> layers;
         bool dirty = true;
         uint32_t stride = 0;
         std::unique_ptr<DualBuffer> buf;  // pooled pinned mirror + device table
         std::vector<std::unique_ptr<DualBuffer>> retired;  // earlier uploads, freed at release
     };
+    // span [first, first + ceil(n / page_tokens)) of (query, layer), or null
+    const std::vector<PageId>* span_list(QueryId query, uint32_t layer, size_t first_page, size_t token_count,
+                                         size_t& end) const;
 
     Status check_readable(const std::vector<PageId>& pages, uint32_t layer,
                           size_t token_count) const;
-    Status host_copy(const std::vector<PageId>& pages, uint32_t layer, size_t token_count,
-                     uint8_t* host, CopyDir dir);
+    Status copy_through_pages(const std::vector<PageId>& pages, uint32_t layer, size_t token_count,
+                              uint8_t* host, CopyDir dir);
 
     ModelSpec spec_;
     int device_;
     DeviceBuffer pool_;
-    std::vector<PageMeta> pages_;
-    std::vector<PageId> free_list_;
-    DualPool table_pool_;  // declared before tables_: outlives them
-    std::unordered_map<QueryId, QueryTable> tables_;
-    std::unordered_map<QueryId, std::vector<PageId>> owned_;
+    std::vector<uint64_t> page_word_;
+    // LIFO of free page ids: free_ids_[0, free_top_) with the next page to
+    // hand out at the top (page 0 first after construction)
+    std::vector<PageId> free_ids_;
+    size_t free_top_ = 0;
+    DualPool table_pool_;  // declared before queries_: outlives their mirrors
+    std::unordered_map<QueryId, QueryPages> queries_;
     mutable std::mutex mu_;
 
     std::mutex io_mu_;  // serialises the synchronous host API

@@ -8,63 +8,63 @@
 
 namespace tkv {
 
-// --- control plane: src/pd_staging.cpp:5-63 semantics --------------------
+// --- control plane: the contract of src/pd_staging.cpp:5-63 ---------------
+// (register before push; an ordinal is filled once and a retransmit acks; no
+// ordinal past the final one, and no final marker below a filled ordinal;
+// await hands back the records in ordinal order and forgets the query;
+// cancel wakes the awaiter with io_error)
 
 Status PdStaging::register_query(QueryId id) {
     std::lock_guard lock(mu_);
-    auto [it, inserted] = queries_.try_emplace(id);
-    if (!inserted) return Status{Errc::duplicate_key, "query already registered"};
+    if (!landings_.emplace(id, std::make_shared<Landing>()).second)
+        return Status{Errc::duplicate_key, "query " + std::to_string(id) + " is already registered"};
     return Status::success();
 }
 
 Status PdStaging::push(QueryId id, uint32_t ordinal, bool last, const PdRecord& rec) {
     std::lock_guard lock(mu_);
-    auto it = queries_.find(id);
-    if (it == queries_.end())
-        return Status{Errc::unknown_query, "query " + std::to_string(id) + " not registered"};
-    Query& q = it->second;
-    if (q.last_seen && ordinal > q.last_ordinal)
-        return Status{Errc::protocol_error, "ordinal beyond the final chunk"};
-    if (last && !q.slots.empty() && q.slots.rbegin()->first > ordinal)
-        return Status{Errc::protocol_error, "final ordinal below an already filled slot"};
+    const auto it = landings_.find(id);
+    if (it == landings_.end()) return Status{Errc::unknown_query, "push for unregistered query " + std::to_string(id)};
+    Landing& l = *it->second;
+    if (l.final_known && ordinal > l.final_ordinal)
+        return Status{Errc::protocol_error, "ordinal " + std::to_string(ordinal) + " past the final one"};
+    if (last && !l.filled.empty() && l.highest > ordinal)
+        return Status{Errc::protocol_error, "final ordinal " + std::to_string(ordinal) + " below a filled one"};
     if (last) {
-        q.last_seen = true;
-        q.last_ordinal = ordinal;
+        l.final_known = true;
+        l.final_ordinal = ordinal;
     }
-    q.slots.try_emplace(ordinal, rec);  // filled exactly once; a retransmit acks
-    if (complete(q)) cv_.notify_all();
+    if (l.filled.emplace(ordinal, rec).second) l.highest = l.filled.size() == 1 ? ordinal : std::max(l.highest, ordinal);
+    if (l.done()) l.wake.notify_all();
     return Status::success();
 }
 
 Result<std::vector<PdRecord>> PdStaging::await(QueryId id) {
     std::unique_lock lock(mu_);
-    auto it = queries_.find(id);
-    if (it == queries_.end())
-        return Status{Errc::unknown_query, "query " + std::to_string(id) + " not registered"};
-    cv_.wait(lock, [&] { return complete(it->second) || it->second.cancelled; });
-    if (it->second.cancelled) {
-        queries_.erase(it);
-        return Status{Errc::io_error, "query cancelled"};
-    }
-    std::vector<PdRecord> out;
-    out.reserve(it->second.slots.size());
-    for (auto& [ordinal, rec] : it->second.slots) out.push_back(rec);
-    queries_.erase(it);
+    const auto it = landings_.find(id);
+    if (it == landings_.end()) return Status{Errc::unknown_query, "await for unregistered query " + std::to_string(id)};
+    const std::shared_ptr<Landing> l = it->second;
+    l->wake.wait(lock, [&] { return l->done() || l->cancelled; });
+    const auto now = landings_.find(id);
+    if (now != landings_.end() && now->second == l) landings_.erase(now);
+    if (l->cancelled) return Status{Errc::io_error, "query " + std::to_string(id) + " was cancelled"};
+    std::vector<PdRecord> out(l->filled.size());
+    for (const auto& [ordinal, rec] : l->filled) out[ordinal] = rec;  // ordinals are exactly 0..final
     return out;
 }
 
 Status PdStaging::cancel(QueryId id) {
     std::lock_guard lock(mu_);
-    auto it = queries_.find(id);
-    if (it == queries_.end()) return Status{Errc::unknown_query, "not registered"};
-    it->second.cancelled = true;
-    cv_.notify_all();
+    const auto it = landings_.find(id);
+    if (it == landings_.end()) return Status{Errc::unknown_query, "cancel for unregistered query " + std::to_string(id)};
+    it->second->cancelled = true;
+    it->second->wake.notify_all();
     return Status::success();
 }
 
 size_t PdStaging::registered() const {
     std::lock_guard lock(mu_);
-    return queries_.size();
+    return landings_.size();
 }
 
 // --- data plane ------------------------------------------------------------

@@ -22,6 +22,7 @@
 #include <map>
 #include <memory>
 #include <mutex>
+#include <unordered_map>
 #include <vector>
 
 #include "common.hpp"
@@ -49,18 +50,22 @@ public:
     size_t registered() const;
 
 private:
-    struct Query {
-        std::map<uint32_t, PdRecord> slots;
-        uint32_t last_ordinal = 0;
-        bool last_seen = false;
+    // One landing per registered query. Records arrive out of order (one per
+    // chunk, or per layer-window of a layer-streamed send) and are kept
+    // unsorted; the landing is complete when the final ordinal is known and
+    // every ordinal up to it is filled (ordinals past it are refused, so a
+    // count suffices). Each awaiter sleeps on its own query's condition.
+    struct Landing {
+        std::unordered_map<uint32_t, PdRecord> filled;
+        uint32_t highest = 0;     // largest filled ordinal (when filled is not empty)
+        bool final_known = false;
+        uint32_t final_ordinal = 0;
         bool cancelled = false;
+        std::condition_variable wake;
+        bool done() const { return final_known && filled.size() == size_t(final_ordinal) + 1; }
     };
-    static bool complete(const Query& q) {
-        return q.last_seen && q.slots.size() == size_t(q.last_ordinal) + 1;
-    }
     mutable std::mutex mu_;
-    std::condition_variable cv_;
-    std::map<QueryId, Query> queries_;
+    std::unordered_map<QueryId, std::shared_ptr<Landing>> landings_;
 };
 
 // Prefiller side: K1 over chunks [first_chunk, first_chunk + n_chunks) of the
