@@ -328,6 +328,9 @@ uint64_t tkv_connector_hash_launches(tkv_connector* c);
  * index decides the rest in the lookup launches): a memo hit that failed
  * verification, or a stored chunk the memo had no link for. */
 uint64_t tkv_connector_lookups_host_decided(tkv_connector* c);
+/* Lookup rows decided absent by the absence witness (no SHA-256 computed):
+ * no present digest of the tier has that row's prefix. */
+uint64_t tkv_connector_lookups_witnessed(tkv_connector* c);
 
 void tkv_meta_destroy(tkv_meta* m);
 int tkv_meta_layerwise(tkv_meta* m);

@@ -141,6 +141,7 @@ SIGNATURES = {
     "tkv_connector_debug_poison_memo": (ct.c_int, [vp]),
     "tkv_connector_hash_launches": (ct.c_uint64, [vp]),
     "tkv_connector_lookups_host_decided": (ct.c_uint64, [vp]),
+    "tkv_connector_lookups_witnessed": (ct.c_uint64, [vp]),
     "tkv_meta_destroy": (None, [vp]),
     "tkv_meta_layerwise": (ct.c_int, [vp]),
     "tkv_meta_loaded_tokens": (sz, [vp, ct.c_uint64]),

@@ -373,6 +373,10 @@ class Engine:
     def lookups_host_decided(self) -> int:
         return int(self.L.tkv_connector_lookups_host_decided(self.conn))
 
+    def lookups_witnessed(self) -> int:
+        """Lookup rows the absence witness decided (absent, no SHA)."""
+        return int(self.L.tkv_connector_lookups_witnessed(self.conn))
+
     def hash_launches(self) -> int:
         return int(self.L.tkv_connector_hash_launches(self.conn))
 

@@ -686,6 +686,13 @@ int tkv_connector_debug_poison_memo(tkv_connector* c) {
 }
 uint64_t tkv_connector_hash_launches(tkv_connector* c) { return c->c->hasher().launches(); }
 uint64_t tkv_connector_lookups_host_decided(tkv_connector* c) { return c->c->hasher().host_decided(); }
+uint64_t tkv_connector_lookups_witnessed(tkv_connector* c) {
+    try {
+        return c->c->hasher().memo_stats().witnessed;
+    } catch (...) {
+        return 0;
+    }
+}
 
 // ---- PD -----------------------------------------------------------------------
 

@@ -304,6 +304,9 @@ std::vector<size_t> Connector::get_num_new_matched_tokens(
     const size_t cs = store_.config().chunk_size;
     static const bool trace = std::getenv("TKV_TRACE_LOOKUP") != nullptr;
     const auto t0 = std::chrono::steady_clock::now();
+    size_t tokens = 0;
+    for (const auto& p : prompts) tokens += p.size();
+    if (tokens * sizeof(TokenId) >= (128u << 10)) host_copy_prime();  // the copies below are parallel
     // The query state keeps a copy of each prompt; it is made while the
     // lookup's first launch runs (pooled buffers, swapped in below).
     std::vector<PinnedTokens> staged(ids.size());

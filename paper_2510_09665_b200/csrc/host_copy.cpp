@@ -62,6 +62,10 @@ public:
         for (auto& t : helpers_) t.join();
     }
     bool enabled() const { return !helpers_.empty(); }
+    void prime() {
+        wake_.fetch_add(1, std::memory_order_release);
+        wake_.notify_all();
+    }
 
     void run(void* dst, const void* src, size_t n) {
         std::unique_lock<std::mutex> lock(job_mu_, std::try_to_lock);
@@ -104,11 +108,11 @@ private:
     void loop() {
         uint32_t seen = wake_.load();
         while (!stop_.load(std::memory_order_relaxed)) {
-            // spin ~50 us for the next job, then sleep until woken
+            // spin ~100 us for the next job (or prime), then sleep until woken
             const auto t0 = std::chrono::steady_clock::now();
             uint32_t w;
             while ((w = wake_.load(std::memory_order_acquire)) == seen &&
-                   std::chrono::steady_clock::now() - t0 < std::chrono::microseconds(50))
+                   std::chrono::steady_clock::now() - t0 < std::chrono::microseconds(100))
                 _mm_pause();
             if (w == seen) {
                 wake_.wait(seen, std::memory_order_acquire);
@@ -140,6 +144,11 @@ CopyCrew& crew() {
 }
 
 }  // namespace
+
+void host_copy_prime() {
+    CopyCrew& c = crew();
+    if (c.enabled()) c.prime();
+}
 
 void host_copy(void* dst, const void* src, size_t n) {
     if (n < kParallelMin) {

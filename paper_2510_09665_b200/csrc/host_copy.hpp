@@ -14,4 +14,9 @@ namespace tkv {
 // costs nothing but its share.
 void host_copy(void* dst, const void* src, size_t n);
 
+// Wakes the helpers ahead of a burst of copies (a lookup calls it on entry):
+// they then spin for the next ~100 us instead of sleeping, so the copies
+// that follow find them awake (a futex wake-up costs tens of microseconds).
+void host_copy_prime();
+
 }  // namespace tkv

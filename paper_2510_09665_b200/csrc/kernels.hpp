@@ -106,11 +106,28 @@ struct HashParams {
 // Distinct digests never touch each other's slots except through CAS claims
 // of empty slots, so the parallel apply is race-free. Home slot: the
 // digest's first 4 bytes (little-endian) & mask.
+//
+// Absence witness (round 2): with `witness` set, the apply also keeps the set
+// W of prefix keys (the memo's probe key, a fingerprint of the whole token
+// prefix) of every present digest, found through the link index (digest ->
+// prefix key, filled by every memo insertion). A present digest whose key is
+// unknown (hashed without this memo, or before a memo reset) is counted in
+// *unknown instead. While *unknown == 0, a row whose prefix key is not in W
+// is absent from the tier without computing its SHA-256: equal digests mean
+// equal prefixes (the assumption the digest keys rest on), and equal
+// prefixes have equal keys. A key in W only means "maybe": the row is then
+// hashed as before. Presence slot words 9-10 keep the key counted at the
+// digest's add (word 11: 1 = in W, 2 = unknown), so its removal undoes
+// exactly that.
 struct PresenceView {
     uint32_t* slots = nullptr;            // device, [mask + 1] x 16 words
     uint32_t mask = 0;
     const uint32_t* updates = nullptr;    // device-visible (mapped host): n_updates x {digest words[8], present}
     uint32_t n_updates = 0;
+    unsigned long long* witness = nullptr;  // [mask + 1] x {key, count}: W (optional)
+    unsigned int* unknown = nullptr;        // present digests with no known key
+    const uint32_t* links = nullptr;        // link index, [link_mask + 1] x 16 words
+    uint32_t link_mask = 0;
 };
 
 // Lookup outputs of the memo probe / hash kernels with a presence index:
@@ -142,12 +159,16 @@ struct MemoView {
     uint32_t slot_mask = 0;
     uint32_t entry_cap = 0;               // <= 2^24
     uint32_t entry_words = 0;             // 17 + chunk_size
-    unsigned long long* stats = nullptr;  // [0] hits, [1] misses (optional)
+    unsigned long long* stats = nullptr;  // [0] hits, [1] misses, [2] rows the witness decided (optional)
     uint32_t max_rows = 0;                // hash at most this many rows per chain (0 = all)
     uint32_t* first_miss_out = nullptr;   // verify also publishes first_miss here (mapped host)
     PresenceView presence;                // optional: decide the stored prefix on the device
     LookupOut lookup;                     // with presence: per-chain results (mapped host)
     uint32_t* first_absent = nullptr;     // with presence: per chain, first memo hit that is absent
+    // link index: digest -> prefix key of every inserted link (64-byte slots
+    // {digest bytes as 8 words, state, key lo, key hi}); feeds the witness
+    uint32_t* links = nullptr;
+    uint32_t link_mask = 0;
 };
 
 // With a memo whose first_miss is set: probes every row of every chain in

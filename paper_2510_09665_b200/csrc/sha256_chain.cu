@@ -298,6 +298,93 @@ __device__ __forceinline__ bool memo_probe(const MemoView& M, uint64_t key, uint
     return false;
 }
 
+// ---- link index (MemoView::links): digest -> prefix key ---------------------
+// slot states of the link and presence tables
+constexpr uint32_t kSlotEmpty = 0, kSlotPresent = 1, kSlotGone = 2, kSlotClaim = 3;
+
+// One thread; h = the digest as SHA state words. A digest already indexed is
+// left alone (same digest, same prefix, same key); a full table drops it.
+__device__ void link_insert(uint32_t* links, uint32_t mask, const uint32_t h[8], uint64_t key) {
+    uint32_t b[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) b[i] = __byte_perm(h[i], 0, 0x0123);
+    uint32_t i = b[0] & mask;
+    for (uint32_t n = 0; n <= mask;) {
+        uint32_t* sp = links + 16ull * i;
+        const uint32_t st = atomicAdd(sp + 8, 0u);
+        if (st == kSlotEmpty) {
+            if (atomicCAS(sp + 8, kSlotEmpty, kSlotClaim) == kSlotEmpty) {
+#pragma unroll
+                for (int k = 0; k < 8; ++k) sp[k] = b[k];
+                sp[9] = uint32_t(key);
+                sp[10] = uint32_t(key >> 32);
+                __threadfence();
+                atomicExch(sp + 8, kSlotPresent);
+                return;
+            }
+            continue;
+        }
+        if (st == kSlotClaim) continue;
+        bool eq = true;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) eq &= __ldcg(sp + k) == b[k];
+        if (eq) return;
+        i = (i + 1) & mask;
+        ++n;
+    }
+}
+
+// The prefix key of a digest (bytes as words), if a link recorded it.
+__device__ bool link_find(const uint32_t* links, uint32_t mask, const uint32_t b[8], uint64_t* key) {
+    uint32_t i = b[0] & mask;
+    for (uint32_t n = 0; n <= mask;) {
+        const uint32_t* sp = links + 16ull * i;
+        const uint32_t st = atomicAdd(const_cast<uint32_t*>(sp + 8), 0u);
+        if (st == kSlotEmpty) return false;
+        if (st == kSlotClaim) continue;  // being published: wait for it
+        bool eq = true;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) eq &= __ldcg(sp + k) == b[k];
+        if (eq) {
+            *key = uint64_t(__ldcg(sp + 9)) | (uint64_t(__ldcg(sp + 10)) << 32);
+            return true;
+        }
+        i = (i + 1) & mask;
+        ++n;
+    }
+    return false;
+}
+
+// ---- absence witness W (PresenceView::witness): prefix key -> count ---------
+__device__ __forceinline__ unsigned long long witness_key(uint64_t key) { return key ? key : 1ull; }
+
+__device__ void witness_add(const PresenceView& P, uint64_t key, int delta) {
+    const unsigned long long k = witness_key(key);
+    uint32_t i = uint32_t(k ^ (k >> 32)) & P.mask;
+    for (uint32_t n = 0; n <= P.mask; ++n, i = (i + 1) & P.mask) {
+        unsigned long long* sp = P.witness + 2ull * i;
+        const unsigned long long old = atomicCAS(sp, 0ull, k);
+        if (old == 0ull || old == k) {
+            atomicAdd(reinterpret_cast<unsigned int*>(sp + 1), unsigned(delta));
+            return;
+        }
+    }
+}
+
+// May the tier hold a digest whose prefix key is `key`? (false = certainly not)
+__device__ bool witness_may_hold(const PresenceView& P, uint64_t key) {
+    if (P.witness == nullptr || __ldcg(P.unknown) != 0u) return true;
+    const unsigned long long k = witness_key(key);
+    uint32_t i = uint32_t(k ^ (k >> 32)) & P.mask;
+    for (uint32_t n = 0; n <= P.mask; ++n, i = (i + 1) & P.mask) {
+        const unsigned long long* sp = P.witness + 2ull * i;
+        const unsigned long long v = __ldcg(sp);
+        if (v == 0ull) return false;
+        if (v == k) return __ldcg(reinterpret_cast<const unsigned int*>(sp + 1)) != 0u;
+    }
+    return true;
+}
+
 __device__ __forceinline__ void memo_insert(const MemoView& M, const uint32_t* s_parent, const uint32_t* s_tok,
                                             uint32_t n, uint64_t key, uint32_t lane, const uint32_t h[8]) {
     unsigned int e = 0;
@@ -327,14 +414,14 @@ __device__ __forceinline__ void memo_insert(const MemoView& M, const uint32_t* s
             atomicExch(sp, packed);  // publish: readers acquire the tag, then the digest
             break;
         }
+        if (M.links != nullptr) link_insert(M.links, M.link_mask, h, key);
     }
 }
 
 // ---- presence index probe (PresenceView, kernels.hpp) ----------------------
 constexpr uint32_t kDecided = 0x80000000u;
 
-// Slot states of the presence index (PresenceView).
-constexpr uint32_t kSlotEmpty = 0, kSlotPresent = 1, kSlotGone = 2, kSlotClaim = 3;
+// Slot states of the presence index (PresenceView): kSlot* above.
 
 // Is the digest whose words (digest bytes, little-endian) are b[8] in the
 // table? Tombstones keep probe runs contiguous; a slot's digest and state
@@ -360,12 +447,37 @@ __device__ __forceinline__ bool presence_has(const PresenceView& P, const uint32
     return presence_has_words(P, b);
 }
 
+// The witness side of a digest turning present (slot sp, digest b): its
+// prefix key goes into W, or the digest is counted unknown.
+__device__ __forceinline__ void witness_count_add(const PresenceView& P, uint32_t* sp, const uint32_t b[8]) {
+    if (P.witness == nullptr) return;
+    uint64_t key = 0;
+    if (P.links != nullptr && link_find(P.links, P.link_mask, b, &key)) {
+        sp[9] = uint32_t(key);
+        sp[10] = uint32_t(key >> 32);
+        sp[11] = 1;
+        witness_add(P, key, 1);
+    } else {
+        sp[11] = 2;
+        atomicAdd(P.unknown, 1u);
+    }
+}
+
+// ... and of it turning absent: exactly what its add counted.
+__device__ __forceinline__ void witness_count_remove(const PresenceView& P, const uint32_t* sp) {
+    if (P.witness == nullptr) return;
+    const uint32_t mode = __ldcg(sp + 11);
+    if (mode == 1) witness_add(P, uint64_t(__ldcg(sp + 9)) | (uint64_t(__ldcg(sp + 10)) << 32), -1);
+    else if (mode == 2) atomicSub(P.unknown, 1u);
+}
+
 // Applies one pending change (one thread per distinct digest): find the
 // digest's slot in its probe run and set its state, or claim the run's first
 // empty slot (CAS; a concurrent claimer of the same slot publishes its own
 // digest, which we then compare and step past). Removing an absent digest is
 // a no-op; slots are never reused within a table generation (the host
-// rebuilds the table before the tombstones fill it).
+// rebuilds the table before the tombstones fill it). Only real transitions
+// (absent -> present, present -> absent) touch the witness.
 __device__ void presence_apply(const PresenceView& P, const uint32_t* u) {
     uint32_t b[8];
 #pragma unroll
@@ -380,6 +492,7 @@ __device__ void presence_apply(const PresenceView& P, const uint32_t* u) {
             if (atomicCAS(sp + 8, kSlotEmpty, kSlotClaim) == kSlotEmpty) {
 #pragma unroll
                 for (int k = 0; k < 8; ++k) sp[k] = b[k];
+                witness_count_add(P, sp, b);
                 __threadfence();
                 atomicExch(sp + 8, kSlotPresent);
                 return;
@@ -392,7 +505,9 @@ __device__ void presence_apply(const PresenceView& P, const uint32_t* u) {
 #pragma unroll
         for (int k = 0; k < 8; ++k) eq &= __ldcg(sp + k) == b[k];
         if (eq) {
-            atomicExch(sp + 8, present ? kSlotPresent : kSlotGone);
+            const uint32_t old = atomicExch(sp + 8, present ? kSlotPresent : kSlotGone);
+            if (present && old != kSlotPresent) witness_count_add(P, sp, b);
+            if (!present && old == kSlotPresent) witness_count_remove(P, sp);
             return;
         }
         i = (i + 1) & P.mask;
@@ -732,6 +847,12 @@ memo_probe_kernel(const ChainDesc* __restrict__ chains, const HashParams P, uint
                 M.first_miss[blockIdx.x] = rows;  // nothing to hash
                 M.lookup.present_out[blockIdx.x] = absent | kDecided;
                 M.lookup.known_out[blockIdx.x] = absent + 1;
+            } else if (first < rows && !witness_may_hold(M.presence, keys[first])) {
+                // no present digest has this row's prefix: absent, no SHA
+                if (M.stats != nullptr) atomicAdd(M.stats + 2, 1ull);
+                M.first_miss[blockIdx.x] = rows;
+                M.lookup.present_out[blockIdx.x] = first | kDecided;
+                M.lookup.known_out[blockIdx.x] = first;
             } else {
                 M.first_miss[blockIdx.x] = first;
                 M.lookup.present_out[blockIdx.x] = first | (first >= rows ? kDecided : 0u);
@@ -907,7 +1028,24 @@ first_row_kernel(const uint32_t* __restrict__ tokens, const ChainDesc* __restric
         }
         if (M.stats != nullptr && lane == 0) atomicAdd(M.stats + (hit ? 0 : 1), 1ull);
         row_was_hit = hit;
-        if (hit) {
+        // the pending presence changes (and the witness) are applied from here on
+        if (lane == 0 && apply_warps != 0) {
+            while (atomicAdd(&applied_warps, 0u) < apply_warps) {
+            }
+            __threadfence();
+        }
+        __syncwarp();
+        bool witnessed_absent = false;
+        if (!hit && M.presence.slots != nullptr) {
+            if (lane == 0) {
+                witnessed_absent = !witness_may_hold(M.presence, key);
+                if (witnessed_absent && M.stats != nullptr) atomicAdd(M.stats + 2, 1ull);
+            }
+            witnessed_absent = __shfl_sync(0xffffffffu, witnessed_absent, 0);
+        }
+        if (witnessed_absent) {
+            flag |= 4u;  // absent, digest not computed
+        } else if (hit) {
 #pragma unroll
             for (int i = 0; i < 8; ++i) h[i] = d[i];
         } else {
@@ -929,12 +1067,7 @@ first_row_kernel(const uint32_t* __restrict__ tokens, const ChainDesc* __restric
             for (int i = 0; i < 8; ++i) h[i] = st[i];
         }
         if (trace != nullptr) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_hashed));
-        if (lane == 0 && apply_warps != 0) {
-            while (atomicAdd(&applied_warps, 0u) < apply_warps) {
-            }
-            __threadfence();
-        }
-        if (lane == 0 && M.presence.slots != nullptr && presence_has(M.presence, h)) flag |= 2u;
+        if (lane == 0 && M.presence.slots != nullptr && !witnessed_absent && presence_has(M.presence, h)) flag |= 2u;
     }
     uint32_t hl = 0;
 #pragma unroll
@@ -955,7 +1088,7 @@ first_row_kernel(const uint32_t* __restrict__ tokens, const ChainDesc* __restric
     }
     // ... then the memo link of a hashed row (the host syncs the stream
     // before the next launch reads the memo)
-    if (n > 0 && M.slots != nullptr && !row_was_hit) memo_insert(M, s.parent, s.tok, n, row_key, lane, h);
+    if (n > 0 && M.slots != nullptr && !row_was_hit && !(flag & 4u)) memo_insert(M, s.parent, s.tok, n, row_key, lane, h);
 }
 
 // The pending presence changes alone (one thread each), before a lookup.

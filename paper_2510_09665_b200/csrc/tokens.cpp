@@ -219,6 +219,10 @@ void KeyHasher::enable_presence(size_t max_entries, PresenceDrain drain) {
     while (cap < 4 * max_entries) cap <<= 1;
     presence_table_.reserve(cap * 64);
     TKV_CUDA(cudaMemsetAsync(presence_table_.ptr, 0, cap * 64, stream_));
+    witness_table_.reserve(cap * 16);
+    witness_meta_.reserve(64);
+    TKV_CUDA(cudaMemsetAsync(witness_table_.ptr, 0, cap * 16, stream_));
+    TKV_CUDA(cudaMemsetAsync(witness_meta_.ptr, 0, 64, stream_));
     TKV_CUDA(cudaStreamSynchronize(stream_));
     presence_mask_ = uint32_t(cap - 1);
     presence_used_ = 0;
@@ -241,6 +245,8 @@ void KeyHasher::presence_sync_locked(MemoView& m) {
     }
     if (reset) {
         TKV_CUDA(cudaMemsetAsync(presence_table_.ptr, 0, cap * 64, stream_));
+        TKV_CUDA(cudaMemsetAsync(witness_table_.ptr, 0, cap * 16, stream_));
+        TKV_CUDA(cudaMemsetAsync(witness_meta_.ptr, 0, 64, stream_));
         presence_used_ = 0;
     }
     presence_used_ += adds;
@@ -255,6 +261,13 @@ void KeyHasher::presence_sync_locked(MemoView& m) {
     m.presence.mask = presence_mask_;
     m.presence.updates = reinterpret_cast<const uint32_t*>(h_updates_.dev);
     m.presence.n_updates = uint32_t(n);
+    // the absence witness needs the memo's link index (TKV_NO_WITNESS: off)
+    static const bool no_witness = std::getenv("TKV_NO_WITNESS") != nullptr;
+    const bool witness = memo_.links != nullptr && !no_witness;
+    m.presence.witness = witness ? reinterpret_cast<unsigned long long*>(witness_table_.ptr) : nullptr;
+    m.presence.unknown = witness ? reinterpret_cast<unsigned int*>(witness_meta_.ptr) : nullptr;
+    m.presence.links = memo_.links;
+    m.presence.link_mask = memo_.link_mask;
 }
 
 // Cold-lookup fast path: row 0 of every chain in one launch (first_row
@@ -339,7 +352,7 @@ bool KeyHasher::first_row_lookup(const std::vector<TokenSpanView>& seqs, const s
     for (size_t i = 0; i < n_chains; ++i) {
         present_rows[i] = 0;
         out[i].clear();
-        if (rows[i] == 0) continue;
+        if (rows[i] == 0 || (flags[i] & 4u)) continue;  // (4: absent by the witness, not hashed)
         Digest d;
         std::memcpy(d.data(), dig + 8 * i, 32);
         out[i].push_back(d);
@@ -563,6 +576,9 @@ void KeyHasher::enable_memo(size_t entries) {
     memo_.slot_mask = uint32_t(slots - 1);
     memo_.entry_cap = uint32_t(entries);
     memo_.entry_words = words;
+    link_table_.reserve(slots * 64);  // one link per entry at most, half full at worst
+    memo_.links = reinterpret_cast<uint32_t*>(link_table_.ptr);
+    memo_.link_mask = uint32_t(slots - 1);
     TKV_CUDA(cudaMemsetAsync(memo_meta_.ptr, 0, 64, stream_));
     memo_reset_locked();
     // Keep the slot table (64 B per slot) resident in L2 for this stream's
@@ -593,6 +609,10 @@ void KeyHasher::enable_memo(size_t entries) {
 void KeyHasher::memo_reset_locked() {
     TKV_CUDA(cudaMemsetAsync(memo_.slots, 0, (size_t(memo_.slot_mask) + 1) * 64, stream_));
     TKV_CUDA(cudaMemsetAsync(memo_.counter, 0, sizeof(unsigned int), stream_));
+    // the links go too: present digests added from now on without a link are
+    // counted unknown (the witness is then off until they leave the tier);
+    // those already counted keep their key in the presence slot
+    if (memo_.links) TKV_CUDA(cudaMemsetAsync(memo_.links, 0, (size_t(memo_.link_mask) + 1) * 64, stream_));
     memo_used_bound_ = 0;
     ++memo_resets_;
 }
@@ -601,7 +621,7 @@ KeyHasher::MemoStats KeyHasher::memo_stats() {
     std::lock_guard lock(mu_);
     MemoStats s;
     if (!memo_.slots) return s;
-    unsigned long long st[2] = {0, 0};
+    unsigned long long st[3] = {0, 0, 0};
     TKV_CUDA(cudaMemcpyAsync(st, memo_.stats, sizeof st, cudaMemcpyDeviceToHost, stream_));
     TKV_CUDA(cudaStreamSynchronize(stream_));
     s.hits = st[0];
@@ -609,6 +629,7 @@ KeyHasher::MemoStats KeyHasher::memo_stats() {
     s.capacity = memo_.entry_cap;
     s.resets = memo_resets_ - 1;  // the enabling clear is not a reset
     s.rehashes = memo_rehashes_;
+    s.witnessed = st[2];
     return s;
 }
 

@@ -92,6 +92,7 @@ public:
     void enable_memo(size_t entries);
     struct MemoStats {
         uint64_t hits = 0, misses = 0, capacity = 0, resets = 0, rehashes = 0;
+        uint64_t witnessed = 0;  // lookup rows decided absent by the witness (no SHA)
     };
     MemoStats memo_stats();
     // Test hook: corrupt every memo slot's digest (hits must then fail
@@ -122,6 +123,8 @@ private:
     std::unordered_set<uint64_t> seen_row0_;            // route hint: first chunks looked up before
     PresenceDrain presence_drain_;
     DeviceBuffer presence_table_;
+    DeviceBuffer witness_table_, witness_meta_;  // absence witness W + unknown count (kernels.hpp)
+    DeviceBuffer link_table_;                    // memo link index: digest -> prefix key
     PinnedBuffer h_updates_;
     uint32_t presence_mask_ = 0;
     size_t presence_used_ = 0;  // slots claimed since the table was cleared (upper bound)

@@ -277,3 +277,141 @@ def test_presence_many_changes_between_lookups(tkv, C):
     assert e.get_num_new_matched_tokens(4, other) == len(other) - 1
     e.finish_query(4)
     e.close()
+
+
+def test_absence_witness_decides_without_sha(tkv, C):
+    """The absence witness (kernels.hpp PresenceView): a row whose prefix key
+    no present digest has is absent without its SHA-256 — the cold first row
+    of a new document (first-row kernel) and the question row after a stored
+    document (probe kernel). A present digest with no memo link (seeded into
+    the tier) turns the witness off until it leaves; clears and evictions keep
+    W exact. Every hit length equals the host index's LPM."""
+    from paper_2510_09665_b200.api import Engine
+    rng = np.random.default_rng(21)
+    e = Engine(num_layers=2, bpt=64, page_tokens=16, tag=TAG, chunk_size=256, ram_slots=8, num_pages=4096)
+
+    def lpm(p):
+        keys = C.chunk_keys(p, 256, TAG)
+        k = 0
+        while k < len(keys) and e.contains(keys[k]):
+            k += 1
+        return min(len(p) - 1, 256 * k) if len(p) else 0
+
+    qid = [100]
+
+    def lookup(p):
+        qid[0] += 1
+        m = e.get_num_new_matched_tokens(qid[0], p)
+        e.finish_query(qid[0])
+        assert m == lpm(p)
+        return m
+
+    def store(p):
+        qid[0] += 1
+        q = qid[0]
+        e.get_num_new_matched_tokens(q, p)
+        e.bind_pages(q, len(p))
+        e.update_state_after_alloc(q, (len(p) + 15) // 16, 0)
+        m = e.build_connector_meta([(q, p)])
+        S.transfer(e, m, q, p)
+        e.drop_meta(m)
+        e.finish_query(q)
+        e.release_query(q)
+
+    doc = rng.integers(0, 128256, size=256 * 4, dtype=np.uint32)
+    store(doc)                                             # 4 chunks, linked by the planning hash
+    w0 = e.lookups_witnessed()
+    assert lookup(rng.integers(0, 128256, size=700, dtype=np.uint32)) == 0   # cold: first row witnessed
+    assert e.lookups_witnessed() == w0 + 1
+    q = np.concatenate([doc, rng.integers(0, 128256, size=60, dtype=np.uint32)])
+    assert lookup(q) == 1024                               # stored doc + question: question row witnessed
+    assert e.lookups_witnessed() == w0 + 2
+    fork = np.concatenate([doc[:512], rng.integers(0, 128256, size=300, dtype=np.uint32)])
+    assert lookup(fork) == 512                             # diverges inside chunk 2
+    assert e.lookups_witnessed() == w0 + 3
+    # a present digest without a link: the witness is off, results unchanged
+    seeded = rng.integers(0, 128256, size=256 * 2, dtype=np.uint32)
+    e.seed_store(seeded, 512)
+    w1 = e.lookups_witnessed()
+    assert lookup(rng.integers(0, 128256, size=400, dtype=np.uint32)) == 0
+    assert lookup(q) == 1024
+    assert lookup(seeded) == 511
+    assert e.lookups_witnessed() == w1
+    for k in C.chunk_keys(seeded, 256, TAG):               # they leave: the witness is back
+        assert e.store_clear(k) == 1
+    assert lookup(rng.integers(0, 128256, size=400, dtype=np.uint32)) == 0
+    assert e.lookups_witnessed() == w1 + 1
+    # evictions: the tier holds 8 chunks; two more documents push doc out
+    for _ in range(2):
+        store(rng.integers(0, 128256, size=256 * 3, dtype=np.uint32))
+    lookup(q)
+    lookup(doc)
+    lookup(fork)
+    assert e.store_clear(C.chunk_keys(doc, 256, TAG)[0]) in (0, 1)
+    lookup(q)
+    e.close()
+
+
+def test_absence_witness_random_trace(tkv, C):
+    """Random stores (through the connector), seeds without links, clears
+    and evictions interleaved with lookups of prefixes, forks and fresh
+    prompts: every hit length equals the host index's LPM, and the witness
+    decides a good share of the absent rows."""
+    from paper_2510_09665_b200.api import Engine
+    rng = np.random.default_rng(5)
+    e = Engine(num_layers=1, bpt=32, page_tokens=16, tag=TAG, chunk_size=256, ram_slots=24, num_pages=8192)
+    docs, qid = [], [0]
+
+    def lpm(p):
+        keys = C.chunk_keys(p, 256, TAG)
+        k = 0
+        while k < len(keys) and e.contains(keys[k]):
+            k += 1
+        return min(len(p) - 1, 256 * k) if len(p) else 0
+
+    def next_q():
+        qid[0] += 1
+        return qid[0]
+
+    seeded = []
+    for step in range(160):
+        op = rng.random()
+        if op < 0.25 or not docs:
+            p = rng.integers(0, 128256, size=int(rng.integers(1, 6)) * 256 + int(rng.integers(0, 200)), dtype=np.uint32)
+            q = next_q()
+            e.get_num_new_matched_tokens(q, p)
+            e.bind_pages(q, len(p))
+            e.update_state_after_alloc(q, (len(p) + 15) // 16, 0)
+            m = e.build_connector_meta([(q, p)])
+            S.transfer(e, m, q, p)
+            e.drop_meta(m)
+            e.finish_query(q)
+            e.release_query(q)
+            docs.append(p)
+        elif op < 0.30:
+            p = rng.integers(0, 128256, size=256 * int(rng.integers(1, 3)), dtype=np.uint32)
+            e.seed_store(p, len(p))
+            seeded.append(p)
+        elif op < 0.38 and seeded:
+            p = seeded.pop(int(rng.integers(0, len(seeded))))
+            for k in C.chunk_keys(p, 256, TAG):
+                e.store_clear(k)
+        elif op < 0.42:
+            d = docs[int(rng.integers(0, len(docs)))]
+            for k in C.chunk_keys(d, 256, TAG)[int(rng.integers(0, 3)):]:
+                e.store_clear(k)
+        else:
+            d = docs[int(rng.integers(0, len(docs)))]
+            r = rng.random()
+            if r < 0.4:
+                p = np.concatenate([d, rng.integers(0, 128256, size=int(rng.integers(1, 100)), dtype=np.uint32)])
+            elif r < 0.7:
+                cut = int(rng.integers(1, len(d) + 1))
+                p = np.concatenate([d[:cut], rng.integers(0, 128256, size=int(rng.integers(1, 400)), dtype=np.uint32)])
+            else:
+                p = rng.integers(0, 128256, size=int(rng.integers(1, 1500)), dtype=np.uint32)
+            q = next_q()
+            assert e.get_num_new_matched_tokens(q, p) == lpm(p), step
+            e.finish_query(q)
+    assert e.lookups_witnessed() > 10
+    e.close()
