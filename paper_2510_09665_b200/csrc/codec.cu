@@ -9,7 +9,7 @@
 // division / multiplication are IEEE correctly rounded on both sides, so the
 // bytes match. One launch covers a batch of chunk payloads. Decode is
 // HBM-bound; encode reads the payload twice (absmax, then quantise) and its
-// quantise pass is issue-bound (DMUL + 3 DADD + integer work per lane).
+// quantise pass is issue-bound (DADD + DFMA + integer work per lane).
 // A single-pass variant — absmax units of item k+1 claimed before the
 // quantise units of item k from one atomic work queue, the quantise re-read
 // served from L2 — cut DRAM reads from 2.0x to 1.12x payload but ran slower
@@ -85,25 +85,23 @@ q8_absmax_kernel(const CodecItem* __restrict__ items, const uint32_t* __restrict
     }
 }
 
-// round(double(lane) / double(scale)) without the division (codec.cpp:42-44).
-// scale is a float (24-bit significand M) and |lane| <= 32768, so a quotient
-// that is not exactly k + 1/2 lies at least 1/(2M) >= 2^-25 away from every
-// half-integer, while lane * (1/scale) in double is within ~6e-14 of the
-// quotient. So round-half-away-from-zero of the quotient is
-// floor(|product| + 1/2 + 1e-10): the 1e-10 lifts an exact tie that the
-// product missed by ~1e-13 over the half-integer, and is far too small to
-// move any other quotient across one. (The reference's correctly rounded
-// double quotient rounds the same way for the same reason.)
-// Both conversions stay off the XU pipe (76 % busy with I2F/F2I.F64 when
-// they were conversions; 171 -> 160 us): |lane| -> double is the exact 2^52
-// magic subtraction, and the truncation is a round-toward-zero add of 2^52,
-// whose low word is floor(t) for 0 <= t < 2^32. The product is __dmul_rn so
-// it is never contracted into an FMA with the + 1/2.
-__device__ __forceinline__ uint32_t quant(int32_t lane, double inv) {
+// round(double(lane) / double(scale)) without the division (codec.cpp:42-44),
+// in two FP64 instructions per lane. scale is a float (24-bit significand M)
+// and |lane| <= 32768, so a quotient Q = |lane| / scale that is not exactly
+// k + 1/2 lies at least 1/(2M) >= 2^-25 away from every half-integer. With
+// inv = 1/scale rounded UP, Q' = |lane| * inv (exact inside the FMA) is in
+// [Q, Q + 2^-45]: an exact tie stays on or just above k + 1/2 (rounds away
+// from zero, as round() does) and no other quotient crosses a half-integer.
+// fma.rz(|lane|, inv, 2^45 + 1/2) then holds floor(Q' + 1/2) in its integer
+// part (round-toward-zero onto the 2^-7 grid of [2^45, 2^46) cannot cross an
+// integer), i.e. bits 7.. of the low word. |lane| -> double is the exact 2^52
+// magic subtraction (no conversion on the XU pipe). (The reference's
+// correctly rounded double quotient rounds the same way for the same reason.)
+__device__ __forceinline__ uint32_t quant(int32_t lane, double inv_up) {
     constexpr double kMagic = 4503599627370496.0;  // 2^52
     const double al = __hiloint2double(0x43300000, abs(lane)) - kMagic;  // exact, |lane| <= 32768
-    const double t = __dadd_rz(__dmul_rn(al, inv) + (0.5 + 1e-10), kMagic);
-    const uint32_t q = min(uint32_t(__double2loint(t)), 127u);
+    const double t = __fma_rz(al, inv_up, 35184372088832.5);               // 2^45 + 1/2
+    const uint32_t q = min(uint32_t(__double2loint(t)) >> 7, 127u);
     return (lane < 0 ? 0u - q : q) & 0xffu;
 }
 
@@ -118,7 +116,7 @@ q8_encode_kernel(const CodecItem* __restrict__ items, const uint32_t* __restrict
         }
         const CodecItem it = items[lo];
         const float scale = float(double(maxabs[lo]) / 127.0);
-        const double inv = scale > 0.f ? 1.0 / double(scale) : 0.0;  // scale 0: every lane is 0
+        const double inv = scale > 0.f ? __drcp_ru(double(scale)) : 0.0;  // scale 0: every lane is 0
         const uint32_t local = seg - seg_base[lo];
         if (local == 0 && threadIdx.x == 0) {
             const uint32_t len = uint32_t(it.bytes);
