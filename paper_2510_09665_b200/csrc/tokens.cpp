@@ -414,7 +414,10 @@ std::vector<std::vector<Digest>> KeyHasher::hash_prefix(const std::vector<TokenS
         const double ts0 = trace_lookup() ? now_us() : 0;
         presence_sync_locked(memo_);
         const uint32_t n_upd = memo_.presence.n_updates;
-        if (use_first_row && n_chains > 2) {
+        // a multi-CTA first-row launch, or more changes than its apply warps
+        // take in one round (each change probes the link index and the
+        // witness): the whole grid applies them first
+        if (use_first_row && (n_chains > 2 || n_upd > 192)) {
             TKV_CUDA(launch_presence_apply(memo_.presence, stream_));
             memo_.presence.n_updates = 0;
         }
