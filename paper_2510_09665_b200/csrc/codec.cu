@@ -29,10 +29,6 @@ constexpr uint64_t kSeg = 64 * 1024;  // payload bytes per CTA work item
 constexpr int kUnroll = 4;            // 16-byte vectors in flight per thread
 constexpr uint64_t kStride = 16 * kThreads;
 
-__device__ __forceinline__ int32_t lane16(uint32_t w, int half) {
-    return int32_t(int16_t(uint16_t(w >> (16 * half))));
-}
-
 // Grid-stride over (item, segment): per-item max |lane| into maxabs[item].
 __global__ void __launch_bounds__(kThreads)
 q8_absmax_kernel(const CodecItem* __restrict__ items, const uint32_t* __restrict__ seg_base,
@@ -105,6 +101,53 @@ __device__ __forceinline__ uint32_t quant(int32_t lane, double inv_up) {
     return (lane < 0 ? 0u - q : q) & 0xffu;
 }
 
+// Four lanes (two little-endian words) -> four q8 bytes, the vector path of
+// the encode: |lane| as the low word of the double 2^52 + |lane| (one move
+// of the constant high word), then ONE fma.rz per lane:
+//   fma.rz(2^52 + |lane|, inv, c),  c = 2^44 + 1/2 - 2^52 inv  (kFold)
+// is exactly 2^44 + 1/2 + |lane| inv rounded toward zero onto the 2^-8 grid
+// of [2^44, 2^45), so byte 1 of its low word is floor(Q' + 1/2) — quant()'s
+// value. c is exact when inv < 1/2 (scale > 2: c is a multiple of inv's ulp
+// below 2^53 of them); smaller scales take quant()'s subtraction first
+// (!kFold). No clamp: |lane| <= max|lane| = 127 * scale * (1 +- 2^-24), so
+// the byte is at most 127. Signs are applied bytewise: prmt's sign-replicate
+// mode turns each lane's high byte into a 0x00 / 0xff mask, and for
+// n <= 127, ((n ^ 0x7f) + 1) ^ 0x80 = -n mod 256 with no carry between bytes.
+template <bool kFold>
+__device__ __forceinline__ uint32_t quant4(uint32_t w0, uint32_t w1, double inv, double c) {
+    constexpr double kMagic = 4503599627370496.0;  // 2^52
+    const uint32_t a0 = __vabs2(w0), a1 = __vabs2(w1);  // -32768 -> 0x8000 (non-saturating)
+    const uint32_t mag[4] = {a0 & 0xffffu, a0 >> 16, a1 & 0xffffu, a1 >> 16};
+    uint32_t t[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        const double x = __hiloint2double(0x43300000, int(mag[k]));
+        t[k] = uint32_t(__double2loint(kFold ? __fma_rz(x, inv, c) : __fma_rz(x - kMagic, inv, 17592186044416.5)));
+    }
+    const uint32_t n = __byte_perm(__byte_perm(t[0], t[1], 0x0051), __byte_perm(t[2], t[3], 0x0051), 0x5410);
+    uint32_t m;  // 0xff where the lane is negative
+    asm("prmt.b32 %0, %1, %2, 0xFDB9;" : "=r"(m) : "r"(w0), "r"(w1));
+    const uint32_t neg = ((n ^ 0x7f7f7f7fu) + 0x01010101u) ^ 0x80808080u;
+    return (neg & m) | (n & ~m);
+}
+
+template <bool kFold>
+__device__ __forceinline__ void quant_vectors(const uint8_t* __restrict__ src, uint8_t* __restrict__ out,
+                                              uint64_t b0, uint64_t vend, double inv, double c) {
+    for (uint64_t b = b0 + 16 * threadIdx.x; b < vend; b += kStride * kUnroll) {
+        uint4 v[kUnroll];
+#pragma unroll
+        for (int u = 0; u < kUnroll; ++u)
+            if (b + u * kStride < vend) v[u] = __ldcs(reinterpret_cast<const uint4*>(src + b + u * kStride));
+#pragma unroll
+        for (int u = 0; u < kUnroll; ++u) {
+            if (b + u * kStride >= vend) break;
+            __stcs(reinterpret_cast<uint2*>(out + (b + u * kStride) / 2),
+                   make_uint2(quant4<kFold>(v[u].x, v[u].y, inv, c), quant4<kFold>(v[u].z, v[u].w, inv, c)));
+        }
+    }
+}
+
 __global__ void __launch_bounds__(kThreads)
 q8_encode_kernel(const CodecItem* __restrict__ items, const uint32_t* __restrict__ seg_base,
                  uint32_t n_items, uint32_t total_segs, const int* __restrict__ maxabs) {
@@ -135,24 +178,10 @@ q8_encode_kernel(const CodecItem* __restrict__ items, const uint32_t* __restrict
         uint64_t vend = b0;
         if (((reinterpret_cast<uint64_t>(it.src) & 15) | (reinterpret_cast<uint64_t>(out) & 7)) == 0) {
             vend = b0 + ((b1 - b0) & ~uint64_t(15));
-            for (uint64_t b = b0 + 16 * threadIdx.x; b < vend; b += kStride * kUnroll) {
-                uint4 v[kUnroll];
-#pragma unroll
-                for (int u = 0; u < kUnroll; ++u)
-                    if (b + u * kStride < vend) v[u] = __ldcs(reinterpret_cast<const uint4*>(it.src + b + u * kStride));
-#pragma unroll
-                for (int u = 0; u < kUnroll; ++u) {
-                    if (b + u * kStride >= vend) break;
-                    const uint32_t w[4] = {v[u].x, v[u].y, v[u].z, v[u].w};
-                    uint32_t o[2];
-#pragma unroll
-                    for (int k = 0; k < 2; ++k)
-                        o[k] = quant(lane16(w[2 * k], 0), inv) | (quant(lane16(w[2 * k], 1), inv) << 8) |
-                               (quant(lane16(w[2 * k + 1], 0), inv) << 16) |
-                               (quant(lane16(w[2 * k + 1], 1), inv) << 24);
-                    __stcs(reinterpret_cast<uint2*>(out + (b + u * kStride) / 2), make_uint2(o[0], o[1]));
-                }
-            }
+            if (inv < 0.5)  // (uniform per item)
+                quant_vectors<true>(it.src, out, b0, vend, inv, 17592186044416.5 - inv * 4503599627370496.0);
+            else
+                quant_vectors<false>(it.src, out, b0, vend, inv, 0.0);
         }
         for (uint64_t b = vend + 2 * threadIdx.x; b + 2 <= b1; b += 2 * kThreads) {
             const int32_t lane = int32_t(int16_t(uint16_t(it.src[b] | (it.src[b + 1] << 8))));
