@@ -8,13 +8,13 @@
 // round() is round-half-away-from-zero in both C and CUDA, and double
 // division / multiplication are IEEE correctly rounded on both sides, so the
 // bytes match. One launch covers a batch of chunk payloads. Decode is
-// HBM-bound; encode reads the payload twice (absmax, then quantise) and its
-// quantise pass is issue-bound (DADD + DFMA + integer work per lane).
-// A single-pass variant — absmax units of item k+1 claimed before the
-// quantise units of item k from one atomic work queue, the quantise re-read
-// served from L2 — cut DRAM reads from 2.0x to 1.12x payload but ran slower
-// (315 us vs 257 us for 16 x 32 MiB: lower occupancy plus per-unit queue
-// work on an issue-bound pass), so the two kernels stay.
+// HBM-bound; encode reads the payload twice (absmax, then quantise), both
+// passes near DRAM speed (the quantise at one fma.rz per lane, quant4).
+// Single-pass variants — an atomic work queue (round 1), a persistent grid
+// quantising one round behind its absmax (round 2) — cut DRAM reads to
+// 1.05-1.12x payload through L2 reuse but ran slower (0.27-0.37 ms vs 0.25
+// for 16 x 32 MiB: each CTA alternates a DRAM-latency phase and an L2 phase
+// with little memory parallelism), so the two kernels stay.
 #include <cuda_runtime.h>
 
 #include <cstdint>
