@@ -55,6 +55,10 @@ const char* tkv_errc_name(int code);
 const char* tkv_build_info(void);
 /* Kernel launches issued by this library since load (bench gpu_launches). */
 uint64_t tkv_launch_count(void);
+/* The connector's host copy of prompt-sized buffers (memcpy semantics; split
+ * over helper threads with streaming stores from 128 KiB on). Exported for
+ * tests. */
+void tkv_host_copy(void* dst, const void* src, size_t n);
 
 /* ---- geometry: include/tierkv/model.hpp:11-33 ----------------------------- */
 typedef struct tkv_model_spec {

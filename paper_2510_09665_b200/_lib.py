@@ -65,6 +65,7 @@ SIGNATURES = {
     "tkv_errc_name": (ct.c_char_p, [ct.c_int]),
     "tkv_build_info": (ct.c_char_p, []),
     "tkv_launch_count": (ct.c_uint64, []),
+    "tkv_host_copy": (None, [vp, vp, ct.c_size_t]),
     "tkv_plan_tiles": (ct.c_int, [ct.c_void_p, ct.c_uint32, ct.c_uint32, ct.c_uint32, ct.c_uint32,
                                   ct.c_uint32, u32p, u32p]),
     "tkv_gather_layers": (ct.c_int, [ct.POINTER(PagedLayoutC), vp, vp, ct.c_uint32, ct.c_uint32, ct.c_uint32,

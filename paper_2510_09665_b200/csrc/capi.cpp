@@ -9,6 +9,7 @@
 
 #include "connector.hpp"
 #include "copy_plan.hpp"
+#include "host_copy.hpp"
 #include "kernels.hpp"
 #include "paged_store.hpp"
 #include "pd.hpp"
@@ -150,6 +151,7 @@ const char* tkv_last_error(void) { return g_err.c_str(); }
 const char* tkv_errc_name(int code) { return errc_name(Errc(code)); }
 const char* tkv_build_info(void) { return "tierkv_b200 sm_100a " __DATE__ " " __TIME__; }
 uint64_t tkv_launch_count(void) { return launch_count(); }
+void tkv_host_copy(void* dst, const void* src, size_t n) { host_copy(dst, src, n); }
 
 // ---- kernel level -----------------------------------------------------------
 

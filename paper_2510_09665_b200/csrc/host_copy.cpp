@@ -6,6 +6,7 @@
 #include "host_copy.hpp"
 
 #include <emmintrin.h>
+#include <pthread.h>
 
 #include <algorithm>
 #include <atomic>
@@ -48,9 +49,14 @@ void copy_stream(void* dst, const void* src, size_t n) {
     std::memcpy(d + 16 * v, s + 16 * v, n - 16 * v);
 }
 
+// A forked child has the crew's state but none of its threads: it copies
+// alone (its copies never wait for helpers that do not exist).
+std::atomic<bool> g_forked{false};
+
 class CopyCrew {
 public:
     CopyCrew() {
+        pthread_atfork(nullptr, nullptr, [] { g_forked.store(true); });
         const char* e = std::getenv("TKV_COPY_THREADS");  // helpers besides the caller
         unsigned k = e ? unsigned(std::atoi(e)) : std::min(3u, std::max(1u, std::thread::hardware_concurrency() / 4));
         for (unsigned t = 0; t < k; ++t) helpers_.emplace_back([this] { loop(); });
@@ -61,7 +67,7 @@ public:
         wake_.notify_all();
         for (auto& t : helpers_) t.join();
     }
-    bool enabled() const { return !helpers_.empty(); }
+    bool enabled() const { return !helpers_.empty() && !g_forked.load(std::memory_order_relaxed); }
     void prime() {
         wake_.fetch_add(1, std::memory_order_release);
         wake_.notify_all();
@@ -138,9 +144,11 @@ private:
     std::atomic<uint32_t> pieces_{0};
 };
 
+// Never destroyed: helpers may be asleep in a futex at process exit, and a
+// joined-at-exit crew would hang a forked child that inherited it.
 CopyCrew& crew() {
-    static CopyCrew c;
-    return c;
+    static CopyCrew* c = new CopyCrew;
+    return *c;
 }
 
 }  // namespace
