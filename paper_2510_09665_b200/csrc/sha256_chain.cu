@@ -208,40 +208,40 @@ __device__ __forceinline__ void expand_block(const uint32_t* in, uint32_t* out) 
 
 // The 64 rounds with K+W precomputed: only the state recurrence is serial.
 // The round is arranged around its shortest dependent path. With
-//   Y_t  = h_t + (K+W)_t            (h_t = e_{t-3}: known three rounds ahead)
-//   Yd_t = Y_t + d_t                (d_t = a_{t-3}: likewise)
-// both prepared one round early, off the chains,
-//   e_{t+1} = Sigma1(e_t) + Ch(e_t, f_t, g_t) + Yd_t      one IADD3
-//   a_{t+1} = Sigma1(e_t) + Ch(e_t, f_t, g_t) + Y_t + Sigma0(a_t) + Maj(a_t, b_t, c_t)
-// so e advances by SHF -> LOP3 -> IADD3 per round and a by one IADD3 more
-// (round 1's version computed h + K+W + Sigma1 + Ch, then d + T1: four
-// dependent ALU ops on the e chain, ~31 cycles per round measured).
-// An add the compiler may not reassociate (NVVM would otherwise fold the
-// prepared Y_t + d_t back into a three-operand add behind Sigma1 + Ch).
-__device__ __forceinline__ uint32_t add_fixed(uint32_t x, uint32_t y) {
+//   Yd_t = h_t + (K+W)_t + d_t      (h_t = e_{t-3}, d_t = a_{t-3}: known
+//                                    three rounds ahead, prepared off the chains)
+// and T1_t = e_{t+1} - d_t,
+//   e_{t+1} = Sigma1(e_t) + Ch(e_t, f_t, g_t) + Yd_t              one IADD3
+//   a_{t+1} = Sigma0(a_t) + (e_{t+1} + (Maj(a_t, b_t, c_t) - d_t))
+// so each chain is SHF -> LOP3 -> one add per round and a trails e by one
+// add. The adds off the e chain run on the FMA pipe as IMADs (a multiplier
+// ptxas cannot see is 1, so it cannot turn them back into ALU-pipe IADD3s):
+// the ALU pipe keeps the 6 SHF + 4 LOP3 + 1 IADD3 of a round.
+// Measured one chain on one warp (tools/microbench_sha.cu,
+// profiles/r02_k3_round.jsonl): 27.7 cycles per round; round 1's
+// h + KW + S1 + Ch then d + T1 order 30.3, the Y / Yd order 30.0.
+__constant__ uint32_t kOneC = 1u, kMinusOneC = 0xffffffffu;
+
+__device__ __forceinline__ uint32_t mad_c(uint32_t x, uint32_t m, uint32_t y) {
     uint32_t r;
-    asm("add.u32 %0, %1, %2;" : "=r"(r) : "r"(x), "r"(y));
+    asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(r) : "r"(x), "r"(m), "r"(y));
     return r;
 }
 
 __device__ __forceinline__ void compress_kw(uint32_t h[8], const uint32_t* kw) {
+    const uint32_t one = kOneC, mone = kMinusOneC;
     uint32_t a = h[0], b = h[1], c = h[2], d = h[3], e = h[4], f = h[5], g = h[6], hh = h[7];
-    uint32_t y = hh + kw[0];
-    uint32_t yd = y + d;
+    uint32_t yd = mad_c(mad_c(hh, one, kw[0]), one, d);
 #pragma unroll
     for (int t = 0; t < 64; ++t) {
         const uint32_t S1 = rotr(e, 6) ^ rotr(e, 11) ^ rotr(e, 25);
         const uint32_t ch = (e & f) ^ (~e & g);
         const uint32_t S0 = rotr(a, 2) ^ rotr(a, 13) ^ rotr(a, 22);
         const uint32_t mj = (a & b) ^ (a & c) ^ (b & c);
-        // Ch is ready one op before Sigma1: (Ch + Yd) then + Sigma1
-        const uint32_t e_new = add_fixed(S1, add_fixed(ch, yd));
-        const uint32_t t1 = add_fixed(S1, add_fixed(ch, y));
-        const uint32_t a_new = add_fixed(t1, add_fixed(S0, mj));
-        if (t + 1 < 64) {  // next round: h = g, d = c
-            y = g + kw[t + 1];
-            yd = y + c;
-        }
+        const uint32_t mjd = mad_c(d, mone, mj);  // Maj - d
+        const uint32_t e_new = S1 + ch + yd;
+        const uint32_t a_new = mad_c(S0, one, mad_c(e_new, one, mjd));
+        if (t + 1 < 64) yd = mad_c(mad_c(g, one, kw[t + 1]), one, c);  // next round: h = g, d = c
         hh = g;
         g = f;
         f = e;

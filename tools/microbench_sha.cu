@@ -245,6 +245,92 @@ __device__ __forceinline__ void c_v9(uint32_t h[8], const uint32_t* kw, uint32_t
     h[0] += a; h[1] += b; h[2] += c; h[3] += d; h[4] += e; h[5] += f; h[6] += g; h[7] += hh;
 }
 
+// V10: the a chain rebuilt on e_{t+1}: T1 = e_{t+1} - d_t, so
+//   e_{t+1} = Sigma1(e_t) + (Ch + Yd_t)          Yd_t = h_t + KW_t + d_t, off the chains
+//   a_{t+1} = Sigma0(a_t) + (e_{t+1} + (Maj - d_t))
+// each chain is SHF -> LOP3 -> one add per round and a trails e by one add;
+// every add on the FMA pipe (runtime multiplier), the ALU pipe keeps the
+// 6 SHF + 4 LOP3 (20-cycle issue bound)
+__device__ __forceinline__ uint32_t wide_rot(uint32_t x, uint32_t m) {  // rotr via IMAD.WIDE + IMAD
+    const uint64_t p = uint64_t(x) * m;
+    uint32_t r;
+    asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(r) : "r"(uint32_t(p)), "r"(1u), "r"(uint32_t(p >> 32)));
+    return r;
+}
+template <int MODE>
+__device__ __forceinline__ void c_v10(uint32_t h[8], const uint32_t* kw, uint32_t one) {
+    const uint32_t mone = 0u - one;  // -1, opaque to ptxas
+    uint32_t a = h[0], b = h[1], c = h[2], d = h[3], e = h[4], f = h[5], g = h[6], hh = h[7];
+    uint32_t yd = add_rt(add_rt(hh, one, kw[0]), one, d);
+#pragma unroll
+    for (int t = 0; t < 64; ++t) {
+        uint32_t S1, S0;
+        if (MODE == 3) S1 = rotr(e, 6) ^ rotr(e, 11) ^ wide_rot(e, one << 7);  // rotr25 = x * 2^7
+        else S1 = rotr(e, 6) ^ rotr(e, 11) ^ rotr(e, 25);
+        if (MODE == 2 || MODE == 3) S0 = rotr(a, 2) ^ rotr(a, 13) ^ wide_rot(a, one << 10);  // rotr22
+        else S0 = rotr(a, 2) ^ rotr(a, 13) ^ rotr(a, 22);
+        const uint32_t ch = (e & f) ^ (~e & g);
+        const uint32_t mj = (a & b) ^ (a & c) ^ (b & c);
+        const uint32_t mjd = add_rt(d, mone, mj);
+        uint32_t e_new;
+        if (MODE == 1) e_new = S1 + ch + yd;  // one ALU IADD3
+        else e_new = add_rt(S1, one, add_rt(ch, one, yd));
+        const uint32_t a_new = add_rt(S0, one, add_rt(e_new, one, mjd));
+        if (t + 1 < 64) yd = add_rt(add_rt(g, one, kw[t + 1]), one, c);
+        hh = g; g = f; f = e; e = e_new; d = c; c = b; b = a; a = a_new;
+    }
+    h[0] += a; h[1] += b; h[2] += c; h[3] += d; h[4] += e; h[5] += f; h[6] += g; h[7] += hh;
+}
+
+// V14: two lanes per chain. Lane E (even) runs the e chain, lane A (odd) the
+// a chain one round behind; one instruction stream computes Sigma1(e_s) in E
+// and Sigma0(a_{s-1}) in A (per-lane rotate counts), Ch in E and Maj in A,
+// and one SHFL.BFLY per round trades e_{s+1} (A turns it into T1 = e - d)
+// for a_s (E queues it as the d of round s+3).
+__device__ __forceinline__ void c_v14(uint32_t hs[8], const uint32_t* kw_lane, uint32_t one) {
+    const bool A = threadIdx.x & 1;
+    const uint32_t r0 = A ? 2 : 6, r1 = A ? 13 : 11, r2 = A ? 22 : 25;
+    const uint32_t msk = A ? ~0u : 0u;
+    // E: x = (e, f, g, h); A before round 0: x = (b, c, d, -), a0 injected at round 0
+    uint32_t x0 = A ? hs[1] : hs[4], x1 = A ? hs[2] : hs[5], x2 = A ? hs[3] : hs[6], x3 = A ? 0u : hs[7];
+    const uint32_t a0 = hs[0];
+    // d queue (E): after round s's push, q = (a_{s-3}, a_{s-2}, a_{s-1}, a_s);
+    // before round 0: a_{-3}, a_{-2}, a_{-1} = d, c, b of the input state
+    uint32_t q0 = 0, q1 = hs[3], q2 = hs[2], q3 = hs[1];
+    // P for round 0: E: h + KW_0 + d_0; A: unused (its round 0 result is replaced by a0)
+    uint32_t P = x3 + kw_lane[0] + hs[3];
+    uint32_t fe0 = 0, fe1 = 0, fe2 = 0, fe3 = 0;
+#pragma unroll
+    for (int s = 0; s <= 64; ++s) {
+        const uint32_t S = __funnelshift_r(x0, x0, r0) ^ __funnelshift_r(x0, x0, r1) ^ __funnelshift_r(x0, x0, r2);
+        const uint32_t chv = (x0 & x1) ^ (~x0 & x2);
+        const uint32_t mjv = (x0 & x1) ^ (x0 & x2) ^ (x1 & x2);
+        const uint32_t cm = (chv & ~msk) | (mjv & msk);
+        uint32_t nw = add_rt(S, one, add_rt(cm, one, P));
+        if (s == 0) nw = A ? a0 : nw;
+        if (s == 64) { fe0 = x0; fe1 = x1; fe2 = x2; fe3 = x3; }
+        const uint32_t rv = __shfl_xor_sync(0xffffffffu, nw, 1);
+        // shift the history
+        x3 = x2; x2 = x1; x1 = x0; x0 = nw;
+        // d queue (E): rv = a_s arrives; d_{s+1} = a_{s-2} = q1
+        q0 = q1; q1 = q2; q2 = q3; q3 = rv;
+        if (s + 1 <= 64) {
+            // E: P = h_{s+1} + KW_{s+1} + d_{s+1};  A: P = e_{s+1} - d_s (T1_s), d_s = a_{s-3} = x3 (after shift)
+            const uint32_t kwn = kw_lane[s + 1 < 64 ? s + 1 : 63];
+            const uint32_t u = A ? rv : x3;
+            const uint32_t w = A ? (0u - x3) : q1;
+            P = u + kwn + w;
+        }
+    }
+    // E: e f g h = fe0..fe3 (before round 64's shift); A: a b c d = x0..x3
+    const uint32_t s0 = A ? x0 : fe0, s1 = A ? x1 : fe1, s2 = A ? x2 : fe2, s3 = A ? x3 : fe3;
+    const uint32_t o0 = __shfl_xor_sync(0xffffffffu, s0, 1), o1 = __shfl_xor_sync(0xffffffffu, s1, 1);
+    const uint32_t o2 = __shfl_xor_sync(0xffffffffu, s2, 1), o3 = __shfl_xor_sync(0xffffffffu, s3, 1);
+    const uint32_t aa = A ? s0 : o0, bb = A ? s1 : o1, cc = A ? s2 : o2, dd = A ? s3 : o3;
+    const uint32_t ee = A ? o0 : s0, ff = A ? o1 : s1, gg = A ? o2 : s2, hh = A ? o3 : s3;
+    hs[0] += aa; hs[1] += bb; hs[2] += cc; hs[3] += dd; hs[4] += ee; hs[5] += ff; hs[6] += gg; hs[7] += hh;
+}
+
 // op throughput / latency probes (one warp): 8 independent chains (rt) or
 // one dependent chain (lat) of the same op
 template <int OP, bool DEP>
@@ -275,8 +361,8 @@ __global__ void opbench(uint32_t seed, int iters, uint32_t* out, long long* cycl
 
 template <int V>
 __global__ void bench(const uint32_t* kw_g, int blocks, uint32_t* out, long long* cycles, uint32_t one) {
-    __shared__ uint32_t kw[64];
-    for (int i = threadIdx.x; i < 64; i += 32) kw[i] = kw_g[i] + kK[i];
+    __shared__ uint32_t kw[64], kwz[64];
+    for (int i = threadIdx.x; i < 64; i += 32) { kw[i] = kw_g[i] + kK[i]; kwz[i] = 0; }
     __syncwarp();
     uint32_t h[8] = {0x6a09e667, 0xbb67ae85, 0x3c6ef372, 0xa54ff53a, 0x510e527f, 0x9b05688c, 0x1f83d9ab, 0x5be0cd19};
     const long long t0 = clock64();
@@ -291,6 +377,8 @@ __global__ void bench(const uint32_t* kw_g, int blocks, uint32_t* out, long long
         if (V == 7) c_v7(h, kw);
         if (V == 8) c_v8(h, kw, one);
         if (V == 9) c_v9(h, kw, one);
+        if (V >= 10 && V <= 13) c_v10<V - 10>(h, kw, one);
+        if (V == 14) c_v14(h, (threadIdx.x & 1) ? kwz : kw, one);
     }
     const long long t1 = clock64();
     if (threadIdx.x == 0) {
@@ -310,7 +398,7 @@ int main() {
     cudaMemcpy(kw, hw, 256, cudaMemcpyHostToDevice);
     const int blocks = 2000;
     uint32_t ref[8] = {};
-    for (int v = 0; v < 10; ++v) {
+    for (int v = 0; v < 15; ++v) {
         for (int rep = 0; rep < 2; ++rep) {
             switch (v) {
                 case 0: bench<0><<<1, 32>>>(kw, blocks, out, cyc, 1u); break;
@@ -323,6 +411,11 @@ int main() {
                 case 7: bench<7><<<1, 32>>>(kw, blocks, out, cyc, 1u); break;
                 case 8: bench<8><<<1, 32>>>(kw, blocks, out, cyc, 1u); break;
                 case 9: bench<9><<<1, 32>>>(kw, blocks, out, cyc, 1u); break;
+                case 10: bench<10><<<1, 32>>>(kw, blocks, out, cyc, 1u); break;
+                case 11: bench<11><<<1, 32>>>(kw, blocks, out, cyc, 1u); break;
+                case 12: bench<12><<<1, 32>>>(kw, blocks, out, cyc, 1u); break;
+                case 13: bench<13><<<1, 32>>>(kw, blocks, out, cyc, 1u); break;
+                case 14: bench<14><<<1, 32>>>(kw, blocks, out, cyc, 1u); break;
             }
         }
         uint32_t h[8];
