@@ -8,16 +8,23 @@
 // round() is round-half-away-from-zero in both C and CUDA, and double
 // division / multiplication are IEEE correctly rounded on both sides, so the
 // bytes match. One launch covers a batch of chunk payloads. Decode is
-// HBM-bound; encode reads the payload twice (absmax, then quantise), both
-// passes near DRAM speed (the quantise at one fma.rz per lane, quant4).
-// Single-pass variants — an atomic work queue (round 1), a persistent grid
-// quantising one round behind its absmax (round 2) — cut DRAM reads to
-// 1.05-1.12x payload through L2 reuse but ran slower (0.27-0.37 ms vs 0.25
-// for 16 x 32 MiB: each CTA alternates a DRAM-latency phase and an L2 phase
-// with little memory parallelism), so the two kernels stay.
+// HBM-bound. Encode is ONE cooperative launch (q8_encode_fused_kernel):
+// warp-specialised absmax warps stream each item from DRAM once, keeping its
+// lines in L2, and quantise warps of the same CTAs re-read it from L2 one
+// item behind, so DRAM sees the payload once (ncu: 538 MB read for a 537 MB
+// payload) instead of twice. 16 x 32 MiB: 0.179 ms (0.70 of the one-pass
+// bound) vs 0.237 ms for the two-kernel encode, kept as an A/B switch
+// (TKV_Q8_ENCODE=twopass). Earlier single-pass tries — an atomic work queue
+// (round 1), a CTA quantising one segment behind its own absmax — lost
+// their L2 savings to CTAs alternating DRAM and L2 phases.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdint>
+#include <cstdlib>
+#include <cstring>
+#include <map>
+#include <mutex>
 
 #include "kernels.hpp"
 
@@ -131,6 +138,38 @@ __device__ __forceinline__ uint32_t quant4(uint32_t w0, uint32_t w1, double inv,
     return (neg & m) | (n & ~m);
 }
 
+// Signed variant, no magnitude / sign handling (the fused encode). With inv
+// STRICTLY above 1/scale (rounded up, bumped one ulp when the reciprocal is
+// exact), Q' = lane * inv sits within (0, 2^-44] of Q = lane / scale on the
+// side away from zero, so floor(Q' + 1/2) is round-half-away(Q) for either
+// sign: a tie +-(k + 1/2) lands just outside it, and non-ties are >= 2^-25
+// from every half-integer. The lane enters as the exact double
+// (2^52 + (lane + 2^15)) - (2^52 + 2^15) (the bias is the XOR of the sign
+// bit), then fma.rz(lane, inv, 2^44 + 2^43 + 1/2) keeps floor(Q' + 1/2) +
+// 2^44 + 2^43 on the 2^-8 grid of [2^44, 2^45) for |q| <= 128, so byte 1 of
+// its low word is q's int8 bit pattern (2^44 + 2^43 is a multiple of 256).
+__device__ __forceinline__ uint32_t quant4s(uint32_t w0, uint32_t w1, double inv) {
+    constexpr double kBias = 4503599627403264.0;  // 2^52 + 2^15
+    const uint32_t b0 = w0 ^ 0x80008000u, b1 = w1 ^ 0x80008000u;  // lane + 2^15 per halfword
+    const uint32_t u[4] = {b0 & 0xffffu, b0 >> 16, b1 & 0xffffu, b1 >> 16};
+    uint32_t t[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        const double x = __hiloint2double(0x43300000, int(u[k])) - kBias;  // exact
+        t[k] = uint32_t(__double2loint(__fma_rz(x, inv, 26388279066624.5)));  // 2^44 + 2^43 + 1/2
+    }
+    return __byte_perm(__byte_perm(t[0], t[1], 0x0051), __byte_perm(t[2], t[3], 0x0051), 0x5410);
+}
+
+// 1/scale rounded up, and strictly above 1/scale (quant4s' tie argument)
+__device__ __forceinline__ double inv_strict_up(float scale) {
+    if (!(scale > 0.f)) return 0.0;
+    const double sc = double(scale);
+    double inv = __drcp_ru(sc);
+    if (__fma_rn(inv, sc, -1.0) == 0.0) inv = __longlong_as_double(__double_as_longlong(inv) + 1);
+    return inv;
+}
+
 template <bool kFold>
 __device__ __forceinline__ void quant_vectors(const uint8_t* __restrict__ src, uint8_t* __restrict__ out,
                                               uint64_t b0, uint64_t vend, double inv, double c) {
@@ -186,6 +225,194 @@ q8_encode_kernel(const CodecItem* __restrict__ items, const uint32_t* __restrict
         for (uint64_t b = vend + 2 * threadIdx.x; b + 2 <= b1; b += 2 * kThreads) {
             const int32_t lane = int32_t(int16_t(uint16_t(it.src[b] | (it.src[b + 1] << 8))));
             out[b / 2] = uint8_t(quant(lane, inv));
+        }
+    }
+}
+
+// ---- single-pass encode: warp-specialised, item-pipelined persistent grid ---
+//
+// The scale is one per item (the whole chunk payload), so no byte can be
+// quantised before the item's absmax is complete, and the two-kernel encode
+// reads every payload twice from DRAM. Here one cooperative grid (one CTA
+// per SM, all resident) splits each CTA's warps into two roles:
+//   * absmax warps stream item p from DRAM with 256-bit loads that keep
+//     their lines in L2 (L2::evict_last), 8 loads in flight per lane, and
+//     count the CTA in on item p's arrival counter when done;
+//   * quantise warps wait until every CTA arrived for item q (normally
+//     already true: the absmax warps run one item ahead), then re-read item
+//     q from L2 as a last use (L2::evict_first), quantise and stream the
+//     int8 lanes out, and count the CTA in on item q's done counter.
+// The absmax warps start item p only once item p - 2 is quantised
+// everywhere, so L2 holds at most the item being quantised and the one
+// being streamed (2 x 32 MiB chunk payloads of the 8B model in 126 MB).
+// DRAM then sees the payload once plus the int8 output (the 1.5 P of the
+// single-pass bound) and both roles run concurrently: the DRAM stream does
+// not stop while lanes are quantised. Roles synchronise with named barriers
+// (never __syncthreads) and per-item global counters, so there is no
+// grid-wide barrier. Tile -> CTA assignment rotates per item.
+constexpr int kFusedThreads = 1024;
+constexpr int kBarA = 1, kBarB = 2;               // named barriers (0 = __syncthreads)
+
+struct V32 {
+    uint32_t w[8];
+};
+// 256-bit loads (sm_100) carrying an L2 eviction priority
+__device__ __forceinline__ V32 ld_keep_l2(const uint8_t* p) {
+    V32 v;
+    asm volatile("ld.global.L1::no_allocate.L2::evict_last.v8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+                 : "=r"(v.w[0]), "=r"(v.w[1]), "=r"(v.w[2]), "=r"(v.w[3]), "=r"(v.w[4]), "=r"(v.w[5]),
+                   "=r"(v.w[6]), "=r"(v.w[7])
+                 : "l"(p));
+    return v;
+}
+__device__ __forceinline__ V32 ld_last_use(const uint8_t* p) {
+    V32 v;
+    asm volatile("ld.global.L1::no_allocate.L2::evict_first.v8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+                 : "=r"(v.w[0]), "=r"(v.w[1]), "=r"(v.w[2]), "=r"(v.w[3]), "=r"(v.w[4]), "=r"(v.w[5]),
+                   "=r"(v.w[6]), "=r"(v.w[7])
+                 : "l"(p)
+                 : "memory");
+    return v;
+}
+__device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
+    unsigned v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void bar_named(int id, int threads) {
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(threads) : "memory");
+}
+__device__ __forceinline__ void await_count(const unsigned* p, unsigned want) {
+    while (ld_acquire_u32(p) < want) __nanosleep(100);
+}
+__device__ __forceinline__ int lane_at(const uint8_t* p, uint64_t b) {
+    return int32_t(int16_t(uint16_t(p[b] | (p[b + 1] << 8))));
+}
+
+template <int kBThreads, int kBUnroll>
+__device__ __forceinline__ void quant_tiles(const uint8_t* __restrict__ src, uint8_t* __restrict__ out,
+                                            uint64_t vend, uint32_t first, uint32_t ntiles, uint32_t bt,
+                                            double inv) {
+    constexpr uint64_t kStrideB = 32ull * kBThreads;
+    constexpr uint64_t kBTile = kStrideB * kBUnroll;
+    for (uint32_t t = first; t < ntiles; t += gridDim.x) {
+        const uint64_t b = uint64_t(t) * kBTile + 32 * bt;
+        V32 v[kBUnroll];
+#pragma unroll
+        for (int u = 0; u < kBUnroll; ++u)
+            if (b + u * kStrideB < vend) v[u] = ld_last_use(src + b + u * kStrideB);
+#pragma unroll
+        for (int u = 0; u < kBUnroll; ++u) {
+            if (b + u * kStrideB >= vend) break;
+            uint2* o = reinterpret_cast<uint2*>(out + (b + u * kStrideB) / 2);  // blob lanes are 8-aligned
+            __stcs(o, make_uint2(quant4s(v[u].w[0], v[u].w[1], inv), quant4s(v[u].w[2], v[u].w[3], inv)));
+            __stcs(o + 1, make_uint2(quant4s(v[u].w[4], v[u].w[5], inv), quant4s(v[u].w[6], v[u].w[7], inv)));
+        }
+    }
+}
+
+template <int kFThreads, int kAWarps, int kAUnroll, int kBUnroll, int kAhead = 1>
+__global__ void __launch_bounds__(kFThreads, 1)
+q8_encode_fused_kernel(const CodecItem* __restrict__ items, uint32_t n_items, int* __restrict__ maxabs,
+                       unsigned* __restrict__ arrive, unsigned* __restrict__ done) {
+    constexpr int kBWarps = kFThreads / 32 - kAWarps;  // quantise warps per CTA
+    constexpr int kAThreads = 32 * kAWarps, kBThreads = 32 * kBWarps;
+    constexpr uint64_t kATile = 32ull * kAThreads * kAUnroll;
+    constexpr uint64_t kBTile = 32ull * kBThreads * kBUnroll;
+    __shared__ int red[2][kAWarps];
+    const uint32_t G = gridDim.x;
+    auto first_tile = [&](uint32_t item) {  // this CTA's first tile of an item (rotated assignment)
+        const uint32_t rot = uint32_t((uint64_t(item) * 2654435761ull) % G);
+        return (blockIdx.x + G - rot) % G;
+    };
+    const uint32_t warp = threadIdx.x >> 5;
+    if (warp < kAWarps) {  // ---- absmax role
+        const uint32_t at = threadIdx.x;
+        const uint64_t gt = uint64_t(blockIdx.x) * kAThreads + at, gn = uint64_t(G) * kAThreads;
+        constexpr uint64_t kStrideA = 32ull * kAThreads;
+        for (uint32_t p = 0; p < n_items; ++p) {
+            if (p >= kAhead + 1) {  // L2 budget: item p - 1 - kAhead quantised everywhere
+                if (at == 0) await_count(done + p - 1 - kAhead, G);
+                bar_named(kBarA, kAThreads);
+            }
+            const CodecItem it = items[p];
+            const uint64_t lanes_end = it.bytes & ~uint64_t(1);
+            int m = 0;
+            uint64_t vend = 0;
+            if ((reinterpret_cast<uint64_t>(it.src) & 31) == 0) {
+                vend = lanes_end & ~uint64_t(31);
+                const uint32_t ntiles = uint32_t((vend + kATile - 1) / kATile);
+                // signed per-halfword max and min (one VIMNMX each per word);
+                // max|lane| = max(max, -min) in 32 bits (-(-32768) = 32768)
+                uint32_t hi2 = 0, lo2 = 0;
+                for (uint32_t t = first_tile(p); t < ntiles; t += G) {
+                    const uint64_t b = uint64_t(t) * kATile + 32 * at;
+                    V32 v[kAUnroll];
+#pragma unroll
+                    for (int u = 0; u < kAUnroll; ++u) {
+                        if (b + u * kStrideA < vend) v[u] = ld_keep_l2(it.src + b + u * kStrideA);
+                        else v[u] = V32{};
+                    }
+#pragma unroll
+                    for (int u = 0; u < kAUnroll; ++u)
+#pragma unroll
+                        for (int k = 0; k < 8; ++k) {
+                            hi2 = __vmaxs2(hi2, v[u].w[k]);
+                            lo2 = __vmins2(lo2, v[u].w[k]);
+                        }
+                }
+                m = max(max(int(int16_t(hi2 & 0xffffu)), int(int16_t(hi2 >> 16))),
+                        -min(int(int16_t(lo2 & 0xffffu)), int(int16_t(lo2 >> 16))));
+            }
+            for (uint64_t b = vend + 2 * gt; b + 2 <= lanes_end; b += 2 * gn)  // unaligned item / tail
+                m = max(m, abs(lane_at(it.src, b)));
+#pragma unroll
+            for (int off = 16; off; off >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, off));
+            if ((at & 31) == 0) red[p & 1][warp] = m;
+            bar_named(kBarA, kAThreads);
+            if (at == 0) {
+                int mm = 0;
+                for (int i = 0; i < kAWarps; ++i) mm = max(mm, red[p & 1][i]);
+                if (mm) atomicMax(maxabs + p, mm);
+                __threadfence();
+                atomicAdd(arrive + p, 1u);
+            }
+        }
+        return;
+    }
+    // ---- quantise role
+    const uint32_t bt = threadIdx.x - kAThreads;
+    const uint64_t gt = uint64_t(blockIdx.x) * kBThreads + bt, gn = uint64_t(G) * kBThreads;
+    for (uint32_t q = 0; q < n_items; ++q) {
+        if (bt == 0) await_count(arrive + q, G);  // item q's absmax complete everywhere
+        bar_named(kBarB, kBThreads);
+        const CodecItem it = items[q];
+        const float scale = float(double(__ldcg(maxabs + q)) / 127.0);
+        const double inv = inv_strict_up(scale);  // scale 0: every lane is 0
+        if (blockIdx.x == 0 && bt == 0) {
+            const uint32_t len = uint32_t(it.bytes);
+            uint32_t sb;
+            memcpy(&sb, &scale, 4);
+            for (int i = 0; i < 4; ++i) {
+                it.dst[i] = uint8_t(len >> (8 * i));
+                it.dst[4 + i] = uint8_t(sb >> (8 * i));
+            }
+            if (it.bytes & 1) it.dst[8 + it.bytes / 2] = it.src[it.bytes - 1];  // raw odd tail
+        }
+        const uint64_t lanes_end = it.bytes & ~uint64_t(1);
+        uint8_t* out = it.dst + 8;
+        uint64_t vend = 0;
+        if (((reinterpret_cast<uint64_t>(it.src) & 31) | (reinterpret_cast<uint64_t>(out) & 7)) == 0) {
+            vend = lanes_end & ~uint64_t(31);
+            const uint32_t ntiles = uint32_t((vend + kBTile - 1) / kBTile);
+            quant_tiles<kBThreads, kBUnroll>(it.src, out, vend, first_tile(q), ntiles, bt, inv);
+        }
+        for (uint64_t b = vend + 2 * gt; b + 2 <= lanes_end; b += 2 * gn)
+            out[b / 2] = uint8_t(quant(lane_at(it.src, b), inv));
+        bar_named(kBarB, kBThreads);
+        if (bt == 0) {
+            __threadfence();
+            atomicAdd(done + q, 1u);
         }
     }
 }
@@ -268,11 +495,71 @@ int grid(uint32_t segs) { return int(segs < 148u * 8 ? (segs ? segs : 1) : 148u 
 
 uint32_t codec_segments(uint64_t bytes) { return uint32_t((bytes + kSeg - 1) / kSeg) + (bytes == 0); }
 
+namespace {
+// Per-device state of the single-pass encode: resident grid size and the
+// per-item arrival and done counters (grown on demand, zeroed per launch
+// in-stream).
+struct FusedState {
+    int grid = 0;
+    unsigned* arrive = nullptr;
+    uint32_t cap = 0;
+};
+std::mutex g_fused_mu;
+std::map<int, FusedState> g_fused;
+
+bool fused_enabled() {
+    static const bool on = [] {
+        const char* v = std::getenv("TKV_Q8_ENCODE");
+        return !(v && std::strcmp(v, "twopass") == 0);
+    }();
+    return on;
+}
+}  // namespace
+
 cudaError_t launch_q8_encode(const CodecItem* items, const uint32_t* seg_base, uint32_t n_items,
                              uint32_t total_segs, int* maxabs, cudaStream_t s) {
     if (n_items == 0) return cudaSuccess;
     cudaError_t e = cudaMemsetAsync(maxabs, 0, n_items * sizeof(int), s);
     if (e != cudaSuccess) return e;
+    if (fused_enabled()) {
+        int dev = 0;
+        if ((e = cudaGetDevice(&dev)) != cudaSuccess) return e;
+        unsigned* arrive = nullptr;
+        int grid = 0;
+        {
+            std::lock_guard<std::mutex> lk(g_fused_mu);
+            FusedState& st = g_fused[dev];
+            if (st.grid == 0) {
+                int per_sm = 0, sms = 0;
+                if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, q8_encode_fused_kernel<kFusedThreads, 12, 6, 2, 2>, kFusedThreads,
+                                                                        0)) != cudaSuccess)
+                    return e;
+                if ((e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev)) != cudaSuccess) return e;
+                if (per_sm < 1) return cudaErrorCooperativeLaunchTooLarge;
+                st.grid = sms;  // one CTA per SM (launch bounds: 512 threads, 1 per SM)
+            }
+            if (st.cap < 2 * n_items) {
+                // (the old counters may still be read by an in-flight launch on
+                // another stream: leak them rather than free under it)
+                uint32_t cap = std::max<uint32_t>(64, st.cap);
+                while (cap < 2 * n_items) cap *= 2;
+                if ((e = cudaMalloc(&st.arrive, cap * sizeof(unsigned))) != cudaSuccess) return e;
+                st.cap = cap;
+            }
+            arrive = st.arrive;
+            grid = st.grid;
+        }
+        if ((e = cudaMemsetAsync(arrive, 0, 2 * n_items * sizeof(unsigned), s)) != cudaSuccess) return e;
+        unsigned* done = arrive + n_items;
+        void* args[] = {const_cast<CodecItem**>(&items), &n_items, &maxabs, &arrive, &done};
+        note_launch();
+        // 12 absmax warps x 6 x 32-byte loads in flight, 20 quantise warps x 2,
+        // absmax up to two items ahead of the quantise (measured against
+        // 4-24 absmax warps, 1-3 items ahead: tools/run_codec.sh history in
+        // profiles/r02_codec.jsonl)
+        const void* fn = reinterpret_cast<const void*>(q8_encode_fused_kernel<kFusedThreads, 12, 6, 2, 2>);
+        return cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(kFusedThreads), args, 0, s);
+    }
     note_launch();
     q8_absmax_kernel<<<grid(total_segs), kThreads, 0, s>>>(items, seg_base, n_items, total_segs, maxabs);
     note_launch();

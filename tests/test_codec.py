@@ -126,3 +126,66 @@ def test_device_q8_decode_any_scale_bits(tkv, C):
     outs = q8_decode([torch.from_numpy(b.copy()).cuda() for b in blobs], [n] * len(blobs))
     for s, b, o in zip(scales, blobs, outs):
         assert np.array_equal(o.cpu().numpy(), C.q8_decode(b)), s
+
+
+@pytest.mark.gpu
+def test_device_q8_encode_batch_pipeline(tkv, C):
+    """A batch that exercises the single-pass encode's item pipeline: several
+    multi-MiB items (absmax of item p overlapped with the quantise of item
+    p - 1), ragged and odd lengths, an empty item, and payloads / blobs at
+    offsets that break the 32-byte vector path (scalar fallback inside the
+    same launch). Every blob byte equals the oracle's."""
+    from paper_2510_09665_b200.api import q8_encode
+    rng = np.random.default_rng(77)
+    sizes = [32 << 20, (3 << 20) + 6, (1 << 20) + 1, 0, 2, (5 << 20) + 32, 4096 + 3, 8 << 20]
+    offsets = [0, 0, 0, 0, 0, 2, 6, 0]  # bytes into a larger allocation: unaligned src
+    srcs, host = [], []
+    for n, off in zip(sizes, offsets):
+        lanes = np.clip(rng.normal(0, 2500 + n % 7000, size=(n + off + 1) // 2 + 1), -32768, 32767).astype(np.int16)
+        buf = lanes.view(np.uint8)[: n + off].copy()
+        if n >= 2:
+            pos = off + ((n // 3) & ~1)
+            buf[pos:pos + 2] = [0x00, 0x80]  # one -32768 lane
+        host.append(buf[off:])
+        srcs.append(torch.from_numpy(buf).cuda()[off:])
+    blobs = q8_encode(srcs)
+    for n, p, b in zip(sizes, host, blobs):
+        assert np.array_equal(b.cpu().numpy(), C.q8_encode(p)), n
+
+
+@pytest.mark.gpu
+def test_q8_twopass_variant_subprocess():
+    """The two-kernel encode (absmax, then quantise) stays selectable with
+    TKV_Q8_ENCODE=twopass (read once per process): the encode parity tests in
+    a child process."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, TKV_Q8_ENCODE="twopass")
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-m", "gpu",
+                        "tests/test_codec.py::test_device_q8_matches_oracle",
+                        "tests/test_codec.py::test_device_q8_encode_batch_pipeline",
+                        "tests/test_codec.py::test_device_q8_encode_every_lane"],
+                       cwd=root, env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("maxabs", [1, 2, 127, 254, 508, 1000, 12345, 32768])
+def test_device_q8_encode_every_lane_vector_path(tkv, C, maxabs):
+    """Every lane value in [-maxabs, maxabs], tiled to >= 1 MiB so the
+    encode's 32-byte vector path (not only its scalar tail) meets them:
+    power-of-two scales (maxabs 127 / 254 / 508: an exact reciprocal, the
+    tie case that needs the reciprocal bumped above 1/scale) and the exact
+    .5 ties of tiny scales."""
+    from paper_2510_09665_b200.api import q8_encode
+    lanes = np.arange(-maxabs, min(maxabs, 32767) + 1, dtype=np.int64)
+    lanes = np.concatenate([lanes, [-maxabs if maxabs == 32768 else maxabs]])
+    reps = max(1, (1 << 19) // lanes.size + 1)
+    rng = np.random.default_rng(maxabs + 1)
+    tiled = np.tile(lanes, reps)
+    rng.shuffle(tiled)
+    p = tiled.astype(np.int16).view(np.uint8)
+    blob = q8_encode([torch.from_numpy(p.copy()).cuda()])[0].cpu().numpy()
+    assert np.array_equal(blob, C.q8_encode(p))

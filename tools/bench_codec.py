@@ -59,12 +59,18 @@ def main(n_items=16, nbytes=32 << 20, reps=5):
         return min(ts)
     te, td = timed(enc), timed(dec)
     payload = n_items * nbytes
-    res = {"codec": "q8-scale", "items": n_items, "payload_bytes_per_item": nbytes,
+    peak = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))).get("hbm_gbs", 6650.0) \
+        if os.path.exists(os.path.join(ROOT, "MEASURED_PEAKS.json")) else 6650.0
+    res = {"codec": "q8-scale", "encode_variant": os.environ.get("TKV_Q8_ENCODE", "fused"),
+           "items": n_items, "payload_bytes_per_item": nbytes,
            "encode_ms": round(te, 4), "decode_ms": round(td, 4),
-           # DRAM traffic of this two-pass encode (payload read twice, half
-           # written) and the algorithmic minimum (read once, half written)
-           "encode_hbm_gbps": round(2.5 * payload / te / 1e6, 1),
+           # the two-pass encode's DRAM traffic (payload read twice, half
+           # written) and the algorithmic minimum (read once, half written),
+           # which the single-pass (fused) encode moves when L2 keeps the item
+           "encode_twopass_traffic_gbps": round(2.5 * payload / te / 1e6, 1),
            "encode_algorithmic_gbps": round(1.5 * payload / te / 1e6, 1),
+           "encode_frac_one_pass_bound": round(1.5 * payload / te / 1e6 / peak, 4),
+           "decode_frac": round(1.5 * payload / td / 1e6 / peak, 4), "peak": peak,
            "decode_hbm_gbps": round(1.5 * payload / td / 1e6, 1),
            "encode_payload_gbps": round(payload / te / 1e6, 1), "decode_payload_gbps": round(payload / td / 1e6, 1)}
     import oracle
