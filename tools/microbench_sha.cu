@@ -331,6 +331,56 @@ __device__ __forceinline__ void c_v14(uint32_t hs[8], const uint32_t* kw_lane, u
     hs[0] += aa; hs[1] += bb; hs[2] += cc; hs[3] += dd; hs[4] += ee; hs[5] += ff; hs[6] += gg; hs[7] += hh;
 }
 
+// V15: V14 with lane A two rounds behind lane E: both transfers of the
+// per-round SHFL.BFLY (e_{s+1} to A, a_{s-1} to E) get one round of slack,
+// the lane-dependent sign of the d / T1 term is an IMAD with a per-lane +-1
+// (no select), Ch / Maj picked with one LOP3 against a lane mask.
+__device__ __forceinline__ void c_v15(uint32_t hs[8], const uint32_t* kw_lane, uint32_t one) {
+    const bool A = threadIdx.x & 1;
+    const uint32_t r0 = A ? 2 : 6, r1 = A ? 13 : 11, r2 = A ? 22 : 25;
+    const uint32_t msk = A ? ~0u : 0u;
+    const uint32_t sgn = A ? (0u - one) : one;  // x3 enters P with + (E) or - (A)
+    // E: x = (e, f, g, h) = (e_0, e_-1, e_-2, e_-3).
+    // A before round 0: x = (a_-2, a_-3, a_-4, a_-5); rounds 0 and 1 inject a_-1 (= b) and a_0 (= a).
+    // a_-k for k = 1..3 are b, c, d; a_-4, a_-5 never enter a result (A's rounds 0, 1 are replaced).
+    uint32_t x0 = A ? hs[2] : hs[4], x1 = A ? hs[3] : hs[5], x2 = A ? 0u : hs[6], x3 = A ? 0u : hs[7];
+    // rv_prev: the value received one round earlier. E's P for round 0 / 1 needs
+    // d_0 = a_-3 = d and d_1 = a_-2 = c, which no round delivers: seeded.
+    uint32_t P = x3 + kw_lane[0] + hs[3];  // E: h_0 + KW_0 + d_0 (A: unused, round 0 replaced)
+    uint32_t rv_prev = 0, rv = 0;
+    uint32_t fe0 = 0, fe1 = 0, fe2 = 0, fe3 = 0;
+#pragma unroll
+    for (int s = 0; s <= 65; ++s) {
+        const uint32_t S = __funnelshift_r(x0, x0, r0) ^ __funnelshift_r(x0, x0, r1) ^ __funnelshift_r(x0, x0, r2);
+        const uint32_t chv = (x0 & x1) ^ (~x0 & x2);
+        const uint32_t mjv = (x0 & x1) ^ (x0 & x2) ^ (x1 & x2);
+        const uint32_t cm = (chv & ~msk) | (mjv & msk);
+        uint32_t nw = S + cm + P;
+        if (s == 0) nw = A ? hs[1] : nw;  // a_-1
+        if (s == 1) nw = A ? hs[0] : nw;  // a_0
+        if (s == 64) { fe0 = x0; fe1 = x1; fe2 = x2; fe3 = x3; }
+        rv_prev = rv;
+        rv = __shfl_xor_sync(0xffffffffu, nw, 1);  // E gets a_{s-1}, A gets e_{s+1}
+        x3 = x2; x2 = x1; x1 = x0; x0 = nw;
+        // P for round s + 1:
+        //   E: h_{s+1} + KW_{s+1} + d_{s+1},  h = x3 (= e_{s-2}), d_{s+1} = a_{s-2} = rv_prev
+        //   A: e_s - d_{s-1} (= T1_{s-1}, for a_s),  e_s = rv_prev, d_{s-1} = a_{s-4} = x3
+        // with A's round s computing a_{s-1}: its history after the shift is
+        // (a_{s-1}, a_{s-2}, a_{s-3}, a_{s-4}), so T1 for round s + 1 (a_s) is
+        // e_s - a_{s-4}.
+        uint32_t dE = rv_prev;
+        if (s == 0 && !A) dE = hs[2];  // E: d_1 = a_-2 = c (no round delivered it)
+        const uint32_t kwn = kw_lane[s + 1 < 64 ? s + 1 : 63];
+        P = add_rt(x3, sgn, add_rt(dE, one, kwn));
+    }
+    // E: e f g h = fe0..fe3 (state before round 64's shift); A: a b c d after round 65
+    const uint32_t s0 = A ? x0 : fe0, s1 = A ? x1 : fe1, s2 = A ? x2 : fe2, s3 = A ? x3 : fe3;
+    const uint32_t o0 = __shfl_xor_sync(0xffffffffu, s0, 1), o1 = __shfl_xor_sync(0xffffffffu, s1, 1);
+    const uint32_t o2 = __shfl_xor_sync(0xffffffffu, s2, 1), o3 = __shfl_xor_sync(0xffffffffu, s3, 1);
+    hs[0] += A ? s0 : o0; hs[1] += A ? s1 : o1; hs[2] += A ? s2 : o2; hs[3] += A ? s3 : o3;
+    hs[4] += A ? o0 : s0; hs[5] += A ? o1 : s1; hs[6] += A ? o2 : s2; hs[7] += A ? o3 : s3;
+}
+
 // op throughput / latency probes (one warp): 8 independent chains (rt) or
 // one dependent chain (lat) of the same op
 template <int OP, bool DEP>
@@ -379,6 +429,7 @@ __global__ void bench(const uint32_t* kw_g, int blocks, uint32_t* out, long long
         if (V == 9) c_v9(h, kw, one);
         if (V >= 10 && V <= 13) c_v10<V - 10>(h, kw, one);
         if (V == 14) c_v14(h, (threadIdx.x & 1) ? kwz : kw, one);
+        if (V == 15) c_v15(h, (threadIdx.x & 1) ? kwz : kw, one);
     }
     const long long t1 = clock64();
     if (threadIdx.x == 0) {
@@ -398,7 +449,7 @@ int main() {
     cudaMemcpy(kw, hw, 256, cudaMemcpyHostToDevice);
     const int blocks = 2000;
     uint32_t ref[8] = {};
-    for (int v = 0; v < 15; ++v) {
+    for (int v = 0; v < 16; ++v) {
         for (int rep = 0; rep < 2; ++rep) {
             switch (v) {
                 case 0: bench<0><<<1, 32>>>(kw, blocks, out, cyc, 1u); break;
@@ -416,6 +467,7 @@ int main() {
                 case 12: bench<12><<<1, 32>>>(kw, blocks, out, cyc, 1u); break;
                 case 13: bench<13><<<1, 32>>>(kw, blocks, out, cyc, 1u); break;
                 case 14: bench<14><<<1, 32>>>(kw, blocks, out, cyc, 1u); break;
+                case 15: bench<15><<<1, 32>>>(kw, blocks, out, cyc, 1u); break;
             }
         }
         uint32_t h[8];
