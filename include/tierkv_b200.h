@@ -124,6 +124,34 @@ int tkv_scatter_layers(const tkv_paged_layout* layout, const tkv_xfer_desc* desc
                        uint32_t layer_begin, uint32_t n_layers, uint32_t pages_per_tile,
                        uint64_t addr_or, int ctas, void* stream);
 
+/* Affine launch form of a descriptor list: one query's consecutive chunks
+ * (one page table, consecutive page-table columns, equally spaced chunk
+ * bases, one layer stride, every descriptor full but the last). The unit
+ * kernel then derives every address from the launch parameters, so the
+ * page-table entry is the only load in front of the data — the layerwise
+ * connector's one-layer launches take this form (same replaced reference
+ * functions as tkv_gather_layers / tkv_scatter_layers). tkv_affine_form
+ * returns 0 and fills *out when the HOST copy of the descriptors has the
+ * form, TKV_NOT_FOUND otherwise. The affine launches need 16-byte-aligned
+ * rows and bases and one plane (token_stride == bpt); any size. */
+typedef struct tkv_affine_plan {
+    uint32_t n_desc;
+    uint32_t pages_per_desc;
+    uint32_t last_tokens;
+    uint32_t first_page;
+    const int32_t* table_dev;
+    uint32_t table_stride;
+    uint32_t pad;
+    uint64_t chunk0;
+    uint64_t chunk_stride;
+    uint64_t layer_stride;
+} tkv_affine_plan;
+int tkv_affine_form(const tkv_xfer_desc* descs, uint32_t n, uint32_t page_tokens, tkv_affine_plan* out);
+int tkv_gather_layers_affine(const tkv_paged_layout* layout, const tkv_affine_plan* plan, uint32_t layer_begin,
+                             uint32_t n_layers, int ctas, void* stream);
+int tkv_scatter_layers_affine(const tkv_paged_layout* layout, const tkv_affine_plan* plan, uint32_t layer_begin,
+                              uint32_t n_layers, int ctas, void* stream);
+
 /* K3: one chained SHA-256 key sequence per chain (KeyChain::next,
  * src/tokens.cpp:22-42). out_dev gets 32 bytes per chunk at rows
  * out_first.. of each chain. tag_len <= 256. */

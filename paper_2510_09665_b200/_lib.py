@@ -38,6 +38,13 @@ class XferDescC(ct.Structure):
                 ("pad", ct.c_uint32)]
 
 
+class AffinePlanC(ct.Structure):
+    _fields_ = [("n_desc", ct.c_uint32), ("pages_per_desc", ct.c_uint32), ("last_tokens", ct.c_uint32),
+                ("first_page", ct.c_uint32), ("table_dev", ct.c_void_p), ("table_stride", ct.c_uint32),
+                ("pad", ct.c_uint32), ("chunk0", ct.c_uint64), ("chunk_stride", ct.c_uint64),
+                ("layer_stride", ct.c_uint64)]
+
+
 class ChainDescC(ct.Structure):
     _fields_ = [("token_off", ct.c_uint64), ("n_tokens", ct.c_uint32), ("out_first", ct.c_uint32),
                 ("parent", ct.c_uint8 * 32)]
@@ -72,6 +79,11 @@ SIGNATURES = {
                                      ct.c_uint32, ct.c_uint32, ct.c_uint64, ct.c_int, vp]),
     "tkv_scatter_layers": (ct.c_int, [ct.POINTER(PagedLayoutC), vp, vp, ct.c_uint32, ct.c_uint32, ct.c_uint32,
                                       ct.c_uint32, ct.c_uint32, ct.c_uint64, ct.c_int, vp]),
+    "tkv_affine_form": (ct.c_int, [vp, ct.c_uint32, ct.c_uint32, ct.POINTER(AffinePlanC)]),
+    "tkv_gather_layers_affine": (ct.c_int, [ct.POINTER(PagedLayoutC), ct.POINTER(AffinePlanC), ct.c_uint32,
+                                            ct.c_uint32, ct.c_int, vp]),
+    "tkv_scatter_layers_affine": (ct.c_int, [ct.POINTER(PagedLayoutC), ct.POINTER(AffinePlanC), ct.c_uint32,
+                                             ct.c_uint32, ct.c_int, vp]),
     "tkv_hash_chains": (ct.c_int, [vp, vp, ct.c_uint32, ct.c_uint32, ct.c_char_p, ct.c_uint32, vp, vp]),
     "tkv_synth_pages": (ct.c_int, [ct.POINTER(PagedLayoutC), vp, vp, ct.c_uint32, ct.c_uint64, ct.c_uint32,
                                    ct.c_uint32, ct.c_uint32, ct.c_uint32, vp]),

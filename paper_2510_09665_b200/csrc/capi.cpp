@@ -182,6 +182,53 @@ static int paged(const tkv_paged_layout* layout, const tkv_xfer_desc* descs, con
     return cuda(launch_paged_copy(to_layout(layout), P, dir, ctas, cudaStream_t(stream)));
 }
 
+int tkv_affine_form(const tkv_xfer_desc* descs, uint32_t n, uint32_t page_tokens, tkv_affine_plan* out) {
+    if (!descs || !out) return fail(Errc::invalid_argument, "null pointer");
+    std::vector<XferDesc> d(reinterpret_cast<const XferDesc*>(descs), reinterpret_cast<const XferDesc*>(descs) + n);
+    PagedCopyPlan P;
+    if (!affine_form(d, page_tokens, P)) return int(Errc::not_found);
+    out->n_desc = n;
+    out->pages_per_desc = P.aff_pages;
+    out->last_tokens = P.aff_last_tokens;
+    out->first_page = P.aff_first_page;
+    out->table_dev = P.aff_table;
+    out->table_stride = P.aff_table_stride;
+    out->pad = 0;
+    out->chunk0 = P.aff_chunk0;
+    out->chunk_stride = P.aff_chunk_stride;
+    out->layer_stride = P.aff_layer_stride;
+    return 0;
+}
+
+static int paged_affine(const tkv_paged_layout* layout, const tkv_affine_plan* a, uint32_t l0, uint32_t nl,
+                        int ctas, void* stream, CopyDir dir) {
+    if (!layout || !a) return fail(Errc::invalid_argument, "null pointer");
+    if (a->n_desc == 0 || a->pages_per_desc == 0) return fail(Errc::invalid_argument, "empty affine plan");
+    PagedCopyPlan P;
+    P.n_desc = a->n_desc;
+    P.layer_begin = l0;
+    P.n_layers = nl;
+    P.aff_pages = a->pages_per_desc;
+    P.aff_last_tokens = a->last_tokens;
+    P.aff_first_page = a->first_page;
+    P.aff_table_stride = a->table_stride;
+    P.aff_table = a->table_dev;
+    P.aff_chunk0 = a->chunk0;
+    P.aff_chunk_stride = a->chunk_stride;
+    P.aff_layer_stride = a->layer_stride;
+    return cuda(launch_paged_copy_affine(to_layout(layout), P, dir, ctas, cudaStream_t(stream)));
+}
+
+int tkv_gather_layers_affine(const tkv_paged_layout* layout, const tkv_affine_plan* plan, uint32_t l0,
+                             uint32_t nl, int ctas, void* stream) {
+    return paged_affine(layout, plan, l0, nl, ctas, stream, CopyDir::gather);
+}
+
+int tkv_scatter_layers_affine(const tkv_paged_layout* layout, const tkv_affine_plan* plan, uint32_t l0,
+                              uint32_t nl, int ctas, void* stream) {
+    return paged_affine(layout, plan, l0, nl, ctas, stream, CopyDir::scatter);
+}
+
 int tkv_gather_layers(const tkv_paged_layout* layout, const tkv_xfer_desc* descs, const uint32_t* tb,
                       uint32_t n_desc, uint32_t tiles, uint32_t l0, uint32_t nl, uint32_t ppt,
                       uint64_t addr_or, int ctas, void* stream) {

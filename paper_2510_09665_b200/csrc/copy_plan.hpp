@@ -34,6 +34,35 @@ inline uint32_t pages_per_tile_one_layer(size_t page_bytes) {
     return page_bytes % 256 == 0 ? 1u : pages_per_tile(page_bytes);
 }
 
+// The affine form of a descriptor list (PagedCopyPlan::aff_*), if it has one:
+// one page table, consecutive page-table columns, equally spaced chunk bases,
+// one layer stride, full descriptors but the last. Fills `out`, or returns
+// false.
+inline bool affine_form(const std::vector<XferDesc>& d, uint32_t page_tokens, PagedCopyPlan& out) {
+    if (d.empty() || page_tokens == 0) return false;
+    const XferDesc& a = d[0];
+    const uint32_t pages = (a.n_tokens + page_tokens - 1) / page_tokens;
+    if (pages == 0) return false;
+    const uint64_t cs = d.size() > 1 ? d[1].chunk - a.chunk : 0;
+    for (size_t i = 0; i < d.size(); ++i) {
+        const XferDesc& x = d[i];
+        const bool last = i + 1 == d.size();
+        if (x.table != a.table || x.table_stride != a.table_stride || x.layer_stride != a.layer_stride) return false;
+        if (x.first_page != a.first_page + uint32_t(i) * pages || x.chunk != a.chunk + i * cs) return false;
+        if (last ? (x.n_tokens == 0 || x.n_tokens > pages * page_tokens) : x.n_tokens != pages * page_tokens)
+            return false;
+    }
+    out.aff_pages = pages;
+    out.aff_last_tokens = d.back().n_tokens;
+    out.aff_first_page = a.first_page;
+    out.aff_table_stride = a.table_stride;
+    out.aff_table = a.table;
+    out.aff_chunk0 = a.chunk;
+    out.aff_chunk_stride = cs;
+    out.aff_layer_stride = a.layer_stride;
+    return true;
+}
+
 struct DevicePlan {
     size_t n_desc = 0;
     size_t variants = 0;
@@ -43,6 +72,7 @@ struct DevicePlan {
     size_t off_tb1 = 0, off_tball = 0;
     DualPool* pool = nullptr;
     std::unique_ptr<DualBuffer> buf;
+    std::vector<PagedCopyPlan> affine;  // per variant: aff_* fields (aff_pages 0: none)
 
     DevicePlan() = default;
     DevicePlan(const DevicePlan&) = delete;
@@ -76,6 +106,8 @@ struct DevicePlan {
             std::memcpy(h + v * n_desc * sizeof(XferDesc), vars[v].data(), n_desc * sizeof(XferDesc));
             for (const auto& d : vars[v]) addr_or |= d.chunk | d.layer_stride;
         }
+        affine.assign(variants, PagedCopyPlan{});
+        for (size_t v = 0; v < variants; ++v) affine_form(vars[v], page_tokens, affine[v]);
         std::memcpy(h + off_tb1, tb1.data(), tb1.size() * 4);
         std::memcpy(h + off_tball, tball.data(), tball.size() * 4);
         // SM copy from the mapped pinned side: a copy-engine upload would queue
@@ -97,6 +129,17 @@ struct DevicePlan {
         p.n_layers = n_layers;
         p.pages_per_tile = one ? ppt_1 : ppt_all;
         p.addr_or = addr_or;
+        if (one && ppt_1 == 1 && variant < affine.size() && affine[variant].aff_pages) {
+            const PagedCopyPlan& f = affine[variant];
+            p.aff_pages = f.aff_pages;
+            p.aff_last_tokens = f.aff_last_tokens;
+            p.aff_first_page = f.aff_first_page;
+            p.aff_table_stride = f.aff_table_stride;
+            p.aff_table = f.aff_table;
+            p.aff_chunk0 = f.aff_chunk0;
+            p.aff_chunk_stride = f.aff_chunk_stride;
+            p.aff_layer_stride = f.aff_layer_stride;
+        }
         return p;
     }
 };

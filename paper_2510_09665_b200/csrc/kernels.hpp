@@ -64,6 +64,19 @@ struct PagedCopyPlan {
     uint32_t n_layers = 1;             // layers moved by this launch
     uint32_t pages_per_tile = 1;
     uint64_t addr_or = 0;              // OR of every desc chunk base and layer stride (alignment)
+    // Affine one-layer plan (0 pages = not affine): descriptor i moves
+    // aff_pages pages from page-table column aff_first_page + i * aff_pages of
+    // aff_table into aff_chunk0 + i * aff_chunk_stride, every descriptor full
+    // but the last (aff_last_tokens rows). The unit kernel then computes every
+    // address from these fields: the page id is its only dependent load.
+    uint32_t aff_pages = 0;
+    uint32_t aff_last_tokens = 0;
+    uint32_t aff_first_page = 0;
+    uint32_t aff_table_stride = 0;
+    const int32_t* aff_table = nullptr;
+    uint64_t aff_chunk0 = 0;
+    uint64_t aff_chunk_stride = 0;
+    uint64_t aff_layer_stride = 0;
 };
 
 // Tiles of one descriptor for a launch over n_layers (host + device agree).
@@ -76,6 +89,10 @@ inline uint32_t tiles_for(uint32_t n_tokens, uint32_t page_tokens, uint32_t page
 // Launches the copy; `ctas` = grid size (0 = 2 x SM count). Returns launch error.
 cudaError_t launch_paged_copy(const PagedLayout& layout, const PagedCopyPlan& plan, CopyDir dir,
                               int ctas, cudaStream_t stream);
+// The unit kernel over an affine plan alone (aff_* set; descs / tile_base
+// unused), any launch size.
+cudaError_t launch_paged_copy_affine(const PagedLayout& layout, const PagedCopyPlan& plan, CopyDir dir,
+                                     int ctas, cudaStream_t stream);
 
 // ---------------------------------------------------------------------------
 // K3: chained SHA-256 chunk keys (KeyChain::next, src/tokens.cpp:22-42).

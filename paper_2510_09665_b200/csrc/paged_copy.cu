@@ -194,9 +194,65 @@ constexpr int kUnitVecs = kUnitBytes / 16 / 32;  // vectors per lane per unit
 constexpr uint32_t kSmemDescs = 4096;
 constexpr uint64_t kUnitMaxBytes = 512ull << 20;
 
+// Affine plans (PagedCopyPlan::aff_*: one query's consecutive chunks, the
+// connector's usual one-layer launch): every address comes from the launch
+// parameters, so the page-table entry is the only load in front of the data
+// (the general path below adds the descriptor prefix, a block barrier, the
+// search and the descriptor itself: ~2 us per launch at 8 MiB,
+// tools/microbench_k12_small.cu).
+__device__ __forceinline__ void units_affine(const PagedLayout& L, const PagedCopyPlan& P, int dir,
+                                             uint32_t parts, uint32_t part_bytes) {
+    const uint32_t U = P.aff_pages;
+    const uint32_t pages1 = (P.n_desc - 1) * U + (P.aff_last_tokens + L.page_tokens - 1) / L.page_tokens;
+    const uint32_t total = pages1 * P.n_layers * parts;
+    const uint32_t lane = threadIdx.x & 31;
+    const uint32_t warps = gridDim.x * (kThreads / 32);
+    const uint32_t w = blockIdx.x * (kThreads / 32) + (threadIdx.x >> 5);
+    const uint32_t u0 = uint32_t(uint64_t(total) * w / warps);
+    const uint32_t u1 = uint32_t(uint64_t(total) * (w + 1) / warps);
+    const uint64_t page_run = uint64_t(L.page_tokens) * L.bpt;
+    for (uint32_t u = u0; u < u1; ++u) {
+        const uint32_t g = u / parts, q = u - g * parts;
+        const uint32_t ll = g / pages1, g1 = g - ll * pages1;
+        const uint32_t d = g1 / U, j = g1 - d * U;
+        const uint32_t layer = P.layer_begin + ll;
+        const uint32_t n_tokens = d + 1 == P.n_desc ? P.aff_last_tokens : U * L.page_tokens;
+        const uint32_t page_valid = min(L.page_tokens, n_tokens - j * L.page_tokens) * L.bpt;
+        const uint32_t begin = q * part_bytes;
+        const uint32_t end = min(begin + part_bytes, page_valid);
+        if (begin >= end) continue;
+        const uint32_t page = uint32_t(__ldg(P.aff_table + uint64_t(L.shared_table ? 0 : layer) * P.aff_table_stride +
+                                             P.aff_first_page + g1));
+        const uint64_t pbase =
+            L.layer_base ? __ldg(reinterpret_cast<const unsigned long long*>(L.layer_base) + layer) : L.base;
+        const uint8_t* page_p = reinterpret_cast<const uint8_t*>(pbase + uint64_t(page) * L.page_stride);
+        const uint64_t chunk = P.aff_chunk0 + uint64_t(d) * P.aff_chunk_stride + uint64_t(layer) * P.aff_layer_stride +
+                               uint64_t(j) * page_run;
+        const uint8_t* src = dir == int(CopyDir::gather) ? page_p + begin : reinterpret_cast<const uint8_t*>(chunk + begin);
+        uint8_t* dst = dir == int(CopyDir::gather) ? reinterpret_cast<uint8_t*>(chunk + begin)
+                                                   : const_cast<uint8_t*>(page_p + begin);
+        const uint32_t nv = (end - begin) >> 4;
+        int4 v[kUnitVecs];
+#pragma unroll
+        for (int k = 0; k < kUnitVecs; ++k) {
+            const uint32_t i = lane + 32u * k;
+            if (i < nv) v[k] = __ldcs(reinterpret_cast<const int4*>(src) + i);
+        }
+#pragma unroll
+        for (int k = 0; k < kUnitVecs; ++k) {
+            const uint32_t i = lane + 32u * k;
+            if (i < nv) __stcs(reinterpret_cast<int4*>(dst) + i, v[k]);
+        }
+    }
+}
+
 __global__ void __launch_bounds__(kThreads, 2)
 paged_copy_units_kernel(const PagedLayout L, const PagedCopyPlan P, const int dir, const uint32_t parts,
                         const uint32_t part_bytes) {
+    if (P.aff_pages) {  // (uniform over the launch)
+        units_affine(L, P, dir, parts, part_bytes);
+        return;
+    }
     __shared__ uint32_t s_pb[kSmemDescs + 1];
     const uint32_t nl = P.n_layers;
     const bool smem = P.n_desc <= kSmemDescs;
@@ -450,8 +506,49 @@ int sm_count() {
 
 }  // namespace
 
-cudaError_t launch_paged_copy(const PagedLayout& L, const PagedCopyPlan& P, CopyDir dir, int ctas,
+namespace {
+// TKV_PAGED_AFFINE=0: plans built in affine form take the general unit-kernel
+// path anyway (A/B measurements only).
+bool affine_enabled() {
+    static const bool on = [] {
+        const char* v = std::getenv("TKV_PAGED_AFFINE");
+        return !(v && std::strcmp(v, "0") == 0);
+    }();
+    return on;
+}
+
+// 4 KiB pieces of a page run (the unit kernel's units)
+void unit_parts(uint64_t page_bytes, uint32_t& parts, uint32_t& part_bytes) {
+    parts = uint32_t((page_bytes + kUnitBytes - 1) / kUnitBytes);
+    part_bytes = uint32_t(((page_bytes + parts - 1) / parts + 15) & ~uint64_t(15));
+}
+}  // namespace
+
+cudaError_t launch_paged_copy_affine(const PagedLayout& L, const PagedCopyPlan& P, CopyDir dir, int ctas,
+                                     cudaStream_t stream) {
+    if (P.aff_pages == 0 || P.n_desc == 0 || P.n_layers == 0) return cudaSuccess;
+    const uint64_t a = L.bpt | L.page_stride | L.base | P.aff_chunk0 | P.aff_chunk_stride | P.aff_layer_stride;
+    if ((a & 15) || L.n_planes != 1 || L.token_stride != L.bpt || L.page_tokens == 0) return cudaErrorInvalidValue;
+    if (P.aff_last_tokens == 0 || P.aff_last_tokens > P.aff_pages * L.page_tokens) return cudaErrorInvalidValue;
+    const uint64_t page_bytes = uint64_t(L.page_tokens) * L.bpt;
+    uint32_t parts, part_bytes;
+    unit_parts(page_bytes, parts, part_bytes);
+    const uint64_t pages1 =
+        uint64_t(P.n_desc - 1) * P.aff_pages + (P.aff_last_tokens + L.page_tokens - 1) / L.page_tokens;
+    const uint64_t units = pages1 * P.n_layers * parts;
+    if (units >= (1ull << 32)) return cudaErrorInvalidValue;
+    if (ctas <= 0) ctas = 2 * sm_count();
+    const uint64_t want = (units + kThreads / 32 - 1) / (kThreads / 32);
+    if (uint64_t(ctas) > want) ctas = int(want);
+    note_launch();
+    paged_copy_units_kernel<<<ctas, kThreads, 0, stream>>>(L, P, int(dir), parts, part_bytes);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_paged_copy(const PagedLayout& L, const PagedCopyPlan& Pin, CopyDir dir, int ctas,
                               cudaStream_t stream) {
+    PagedCopyPlan P = Pin;
+    if (!affine_enabled()) P.aff_pages = 0;
     if (P.total_tiles == 0 || P.n_desc == 0) return cudaSuccess;
     if (P.pages_per_tile == 0 || P.pages_per_tile > kMaxPagesPerTile) return cudaErrorInvalidValue;
     if (ctas <= 0) ctas = 2 * sm_count();
@@ -475,8 +572,8 @@ cudaError_t launch_paged_copy(const PagedLayout& L, const PagedCopyPlan& P, Copy
     // at 5 GiB, profiles/r02_k12_layers.jsonl).
     const uint64_t launch_bytes = uint64_t(P.total_tiles) * page_bytes;
     if ((a & 15) == 0 && contig && P.pages_per_tile == 1 && launch_bytes <= kUnitMaxBytes && !force_tile) {
-        const uint32_t parts = uint32_t((page_bytes + kUnitBytes - 1) / kUnitBytes);
-        const uint32_t part_bytes = uint32_t(((page_bytes + parts - 1) / parts + 15) & ~uint64_t(15));
+        uint32_t parts, part_bytes;
+        unit_parts(page_bytes, parts, part_bytes);
         if (uint64_t(P.total_tiles) * parts < (1ull << 32)) {
             const uint64_t units = uint64_t(P.total_tiles) * parts;
             const uint64_t want = (units + kThreads / 32 - 1) / (kThreads / 32);  // at least one unit per warp

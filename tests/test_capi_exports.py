@@ -57,3 +57,36 @@ def test_product_does_not_import_oracle():
                 src = open(os.path.join(dirpath, f)).read()
                 assert not re.search(r"^\s*(import|from)\s+oracle\b", src, re.M), f
                 assert "tierkv_oracle" not in src and "libtierkv_ref" not in src, f
+
+
+def test_affine_form_host_rules():
+    """tkv_affine_form (host only, no device work): consecutive chunks of one
+    query have the form; a gap in the page columns, a second table, a short
+    chunk before the last or uneven chunk spacing does not."""
+    import ctypes as ct
+
+    from paper_2510_09665_b200._lib import AffinePlanC, XferDescC, lib
+
+    def descs(n=4, last=100, cs=1 << 20, fp_step=16, tables=None, short_at=None, bump_at=None):
+        out = []
+        for i in range(n):
+            d = XferDescC(chunk=(1 << 30) + i * cs + (4096 if i == bump_at else 0), layer_stride=1 << 16, table_dev=(tables or [0x1000] * n)[i],
+                          table_stride=512, first_page=3 + i * fp_step,
+                          n_tokens=(last if i + 1 == n else (200 if i == short_at else 256)))
+            out.append(d)
+        return (XferDescC * n)(*out)
+
+    def form(arr):
+        p = AffinePlanC()
+        rc = lib().tkv_affine_form(ct.cast(arr, ct.c_void_p), len(arr), 16, ct.byref(p))
+        return rc, p
+    rc, p = form(descs())
+    assert rc == 0 and (p.n_desc, p.pages_per_desc, p.last_tokens, p.first_page) == (4, 16, 100, 3)
+    assert p.chunk_stride == 1 << 20 and p.layer_stride == 1 << 16 and p.table_stride == 512
+    rc, p = form(descs(n=1, last=256))
+    assert rc == 0 and p.pages_per_desc == 16 and p.last_tokens == 256
+    assert form(descs(fp_step=17))[0] != 0
+    assert form(descs(tables=[0x1000, 0x1000, 0x2000, 0x1000]))[0] != 0
+    assert form(descs(short_at=1))[0] != 0
+    assert form(descs(last=0))[0] != 0
+    assert form(descs(bump_at=2))[0] != 0

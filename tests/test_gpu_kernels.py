@@ -456,3 +456,92 @@ def test_unit_kernel_many_descriptors(tkv, C):
     rng = np.random.default_rng(4500)
     spans = [(0, int(rng.integers(1, 17)), 16) for _ in range(4500)]  # each its own one-page table
     _multi_layer_case(tkv, C, 64, 2, spans, seed=4501, ppt=1, per_layer=True)
+
+
+def _affine_descs(n_chunks, last_tokens, pt, bpt, L, chunk0, table_dev, table_stride, first_page, rec=256):
+    from paper_2510_09665_b200.api import XferDescC
+    out = []
+    for i in range(n_chunks):
+        d = XferDescC()
+        d.chunk = chunk0 + i * L * rec * bpt
+        d.layer_stride = rec * bpt
+        d.table_dev = table_dev
+        d.table_stride = table_stride
+        d.first_page = first_page + i * (rec // pt)
+        d.n_tokens = rec if i + 1 < n_chunks else last_tokens
+        out.append(d)
+    return out
+
+
+@pytest.mark.parametrize("bpt,last,shared,layer_base", [(4096, 256, False, False), (512, 88, False, False),
+                                                         (16, 7, True, False), (1024, 200, False, True),
+                                                         (48, 256, True, True)])
+def test_affine_launches_match_oracle(tkv, C, bpt, last, shared, layer_base):
+    """The affine launch form (one query's consecutive chunks): K1 per layer
+    and over all layers, K2 back, against the oracle's per-page memcpy
+    restatement — full and ragged last chunk, a shared (layer-independent)
+    page table, per-layer pool bases."""
+    from paper_2510_09665_b200._lib import AffinePlanC, XferDescC, check, lib
+    rng = np.random.default_rng(bpt + last)
+    pt, L, n_chunks, first = 16, 3, 4, 2
+    page_bytes = pt * bpt
+    pages_q = first + (n_chunks * 256) // pt
+    n_pages = L * pages_q + 8
+    pool_h = rng.integers(0, 256, size=n_pages * page_bytes, dtype=np.uint8)
+    perm = rng.permutation(n_pages).astype(np.int32)
+    rows = 1 if shared else L
+    tab = perm[:rows * pages_q].reshape(rows, pages_q).copy()
+    if layer_base:  # per-layer pools: layer l's page p at bases[l] + p * page_bytes (one pool, offset bases)
+        pool = torch.from_numpy(np.concatenate([pool_h] * L)).cuda()
+        bases = torch.tensor([pool.data_ptr() + l * n_pages * page_bytes for l in range(L)], dtype=torch.int64).cuda()
+        host_pool = [pool_h] * L
+    else:
+        pool = torch.from_numpy(pool_h).cuda()
+        bases = None
+        host_pool = [pool_h] * L
+    d_tab = torch.from_numpy(tab).cuda()
+    ch = torch.zeros(n_chunks * L * 256 * bpt, dtype=torch.uint8, device="cuda")
+    descs = _affine_descs(n_chunks, last, pt, bpt, L, ch.data_ptr(), d_tab.data_ptr(), pages_q, first)
+    arr = (XferDescC * n_chunks)(*descs)
+    plan = AffinePlanC()
+    assert lib().tkv_affine_form(ct.cast(arr, ct.c_void_p), n_chunks, pt, ct.byref(plan)) == 0
+    assert plan.pages_per_desc == 16 and plan.last_tokens == last and plan.chunk_stride == L * 256 * bpt
+    layout = tkv.api.PagedLayoutC(base=0 if layer_base else pool.data_ptr(),
+                                  layer_base_dev=bases.data_ptr() if layer_base else None, page_stride=page_bytes,
+                                  plane_stride=0, token_stride=bpt, plane_bytes=bpt, n_planes=1, page_tokens=pt,
+                                  bpt=bpt, shared_table=int(shared))
+
+    def want_chunks(pools):
+        out = np.zeros(ch.numel(), np.uint8)
+        for i in range(n_chunks):
+            n = 256 if i + 1 < n_chunks else last
+            for layer in range(L):
+                t = tab[0 if shared else layer, first + i * 16:]
+                o = i * L * 256 * bpt + layer * 256 * bpt
+                out[o:o + n * bpt] = C.gather_tokens(pools[layer], page_bytes, t, bpt, n)
+        return out
+    for per_layer in (True, False):
+        ch.zero_()
+        for l0, nl in ([(layer, 1) for layer in range(L)] if per_layer else [(0, L)]):
+            check(lib().tkv_gather_layers_affine(ct.byref(layout), ct.byref(plan), l0, nl, 0, None))
+        torch.cuda.synchronize()
+        assert np.array_equal(ch.cpu().numpy(), want_chunks(host_pool)), per_layer
+    # K2: fresh chunk bytes back into the pages
+    src = rng.integers(0, 256, size=ch.numel(), dtype=np.uint8)
+    ch.copy_(torch.from_numpy(src))
+    ref = [p.copy() for p in ([pool_h] if not layer_base else [pool_h.copy() for _ in range(L)])]
+    for i in range(n_chunks):
+        n = 256 if i + 1 < n_chunks else last
+        for layer in range(L):
+            t = tab[0 if shared else layer, first + i * 16:]
+            o = i * L * 256 * bpt + layer * 256 * bpt
+            C.scatter_tokens(ref[layer if layer_base else 0], page_bytes, t, bpt, n, src[o:o + n * bpt])
+    for layer in range(L):
+        check(lib().tkv_scatter_layers_affine(ct.byref(layout), ct.byref(plan), layer, 1, 0, None))
+    torch.cuda.synchronize()
+    got = pool.cpu().numpy()
+    if layer_base:
+        for layer in range(L):
+            assert np.array_equal(got[layer * n_pages * page_bytes:(layer + 1) * n_pages * page_bytes], ref[layer])
+    else:
+        assert np.array_equal(got, ref[0])

@@ -29,11 +29,14 @@ def main():
     ap.add_argument("--layers", type=int, default=80)
     ap.add_argument("--reps", type=int, default=5)
     ap.add_argument("--ctas", type=int, default=0)
+    ap.add_argument("--affine", action="store_true",
+                    help="launch through tkv_*_layers_affine (the connector's one-query form) instead of "
+                         "the descriptor-list entry points")
     args = ap.parse_args()
     import numpy as np
     import torch
 
-    from paper_2510_09665_b200._lib import check, lib
+    from paper_2510_09665_b200._lib import AffinePlanC, check, lib
     from paper_2510_09665_b200.api import Engine, XferDescC, plan_tiles
     peak = 6650.0
     try:
@@ -81,8 +84,15 @@ def main():
             ao |= d.chunk | d.layer_stride
         layout = e.layout()
         payload = n * bpt
+        aff = AffinePlanC()
+        check(lib_.tkv_affine_form(ct.cast(arr, ct.c_void_p), len(descs), 16, ct.byref(aff)))
+        affine_fn = {id(lib_.tkv_gather_layers): lib_.tkv_gather_layers_affine,
+                     id(lib_.tkv_scatter_layers): lib_.tkv_scatter_layers_affine}
 
         def launch(fn, layer):
+            if args.affine:
+                check(affine_fn[id(fn)](ct.byref(layout), ct.byref(aff), layer, 1, args.ctas, stream.cuda_stream))
+                return
             check(fn(ct.byref(layout), d_desc.data_ptr(), d_tb.data_ptr(), len(descs), int(tb[-1]), layer, 1,
                      ppt, ao, args.ctas, stream.cuda_stream))
 
@@ -130,7 +140,8 @@ def main():
                 per_launch_noev = e0.elapsed_time(e1) / L
             med = statistics.median(times)
             gbs = 2 * payload / (med / 1e3) / 1e9
-            print(json.dumps({"kernel": name, "variant": os.environ.get("TKV_PAGED_KERNEL", "unit"), "bpt": bpt, "launch_mib": round(payload / 2**20, 2),
+            variant = "unit-affine" if args.affine else os.environ.get("TKV_PAGED_KERNEL", "unit")
+            print(json.dumps({"kernel": name, "variant": variant, "bpt": bpt, "launch_mib": round(payload / 2**20, 2),
                               "launch_ms_median": round(med, 5), "launch_ms_min": round(min(times), 5),
                               "gbs": round(gbs, 1), "frac": round(gbs / peak, 4),
                               "back_to_back_gbs": round(2 * payload * L / (span / 1e3) / 1e9, 1),
