@@ -195,14 +195,18 @@ int tkv_ce_copy(const void* src, void* dst, uint64_t bytes, void* stream);
  * batch of payloads. Encode: src = payload, dst = blob, bytes = payload
  * length; blob = u32 len | f32 scale | int8 lanes | odd tail byte
  * (tkv_q8_blob_bytes). Decode: src = blob, dst = payload, bytes = original
- * length. seg_base (n+1 entries) comes from tkv_codec_plan; maxabs_dev is
- * n ints of scratch. */
+ * length. seg_base (n+1 entries) comes from tkv_codec_plan; scratch_dev
+ * (the maxabs_dev argument) is tkv_q8_encode_scratch_bytes(n) bytes of
+ * device scratch per call — per-item absmax and the single-pass encode's two
+ * per-item counters — and must not be shared by encodes that may run
+ * concurrently. */
 typedef struct tkv_codec_item {
     const uint8_t* src_dev;
     uint8_t* dst_dev;
     uint64_t bytes;
 } tkv_codec_item;
 uint64_t tkv_q8_blob_bytes(uint64_t payload_bytes);
+uint64_t tkv_q8_encode_scratch_bytes(uint32_t n);
 int tkv_codec_plan(const tkv_codec_item* items, uint32_t n, uint32_t* seg_base_out);
 int tkv_q8_encode(const tkv_codec_item* items_dev, const uint32_t* seg_base_dev, uint32_t n,
                   uint32_t total_segs, int* maxabs_dev, void* stream);

@@ -95,6 +95,7 @@ SIGNATURES = {
     "tkv_q8_blob_bytes": (ct.c_uint64, [ct.c_uint64]),
     "tkv_codec_plan": (ct.c_int, [vp, ct.c_uint32, u32p]),
     "tkv_q8_encode": (ct.c_int, [vp, vp, ct.c_uint32, ct.c_uint32, vp, vp]),
+    "tkv_q8_encode_scratch_bytes": (ct.c_uint64, [ct.c_uint32]),
     "tkv_q8_decode": (ct.c_int, [vp, vp, ct.c_uint32, ct.c_uint32, vp]),
     "tkv_chunk_keys": (ct.c_int, [ct.c_char_p, sz, u32p, sz, u8p, szp]),
     "tkv_keychain_next": (ct.c_int, [ct.c_char_p, sz, u8p, u32p, sz, u8p]),

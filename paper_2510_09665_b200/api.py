@@ -488,7 +488,8 @@ def _codec_launch(fn, srcs, dsts, sizes, with_scratch: bool, stream=None):
     d_seg = torch.from_numpy(seg.view(np.int32)).to(dev)
     s = stream.cuda_stream if stream is not None else torch.cuda.current_stream(dev).cuda_stream
     if with_scratch:
-        scratch = torch.zeros(len(srcs), dtype=torch.int32, device=dev)
+        nbytes = int(lib().tkv_q8_encode_scratch_bytes(len(srcs)))
+        scratch = torch.zeros(nbytes // 4, dtype=torch.int32, device=dev)
         check(fn(d_items.data_ptr(), d_seg.data_ptr(), len(srcs), int(seg[-1]), scratch.data_ptr(), s))
     else:
         check(fn(d_items.data_ptr(), d_seg.data_ptr(), len(srcs), int(seg[-1]), s))

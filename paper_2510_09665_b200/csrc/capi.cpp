@@ -311,6 +311,8 @@ int tkv_codec_plan(const tkv_codec_item* items, uint32_t n, uint32_t* seg_base) 
     return 0;
 }
 
+uint64_t tkv_q8_encode_scratch_bytes(uint32_t n) { return q8_encode_scratch_bytes(n); }
+
 int tkv_q8_encode(const tkv_codec_item* items, const uint32_t* seg_base, uint32_t n, uint32_t segs,
                   int* maxabs, void* stream) {
     return cuda(launch_q8_encode(reinterpret_cast<const CodecItem*>(items), seg_base, n, segs, maxabs,

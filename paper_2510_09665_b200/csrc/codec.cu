@@ -251,6 +251,7 @@ q8_encode_kernel(const CodecItem* __restrict__ items, const uint32_t* __restrict
 // (never __syncthreads) and per-item global counters, so there is no
 // grid-wide barrier. Tile -> CTA assignment rotates per item.
 constexpr int kFusedThreads = 1024;
+constexpr uint32_t kCounterStride = 32;  // unsigned per counter: one 128-byte line each
 constexpr int kBarA = 1, kBarB = 2;               // named barriers (0 = __syncthreads)
 
 struct V32 {
@@ -332,7 +333,7 @@ q8_encode_fused_kernel(const CodecItem* __restrict__ items, uint32_t n_items, in
         constexpr uint64_t kStrideA = 32ull * kAThreads;
         for (uint32_t p = 0; p < n_items; ++p) {
             if (p >= kAhead + 1) {  // L2 budget: item p - 1 - kAhead quantised everywhere
-                if (at == 0) await_count(done + p - 1 - kAhead, G);
+                if (at == 0) await_count(done + uint64_t(p - 1 - kAhead) * kCounterStride, G);
                 bar_named(kBarA, kAThreads);
             }
             const CodecItem it = items[p];
@@ -375,7 +376,7 @@ q8_encode_fused_kernel(const CodecItem* __restrict__ items, uint32_t n_items, in
                 for (int i = 0; i < kAWarps; ++i) mm = max(mm, red[p & 1][i]);
                 if (mm) atomicMax(maxabs + p, mm);
                 __threadfence();
-                atomicAdd(arrive + p, 1u);
+                atomicAdd(arrive + uint64_t(p) * kCounterStride, 1u);
             }
         }
         return;
@@ -384,7 +385,7 @@ q8_encode_fused_kernel(const CodecItem* __restrict__ items, uint32_t n_items, in
     const uint32_t bt = threadIdx.x - kAThreads;
     const uint64_t gt = uint64_t(blockIdx.x) * kBThreads + bt, gn = uint64_t(G) * kBThreads;
     for (uint32_t q = 0; q < n_items; ++q) {
-        if (bt == 0) await_count(arrive + q, G);  // item q's absmax complete everywhere
+        if (bt == 0) await_count(arrive + uint64_t(q) * kCounterStride, G);  // item q's absmax complete everywhere
         bar_named(kBarB, kBThreads);
         const CodecItem it = items[q];
         const float scale = float(double(__ldcg(maxabs + q)) / 127.0);
@@ -412,7 +413,7 @@ q8_encode_fused_kernel(const CodecItem* __restrict__ items, uint32_t n_items, in
         bar_named(kBarB, kBThreads);
         if (bt == 0) {
             __threadfence();
-            atomicAdd(done + q, 1u);
+            atomicAdd(done + uint64_t(q) * kCounterStride, 1u);
         }
     }
 }
@@ -493,19 +494,16 @@ int grid(uint32_t segs) { return int(segs < 148u * 8 ? (segs ? segs : 1) : 148u 
 
 }  // namespace
 
+uint64_t q8_encode_scratch_bytes(uint32_t n) {
+    return ((uint64_t(n) * 4 + 127) & ~uint64_t(127)) + 2ull * n * kCounterStride * 4;
+}
+
 uint32_t codec_segments(uint64_t bytes) { return uint32_t((bytes + kSeg - 1) / kSeg) + (bytes == 0); }
 
 namespace {
-// Per-device state of the single-pass encode: resident grid size and the
-// per-item arrival and done counters (grown on demand, zeroed per launch
-// in-stream).
-struct FusedState {
-    int grid = 0;
-    unsigned* arrive = nullptr;
-    uint32_t cap = 0;
-};
+// Resident grid of the single-pass encode per device (one CTA per SM).
 std::mutex g_fused_mu;
-std::map<int, FusedState> g_fused;
+std::map<int, int> g_fused_grid;
 
 bool fused_enabled() {
     static const bool on = [] {
@@ -522,41 +520,38 @@ cudaError_t launch_q8_encode(const CodecItem* items, const uint32_t* seg_base, u
     cudaError_t e = cudaMemsetAsync(maxabs, 0, n_items * sizeof(int), s);
     if (e != cudaSuccess) return e;
     if (fused_enabled()) {
+        // scratch (q8_encode_scratch_bytes): maxabs[n], then one 128-byte
+        // line per item for its arrival counter and one for its done counter
+        // (spinning warps never share a line with another item's atomics) —
+        // in the caller's per-call scratch, so concurrent encodes never share
+        // them
+        unsigned* arrive = reinterpret_cast<unsigned*>(reinterpret_cast<uint8_t*>(maxabs) +
+                                                       ((uint64_t(n_items) * 4 + 127) & ~uint64_t(127)));
+        unsigned* done = arrive + uint64_t(n_items) * kCounterStride;
         int dev = 0;
         if ((e = cudaGetDevice(&dev)) != cudaSuccess) return e;
-        unsigned* arrive = nullptr;
         int grid = 0;
         {
             std::lock_guard<std::mutex> lk(g_fused_mu);
-            FusedState& st = g_fused[dev];
-            if (st.grid == 0) {
+            int& g = g_fused_grid[dev];
+            if (g == 0) {
                 int per_sm = 0, sms = 0;
-                if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, q8_encode_fused_kernel<kFusedThreads, 12, 6, 2, 2>, kFusedThreads,
-                                                                        0)) != cudaSuccess)
+                if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+                         &per_sm, q8_encode_fused_kernel<kFusedThreads, 12, 6, 2, 2>, kFusedThreads, 0)) != cudaSuccess)
                     return e;
                 if ((e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev)) != cudaSuccess) return e;
                 if (per_sm < 1) return cudaErrorCooperativeLaunchTooLarge;
-                st.grid = sms;  // one CTA per SM (launch bounds: 512 threads, 1 per SM)
+                g = sms;  // one CTA per SM (launch bounds: 1024 threads, 1 per SM)
             }
-            if (st.cap < 2 * n_items) {
-                // (the old counters may still be read by an in-flight launch on
-                // another stream: leak them rather than free under it)
-                uint32_t cap = std::max<uint32_t>(64, st.cap);
-                while (cap < 2 * n_items) cap *= 2;
-                if ((e = cudaMalloc(&st.arrive, cap * sizeof(unsigned))) != cudaSuccess) return e;
-                st.cap = cap;
-            }
-            arrive = st.arrive;
-            grid = st.grid;
+            grid = g;
         }
-        if ((e = cudaMemsetAsync(arrive, 0, 2 * n_items * sizeof(unsigned), s)) != cudaSuccess) return e;
-        unsigned* done = arrive + n_items;
+        if ((e = cudaMemsetAsync(arrive, 0, 2ull * n_items * kCounterStride * sizeof(unsigned), s)) != cudaSuccess)
+            return e;
         void* args[] = {const_cast<CodecItem**>(&items), &n_items, &maxabs, &arrive, &done};
         note_launch();
         // 12 absmax warps x 6 x 32-byte loads in flight, 20 quantise warps x 2,
         // absmax up to two items ahead of the quantise (measured against
-        // 4-24 absmax warps, 1-3 items ahead: tools/run_codec.sh history in
-        // profiles/r02_codec.jsonl)
+        // 4-24 absmax warps, 1-3 items ahead: profiles/r02_codec.jsonl)
         const void* fn = reinterpret_cast<const void*>(q8_encode_fused_kernel<kFusedThreads, 12, 6, 2, 2>);
         return cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(kFusedThreads), args, 0, s);
     }

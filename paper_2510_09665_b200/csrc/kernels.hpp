@@ -252,6 +252,9 @@ struct CodecItem {
 };
 uint32_t codec_segments(uint64_t bytes);
 inline uint64_t q8_blob_bytes(uint64_t payload) { return 8 + payload / 2 + (payload & 1); }
+// maxabs: q8_encode_scratch_bytes(n_items) of per-call scratch (absmax per
+// item, then the single-pass encode's arrival and done counters per item)
+uint64_t q8_encode_scratch_bytes(uint32_t n);
 cudaError_t launch_q8_encode(const CodecItem* items, const uint32_t* seg_base, uint32_t n_items,
                              uint32_t total_segs, int* maxabs, cudaStream_t stream);
 cudaError_t launch_q8_decode(const CodecItem* items, const uint32_t* seg_base, uint32_t n_items,

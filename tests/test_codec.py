@@ -3,6 +3,8 @@ oracle against the reference (CPU), and the device codec against the oracle
 byte for byte (GPU). Cases follow test_formats.cpp:137-186 — lengths 2, 100,
 4096, 4097, all-zero, the -32768 lane, truncated blobs — plus large payloads
 that span many CTA segments."""
+import ctypes as ct
+
 import numpy as np
 import pytest
 import torch
@@ -189,3 +191,33 @@ def test_device_q8_encode_every_lane_vector_path(tkv, C, maxabs):
     p = tiled.astype(np.int16).view(np.uint8)
     blob = q8_encode([torch.from_numpy(p.copy()).cuda()])[0].cpu().numpy()
     assert np.array_equal(blob, C.q8_encode(p))
+
+
+@pytest.mark.gpu
+def test_device_q8_encode_concurrent_streams(tkv, C):
+    """Encodes issued back to back on two streams with no synchronisation in
+    between (each with its own scratch: the single-pass encode's per-item
+    counters live there) both produce the oracle's bytes."""
+    from paper_2510_09665_b200._lib import CodecItemC, check, lib, u32p
+    rng = np.random.default_rng(31)
+    streams = [torch.cuda.Stream(), torch.cuda.Stream()]
+    jobs = []
+    for k in range(2):
+        ps = [np.clip(rng.normal(0, 900 * (k + 1), size=(3 << 19) + 17 * k), -32768, 32767).astype(np.int16)
+              .view(np.uint8).copy() for _ in range(3)]
+        src = [torch.from_numpy(p).cuda() for p in ps]
+        blobs = [torch.empty(int(lib().tkv_q8_blob_bytes(p.size)), dtype=torch.uint8, device="cuda") for p in ps]
+        items = (CodecItemC * 3)(*[CodecItemC(s.data_ptr(), b.data_ptr(), p.size) for s, b, p in zip(src, blobs, ps)])
+        seg = np.zeros(4, np.uint32)
+        check(lib().tkv_codec_plan(ct.cast(items, ct.c_void_p), 3, seg.ctypes.data_as(u32p)))
+        d_items = torch.frombuffer(bytearray(bytes(items)), dtype=torch.uint8).cuda()
+        d_seg = torch.from_numpy(seg.view(np.int32)).cuda()
+        scratch = torch.zeros(int(lib().tkv_q8_encode_scratch_bytes(3)) // 4, dtype=torch.int32, device="cuda")
+        jobs.append((ps, src, blobs, d_items, d_seg, int(seg[-1]), scratch))
+    torch.cuda.synchronize()
+    for (ps, src, blobs, d_items, d_seg, segs, scratch), s in zip(jobs, streams):
+        check(lib().tkv_q8_encode(d_items.data_ptr(), d_seg.data_ptr(), 3, segs, scratch.data_ptr(), s.cuda_stream))
+    torch.cuda.synchronize()
+    for ps, _, blobs, *_ in jobs:
+        for p, b in zip(ps, blobs):
+            assert np.array_equal(b.cpu().numpy(), C.q8_encode(p))

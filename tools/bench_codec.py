@@ -36,7 +36,7 @@ def main(n_items=16, nbytes=32 << 20, reps=5):
                 torch.from_numpy(seg.view(np.int32)).cuda(), int(seg[-1]))
     ei, es, en = plan(pay, blobs)
     di, ds, dn = plan(blobs, outs)
-    scratch = torch.zeros(n_items, dtype=torch.int32, device="cuda")
+    scratch = torch.zeros(int(lib().tkv_q8_encode_scratch_bytes(n_items)) // 4, dtype=torch.int32, device="cuda")
     s = torch.cuda.current_stream().cuda_stream
 
     def enc():
