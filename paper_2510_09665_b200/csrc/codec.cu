@@ -519,7 +519,10 @@ cudaError_t launch_q8_encode(const CodecItem* items, const uint32_t* seg_base, u
     if (n_items == 0) return cudaSuccess;
     cudaError_t e = cudaMemsetAsync(maxabs, 0, n_items * sizeof(int), s);
     if (e != cudaSuccess) return e;
-    if (fused_enabled()) {
+    // The single-pass encode pays a grid-wide hand-off per item (a few us):
+    // batches of small items (under ~1 MiB on average: 16 segments) take the
+    // two-kernel encode, whose segments spread across items freely.
+    if (fused_enabled() && uint64_t(total_segs) >= 16ull * n_items) {
         // scratch (q8_encode_scratch_bytes): maxabs[n], then one 128-byte
         // line per item for its arrival counter and one for its done counter
         // (spinning warps never share a line with another item's atomics) —
