@@ -13,7 +13,11 @@
       token question per query; seeded 50 % / 90 % document reuse; lookup
       (K3 + LPM) + retrieve of the document prefix (hits) or cold store
       (misses). Lookup latency split by hit / miss.
-  c5  needs >= 2 GPUs: bench.py at N >= 2 reports it ("pd").
+  c5  PD transfer. Across GPUs (NVLink pairs) only at N >= 2: bench.py's
+      "pd". Here c5_loopback: the same pair transfer (70B KV, TP=4 head
+      shard, 32K tokens = 2.5 GiB) with prefill and decode engines on ONE
+      GPU — every send path, the PdStaging ordinal contract and the land,
+      byte-verified; HBM-bound, not an NVLink number.
 
 Every config verifies its bytes on the device after the timed work: the page
 image of every request against synth (retrieved prefix + computed tokens),
@@ -341,11 +345,92 @@ def c4(queries=8, reuse=0.5, pcie=None, cpu=True):
     return out
 
 
+def c5_loopback(reps=3, cpu=True):
+    """Config 5's per-pair PD transfer (run_pd, src/sim_engine.cpp:374-472)
+    with the prefill and the decode engine on the same GPU: the prefilled
+    32K-token prompt's KV (70B, 80 layers, TP=4 head shard: bpt 1024) moves
+    into the decoder's landing buffer by each send path — K1 straight into
+    the landing buffer (SM-direct), K1 into local staging + copy-engine copy
+    (CE-staged), and layer-streamed at page (16-token window) granularity —
+    then the decoder takes the chunk records out of order with a duplicate
+    through PdStaging, lands them with one K2 and checks every page word
+    against synth. Same device, so the bound is HBM (K1 reads and writes each
+    byte: 2 x payload), not NVLink."""
+    from paper_2510_09665_b200.api import PdLayerSender, PdRecordC, PdStaging, pd_land, pd_send, pd_send_staged
+    tag, L, bpt, n, q = "llama-3.1-70b", 80, 4096 // 4, 32768, 7
+    chunks, stride = (n + 255) // 256, L * 256 * bpt
+    mk = dict(num_layers=L, bpt=bpt, page_tokens=16, tag=tag, chunk_size=256, ram_slots=2,
+              num_pages=(n // 16 + 16) * L, device=0)
+    pre, dec = Engine(**mk), Engine(**mk)
+    out = {"workload": "c5 (one GPU): 70B KV, TP=4 shard (bpt 1024), 32768-token prompt, one prefill -> decode "
+                       "pair's chunks (2.5 GiB), prefill and decode engines on the same B200",
+           "note": "no NVLink on a 1-GPU box: the NVLink pairs are bench.py's 'pd' at N >= 2"}
+    try:
+        prompt = toks(n, 999)
+        assert pre.bind_pages(q, n) == 0
+        pre.compute_range(q, prompt, 0, n)
+        landing = torch.empty(chunks * stride, dtype=torch.uint8, device="cuda")
+        staging = torch.empty(chunks * stride, dtype=torch.uint8, device="cuda")
+        payload = n * L * bpt
+        torch.cuda.synchronize()
+
+        def timed(fn):
+            best, res = 1e9, None
+            for it in range(reps + 1):
+                torch.cuda.synchronize()
+                t0 = time.perf_counter()
+                res = fn()
+                torch.cuda.synchronize()
+                if it:
+                    best = min(best, time.perf_counter() - t0)
+            return best, res
+
+        def streamed():
+            snd = PdLayerSender(pre, q, n, 16, landing.data_ptr(), L * 16 * bpt)
+            for layer in range(L):
+                assert snd.layer(layer) == 0
+            r = snd.finish()
+            snd.close()
+            return r
+        t_ce, _ = timed(lambda: pd_send_staged(pre, q, n, landing.data_ptr(), stride, staging.data_ptr()))
+        t_pg, wrecs = timed(streamed)
+        assert len(wrecs) == (n + 15) // 16
+        t_sm, recs = timed(lambda: pd_send(pre, q, n, landing.data_ptr(), stride))  # landed bytes come from it
+        st = PdStaging()
+        assert st.register_query(q) == 0
+        for o in list(range(chunks))[::-1] + [0]:  # out of order + a duplicate
+            r = recs[o]
+            assert st.push(q, o, o == chunks - 1, PdRecordC(addr=r.addr, bytes=r.bytes, token_count=r.token_count,
+                                                            first_token=r.first_token)) == 0
+        rc, landed = st.await_(q)
+        assert rc == 0 and len(landed) == chunks
+        assert dec.bind_pages(q, n) == 0
+        t_land, _ = timed(lambda: pd_land(dec, q, landed))  # idempotent: the same records each time
+        mism = dec.verify_range(q, prompt, 0, n)
+        st.close()
+        g = lambda t: round(payload / t / 1e9, 1)  # noqa: E731
+        out.update({"bytes": payload, "sm_direct_gbps": g(t_sm), "ce_staged_gbps": g(t_ce),
+                    "layer_streamed_page_gbps": g(t_pg), "land_gbps": g(t_land),
+                    "sm_direct_hbm_algorithmic_gbps": round(2 * payload / t_sm / 1e9, 1),
+                    "verify": {"page_mismatch_words": mism, "chunks_landed": len(landed)},
+                    "timing": "min of 3 synchronised calls after one warm-up (each send returns after its "
+                              "bytes landed)"})
+        if cpu:
+            sys.path.insert(0, ROOT)
+            import bench as _bench
+            out["cpu_baseline"] = _bench.reference_pd_gbps(L, bpt)
+    finally:
+        pre.close()
+        dec.close()
+    return out
+
+
 def run_all(pcie=None, cpu=True, wave=8, queries=8):
     out = {}
     for name, fn in (("c1", lambda: c1(3, pcie, cpu)), ("c2", lambda: c2(wave, pcie, cpu)),
                      ("c4_reuse50", lambda: c4(queries, 0.5, pcie, cpu)),
-                     ("c4_reuse90", lambda: c4(queries, 0.9, pcie, cpu))):
+                     ("c4_reuse90", lambda: c4(queries, 0.9, pcie, cpu)),
+                     ("c5_loopback", lambda: c5_loopback(3, cpu))):
         t0 = time.time()
         try:
             out[name] = fn()
@@ -358,7 +443,7 @@ def run_all(pcie=None, cpu=True, wave=8, queries=8):
 
 if __name__ == "__main__":
     ap = argparse.ArgumentParser()
-    ap.add_argument("--only", default="c1,c2,c4")
+    ap.add_argument("--only", default="c1,c2,c4,c5")
     ap.add_argument("--wave", type=int, default=8)
     ap.add_argument("--queries", type=int, default=8)
     ap.add_argument("--no-cpu", action="store_true")
@@ -371,3 +456,5 @@ if __name__ == "__main__":
     if "c4" in a.only:
         print(json.dumps(c4(a.queries, 0.5, cpu=cpu)), flush=True)
         print(json.dumps(c4(a.queries, 0.9, cpu=cpu)), flush=True)
+    if "c5" in a.only:
+        print(json.dumps(c5_loopback(3, cpu=cpu)), flush=True)
