@@ -505,12 +505,16 @@ namespace {
 std::mutex g_fused_mu;
 std::map<int, int> g_fused_grid;
 
-bool fused_enabled() {
-    static const bool on = [] {
+// TKV_Q8_ENCODE: unset = by batch shape (below), "fused" = the single-pass
+// encode for every batch, "twopass" = the two kernels for every batch.
+int encode_mode() {
+    static const int mode = [] {
         const char* v = std::getenv("TKV_Q8_ENCODE");
-        return !(v && std::strcmp(v, "twopass") == 0);
+        if (v && std::strcmp(v, "twopass") == 0) return 2;
+        if (v && std::strcmp(v, "fused") == 0) return 1;
+        return 0;
     }();
-    return on;
+    return mode;
 }
 }  // namespace
 
@@ -519,10 +523,14 @@ cudaError_t launch_q8_encode(const CodecItem* items, const uint32_t* seg_base, u
     if (n_items == 0) return cudaSuccess;
     cudaError_t e = cudaMemsetAsync(maxabs, 0, n_items * sizeof(int), s);
     if (e != cudaSuccess) return e;
-    // The single-pass encode pays a grid-wide hand-off per item (a few us):
-    // batches of small items (under ~1 MiB on average: 16 segments) take the
-    // two-kernel encode, whose segments spread across items freely.
-    if (fused_enabled() && uint64_t(total_segs) >= 16ull * n_items) {
+    // The single-pass encode saves one DRAM read of each item (P / 6.4 TB/s:
+    // ~5 us per 32 MiB) but pays a grid-wide hand-off per item (~4 us) and a
+    // pipeline fill of one item: it wins from ~24 MiB items on and with a
+    // few items to overlap (16 x 32 MiB: 0.18 vs 0.24 ms; 6 x 80 MiB: 0.197
+    // vs 0.221; 64 x 8 MiB: 0.288 vs 0.239; 4 x 10 MiB: 0.032 vs 0.027,
+    // profiles/r02_codec.jsonl). Other batches take the two-kernel encode.
+    const int mode = encode_mode();
+    if (mode == 1 || (mode == 0 && n_items >= 3 && uint64_t(total_segs) >= 384ull * n_items)) {
         // scratch (q8_encode_scratch_bytes): maxabs[n], then one 128-byte
         // line per item for its arrival counter and one for its done counter
         // (spinning warps never share a line with another item's atomics) —

@@ -156,20 +156,24 @@ def test_device_q8_encode_batch_pipeline(tkv, C):
 
 
 @pytest.mark.gpu
-def test_q8_twopass_variant_subprocess():
-    """The two-kernel encode (absmax, then quantise) stays selectable with
-    TKV_Q8_ENCODE=twopass (read once per process): the encode parity tests in
-    a child process."""
+@pytest.mark.parametrize("mode", ["twopass", "fused"])
+def test_q8_encode_variant_subprocess(mode):
+    """Both encodes on every shape: the batch shape picks the single-pass
+    (fused) encode only for several items of >= 24 MiB, so the encode parity
+    tests run again in child processes with TKV_Q8_ENCODE=twopass and
+    TKV_Q8_ENCODE=fused (read once per process) forcing one of them."""
     import os
     import subprocess
     import sys
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    env = dict(os.environ, TKV_Q8_ENCODE="twopass")
+    env = dict(os.environ, TKV_Q8_ENCODE=mode)
     r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-m", "gpu",
                         "tests/test_codec.py::test_device_q8_matches_oracle",
                         "tests/test_codec.py::test_device_q8_encode_batch_pipeline",
-                        "tests/test_codec.py::test_device_q8_encode_every_lane"],
-                       cwd=root, env=env, capture_output=True, text=True, timeout=600)
+                        "tests/test_codec.py::test_device_q8_encode_every_lane",
+                        "tests/test_codec.py::test_device_q8_encode_every_lane_vector_path",
+                        "tests/test_codec.py::test_device_q8_encode_concurrent_streams"],
+                       cwd=root, env=env, capture_output=True, text=True, timeout=900)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
 
 

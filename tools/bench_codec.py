@@ -61,7 +61,7 @@ def main(n_items=16, nbytes=32 << 20, reps=5):
     payload = n_items * nbytes
     peak = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))).get("hbm_gbs", 6650.0) \
         if os.path.exists(os.path.join(ROOT, "MEASURED_PEAKS.json")) else 6650.0
-    res = {"codec": "q8-scale", "encode_variant": os.environ.get("TKV_Q8_ENCODE", "fused"),
+    res = {"codec": "q8-scale", "encode_variant": os.environ.get("TKV_Q8_ENCODE", "auto (by batch shape)"),
            "items": n_items, "payload_bytes_per_item": nbytes,
            "encode_ms": round(te, 4), "decode_ms": round(td, 4),
            # the two-pass encode's DRAM traffic (payload read twice, half
