@@ -12,9 +12,10 @@
 // warp-specialised absmax warps stream each item from DRAM once, keeping its
 // lines in L2, and quantise warps of the same CTAs re-read it from L2 one
 // item behind, so DRAM sees the payload once (ncu: 538 MB read for a 537 MB
-// payload) instead of twice. 16 x 32 MiB: 0.179 ms (0.70 of the one-pass
-// bound) vs 0.237 ms for the two-kernel encode, kept as an A/B switch
-// (TKV_Q8_ENCODE=twopass). Earlier single-pass tries — an atomic work queue
+// payload) instead of twice. 16 x 32 MiB: 0.177-0.187 ms (0.67-0.71 of the
+// one-pass bound) vs 0.237 ms for the two-kernel encode, which batches of
+// small or few items keep (launch_q8_encode; TKV_Q8_ENCODE=fused|twopass
+// forces one). Earlier single-pass tries — an atomic work queue
 // (round 1), a CTA quantising one segment behind its own absmax — lost
 // their L2 savings to CTAs alternating DRAM and L2 phases.
 #include <cuda_runtime.h>
