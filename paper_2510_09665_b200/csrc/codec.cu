@@ -110,36 +110,7 @@ __device__ __forceinline__ uint32_t quant(int32_t lane, double inv_up) {
 }
 
 // Four lanes (two little-endian words) -> four q8 bytes, the vector path of
-// the encode: |lane| as the low word of the double 2^52 + |lane| (one move
-// of the constant high word), then ONE fma.rz per lane:
-//   fma.rz(2^52 + |lane|, inv, c),  c = 2^44 + 1/2 - 2^52 inv  (kFold)
-// is exactly 2^44 + 1/2 + |lane| inv rounded toward zero onto the 2^-8 grid
-// of [2^44, 2^45), so byte 1 of its low word is floor(Q' + 1/2) — quant()'s
-// value. c is exact when inv < 1/2 (scale > 2: c is a multiple of inv's ulp
-// below 2^53 of them); smaller scales take quant()'s subtraction first
-// (!kFold). No clamp: |lane| <= max|lane| = 127 * scale * (1 +- 2^-24), so
-// the byte is at most 127. Signs are applied bytewise: prmt's sign-replicate
-// mode turns each lane's high byte into a 0x00 / 0xff mask, and for
-// n <= 127, ((n ^ 0x7f) + 1) ^ 0x80 = -n mod 256 with no carry between bytes.
-template <bool kFold>
-__device__ __forceinline__ uint32_t quant4(uint32_t w0, uint32_t w1, double inv, double c) {
-    constexpr double kMagic = 4503599627370496.0;  // 2^52
-    const uint32_t a0 = __vabs2(w0), a1 = __vabs2(w1);  // -32768 -> 0x8000 (non-saturating)
-    const uint32_t mag[4] = {a0 & 0xffffu, a0 >> 16, a1 & 0xffffu, a1 >> 16};
-    uint32_t t[4];
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-        const double x = __hiloint2double(0x43300000, int(mag[k]));
-        t[k] = uint32_t(__double2loint(kFold ? __fma_rz(x, inv, c) : __fma_rz(x - kMagic, inv, 17592186044416.5)));
-    }
-    const uint32_t n = __byte_perm(__byte_perm(t[0], t[1], 0x0051), __byte_perm(t[2], t[3], 0x0051), 0x5410);
-    uint32_t m;  // 0xff where the lane is negative
-    asm("prmt.b32 %0, %1, %2, 0xFDB9;" : "=r"(m) : "r"(w0), "r"(w1));
-    const uint32_t neg = ((n ^ 0x7f7f7f7fu) + 0x01010101u) ^ 0x80808080u;
-    return (neg & m) | (n & ~m);
-}
-
-// Signed variant, no magnitude / sign handling (the fused encode). With inv
+// both encodes, with no magnitude / sign handling. With inv
 // STRICTLY above 1/scale (rounded up, bumped one ulp when the reciprocal is
 // exact), Q' = lane * inv sits within (0, 2^-44] of Q = lane / scale on the
 // side away from zero, so floor(Q' + 1/2) is round-half-away(Q) for either
@@ -171,9 +142,8 @@ __device__ __forceinline__ double inv_strict_up(float scale) {
     return inv;
 }
 
-template <bool kFold>
 __device__ __forceinline__ void quant_vectors(const uint8_t* __restrict__ src, uint8_t* __restrict__ out,
-                                              uint64_t b0, uint64_t vend, double inv, double c) {
+                                              uint64_t b0, uint64_t vend, double inv) {
     for (uint64_t b = b0 + 16 * threadIdx.x; b < vend; b += kStride * kUnroll) {
         uint4 v[kUnroll];
 #pragma unroll
@@ -183,7 +153,7 @@ __device__ __forceinline__ void quant_vectors(const uint8_t* __restrict__ src, u
         for (int u = 0; u < kUnroll; ++u) {
             if (b + u * kStride >= vend) break;
             __stcs(reinterpret_cast<uint2*>(out + (b + u * kStride) / 2),
-                   make_uint2(quant4<kFold>(v[u].x, v[u].y, inv, c), quant4<kFold>(v[u].z, v[u].w, inv, c)));
+                   make_uint2(quant4s(v[u].x, v[u].y, inv), quant4s(v[u].z, v[u].w, inv)));
         }
     }
 }
@@ -199,7 +169,7 @@ q8_encode_kernel(const CodecItem* __restrict__ items, const uint32_t* __restrict
         }
         const CodecItem it = items[lo];
         const float scale = float(double(maxabs[lo]) / 127.0);
-        const double inv = scale > 0.f ? __drcp_ru(double(scale)) : 0.0;  // scale 0: every lane is 0
+        const double inv = inv_strict_up(scale);  // scale 0: every lane is 0
         const uint32_t local = seg - seg_base[lo];
         if (local == 0 && threadIdx.x == 0) {
             const uint32_t len = uint32_t(it.bytes);
@@ -218,10 +188,7 @@ q8_encode_kernel(const CodecItem* __restrict__ items, const uint32_t* __restrict
         uint64_t vend = b0;
         if (((reinterpret_cast<uint64_t>(it.src) & 15) | (reinterpret_cast<uint64_t>(out) & 7)) == 0) {
             vend = b0 + ((b1 - b0) & ~uint64_t(15));
-            if (inv < 0.5)  // (uniform per item)
-                quant_vectors<true>(it.src, out, b0, vend, inv, 17592186044416.5 - inv * 4503599627370496.0);
-            else
-                quant_vectors<false>(it.src, out, b0, vend, inv, 0.0);
+            quant_vectors(it.src, out, b0, vend, inv);
         }
         for (uint64_t b = vend + 2 * threadIdx.x; b + 2 <= b1; b += 2 * kThreads) {
             const int32_t lane = int32_t(int16_t(uint16_t(it.src[b] | (it.src[b + 1] << 8))));
