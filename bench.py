@@ -959,6 +959,7 @@ def run_b200(args):
     bind_to_gpu_numa(local)
     if world > 1:
         if backend() == "nccl":
+            torch.cuda.set_device(local)  # NCCL collectives run on the current device
             dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
         else:
             dist.init_process_group(backend())
