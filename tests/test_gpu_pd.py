@@ -184,3 +184,15 @@ def test_pd_layer_streamed_page_and_chunk_granularity(tkv, C, late):
     assert snd.layer(L) == 16  # invalid_argument: out of range
     snd.close()
     pre.close()
+
+
+def test_c5_loopback_config_small():
+    """bench.py's configs.c5_loopback at a small size: every send path, the
+    PdStaging contract and the land run and the landed page image is exact."""
+    import os
+    import sys
+    sys.path.insert(0, os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tools"))
+    import bench_configs
+    r = bench_configs.c5_loopback(reps=1, cpu=False, n=1000, L=4)
+    assert r["verify"]["page_mismatch_words"] == 0 and r["verify"]["chunks_landed"] == 4, r
+    assert r["sm_direct_gbps"] > 0 and r["ce_staged_gbps"] > 0 and r["layer_streamed_page_gbps"] > 0

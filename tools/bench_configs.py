@@ -345,7 +345,7 @@ def c4(queries=8, reuse=0.5, pcie=None, cpu=True):
     return out
 
 
-def c5_loopback(reps=3, cpu=True):
+def c5_loopback(reps=3, cpu=True, n=32768, L=80):
     """Config 5's per-pair PD transfer (run_pd, src/sim_engine.cpp:374-472)
     with the prefill and the decode engine on the same GPU: the prefilled
     32K-token prompt's KV (70B, 80 layers, TP=4 head shard: bpt 1024) moves
@@ -357,13 +357,14 @@ def c5_loopback(reps=3, cpu=True):
     against synth. Same device, so the bound is HBM (K1 reads and writes each
     byte: 2 x payload), not NVLink."""
     from paper_2510_09665_b200.api import PdLayerSender, PdRecordC, PdStaging, pd_land, pd_send, pd_send_staged
-    tag, L, bpt, n, q = "llama-3.1-70b", 80, 4096 // 4, 32768, 7
+    tag, bpt, q = "llama-3.1-70b", 4096 // 4, 7
     chunks, stride = (n + 255) // 256, L * 256 * bpt
     mk = dict(num_layers=L, bpt=bpt, page_tokens=16, tag=tag, chunk_size=256, ram_slots=2,
               num_pages=(n // 16 + 16) * L, device=0)
     pre, dec = Engine(**mk), Engine(**mk)
-    out = {"workload": "c5 (one GPU): 70B KV, TP=4 shard (bpt 1024), 32768-token prompt, one prefill -> decode "
-                       "pair's chunks (2.5 GiB), prefill and decode engines on the same B200",
+    out = {"workload": f"c5 (one GPU): 70B KV ({L} layers), TP=4 shard (bpt 1024), {n}-token prompt, one prefill "
+                       f"-> decode pair's chunks ({n * L * bpt / 2**30:.2f} GiB), prefill and decode engines on the "
+                       "same B200",
            "note": "no NVLink on a 1-GPU box: the NVLink pairs are bench.py's 'pd' at N >= 2"}
     try:
         prompt = toks(n, 999)
