@@ -1029,6 +1029,7 @@ def run_b200(args):
     torch.cuda.synchronize()
     lib_ = bench.e.L
     launches0 = lib_.tkv_launch_count()
+    copies0 = bench.e.copy_runs()
     w0 = time.time()
     start = torch.cuda.Event(enable_timing=True)
     end = torch.cuda.Event(enable_timing=True)
@@ -1049,6 +1050,8 @@ def run_b200(args):
     time.sleep(0.25)  # let the sampler deliver the samples taken inside the region
     clk.__exit__()
     e2e_launches = lib_.tkv_launch_count() - launches0
+    copies1 = bench.e.copy_runs()
+    host_pieces, host_copies = copies1[0] - copies0[0], copies1[1] - copies0[1]
     # parity of the timed schedule itself: every suffix chunk the timed steps
     # stored that the tier still holds, read back from its slot on device
     ts_mism, ts_ok, ts_gone = bench.verify_stored_steps([args.warmup + k for k in range(args.steps)])
@@ -1147,9 +1150,13 @@ def run_b200(args):
         "e2e": {"value": round(e2e, 2), "unit": "GB/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                 "ms_per_step": round(e2e_ms, 3), "wall_ms_per_step": round(1e3 * wall / args.steps, 3),
                 "path": "C-ABI connector: K3 lookup, "
-                        + ("zero-copy K2 loads" if args.load_zero_copy else "CE batched H2D + K2 scatter")
+                        + ("zero-copy K2 loads" if args.load_zero_copy else "CE pitched H2D + K2 scatter")
                         + ", " + ("K1 zero-copy store" if args.store_zero_copy
-                                  else "K1 gather to HBM ring + CE batched D2H store")},
+                                  else "K1 gather to HBM ring + CE pitched D2H store"),
+                "host_tier_pieces": host_pieces, "host_tier_copies": host_copies,
+                "host_tier_copy_note": "chunk-layer slices moved by the copy engines in the timed region and "
+                                       "the copies issued for them (one cudaMemcpy2DAsync per run of slots "
+                                       "at a constant pitch)"},
         "roofline": {"bound": "hbm", "kernel": dom, "achieved": round(achieved, 1), "peak": hbm_peak,
                      "unit": "GB/s", "frac": round(achieved / hbm_peak, 4),
                      **ncu_traffic(dom, dom_bytes, bench), "peak_source": peak_source},

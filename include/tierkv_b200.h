@@ -190,6 +190,17 @@ int tkv_sm_copy(const void* src, void* dst, uint64_t bytes, void* stream);
  * (cudaMemcpyAsync, kind Default) on `stream`: the link probes (PCIe, NVLink
  * peer copy) the bench reports its rooflines against. */
 int tkv_ce_copy(const void* src, void* dst, uint64_t bytes, void* stream);
+/* Copy-engine copies of n pieces dst[i] <- src[i] (sizes[i] bytes) on
+ * `stream` (cudaMemcpyDefault), grouped into pitched runs: pieces whose
+ * addresses both advance by one constant step go as one 2D copy. The
+ * connector's host-tier path (a layer's chunk slices in their slots). */
+int tkv_ce_copy_pieces(void* const* dst, const void* const* src, const size_t* sizes, size_t n,
+                       void* stream);
+/* The grouping tkv_ce_copy_pieces applies (host only, no device call): fills
+ * first[k], rows[k] for each run k (capacity n) and returns the run count.
+ * Pitches above pitch_max never form a run. */
+size_t tkv_plan_copy_runs(void* const* dst, const void* const* src, const size_t* sizes, size_t n,
+                          size_t pitch_max, size_t* first, size_t* rows);
 
 /* q8-scale codec (Q8ScaleCodec, src/codec.cpp:27-91), bit-exact, over a
  * batch of payloads. Encode: src = payload, dst = blob, bytes = payload
@@ -354,6 +365,10 @@ int tkv_connector_append_decode_batch(tkv_connector* c, size_t n, const uint64_t
 int tkv_connector_finish_query(tkv_connector* c, uint64_t query, uint8_t* digests_out, size_t cap,
                                size_t* n);
 size_t tkv_connector_staging_peak(tkv_connector* c);
+/* Host-tier copy-engine traffic so far: out[0] = chunk-layer pieces copied,
+ * out[1] = copies issued for them (pieces at a constant slot / ring pitch go
+ * as one pitched copy). */
+void tkv_connector_copy_runs(tkv_connector* c, uint64_t out[2]);
 /* Prefix-digest memo counters: hits, misses (chunk links), capacity, resets,
  * re-hashed launches (a hit failed verification). */
 int tkv_connector_memo_stats(tkv_connector* c, uint64_t out[5]);

@@ -6,7 +6,7 @@ PagedKVStore, TieredStore, KeyChain) and drives hand-written sm_100a kernels
 only loads that library (``_lib``) and wraps it (``api``); it never computes a
 byte itself and has no CPU fallback.
 """
-from ._lib import LIB_PATH, TkvError, lib  # noqa: F401
+from ._lib import LIB_PATH, TkvError, check, lib  # noqa: F401
 
 
 def build(verbose: bool = False) -> str:

@@ -91,6 +91,8 @@ SIGNATURES = {
                                     ct.c_uint32, ct.c_uint32, ct.c_uint32, vp, vp]),
     "tkv_synth_chunk": (ct.c_int, [vp, ct.c_uint64, ct.c_uint32, ct.c_uint32, ct.c_uint32, ct.c_uint32, vp, vp]),
     "tkv_sm_copy": (ct.c_int, [vp, vp, ct.c_uint64, vp]),
+    "tkv_ce_copy_pieces": (ct.c_int, [vp, vp, vp, ct.c_size_t, vp]),
+    "tkv_plan_copy_runs": (ct.c_size_t, [vp, vp, vp, ct.c_size_t, ct.c_size_t, vp, vp]),
     "tkv_ce_copy": (ct.c_int, [vp, vp, ct.c_uint64, vp]),
     "tkv_q8_blob_bytes": (ct.c_uint64, [ct.c_uint64]),
     "tkv_codec_plan": (ct.c_int, [vp, ct.c_uint32, u32p]),
@@ -151,6 +153,7 @@ SIGNATURES = {
     "tkv_connector_append_decode_batch": (ct.c_int, [vp, sz, u64p, u32p, ct.POINTER(ct.c_int)]),
     "tkv_connector_finish_query": (ct.c_int, [vp, ct.c_uint64, u8p, sz, szp]),
     "tkv_connector_staging_peak": (sz, [vp]),
+    "tkv_connector_copy_runs": (None, [vp, u64p]),
     "tkv_connector_memo_stats": (ct.c_int, [vp, u64p]),
     "tkv_connector_debug_poison_memo": (ct.c_int, [vp]),
     "tkv_connector_hash_launches": (ct.c_uint64, [vp]),

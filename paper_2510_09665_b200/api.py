@@ -370,6 +370,12 @@ class Engine:
     def staging_peak(self) -> int:
         return int(self.L.tkv_connector_staging_peak(self.conn))
 
+    def copy_runs(self) -> tuple[int, int]:
+        """(pieces, copies): host-tier chunk-layer pieces and the copy-engine copies they took."""
+        out = (ct.c_uint64 * 2)()
+        self.L.tkv_connector_copy_runs(self.conn, out)
+        return int(out[0]), int(out[1])
+
     def lookups_host_decided(self) -> int:
         return int(self.L.tkv_connector_lookups_host_decided(self.conn))
 

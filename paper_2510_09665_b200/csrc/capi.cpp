@@ -265,6 +265,23 @@ int tkv_ce_copy(const void* src, void* dst, uint64_t bytes, void* stream) {
     return cuda(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, cudaStream_t(stream)));
 }
 
+int tkv_ce_copy_pieces(void* const* dst, const void* const* src, const size_t* sizes, size_t n,
+                       void* stream) {
+    if (n && (!dst || !src || !sizes)) return fail(Errc::invalid_argument, "null pointer");
+    return cuda(ce_copy_pieces(dst, src, sizes, n, cudaMemcpyDefault, cudaStream_t(stream)));
+}
+
+size_t tkv_plan_copy_runs(void* const* dst, const void* const* src, const size_t* sizes, size_t n,
+                          size_t pitch_max, size_t* first, size_t* rows) {
+    std::vector<CopyRun> runs(n);
+    const size_t k = plan_copy_runs(dst, src, sizes, n, pitch_max, runs.data());
+    for (size_t i = 0; i < k; ++i) {
+        if (first) first[i] = runs[i].first;
+        if (rows) rows[i] = runs[i].rows;
+    }
+    return k;
+}
+
 static SynthArgs synth_args(const uint32_t* tokens, const int32_t* table, uint32_t stride,
                             uint64_t seed, uint32_t p0, uint32_t p1, uint32_t l0, uint32_t l1) {
     SynthArgs a;
@@ -718,6 +735,11 @@ int tkv_connector_finish_query(tkv_connector* c, uint64_t q, uint8_t* out, size_
     });
 }
 size_t tkv_connector_staging_peak(tkv_connector* c) { return c->c->staging_peak_bytes(); }
+void tkv_connector_copy_runs(tkv_connector* c, uint64_t out[2]) {
+    const auto s = c->c->copy_stats();
+    out[0] = s.pieces;
+    out[1] = s.runs;
+}
 int tkv_connector_memo_stats(tkv_connector* c, uint64_t out[5]) {
     return guard([&] {
         auto s = c->c->hasher().memo_stats();

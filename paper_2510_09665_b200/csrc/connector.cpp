@@ -573,11 +573,9 @@ void Connector::enqueue_load_layers(BatchState& b, uint32_t upto) {
     const size_t bpt = model.bytes_per_token_per_layer;
     const PagedLayout layout = pages_.layout();
     const size_t n = b.loads.size();
-    std::vector<void*> dst(n), src(n);
+    std::vector<void*> dst(n);
+    std::vector<const void*> src(n);
     std::vector<size_t> sizes(n);
-    cudaMemcpyAttributes attr{};
-    attr.srcAccessOrder = cudaMemcpySrcAccessOrderStream;
-    size_t attr_idx = 0, fail_idx = 0;
     upto = std::min(upto, b.num_layers);
     for (uint32_t l = b.next_load; l < upto; ++l) {
         const uint32_t r = l % b.load_depth;
@@ -588,8 +586,8 @@ void Connector::enqueue_load_layers(BatchState& b, uint32_t upto) {
             dst[i] = load_ring_.buf.ptr + size_t(r) * b.load_layer_bytes + it.staging_off;
             sizes[i] = it.span.length() * bpt;
         }
-        TKV_CUDA(cudaMemcpyBatchAsync(dst.data(), src.data(), sizes.data(), n, &attr, &attr_idx, 1,
-                                      &fail_idx, h2d_stream_));
+        TKV_CUDA(ce_copy_pieces(dst.data(), src.data(), sizes.data(), n, cudaMemcpyHostToDevice,
+                                h2d_stream_, &copy_stats_));
         b.h2d_done[l].record(h2d_stream_);
         b.h2d_done[l].wait_on(load_stream_);
         TKV_CUDA(launch_paged_copy(layout, b.load_plan.plan(r, l, 1), CopyDir::scatter,
@@ -807,7 +805,8 @@ Status Connector::store_layers(BatchState& b, uint32_t first, uint32_t last) {
                                    cfg_.load_ctas, store_stream_));
         b.gathered[l].record(store_stream_);
         b.gathered[l].wait_on(d2h_stream_);
-        std::vector<void*> dst, src;
+        std::vector<void*> dst;
+        std::vector<const void*> src;
         std::vector<size_t> sizes;
         for (const auto& s : b.stores) {
             if (s.w.kind != SlotWrite::Kind::write) continue;
@@ -815,11 +814,8 @@ Status Connector::store_layers(BatchState& b, uint32_t first, uint32_t last) {
             src.push_back(b.store_ring->buf.ptr + size_t(r) * b.store_layer_bytes + s.staging_off);
             sizes.push_back(s.rows * bpt);
         }
-        cudaMemcpyAttributes attr{};
-        attr.srcAccessOrder = cudaMemcpySrcAccessOrderStream;
-        size_t attr_idx = 0, fail_idx = 0;
-        TKV_CUDA(cudaMemcpyBatchAsync(dst.data(), src.data(), sizes.data(), dst.size(), &attr,
-                                      &attr_idx, 1, &fail_idx, d2h_stream_));
+        TKV_CUDA(ce_copy_pieces(dst.data(), src.data(), sizes.data(), dst.size(),
+                                cudaMemcpyDeviceToHost, d2h_stream_, &copy_stats_));
         b.d2h_done[l].record(d2h_stream_);
     }
     return Status::success();

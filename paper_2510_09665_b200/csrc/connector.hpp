@@ -33,6 +33,7 @@
 #include <unordered_map>
 #include <vector>
 
+#include "ce_copy.hpp"
 #include "common.hpp"
 #include "paged_store.hpp"
 #include "store.hpp"
@@ -157,6 +158,11 @@ public:
     KeyHasher& hasher() { return hasher_; }
     // Device staging high-water mark (bytes) across batches.
     size_t staging_peak_bytes() const { return staging_peak_; }
+    // Host-tier copy-engine pieces and the copies they went out as (ce_copy.hpp).
+    CopyRunStats copy_stats() {
+        std::lock_guard io(io_mu_);
+        return copy_stats_;
+    }
 
 private:
     friend struct detail::BatchState;
@@ -206,6 +212,7 @@ private:
     StagingRing load_ring_;
     std::vector<std::unique_ptr<StagingRing>> store_rings_;
     size_t staging_peak_ = 0;
+    CopyRunStats copy_stats_;  // guarded by io_mu_
     std::mutex io_mu_;  // one batch enqueues at a time
 
     mutable std::mutex mu_;
