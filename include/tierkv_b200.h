@@ -191,11 +191,12 @@ int tkv_sm_copy(const void* src, void* dst, uint64_t bytes, void* stream);
  * peer copy) the bench reports its rooflines against. */
 int tkv_ce_copy(const void* src, void* dst, uint64_t bytes, void* stream);
 /* Copy-engine copies of n pieces dst[i] <- src[i] (sizes[i] bytes) on
- * `stream` (cudaMemcpyDefault), grouped into pitched runs: pieces whose
- * addresses both advance by one constant step go as one 2D copy. The
- * connector's host-tier path (a layer's chunk slices in their slots). */
+ * `stream`, grouped into pitched runs: pieces whose addresses both advance by
+ * one constant step go as one 2D copy. `kind` is a cudaMemcpyKind value
+ * (1 host->device, 2 device->host). The connector's host-tier path (a
+ * layer's chunk slices in their slots). */
 int tkv_ce_copy_pieces(void* const* dst, const void* const* src, const size_t* sizes, size_t n,
-                       void* stream);
+                       int kind, void* stream);
 /* The grouping tkv_ce_copy_pieces applies (host only, no device call): fills
  * first[k], rows[k] for each run k (capacity n) and returns the run count.
  * Pitches above pitch_max never form a run. */

@@ -91,7 +91,7 @@ SIGNATURES = {
                                     ct.c_uint32, ct.c_uint32, ct.c_uint32, vp, vp]),
     "tkv_synth_chunk": (ct.c_int, [vp, ct.c_uint64, ct.c_uint32, ct.c_uint32, ct.c_uint32, ct.c_uint32, vp, vp]),
     "tkv_sm_copy": (ct.c_int, [vp, vp, ct.c_uint64, vp]),
-    "tkv_ce_copy_pieces": (ct.c_int, [vp, vp, vp, ct.c_size_t, vp]),
+    "tkv_ce_copy_pieces": (ct.c_int, [vp, vp, vp, ct.c_size_t, ct.c_int, vp]),
     "tkv_plan_copy_runs": (ct.c_size_t, [vp, vp, vp, ct.c_size_t, ct.c_size_t, vp, vp]),
     "tkv_ce_copy": (ct.c_int, [vp, vp, ct.c_uint64, vp]),
     "tkv_q8_blob_bytes": (ct.c_uint64, [ct.c_uint64]),

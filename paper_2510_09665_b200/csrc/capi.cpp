@@ -266,9 +266,11 @@ int tkv_ce_copy(const void* src, void* dst, uint64_t bytes, void* stream) {
 }
 
 int tkv_ce_copy_pieces(void* const* dst, const void* const* src, const size_t* sizes, size_t n,
-                       void* stream) {
+                       int kind, void* stream) {
     if (n && (!dst || !src || !sizes)) return fail(Errc::invalid_argument, "null pointer");
-    return cuda(ce_copy_pieces(dst, src, sizes, n, cudaMemcpyDefault, cudaStream_t(stream)));
+    if (kind != cudaMemcpyHostToDevice && kind != cudaMemcpyDeviceToHost)
+        return fail(Errc::invalid_argument, "kind must be 1 (host->device) or 2 (device->host)");
+    return cuda(ce_copy_pieces(dst, src, sizes, n, cudaMemcpyKind(kind), cudaStream_t(stream)));
 }
 
 size_t tkv_plan_copy_runs(void* const* dst, const void* const* src, const size_t* sizes, size_t n,

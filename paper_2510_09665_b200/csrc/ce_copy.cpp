@@ -85,20 +85,32 @@ cudaError_t ce_copy_pieces(void* const* dst, const void* const* src, const size_
     thread_local std::vector<CopyRun> runs;
     runs.resize(n);
     const size_t k = plan_copy_runs(dst, src, sizes, n, pmax, runs.data());
+    uint64_t issued = 0;
     for (size_t r = 0; r < k; ++r) {
         const CopyRun& c = runs[r];
-        cudaError_t e = cudaSuccess;
         if (c.width == 0) continue;
-        if (c.rows == 1)
-            e = cudaMemcpyAsync(dst[c.first], src[c.first], c.width, kind, stream);
-        else
-            e = cudaMemcpy2DAsync(dst[c.first], c.dst_pitch, src[c.first], c.src_pitch, c.width,
-                                  c.rows, kind, stream);
+        // The runtime checks a pitched copy's whole extent, pitch x rows, on
+        // both sides: the last row of a run over the slab's last slot would
+        // reach past the allocation by pitch - width. The last row therefore
+        // goes as its own copy and the 2D copy covers rows - 1, whose extent
+        // ends where the last row starts.
+        const char* s0 = static_cast<const char*>(src[c.first]);
+        char* d0 = static_cast<char*>(dst[c.first]);
+        const size_t body = c.rows - 1;
+        cudaError_t e = cudaSuccess;
+        if (body >= 2)
+            e = cudaMemcpy2DAsync(d0, c.dst_pitch, s0, c.src_pitch, c.width, body, kind, stream);
+        else if (body == 1)
+            e = cudaMemcpyAsync(d0, s0, c.width, kind, stream);
         if (e != cudaSuccess) return e;
+        if (body) ++issued;
+        e = cudaMemcpyAsync(d0 + body * c.dst_pitch, s0 + body * c.src_pitch, c.width, kind, stream);
+        if (e != cudaSuccess) return e;
+        ++issued;
     }
     if (stats) {
         stats->pieces += n;
-        stats->runs += k;
+        stats->runs += issued;
     }
     return cudaSuccess;
 }

@@ -95,16 +95,19 @@ def test_ce_copy_pieces_byte_exact(tkv):
     host.copy_(torch.randint(0, 256, (slot * nslots,), dtype=torch.uint8))
     rng = np.random.default_rng(3)
     s = torch.cuda.Stream()
-    for case in ["ascending", "descending", "mixed", "random", "ragged"]:
+    for case in ["ascending", "descending", "mixed", "random", "ragged", "slab_end", "slab_end_down"]:
         n = 32
+        # slab_end*: the run ends on the allocation's last slot, first layer of
+        # the slot, so pitch x rows reaches past the allocation
         slots = {"ascending": np.arange(n), "descending": np.arange(n)[::-1],
-                 "mixed": np.concatenate([np.arange(10), np.arange(30, 20, -1), np.arange(40, 52)]),
+                 "slab_end": np.arange(nslots - n, nslots), "slab_end_down": np.arange(nslots - n, nslots)[::-1],
+                 "mixed": np.concatenate([np.arange(10), np.arange(30, 20, -1), np.arange(36, 48)]),
                  "random": rng.permutation(nslots)[:n], "ragged": np.arange(n)}[case]
         n = len(slots)
-        layer = int(rng.integers(0, slot // w))
+        layer = 0 if case.startswith("slab_end") else int(rng.integers(0, slot // w))
         sizes = [w] * n if case != "ragged" else [int(x) for x in rng.choice([0, 16, w // 2, w], size=n)]
         offs = np.concatenate([[0], np.cumsum(sizes)[:-1]]).astype(np.int64)
-        if case == "descending":  # ring order follows the (descending) slot order
+        if case in ("descending", "slab_end_down"):  # ring order follows the (descending) slot order
             offs = offs[::-1].copy()
         ring = torch.zeros(int(sum(sizes)) + 64, dtype=torch.uint8, device="cuda")
         hsrc = [host.data_ptr() + int(sl) * slot + layer * w for sl in slots]
@@ -112,7 +115,8 @@ def test_ce_copy_pieces_byte_exact(tkv):
         D = (ct.c_void_p * n)(*ddst)
         S = (ct.c_void_p * n)(*hsrc)
         Z = (ct.c_size_t * n)(*sizes)
-        tkv.check(L.tkv_ce_copy_pieces(D, S, Z, n, ct.c_void_p(s.cuda_stream)))
+        rc = L.tkv_ce_copy_pieces(D, S, Z, n, 1, ct.c_void_p(s.cuda_stream))
+        assert rc == 0, (case, "h2d", L.tkv_last_error())
         s.synchronize()
         got = ring.cpu().numpy()
         hn = host.numpy()
@@ -120,10 +124,11 @@ def test_ce_copy_pieces_byte_exact(tkv):
             a = int(slots[i]) * slot + layer * w
             assert np.array_equal(got[offs[i]:offs[i] + sizes[i]], hn[a:a + sizes[i]]), (case, i)
         # and back: D2H into a fresh host image at the same slots
-        back = torch.zeros_like(host)
+        back = torch.zeros(host.shape, dtype=torch.uint8, pin_memory=True)
         D = (ct.c_void_p * n)(*[back.data_ptr() + int(sl) * slot + layer * w for sl in slots])
         S = (ct.c_void_p * n)(*ddst)
-        tkv.check(L.tkv_ce_copy_pieces(D, S, Z, n, ct.c_void_p(s.cuda_stream)))
+        rc = L.tkv_ce_copy_pieces(D, S, Z, n, 2, ct.c_void_p(s.cuda_stream))
+        assert rc == 0, (case, "d2h", L.tkv_last_error())
         s.synchronize()
         bn = back.numpy()
         for i in range(n):
