@@ -89,22 +89,13 @@ cudaError_t ce_copy_pieces(void* const* dst, const void* const* src, const size_
     for (size_t r = 0; r < k; ++r) {
         const CopyRun& c = runs[r];
         if (c.width == 0) continue;
-        // The runtime checks a pitched copy's whole extent, pitch x rows, on
-        // both sides: the last row of a run over the slab's last slot would
-        // reach past the allocation by pitch - width. The last row therefore
-        // goes as its own copy and the 2D copy covers rows - 1, whose extent
-        // ends where the last row starts.
-        const char* s0 = static_cast<const char*>(src[c.first]);
-        char* d0 = static_cast<char*>(dst[c.first]);
-        const size_t body = c.rows - 1;
-        cudaError_t e = cudaSuccess;
-        if (body >= 2)
-            e = cudaMemcpy2DAsync(d0, c.dst_pitch, s0, c.src_pitch, c.width, body, kind, stream);
-        else if (body == 1)
-            e = cudaMemcpyAsync(d0, s0, c.width, kind, stream);
-        if (e != cudaSuccess) return e;
-        if (body) ++issued;
-        e = cudaMemcpyAsync(d0 + body * c.dst_pitch, s0 + body * c.src_pitch, c.width, kind, stream);
+        // A run's pitch x rows extent may reach past the slab by one pitch
+        // less a width; the runtime accepts that for allocated and registered
+        // pinned memory alike (tools/probe_pitch_extent.cu).
+        cudaError_t e =
+            c.rows == 1 ? cudaMemcpyAsync(dst[c.first], src[c.first], c.width, kind, stream)
+                        : cudaMemcpy2DAsync(dst[c.first], c.dst_pitch, src[c.first], c.src_pitch,
+                                            c.width, c.rows, kind, stream);
         if (e != cudaSuccess) return e;
         ++issued;
     }

@@ -5,10 +5,9 @@
 // place in the packed HBM staging ring. The pieces are grouped into runs of
 // equal width whose source and destination addresses both advance by a
 // constant pitch (consecutive slots of the slab against consecutive ring
-// offsets), and each run goes to the copy engine as one pitched copy
-// (cudaMemcpy2DAsync: width = piece bytes, height = run length - 1) plus
-// one plain copy of its last piece (the runtime checks pitch x height against
-// the allocation); a lone piece is a plain cudaMemcpyAsync. Per-piece copies of 1 MiB pieces reach only
+// offsets), and each run goes to the copy engine as ONE pitched copy
+// (cudaMemcpy2DAsync: width = piece bytes, height = run length); a lone piece
+// is a plain cudaMemcpyAsync. Per-piece copies of 1 MiB pieces reach only
 // 46 GB/s one way and 49-63 GB/s both ways on this box
 // (profiles/r01_microbench_streams.txt), one large copy 55 / 94.
 #pragma once
