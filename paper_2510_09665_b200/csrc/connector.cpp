@@ -432,8 +432,11 @@ ConnectorMetadata Connector::build_connector_meta(const SchedulerOutput& out) {
 // size stop reallocating (each growth synchronizes the ring's streams and
 // calls cudaMalloc, which must not recur inside a serving loop).
 size_t Connector::ring_growth(size_t need, size_t current, uint32_t depth) const {
+    // Twice what is needed (a first reservation included): a later, larger
+    // batch (config 2's waves) must not reallocate, since freeing the old ring
+    // waits for every transfer in flight.
     const size_t cap = size_t(depth) * cfg_.staging_budget_bytes;
-    return std::max(need, std::min(2 * current, cap));
+    return std::max(need, std::min(2 * std::max(current, need), cap));
 }
 
 // --- loads -----------------------------------------------------------------
