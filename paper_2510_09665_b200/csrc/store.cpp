@@ -1,6 +1,7 @@
 #include "store.hpp"
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 
 #include "record.hpp"
@@ -109,7 +110,10 @@ TieredStore::TieredStore(StoreConfig cfg) : cfg_(std::move(cfg)) {
     cfg_.model.validate(cfg_.chunk_size);
     slot_bytes_ = cfg_.model.chunk_bytes(cfg_.chunk_size);
     const size_t slots = cfg_.ram_pool_bytes / slot_bytes_;
-    slab_.huge = true;
+    // TKV_SLAB_HUGE=0: cudaHostAlloc'ed slab instead of registered huge pages
+    // (A/B measurements only).
+    const char* hv = std::getenv("TKV_SLAB_HUGE");
+    slab_.huge = !(hv && std::strcmp(hv, "0") == 0);
     if (slots) slab_.reserve(slots * slot_bytes_);
     free_slots_.reserve(slots);
     for (size_t i = slots; i > 0; --i) free_slots_.push_back(uint32_t(i - 1));  // slot 0 first
