@@ -209,6 +209,9 @@ std::vector<Result<SlotWrite>> TieredStore::begin_write_batch(
     // put has been applied (store.cpp:455-460).
     std::unordered_map<Digest, uint32_t, DigestHasher> pending;
     for (const auto& s : specs) ++pending[s.digest];
+    // Per written output: the largest token count its slot may take (below
+    // chunk_size only for the slot of an own-loaded victim with fewer tokens).
+    std::vector<std::pair<size_t, uint32_t>> written;
     for (const auto& s : specs) {
         --pending[s.digest];
         if (s.token_count == 0 || s.token_count > cfg_.chunk_size) {
@@ -238,6 +241,7 @@ std::vector<Result<SlotWrite>> TieredStore::begin_write_batch(
             out.emplace_back(std::move(w));
             continue;
         }
+        uint32_t victim_limit = cfg_.chunk_size;
         if (free_slots_.empty()) {
             const Digest* victim = nullptr;
             uint64_t oldest = ~uint64_t(0);
@@ -278,7 +282,10 @@ std::vector<Result<SlotWrite>> TieredStore::begin_write_batch(
                 batch_new.erase(bn);
             }
             free_slots_.push_back(vit->second.slot);
-            if (vit->second.state == Entry::State::present) presence_changed(vit->first, false);
+            if (vit->second.state == Entry::State::present) {
+                if (vit->second.share_count) victim_limit = vit->second.token_count;
+                presence_changed(vit->first, false);
+            }
             index_.erase(vit);
         }
         const uint32_t slot = free_slots_.back();
@@ -297,8 +304,32 @@ std::vector<Result<SlotWrite>> TieredStore::begin_write_batch(
         w.dev = slab_.dev + size_t(slot) * slot_bytes_;
         w.handle = PutHandle(e.writer);
         batch_new[s.digest] = out.size();
+        written.emplace_back(out.size(), victim_limit);
         index_.emplace(s.digest, std::move(e));
         out.emplace_back(std::move(w));
+    }
+    // Which slot a chunk takes is not part of the outcome (the reference
+    // replays only which chunks stay): the full chunks written by this batch
+    // take their slots in ascending order, so consecutive chunks land in
+    // consecutive slots wherever the freed slots allow and the per-layer
+    // host copies go as pitched runs (ce_copy.hpp). Slots limited by an
+    // own-loaded victim keep their chunk.
+    std::vector<size_t> idx;
+    std::vector<uint32_t> slots;
+    for (const auto& [o, limit] : written) {
+        if (!out[o].ok() || out[o].value().kind != SlotWrite::Kind::write) continue;  // dropped
+        if (limit < cfg_.chunk_size || specs[o].token_count != cfg_.chunk_size) continue;
+        idx.push_back(o);
+        slots.push_back(index_.at(specs[o].digest).slot);
+    }
+    if (idx.size() > 1 && !std::is_sorted(slots.begin(), slots.end())) {
+        std::sort(slots.begin(), slots.end());
+        for (size_t k = 0; k < idx.size(); ++k) {
+            SlotWrite& w = out[idx[k]].value();
+            index_.at(specs[idx[k]].digest).slot = slots[k];
+            w.host = slab_.host + size_t(slots[k]) * slot_bytes_;
+            w.dev = slab_.dev + size_t(slots[k]) * slot_bytes_;
+        }
     }
     return out;
 }

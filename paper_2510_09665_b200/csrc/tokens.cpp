@@ -97,7 +97,13 @@ MemoView KeyHasher::stage_locked(const std::vector<TokenSpanView>& seqs, const s
     const size_t ch_bytes = seqs.size() * sizeof(ChainDesc);
     d_tokens_.reserve(grow(tok_bytes + 64));
     d_chains_.reserve(grow(ch_bytes + 64));
-    d_out_.reserve(grow(total_chunks * 32));
+    if (d_out_.bytes < total_chunks * 32) {
+        d_out_.reserve(grow(total_chunks * 32));
+        // rows past a chain's first absent chunk are never hashed, but the
+        // verify pass copies every row out (the host reads only the hashed
+        // ones): defined bytes, not stale allocations
+        TKV_CUDA(cudaMemsetAsync(d_out_.ptr, 0, d_out_.bytes, stream_));
+    }
     h_bad_.reserve(grow(seqs.size() * sizeof(unsigned int)));
     h_first_.reserve(grow(seqs.size() * sizeof(uint32_t)));
     auto* bad = reinterpret_cast<unsigned int*>(h_bad_.host);

@@ -136,3 +136,46 @@ def test_ce_copy_pieces_byte_exact(tkv):
             assert np.array_equal(bn[a:a + sizes[i]], hn[a:a + sizes[i]]), (case, "d2h", i)
         written = sum(sizes)
         assert int(np.count_nonzero(bn)) <= written
+
+
+@pytest.mark.gpu
+def test_reverse_evictions_keep_pitched_runs(tkv, C):
+    """A batch whose LRU victims free slots in descending order still writes
+    (and later reads) its full chunks as one pitched run per layer: the store
+    hands a batch's slots out in ascending order (store.cpp
+    begin_write_batch). Bytes checked against synth after the reload."""
+    import scenarios as S
+    from paper_2510_09665_b200.api import Engine
+    cs, L = S.CONN["chunk_size"], S.CONN["num_layers"]
+    e = Engine(**S.CONN, ram_slots=8, num_pages=512)
+    state = {"qid": 1}
+
+    def serve(p):
+        q = state["qid"]
+        state["qid"] += 1
+        m_ = e.get_num_new_matched_tokens(q, p)
+        e.bind_pages(q, len(p))
+        e.update_state_after_alloc(q, (len(p) + 15) // 16, (m_ + 15) // 16)
+        m = e.build_connector_meta([(q, p)])
+        S.transfer(e, m, q, p)
+        ok = S.pages_equal_synth(e, q, p, len(p), C)
+        e.drop_meta(m)
+        e.finish_query(q)
+        e.release_query(q)
+        return m_, ok
+
+    singles = [S.make_prompt(cs, 500 + i) for i in range(8)]
+    for p in singles:  # slots 0..7
+        assert serve(p) == (0, True)
+    for p in singles[::-1]:  # touched 7 first: LRU victims come out 7, 6, 5, ...
+        assert serve(p) == (cs - 1, True)
+    q = S.make_prompt(4 * cs + 1, 900)  # 4 full chunks + a 1-token tail
+    p0, c0 = e.copy_runs()
+    assert serve(q) == (0, True)  # stores 5 chunks into slots 7..3
+    p1, c1 = e.copy_runs()
+    assert p1 - p0 == 5 * L
+    assert c1 - c0 == 2 * L, (p1 - p0, c1 - c0)  # full chunks one run, the tail alone
+    assert serve(q) == (4 * cs, True)  # loads the 4 full chunks
+    p2, c2 = e.copy_runs()
+    assert p2 - p1 == 4 * L and c2 - c1 == L, (p2 - p1, c2 - c1)
+    e.close()

@@ -195,6 +195,7 @@ def c1(reps=3, pcie=None, cpu=True):
             rt.append(t2 - t1b)
     sb, rb = n * L8 * BPT8, (n - 1) * L8 * BPT8
     s, r_ = float(np.median(st)), float(np.median(rt))
+    host_copies = dict(zip(("host_tier_pieces", "host_tier_copies"), e.copy_runs()))
     e.close()
     out = {"workload": "c1: Llama-3.1-8B KV (32 L x 4096 B), one 4096-token prompt: cold store, then warm "
                        "retrieve (4095 tokens), chunk 256, page 16",
@@ -203,7 +204,7 @@ def c1(reps=3, pcie=None, cpu=True):
            "e2e": {"value": round((sb + rb) / (s + r_) / 1e9, 2), "unit": "GB/s",
                    "tokens_per_s": round((2 * n - 1) / (s + r_), 1), "reps": reps},
            "store": _fracs(sb / s / 1e9, pcie), "retrieve": _fracs(rb / r_ / 1e9, pcie),
-           "verify": v.out()}
+           "verify": v.out(), **host_copies}
     if cpu:
         ref_s = ref_batch_gbps([(1, toks(n, 100))], L8, BPT8, TAG8, lambda p: 0)
         ref_r = ref_batch_gbps([(1, toks(n, 100))], L8, BPT8, TAG8, lambda p: len(p))
@@ -251,6 +252,7 @@ def c2(wave=8, pcie=None, cpu=True, n_req=64):
         total_t += t
         waves.append(round(lo * L8 * BPT8 / t / 1e9, 2))
     gb = total_loaded * L8 * BPT8
+    host_copies = dict(zip(("host_tier_pieces", "host_tier_copies"), e.copy_runs()))
     e.close()
     out = {"workload": f"c2: Llama-3.1-8B KV, {n_req} requests of 8K-32K tokens (mean {int(np.mean(lens))}), "
                        f"prefix-hit retrieve from the pinned tier, {wave} requests per scheduling iteration "
@@ -258,7 +260,7 @@ def c2(wave=8, pcie=None, cpu=True, n_req=64):
                        f"warm-up retrieve of the first wave)",
            "e2e": {"value": round(gb / total_t / 1e9, 2), "unit": "GB/s",
                    "tokens_per_s": round(total_loaded / total_t, 1), "bytes": gb, "seconds": round(total_t, 3)},
-           "wave_gbps": waves, **_fracs(gb / total_t / 1e9, pcie), "verify": v.out()}
+           "wave_gbps": waves, **_fracs(gb / total_t / 1e9, pcie), "verify": v.out(), **host_copies}
     if cpu:
         sample = batch[:1]
         ref = ref_batch_gbps(sample, L8, BPT8, TAG8, lambda p: len(p))
@@ -322,6 +324,7 @@ def c4(queries=8, reuse=0.5, pcie=None, cpu=True):
         probe[kind] = round(1e3 * best, 3)
         qid += 1
     memo = e.memo_stats()
+    host_copies = dict(zip(("host_tier_pieces", "host_tier_copies"), e.copy_runs()))
     e.close()
     med = (lambda xs: round(1e3 * float(np.median(xs)), 3) if xs else None)
     out = {"workload": f"c4: Llama-3.1-8B KV, {n_docs} shared 131072-token documents + 20-100 token question, "
@@ -334,7 +337,7 @@ def c4(queries=8, reuse=0.5, pcie=None, cpu=True):
            "lookup_ms_miss": med([t for t, h in zip(t_lookup, hit_flags) if not h]),
            "lookup_probe_ms": {**probe, "method": "best of 3 on one prompt (a stored document + 60-token "
                                                   "question / a cold 128K document), as the reference's"},
-           "memo": memo, "verify": v.out()}
+           "memo": memo, "verify": v.out(), **host_copies}
     if cpu:
         import oracle
         if oracle.ref_available():
