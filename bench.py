@@ -129,8 +129,18 @@ def coll_device(dev):
     return dev if backend() == "nccl" else "cpu"
 
 
+_CTL_GROUP = None  # host-side (gloo) group for the per-step control exchange under NCCL
+
+
 def agree_loaded(loaded, device):
+    """The TP hit-length agreement (one MIN all-reduce per step). Under NCCL it
+    runs on a gloo group over host memory: a device tensor would need a small
+    copy-engine H2D and D2H every step, and those queue behind the layer's KV
+    transfers on the copy engines (the stall the engine's prompt uploads
+    avoid with SM copies)."""
     from paper_2510_09665_b200.tp import agree_loaded as agree
+    if _CTL_GROUP is not None:
+        return agree(loaded, "cpu", group=_CTL_GROUP)
     return agree(loaded, device)
 
 
@@ -961,6 +971,8 @@ def run_b200(args):
         if backend() == "nccl":
             torch.cuda.set_device(local)  # NCCL collectives run on the current device
             dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+            global _CTL_GROUP
+            _CTL_GROUP = dist.new_group(backend="gloo")
         else:
             dist.init_process_group(backend())
     # nvidia-smi (NVML init) takes a second or more to come up and perturbs the
