@@ -7,6 +7,8 @@
 //           host pitch = slot bytes) -- what csrc/ce_copy.cpp issues for a
 //           run of consecutive slots
 //   one   : a single large contiguous copy of the same bytes (upper bound)
+//   split : as 2d, but each layer's D2H in two pitched copies (56 + 8 rows:
+//           a store batch whose slots are two runs)
 // in H2D only, D2H only, and both directions at once.
 // Build: nvcc -O3 -gencode arch=compute_100a,code=sm_100a tools/microbench_pitched.cu -o /tmp/mbp
 #include <cuda_runtime.h>
@@ -35,7 +37,7 @@ int main() {
   auto h2d = [&](int mode, int l) {
     if (mode == 0) for (int i = 0; i < N; ++i)
       CK(cudaMemcpyAsync(dh + l * layer + i * piece, hh + i * slot + l * piece, piece, cudaMemcpyHostToDevice, a));
-    else if (mode == 1)
+    else if (mode == 1 || mode == 3)
       CK(cudaMemcpy2DAsync(dh + l * layer, piece, hh + l * piece, slot, piece, N, cudaMemcpyHostToDevice, a));
     else CK(cudaMemcpyAsync(dh + l * layer, hh + l * layer, layer, cudaMemcpyHostToDevice, a));
   };
@@ -44,11 +46,16 @@ int main() {
       CK(cudaMemcpyAsync(hd + i * slot + l * piece, dd + l * layer + i * piece, piece, cudaMemcpyDeviceToHost, b));
     else if (mode == 1)
       CK(cudaMemcpy2DAsync(hd + l * piece, slot, dd + l * layer, piece, piece, N, cudaMemcpyDeviceToHost, b));
+    else if (mode == 3) {
+      CK(cudaMemcpy2DAsync(hd + l * piece, slot, dd + l * layer, piece, piece, N - 8, cudaMemcpyDeviceToHost, b));
+      CK(cudaMemcpy2DAsync(hd + (N - 8) * slot + l * piece, slot, dd + l * layer + (N - 8) * piece, piece, piece, 8,
+                           cudaMemcpyDeviceToHost, b));
+    }
     else CK(cudaMemcpyAsync(hd + l * layer, dd + l * layer, layer, cudaMemcpyDeviceToHost, b));
   };
-  const char* names[] = {"piece", "2d", "one"};
+  const char* names[] = {"piece", "2d", "one", "split"};
   const char* dirs[] = {"h2d", "d2h", "both"};
-  for (int mode = 0; mode < 3; ++mode)
+  for (int mode = 0; mode < 4; ++mode)
     for (int dir = 0; dir < 3; ++dir)
       for (int rep = 0; rep < 2; ++rep) {
         CK(cudaDeviceSynchronize());
