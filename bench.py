@@ -83,7 +83,7 @@ def parse_args_list(argv):
     ap.add_argument("--store-ctas", type=int, default=0)
     ap.add_argument("--staging-depth", type=int, default=2)
     ap.add_argument("--ram-slots", type=int, default=0,
-                    help="pinned tier slots (0: prefix + two suffixes + 8, so the timed steps evict)")
+                    help="pinned tier slots (0: prefix + two suffixes, so the timed steps evict)")
     ap.add_argument("--profile-kernels", action="store_true", help="only run the K1/K2 device-resident loop")
     ap.add_argument("--trace", action="store_true", help="host time of every call of one step")
     ap.add_argument("--no-pd", action="store_true", help="skip the N>=2 PD-over-NVLink pairs")
@@ -407,11 +407,15 @@ class B200Bench:
         chunks = (self.n + 255) // 256
         self.stream = torch.cuda.Stream(self.dev)
         # Two requests in flight (pipelined schedule): pages for both, and pinned
-        # slots for the prefix plus two suffixes still being written.
+        # slots for exactly the prefix plus two suffixes: when request k+1
+        # reserves, request k's suffix is still being written (not evictable)
+        # and request k-1's is committed, so the LRU evicts k-1's suffix, 64
+        # consecutive slots (one pitched copy per layer; spare slots would
+        # float and split every later store batch into two runs).
         pages = 2 * (self.n // 16 + 16) * self.L
         suffix_chunks = (self.n - self.n_pre + 255) // 256
         self.e = Engine(num_layers=self.L, bpt=self.bpt, page_tokens=16, tag=TAG, chunk_size=256,
-                        ram_slots=args.ram_slots or chunks + suffix_chunks + 8, num_pages=pages, layerwise=True,
+                        ram_slots=args.ram_slots or chunks + suffix_chunks, num_pages=pages, layerwise=True,
                         staging_budget=1 << 34, staging_depth=args.staging_depth,
                         load_zero_copy=args.load_zero_copy, store_zero_copy=args.store_zero_copy,
                         store_ctas=args.store_ctas, device=local,
