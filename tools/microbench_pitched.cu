@@ -23,7 +23,7 @@
 int main() {
   CK(cudaSetDevice(0));
   const int pk = std::getenv("PIECE_KB") ? std::atoi(std::getenv("PIECE_KB")) : 1024;
-  const int L = 40, N = 64;
+  const int L = std::getenv("LAYERS") ? std::atoi(std::getenv("LAYERS")) : 40, N = 64;
   const size_t piece = size_t(pk) << 10, layer = size_t(N) * piece, total = size_t(L) * layer;
   const size_t slot = size_t(L) * piece;  // one chunk's [L][T][bpt] payload
   char *dh, *dd, *hh, *hd;
