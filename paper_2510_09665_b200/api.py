@@ -558,7 +558,7 @@ class PdStaging:
 
 def pd_send(engine: "Engine", qid: int, n_tokens: int, landing_ptr: int, chunk_stride: int):
     """Prefiller: gather the query's chunks (all layers) into landing memory."""
-    cap = 1 << 14
+    cap = (n_tokens + engine.chunk_size - 1) // engine.chunk_size + 1
     out = (PdRecordC * cap)()
     n = ct.c_size_t(0)
     check(lib().tkv_pd_send(engine.pages, qid, n_tokens, engine.chunk_size, landing_ptr, chunk_stride,
@@ -569,7 +569,7 @@ def pd_send(engine: "Engine", qid: int, n_tokens: int, landing_ptr: int, chunk_s
 def pd_send_staged(engine: "Engine", qid: int, n_tokens: int, landing_ptr: int, chunk_stride: int,
                    staging_ptr: int, group_bytes: int = 0):
     """Prefiller, copy-engine variant: K1 into local staging, CE peer copies."""
-    cap = 1 << 14
+    cap = (n_tokens + engine.chunk_size - 1) // engine.chunk_size + 1
     out = (PdRecordC * cap)()
     n = ct.c_size_t(0)
     check(lib().tkv_pd_send_staged(engine.pages, qid, n_tokens, engine.chunk_size, landing_ptr, chunk_stride,

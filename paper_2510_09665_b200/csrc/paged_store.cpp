@@ -174,6 +174,11 @@ const std::vector<PageId>* PagedKVStore::span_list(QueryId query, uint32_t layer
 Status PagedKVStore::check_readable_span(QueryId query, uint32_t layer, size_t first_page,
                                          size_t token_count) const {
     std::lock_guard lock(mu_);
+    return readable_locked(query, layer, first_page, token_count);
+}
+
+Status PagedKVStore::readable_locked(QueryId query, uint32_t layer, size_t first_page,
+                                     size_t token_count) const {
     size_t end = 0;
     const auto* list = span_list(query, layer, first_page, token_count, end);
     if (list == nullptr)
@@ -187,6 +192,11 @@ Status PagedKVStore::check_readable_span(QueryId query, uint32_t layer, size_t f
 Status PagedKVStore::check_writable_span(QueryId query, uint32_t layer, size_t first_page,
                                          size_t token_count) const {
     std::lock_guard lock(mu_);
+    return writable_locked(query, layer, first_page, token_count);
+}
+
+Status PagedKVStore::writable_locked(QueryId query, uint32_t layer, size_t first_page,
+                                     size_t token_count) const {
     size_t end = 0;
     const auto* list = span_list(query, layer, first_page, token_count, end);
     if (list == nullptr) return Status{Errc::size_mismatch, "span larger than the bound pages"};
@@ -202,6 +212,39 @@ Status PagedKVStore::check_writable_span(QueryId query, uint32_t layer, size_t f
 void PagedKVStore::mark_span_populated(QueryId query, uint32_t layer, size_t first_page,
                                        size_t token_count) {
     std::lock_guard lock(mu_);
+    populate_locked(query, layer, first_page, token_count);
+}
+
+Status PagedKVStore::check_readable_spans(QueryId query, const std::vector<PageSpan>& spans, uint32_t l0,
+                                          uint32_t l1) const {
+    std::lock_guard lock(mu_);
+    for (const auto& sp : spans)
+        for (uint32_t l = l0; l < l1; ++l) {
+            Status st = readable_locked(query, l, sp.first_page, sp.token_count);
+            if (!st.ok()) return st;
+        }
+    return Status::success();
+}
+
+Status PagedKVStore::check_writable_spans(QueryId query, const std::vector<PageSpan>& spans, uint32_t l0,
+                                          uint32_t l1) const {
+    std::lock_guard lock(mu_);
+    for (const auto& sp : spans)
+        for (uint32_t l = l0; l < l1; ++l) {
+            Status st = writable_locked(query, l, sp.first_page, sp.token_count);
+            if (!st.ok()) return st;
+        }
+    return Status::success();
+}
+
+void PagedKVStore::mark_spans_populated(QueryId query, const std::vector<PageSpan>& spans, uint32_t l0,
+                                        uint32_t l1) {
+    std::lock_guard lock(mu_);
+    for (const auto& sp : spans)
+        for (uint32_t l = l0; l < l1; ++l) populate_locked(query, l, sp.first_page, sp.token_count);
+}
+
+void PagedKVStore::populate_locked(QueryId query, uint32_t layer, size_t first_page, size_t token_count) {
     const auto it = queries_.find(query);
     if (it == queries_.end() || it->second.layers.size() <= layer) return;
     const auto& list = it->second.layers[layer];

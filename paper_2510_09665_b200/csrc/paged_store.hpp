@@ -63,6 +63,16 @@ public:
                                size_t token_count) const;
     // Marks the pages covering [first_page, +ceil(n/pt)) of the span populated.
     void mark_span_populated(QueryId query, uint32_t layer, size_t first_page, size_t token_count);
+    // The three above over many spans of one query and layers [l0, l1),
+    // span by span and layer by layer within a span (the order, hence the
+    // first error, of one call per (span, layer)), under one lock: a PD
+    // send / land of a 32K-token prompt is 128 chunks x 80 layers.
+    struct PageSpan {
+        size_t first_page = 0, token_count = 0;
+    };
+    Status check_readable_spans(QueryId query, const std::vector<PageSpan>& spans, uint32_t l0, uint32_t l1) const;
+    Status check_writable_spans(QueryId query, const std::vector<PageSpan>& spans, uint32_t l0, uint32_t l1) const;
+    void mark_spans_populated(QueryId query, const std::vector<PageSpan>& spans, uint32_t l0, uint32_t l1);
 
     // --- reference-shaped single-layer host API (tests, tools) -------------
     // Synchronous: these move bytes between host memory and pages with the
@@ -100,6 +110,10 @@ private:
     // span [first, first + ceil(n / page_tokens)) of (query, layer), or null
     const std::vector<PageId>* span_list(QueryId query, uint32_t layer, size_t first_page, size_t token_count,
                                          size_t& end) const;
+    // bodies of the span checks / mark; caller holds mu_
+    Status readable_locked(QueryId query, uint32_t layer, size_t first_page, size_t token_count) const;
+    Status writable_locked(QueryId query, uint32_t layer, size_t first_page, size_t token_count) const;
+    void populate_locked(QueryId query, uint32_t layer, size_t first_page, size_t token_count);
 
     Status check_readable(const std::vector<PageId>& pages, uint32_t layer,
                           size_t token_count) const;

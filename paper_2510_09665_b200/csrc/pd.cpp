@@ -106,14 +106,22 @@ Status pd_describe(PagedKVStore& pages, QueryId query, size_t n_tokens, size_t c
     if (chunk_size == 0 || chunk_size % pt) return Status{Errc::invalid_argument, "chunk size"};
     auto t = pages.device_table(query, stream);
     if (!t.ok()) return t.status();
+    // Per chunk, its layers' readability then its landing size (the first
+    // failure in that order is the result). Chunk 0 is the largest, so a
+    // size failure is chunk 0's, after chunk 0's readability.
+    std::vector<PagedKVStore::PageSpan> spans;
+    for (size_t start = 0; start < n_tokens; start += chunk_size)
+        spans.push_back({start / pt, std::min(chunk_size, n_tokens - start)});
+    const bool too_big = !spans.empty() && uint64_t(spec.num_layers) * spans[0].token_count * bpt > chunk_stride;
+    if (check_layers) {
+        if (too_big) spans.resize(1);
+        Status st = pages.check_readable_spans(query, spans, 0, spec.num_layers);
+        if (!st.ok()) return st;
+    }
+    if (too_big) return Status{Errc::size_mismatch, "landing slot too small"};
     for (size_t start = 0, i = 0; start < n_tokens; start += chunk_size, ++i) {
         const size_t n = std::min(chunk_size, n_tokens - start);
-        for (uint32_t l = 0; check_layers && l < spec.num_layers; ++l) {
-            Status st = pages.check_readable_span(query, l, start / pt, n);
-            if (!st.ok()) return st;
-        }
         const uint64_t bytes = uint64_t(spec.num_layers) * n * bpt;
-        if (bytes > chunk_stride) return Status{Errc::size_mismatch, "landing slot too small"};
         recs.push_back(PdRecord{landing + i * chunk_stride, bytes, uint32_t(n), uint32_t(start)});
         XferDesc x;
         x.chunk = base + i * chunk_stride;
@@ -209,8 +217,11 @@ Status PdLayerSender::send_layer(uint32_t layer, cudaStream_t engine_stream) {
     if (layer >= spec.num_layers) return Status{Errc::invalid_argument, "layer out of range"};
     if (sent_[layer]) return Status{Errc::duplicate_key, "layer already sent"};
     const uint32_t pt = spec.page_tokens;
-    for (const auto& r : recs_) {  // the engine computed this layer (check_readable)
-        Status st = pages_.check_readable_span(query_, layer, r.first_token / pt, r.token_count);
+    {  // the engine computed this layer (check_readable)
+        std::vector<PagedKVStore::PageSpan> spans;
+        spans.reserve(recs_.size());
+        for (const auto& r : recs_) spans.push_back({r.first_token / pt, r.token_count});
+        Status st = pages_.check_readable_spans(query_, spans, layer, layer + 1);
         if (!st.ok()) return st;
     }
     sent_[layer] = true;
@@ -239,15 +250,25 @@ Status pd_land_chunks(PagedKVStore& pages, QueryId query, const std::vector<PdRe
     const size_t bpt = spec.bytes_per_token_per_layer;
     auto t = pages.device_table(query, stream);
     if (!t.ok()) return t.status();
+    // Per record: alignment, size, then every layer's pages writable; the
+    // first failure in that order is the result (the page checks of the
+    // records before the first malformed one run in one batch).
+    size_t bad = records.size();
+    Status bad_st;
+    for (size_t i = 0; i < records.size() && bad == records.size(); ++i) {
+        const auto& r = records[i];
+        if (r.first_token % pt)
+            bad = i, bad_st = Status{Errc::invalid_argument, "record not page aligned"};
+        else if (r.bytes != uint64_t(spec.num_layers) * r.token_count * bpt)
+            bad = i, bad_st = Status{Errc::size_mismatch, "pushed record size"};  // sim_engine.cpp:461-462
+    }
+    std::vector<PagedKVStore::PageSpan> spans;
+    spans.reserve(bad);
+    for (size_t i = 0; i < bad; ++i) spans.push_back({records[i].first_token / pt, records[i].token_count});
+    if (Status st = pages.check_writable_spans(query, spans, 0, spec.num_layers); !st.ok()) return st;
+    if (bad < records.size()) return bad_st;
     std::vector<XferDesc> descs;
     for (const auto& r : records) {
-        if (r.first_token % pt) return Status{Errc::invalid_argument, "record not page aligned"};
-        if (r.bytes != uint64_t(spec.num_layers) * r.token_count * bpt)
-            return Status{Errc::size_mismatch, "pushed record size"};  // sim_engine.cpp:461-462
-        for (uint32_t l = 0; l < spec.num_layers; ++l) {
-            Status st = pages.check_writable_span(query, l, r.first_token / pt, r.token_count);
-            if (!st.ok()) return st;
-        }
         XferDesc x;
         x.chunk = r.addr;
         x.layer_stride = uint64_t(r.token_count) * bpt;
@@ -262,9 +283,7 @@ Status pd_land_chunks(PagedKVStore& pages, QueryId query, const std::vector<PdRe
     plan.build(pd_plan_pool(), {descs}, pt, pages.page_bytes(), spec.num_layers, stream);
     TKV_CUDA(launch_paged_copy(pages.layout(), plan.plan(0, 0, spec.num_layers),
                                CopyDir::scatter, ctas, stream));
-    for (const auto& r : records)
-        for (uint32_t l = 0; l < spec.num_layers; ++l)
-            pages.mark_span_populated(query, l, r.first_token / pt, r.token_count);
+    pages.mark_spans_populated(query, spans, 0, spec.num_layers);
     TKV_CUDA(cudaStreamSynchronize(stream));  // plan buffers are freed on return
     return Status::success();
 }
